@@ -1,0 +1,168 @@
+/*
+ * wavecell_b200.h -- C ABI of the B200 (sm_100a) explicit wave-stepping hot path.
+ *
+ * The reference (`wavecell`, arXiv 2501.19013) is a pure-Python package whose
+ * time-marching loop runs in SciPy's C++ CSR matvec.  Its "FFI boundary" is the
+ * Python function API of `wavecell.timeint` / `wavecell.linalg`; every entry
+ * point below replaces one of those functions (or the operator object it
+ * consumes) and is bound from Python through ctypes by
+ * `paper_2501_19013_b200/_lib.py` (see INTEGRATION.md for the binding stub).
+ *
+ * Conventions
+ *   - Plain C types only: host pointers, int64 sizes, fp64 values.  No torch
+ *     or CUDA types cross the boundary (the stream is exported as void*).
+ *   - Vectors are in the reference's *compact DOF order*
+ *     (src/assembly.py:159-180, lex = (fx*n1 + fy)*n1 + fz, x slowest).
+ *   - All inputs are deep-copied to the device; inputs are never mutated
+ *     (the reference copies psi0/v0, src/timeint.py:162-164).
+ *   - Every function returns a WCB_* status code; wcb_last_error() gives a
+ *     thread-local message.  The Python shim re-raises the reference's
+ *     exception types (DivergenceError, RuntimeError, ValueError).
+ *   - Calls are synchronous with respect to the host: when a call returns,
+ *     its outputs are in the caller's buffers.
+ */
+#ifndef WAVECELL_B200_H
+#define WAVECELL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WCB_ABI_VERSION 1
+
+enum wcb_status {
+    WCB_OK = 0,
+    WCB_E_ARG = 1,          /* invalid argument -> ValueError                        */
+    WCB_E_CUDA = 2,         /* CUDA runtime failure -> RuntimeError                  */
+    WCB_E_DIVERGED = 3,     /* max|psi| > 1e12 or non-finite -> DivergenceError       */
+    WCB_E_NOCONV = 4,       /* power iteration hit max_iter -> RuntimeError           */
+    WCB_E_UNSUPPORTED = 5   /* operator/shape combination not built -> NotImplemented */
+};
+
+typedef struct wcb_context wcb_context;    /* one device + one stream + events      */
+typedef struct wcb_operator wcb_operator;  /* device-resident stiffness K            */
+typedef struct wcb_cdm_plan wcb_cdm_plan;  /* device-resident M, F_s, observers      */
+typedef struct wcb_imex_plan wcb_imex_plan;/* device-resident IMEX split + S_cc LU   */
+
+/* StageTimings, src/timeint.py:46-56 (seconds, from CUDA events). */
+typedef struct {
+    double factorization;
+    double rhs;
+    double backward_insertion;
+} wcb_timings;
+
+/* DivergenceError(step, amplitude), src/timeint.py:36-43,91-94. */
+typedef struct {
+    int64_t step;        /* first step k with max|psi_k| > 1e12 or non-finite; -1 if none */
+    double amplitude;    /* max|psi_k| at that step                                   */
+} wcb_divergence;
+
+/* Observer matrix obs_mat (CSR, n_obs x n_dof), src/timeint.py:97-106,
+ * src/harness.py:59-98.  Entries are summed in stored order. */
+typedef struct {
+    int64_t n_obs;
+    const int64_t* indptr;   /* n_obs + 1 */
+    const int64_t* indices;  /* nnz, compact DOF ids */
+    const double* data;      /* nnz */
+} wcb_observer;
+
+/* Matrix-free spectral-cell (GLL Lagrange) stiffness on a Cartesian grid.
+ * Uncut cells: sk * (k1 (x) m1 [(x) m1] + ...) applied by sum factorisation
+ *   (src/assembly.py:263-295, TensorSystem.k_matvec src/assembly.py:674-684).
+ * Cut cells: dense physical K_o = sk (K_in + alpha K_out) per cell
+ *   (src/assembly.py:575-583), local DOF order z fastest (src/assembly.py:85-89). */
+typedef struct {
+    int32_t dim;                 /* 2 or 3                                              */
+    int32_t p;                   /* polynomial degree (2D: 1..6, 3D: 1..4)              */
+    int64_t n_e[3];              /* cells per axis, axis 0 slowest (x)                 */
+    const double* k1;            /* (p+1)^2 row-major 1D GL-exact stiffness (reference) */
+    const double* m1;            /* (p+1)^2 row-major 1D GL-exact mass (reference)      */
+    double sk;                   /* rho c^2 (h/2)^(dim-2), src/assembly.py:504-505      */
+    const int8_t* cell_class;    /* prod(n_e) ElementClass (0 out,1 in,2 cut), lex      */
+    int64_t n_dof;               /* compact DOFs                                        */
+    const int64_t* lex_of_compact; /* n_dof node lex ids (src/assembly.py:173)          */
+    int64_t n_cut;               /* number of cut cells                                 */
+    const int64_t* cut_cells;    /* n_cut cell lex ids, ascending                       */
+    const double* cut_K;         /* n_cut * L * L physical element stiffness, L=(p+1)^dim */
+} wcb_scm_desc;
+
+/* ---- library / context ------------------------------------------------- */
+int wcb_abi_version(void);
+const char* wcb_last_error(void);
+int wcb_device_count(int* out);
+int wcb_context_create(int device, wcb_context** out);
+int wcb_context_destroy(wcb_context* ctx);
+void* wcb_context_stream(wcb_context* ctx);        /* cudaStream_t of the context          */
+int64_t wcb_context_launches(wcb_context* ctx);    /* kernels launched so far (counter)     */
+
+/* ---- operators: replace the K consumed by the integrators ---------------- */
+/* scipy CSR K from assemble()/_to_csr, src/assembly.py:518-612 (IGA and generic path). */
+int wcb_operator_csr_create(wcb_context* ctx, int64_t n, const int64_t* indptr,
+                            const int32_t* indices, const double* data,
+                            wcb_operator** out);
+/* Matrix-free SCM K (replaces the CSR K of Lagrange systems, src/assembly.py:554-583). */
+int wcb_operator_scm_create(wcb_context* ctx, const wcb_scm_desc* desc, wcb_operator** out);
+int wcb_operator_destroy(wcb_operator* op);
+int64_t wcb_operator_n(const wcb_operator* op);
+/* y = K @ x on host buffers (K.__matmul__, src/timeint.py:175,182). */
+int wcb_operator_apply(wcb_operator* op, const double* x, double* y);
+
+/* ---- critical time step: max_gen_eig, src/linalg.py:89-122 --------------- */
+/* Power iteration on M^-1 K with diagonal M; x0 is the normalised seeded start
+ * vector (src/linalg.py:103-105).  Returns WCB_E_NOCONV after max_iter. */
+int wcb_max_gen_eig(wcb_operator* K, const double* m_diag, const double* x0,
+                    double tol, int64_t max_iter, double* lam, int64_t* n_iter);
+
+/* ---- central difference method: cdm_run, src/timeint.py:159-193 ---------- */
+/* Diagonal M only (the factorize() fast path, src/linalg.py:63-69).  F_s may be
+ * sparse: only its nonzeros are kept on the device. */
+int wcb_cdm_plan_create(wcb_operator* K, const double* m_diag, const double* F_s,
+                        const wcb_observer* obs, wcb_cdm_plan** out);
+int wcb_cdm_plan_destroy(wcb_cdm_plan* plan);
+/* ft[k] = f_t(k*dt) for k = 0..n_t-1 (f_t(0.0) == ft[0] is the bootstrap force).
+ * psi0 / v0 may be NULL (zeros).  obs_out is n_obs x (n_t+1) row-major or NULL.
+ * Returns WCB_E_DIVERGED with *div filled on divergence. */
+int wcb_cdm_plan_run(wcb_cdm_plan* plan, const double* ft, double dt, int64_t n_t,
+                     const double* psi0, const double* v0, double* psi_out,
+                     double* obs_out, wcb_divergence* div, wcb_timings* tm);
+/* Same loop on device-resident buffers (cudaMalloc'd by the caller on the
+ * context's device): d_ft (n_t), d_psi0/d_v0 (n, may be NULL), d_psi_out (n),
+ * d_obs_out (n_obs*(n_t+1) or NULL).  Used by bench.py for the HBM-resident
+ * number; synchronous on return. */
+int wcb_cdm_plan_run_device(wcb_cdm_plan* plan, const double* d_ft, double dt,
+                            int64_t n_t, const double* d_psi0, const double* d_v0,
+                            double* d_psi_out, double* d_obs_out,
+                            wcb_divergence* div, wcb_timings* tm);
+
+/* ---- implicit-explicit split: imex_run, src/timeint.py:196-292 ----------- */
+/* d rows: diagonal mass m_d (src/timeint.py:223-236); c rows: S_cc = M_cc +
+ * beta dt^2 K_cc prefactorised on the host as Pr S_cc Pc = L U (SuperLU,
+ * src/linalg.py:70-80) and M_cc likewise; both triangular solves run on the
+ * device every step.  Factors are CSR (L unit-lower, U upper incl. diagonal). */
+typedef struct {
+    int64_t n;                      /* factor dimension                           */
+    const int64_t* perm_r;          /* row permutation: (Pr b)[perm_r[i]] = b[i]    */
+    const int64_t* perm_c;          /* col permutation: x[i] = z[perm_c[i]]         */
+    const int64_t* L_indptr; const int32_t* L_indices; const double* L_data;
+    const int64_t* U_indptr; const int32_t* U_indices; const double* U_data;
+} wcb_lu;
+
+int wcb_imex_plan_create(wcb_operator* K, int64_t n_c, const int64_t* c_idx,
+                         int64_t n_d, const int64_t* d_idx, const double* m_d,
+                         const wcb_lu* S_cc, const wcb_lu* M_cc, const double* F_s,
+                         const wcb_observer* obs, wcb_imex_plan** out);
+int wcb_imex_plan_destroy(wcb_imex_plan* plan);
+/* ft_k[k] = f_t(k*dt), ft_new[k] = f_t(k*dt + dt) (src/timeint.py:259-260),
+ * f0 = f_t(0.0).  psi_dot_out (n) receives v when d is empty, else untouched. */
+int wcb_imex_plan_run(wcb_imex_plan* plan, double f0, const double* ft_k,
+                      const double* ft_new, double dt, int64_t n_t, double beta,
+                      double gamma, const double* psi0, const double* v0,
+                      double* psi_out, double* psi_dot_out, double* obs_out,
+                      wcb_divergence* div, wcb_timings* tm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WAVECELL_B200_H */

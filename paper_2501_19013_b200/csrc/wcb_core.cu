@@ -1,0 +1,629 @@
+// Context, error plumbing, generic vector kernels, the CDM time loop driver
+// (src/timeint.py:159-193) and the power iteration (src/linalg.py:89-130).
+#include "wcb_internal.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+namespace wcb {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return WCB_E_ARG;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return WCB_E_ARG;
+    }
+}
+
+static int grid_for(const Context* ctx, int64_t n, int block = 256) {
+    int64_t g = ceil_div(std::max<int64_t>(n, 1), block);
+    int64_t cap = (int64_t)ctx->sm_count * 8;
+    return (int)std::min(g, cap);
+}
+
+// ------------------------------------------------------------ kernels -----
+__global__ void k_scatter(int64_t n, const int64_t* __restrict__ map,
+                          const double* __restrict__ src, double* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[map[i]] = src[i];
+}
+__global__ void k_gather(int64_t n, const int64_t* __restrict__ map,
+                         const double* __restrict__ src, double* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[map[i]];
+}
+
+void launch_scatter(Context* ctx, int64_t n, const int64_t* d_map, const double* src,
+                    double* dst_state) {
+    if (n == 0) return;
+    k_scatter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, d_map, src, dst_state);
+    ctx->launches++;
+    WCB_CHECK_LAUNCH();
+}
+void launch_gather(Context* ctx, int64_t n, const int64_t* d_map, const double* src_state,
+                   double* dst) {
+    if (n == 0) return;
+    k_gather<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(n, d_map, src_state, dst);
+    ctx->launches++;
+    WCB_CHECK_LAUNCH();
+}
+
+// m_state = m at DOF slots, 1 elsewhere; minv = 1/m at DOF slots, 0 elsewhere.
+__global__ void k_mass_state(int64_t n, const int64_t* __restrict__ map,
+                             const double* __restrict__ m, double* __restrict__ m_state,
+                             double* __restrict__ minv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t s = map[i];
+        m_state[s] = m[i];
+        minv[s] = 1.0 / m[i];
+    }
+}
+__global__ void k_fill(int64_t n, double v, double* __restrict__ x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+// CDM bootstrap, src/timeint.py:175-176:
+//   a = (f0 F - K psi) / m;  psi_prev = psi - dt v + (0.5 dt dt) a
+__global__ void k_cdm_bootstrap(int64_t ns, const double* __restrict__ psi,
+                                const double* __restrict__ v, const double* __restrict__ Kpsi,
+                                const double* __restrict__ m_state, Source F,
+                                const double* __restrict__ ft, double dt,
+                                double* __restrict__ prev) {
+    const double f0 = ft[0];
+    const double c = 0.5 * dt * dt;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double a = (f0 * source_at(F, i) - Kpsi[i]) / m_state[i];
+        prev[i] = psi[i] - dt * v[i] + c * a;
+    }
+}
+
+// obs[:, k] = obs_mat @ psi, CSR order (scipy csr_matvec), src/timeint.py:105-106.
+__global__ void k_obs_record(int64_t n_obs, const int64_t* __restrict__ indptr,
+                             const int64_t* __restrict__ sidx, const double* __restrict__ val,
+                             const double* __restrict__ psi, double* __restrict__ out,
+                             int64_t stride, int64_t k) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n_obs) return;
+    double s = 0.0;
+    for (int64_t j = indptr[r]; j < indptr[r + 1]; ++j) s += val[j] * psi[sidx[j]];
+    out[r * stride + k] = s;
+}
+
+// ---- power iteration pieces (src/linalg.py:108-119) ----
+constexpr int RB = 256;
+
+// y = t / m ; partial[b] = sum y^2
+__global__ void k_pow_y(int64_t ns, const double* __restrict__ t, const double* __restrict__ m,
+                        double* __restrict__ y, double* __restrict__ part,
+                        const double* __restrict__ sc) {
+    if (sc[3] != 0.0) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < ns; i += (int64_t)gridDim.x * RB) {
+        double yi = t[i] / m[i];
+        y[i] = yi;
+        acc += yi * yi;
+    }
+    double s = block_sum<RB>(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+// sc[0] = ||y||; zero norm -> done (lam = 0)
+__global__ void k_pow_norm(int nparts, const double* __restrict__ part, double* __restrict__ sc,
+                           int64_t it) {
+    if (sc[3] != 0.0) return;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += RB) acc += part[i];
+    double s = block_sum<RB>(acc);
+    if (threadIdx.x == 0) {
+        double ny = sqrt(s);
+        sc[0] = ny;
+        if (ny == 0.0) { sc[1] = 0.0; sc[3] = 2.0; sc[4] = (double)it; }
+    }
+}
+__global__ void k_pow_x(int64_t ns, const double* __restrict__ y, double* __restrict__ x,
+                        const double* __restrict__ sc) {
+    if (sc[3] != 0.0) return;
+    const double ny = sc[0];
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < ns; i += (int64_t)gridDim.x * RB)
+        x[i] = y[i] / ny;
+}
+// partials of x.Kx and x.(m x) (m = 1 at non-DOF slots where x = 0)
+__global__ void k_pow_dots(int64_t ns, const double* __restrict__ x, const double* __restrict__ Kx,
+                           const double* __restrict__ m, double* __restrict__ part,
+                           const double* __restrict__ sc) {
+    if (sc[3] != 0.0) return;
+    double a = 0.0, b = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < ns; i += (int64_t)gridDim.x * RB) {
+        double xi = x[i];
+        a += xi * Kx[i];
+        b += xi * (m[i] * xi);
+    }
+    double sa = block_sum<RB>(a);
+    double sb = block_sum<RB>(b);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = sa;
+        part[2 * blockIdx.x + 1] = sb;
+    }
+}
+// lam = xKx / xMx ; stop when |lam - lam_old| <= tol |lam| (src/linalg.py:116-117)
+__global__ void k_pow_lambda(int nparts, const double* __restrict__ part, double* __restrict__ sc,
+                             double tol, int64_t it) {
+    if (sc[3] != 0.0) return;
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += RB) {
+        a += part[2 * i];
+        b += part[2 * i + 1];
+    }
+    double sa = block_sum<RB>(a);
+    double sb = block_sum<RB>(b);
+    if (threadIdx.x == 0) {
+        double lam = sa / sb;
+        double lam_old = sc[2];
+        sc[1] = lam;
+        if (fabs(lam - lam_old) <= tol * fabs(lam)) {
+            sc[3] = 1.0;
+            sc[4] = (double)it;
+        }
+        sc[2] = lam;
+    }
+}
+
+}  // namespace wcb
+
+using namespace wcb;
+
+// ====================================================================== ABI ==
+extern "C" {
+
+int wcb_abi_version(void) { return WCB_ABI_VERSION; }
+const char* wcb_last_error(void) { return g_last_error.c_str(); }
+
+int wcb_device_count(int* out) {
+    return guarded([&] {
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) n = 0;
+        *out = n;
+        return WCB_OK;
+    });
+}
+
+int wcb_context_create(int device, wcb_context** out) {
+    return guarded([&] {
+        WCB_REQUIRE(out != nullptr, "out is NULL");
+        std::unique_ptr<wcb_context> c(new wcb_context());
+        Context& x = c->c;
+        x.device = device;
+        WCB_CUDA(cudaSetDevice(device));
+        int major = 0;
+        WCB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        if (major != 10)
+            throw Error{WCB_E_UNSUPPORTED,
+                        "wavecell_b200 is built for sm_100a (B200); device has compute "
+                        "capability major " + std::to_string(major)};
+        WCB_CUDA(cudaDeviceGetAttribute(&x.sm_count, cudaDevAttrMultiProcessorCount, device));
+        WCB_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
+        WCB_CUDA(cudaEventCreate(&x.ev0));
+        WCB_CUDA(cudaEventCreate(&x.ev1));
+        WCB_CUDA(cudaEventCreate(&x.ev2));
+        x.partials.alloc(2 * (size_t)x.sm_count * 8 + 64);
+        x.scalars.alloc(16);
+        WCB_CUDA(cudaMallocHost(&x.h_scalars, 16 * sizeof(double)));
+        *out = c.release();
+        return WCB_OK;
+    });
+}
+
+int wcb_context_destroy(wcb_context* ctx) {
+    if (!ctx) return WCB_OK;
+    return guarded([&] {
+        Context& x = ctx->c;
+        cudaSetDevice(x.device);
+        cudaStreamSynchronize(x.stream);
+        x.partials.release();
+        x.scalars.release();
+        if (x.h_scalars) cudaFreeHost(x.h_scalars);
+        cudaEventDestroy(x.ev0);
+        cudaEventDestroy(x.ev1);
+        cudaEventDestroy(x.ev2);
+        cudaStreamDestroy(x.stream);
+        delete ctx;
+        return WCB_OK;
+    });
+}
+
+void* wcb_context_stream(wcb_context* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+int64_t wcb_context_launches(wcb_context* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int wcb_operator_csr_create(wcb_context* ctx, int64_t n, const int64_t* indptr,
+                            const int32_t* indices, const double* data, wcb_operator** out) {
+    return guarded([&] {
+        WCB_REQUIRE(ctx && out, "NULL argument");
+        WCB_REQUIRE(n >= 0, "negative n");
+        WCB_CUDA(cudaSetDevice(ctx->c.device));
+        std::unique_ptr<wcb_operator> o(new wcb_operator());
+        o->op = make_csr_operator(&ctx->c, n, indptr, indices, data);
+        *out = o.release();
+        return WCB_OK;
+    });
+}
+
+int wcb_operator_scm_create(wcb_context* ctx, const wcb_scm_desc* desc, wcb_operator** out) {
+    return guarded([&] {
+        WCB_REQUIRE(ctx && desc && out, "NULL argument");
+        WCB_CUDA(cudaSetDevice(ctx->c.device));
+        std::unique_ptr<wcb_operator> o(new wcb_operator());
+        o->op = make_scm_operator(&ctx->c, desc);
+        *out = o.release();
+        return WCB_OK;
+    });
+}
+
+int wcb_operator_destroy(wcb_operator* op) {
+    if (!op) return WCB_OK;
+    return guarded([&] {
+        cudaSetDevice(op->op->ctx->device);
+        cudaStreamSynchronize(op->op->ctx->stream);
+        delete op->op;
+        delete op;
+        return WCB_OK;
+    });
+}
+
+int64_t wcb_operator_n(const wcb_operator* op) { return op ? op->op->n : -1; }
+
+int wcb_operator_apply(wcb_operator* o, const double* x, double* y) {
+    return guarded([&] {
+        WCB_REQUIRE(o && x && y, "NULL argument");
+        Operator* op = o->op;
+        Context* ctx = op->ctx;
+        WCB_CUDA(cudaSetDevice(ctx->device));
+        const int64_t n = op->n;
+        if (n == 0) return WCB_OK;
+        DevBuf<double> dx(n), dy(n), sx(op->n_state), sy(op->n_state);
+        dx.upload(x, n, ctx->stream);
+        sx.zero(ctx->stream);
+        op->scatter(dx.p, sx.p);
+        op->apply(sx.p, sy.p);
+        op->gather(sy.p, dy.p);
+        WCB_CUDA(cudaMemcpyAsync(y, dy.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        return WCB_OK;
+    });
+}
+
+// ---------------------------------------------------------- max_gen_eig ----
+int wcb_max_gen_eig(wcb_operator* o, const double* m_diag, const double* x0, double tol,
+                    int64_t max_iter, double* lam, int64_t* n_iter) {
+    return guarded([&] {
+        WCB_REQUIRE(o && m_diag && x0 && lam && n_iter, "NULL argument");
+        Operator* op = o->op;
+        Context* ctx = op->ctx;
+        WCB_CUDA(cudaSetDevice(ctx->device));
+        const int64_t n = op->n, ns = op->n_state;
+        WCB_REQUIRE(n > 0, "empty operator");
+        cudaStream_t s = ctx->stream;
+        DevBuf<double> dm(n), dx0(n), m_state(ns), minv(ns), x(ns), t(ns), y(ns);
+        DevBuf<int64_t> map;
+        dm.upload(m_diag, n, s);
+        dx0.upload(x0, n, s);
+        // mass in state layout (1 at non-DOF slots so y = 0/1 = 0 there)
+        k_fill<<<grid_for(ctx, ns), 256, 0, s>>>(ns, 1.0, m_state.p);
+        ctx->launches++;
+        {
+            const std::vector<int64_t>& si = op->state_index();
+            map.alloc(n);
+            map.upload(si.data(), n, s);
+            k_mass_state<<<grid_for(ctx, n), 256, 0, s>>>(n, map.p, dm.p, m_state.p, minv.p);
+            ctx->launches++;
+        }
+        x.zero(s);
+        op->scatter(dx0.p, x.p);
+        t.zero(s);
+        y.zero(s);
+        WCB_CHECK_LAUNCH();
+        const int gb = grid_for(ctx, ns, RB);
+        double init[8] = {0.0, 0.0, INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0};
+        WCB_CUDA(cudaMemcpyAsync(ctx->scalars.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        double* sc = ctx->scalars.p;
+        double* part = ctx->partials.p;
+        const int64_t batch = 16;
+        int64_t it = 1;
+        bool done = false;
+        while (!done && it <= max_iter) {
+            int64_t end = std::min<int64_t>(max_iter, it + batch - 1);
+            for (; it <= end; ++it) {
+                op->apply(x.p, t.p);
+                k_pow_y<<<gb, RB, 0, s>>>(ns, t.p, m_state.p, y.p, part, sc);
+                k_pow_norm<<<1, RB, 0, s>>>(gb, part, sc, it);
+                k_pow_x<<<gb, RB, 0, s>>>(ns, y.p, x.p, sc);
+                op->apply(x.p, t.p);
+                k_pow_dots<<<gb, RB, 0, s>>>(ns, x.p, t.p, m_state.p, part, sc);
+                k_pow_lambda<<<1, RB, 0, s>>>(gb, part, sc, tol, it);
+                ctx->launches += 5;
+            }
+            WCB_CHECK_LAUNCH();
+            WCB_CUDA(cudaMemcpyAsync(ctx->h_scalars, sc, 8 * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s));
+            WCB_CUDA(cudaStreamSynchronize(s));
+            done = ctx->h_scalars[3] != 0.0;
+        }
+        if (!done) {
+            char buf[160];
+            snprintf(buf, sizeof(buf),
+                     "power iteration did not converge in %lld iterations (last estimate %.6e)",
+                     (long long)max_iter, ctx->h_scalars[2]);
+            throw Error{WCB_E_NOCONV, buf};
+        }
+        *lam = ctx->h_scalars[1];
+        *n_iter = (int64_t)ctx->h_scalars[4];
+        return WCB_OK;
+    });
+}
+
+}  // extern "C"
+
+// ============================================================= CDM plan ====
+struct wcb_cdm_plan {
+    Operator* op = nullptr;
+    DevBuf<double> m_state, minv;
+    DevBuf<double> F_dense;
+    DevBuf<int64_t> F_idx;
+    DevBuf<double> F_val;
+    Source src;
+    int64_t n_obs = 0;
+    DevBuf<int64_t> obs_indptr, obs_idx;
+    DevBuf<double> obs_val;
+    DevBuf<double> A, B, V, T, cin, cout;
+    DevBuf<double> ft;
+    DevBuf<unsigned long long> amp;
+    std::vector<unsigned long long> h_amp;
+};
+
+namespace wcb {
+
+static void run_cdm_device(wcb_cdm_plan* P, const double* d_ft, double dt, int64_t n_t,
+                           const double* d_psi0, const double* d_v0, double* d_psi_out,
+                           double* d_obs_out, wcb_divergence* div, wcb_timings* tm) {
+    Operator* op = P->op;
+    Context* ctx = op->ctx;
+    cudaStream_t s = ctx->stream;
+    const int64_t n = op->n, ns = op->n_state;
+    if (div) { div->step = -1; div->amplitude = 0.0; }
+    if (tm) { tm->factorization = 0.0; tm->rhs = 0.0; tm->backward_insertion = 0.0; }
+    if (P->A.n != (size_t)ns) {
+        P->A.alloc(ns); P->B.alloc(ns); P->V.alloc(ns); P->T.alloc(ns);
+        P->A.zero(s); P->B.zero(s); P->V.zero(s); P->T.zero(s);
+    }
+    if (P->amp.n < (size_t)(n_t + 1)) P->amp.alloc(n_t + 1);
+    P->amp.zero(s);
+    // initial state: zeros unless given (src/timeint.py:162-163)
+    P->A.zero(s);
+    P->V.zero(s);
+    if (d_psi0) op->scatter(d_psi0, P->A.p);
+    if (d_v0) op->scatter(d_v0, P->V.p);
+    const int g = grid_for(ctx, ns);
+    // bootstrap a0, psi_{-1}
+    op->apply(P->A.p, P->T.p);
+    k_cdm_bootstrap<<<g, 256, 0, s>>>(ns, P->A.p, P->V.p, P->T.p, P->m_state.p, P->src, d_ft, dt,
+                                      P->B.p);
+    ctx->launches++;
+    WCB_CHECK_LAUNCH();
+    const int64_t stride = n_t + 1;
+    auto record = [&](int64_t k, const double* psi) {
+        if (P->n_obs && d_obs_out) {
+            k_obs_record<<<(int)ceil_div(P->n_obs, 64), 64, 0, s>>>(
+                P->n_obs, P->obs_indptr.p, P->obs_idx.p, P->obs_val.p, psi, d_obs_out, stride, k);
+            ctx->launches++;
+        }
+    };
+    record(0, P->A.p);
+    StepArgs a;
+    a.minv = P->minv.p;
+    a.F = P->src;
+    a.ft = d_ft;
+    a.dt2 = dt * dt;
+    double* cur = P->A.p;
+    double* prev = P->B.p;
+    P->h_amp.assign(n_t + 1, 0ULL);
+    const int64_t check_every = 256;
+    int64_t checked = 0;  // amp[1..checked] inspected
+    auto inspect = [&](int64_t upto) -> bool {
+        if (upto <= checked) return false;
+        WCB_CUDA(cudaMemcpyAsync(P->h_amp.data() + checked + 1, P->amp.p + checked + 1,
+                                 (upto - checked) * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
+        WCB_CUDA(cudaStreamSynchronize(s));
+        for (int64_t k = checked + 1; k <= upto; ++k) {
+            double v;
+            unsigned long long b = P->h_amp[k];
+            std::memcpy(&v, &b, sizeof(v));
+            if (!std::isfinite(v) || v > 1.0e12) {
+                if (div) { div->step = k; div->amplitude = v; }
+                return true;
+            }
+        }
+        checked = upto;
+        return false;
+    };
+    WCB_CUDA(cudaEventRecord(ctx->ev0, s));
+    bool diverged = false;
+    for (int64_t k = 0; k < n_t; ++k) {
+        a.cur = cur;
+        a.prev = prev;
+        a.out = prev;  // psi_{k+1} overwrites psi_{k-1} in place
+        a.k = k;
+        a.amp = P->amp.p + (k + 1);
+        op->cdm_step(a);
+        std::swap(cur, prev);
+        record(k + 1, cur);
+        if ((k + 1) % check_every == 0) {
+            WCB_CHECK_LAUNCH();
+            if (inspect(k + 1)) { diverged = true; break; }
+        }
+    }
+    WCB_CUDA(cudaEventRecord(ctx->ev1, s));
+    WCB_CHECK_LAUNCH();
+    if (!diverged) diverged = inspect(n_t);
+    WCB_CUDA(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    WCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    // The K apply and the update are one fused kernel: the whole loop is
+    // reported under "rhs" (src/timeint.py:181-188 splits them in two).
+    if (tm) tm->rhs = ms * 1e-3;
+    if (diverged) throw Error{WCB_E_DIVERGED, "solution diverged"};
+    op->gather(cur, d_psi_out);
+    WCB_CUDA(cudaStreamSynchronize(s));
+    (void)n;
+}
+
+}  // namespace wcb
+
+extern "C" {
+
+int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s,
+                        const wcb_observer* obs, wcb_cdm_plan** out) {
+    return guarded([&] {
+        WCB_REQUIRE(o && m_diag && F_s && out, "NULL argument");
+        Operator* op = o->op;
+        Context* ctx = op->ctx;
+        WCB_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const int64_t n = op->n, ns = op->n_state;
+        for (int64_t i = 0; i < n; ++i)
+            WCB_REQUIRE(m_diag[i] > 0.0 && std::isfinite(m_diag[i]),
+                        "diagonal mass has non-positive entries");
+        std::unique_ptr<wcb_cdm_plan> P(new wcb_cdm_plan());
+        P->op = op;
+        const std::vector<int64_t>& si = op->state_index();
+        DevBuf<int64_t> map(n);
+        map.upload(si.data(), n, s);
+        DevBuf<double> dm(n);
+        dm.upload(m_diag, n, s);
+        P->m_state.alloc(ns);
+        P->minv.alloc(ns);
+        k_fill<<<grid_for(ctx, ns), 256, 0, s>>>(ns, 1.0, P->m_state.p);
+        P->minv.zero(s);
+        if (n) k_mass_state<<<grid_for(ctx, n), 256, 0, s>>>(n, map.p, dm.p, P->m_state.p, P->minv.p);
+        ctx->launches += 2;
+        WCB_CHECK_LAUNCH();
+        // source: sparse when it has few nonzeros
+        std::vector<std::pair<int64_t, double>> nz;
+        for (int64_t i = 0; i < n; ++i)
+            if (F_s[i] != 0.0) nz.emplace_back(si[i], F_s[i]);
+        if ((int64_t)nz.size() * 16 <= n || nz.size() <= 4096) {
+            std::sort(nz.begin(), nz.end());
+            std::vector<int64_t> idx(nz.size());
+            std::vector<double> val(nz.size());
+            for (size_t i = 0; i < nz.size(); ++i) { idx[i] = nz[i].first; val[i] = nz[i].second; }
+            P->F_idx.alloc(idx.size());
+            P->F_val.alloc(val.size());
+            P->F_idx.upload(idx.data(), idx.size(), s);
+            P->F_val.upload(val.data(), val.size(), s);
+            P->src.idx = P->F_idx.p;
+            P->src.val = P->F_val.p;
+            P->src.nnz = (int64_t)idx.size();
+            if (!idx.empty()) { P->src.lo = idx.front(); P->src.hi = idx.back(); }
+        } else {
+            DevBuf<double> dF(n);
+            dF.upload(F_s, n, s);
+            P->F_dense.alloc(ns);
+            P->F_dense.zero(s);
+            op->scatter(dF.p, P->F_dense.p);
+            P->src.dense = P->F_dense.p;
+            WCB_CUDA(cudaStreamSynchronize(s));
+        }
+        if (obs && obs->n_obs > 0) {
+            P->n_obs = obs->n_obs;
+            int64_t nnz = obs->indptr[obs->n_obs];
+            std::vector<int64_t> sidx(nnz);
+            for (int64_t j = 0; j < nnz; ++j) {
+                int64_t c = obs->indices[j];
+                WCB_REQUIRE(c >= 0 && c < n, "observer column out of range");
+                sidx[j] = si[c];
+            }
+            P->obs_indptr.alloc(obs->n_obs + 1);
+            P->obs_indptr.upload(obs->indptr, obs->n_obs + 1, s);
+            P->obs_idx.alloc(std::max<int64_t>(nnz, 1));
+            P->obs_idx.upload(sidx.data(), nnz, s);
+            P->obs_val.alloc(std::max<int64_t>(nnz, 1));
+            P->obs_val.upload(obs->data, nnz, s);
+        }
+        WCB_CUDA(cudaStreamSynchronize(s));
+        *out = P.release();
+        return WCB_OK;
+    });
+}
+
+int wcb_cdm_plan_destroy(wcb_cdm_plan* plan) {
+    if (!plan) return WCB_OK;
+    return guarded([&] {
+        cudaSetDevice(plan->op->ctx->device);
+        cudaStreamSynchronize(plan->op->ctx->stream);
+        delete plan;
+        return WCB_OK;
+    });
+}
+
+int wcb_cdm_plan_run_device(wcb_cdm_plan* P, const double* d_ft, double dt, int64_t n_t,
+                            const double* d_psi0, const double* d_v0, double* d_psi_out,
+                            double* d_obs_out, wcb_divergence* div, wcb_timings* tm) {
+    return guarded([&] {
+        WCB_REQUIRE(P && d_psi_out, "NULL argument");
+        WCB_REQUIRE(n_t >= 0, "negative n_t");
+        WCB_REQUIRE(d_ft, "force table is NULL (it holds max(n_t,1) entries, ft[0] = f_t(0.0))");
+        WCB_CUDA(cudaSetDevice(P->op->ctx->device));
+        run_cdm_device(P, d_ft, dt, n_t, d_psi0, d_v0, d_psi_out, d_obs_out, div, tm);
+        return WCB_OK;
+    });
+}
+
+int wcb_cdm_plan_run(wcb_cdm_plan* P, const double* ft, double dt, int64_t n_t,
+                     const double* psi0, const double* v0, double* psi_out, double* obs_out,
+                     wcb_divergence* div, wcb_timings* tm) {
+    return guarded([&] {
+        WCB_REQUIRE(P && psi_out, "NULL argument");
+        WCB_REQUIRE(n_t >= 0, "negative n_t");
+        Operator* op = P->op;
+        Context* ctx = op->ctx;
+        WCB_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const int64_t n = op->n;
+        DevBuf<double> dft(std::max<int64_t>(n_t, 1)), dpsi0, dv0, dout(std::max<int64_t>(n, 1)),
+            dobs;
+        WCB_REQUIRE(ft, "force table is NULL (it holds max(n_t,1) entries, ft[0] = f_t(0.0))");
+        dft.upload(ft, std::max<int64_t>(n_t, 1), s);
+        if (psi0) { dpsi0.alloc(n); dpsi0.upload(psi0, n, s); }
+        if (v0) { dv0.alloc(n); dv0.upload(v0, n, s); }
+        if (obs_out && P->n_obs) dobs.alloc(P->n_obs * (n_t + 1));
+        run_cdm_device(P, dft.p, dt, n_t, dpsi0.p, dv0.p, dout.p, dobs.p, div, tm);
+        if (n) WCB_CUDA(cudaMemcpyAsync(psi_out, dout.p, n * sizeof(double),
+                                        cudaMemcpyDeviceToHost, s));
+        if (obs_out && P->n_obs)
+            WCB_CUDA(cudaMemcpyAsync(obs_out, dobs.p, P->n_obs * (n_t + 1) * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s));
+        WCB_CUDA(cudaStreamSynchronize(s));
+        return WCB_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,215 @@
+// Internal declarations shared by the wavecell_b200 CUDA translation units.
+// Everything here is C++ behind the extern "C" boundary of include/wavecell_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/wavecell_b200.h"
+
+namespace wcb {
+
+// ---------------------------------------------------------------- errors ----
+void set_error(const std::string& msg);
+struct Error {
+    int code;
+    std::string msg;
+};
+
+#define WCB_CUDA(call)                                                          \
+    do {                                                                        \
+        cudaError_t _e = (call);                                                \
+        if (_e != cudaSuccess)                                                  \
+            throw ::wcb::Error{WCB_E_CUDA, std::string(#call) + ": " +          \
+                                               cudaGetErrorString(_e)};        \
+    } while (0)
+
+#define WCB_CHECK_LAUNCH() WCB_CUDA(cudaGetLastError())
+
+#define WCB_REQUIRE(cond, msg)                                                  \
+    do {                                                                        \
+        if (!(cond)) throw ::wcb::Error{WCB_E_ARG, (msg)};                      \
+    } while (0)
+
+// ------------------------------------------------------------ device buf ----
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) WCB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void upload(const T* h, size_t count, cudaStream_t s) {
+        if (count) WCB_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void zero(cudaStream_t s) {
+        if (n) WCB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+};
+
+// ---------------------------------------------------------------- context ----
+struct Context {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+    int64_t launches = 0;
+    // scratch for deterministic reductions
+    DevBuf<double> partials;   // per-block partial sums
+    DevBuf<double> scalars;    // small scalar slots
+    double* h_scalars = nullptr;  // pinned mirror
+};
+
+// ----------------------------------------------------------- step inputs ----
+// Sparse or dense spatial load F_s in the operator's state layout.
+struct Source {
+    const double* dense = nullptr;   // state-layout dense F_s, or null
+    const int64_t* idx = nullptr;    // sorted state indices of nonzeros
+    const double* val = nullptr;
+    int64_t nnz = 0;
+    int64_t lo = 1, hi = 0;          // idx range (empty when lo > hi)
+};
+
+__device__ __forceinline__ double source_at(const Source& s, int64_t i) {
+    if (s.dense) return s.dense[i];
+    if (i < s.lo || i > s.hi) return 0.0;
+    int64_t a = 0, b = s.nnz - 1;
+    while (a <= b) {
+        int64_t m = (a + b) >> 1;
+        int64_t v = s.idx[m];
+        if (v == i) return s.val[m];
+        if (v < i) a = m + 1; else b = m - 1;
+    }
+    return 0.0;
+}
+
+// One explicit CDM step, src/timeint.py:179-190, fused:
+//   out = 2 cur - prev + dt^2 * minv * (f F - K cur);  amp[0] = max |out|
+// out may alias prev (each entry is read before it is written by one thread).
+struct StepArgs {
+    const double* cur = nullptr;
+    const double* prev = nullptr;
+    double* out = nullptr;
+    const double* minv = nullptr;    // 1/m, 0 at non-DOF state slots
+    Source F;
+    const double* ft = nullptr;      // force table on device
+    int64_t k = 0;                   // f = ft[k]
+    double dt2 = 0.0;
+    unsigned long long* amp = nullptr;
+};
+
+// Reference arithmetic order of src/timeint.py:185:
+//   psi_new = 2.0*psi - psi_prev + (dt*dt) * (rhs / m)
+// with rhs = f*F - K psi; 1/m is precomputed (<= 1 ulp from the division).
+__device__ __forceinline__ double leapfrog(double u, double up, double Ku, double minv,
+                                           double fF, double dt2) {
+    double rhs = fF - Ku;
+    return (2.0 * u - up) + dt2 * (rhs * minv);
+}
+
+__device__ __forceinline__ unsigned long long amp_bits(double v) {
+    // |v| as ordered uint64: NaN (any payload) > +inf > finite.
+    unsigned long long b = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
+    return b;
+}
+
+// Block-wide max of per-thread amp bits, one atomic per block.
+template <int BLOCK>
+__device__ __forceinline__ void block_amp_max(unsigned long long v, unsigned long long* slot) {
+    __shared__ unsigned long long red[BLOCK / 32];
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < BLOCK / 32 ? red[lane] : 0ULL;
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+            v = w > v ? w : v;
+        }
+        if (lane == 0 && v) atomicMax(slot, v);
+    }
+}
+
+// Deterministic block sum (fixed shuffle tree + fixed warp order).
+template <int BLOCK>
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double red[BLOCK / 32];
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < BLOCK / 32; ++w) s += red[w];
+    }
+    return s;  // valid in thread 0
+}
+
+// ---------------------------------------------------------------- operator ----
+struct Operator {
+    Context* ctx = nullptr;
+    int64_t n = 0;          // compact DOFs
+    int64_t n_state = 0;    // length of a state vector on the device
+    virtual ~Operator() = default;
+    virtual const char* name() const = 0;
+    // state index of each compact DOF (host copy, for observers / sources)
+    virtual const std::vector<int64_t>& state_index() const = 0;
+    // compact <-> state (state slots without a DOF are zero)
+    virtual void scatter(const double* d_compact, double* d_state) = 0;
+    virtual void gather(const double* d_state, double* d_compact) = 0;
+    // y = K x in state layout
+    virtual void apply(const double* d_x, double* d_y) = 0;
+    // fused explicit step
+    virtual void cdm_step(const StepArgs& a) = 0;
+    // algorithmic bytes of one fused step (for the roofline)
+    virtual double step_bytes() const = 0;
+};
+
+Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* indptr,
+                            const int32_t* indices, const double* data);
+Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d);
+
+// generic elementwise kernels (wcb_core.cu)
+void launch_scatter(Context* ctx, int64_t n, const int64_t* d_map, const double* src,
+                    double* dst_state);
+void launch_gather(Context* ctx, int64_t n, const int64_t* d_map, const double* src_state,
+                   double* dst);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace wcb
+
+struct wcb_context {
+    wcb::Context c;
+};
+struct wcb_operator {
+    wcb::Operator* op;
+};

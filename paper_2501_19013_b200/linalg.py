@@ -1,0 +1,93 @@
+"""Critical time step on the device: drop-in for ``wavecell.linalg``
+``max_gen_eig`` / ``dt_crit`` (src/linalg.py:89-130).
+
+Same signature, same seeded start vector (``default_rng(seed)``, normalised,
+compact DOF order, src/linalg.py:103-105), same Rayleigh-quotient estimate and
+stopping rule ``|lam - lam_old| <= tol |lam|`` (src/linalg.py:116-117).  The
+iteration runs in HBM through the operator's own apply kernel; only the
+converged estimate comes back.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from .operators import DeviceOperator, as_device_operator
+
+
+class IndefiniteMatrixError(RuntimeError):
+    """The matrix handed to ``factorize`` is not positive definite
+    (src/linalg.py:23-24)."""
+
+
+def is_structurally_diagonal(A) -> bool:
+    """True if all stored nonzero entries of A lie on the diagonal
+    (src/linalg.py:45-49)."""
+    coo = sp.csr_matrix(A).tocoo()
+    mask = coo.data != 0.0
+    return bool(np.all(coo.row[mask] == coo.col[mask]))
+
+
+def diagonal_mass(M) -> np.ndarray:
+    """The diagonal of a structurally diagonal SPD mass, with the checks of
+    ``factorize``'s fast path (src/linalg.py:63-69)."""
+    if isinstance(M, np.ndarray) and M.ndim == 1:
+        d = np.ascontiguousarray(M, dtype=np.float64)
+    else:
+        A = sp.csr_matrix(M)
+        if A.shape[0] != A.shape[1]:
+            raise ValueError("matrix must be square")
+        if not is_structurally_diagonal(A):
+            raise NotImplementedError(
+                "the device integrators need a diagonal (lumped / nodal) mass matrix; "
+                "use imex_run for a consistent cut-cell mass block")
+        d = np.ascontiguousarray(A.diagonal(), dtype=np.float64)
+    if np.any(d <= 0.0) or not np.all(np.isfinite(d)):
+        raise IndefiniteMatrixError(
+            "diagonal matrix has non-positive entries; "
+            "check the stabilization and lumping settings")
+    return d
+
+
+def start_vector(n: int, seed: int) -> np.ndarray:
+    """Seeded normalised start vector of src/linalg.py:103-105."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(n)
+    x /= np.linalg.norm(x)
+    return x
+
+
+def max_gen_eig(K, M, tol=1e-9, max_iter=50000, seed=0, device: int | None = None):
+    """Largest eigenvalue of ``K x = lam M x`` by power iteration on the device.
+
+    Returns ``(lam, n_iter)`` like src/linalg.py:89-122.
+    """
+    op = as_device_operator(K, device=device)
+    n = op.n
+    m = diagonal_mass(M)
+    if m.shape[0] != n:
+        raise ValueError("K and M sizes differ")
+    x0 = start_vector(n, seed)
+    lam = _lib.C.c_double(0.0)
+    it = _lib.C.c_int64(0)
+    code = _lib.load().wcb_max_gen_eig(op.handle, _lib.dptr(m), _lib.dptr(x0), float(tol),
+                                       int(max_iter), _lib.C.byref(lam), _lib.C.byref(it))
+    if code == _lib.WCB_E_NOCONV:
+        raise RuntimeError(_lib.last_error())
+    _lib.check(code)
+    return float(lam.value), int(it.value)
+
+
+def dt_crit(K, M, tol=1e-9, seed=0, device: int | None = None) -> float:
+    """Critical time step of central differences, ``2 / sqrt(lam_max(K, M))``
+    (src/linalg.py:125-130)."""
+    lam, _ = max_gen_eig(K, M, tol=tol, seed=seed, device=device)
+    if lam <= 0.0:
+        raise ValueError("largest generalized eigenvalue must be positive")
+    return 2.0 / np.sqrt(lam)
+
+
+__all__ = ["IndefiniteMatrixError", "is_structurally_diagonal", "diagonal_mass",
+           "start_vector", "max_gen_eig", "dt_crit", "DeviceOperator"]

@@ -1,0 +1,170 @@
+"""Device-resident stiffness operators (the ``K`` the integrators consume).
+
+The reference integrators accept anything with ``K @ x`` (scipy CSR from
+``assemble``, src/assembly.py:518-612, or the separable ``LinearOperator`` of
+``TensorSystem``, src/assembly.py:674-690).  Here ``K`` is uploaded once into
+HBM and stays there across every step of every run:
+
+* :class:`CsrOperator` -- any scipy sparse / dense matrix (IGA B-spline path,
+  generic systems).
+* :class:`ScmOperator` -- matrix-free spectral-cell stiffness on a Cartesian
+  grid: sum-factorised uncut cells plus dense cut cells.
+
+``op @ x`` works on host vectors (one device round trip) so an operator can be
+handed to any code written against the reference's duck type.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+
+
+class DeviceOperator:
+    """Base class: an opaque ``wcb_operator`` handle on one device."""
+
+    kind = "abstract"
+
+    def __init__(self, handle, n: int, ctx: _lib.Context):
+        self._h = handle
+        self.n = int(n)
+        self.ctx = ctx
+        self.shape = (self.n, self.n)
+        self.dtype = np.dtype(np.float64)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def matvec(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.shape != (self.n,):
+            raise ValueError(f"expected shape ({self.n},), got {x.shape}")
+        y = np.empty(self.n)
+        _lib.check(_lib.load().wcb_operator_apply(self._h, _lib.dptr(x), _lib.dptr(y)))
+        return y
+
+    def __matmul__(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        if x.ndim == 2:
+            return np.stack([self.matvec(x[:, j]) for j in range(x.shape[1])], axis=1)
+        return self.matvec(x)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().wcb_operator_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class CsrOperator(DeviceOperator):
+    """CSR ``K`` in HBM (int64 row pointers, int32 columns, fp64 values)."""
+
+    kind = "csr"
+
+    def __init__(self, K, device: int | None = None):
+        A = sp.csr_matrix(K, dtype=np.float64)
+        if A.shape[0] != A.shape[1]:
+            raise ValueError("matrix must be square")
+        A.sum_duplicates()
+        n = A.shape[0]
+        indptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(A.indices, dtype=np.int32)
+        data = np.ascontiguousarray(A.data, dtype=np.float64)
+        ctx = _lib.context(device)
+        h = _lib.C.c_void_p()
+        _lib.check(_lib.load().wcb_operator_csr_create(
+            ctx.handle, n, _lib.i64ptr(indptr), _lib.i32ptr(indices), _lib.dptr(data),
+            _lib.C.byref(h)))
+        super().__init__(h, n, ctx)
+        self.nnz = int(data.shape[0])
+
+
+class ScmOperator(DeviceOperator):
+    """Matrix-free spectral-cell-method stiffness on a Cartesian cell grid.
+
+    Parameters mirror what ``assemble`` consumes (src/assembly.py:518-583):
+    the shared uncut 1D factors ``m1, k1`` (src/assembly.py:263-272), the cell
+    classification (src/geometry.py:36-41, 0 outside / 1 inside / 2 cut), the
+    compact DOF map (src/assembly.py:159-180) and the physical cut-cell
+    stiffness matrices ``sk (K_in + alpha K_out)`` (src/assembly.py:582).
+    """
+
+    kind = "scm"
+
+    def __init__(self, dim: int, p: int, n_e, k1, m1, sk: float, cell_class,
+                 lex_of_compact, cut_cells, cut_K, device: int | None = None):
+        dim = int(dim)
+        p = int(p)
+        n_e = tuple(int(v) for v in n_e)
+        if len(n_e) != dim:
+            raise ValueError("n_e must have dim entries")
+        L = (p + 1) ** dim
+        self._k1 = np.ascontiguousarray(k1, dtype=np.float64).reshape(p + 1, p + 1)
+        self._m1 = np.ascontiguousarray(m1, dtype=np.float64).reshape(p + 1, p + 1)
+        self._cls = np.ascontiguousarray(cell_class, dtype=np.int8).reshape(-1)
+        if self._cls.shape[0] != int(np.prod(n_e)):
+            raise ValueError("cell_class must have prod(n_e) entries")
+        self._lex = np.ascontiguousarray(lex_of_compact, dtype=np.int64)
+        self._cut = np.ascontiguousarray(cut_cells, dtype=np.int64).reshape(-1)
+        self._cutK = np.ascontiguousarray(cut_K, dtype=np.float64).reshape(-1)
+        if self._cutK.shape[0] != self._cut.shape[0] * L * L:
+            raise ValueError("cut_K must hold n_cut * L * L values")
+        desc = _lib.ScmDesc()
+        desc.dim = dim
+        desc.p = p
+        for i in range(3):
+            desc.n_e[i] = n_e[i] if i < dim else 1
+        desc.k1 = _lib.dptr(self._k1)
+        desc.m1 = _lib.dptr(self._m1)
+        desc.sk = float(sk)
+        desc.cell_class = _lib.i8ptr(self._cls)
+        desc.n_dof = self._lex.shape[0]
+        desc.lex_of_compact = _lib.i64ptr(self._lex)
+        desc.n_cut = self._cut.shape[0]
+        desc.cut_cells = _lib.i64ptr(self._cut) if self._cut.size else None
+        desc.cut_K = _lib.dptr(self._cutK) if self._cutK.size else None
+        ctx = _lib.context(device)
+        h = _lib.C.c_void_p()
+        _lib.check(_lib.load().wcb_operator_scm_create(ctx.handle, _lib.C.byref(desc),
+                                                       _lib.C.byref(h)))
+        super().__init__(h, self._lex.shape[0], ctx)
+        self.dim, self.p, self.n_e, self.sk = dim, p, n_e, float(sk)
+        self.n_cut = int(self._cut.shape[0])
+
+
+_cache: dict[int, tuple] = {}
+
+
+def as_device_operator(K, device: int | None = None) -> DeviceOperator:
+    """Device operator for ``K`` (cached per host object while it lives)."""
+    if isinstance(K, DeviceOperator):
+        return K
+    key = id(K)
+    hit = _cache.get(key)
+    if hit is not None:
+        ref, op = hit
+        if ref() is K and (device is None or op.ctx.device == device):
+            return op
+    if sp.issparse(K) or isinstance(K, np.ndarray) or isinstance(K, np.matrix):
+        op = CsrOperator(K, device=device)
+    else:
+        raise TypeError(
+            f"unsupported stiffness operator type {type(K).__name__}: pass a scipy "
+            "sparse matrix, a dense array, or a paper_2501_19013_b200 DeviceOperator")
+    try:
+        ref = weakref.ref(K)
+    except TypeError:
+        return op
+    _cache[key] = (ref, op)
+    weakref.finalize(K, _cache.pop, key, None)
+    return op

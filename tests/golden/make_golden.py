@@ -1,0 +1,217 @@
+"""Generate golden vectors by running the REFERENCE package (read-only at
+/root/reference/pkg/src) in this container.
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+The fixtures pin the CPU oracle (oracle/timeint.py) and the device parity
+tests to the reference's own outputs.  The reference does not exist on the GPU
+box; only the committed .npz files travel.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+import scipy.sparse as sp
+
+REF = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF))
+sys.dont_write_bytecode = True
+
+from wavecell import assembly as A                      # noqa: E402
+from wavecell import basis as B                         # noqa: E402
+from wavecell import geometry as G                      # noqa: E402
+from wavecell import harness as H                       # noqa: E402
+from wavecell import linalg as LA                       # noqa: E402
+from wavecell import stabilization as S                 # noqa: E402
+from wavecell import timeint as T                       # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def save(name, **arrays):
+    np.savez_compressed(OUT / f"{name}.npz", **arrays)
+    size = (OUT / f"{name}.npz").stat().st_size
+    print(f"{name}.npz  {size / 1024:.1f} KiB")
+
+
+def csr_parts(prefix, M):
+    M = sp.csr_matrix(M)
+    return {f"{prefix}_indptr": M.indptr.astype(np.int64),
+            f"{prefix}_indices": M.indices.astype(np.int64),
+            f"{prefix}_data": M.data, f"{prefix}_shape": np.array(M.shape)}
+
+
+def bar_system():
+    h = 1.0 / 3.0
+    M = sp.diags([h / 2.0, h, h, h / 2.0]).tocsr()
+    K1 = np.array([[1.0, -1.0], [-1.0, 1.0]]) / h
+    K = np.zeros((4, 4))
+    for e in range(3):
+        K[e:e + 2, e:e + 2] += K1
+    return M, sp.csr_matrix(K)
+
+
+def gen_bar():
+    M, K = bar_system()
+    F = np.array([0.0, 1.0, 0.5, 0.2])
+    obs = sp.identity(4, format="csr")
+    f = lambda t: np.sin(6.0 * t)           # noqa: E731
+    dt, n_t = 5e-3, 200
+    r_cdm = T.cdm_run(M, K, F, f, dt, n_t, obs_mat=obs)
+    r_nm = T.newmark_run(M, K, F, f, dt, n_t, obs_mat=obs)
+    r_imex = T.imex_run(M, K, F, f, dt, n_t, np.array([1, 2]), np.array([0, 3]), obs_mat=obs)
+    psi0 = np.array([0.1, 0.0, -0.2, 0.05])
+    v0 = np.array([0.0, 0.3, 0.1, -0.1])
+    r_init = T.cdm_run(M, K, F, np.cos, 1e-2, 100, obs_mat=obs, psi0=psi0, v0=v0)
+    Mc = sp.csr_matrix(M.toarray() + 0.05 * np.ones((4, 4)))
+    r_imex_c = T.imex_run(Mc, K, F, f, dt, n_t, np.arange(4), np.array([], dtype=int),
+                          obs_mat=obs)
+    save("bar", M=M.toarray(), Mc=Mc.toarray(), K=K.toarray(), F=F, dt=dt, n_t=n_t,
+         cdm_obs=r_cdm.obs, cdm_psi=r_cdm.psi, nm_obs=r_nm.obs, imex_obs=r_imex.obs,
+         imex_psi=r_imex.psi, imexc_obs=r_imex_c.obs, imexc_vdot=r_imex_c.psi_dot,
+         psi0=psi0, v0=v0, init_obs=r_init.obs, init_psi=r_init.psi)
+
+
+def gen_scalar():
+    M = sp.csr_matrix(np.array([[1.0]]))
+    K = sp.csr_matrix(np.array([[1.0]]))
+    r = T.cdm_run(M, K, np.zeros(1), lambda t: 0.0, 1.99, 10000,
+                  obs_mat=sp.identity(1, format="csr"), psi0=[1.0])
+    try:
+        T.cdm_run(M, K, np.zeros(1), lambda t: 0.0, 2.01, 10000, psi0=[1.0])
+        raise AssertionError("expected divergence")
+    except T.DivergenceError as e:
+        step, amp = e.step, e.amplitude
+    save("scalar", stable_obs=r.obs, stable_psi=r.psi, div_step=step, div_amp=amp)
+
+
+def gen_rand10():
+    rng = np.random.default_rng(6)
+    n = 10
+    M = sp.diags(rng.uniform(0.5, 2.0, n)).tocsr()
+    Am = rng.standard_normal((n, n))
+    K = sp.csr_matrix(Am @ Am.T + n * np.eye(n))
+    F = rng.standard_normal(n)
+    psi0 = rng.standard_normal(n)
+    lam, it = LA.max_gen_eig(K, M)
+    dt = 0.5 * LA.dt_crit(K, M)
+    r = T.cdm_run(M, K, F, lambda t: np.sin(3.0 * t), dt, 200,
+                  obs_mat=sp.identity(n, format="csr"), psi0=psi0)
+    save("rand10", M=M.diagonal(), K=K.toarray(), F=F, psi0=psi0, lam=lam, iters=it, dt=dt,
+         obs=r.obs, psi=r.psi)
+
+
+def scm_desc(grid, cache, params, rho=1.0, c=1.0):
+    """The matrix-free description of a reference Lagrange system."""
+    spec = grid.spec
+    n = spec.p + 1
+    h = grid.h
+    sk = rho * c * c * (h / 2.0)
+    m1, k1 = cache._uncut_1d(0)
+    cut = [tuple(int(v) for v in ijk) for ijk in grid.kept
+           if grid.classes[tuple(ijk)] == G.ElementClass.CUT]
+    n_e = spec.n_e
+    cut_lex = np.array([(i * n_e + j) * n_e + k for i, j, k in cut], dtype=np.int64)
+    order = np.argsort(cut_lex)
+    cut_K = np.stack([sk * (cache.cut_element(cut[o]).K_in
+                            + params.alpha * cache.cut_element(cut[o]).K_out)
+                      for o in order]) if cut else np.zeros((0, n ** 3, n ** 3))
+    return dict(dim=3, p=spec.p, n_e=np.array([n_e] * 3), k1=k1, m1=m1, sk=sk,
+                cell_class=np.asarray(grid.classes, dtype=np.int8).ravel(),
+                lex_of_compact=grid.dofmap.lex_of_compact.astype(np.int64),
+                cut_cells=cut_lex[order], cut_K=cut_K,
+                c_idx=grid.dofmap.c_idx.astype(np.int64),
+                d_idx=grid.dofmap.d_idx.astype(np.int64))
+
+
+def gen_cube(name, p, n_e, alpha, depth, n_t, store_csr, lumping="hrz"):
+    geom = G.ImmersedGeometry.from_angles(0.3, 0.5, (10.0, 10.0, 10.0))
+    grid = G_grid = A.Grid.build(geom, B.BasisSpec(family="lagrange", p=p, n_e=n_e))
+    cache = A.ElementIntegralCache(G_grid, octree_depth=depth)
+    params = S.StabilizationParams(alpha=alpha, lumping=lumping)
+    system = A.assemble(grid, params, source=A.benchmark_source(0.3), cache=cache)
+    obs = H.observer_matrix(grid)
+    desc = scm_desc(grid, cache, params)
+    lam, it = LA.max_gen_eig(system.K, system.M, tol=1e-7, seed=0)
+    dt = T.select_dt(2.0 / np.sqrt(lam))
+    f = lambda t: A.ricker(t, 10.0)         # noqa: E731
+    r = T.cdm_run(system.M, system.K, system.F_s, f, dt, n_t, obs_mat=obs)
+    rng = np.random.default_rng(123)
+    X = rng.standard_normal((system.n_dof, 2))
+    KX = system.K @ X
+    extra = csr_parts("K", system.K) if store_csr else {}
+    save(name, **desc, M=system.M.diagonal(), F=system.F_s, **csr_parts("obs", obs),
+         lam=lam, iters=it, dt=dt, n_t=n_t, psi=r.psi, obs=r.obs, X=X, KX=KX,
+         K_abs_sum=np.abs(system.K).sum(axis=1).A1, **extra)
+
+
+def gen_cube_imex(name, p, n_e, alpha, depth, n_t):
+    geom = G.ImmersedGeometry.from_angles(0.3, 0.5, (10.0, 10.0, 10.0))
+    grid = A.Grid.build(geom, B.BasisSpec(family="lagrange", p=p, n_e=n_e))
+    cache = A.ElementIntegralCache(grid, octree_depth=depth)
+    params = S.StabilizationParams(alpha=alpha)
+    system = A.assemble(grid, params, source=A.benchmark_source(0.3), cache=cache)
+    obs = H.observer_matrix(grid)
+    dm = grid.dofmap
+    dtd = T.imex_critical_time_step(system.K, system.M, dm.d_idx, tol=1e-7)
+    dt = 0.9 * dtd
+    f = lambda t: A.ricker(t, 10.0)         # noqa: E731
+    r = T.imex_run(system.M, system.K, system.F_s, f, dt, n_t, dm.c_idx, dm.d_idx,
+                   obs_mat=obs)
+    desc = scm_desc(grid, cache, params)
+    save(name, **desc, **csr_parts("M", system.M), **csr_parts("K", system.K),
+         F=system.F_s, **csr_parts("obs", obs), dtd=dtd, dt=dt, n_t=n_t, psi=r.psi,
+         obs=r.obs)
+
+
+def gen_basis():
+    """1D ingredients of the spectral-cell / B-spline discretisation."""
+    out = {}
+    x = np.linspace(-1.0, 1.0, 13)
+    for p in range(1, 8):
+        g = B.gll_rule(p)
+        out[f"gll{p}_x"], out[f"gll{p}_w"] = g.nodes, g.weights
+        V, D = B.lagrange_eval(g.nodes, x)
+        out[f"lag{p}_V"], out[f"lag{p}_D"] = V, D
+        gl = B.gl_rule(p + 1)
+        out[f"gl{p + 1}_x"], out[f"gl{p + 1}_w"] = gl.nodes, gl.weights
+    for p in range(1, 6):
+        spec = B.BasisSpec("lagrange", p, 2)
+        geom = G.ImmersedGeometry.from_angles(0.3, 0.5, (0.0, 0.0, 0.0))
+        grid = A.Grid.build(geom, spec, boundary_fitted=True)
+        cache = A.ElementIntegralCache(grid, octree_depth=2)
+        m1, k1 = cache._uncut_1d(0)
+        out[f"m1_{p}"], out[f"k1_{p}"] = m1, k1
+        tabs = cache._dyadic_tables(0)
+        out[f"dy{p}_m1"], out[f"dy{p}_k1"] = tabs["m1"], tabs["k1"]
+    for p in (2, 3):
+        knots = B.open_uniform_knots(7, p)
+        pts = np.linspace(0.0, 1.0, 29)
+        span, V, D = B.bspline_eval(knots, p, pts)
+        out[f"bs{p}_span"], out[f"bs{p}_V"], out[f"bs{p}_D"] = span, V, D
+        spec = B.BasisSpec("bspline", p, 7)
+        for e in (0, 1, 3, 6):
+            Ve, De = spec.eval_element(e, x, knots=knots)
+            out[f"bs{p}_e{e}_V"], out[f"bs{p}_e{e}_D"] = Ve, De
+    save("basis", **out)
+
+
+def gen_lumping():
+    rng = np.random.default_rng(3)
+    C = rng.standard_normal((5, 8, 8))
+    Ms = np.einsum("bij,bkj->bik", C, C) + 8.0 * np.eye(8)
+    save("lumping", M=Ms, hrz=S.hrz_lump(Ms), rowsum=S.row_sum_lump(Ms))
+
+
+if __name__ == "__main__":
+    gen_bar()
+    gen_scalar()
+    gen_rand10()
+    gen_basis()
+    gen_lumping()
+    gen_cube("cube_p2n4", p=2, n_e=4, alpha=1e-6, depth=2, n_t=300, store_csr=True)
+    gen_cube("cube_p3n6", p=3, n_e=6, alpha=1e-8, depth=3, n_t=200, store_csr=False)
+    gen_cube_imex("cube_imex_p2n4", p=2, n_e=4, alpha=1e-12, depth=2, n_t=150)
