@@ -1,0 +1,110 @@
+"""BASELINE.json workloads as seeded synthetic problems.
+
+BASELINE names five configurations but no generator for their random voids
+or source points; the choices fixed here (and recorded in DESIGN.md) are:
+
+* void centres ~ U(0.05, 0.95)^d, radii ~ U(r_min, r_max), drawn in that
+  order from ``np.random.default_rng(seed)``; overlaps allowed;
+* the Ricker point source (f_e = 10, src/assembly.py:43-49) sits at the first
+  ``U(0, 1)^d`` draw of the same generator that lies in the material and in
+  a kept cell;
+* rho = c = 1, psi0 = v0 = 0; lumped mass: GLL nodal on uncut cells, HRZ on
+  cut cells (PAPER section 2.4; row-sum can go indefinite);
+* two observers: the source point and the domain centre (or the nearest
+  material point to it).
+
+The reference geometry (rotated cube) is not used by BASELINE; its own
+benchmark is covered by the golden tests.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .geometry import BallVoids
+from .grid import Grid
+from .problem import ScmProblem
+
+
+@dataclass(frozen=True)
+class ScmConfig:
+    name: str
+    dim: int
+    p: int
+    n_e: int
+    alpha: float
+    depth: int
+    n_t: int
+    fixed_voids: tuple = ()          # ((centre...), r) pairs
+    n_random: int = 0
+    r_range: tuple = (0.0, 0.0)
+    seed: int = 0
+    f_e: float = 10.0
+    safety: float = 0.9
+
+    def scaled(self, n_e: int, n_t: int | None = None) -> "ScmConfig":
+        """Same geometry at another resolution (parity tests at small sizes)."""
+        from dataclasses import replace
+        return replace(self, n_e=int(n_e), n_t=self.n_t if n_t is None else int(n_t),
+                       name=f"{self.name}@{n_e}")
+
+
+CONFIGS = {
+    # 1: 2D SCM p=4, 32x32, centred circular void r=0.25, quadtree depth 3
+    "config1": ScmConfig("config1", 2, 4, 32, 1e-4, 3, 1000,
+                         fixed_voids=(((0.5, 0.5), 0.25),)),
+    # 2: same set-up at 512x512 with 5 random voids r in [0.02, 0.08], 2000 steps
+    "config2": ScmConfig("config2", 2, 4, 512, 1e-4, 3, 2000, n_random=5,
+                         r_range=(0.02, 0.08)),
+    # 5: 3D SCM p=3 on 192^3, centred sphere r=0.3 + 50 random r in [0.005, 0.02]
+    "config5": ScmConfig("config5", 3, 3, 192, 1e-4, 2, 500,
+                         fixed_voids=(((0.5, 0.5, 0.5), 0.3),), n_random=50,
+                         r_range=(0.005, 0.02)),
+}
+
+
+def make_geometry(cfg: ScmConfig, rng):
+    centres = [np.asarray(c, dtype=float) for c, _ in cfg.fixed_voids]
+    radii = [float(r) for _, r in cfg.fixed_voids]
+    if cfg.n_random:
+        cs = rng.uniform(0.05, 0.95, size=(cfg.n_random, cfg.dim))
+        rs = rng.uniform(cfg.r_range[0], cfg.r_range[1], size=cfg.n_random)
+        centres += list(cs)
+        radii += list(rs)
+    return BallVoids(cfg.dim, np.array(centres).reshape(-1, cfg.dim), np.array(radii))
+
+
+def pick_source(grid: Grid, rng, max_tries: int = 100000):
+    for _ in range(max_tries):
+        x = rng.uniform(0.0, 1.0, size=grid.dim)
+        if not bool(grid.geom.contains(x[None])[0]):
+            continue
+        if grid.classes[tuple(grid.locate(x))] == 0:
+            continue
+        return x
+    raise RuntimeError("no admissible source point found")
+
+
+def build_scm(cfg: ScmConfig) -> ScmProblem:
+    """Grid + operators + source + observers for one SCM configuration."""
+    rng = np.random.default_rng(cfg.seed)
+    geom = make_geometry(cfg, rng)
+    grid = Grid.build(geom, "lagrange", cfg.p, cfg.n_e)
+    prob = ScmProblem.build(grid, cfg.alpha, cfg.depth)
+    x_s = pick_source(grid, rng)
+    prob.set_point_source(x_s)
+    centre = np.full(cfg.dim, 0.5)
+    if not bool(geom.contains(centre[None])[0]) or grid.classes[tuple(grid.locate(centre))] == 0:
+        centre = pick_source(grid, rng)
+    prob.set_observers([x_s, centre])
+    return prob
+
+
+def ricker(t, f_e=10.0):
+    """Ricker wavelet (src/assembly.py:43-49)."""
+    t = np.asarray(t, dtype=float)
+    t_s = 2.0 * np.sqrt(6.0) / (np.pi * f_e)
+    q = np.pi * f_e * (t - t_s)
+    return (1.0 - 2.0 * q * q) * np.exp(-q * q)

@@ -1,0 +1,162 @@
+"""Classified Cartesian cell grid and compact DOF map in d = 2 or 3 dimensions.
+
+Restates ``Grid.build`` / ``Grid.dofmap`` / ``_discard_slivers`` of the
+reference (src/assembly.py:92-211) for any dimension and any geometry
+plug-in, vectorised so 192^3-cell grids build in seconds:
+
+* cells are numbered lexicographically, axis 0 slowest;
+* DOFs are numbered ``lex = (f_0 * n1 + f_1) [* n1 + f_2]`` (axis 0 slowest,
+  src/assembly.py:85-89) and compacted to the functions supported on kept
+  (inside or cut) cells (src/assembly.py:159-180);
+* ``c`` = DOFs touching a cut cell, ``d`` = the complement.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import cached_property
+
+import numpy as np
+
+from .basis import Basis1D
+from .geometry import CUT, INSIDE, MIN_VOLUME_FRACTION, OUTSIDE
+
+
+@dataclass
+class DofMap:
+    n1: int
+    dim: int
+    lex_of_compact: np.ndarray   # (n_dof,) int64
+    c_idx: np.ndarray            # sorted compact ids touching a cut cell
+    d_idx: np.ndarray            # complement
+
+    @property
+    def n_dof(self) -> int:
+        return int(self.lex_of_compact.shape[0])
+
+    @cached_property
+    def compact_of_lex(self) -> np.ndarray:
+        out = np.full(self.n1 ** self.dim, -1, dtype=np.int64)
+        out[self.lex_of_compact] = np.arange(self.n_dof, dtype=np.int64)
+        return out
+
+    def cell_dofs(self, basis: Basis1D, cell) -> np.ndarray:
+        """Compact DOF ids of one cell's (p+1)^d functions, last axis fastest."""
+        f0 = [int(basis.first_func(e)) for e in cell]
+        ranges = [np.arange(f, f + basis.p + 1) for f in f0]
+        lex = ranges[0]
+        for r in ranges[1:]:
+            lex = lex[:, None] * self.n1 + r[None, :]
+            lex = lex.ravel()
+        return self.compact_of_lex[lex]
+
+
+def _dilate(mask: np.ndarray, basis: Basis1D) -> np.ndarray:
+    """Node mask: a function is marked if any cell of its support is
+    (separable OR over the 2^d incident cells, axis by axis)."""
+    step = basis.p if basis.family == "lagrange" else 1
+    n_e, n1 = basis.n_e, basis.n_funcs
+    out = mask
+    for ax in range(mask.ndim):
+        shape = list(out.shape)
+        shape[ax] = n1
+        new = np.zeros(shape, dtype=bool)
+        for a in range(basis.p + 1):
+            sl = [slice(None)] * out.ndim
+            sl[ax] = slice(a, a + step * (n_e - 1) + 1, step)
+            new[tuple(sl)] |= out
+        out = new
+    return out
+
+
+class Grid:
+    """Cells of an n_e^d grid over the geometry's domain box, classified."""
+
+    def __init__(self, geom, basis: Basis1D, origin, h, classes):
+        self.geom = geom
+        self.basis = basis
+        self.dim = classes.ndim
+        self.origin = np.asarray(origin, dtype=float)
+        self.h = float(h)
+        self.classes = classes
+
+    @classmethod
+    def build(cls, geom, family: str, p: int, n_e: int,
+              min_volume_fraction: float = MIN_VOLUME_FRACTION, chunk: int = 1 << 20):
+        dim = geom.dim
+        basis = Basis1D(family, p, n_e)
+        origin = np.asarray(geom.domain_lo, dtype=float)
+        h = float((geom.domain_hi[0] - geom.domain_lo[0]) / n_e)
+        n_cells = n_e ** dim
+        classes = np.empty(n_cells, dtype=np.int8)
+        for s in range(0, n_cells, chunk):
+            ids = np.arange(s, min(n_cells, s + chunk))
+            ijk = np.stack(np.unravel_index(ids, (n_e,) * dim), axis=1)
+            lo = origin + ijk * h
+            classes[s:s + ids.shape[0]] = geom.classify_boxes(lo, lo + h)
+        classes = classes.reshape((n_e,) * dim)
+        _discard_slivers(geom, classes, origin, h, min_volume_fraction)
+        return cls(geom, basis, origin, h, classes)
+
+    @property
+    def n_e(self) -> int:
+        return self.basis.n_e
+
+    @property
+    def p(self) -> int:
+        return self.basis.p
+
+    @cached_property
+    def kept(self) -> np.ndarray:
+        return np.argwhere(self.classes != OUTSIDE)
+
+    @cached_property
+    def cut_lex(self) -> np.ndarray:
+        """Lex ids of the cut cells, ascending."""
+        return np.flatnonzero(self.classes.ravel() == CUT).astype(np.int64)
+
+    @cached_property
+    def dofmap(self) -> DofMap:
+        kept_nodes = _dilate(self.classes != OUTSIDE, self.basis)
+        cut_nodes = _dilate(self.classes == CUT, self.basis)
+        lex_of_compact = np.flatnonzero(kept_nodes.ravel()).astype(np.int64)
+        n1 = self.basis.n_funcs
+        compact = np.full(n1 ** self.dim, -1, dtype=np.int64)
+        compact[lex_of_compact] = np.arange(lex_of_compact.shape[0], dtype=np.int64)
+        c_idx = np.sort(compact[np.flatnonzero(cut_nodes.ravel())])
+        d_mask = np.ones(lex_of_compact.shape[0], dtype=bool)
+        d_mask[c_idx] = False
+        dm = DofMap(n1=n1, dim=self.dim, lex_of_compact=lex_of_compact, c_idx=c_idx,
+                    d_idx=np.flatnonzero(d_mask).astype(np.int64))
+        dm.__dict__["compact_of_lex"] = compact
+        return dm
+
+    @property
+    def n_dof(self) -> int:
+        return self.dofmap.n_dof
+
+    def cell_box(self, ijk):
+        lo = self.origin + np.asarray(ijk, dtype=float) * self.h
+        return lo, lo + self.h
+
+    def locate(self, x):
+        """Cell index containing point x (clamped to the grid)."""
+        idx = np.floor((np.asarray(x, dtype=float) - self.origin) / self.h).astype(int)
+        return np.clip(idx, 0, self.n_e - 1)
+
+
+def _discard_slivers(geom, classes, origin, h, min_volume_fraction):
+    """Demote cut cells with physical fraction below the threshold to outside
+    (src/assembly.py:187-211)."""
+    if min_volume_fraction <= 0.0:
+        return
+    flat = classes.reshape(-1)
+    cut = np.flatnonzero(flat == CUT)
+    if cut.shape[0] == 0:
+        return
+    ijk = np.stack(np.unravel_index(cut, classes.shape), axis=1)
+    lo = origin + ijk * h
+    for s in geom.sliver_candidates(lo, h):
+        frac = geom.volume_fraction(lo[s], lo[s] + h, stop_above=min_volume_fraction)
+        if frac < min_volume_fraction:
+            flat[cut[s]] = OUTSIDE

@@ -1,0 +1,193 @@
+"""Spectral-cell (GLL Lagrange) systems in the form the device consumes.
+
+``ScmProblem.build`` restates the reference assembly (src/assembly.py:518-603)
+without ever forming the global CSR stiffness: it keeps the shared uncut 1D
+factors ``m1, k1`` (src/assembly.py:263-295), the physical cut-cell
+stiffness ``K_o = sk (K_in + alpha K_out)`` (src/assembly.py:582) and the
+lumped diagonal mass (GLL nodal on uncut cells, src/assembly.py:289-291;
+HRZ or row-sum on cut cells, src/assembly.py:586-592).  ``csr_stiffness``
+assembles the same operator as a scipy CSR for cross-checks at small sizes.
+
+Sources and observers are point evaluations of the basis
+(src/harness.py:59-98): ``F_s = rho * alpha(x_s) * N(x_s)``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from .basis import Basis1D, gll_rule, uncut_1d
+from .cutcell import CutCellIntegrator, hrz_lump, row_sum_lump
+from .geometry import CUT, INSIDE, OUTSIDE
+from .grid import Grid
+
+
+def _kron_list(mats):
+    out = mats[0]
+    for m in mats[1:]:
+        out = np.kron(out, m)
+    return out
+
+
+@dataclass
+class ScmProblem:
+    grid: Grid
+    rho: float
+    c: float
+    alpha: float
+    depth: int
+    lumping: str
+    sk: float
+    sm: float
+    m1: np.ndarray
+    k1: np.ndarray
+    cut_K: np.ndarray          # (n_cut, L, L) physical stiffness of cut cells
+    cut_M: np.ndarray          # (n_cut, L) lumped mass of cut cells
+    m_diag: np.ndarray         # (n_dof,) assembled lumped mass
+    F_s: np.ndarray = field(default=None)
+    obs_mat: sp.csr_matrix = field(default=None)
+    source_point: np.ndarray = field(default=None)
+
+    # ------------------------------------------------------------ build --
+    @classmethod
+    def build(cls, grid: Grid, alpha: float, depth: int, rho: float = 1.0, c: float = 1.0,
+              lumping: str = "hrz"):
+        if grid.basis.family != "lagrange":
+            raise ValueError("ScmProblem needs the Lagrange (GLL) family")
+        if lumping not in ("hrz", "row_sum"):
+            raise ValueError("the explicit device path needs a lumped cut-cell mass")
+        d, p, h = grid.dim, grid.p, grid.h
+        n = p + 1
+        L = n ** d
+        # src/assembly.py:504-505 for d = 3; (h/2)^(d-2) and (h/2)^d in general
+        sk = rho * c * c * (h / 2.0) ** (d - 2)
+        sm = rho * (h / 2.0) ** d
+        m1, k1 = uncut_1d(grid.basis, 0)
+        cut = grid.cut_lex
+        integ = CutCellIntegrator(grid, depth)
+        cut_K = np.empty((cut.shape[0], L, L))
+        cut_M = np.empty((cut.shape[0], L))
+        shape = (grid.n_e,) * d
+        for j, cl in enumerate(cut):
+            ijk = np.unravel_index(int(cl), shape)
+            Mi, Mo, Ki, Ko = integ.integrate(ijk)
+            cut_K[j] = sk * (Ki + alpha * Ko)
+            M_o = sm * (Mi + alpha * Mo)
+            cut_M[j] = hrz_lump(M_o) if lumping == "hrz" else row_sum_lump(M_o)
+        prob = cls(grid=grid, rho=rho, c=c, alpha=alpha, depth=depth, lumping=lumping,
+                   sk=sk, sm=sm, m1=m1, k1=k1, cut_K=cut_K, cut_M=cut_M,
+                   m_diag=np.zeros(0))
+        prob.m_diag = prob._assemble_mass()
+        return prob
+
+    @property
+    def n_dof(self) -> int:
+        return self.grid.n_dof
+
+    def _assemble_mass(self) -> np.ndarray:
+        """Diagonal mass: sm * (w (x) w [(x) w]) on uncut kept cells, the lumped
+        cut-cell vectors elsewhere, summed per DOF."""
+        g = self.grid
+        d, p, n_e = g.dim, g.p, g.n_e
+        n1 = g.basis.n_funcs
+        w = gll_rule(p)[1]
+        uncut = (g.classes == INSIDE).astype(float)
+        node = np.zeros((n1,) * d)
+        for local in np.ndindex(*([p + 1] * d)):
+            wt = self.sm * np.prod([w[a] for a in local])
+            sl = tuple(slice(a, a + p * (n_e - 1) + 1, p) for a in local)
+            node[sl] += wt * uncut
+        node = node.ravel()
+        m = node[g.dofmap.lex_of_compact]
+        cut = g.cut_lex
+        if cut.shape[0]:
+            dofs = self.cut_dofs()
+            np.add.at(m, dofs.ravel(), self.cut_M.ravel())
+        return m
+
+    def cut_dofs(self) -> np.ndarray:
+        """(n_cut, L) compact DOF ids of every cut cell."""
+        g = self.grid
+        shape = (g.n_e,) * g.dim
+        return np.stack([g.dofmap.cell_dofs(g.basis, np.unravel_index(int(c), shape))
+                         for c in g.cut_lex]) if g.cut_lex.size else \
+            np.zeros((0, (g.p + 1) ** g.dim), dtype=np.int64)
+
+    # ------------------------------------------------------------ points --
+    def point_row(self, x):
+        """(dofs, values) of the basis functions at a grid-frame point."""
+        g = self.grid
+        x = np.asarray(x, dtype=float)
+        idx = g.locate(x)
+        lo, _ = g.cell_box(idx)
+        xi = np.clip(2.0 * (x - lo) / g.h - 1.0, -1.0, 1.0)
+        V = [g.basis.eval(int(idx[k]), np.array([xi[k]]))[0][0] for k in range(g.dim)]
+        vals = _kron_list([v.reshape(1, -1) for v in V]).ravel()
+        dofs = g.dofmap.cell_dofs(g.basis, idx)
+        if np.any(dofs < 0):
+            raise ValueError("point lies in a discarded cell")
+        return dofs, vals, idx
+
+    def set_point_source(self, x_s):
+        """F_s = rho * alpha(x_s) * N(x_s): a Dirac load at x_s."""
+        dofs, vals, idx = self.point_row(x_s)
+        a = 1.0 if bool(self.grid.geom.contains(np.asarray(x_s)[None])[0]) else self.alpha
+        F = np.zeros(self.n_dof)
+        np.add.at(F, dofs, self.rho * a * vals)
+        self.F_s = F
+        self.source_point = np.asarray(x_s, dtype=float)
+        return F
+
+    def set_observers(self, points):
+        rows, cols, vals = [], [], []
+        for i, x in enumerate(points):
+            dofs, v, _ = self.point_row(x)
+            rows.extend([i] * dofs.shape[0])
+            cols.extend(dofs.tolist())
+            vals.extend(v.tolist())
+        self.obs_mat = sp.csr_matrix((vals, (rows, cols)), shape=(len(points), self.n_dof))
+        return self.obs_mat
+
+    # ----------------------------------------------------------- device --
+    def device_operator(self, device=None):
+        from ..operators import ScmOperator
+        g = self.grid
+        return ScmOperator(dim=g.dim, p=g.p, n_e=(g.n_e,) * g.dim, k1=self.k1, m1=self.m1,
+                           sk=self.sk, cell_class=g.classes.ravel(),
+                           lex_of_compact=g.dofmap.lex_of_compact, cut_cells=g.cut_lex,
+                           cut_K=self.cut_K, device=device)
+
+    def mass_matrix(self) -> sp.csr_matrix:
+        return sp.diags(self.m_diag).tocsr()
+
+    # -------------------------------------------------------------- CSR --
+    def csr_stiffness(self) -> sp.csr_matrix:
+        """Global stiffness as CSR (small problems; cross-checks only)."""
+        g = self.grid
+        d, p = g.dim, g.p
+        L = (p + 1) ** d
+        mats = [self.m1] * d
+        K_ref = np.zeros((L, L))
+        for k in range(d):
+            parts = list(mats)
+            parts[k] = self.k1
+            K_ref += _kron_list(parts)
+        K_ref *= self.sk
+        shape = (g.n_e,) * d
+        uncut = np.flatnonzero(g.classes.ravel() == INSIDE)
+        rows, cols, vals = [], [], []
+        rr, cc = np.divmod(np.arange(L * L), L)
+        for cl in uncut:
+            dofs = g.dofmap.cell_dofs(g.basis, np.unravel_index(int(cl), shape))
+            rows.append(dofs[rr]); cols.append(dofs[cc]); vals.append(K_ref.ravel())
+        for j, dofs in enumerate(self.cut_dofs()):
+            rows.append(dofs[rr]); cols.append(dofs[cc]); vals.append(self.cut_K[j].ravel())
+        if not rows:
+            return sp.csr_matrix((self.n_dof, self.n_dof))
+        A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                          shape=(self.n_dof, self.n_dof)).tocsr()
+        A.eliminate_zeros()
+        return A
