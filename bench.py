@@ -1,0 +1,353 @@
+"""Benchmark: DOF-updates/s of explicit wave stepping (BASELINE.json metric).
+
+Workload (N=1): BASELINE config 2 -- 2D acoustic spectral-cell method, GLL
+p=4 on 512x512 cells, 5 seeded random circular voids (r 0.02-0.08), HRZ-lumped
+cut cells, Ricker point source, 2000 central-difference steps at 0.9 x the
+power-iteration critical step.  One bench "step" = one full ``cdm_run`` of the
+configuration (2000 time steps) through the device plan.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Arms
+* ``b200`` (default): ``value`` = DOF-updates/s with all inputs resident in
+  HBM (CUDA events on the library's stream, L2 flushed between steps);
+  ``e2e`` = the same metric through the public ``cdm_run`` with host arrays
+  (H2D of M, F_s, force table and D2H of psi and observers inside the timed
+  region); ``roofline`` for the fused SCM step kernel; ``cpu_baseline`` = the
+  oracle's C restatement of the reference CSR loop on the host cores.
+* ``reference``: the reference CPU path (oracle C port of the CSR CDM loop,
+  all host threads) on the same configuration; bounded sample per step.
+
+N>1 (torchrun): every rank runs an independent replica of the workload on its
+own GPU (config 2 is a single-GPU configuration; weak scaling, no data-path
+collective); timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "DOF-updates/s (DOFs×steps/s) of explicit wave stepping; % of HBM roofline"
+UNIT = "DOF-updates/s"
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def reduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def build_workload(name: str):
+    from paper_2501_19013_b200.setup.configs import CONFIGS, build_scm
+    cfg = CONFIGS[name]
+    t0 = time.perf_counter()
+    prob = build_scm(cfg)
+    return cfg, prob, time.perf_counter() - t0
+
+
+def cpu_sample(prob, dt, target_s=10.0, threads=0):
+    """Oracle C port of the reference CSR CDM loop on a bounded sample."""
+    from oracle import cpu
+    from paper_2501_19013_b200.setup.configs import ricker
+    from paper_2501_19013_b200.timeint import force_table
+    K = cpu.scm_csr(prob)
+    f = lambda t: ricker(t, 10.0)  # noqa: E731
+    probe = 3
+    t0 = time.perf_counter()
+    cpu.cdm_run(K, prob.m_diag, prob.F_s, force_table(f, dt, probe), dt, probe, threads=threads)
+    per = (time.perf_counter() - t0) / probe
+    n_s = int(max(3, min(2000, target_s / max(per, 1e-6))))
+    ft = force_table(f, dt, n_s)
+    t0 = time.perf_counter()
+    cpu.cdm_run(K, prob.m_diag, prob.F_s, ft, dt, n_s, threads=threads)
+    el = time.perf_counter() - t0
+    used = threads if threads > 0 else cpu.max_threads()
+    return prob.n_dof * n_s / el, n_s, el, used, K
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from oracle import cpu
+    cfg, prob, _ = build_workload(args.config)
+    lam = _host_lambda(prob)
+    dt = cfg.safety * 2.0 / np.sqrt(lam)
+    from paper_2501_19013_b200.setup.configs import ricker
+    from paper_2501_19013_b200.timeint import force_table
+    K = cpu.scm_csr(prob)
+    f = lambda t: ricker(t, 10.0)  # noqa: E731
+    threads = cpu.max_threads()
+    probe = 2
+    t0 = time.perf_counter()
+    cpu.cdm_run(K, prob.m_diag, prob.F_s, force_table(f, dt, probe), dt, probe, threads=threads)
+    per = (time.perf_counter() - t0) / probe
+    n_s = int(max(2, min(cfg.n_t, args.cpu_seconds / max(per, 1e-6))))
+    ft = force_table(f, dt, n_s)
+    for _ in range(args.warmup):
+        cpu.cdm_run(K, prob.m_diag, prob.F_s, ft, dt, min(n_s, 2), threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu.cdm_run(K, prob.m_diag, prob.F_s, ft, dt, n_s, threads=threads)
+        times.append(time.perf_counter() - t0)
+    value = prob.n_dof * n_s * args.steps / sum(times)
+    sample = (f"{n_s} of {cfg.n_t} CDM steps per bench step on the config CSR "
+              f"({prob.n_dof} DOFs, nnz {K.nnz}); host {cpu.host_cpu_model()}, "
+              f"nproc {cpu.host_cores()}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, prob),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _host_lambda(prob):
+    """Critical step for the CPU arm: oracle power iteration on the CSR."""
+    from oracle import cpu, timeint as O
+    K = cpu.scm_csr(prob)
+    lam, _ = O.max_gen_eig(K, prob.mass_matrix(), tol=1e-7, seed=0)
+    return lam
+
+
+def workload_config(cfg, prob):
+    g = prob.grid
+    return {"workload": f"{cfg.name}: {g.dim}D acoustic SCM GLL p={g.p}, {g.n_e}^{g.dim} cells, "
+                        f"{len(prob.grid.geom.radii)} circular voids, alpha={cfg.alpha}, "
+                        f"HRZ cut cells, Ricker point source, {cfg.n_t} CDM steps at 0.9 dt_crit",
+            "n_dof": int(prob.n_dof), "n_t": int(cfg.n_t), "n_cut": int(g.cut_lex.shape[0]),
+            "seed": cfg.seed,
+            "l2": "flushed (256 MiB write) between bench steps; inside one run the 131 MB "
+                  "working set is re-read every time step as the real loop does"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--config", default="config2")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        barrier(world)
+        return
+
+    import torch
+    os.environ["WAVECELL_B200_DEVICE"] = str(local)
+    torch.cuda.set_device(local)
+    from paper_2501_19013_b200 import _lib
+    from paper_2501_19013_b200.linalg import max_gen_eig
+    from paper_2501_19013_b200.setup.configs import ricker
+    from paper_2501_19013_b200.timeint import CdmPlan, cdm_run, force_table
+
+    cfg, prob, t_build = build_workload(args.config)
+    ctx = _lib.context(local)
+    op = prob.device_operator(device=local)
+    M = prob.mass_matrix()
+    t0 = time.perf_counter()
+    lam, iters = max_gen_eig(op, M, tol=1e-7, seed=cfg.seed, device=local)
+    t_eig = time.perf_counter() - t0
+    dt = cfg.safety * 2.0 / np.sqrt(lam)
+    n_t = cfg.n_t
+    f = lambda t: ricker(t, cfg.f_e)  # noqa: E731
+    ft = force_table(f, dt, n_t)
+    plan = CdmPlan(M, op, prob.F_s, obs_mat=prob.obs_mat, device=local)
+    n = prob.n_dof
+    dev = torch.device("cuda", local)
+    d_ft = torch.from_numpy(ft).to(dev)
+    d_psi = torch.empty(n, dtype=torch.float64, device=dev)
+    d_obs = torch.empty(plan.n_obs * (n_t + 1), dtype=torch.float64, device=dev)
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)  # 256 MiB > L2
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    torch.cuda.synchronize()
+    lib = _lib.load()
+
+    def run_device():
+        div = _lib.Divergence()
+        tm = _lib.Timings()
+        code = lib.wcb_cdm_plan_run_device(plan.handle, d_ft.data_ptr(), dt, n_t, None, None,
+                                           d_psi.data_ptr(), d_obs.data_ptr(),
+                                           _lib.C.byref(div), _lib.C.byref(tm))
+        _lib.check(code)
+        return tm.rhs
+
+    for _ in range(args.warmup):
+        run_device()
+    torch.cuda.synchronize()
+    barrier(world)
+    launches0 = ctx.launches
+    times, loop_times = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            loop_times.append(run_device())
+            ev1.record(stream)
+            ev1.synchronize()
+            times.append(ev0.elapsed_time(ev1) * 1e-3)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = ctx.launches - launches0
+    total = reduce_max(sum(times), world)
+    value = n * n_t * args.steps * world / total
+    psi = d_psi.cpu().numpy()
+    assert np.all(np.isfinite(psi)), "non-finite field"
+
+    # end to end through the public API (host arrays in, host arrays out)
+    e2e_times = []
+    for i in range(max(2, min(args.steps, 5))):
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        r = cdm_run(M, op, prob.F_s, f, dt, n_t, obs_mat=prob.obs_mat, device=local)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_t = reduce_max(sum(e2e_times) / len(e2e_times), world)
+    e2e_value = n * n_t * world / e2e_t
+    h2d = 8 * (2 * n + max(n_t, 1)) + prob.obs_mat.nnz * 24 + 8 * (plan.n_obs + 1)
+    d2h = 8 * n + 8 * plan.n_obs * (n_t + 1)
+    rel = np.linalg.norm(r.psi - psi) / max(np.linalg.norm(psi), 1e-300)
+
+    # roofline of the fused step kernel: algorithmic bytes per time step
+    L = (prob.grid.p + 1) ** prob.grid.dim
+    n_cut = int(prob.grid.cut_lex.shape[0])
+    bytes_step = 32.0 * n + 8.0 * L * (L + 1) / 2 * n_cut
+    per_step_s = sum(loop_times) / (args.steps * n_t)
+    achieved = bytes_step / per_step_s / 1e9
+    peak, peak_kind = measured_peaks()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded voids and source, BASELINE config shapes)",
+            "config": workload_config(cfg, prob) | {
+                "parallelism": f"{world} independent replica(s), one per GPU",
+                "dt": dt, "lambda_max": lam, "power_iterations": iters,
+                "setup_s": round(t_build, 2), "power_iteration_s": round(t_eig, 3)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": f"k_scm2d<{prob.grid.p},STEP> + k_cut_apply per time step",
+                         "bytes_per_launch": bytes_step,
+                         "launch_us": per_step_s * 1e6, "peak_kind": peak_kind},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "rel_l2_vs_resident": rel},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary()}
+    if rank == 0 and not args.no_cpu:
+        cv, n_s, el, used, _ = cpu_sample(prob, dt, target_s=args.cpu_seconds)
+        from oracle import cpu
+        line["cpu_baseline"] = {
+            "value": cv, "unit": UNIT, "cores": used, "kind": "port",
+            "sample": f"{n_s} CDM steps of {cfg.name} on its CSR ({el:.1f} s), C/OpenMP "
+                      f"restatement of src/timeint.py:159-193; host {cpu.host_cpu_model()}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    barrier(world)
+
+
+if __name__ == "__main__":
+    main()
