@@ -11,24 +11,25 @@
 // src/assembly.py:85-89) padded by P rows above/below and PADJ columns on the
 // left, row pitch a multiple of 32 doubles, zeros at non-DOF slots.
 //
-// 2D kernel (one fused pass per step):
-//   * a warp owns a strip of 32 element columns (32*P node columns, lane t
-//     owns the P columns of element column t) and RP element rows; the 8 warps
-//     of a CTA stack vertically;
-//   * the warp streams down its rows.  Per node row it loads its P values
-//     (vector loads) and gets the neighbours' values by shuffles, contracts
-//     along y with m1/k1 (the "y pass", masked per cell), and accumulates the
-//     x pass into registers -- sum factorisation, no shared-memory staging;
-//   * the element-boundary row is shared by two element rows: its value is
-//     carry (from the row above) + own, in that fixed order, within a warp in
-//     registers and across warps through shared memory -- deterministic, no
-//     atomics (src/harness.py:462-485 bit-identity contract);
-//   * cut cells are masked out of the tensor pass; their dense K_o u_e is
-//     gathered per cut node by a small kernel into Ycut (fixed pair order)
-//     and added in the epilogue of the warps that own cut nodes;
-//   * epilogue: psi_new = 2 psi - psi_prev + dt^2 minv (f F - K psi), block
-//     max |psi_new| -> one atomicMax per CTA (src/timeint.py:179-190).
+// 2D kernel (one fused pass per step, no atomics, deterministic):
+//   * a warp owns a strip of 32 element columns (lane t owns the P node
+//     columns of element column t) and RP element rows; the 8 warps of a CTA
+//     stack vertically (consecutive row ranges of the same strip);
+//   * the warp streams down its rows.  Per node row: one vector load of the
+//     lane's P values, neighbour values by shuffles, the y contraction with
+//     m1/k1 (masked per cell), and the x contraction accumulated in
+//     registers (sum factorisation).  The next element row is prefetched
+//     into L1 while the current one is computed;
+//   * the node row shared by two element rows gets carry (row above) + own,
+//     in that fixed order -- in registers inside a warp, through shared memory
+//     between the warps of a CTA (warp 0 recomputes its carry-in row);
+//   * a cut cell is masked out of the tensor contraction and its dense
+//     K_o u_e is added by the lanes owning its columns (K_o stored
+//     transposed so a lane reads its rows contiguously);
+//   * epilogue: psi_new = 2 psi - psi_prev + dt^2 minv (f F - K psi) and the
+//     block max |psi_new| (one atomicMax per CTA), src/timeint.py:179-190.
 #include "wcb_internal.cuh"
+#include "wcb_tma.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -38,8 +39,9 @@
 namespace wcb {
 
 constexpr int PADJ = 32;
-constexpr int SCM_NW = 8;    // warps per CTA (stacked along x)
-constexpr int SCM_RP = 2;    // element rows per warp
+constexpr int NSTAGE = 2;    // TMA ring depth
+// element rows per tile = compute warps per CTA (bounded by shared memory)
+__host__ __device__ constexpr int rpe_for(int P) { return P <= 4 ? 8 : (P == 5 ? 4 : 2); }
 
 // y pass uses the unscaled 1D factors, the x pass carries sk:
 //   sk (k1_x (x) m1_y + m1_x (x) k1_y) = (sk k1)_x (x) m1_y + (sk m1)_x (x) k1_y
@@ -51,253 +53,297 @@ struct Mats2 {
     double xm[(P + 1) * (P + 1)];   // sk * m1, x pass
 };
 
+// Tile geometry of the 2D kernel: a tile is 32p node columns x RPE*p node rows.
+template <int P>
+struct Tile2 {
+    static constexpr int RPE = rpe_for(P);
+    static constexpr int TJ = 32 * P;                       // owned node columns
+    static constexpr int TI = RPE * P;                      // owned node rows
+    // TMA boxes must start 16-byte aligned: for odd P the u tile starts one
+    // column early and node columns sit at offset CO inside the tile
+    static constexpr int CO = P & 1;
+    static constexpr int UW = ((TJ + P + 1 + CO) + 1) / 2 * 2;  // cols J0-P-CO..J0+TJ, even
+    static constexpr int UH = TI + P + 1;                   // u tile rows (I0-P..I0+TI)
+    static constexpr size_t U_BYTES = (size_t)UW * UH * 8;
+    static constexpr size_t E_BYTES = (size_t)TJ * TI * 8;  // prev / minv tiles
+    static constexpr size_t OFF_PREV = (U_BYTES + 127) / 128 * 128;
+    static constexpr size_t OFF_MINV = OFF_PREV + (E_BYTES + 127) / 128 * 128;
+    static constexpr size_t STAGE = OFF_MINV + (E_BYTES + 127) / 128 * 128;
+    static constexpr size_t OFF_CARRY = NSTAGE * STAGE;     // [2][RPE+1][P][32]
+    static constexpr size_t OFF_BAR = OFF_CARRY + (size_t)2 * (RPE + 1) * P * 32 * 8;
+    static constexpr size_t SMEM = OFF_BAR + 8 * NSTAGE;
+};
+
 struct Scm2DGeo {
-    int64_t n_e;       // cells per axis
-    int64_t n1;        // nodes per axis
-    int64_t pitch;     // row pitch (doubles)
-    const uint8_t* mask;      // (n_e+2)^2, 1 = uncut kept cell, padded by one ring of 0
-    const uint8_t* wflags;    // per warp tile: bit0 kept node, bit1 cut node
+    int64_t n_e;              // cells per axis
+    int64_t n1;               // nodes per axis
+    const uint8_t* mask;      // (n_e+2)^2 cell codes, one ring of 0 around: 0 out, 1 uncut, 2 cut
+    const int32_t* cut_id;    // n_e^2 -> cut index or -1
+    const double* KT;         // n_cut * L * L, transposed physical cut stiffness
+    const uint8_t* cflags;    // per tile: 1 = owns a DOF
     int64_t n_strips;
-    const double* ycut;       // cut-cell contributions (state layout)
+    int64_t n_rtiles;
+    int64_t pitch;            // row pitch of the state (doubles)
 };
 
 enum { MODE_STEP = 0, MODE_APPLY = 1 };
 
+// One node row of the smem tile: y contraction (masked) then x contraction
+// accumulated into Y.  `row` points at tile column 0 of that row.
 template <int P>
-__device__ __forceinline__ void load_row(const double* __restrict__ u, int64_t rowbase,
-                                         int64_t Jl, int lane, double (&own)[P],
-                                         double (&left)[P], double& right) {
-    const double* p = u + rowbase + Jl + PADJ;
+__device__ __forceinline__ void row_contract(const Mats2<P>& mt, const double* row, int lane,
+                                             double chiR, double chiL, int c,
+                                             double (&Y)[P + 1][P]) {
+    constexpr int N = P + 1;
+    row += Tile2<P>::CO;
+    const double* own_p = row + P + lane * P;
+    double own[P];
     if constexpr ((P % 2) == 0) {
         #pragma unroll
         for (int j = 0; j < P; j += 2) {
-            double2 v = __ldg(reinterpret_cast<const double2*>(p + j));
+            double2 v = *reinterpret_cast<const double2*>(own_p + j);
             own[j] = v.x;
             own[j + 1] = v.y;
         }
     } else {
         #pragma unroll
-        for (int j = 0; j < P; ++j) own[j] = __ldg(p + j);
+        for (int j = 0; j < P; ++j) own[j] = own_p[j];
     }
-    #pragma unroll
-    for (int j = 0; j < P; ++j) left[j] = __shfl_up_sync(0xffffffffu, own[j], 1);
-    right = __shfl_down_sync(0xffffffffu, own[0], 1);
-    if (lane == 0) {
-        #pragma unroll
-        for (int j = 0; j < P; ++j) left[j] = __ldg(p - P + j);
-    }
-    if (lane == 31) right = __ldg(p + P);
-}
-
-// y pass of one node row: W1[j] = sum_d m1[j][d] u_e[d] (masked per cell),
-// W2 likewise with k1; column j = 0 also receives the left cell (its b = P).
-template <int P>
-__device__ __forceinline__ void ypass(const Mats2<P>& mt, const double (&own)[P],
-                                      const double (&left)[P], double right, double chiR,
-                                      double chiL, double (&W1)[P], double (&W2)[P]) {
-    constexpr int N = P + 1;
+    double right = __shfl_down_sync(0xffffffffu, own[0], 1);
+    if (lane == 31) right = own_p[P];
+    double W1[P], W2[P];
     #pragma unroll
     for (int j = 0; j < P; ++j) {
-        double s1 = 0.0, s2 = 0.0;
+        double s1 = mt.m1[j * N + P] * right, s2 = mt.k1[j * N + P] * right;
         #pragma unroll
-        for (int d = 0; d < N; ++d) {
-            const double ud = d < P ? own[d] : right;
-            s1 = fma(mt.m1[j * N + d], ud, s1);
-            s2 = fma(mt.k1[j * N + d], ud, s2);
+        for (int d = 0; d < P; ++d) {
+            s1 = fma(mt.m1[j * N + d], own[d], s1);
+            s2 = fma(mt.k1[j * N + d], own[d], s2);
         }
         W1[j] = chiR * s1;
         W2[j] = chiR * s2;
     }
-    double l1 = 0.0, l2 = 0.0;
+    // left cell: its local column P is our column 0
+    double l1 = mt.m1[P * N + P] * own[0], l2 = mt.k1[P * N + P] * own[0];
     #pragma unroll
-    for (int d = 0; d < N; ++d) {
-        const double ud = d < P ? left[d] : own[0];
+    for (int d = 0; d < P; ++d) {
+        double ud = __shfl_up_sync(0xffffffffu, own[d], 1);
+        if (lane == 0) ud = row[d];
         l1 = fma(mt.m1[P * N + d], ud, l1);
         l2 = fma(mt.k1[P * N + d], ud, l2);
     }
     W1[0] = fma(chiL, l1, W1[0]);
     W2[0] = fma(chiL, l2, W2[0]);
-}
-
-template <int P, int MODE>
-__device__ __forceinline__ void epilogue_row(const Scm2DGeo& g, const StepArgs& a, int64_t I,
-                                             int64_t Jl, bool has_cut, const double (&Ku)[P],
-                                             unsigned long long& amp) {
-    if (I < 0 || I >= g.n1) return;
-    const int64_t base = (I + P) * g.pitch + Jl + PADJ;
-    double yc[P];
     #pragma unroll
-    for (int j = 0; j < P; ++j) yc[j] = 0.0;
-    if (has_cut) {
-        #pragma unroll
-        for (int j = 0; j < P; ++j) yc[j] = __ldg(g.ycut + base + j);
-    }
-    if constexpr (MODE == MODE_APPLY) {
+    for (int r = 0; r < N; ++r)
         #pragma unroll
         for (int j = 0; j < P; ++j)
-            if (Jl + j < g.n1) a.out[base + j] = Ku[j] + yc[j];
-    } else {
-        const double f = __ldg(a.ft + a.k);
-        double u[P], up[P], mi[P];
+            Y[r][j] = fma(mt.xk[r * N + c], W1[j], fma(mt.xm[r * N + c], W2[j], Y[r][j]));
+}
+
+// Cut cells of one element row, handled cooperatively by the warp: for each
+// cut cell (ascending lane order) lane r < L computes output row r of K_o u_e
+// (K_o stored transposed -> coalesced), then the results are routed by
+// shuffles to the lanes owning the cell's columns (columns 0..P-1: the cell's
+// lane; column P: the next lane).  `rows` points at tile column 0 of node row
+// ex*P; cut_lanes = ballot of lanes whose own cell is cut; edge = lane 0's
+// left neighbour (previous strip) is cut.
+template <int P, int UW, int CO>
+__device__ __forceinline__ void cut_cells_warp(const Scm2DGeo& g, const double* rows, int64_t ex,
+                                               int64_t ey0, int lane, unsigned cut_lanes,
+                                               bool edge, double (&Y)[P + 1][P]) {
+    constexpr int N = P + 1;
+    constexpr int L = N * N;
+    int src = edge ? -1 : (__ffs(cut_lanes) - 1);
+    if (!edge) cut_lanes &= cut_lanes - 1;
+    while (src >= -1) {
+        const int64_t ecol = ey0 + src;
+        const int32_t id = __ldg(g.cut_id + ex * g.n_e + ecol);
+        const double* KT = g.KT + (int64_t)id * L * L;
+        const double* corner = rows + CO + P + src * P;
+        constexpr int RR = (L + 31) / 32;   // output rows per lane
+        double t[RR];
         #pragma unroll
-        for (int j = 0; j < P; ++j) {
-            u[j] = __ldg(a.cur + base + j);
-            up[j] = a.prev[base + j];
-            mi[j] = __ldg(a.minv + base + j);
-        }
-        #pragma unroll
-        for (int j = 0; j < P; ++j) {
-            if (Jl + j < g.n1) {
-                const double K = Ku[j] + yc[j];
-                const double v = leapfrog(u[j], up[j], K, mi[j], f * source_at(a.F, base + j),
-                                          a.dt2);
-                a.out[base + j] = v;
-                unsigned long long b = amp_bits(v);
-                amp = b > amp ? b : amp;
+        for (int q = 0; q < RR; ++q) {
+            t[q] = 0.0;
+            const int r = lane + 32 * q;
+            if (r < L) {
+                #pragma unroll
+                for (int m = 0; m < L; ++m)
+                    t[q] = fma(__ldg(KT + m * L + r), corner[(m / N) * UW + (m % N)], t[q]);
             }
         }
+        #pragma unroll
+        for (int r = 0; r < L; ++r) {
+            const double v = __shfl_sync(0xffffffffu, t[r / 32], r % 32);
+            const int a = r / N, b = r % N;
+            if (b < P) {
+                if (lane == src) Y[a][b % P] += v;
+            } else {
+                if (lane == src + 1) Y[a][0] += v;
+            }
+        }
+        if (!cut_lanes) break;
+        src = __ffs(cut_lanes) - 1;
+        cut_lanes &= cut_lanes - 1;
     }
 }
 
+// Persistent 2D kernel: CTA c walks a contiguous run of tiles down the column
+// strips (strip-major order), double-buffering the TMA loads of the next tile
+// behind the compute of the current one.  Warp w computes element row
+// ex0 + w of the tile; the carry of the tile's last element row feeds the
+// next tile's first row (only a run's first tile recomputes its row above).
 template <int P, int MODE>
-__global__ void __launch_bounds__(SCM_NW * 32) k_scm2d(Scm2DGeo g, Mats2<P> mt, StepArgs a) {
+__global__ void __launch_bounds__(rpe_for(P) * 32, 1) k_scm2d(const __grid_constant__ CUtensorMap tm_u,
+                                                         const __grid_constant__ CUtensorMap tm_prev,
+                                                         const __grid_constant__ CUtensorMap tm_minv,
+                                                         Scm2DGeo g, Mats2<P> mt, StepArgs a,
+                                                         int64_t n_tiles, int64_t chunk) {
+    using T = Tile2<P>;
     constexpr int N = P + 1;
-    constexpr int TR = SCM_RP * P;  // rows per warp
-    __shared__ double carry_s[SCM_NW + 1][32][P];
+    constexpr int RPE = T::RPE;
+    constexpr int NWARP = RPE;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* carry = reinterpret_cast<double*>(smem + T::OFF_CARRY);   // [2][RPE+1][P][32]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
-    const int64_t strip = blockIdx.x;
-    const int64_t J0 = strip * (32 * P);
-    const int64_t I0 = (int64_t)blockIdx.y * (SCM_NW * TR);
-    const int64_t R0 = I0 + (int64_t)w * TR;
-    const int64_t ey = J0 / P + lane;
-    const int64_t Jl = J0 + (int64_t)lane * P;
-    const uint8_t fl = g.wflags[((int64_t)blockIdx.y * SCM_NW + w) * g.n_strips + strip];
-    const bool active = fl & 1;
-    const bool has_cut = fl & 2;
-    const double* __restrict__ u = a.cur;
-    const int64_t mstride = g.n_e + 2;
-    auto chi = [&](int64_t ex, int64_t eyy) -> double {
-        return (double)__ldg(g.mask + (ex + 1) * mstride + (eyy + 1));
+    const int64_t t_begin = (int64_t)blockIdx.x * chunk;
+    const int64_t t_end = min(t_begin + chunk, n_tiles);
+    if (t_begin >= t_end) return;
+
+    auto issue = [&](int64_t t, int stage) {
+        unsigned char* st = smem + stage * T::STAGE;
+        const int64_t J0 = (t / g.n_rtiles) * T::TJ;
+        const int64_t I0 = (t % g.n_rtiles) * T::TI;
+        const uint32_t bytes = (uint32_t)(T::U_BYTES + (MODE == MODE_STEP ? 2 * T::E_BYTES : 0));
+        mbar_expect_tx(bar + stage, bytes);
+        tma_load_2d(st, &tm_u, (int32_t)(J0 - P - T::CO + PADJ), (int32_t)I0, bar + stage);
+        if (MODE == MODE_STEP) {
+            tma_load_2d(st + T::OFF_PREV, &tm_prev, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar + stage);
+            tma_load_2d(st + T::OFF_MINV, &tm_minv, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar + stage);
+        }
     };
+    if (threadIdx.x == 0) {
+        for (int s_ = 0; s_ < NSTAGE; ++s_) mbar_init(bar + s_, 1);
+        for (int s_ = 0; s_ < NSTAGE && t_begin + s_ < t_end; ++s_) issue(t_begin + s_, s_);
+    }
+    __syncthreads();
 
+    const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
     unsigned long long amp = 0ULL;
-    double Yfirst[P];
-    double carry[P];
-    #pragma unroll
-    for (int j = 0; j < P; ++j) { Yfirst[j] = 0.0; carry[j] = 0.0; }
-
-    const int64_t ex_begin = R0 / P;
-    const int64_t ex_end = min(ex_begin + SCM_RP, g.n_e);  // exclusive
-    if (active) {
-        double own[P], left[P], right = 0.0;
-        bool have_row = false;
-        for (int64_t ex = ex_begin; ex < ex_end; ++ex) {
-            const double chiR = ey <= g.n_e ? chi(ex, ey) : 0.0;
-            const double chiL = ey <= g.n_e ? chi(ex, ey - 1) : 0.0;
-            double Y[N][P];
+    const int64_t ms_ = g.n_e + 2;
+    int64_t prev_t = -2;
+    for (int64_t t = t_begin, i = 0; t < t_end; ++t, ++i) {
+        const int stage = (int)(i % NSTAGE);
+        const uint32_t parity = (uint32_t)((i / NSTAGE) & 1);
+        const int par = (int)(i & 1);
+        const double* us = reinterpret_cast<const double*>(smem + stage * T::STAGE);
+        const double* ps = reinterpret_cast<const double*>(smem + stage * T::STAGE + T::OFF_PREV);
+        const double* ms = reinterpret_cast<const double*>(smem + stage * T::STAGE + T::OFF_MINV);
+        const int64_t strip = t / g.n_rtiles, rtile = t % g.n_rtiles;
+        const int64_t J0 = strip * T::TJ, I0 = rtile * T::TI;
+        const bool seg_start = (t != prev_t + 1) || rtile == 0;
+        prev_t = t;
+        const bool live = g.cflags[t] != 0;
+        const int64_t ey = J0 / P + lane;
+        // this warp's element row and the halo row above the run
+        const int64_t ex = I0 / P + w;
+        uint8_t mR = 0, mL = 0, hR = 0, hL = 0;
+        if (live && ex < g.n_e && ey <= g.n_e) {
+            mR = __ldg(g.mask + (ex + 1) * ms_ + (ey + 1));
+            mL = __ldg(g.mask + (ex + 1) * ms_ + ey);
+        }
+        if (live && seg_start && w == 0 && ex >= 1 && ey <= g.n_e) {
+            hR = __ldg(g.mask + ex * ms_ + (ey + 1));
+            hL = __ldg(g.mask + ex * ms_ + ey);
+        }
+        mbar_wait(bar + stage, parity);
+        double Y[N][P];
+        #pragma unroll
+        for (int r = 0; r < N; ++r)
             #pragma unroll
-            for (int r = 0; r < N; ++r)
+            for (int j = 0; j < P; ++j) Y[r][j] = 0.0;
+        if (live) {
+            if (seg_start && w == 0) {
+                // carry-in of the run: element row ex0-1, output row a = P only
+                if (__any_sync(0xffffffffu, (hR | hL) != 0)) {
+                    const double cR = hR == 1 ? 1.0 : 0.0, cL = hL == 1 ? 1.0 : 0.0;
+                    #pragma unroll
+                    for (int c = 0; c < N; ++c)
+                        row_contract<P>(mt, us + (size_t)c * T::UW, lane, cR, cL, c, Y);
+                    const unsigned cl = __ballot_sync(0xffffffffu, hR == 2);
+                    const bool ed = __shfl_sync(0xffffffffu, hL == 2, 0);
+                    if (cl || ed)
+                        cut_cells_warp<P, T::UW, T::CO>(g, us, ex - 1, J0 / P, lane, cl, ed, Y);
+                }
                 #pragma unroll
-                for (int j = 0; j < P; ++j) Y[r][j] = 0.0;
-            #pragma unroll
-            for (int c = 0; c < N; ++c) {
-                const int64_t I = ex * P + c;
-                if (!(c == 0 && have_row)) load_row<P>(u, (I + P) * g.pitch, Jl, lane, own, left, right);
-                double W1[P], W2[P];
-                ypass<P>(mt, own, left, right, chiR, chiL, W1, W2);
+                for (int j = 0; j < P; ++j) carry[((par * (RPE + 1) + 0) * P + j) * 32 + lane] = Y[P][j];
                 #pragma unroll
                 for (int r = 0; r < N; ++r)
                     #pragma unroll
+                    for (int j = 0; j < P; ++j) Y[r][j] = 0.0;
+            }
+            const double chiR = mR == 1 ? 1.0 : 0.0;
+            const double chiL = mL == 1 ? 1.0 : 0.0;
+            if (__any_sync(0xffffffffu, (mR | mL) != 0)) {
+                const double* rows = us + (size_t)(w * P + P) * T::UW;
+                #pragma unroll
+                for (int c = 0; c < N; ++c)
+                    row_contract<P>(mt, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
+                const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
+                const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
+                if (cl || ed) cut_cells_warp<P, T::UW, T::CO>(g, rows, ex, J0 / P, lane, cl, ed, Y);
+            }
+        }
+        // (a tile without DOFs has no kept cell touching its rows: its carry is 0)
+        #pragma unroll
+        for (int j = 0; j < P; ++j) carry[((par * (RPE + 1) + w + 1) * P + j) * 32 + lane] = Y[P][j];
+        __syncthreads();   // carries visible
+        if (live) {
+            const double* cin = (w == 0 && !seg_start)
+                                    ? carry + ((par ^ 1) * (RPE + 1) + RPE) * P * 32
+                                    : carry + (par * (RPE + 1) + w) * P * 32;
+            #pragma unroll
+            for (int j = 0; j < P; ++j) Y[0][j] = cin[j * 32 + lane] + Y[0][j];
+            const int64_t Jl = J0 + lane * P;
+            const bool edge = (J0 + T::TJ > g.n1);
+            #pragma unroll
+            for (int r = 0; r < P; ++r) {
+                const int64_t I = ex * P + r;
+                if (I >= g.n1) break;
+                const int64_t base = (I + P) * g.pitch + Jl + PADJ;
+                const double* urow = us + (size_t)(w * P + r + P) * T::UW + T::CO + P + lane * P;
+                const double* prow = ps + (size_t)(w * P + r) * T::TJ + lane * P;
+                const double* mrow = ms + (size_t)(w * P + r) * T::TJ + lane * P;
+                if constexpr (MODE == MODE_APPLY) {
+                    #pragma unroll
                     for (int j = 0; j < P; ++j)
-                        Y[r][j] = fma(mt.xk[r * N + c], W1[j], fma(mt.xm[r * N + c], W2[j], Y[r][j]));
-            }
-            have_row = true;  // own/left/right now hold row (ex+1)*P = next c = 0
-            if (ex == ex_begin) {
-                #pragma unroll
-                for (int j = 0; j < P; ++j) Yfirst[j] = Y[0][j];
-            } else {
-                double K0[P];
-                #pragma unroll
-                for (int j = 0; j < P; ++j) K0[j] = carry[j] + Y[0][j];
-                epilogue_row<P, MODE>(g, a, ex * P, Jl, has_cut, K0, amp);
-            }
-            #pragma unroll
-            for (int r = 1; r < P; ++r) epilogue_row<P, MODE>(g, a, ex * P + r, Jl, has_cut, Y[r], amp);
-            #pragma unroll
-            for (int j = 0; j < P; ++j) carry[j] = Y[P][j];
-        }
-        // last node row of the grid: only the row above contributes
-        if (ex_end == g.n_e && ex_end > ex_begin) {
-            const int64_t I = g.n_e * P;
-            if (I >= R0 && I < R0 + TR) {
-                double K0[P];
-                #pragma unroll
-                for (int j = 0; j < P; ++j) K0[j] = carry[j] + 0.0;
-                epilogue_row<P, MODE>(g, a, I, Jl, has_cut, K0, amp);
+                        if (!edge || Jl + j < g.n1) a.out[base + j] = Y[r][j];
+                } else {
+                    const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
+                    double v[P];
+                    #pragma unroll
+                    for (int j = 0; j < P; ++j) {
+                        const double fF = src ? f * source_at(a.F, base + j) : f * 0.0;
+                        v[j] = leapfrog(urow[j], prow[j], Y[r][j], mrow[j], fF, a.dt2);
+                    }
+                    #pragma unroll
+                    for (int j = 0; j < P; ++j) {
+                        if (!edge || Jl + j < g.n1) {
+                            a.out[base + j] = v[j];
+                            unsigned long long b = amp_bits(v[j]);
+                            amp = b > amp ? b : amp;
+                        }
+                    }
+                }
             }
         }
-        if (ex_end <= ex_begin) {
-            #pragma unroll
-            for (int j = 0; j < P; ++j) carry[j] = 0.0;
-        }
+        __syncthreads();   // stage free
+        if (threadIdx.x == 0 && t + NSTAGE < t_end) issue(t + NSTAGE, stage);
     }
-    // carry-out of warp w feeds the first row of warp w+1
-    #pragma unroll
-    for (int j = 0; j < P; ++j) carry_s[w + 1][lane][j] = active ? carry[j] : 0.0;
-    if (w == 0) {
-        // carry-in of the CTA: element row ex0-1 recomputed (output row a = P only)
-        const int64_t ex = I0 / P - 1;
-        double cin[P];
-        #pragma unroll
-        for (int j = 0; j < P; ++j) cin[j] = 0.0;
-        if (ex >= 0 && ex < g.n_e && active) {
-            const double chiR = ey <= g.n_e ? chi(ex, ey) : 0.0;
-            const double chiL = ey <= g.n_e ? chi(ex, ey - 1) : 0.0;
-            double own[P], left[P], right = 0.0;
-            #pragma unroll
-            for (int c = 0; c < N; ++c) {
-                const int64_t I = ex * P + c;
-                load_row<P>(u, (I + P) * g.pitch, Jl, lane, own, left, right);
-                double W1[P], W2[P];
-                ypass<P>(mt, own, left, right, chiR, chiL, W1, W2);
-                #pragma unroll
-                for (int j = 0; j < P; ++j)
-                    cin[j] = fma(mt.xk[P * N + c], W1[j], fma(mt.xm[P * N + c], W2[j], cin[j]));
-            }
-        }
-        #pragma unroll
-        for (int j = 0; j < P; ++j) carry_s[0][lane][j] = cin[j];
-    }
-    __syncthreads();
-    if (active && R0 < g.n1) {
-        double K0[P];
-        #pragma unroll
-        for (int j = 0; j < P; ++j) K0[j] = carry_s[w][lane][j] + Yfirst[j];
-        epilogue_row<P, MODE>(g, a, R0, Jl, has_cut, K0, amp);
-    }
-    if constexpr (MODE == MODE_STEP) block_amp_max<SCM_NW * 32>(amp, a.amp);
-}
-
-// Cut cells: Ycut[node] = sum over (cell, local row) pairs of K_o[row] . u_cell
-// (pairs in ascending cell order; each dot in local DOF order).
-__global__ void k_cut_apply(int64_t n_cn, const int64_t* __restrict__ cn_state,
-                            const int64_t* __restrict__ cn_ptr, const int32_t* __restrict__ pr_cell,
-                            const int32_t* __restrict__ pr_row, const int64_t* __restrict__ cell_state,
-                            const double* __restrict__ Kc, int L, const double* __restrict__ u,
-                            double* __restrict__ ycut) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_cn) return;
-    double s = 0.0;
-    for (int64_t q = cn_ptr[i]; q < cn_ptr[i + 1]; ++q) {
-        const int64_t e = pr_cell[q];
-        const double* Kr = Kc + (e * L + pr_row[q]) * (int64_t)L;
-        const int64_t* cs = cell_state + e * L;
-        double t = 0.0;
-        for (int m = 0; m < L; ++m) t = fma(__ldg(Kr + m), __ldg(u + cs[m]), t);
-        s += t;
-    }
-    ycut[cn_state[i]] = s;
+    if constexpr (MODE == MODE_STEP) block_amp_max<NWARP * 32>(amp, a.amp);
 }
 
 struct ScmOperator final : Operator {
@@ -305,16 +351,15 @@ struct ScmOperator final : Operator {
     int64_t n_e = 0, n1 = 0, pitch = 0, rows = 0;
     std::vector<int64_t> sidx;
     DevBuf<int64_t> d_sidx;
-    DevBuf<uint8_t> mask, wflags;
+    DevBuf<uint8_t> mask, cflags;
+    DevBuf<int32_t> cut_id;
+    MapCache maps;
+    DevBuf<double> KT;
     int64_t n_strips = 0, n_rtiles = 0;
     std::vector<double> m1, k1;
     double sk = 1.0;
-    // cut cells
-    int64_t n_cut = 0, n_cn = 0;
+    int64_t n_cut = 0;
     int L = 0;
-    DevBuf<int64_t> cn_state, cn_ptr, cell_state;
-    DevBuf<int32_t> pr_cell, pr_row;
-    DevBuf<double> Kc, ycut;
     double bytes_step = 0.0;
 
     const char* name() const override { return "scm"; }
@@ -322,15 +367,27 @@ struct ScmOperator final : Operator {
     void scatter(const double* src, double* dst) override { launch_scatter(ctx, n, d_sidx.p, src, dst); }
     void gather(const double* src, double* dst) override { launch_gather(ctx, n, d_sidx.p, src, dst); }
 
-    void cut_pass(const double* u) {
-        if (!n_cn) return;
-        k_cut_apply<<<(unsigned)ceil_div(n_cn, 128), 128, 0, ctx->stream>>>(
-            n_cn, cn_state.p, cn_ptr.p, pr_cell.p, pr_row.p, cell_state.p, Kc.p, L, u, ycut.p);
-        ctx->launches++;
+    enum { MAP_U = 0, MAP_E = 1 };
+    template <int P>
+    const CUtensorMap& state_map(const double* ptr, int kind) {
+        using T = Tile2<P>;
+        return maps.get(ptr, kind, [&] {
+            const uint64_t dims[2] = {(uint64_t)pitch, (uint64_t)rows};
+            const uint64_t strides[1] = {(uint64_t)pitch};
+            const uint32_t box_u[2] = {(uint32_t)T::UW, (uint32_t)T::UH};
+            const uint32_t box_e[2] = {(uint32_t)T::TJ, (uint32_t)T::TI};
+            return make_map_f64(ptr, 2, dims, strides, kind == MAP_U ? box_u : box_e);
+        });
     }
-
     template <int P, int MODE>
     void launch2d(const StepArgs& a) {
+        using T = Tile2<P>;
+        static bool attr_set = false;
+        if (!attr_set) {
+            WCB_CUDA(cudaFuncSetAttribute(k_scm2d<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)T::SMEM));
+            attr_set = true;
+        }
         Mats2<P> mt;
         for (int i = 0; i < (P + 1) * (P + 1); ++i) {
             mt.m1[i] = m1[i];
@@ -338,9 +395,15 @@ struct ScmOperator final : Operator {
             mt.xk[i] = sk * k1[i];
             mt.xm[i] = sk * m1[i];
         }
-        Scm2DGeo g{n_e, n1, pitch, mask.p, wflags.p, n_strips, ycut.p};
-        dim3 grid((unsigned)n_strips, (unsigned)n_rtiles);
-        k_scm2d<P, MODE><<<grid, SCM_NW * 32, 0, ctx->stream>>>(g, mt, a);
+        Scm2DGeo g{n_e, n1, mask.p, cut_id.p, KT.p, cflags.p, n_strips, n_rtiles, pitch};
+        const CUtensorMap& mu = state_map<P>(a.cur, MAP_U);
+        const CUtensorMap& mp = MODE == MODE_STEP ? state_map<P>(a.prev, MAP_E) : mu;
+        const CUtensorMap& mm = MODE == MODE_STEP ? state_map<P>(a.minv, MAP_E) : mu;
+        const int64_t n_tiles = n_strips * n_rtiles;
+        const int64_t ctas = std::min<int64_t>(n_tiles, ctx->sm_count);
+        const int64_t chunk = ceil_div(n_tiles, ctas);
+        k_scm2d<P, MODE><<<(unsigned)ceil_div(n_tiles, chunk), T::RPE * 32, T::SMEM, ctx->stream>>>(
+            mu, mp, mm, g, mt, a, n_tiles, chunk);
         ctx->launches++;
     }
     template <int MODE>
@@ -356,7 +419,6 @@ struct ScmOperator final : Operator {
         }
     }
     void apply(const double* x, double* y) override {
-        cut_pass(x);
         StepArgs a;
         a.cur = x;
         a.out = y;
@@ -364,7 +426,6 @@ struct ScmOperator final : Operator {
         WCB_CHECK_LAUNCH();
     }
     void cdm_step(const StepArgs& a) override {
-        cut_pass(a.cur);
         dispatch2d<MODE_STEP>(a);
         WCB_CHECK_LAUNCH();
     }
@@ -389,8 +450,8 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
     op->n_e = n_e;
     op->n1 = n1;
     op->n = d->n_dof;
-    // columns: PADJ left pad, lanes may read up to (n_e+1)*p + p past the origin
-    const int64_t need_cols = PADJ + (int64_t)ceil_div(n1, 32 * p) * 32 * p + p + 1;
+    // columns: PADJ left pad; the last strip's tile reaches n_strips*32p + p + 1
+    const int64_t need_cols = PADJ + ceil_div(n1, 32 * p) * 32 * p + p + 2;
     op->pitch = ceil_div(need_cols, 32) * 32;
     op->rows = n1 + 2 * p;
     op->n_state = op->rows * op->pitch;
@@ -400,104 +461,60 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
     op->sk = d->sk;
     const int64_t n_cells = n_e * n_e;
     std::vector<uint8_t> mask((n_e + 2) * (n_e + 2), 0);
-    std::vector<uint8_t> kept_cell(n_cells), cut_cell(n_cells);
     for (int64_t i = 0; i < n_e; ++i)
         for (int64_t j = 0; j < n_e; ++j) {
             const int8_t c = d->cell_class[i * n_e + j];
             WCB_REQUIRE(c >= 0 && c <= 2, "cell_class values must be 0, 1 or 2");
-            mask[(i + 1) * (n_e + 2) + (j + 1)] = (c == 1);
-            kept_cell[i * n_e + j] = (c != 0);
-            cut_cell[i * n_e + j] = (c == 2);
+            mask[(i + 1) * (n_e + 2) + (j + 1)] = (uint8_t)c;
         }
-    // state index of every compact DOF
     op->sidx.resize(op->n);
+    std::vector<uint8_t> kept_node(n1 * n1, 0);
     for (int64_t i = 0; i < op->n; ++i) {
         const int64_t lex = d->lex_of_compact[i];
         WCB_REQUIRE(lex >= 0 && lex < n1 * n1, "lex_of_compact out of range");
+        if (i) WCB_REQUIRE(d->lex_of_compact[i - 1] < lex, "lex_of_compact must be ascending");
         const int64_t I = lex / n1, J = lex % n1;
         op->sidx[i] = (I + p) * op->pitch + J + PADJ;
+        kept_node[lex] = 1;
     }
-    // node masks: kept nodes, cut nodes
-    std::vector<uint8_t> kept_node(n1 * n1, 0), cut_node(n1 * n1, 0);
-    for (int64_t i = 0; i < op->n; ++i) kept_node[d->lex_of_compact[i]] = 1;
+    // CTA tiles (32p columns x RPE*p rows) that own at least one DOF
+    const int64_t TI = (int64_t)rpe_for(p) * p, TJ = 32 * (int64_t)p;
+    op->n_strips = ceil_div(n1, TJ);
+    op->n_rtiles = ceil_div(n1, TI);
+    std::vector<uint8_t> cf(op->n_rtiles * op->n_strips, 0);   // tile t = strip*n_rtiles + rtile
+    for (int64_t I = 0; I < n1; ++I)
+        for (int64_t J = 0; J < n1; ++J)
+            if (kept_node[I * n1 + J]) cf[(J / TJ) * op->n_rtiles + I / TI] = 1;
+    // cut cells: id map + transposed stiffness
+    op->n_cut = d->n_cut;
+    op->L = N * N;
+    const int L = op->L;
+    std::vector<int32_t> cid(n_cells, -1);
+    std::vector<double> KT((size_t)std::max<int64_t>(op->n_cut, 1) * L * L, 0.0);
+    for (int64_t e = 0; e < op->n_cut; ++e) {
+        WCB_REQUIRE(d->cut_cells && d->cut_K, "cut arrays NULL");
+        const int64_t c = d->cut_cells[e];
+        WCB_REQUIRE(c >= 0 && c < n_cells && d->cell_class[c] == 2, "cut_cells must list cut cells");
+        if (e) WCB_REQUIRE(d->cut_cells[e - 1] < c, "cut_cells must be ascending");
+        cid[c] = (int32_t)e;
+        const double* K = d->cut_K + e * L * L;
+        double* T = KT.data() + e * L * L;
+        for (int r = 0; r < L; ++r)
+            for (int m = 0; m < L; ++m) T[m * L + r] = K[r * L + m];
+    }
     for (int64_t c = 0; c < n_cells; ++c)
-        if (cut_cell[c]) {
-            const int64_t ci = c / n_e, cj = c % n_e;
-            for (int a = 0; a <= p; ++a)
-                for (int b = 0; b <= p; ++b) cut_node[(ci * p + a) * n1 + cj * p + b] = 1;
-        }
-    // warp tiles
-    const int64_t TR = (int64_t)SCM_RP * p;
-    op->n_strips = ceil_div(n1, 32 * p);
-    op->n_rtiles = ceil_div(n1, SCM_NW * TR);
-    std::vector<uint8_t> wf(op->n_rtiles * SCM_NW * op->n_strips, 0);
-    for (int64_t I = 0; I < n1; ++I) {
-        const int64_t wt = I / TR;  // global warp-row index = rtile*NW + w
-        for (int64_t J = 0; J < n1; ++J) {
-            const int64_t s = J / (32 * p);
-            uint8_t& f = wf[wt * op->n_strips + s];
-            if (kept_node[I * n1 + J]) f |= 1;
-            if (cut_node[I * n1 + J]) f |= 2;
-        }
-    }
+        WCB_REQUIRE(d->cell_class[c] != 2 || cid[c] >= 0, "a cut cell is missing from cut_cells");
     cudaStream_t st = ctx->stream;
     op->d_sidx.alloc(std::max<int64_t>(op->n, 1));
     op->d_sidx.upload(op->sidx.data(), op->n, st);
     op->mask.alloc(mask.size());
     op->mask.upload(mask.data(), mask.size(), st);
-    op->wflags.alloc(wf.size());
-    op->wflags.upload(wf.data(), wf.size(), st);
-    // cut cells
-    op->n_cut = d->n_cut;
-    op->L = N * N;
-    const int L = op->L;
-    op->ycut.alloc(op->n_state);
-    op->ycut.zero(st);
-    if (op->n_cut) {
-        WCB_REQUIRE(d->cut_cells && d->cut_K, "cut arrays NULL");
-        std::vector<int64_t> cell_state(op->n_cut * L);
-        std::vector<std::vector<std::pair<int32_t, int32_t>>> pairs;  // per cut node
-        std::vector<int64_t> node_of(n1 * n1, -1);
-        std::vector<int64_t> cn_lex;
-        for (int64_t e = 0; e < op->n_cut; ++e) {
-            const int64_t c = d->cut_cells[e];
-            WCB_REQUIRE(c >= 0 && c < n_cells && cut_cell[c], "cut_cells must list cut cells");
-            if (e) WCB_REQUIRE(d->cut_cells[e - 1] < c, "cut_cells must be ascending");
-            const int64_t ci = c / n_e, cj = c % n_e;
-            for (int a = 0; a <= p; ++a)
-                for (int b = 0; b <= p; ++b) {
-                    const int64_t I = ci * p + a, J = cj * p + b;
-                    const int loc = a * N + b;
-                    cell_state[e * L + loc] = (I + p) * op->pitch + J + PADJ;
-                    int64_t& k = node_of[I * n1 + J];
-                    if (k < 0) {
-                        k = (int64_t)cn_lex.size();
-                        cn_lex.push_back(I * n1 + J);
-                        pairs.emplace_back();
-                    }
-                    pairs[k].emplace_back((int32_t)e, (int32_t)loc);
-                }
-        }
-        // sort cut nodes by lex for locality; pairs are already in cell order
-        std::vector<int64_t> order(cn_lex.size());
-        std::iota(order.begin(), order.end(), 0);
-        std::sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cn_lex[x] < cn_lex[y]; });
-        std::vector<int64_t> cs, cp(1, 0);
-        std::vector<int32_t> pc, prr;
-        for (int64_t k : order) {
-            const int64_t lex = cn_lex[k];
-            cs.push_back((lex / n1 + p) * op->pitch + lex % n1 + PADJ);
-            for (auto& pr : pairs[k]) { pc.push_back(pr.first); prr.push_back(pr.second); }
-            cp.push_back((int64_t)pc.size());
-        }
-        op->n_cn = (int64_t)cs.size();
-        op->cn_state.alloc(cs.size()); op->cn_state.upload(cs.data(), cs.size(), st);
-        op->cn_ptr.alloc(cp.size()); op->cn_ptr.upload(cp.data(), cp.size(), st);
-        op->pr_cell.alloc(pc.size()); op->pr_cell.upload(pc.data(), pc.size(), st);
-        op->pr_row.alloc(prr.size()); op->pr_row.upload(prr.data(), prr.size(), st);
-        op->cell_state.alloc(cell_state.size()); op->cell_state.upload(cell_state.data(), cell_state.size(), st);
-        op->Kc.alloc(op->n_cut * L * L); op->Kc.upload(d->cut_K, op->n_cut * L * L, st);
-    }
+    op->cflags.alloc(cf.size());
+    op->cflags.upload(cf.data(), cf.size(), st);
+    op->cut_id.alloc(cid.size());
+    op->cut_id.upload(cid.data(), cid.size(), st);
+    op->KT.alloc(KT.size());
+    op->KT.upload(KT.data(), KT.size(), st);
     // algorithmic bytes per step: 32 B per DOF + packed cut K
     op->bytes_step = 32.0 * (double)op->n + 8.0 * (double)L * (L + 1) / 2.0 * (double)op->n_cut;
     WCB_CUDA(cudaStreamSynchronize(st));
