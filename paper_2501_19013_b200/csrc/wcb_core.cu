@@ -436,12 +436,19 @@ static void run_cdm_device(wcb_cdm_plan* P, const double* d_ft, double dt, int64
             ctx->launches++;
         }
     };
-    record(0, P->A.p);
     StepArgs a;
     a.minv = P->minv.p;
     a.F = P->src;
     a.ft = d_ft;
     a.dt2 = dt * dt;
+    if (P->n_obs && d_obs_out) {
+        a.n_obs = P->n_obs;
+        a.obs_ptr = P->obs_indptr.p;
+        a.obs_idx = P->obs_idx.p;
+        a.obs_val = P->obs_val.p;
+        a.obs_out = d_obs_out;
+        a.obs_stride = stride;
+    }
     double* cur = P->A.p;
     double* prev = P->B.p;
     P->h_amp.assign(n_t + 1, 0ULL);
@@ -473,14 +480,14 @@ static void run_cdm_device(wcb_cdm_plan* P, const double* d_ft, double dt, int64
         a.out = prev;  // psi_{k+1} overwrites psi_{k-1} in place
         a.k = k;
         a.amp = P->amp.p + (k + 1);
-        op->cdm_step(a);
+        op->cdm_step(a);   // also records obs[:, k] from psi_k
         std::swap(cur, prev);
-        record(k + 1, cur);
         if ((k + 1) % check_every == 0) {
             WCB_CHECK_LAUNCH();
             if (inspect(k + 1)) { diverged = true; break; }
         }
     }
+    if (!diverged) record(n_t, cur);
     WCB_CUDA(cudaEventRecord(ctx->ev1, s));
     WCB_CHECK_LAUNCH();
     if (!diverged) diverged = inspect(n_t);

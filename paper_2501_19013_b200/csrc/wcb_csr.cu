@@ -46,6 +46,7 @@ template <int TPR, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_csr_cdm(int64_t n, const int64_t* __restrict__ indptr,
                                                    const int32_t* __restrict__ indices,
                                                    const double* __restrict__ data, StepArgs a) {
+    if (blockIdx.x == 0) record_observers(a);
     const int64_t row = (blockIdx.x * (int64_t)BLOCK + threadIdx.x) / TPR;
     const int lane = threadIdx.x % TPR;
     const bool valid = row < n;

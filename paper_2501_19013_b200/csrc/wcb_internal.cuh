@@ -116,7 +116,26 @@ struct StepArgs {
     int64_t k = 0;                   // f = ft[k]
     double dt2 = 0.0;
     unsigned long long* amp = nullptr;
+    // observer recording of psi_k (= cur) into obs_out[:, k], fused into the
+    // step kernel (one block does it; src/timeint.py:97-106)
+    int64_t n_obs = 0;
+    const int64_t* obs_ptr = nullptr;
+    const int64_t* obs_idx = nullptr;   // state indices
+    const double* obs_val = nullptr;
+    double* obs_out = nullptr;
+    int64_t obs_stride = 0;
 };
+
+// obs[:, k] = obs_mat @ psi_k in CSR order (scipy csr_matvec); call from
+// every thread of exactly one block.
+__device__ __forceinline__ void record_observers(const StepArgs& a) {
+    if (!a.obs_out) return;
+    for (int64_t r = threadIdx.x; r < a.n_obs; r += blockDim.x) {
+        double s = 0.0;
+        for (int64_t j = a.obs_ptr[r]; j < a.obs_ptr[r + 1]; ++j) s += a.obs_val[j] * a.cur[a.obs_idx[j]];
+        a.obs_out[r * a.obs_stride + a.k] = s;
+    }
+}
 
 // Reference arithmetic order of src/timeint.py:185:
 //   psi_new = 2.0*psi - psi_prev + (dt*dt) * (rhs / m)

@@ -39,24 +39,51 @@
 namespace wcb {
 
 constexpr int PADJ = 32;
-constexpr int NSTAGE = 2;    // TMA ring depth
-// element rows per tile = compute warps per CTA (bounded by shared memory)
-__host__ __device__ constexpr int rpe_for(int P) { return P <= 4 ? 8 : (P == 5 ? 4 : 2); }
+// element rows per tile; one compute warp each plus one halo warp
+__host__ __device__ constexpr int rpe_for(int P) { return P <= 4 ? 4 : 2; }
 
-// y pass uses the unscaled 1D factors, the x pass carries sk:
-//   sk (k1_x (x) m1_y + m1_x (x) k1_y) = (sk k1)_x (x) m1_y + (sk m1)_x (x) k1_y
+// The 1D GLL-Lagrange factors m1, k1 are symmetric and centro-symmetric
+// (A[i][j] = A[j][i] = A[P-i][P-j]); only one value per orbit is kept, so all
+// coefficients of the sum factorisation fit in registers.  sk is applied once
+// per output node: sk (k1 (x) m1 + m1 (x) k1) u = sk * [k1 (x) m1 + m1 (x) k1] u.
+__host__ __device__ constexpr int orb_key(int P, int i, int j) {
+    // canonical representative: lexicographically smallest of the 4 images
+    int a0 = i * 16 + j, a1 = j * 16 + i, a2 = (P - i) * 16 + (P - j), a3 = (P - j) * 16 + (P - i);
+    int m = a0 < a1 ? a0 : a1;
+    m = m < a2 ? m : a2;
+    return m < a3 ? m : a3;
+}
+__host__ __device__ constexpr int orb_count(int P) {
+    int n = 0;
+    for (int i = 0; i <= P; ++i)
+        for (int j = 0; j <= P; ++j)
+            if (orb_key(P, i, j) == i * 16 + j) ++n;
+    return n;
+}
+__host__ __device__ constexpr int orb(int P, int i, int j) {
+    const int key = orb_key(P, i, j);
+    int n = 0;
+    for (int a = 0; a <= P; ++a)
+        for (int b = 0; b <= P; ++b)
+            if (orb_key(P, a, b) == a * 16 + b) {
+                if (a * 16 + b == key) return n;
+                ++n;
+            }
+    return -1;
+}
+
 template <int P>
 struct Mats2 {
-    double m1[(P + 1) * (P + 1)];   // y pass
-    double k1[(P + 1) * (P + 1)];   // y pass
-    double xk[(P + 1) * (P + 1)];   // sk * k1, x pass
-    double xm[(P + 1) * (P + 1)];   // sk * m1, x pass
+    double m[orb_count(P)];   // m1 orbit representatives
+    double k[orb_count(P)];   // k1 orbit representatives
 };
 
-// Tile geometry of the 2D kernel: a tile is 32p node columns x RPE*p node rows.
+// Tile geometry of the 2D kernel: a tile is 32p node columns x RPE*p node rows;
+// only psi_k (with its halo) is staged in shared memory by TMA.
 template <int P>
 struct Tile2 {
     static constexpr int RPE = rpe_for(P);
+    static constexpr int NWARP = RPE + 1;
     static constexpr int TJ = 32 * P;                       // owned node columns
     static constexpr int TI = RPE * P;                      // owned node rows
     // TMA boxes must start 16-byte aligned: for odd P the u tile starts one
@@ -65,13 +92,9 @@ struct Tile2 {
     static constexpr int UW = ((TJ + P + 1 + CO) + 1) / 2 * 2;  // cols J0-P-CO..J0+TJ, even
     static constexpr int UH = TI + P + 1;                   // u tile rows (I0-P..I0+TI)
     static constexpr size_t U_BYTES = (size_t)UW * UH * 8;
-    static constexpr size_t E_BYTES = (size_t)TJ * TI * 8;  // prev / minv tiles
-    static constexpr size_t OFF_PREV = (U_BYTES + 127) / 128 * 128;
-    static constexpr size_t OFF_MINV = OFF_PREV + (E_BYTES + 127) / 128 * 128;
-    static constexpr size_t STAGE = OFF_MINV + (E_BYTES + 127) / 128 * 128;
-    static constexpr size_t OFF_CARRY = NSTAGE * STAGE;     // [2][RPE+1][P][32]
-    static constexpr size_t OFF_BAR = OFF_CARRY + (size_t)2 * (RPE + 1) * P * 32 * 8;
-    static constexpr size_t SMEM = OFF_BAR + 8 * NSTAGE;
+    static constexpr size_t OFF_CARRY = (U_BYTES + 127) / 128 * 128;   // [RPE+1][P][32]
+    static constexpr size_t OFF_BAR = OFF_CARRY + (size_t)(RPE + 1) * P * 32 * 8;
+    static constexpr size_t SMEM = OFF_BAR + 8;
 };
 
 struct Scm2DGeo {
@@ -80,7 +103,7 @@ struct Scm2DGeo {
     const uint8_t* mask;      // (n_e+2)^2 cell codes, one ring of 0 around: 0 out, 1 uncut, 2 cut
     const int32_t* cut_id;    // n_e^2 -> cut index or -1
     const double* KT;         // n_cut * L * L, transposed physical cut stiffness
-    const uint8_t* cflags;    // per tile: 1 = owns a DOF
+    const uint8_t* cflags;    // per tile (strip-major): 1 = owns a DOF
     int64_t n_strips;
     int64_t n_rtiles;
     int64_t pitch;            // row pitch of the state (doubles)
@@ -91,8 +114,9 @@ enum { MODE_STEP = 0, MODE_APPLY = 1 };
 // One node row of the smem tile: y contraction (masked) then x contraction
 // accumulated into Y.  `row` points at tile column 0 of that row.
 template <int P>
-__device__ __forceinline__ void row_contract(const Mats2<P>& mt, const double* row, int lane,
-                                             double chiR, double chiL, int c,
+__device__ __forceinline__ void row_contract(const double (&mc)[orb_count(P)],
+                                             const double (&kc)[orb_count(P)], const double* row,
+                                             int lane, double chiR, double chiL, int c,
                                              double (&Y)[P + 1][P]) {
     constexpr int N = P + 1;
     row += Tile2<P>::CO;
@@ -114,23 +138,23 @@ __device__ __forceinline__ void row_contract(const Mats2<P>& mt, const double* r
     double W1[P], W2[P];
     #pragma unroll
     for (int j = 0; j < P; ++j) {
-        double s1 = mt.m1[j * N + P] * right, s2 = mt.k1[j * N + P] * right;
+        double s1 = mc[orb(P, j, P)] * right, s2 = kc[orb(P, j, P)] * right;
         #pragma unroll
         for (int d = 0; d < P; ++d) {
-            s1 = fma(mt.m1[j * N + d], own[d], s1);
-            s2 = fma(mt.k1[j * N + d], own[d], s2);
+            s1 = fma(mc[orb(P, j, d)], own[d], s1);
+            s2 = fma(kc[orb(P, j, d)], own[d], s2);
         }
         W1[j] = chiR * s1;
         W2[j] = chiR * s2;
     }
     // left cell: its local column P is our column 0
-    double l1 = mt.m1[P * N + P] * own[0], l2 = mt.k1[P * N + P] * own[0];
+    double l1 = mc[orb(P, P, P)] * own[0], l2 = kc[orb(P, P, P)] * own[0];
     #pragma unroll
     for (int d = 0; d < P; ++d) {
         double ud = __shfl_up_sync(0xffffffffu, own[d], 1);
         if (lane == 0) ud = row[d];
-        l1 = fma(mt.m1[P * N + d], ud, l1);
-        l2 = fma(mt.k1[P * N + d], ud, l2);
+        l1 = fma(mc[orb(P, P, d)], ud, l1);
+        l2 = fma(kc[orb(P, P, d)], ud, l2);
     }
     W1[0] = fma(chiL, l1, W1[0]);
     W2[0] = fma(chiL, l2, W2[0]);
@@ -138,7 +162,7 @@ __device__ __forceinline__ void row_contract(const Mats2<P>& mt, const double* r
     for (int r = 0; r < N; ++r)
         #pragma unroll
         for (int j = 0; j < P; ++j)
-            Y[r][j] = fma(mt.xk[r * N + c], W1[j], fma(mt.xm[r * N + c], W2[j], Y[r][j]));
+            Y[r][j] = fma(kc[orb(P, r, c)], W1[j], fma(mc[orb(P, r, c)], W2[j], Y[r][j]));
 }
 
 // Cut cells of one element row, handled cooperatively by the warp: for each
@@ -189,161 +213,123 @@ __device__ __forceinline__ void cut_cells_warp(const Scm2DGeo& g, const double* 
     }
 }
 
-// Persistent 2D kernel: CTA c walks a contiguous run of tiles down the column
-// strips (strip-major order), double-buffering the TMA loads of the next tile
-// behind the compute of the current one.  Warp w computes element row
-// ex0 + w of the tile; the carry of the tile's last element row feeds the
-// next tile's first row (only a run's first tile recomputes its row above).
+// One CTA per tile (grid = strips x row tiles).  The halo warp recomputes
+// the element row above the tile (its output row a = P only); warp w < RPE
+// computes element row ex0 + w.  psi_k arrives by one TMA box; psi_{k-1} and
+// 1/m are read straight from global memory in the epilogue.
 template <int P, int MODE>
-__global__ void __launch_bounds__(rpe_for(P) * 32, 1) k_scm2d(const __grid_constant__ CUtensorMap tm_u,
-                                                         const __grid_constant__ CUtensorMap tm_prev,
-                                                         const __grid_constant__ CUtensorMap tm_minv,
-                                                         Scm2DGeo g, Mats2<P> mt, StepArgs a,
-                                                         int64_t n_tiles, int64_t chunk) {
+__global__ void __launch_bounds__(Tile2<P>::NWARP * 32) k_scm2d(const __grid_constant__ CUtensorMap tm_u,
+                                                               Scm2DGeo g, Mats2<P> mt, double sk,
+                                                               StepArgs a) {
     using T = Tile2<P>;
     constexpr int N = P + 1;
     constexpr int RPE = T::RPE;
-    constexpr int NWARP = RPE;
     extern __shared__ __align__(128) unsigned char smem[];
-    double* carry = reinterpret_cast<double*>(smem + T::OFF_CARRY);   // [2][RPE+1][P][32]
+    const double* us = reinterpret_cast<const double*>(smem);
+    double* carry = reinterpret_cast<double*>(smem + T::OFF_CARRY);   // [RPE+1][P][32]
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
-    const int64_t t_begin = (int64_t)blockIdx.x * chunk;
-    const int64_t t_end = min(t_begin + chunk, n_tiles);
-    if (t_begin >= t_end) return;
-
-    auto issue = [&](int64_t t, int stage) {
-        unsigned char* st = smem + stage * T::STAGE;
-        const int64_t J0 = (t / g.n_rtiles) * T::TJ;
-        const int64_t I0 = (t % g.n_rtiles) * T::TI;
-        const uint32_t bytes = (uint32_t)(T::U_BYTES + (MODE == MODE_STEP ? 2 * T::E_BYTES : 0));
-        mbar_expect_tx(bar + stage, bytes);
-        tma_load_2d(st, &tm_u, (int32_t)(J0 - P - T::CO + PADJ), (int32_t)I0, bar + stage);
-        if (MODE == MODE_STEP) {
-            tma_load_2d(st + T::OFF_PREV, &tm_prev, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar + stage);
-            tma_load_2d(st + T::OFF_MINV, &tm_minv, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar + stage);
-        }
-    };
+    const int64_t strip = blockIdx.x, rtile = blockIdx.y;
+    if (MODE == MODE_STEP && blockIdx.x == 0 && blockIdx.y == 0) record_observers(a);
+    if (!g.cflags[strip * g.n_rtiles + rtile]) return;   // tile without DOFs
+    const int64_t J0 = strip * T::TJ, I0 = rtile * T::TI;
     if (threadIdx.x == 0) {
-        for (int s_ = 0; s_ < NSTAGE; ++s_) mbar_init(bar + s_, 1);
-        for (int s_ = 0; s_ < NSTAGE && t_begin + s_ < t_end; ++s_) issue(t_begin + s_, s_);
+        mbar_init(bar, 1);
+        mbar_expect_tx(bar, (uint32_t)T::U_BYTES);
+        tma_load_2d(smem, &tm_u, (int32_t)(J0 - P - T::CO + PADJ), (int32_t)I0, bar);
     }
-    __syncthreads();
+    // cell codes (and the epilogue's psi_{k-1}, 1/m) while the tile is in flight
+    const bool halo = (w == RPE);
+    const int64_t ex = halo ? I0 / P - 1 : I0 / P + w;
+    const int64_t ey = J0 / P + lane;
+    uint8_t mR = 0, mL = 0;
+    if (ex >= 0 && ex < g.n_e && ey <= g.n_e) {
+        const int64_t ms_ = g.n_e + 2;
+        mR = __ldg(g.mask + (ex + 1) * ms_ + (ey + 1));
+        mL = __ldg(g.mask + (ex + 1) * ms_ + ey);
+    }
+    const int64_t Jl = J0 + lane * P;
+    if (MODE == MODE_STEP && !halo) {
+        #pragma unroll
+        for (int r = 0; r < P; ++r) {
+            const int64_t base = (ex * P + r + P) * g.pitch + Jl + PADJ;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.prev + base));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.minv + base));
+        }
+    }
+    __syncthreads();   // barrier init visible
+    mbar_wait(bar, 0);
 
-    const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
-    unsigned long long amp = 0ULL;
-    const int64_t ms_ = g.n_e + 2;
-    int64_t prev_t = -2;
-    for (int64_t t = t_begin, i = 0; t < t_end; ++t, ++i) {
-        const int stage = (int)(i % NSTAGE);
-        const uint32_t parity = (uint32_t)((i / NSTAGE) & 1);
-        const int par = (int)(i & 1);
-        const double* us = reinterpret_cast<const double*>(smem + stage * T::STAGE);
-        const double* ps = reinterpret_cast<const double*>(smem + stage * T::STAGE + T::OFF_PREV);
-        const double* ms = reinterpret_cast<const double*>(smem + stage * T::STAGE + T::OFF_MINV);
-        const int64_t strip = t / g.n_rtiles, rtile = t % g.n_rtiles;
-        const int64_t J0 = strip * T::TJ, I0 = rtile * T::TI;
-        const bool seg_start = (t != prev_t + 1) || rtile == 0;
-        prev_t = t;
-        const bool live = g.cflags[t] != 0;
-        const int64_t ey = J0 / P + lane;
-        // this warp's element row and the halo row above the run
-        const int64_t ex = I0 / P + w;
-        uint8_t mR = 0, mL = 0, hR = 0, hL = 0;
-        if (live && ex < g.n_e && ey <= g.n_e) {
-            mR = __ldg(g.mask + (ex + 1) * ms_ + (ey + 1));
-            mL = __ldg(g.mask + (ex + 1) * ms_ + ey);
-        }
-        if (live && seg_start && w == 0 && ex >= 1 && ey <= g.n_e) {
-            hR = __ldg(g.mask + ex * ms_ + (ey + 1));
-            hL = __ldg(g.mask + ex * ms_ + ey);
-        }
-        mbar_wait(bar + stage, parity);
-        double Y[N][P];
+    double mc[orb_count(P)], kc[orb_count(P)];
+    #pragma unroll
+    for (int i = 0; i < orb_count(P); ++i) { mc[i] = mt.m[i]; kc[i] = mt.k[i]; }
+    const int rbase = halo ? -P : w * P;   // tile row of node row ex*P, minus P
+    double Y[N][P];
+    #pragma unroll
+    for (int r = 0; r < N; ++r)
         #pragma unroll
-        for (int r = 0; r < N; ++r)
-            #pragma unroll
-            for (int j = 0; j < P; ++j) Y[r][j] = 0.0;
-        if (live) {
-            if (seg_start && w == 0) {
-                // carry-in of the run: element row ex0-1, output row a = P only
-                if (__any_sync(0xffffffffu, (hR | hL) != 0)) {
-                    const double cR = hR == 1 ? 1.0 : 0.0, cL = hL == 1 ? 1.0 : 0.0;
-                    #pragma unroll
-                    for (int c = 0; c < N; ++c)
-                        row_contract<P>(mt, us + (size_t)c * T::UW, lane, cR, cL, c, Y);
-                    const unsigned cl = __ballot_sync(0xffffffffu, hR == 2);
-                    const bool ed = __shfl_sync(0xffffffffu, hL == 2, 0);
-                    if (cl || ed)
-                        cut_cells_warp<P, T::UW, T::CO>(g, us, ex - 1, J0 / P, lane, cl, ed, Y);
-                }
-                #pragma unroll
-                for (int j = 0; j < P; ++j) carry[((par * (RPE + 1) + 0) * P + j) * 32 + lane] = Y[P][j];
-                #pragma unroll
-                for (int r = 0; r < N; ++r)
-                    #pragma unroll
-                    for (int j = 0; j < P; ++j) Y[r][j] = 0.0;
-            }
-            const double chiR = mR == 1 ? 1.0 : 0.0;
-            const double chiL = mL == 1 ? 1.0 : 0.0;
-            if (__any_sync(0xffffffffu, (mR | mL) != 0)) {
-                const double* rows = us + (size_t)(w * P + P) * T::UW;
-                #pragma unroll
-                for (int c = 0; c < N; ++c)
-                    row_contract<P>(mt, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
-                const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
-                const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
-                if (cl || ed) cut_cells_warp<P, T::UW, T::CO>(g, rows, ex, J0 / P, lane, cl, ed, Y);
-            }
-        }
-        // (a tile without DOFs has no kept cell touching its rows: its carry is 0)
+        for (int j = 0; j < P; ++j) Y[r][j] = 0.0;
+    if (__any_sync(0xffffffffu, (mR | mL) != 0)) {
+        const double chiR = mR == 1 ? 1.0 : 0.0;
+        const double chiL = mL == 1 ? 1.0 : 0.0;
+        const double* rows = us + (size_t)(rbase + P) * T::UW;
         #pragma unroll
-        for (int j = 0; j < P; ++j) carry[((par * (RPE + 1) + w + 1) * P + j) * 32 + lane] = Y[P][j];
-        __syncthreads();   // carries visible
-        if (live) {
-            const double* cin = (w == 0 && !seg_start)
-                                    ? carry + ((par ^ 1) * (RPE + 1) + RPE) * P * 32
-                                    : carry + (par * (RPE + 1) + w) * P * 32;
-            #pragma unroll
-            for (int j = 0; j < P; ++j) Y[0][j] = cin[j * 32 + lane] + Y[0][j];
-            const int64_t Jl = J0 + lane * P;
-            const bool edge = (J0 + T::TJ > g.n1);
-            #pragma unroll
-            for (int r = 0; r < P; ++r) {
-                const int64_t I = ex * P + r;
-                if (I >= g.n1) break;
-                const int64_t base = (I + P) * g.pitch + Jl + PADJ;
-                const double* urow = us + (size_t)(w * P + r + P) * T::UW + T::CO + P + lane * P;
-                const double* prow = ps + (size_t)(w * P + r) * T::TJ + lane * P;
-                const double* mrow = ms + (size_t)(w * P + r) * T::TJ + lane * P;
-                if constexpr (MODE == MODE_APPLY) {
-                    #pragma unroll
-                    for (int j = 0; j < P; ++j)
-                        if (!edge || Jl + j < g.n1) a.out[base + j] = Y[r][j];
-                } else {
-                    const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
-                    double v[P];
-                    #pragma unroll
-                    for (int j = 0; j < P; ++j) {
-                        const double fF = src ? f * source_at(a.F, base + j) : f * 0.0;
-                        v[j] = leapfrog(urow[j], prow[j], Y[r][j], mrow[j], fF, a.dt2);
-                    }
-                    #pragma unroll
-                    for (int j = 0; j < P; ++j) {
-                        if (!edge || Jl + j < g.n1) {
-                            a.out[base + j] = v[j];
-                            unsigned long long b = amp_bits(v[j]);
-                            amp = b > amp ? b : amp;
-                        }
-                    }
-                }
-            }
-        }
-        __syncthreads();   // stage free
-        if (threadIdx.x == 0 && t + NSTAGE < t_end) issue(t + NSTAGE, stage);
+        for (int c = 0; c < N; ++c) row_contract<P>(mc, kc, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
+        const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
+        const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
+        if (cl || ed) cut_cells_warp<P, T::UW, T::CO>(g, rows, ex, J0 / P, lane, cl, ed, Y);
     }
-    if constexpr (MODE == MODE_STEP) block_amp_max<NWARP * 32>(amp, a.amp);
+    // row a = P of element row ex is row a = 0 of element row ex+1
+    #pragma unroll
+    for (int j = 0; j < P; ++j) carry[((halo ? 0 : w + 1) * P + j) * 32 + lane] = Y[P][j];
+    __syncthreads();
+    unsigned long long amp = 0ULL;
+    if (!halo) {
+        #pragma unroll
+        for (int j = 0; j < P; ++j) Y[0][j] = carry[(w * P + j) * 32 + lane] + Y[0][j];
+        #pragma unroll
+        for (int r = 0; r < P; ++r)
+            #pragma unroll
+            for (int j = 0; j < P; ++j) Y[r][j] *= sk;
+        const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
+        const bool edge = (J0 + T::TJ > g.n1);
+        #pragma unroll
+        for (int r = 0; r < P; ++r) {
+            const int64_t I = ex * P + r;
+            if (I >= g.n1) break;
+            const int64_t base = (I + P) * g.pitch + Jl + PADJ;
+            const double* urow = us + (size_t)(rbase + r + P) * T::UW + T::CO + P + lane * P;
+            if constexpr (MODE == MODE_APPLY) {
+                #pragma unroll
+                for (int j = 0; j < P; ++j)
+                    if (!edge || Jl + j < g.n1) a.out[base + j] = Y[r][j];
+            } else {
+                double up[P], mi[P];
+                #pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    up[j] = a.prev[base + j];
+                    mi[j] = __ldg(a.minv + base + j);
+                }
+                const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
+                double v[P];
+                #pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    const double fF = src ? f * source_at(a.F, base + j) : f * 0.0;
+                    v[j] = leapfrog(urow[j], up[j], Y[r][j], mi[j], fF, a.dt2);
+                }
+                #pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    if (!edge || Jl + j < g.n1) {
+                        a.out[base + j] = v[j];
+                        unsigned long long b = amp_bits(v[j]);
+                        amp = b > amp ? b : amp;
+                    }
+                }
+            }
+        }
+    }
+    if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
 }
 
 struct ScmOperator final : Operator {
@@ -367,16 +353,14 @@ struct ScmOperator final : Operator {
     void scatter(const double* src, double* dst) override { launch_scatter(ctx, n, d_sidx.p, src, dst); }
     void gather(const double* src, double* dst) override { launch_gather(ctx, n, d_sidx.p, src, dst); }
 
-    enum { MAP_U = 0, MAP_E = 1 };
     template <int P>
-    const CUtensorMap& state_map(const double* ptr, int kind) {
+    const CUtensorMap& state_map(const double* ptr) {
         using T = Tile2<P>;
-        return maps.get(ptr, kind, [&] {
+        return maps.get(ptr, 0, [&] {
             const uint64_t dims[2] = {(uint64_t)pitch, (uint64_t)rows};
             const uint64_t strides[1] = {(uint64_t)pitch};
-            const uint32_t box_u[2] = {(uint32_t)T::UW, (uint32_t)T::UH};
-            const uint32_t box_e[2] = {(uint32_t)T::TJ, (uint32_t)T::TI};
-            return make_map_f64(ptr, 2, dims, strides, kind == MAP_U ? box_u : box_e);
+            const uint32_t box[2] = {(uint32_t)T::UW, (uint32_t)T::UH};
+            return make_map_f64(ptr, 2, dims, strides, box);
         });
     }
     template <int P, int MODE>
@@ -389,21 +373,15 @@ struct ScmOperator final : Operator {
             attr_set = true;
         }
         Mats2<P> mt;
-        for (int i = 0; i < (P + 1) * (P + 1); ++i) {
-            mt.m1[i] = m1[i];
-            mt.k1[i] = k1[i];
-            mt.xk[i] = sk * k1[i];
-            mt.xm[i] = sk * m1[i];
-        }
+        for (int i = 0; i <= P; ++i)
+            for (int j = 0; j <= P; ++j)
+                if (orb_key(P, i, j) == i * 16 + j) {
+                    mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
+                    mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
+                }
         Scm2DGeo g{n_e, n1, mask.p, cut_id.p, KT.p, cflags.p, n_strips, n_rtiles, pitch};
-        const CUtensorMap& mu = state_map<P>(a.cur, MAP_U);
-        const CUtensorMap& mp = MODE == MODE_STEP ? state_map<P>(a.prev, MAP_E) : mu;
-        const CUtensorMap& mm = MODE == MODE_STEP ? state_map<P>(a.minv, MAP_E) : mu;
-        const int64_t n_tiles = n_strips * n_rtiles;
-        const int64_t ctas = std::min<int64_t>(n_tiles, ctx->sm_count);
-        const int64_t chunk = ceil_div(n_tiles, ctas);
-        k_scm2d<P, MODE><<<(unsigned)ceil_div(n_tiles, chunk), T::RPE * 32, T::SMEM, ctx->stream>>>(
-            mu, mp, mm, g, mt, a, n_tiles, chunk);
+        dim3 grid((unsigned)n_strips, (unsigned)n_rtiles);
+        k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(state_map<P>(a.cur), g, mt, sk, a);
         ctx->launches++;
     }
     template <int MODE>
@@ -499,8 +477,10 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
         cid[c] = (int32_t)e;
         const double* K = d->cut_K + e * L * L;
         double* T = KT.data() + e * L * L;
+        // stored transposed and divided by sk: the kernel scales every
+        // output node by sk once (tensor and cut parts alike)
         for (int r = 0; r < L; ++r)
-            for (int m = 0; m < L; ++m) T[m * L + r] = K[r * L + m];
+            for (int m = 0; m < L; ++m) T[m * L + r] = K[r * L + m] / d->sk;
     }
     for (int64_t c = 0; c < n_cells; ++c)
         WCB_REQUIRE(d->cell_class[c] != 2 || cid[c] >= 0, "a cut cell is missing from cut_cells");
