@@ -336,7 +336,7 @@ def main():
                 "setup_s": round(t_build, 2), "power_iteration_s": round(t_eig, 3)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": f"k_scm2d<{prob.grid.p},STEP> + k_cut_apply per time step",
+                         "kernel": f"k_scm{prob.grid.dim}d<{prob.grid.p},STEP> (one fused launch per time step)",
                          "bytes_per_launch": bytes_step,
                          "launch_us": per_step_s * 1e6, "peak_kind": peak_kind},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),

@@ -28,8 +28,7 @@
 //     transposed so a lane reads its rows contiguously);
 //   * epilogue: psi_new = 2 psi - psi_prev + dt^2 minv (f F - K psi) and the
 //     block max |psi_new| (one atomicMax per CTA), src/timeint.py:179-190.
-#include "wcb_internal.cuh"
-#include "wcb_tma.cuh"
+#include "wcb_scm.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -38,45 +37,8 @@
 
 namespace wcb {
 
-constexpr int PADJ = 32;
 // element rows per tile; one compute warp each plus one halo warp
 __host__ __device__ constexpr int rpe_for(int P) { return P <= 4 ? 4 : 2; }
-
-// The 1D GLL-Lagrange factors m1, k1 are symmetric and centro-symmetric
-// (A[i][j] = A[j][i] = A[P-i][P-j]); only one value per orbit is kept, so all
-// coefficients of the sum factorisation fit in registers.  sk is applied once
-// per output node: sk (k1 (x) m1 + m1 (x) k1) u = sk * [k1 (x) m1 + m1 (x) k1] u.
-__host__ __device__ constexpr int orb_key(int P, int i, int j) {
-    // canonical representative: lexicographically smallest of the 4 images
-    int a0 = i * 16 + j, a1 = j * 16 + i, a2 = (P - i) * 16 + (P - j), a3 = (P - j) * 16 + (P - i);
-    int m = a0 < a1 ? a0 : a1;
-    m = m < a2 ? m : a2;
-    return m < a3 ? m : a3;
-}
-__host__ __device__ constexpr int orb_count(int P) {
-    int n = 0;
-    for (int i = 0; i <= P; ++i)
-        for (int j = 0; j <= P; ++j)
-            if (orb_key(P, i, j) == i * 16 + j) ++n;
-    return n;
-}
-__host__ __device__ constexpr int orb(int P, int i, int j) {
-    const int key = orb_key(P, i, j);
-    int n = 0;
-    for (int a = 0; a <= P; ++a)
-        for (int b = 0; b <= P; ++b)
-            if (orb_key(P, a, b) == a * 16 + b) {
-                if (a * 16 + b == key) return n;
-                ++n;
-            }
-    return -1;
-}
-
-template <int P>
-struct Mats2 {
-    double m[orb_count(P)];   // m1 orbit representatives
-    double k[orb_count(P)];   // k1 orbit representatives
-};
 
 // Tile geometry of the 2D kernel: a tile is 32p node columns x RPE*p node rows;
 // only psi_k (with its halo) is staged in shared memory by TMA.
@@ -108,8 +70,6 @@ struct Scm2DGeo {
     int64_t n_rtiles;
     int64_t pitch;            // row pitch of the state (doubles)
 };
-
-enum { MODE_STEP = 0, MODE_APPLY = 1 };
 
 // One node row of the smem tile: y contraction (masked) then x contraction
 // accumulated into Y.  `row` points at tile column 0 of that row.
@@ -335,6 +295,7 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32) k_scm2d(const __grid_con
 struct ScmOperator final : Operator {
     int dim = 2, p = 4;
     int64_t n_e = 0, n1 = 0, pitch = 0, rows = 0;
+    int64_t pplane = 0, n_zs = 0, n_xt = 0;   // 3D
     std::vector<int64_t> sidx;
     DevBuf<int64_t> d_sidx;
     DevBuf<uint8_t> mask, cflags;
@@ -396,23 +357,57 @@ struct ScmOperator final : Operator {
             default: throw Error{WCB_E_UNSUPPORTED, "2D SCM kernel built for p = 1..6"};
         }
     }
+    template <int P>
+    const CUtensorMap& state_map3(const double* ptr) {
+        using T = Tile3<P>;
+        return maps.get(ptr, 3, [&] {
+            const uint64_t dims[3] = {(uint64_t)pitch, (uint64_t)rows, (uint64_t)rows};
+            const uint64_t strides[2] = {(uint64_t)pitch, (uint64_t)pplane};
+            const uint32_t box[3] = {(uint32_t)T::UW, (uint32_t)T::UR, (uint32_t)T::UP};
+            return make_map_f64(ptr, 3, dims, strides, box);
+        });
+    }
+    template <int P, int MODE>
+    void launch3d(const StepArgs& a) {
+        Mats2<P> mt;
+        for (int i = 0; i <= P; ++i)
+            for (int j = 0; j <= P; ++j)
+                if (orb_key(P, i, j) == i * 16 + j) {
+                    mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
+                    mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
+                }
+        Scm3DGeo g{n_e, n1, pitch, pplane, mask.p, cut_id.p, KT.p, cflags.p, n_zs, n_xt};
+        launch_scm3d<P, MODE>(ctx, state_map3<P>(a.cur), g, mt, sk, a);
+    }
+    template <int MODE>
+    void dispatch3d(const StepArgs& a) {
+        switch (p) {
+            case 1: launch3d<1, MODE>(a); break;
+            case 2: launch3d<2, MODE>(a); break;
+            case 3: launch3d<3, MODE>(a); break;
+            case 4: launch3d<4, MODE>(a); break;
+            default: throw Error{WCB_E_UNSUPPORTED, "3D SCM kernel built for p = 1..4"};
+        }
+    }
     void apply(const double* x, double* y) override {
         StepArgs a;
         a.cur = x;
         a.out = y;
-        dispatch2d<MODE_APPLY>(a);
+        if (dim == 3) dispatch3d<MODE_APPLY>(a); else dispatch2d<MODE_APPLY>(a);
         WCB_CHECK_LAUNCH();
     }
     void cdm_step(const StepArgs& a) override {
-        dispatch2d<MODE_STEP>(a);
+        if (dim == 3) dispatch3d<MODE_STEP>(a); else dispatch2d<MODE_STEP>(a);
         WCB_CHECK_LAUNCH();
     }
     double step_bytes() const override { return bytes_step; }
 };
 
+static Operator* make_scm3d(Context* ctx, const wcb_scm_desc* d);
+
 Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
     WCB_REQUIRE(d->dim == 2 || d->dim == 3, "dim must be 2 or 3");
-    if (d->dim == 3) throw Error{WCB_E_UNSUPPORTED, "3D SCM kernel not built yet"};
+    if (d->dim == 3) return make_scm3d(ctx, d);
     const int p = d->p;
     WCB_REQUIRE(p >= 1 && p <= 6, "p must be in 1..6 for the 2D kernel");
     WCB_REQUIRE(d->n_e[0] == d->n_e[1] && d->n_e[0] >= 1, "square grids only (n_e[0] == n_e[1])");
@@ -496,6 +491,96 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
     op->KT.alloc(KT.size());
     op->KT.upload(KT.data(), KT.size(), st);
     // algorithmic bytes per step: 32 B per DOF + packed cut K
+    op->bytes_step = 32.0 * (double)op->n + 8.0 * (double)L * (L + 1) / 2.0 * (double)op->n_cut;
+    WCB_CUDA(cudaStreamSynchronize(st));
+    return guard.release();
+}
+
+
+// 3D: state = planes (x) of rows (y) of columns (z), padded by p planes/rows
+// on each side and PADJ columns on the left.
+static Operator* make_scm3d(Context* ctx, const wcb_scm_desc* d) {
+    const int p = d->p;
+    WCB_REQUIRE(p >= 1 && p <= 4, "p must be in 1..4 for the 3D kernel");
+    WCB_REQUIRE(d->n_e[0] == d->n_e[1] && d->n_e[1] == d->n_e[2] && d->n_e[0] >= 1,
+                "cubic grids only (n_e equal on all axes)");
+    WCB_REQUIRE(d->k1 && d->m1 && d->cell_class && (d->n_dof == 0 || d->lex_of_compact),
+                "NULL array in SCM descriptor");
+    auto* op = new ScmOperator();
+    std::unique_ptr<ScmOperator> guard(op);
+    op->ctx = ctx;
+    op->dim = 3;
+    op->p = p;
+    const int64_t n_e = d->n_e[0];
+    const int64_t n1 = n_e * p + 1;
+    op->n_e = n_e;
+    op->n1 = n1;
+    op->n = d->n_dof;
+    const int64_t TZ = 32 * (int64_t)p;
+    const int64_t need_cols = PADJ + ceil_div(n1, TZ) * TZ + p + 2;
+    op->pitch = ceil_div(need_cols, 32) * 32;
+    op->rows = n1 + 2 * p;
+    op->pplane = op->rows * op->pitch;
+    op->n_state = op->rows * op->pplane;
+    const int N = p + 1;
+    op->m1.assign(d->m1, d->m1 + N * N);
+    op->k1.assign(d->k1, d->k1 + N * N);
+    op->sk = d->sk;
+    const int64_t s_ = n_e + 2;
+    const int64_t n_cells = n_e * n_e * n_e;
+    std::vector<uint8_t> mask(s_ * s_ * s_, 0);
+    for (int64_t i = 0; i < n_e; ++i)
+        for (int64_t j = 0; j < n_e; ++j)
+            for (int64_t k = 0; k < n_e; ++k) {
+                const int8_t c = d->cell_class[(i * n_e + j) * n_e + k];
+                WCB_REQUIRE(c >= 0 && c <= 2, "cell_class values must be 0, 1 or 2");
+                mask[((i + 1) * s_ + (j + 1)) * s_ + (k + 1)] = (uint8_t)c;
+            }
+    // tiles: z strip (32 cells) x one y node-row block (cell row ey) x RX x cell rows
+    const int RX = rx_for3(p);
+    op->n_zs = ceil_div(n1, TZ);
+    op->n_xt = ceil_div(n1, (int64_t)RX * p);
+    std::vector<uint8_t> cf(op->n_xt * (n_e + 1) * op->n_zs, 0);
+    op->sidx.resize(op->n);
+    const int64_t n1sq = n1 * n1;
+    for (int64_t i = 0; i < op->n; ++i) {
+        const int64_t lex = d->lex_of_compact[i];
+        WCB_REQUIRE(lex >= 0 && lex < n1sq * n1, "lex_of_compact out of range");
+        if (i) WCB_REQUIRE(d->lex_of_compact[i - 1] < lex, "lex_of_compact must be ascending");
+        const int64_t I = lex / n1sq, J = (lex / n1) % n1, K = lex % n1;
+        op->sidx[i] = (I + p) * op->pplane + (J + p) * op->pitch + K + PADJ;
+        const int64_t ey = J / p;   // CTA owning node row J (rows ey*p .. ey*p+p-1)
+        cf[((I / (RX * p)) * (n_e + 1) + ey) * op->n_zs + K / TZ] = 1;
+    }
+    op->n_cut = d->n_cut;
+    op->L = N * N * N;
+    const int L = op->L;
+    std::vector<int32_t> cid(n_cells, -1);
+    std::vector<double> KT((size_t)std::max<int64_t>(op->n_cut, 1) * L * L, 0.0);
+    for (int64_t e = 0; e < op->n_cut; ++e) {
+        WCB_REQUIRE(d->cut_cells && d->cut_K, "cut arrays NULL");
+        const int64_t c = d->cut_cells[e];
+        WCB_REQUIRE(c >= 0 && c < n_cells && d->cell_class[c] == 2, "cut_cells must list cut cells");
+        if (e) WCB_REQUIRE(d->cut_cells[e - 1] < c, "cut_cells must be ascending");
+        cid[c] = (int32_t)e;
+        const double* K = d->cut_K + e * L * L;
+        double* T = KT.data() + e * L * L;
+        for (int r = 0; r < L; ++r)
+            for (int m = 0; m < L; ++m) T[m * L + r] = K[r * L + m] / d->sk;
+    }
+    for (int64_t c = 0; c < n_cells; ++c)
+        WCB_REQUIRE(d->cell_class[c] != 2 || cid[c] >= 0, "a cut cell is missing from cut_cells");
+    cudaStream_t st = ctx->stream;
+    op->d_sidx.alloc(std::max<int64_t>(op->n, 1));
+    op->d_sidx.upload(op->sidx.data(), op->n, st);
+    op->mask.alloc(mask.size());
+    op->mask.upload(mask.data(), mask.size(), st);
+    op->cflags.alloc(cf.size());
+    op->cflags.upload(cf.data(), cf.size(), st);
+    op->cut_id.alloc(cid.size());
+    op->cut_id.upload(cid.data(), cid.size(), st);
+    op->KT.alloc(KT.size());
+    op->KT.upload(KT.data(), KT.size(), st);
     op->bytes_step = 32.0 * (double)op->n + 8.0 * (double)L * (L + 1) / 2.0 * (double)op->n_cut;
     WCB_CUDA(cudaStreamSynchronize(st));
     return guard.release();

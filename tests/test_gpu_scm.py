@@ -83,15 +83,54 @@ def test_config2_geometry_reduced_scale():
     assert rel(r.psi, psi_ref) <= 1e-10
 
 
-def test_scm_operator_from_reference_cube_rejects_3d_until_built():
-    g = load_golden("cube_p2n4")
-    try:
-        op = ScmOperator(dim=3, p=int(g["p"]), n_e=tuple(g["n_e"]), k1=g["k1"], m1=g["m1"],
-                         sk=float(g["sk"]), cell_class=g["cell_class"],
-                         lex_of_compact=g["lex_of_compact"], cut_cells=g["cut_cells"],
-                         cut_K=g["cut_K"])
-    except NotImplementedError:
-        pytest.skip("3D kernel not built")
-    K = csr_from(g, "K")
-    x = g["X"][:, 0]
+def _cube_op(g):
+    return ScmOperator(dim=3, p=int(g["p"]), n_e=tuple(g["n_e"]), k1=g["k1"], m1=g["m1"],
+                       sk=float(g["sk"]), cell_class=g["cell_class"],
+                       lex_of_compact=g["lex_of_compact"], cut_cells=g["cut_cells"],
+                       cut_K=g["cut_K"])
+
+
+@pytest.mark.parametrize("name", ["cube_p2n4", "cube_p3n6"])
+def test_3d_operator_on_reference_cube(name):
+    """The reference's own rotated-cube benchmark system, built by the
+    reference (golden): device matrix-free K vs the reference CSR K."""
+    g = load_golden(name)
+    op = _cube_op(g)
+    for col in range(g["X"].shape[1]):
+        assert rel(op @ g["X"][:, col], g["KX"][:, col]) <= 1e-13
+
+
+def test_3d_cube_cdm_and_dt_crit_match_reference():
+    g = load_golden("cube_p3n6")
+    op = _cube_op(g)
+    M = sp.diags(g["M"]).tocsr()
+    lam, it = max_gen_eig(op, M, tol=1e-7, seed=0)
+    assert abs(lam - float(g["lam"])) <= 1e-12 * float(g["lam"])
+    assert abs(it - int(g["iters"])) <= 1
+    f = lambda t: ricker(t, 10.0)
+    r = cdm_run(M, op, g["F"], f, float(g["dt"]), int(g["n_t"]), obs_mat=csr_from(g, "obs"))
+    assert rel(r.psi, g["psi"]) <= 1e-10
+    assert rel(r.obs, g["obs"]) <= 1e-10
+
+
+@pytest.mark.parametrize("p,n_e", [(1, 7), (2, 9), (3, 12), (3, 40)])
+def test_3d_sphere_voids_apply_and_cdm(p, n_e):
+    """Config-5 style geometry (sphere + small voids) at reduced size: device
+    apply vs host CSR, and 100 CDM steps vs the CPU oracle loop."""
+    from paper_2501_19013_b200.setup.configs import build_scm as _b
+    from paper_2501_19013_b200.setup.configs import CONFIGS as _C
+    from dataclasses import replace
+    cfg = replace(_C["config5"], p=p, n_e=n_e, n_random=6, r_range=(0.03, 0.08), name="c5s")
+    prob = _b(cfg)
+    from oracle import cpu
+    K = cpu.scm_csr(prob)
+    op = prob.device_operator()
+    x = np.random.default_rng(p).standard_normal(prob.n_dof)
     assert rel(op @ x, K @ x) <= 1e-13
+    M = prob.mass_matrix()
+    lam, _ = max_gen_eig(op, M, tol=1e-7, seed=0)
+    dt = 0.9 * 2.0 / np.sqrt(lam)
+    f = lambda t: ricker(t, 10.0)
+    psi_ref, _, _ = O.cdm_run(M, K, prob.F_s, f, dt, 100)
+    r = cdm_run(M, op, prob.F_s, f, dt, 100)
+    assert rel(r.psi, psi_ref) <= 1e-10
