@@ -155,7 +155,8 @@ int wcb_imex_plan_create(wcb_operator* K, int64_t n_c, const int64_t* c_idx,
                          const wcb_observer* obs, wcb_imex_plan** out);
 int wcb_imex_plan_destroy(wcb_imex_plan* plan);
 /* ft_k[k] = f_t(k*dt), ft_new[k] = f_t(k*dt + dt) (src/timeint.py:259-260),
- * f0 = f_t(0.0).  psi_dot_out (n) receives v when d is empty, else untouched. */
+ * f0 = f_t(0.0).  psi_dot_out (n_c, may be NULL) receives the final v_c in
+ * c order (the reference returns it scattered when d is empty, :285-288). */
 int wcb_imex_plan_run(wcb_imex_plan* plan, double f0, const double* ft_k,
                       const double* ft_new, double dt, int64_t n_t, double beta,
                       double gamma, const double* psi0, const double* v0,

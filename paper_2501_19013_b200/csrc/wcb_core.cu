@@ -108,6 +108,13 @@ __global__ void k_obs_record(int64_t n_obs, const int64_t* __restrict__ indptr,
     out[r * stride + k] = s;
 }
 
+__global__ void k_record_observers(StepArgs a) { record_observers(a); }
+
+void launch_record_observers(Context* ctx, const StepArgs& a) {
+    k_record_observers<<<1, 64, 0, ctx->stream>>>(a);
+    ctx->launches++;
+}
+
 // ---- power iteration pieces (src/linalg.py:108-119) ----
 constexpr int RB = 256;
 

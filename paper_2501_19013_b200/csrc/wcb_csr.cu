@@ -56,9 +56,10 @@ __global__ void __launch_bounds__(BLOCK) k_csr_cdm(int64_t n, const int64_t* __r
         const double f = a.ft[a.k];
         const double u = a.cur[row];
         const double up = a.prev[row];
-        const double v = leapfrog(u, up, Ku, a.minv[row], f * source_at(a.F, row), a.dt2);
+        const double mi = a.minv[row];
+        const double v = leapfrog(u, up, Ku, mi, f * source_at(a.F, row), a.dt2);
         a.out[row] = v;
-        amp = amp_bits(v);
+        amp = mi != 0.0 ? amp_bits(v) : 0ULL;
     }
     block_amp_max<BLOCK>(amp, a.amp);
 }

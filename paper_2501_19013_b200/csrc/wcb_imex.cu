@@ -1,17 +1,472 @@
-// placeholder for the IMEX plan
+// Implicit-explicit split integration on the device: imex_run,
+// src/timeint.py:196-292 (Algorithm 2).
+//
+// Per step k (all on the device, stream-ordered):
+//   1. fused explicit step of the operator on every node (d rows get
+//      psi_d^{k+1} = 2 psi - psi_prev + dt^2 (f(t_k) F - K psi)/m_d, src :261-269;
+//      c slots carry 1/m = 0 and are overwritten next);
+//   2. c predictor psi_c^pred = psi_c + dt v_c + dt^2/2 (1-2beta) a_c, written
+//      into the new state (src :271-274);
+//   3. rhs_c = f(t_k + dt) F_c - (K psi_mixed)_c (src :275) -- K applied to the
+//      c rows only where the operator supports it;
+//   4. a_c = S_cc^-1 rhs_c with S_cc = M_cc + beta dt^2 K_cc prefactorised on
+//      the host (SuperLU, the reference's factorize(), src/linalg.py:70-80):
+//      row permutation, forward solve with L, backward solve with U, column
+//      permutation (src :278);
+//   5. corrector psi_c = pred + beta dt^2 a_c, v_c = v_pred + gamma dt a_c,
+//      and max|psi_c| into the divergence slot (src :279-282).
+// The triangular solves are synchronisation-free: warps take rows in
+// elimination order from an atomic counter, wait (acquire) for the rows they
+// depend on, sum in a fixed lane order and publish (release) their row -- one
+// launch per solve, deterministic results.
 #include "wcb_internal.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+namespace wcb {
+
+struct DevLU {
+    int64_t n = 0;
+    DevBuf<int64_t> perm_r, perm_c;
+    DevBuf<int64_t> Lp, Up;
+    DevBuf<int32_t> Li, Ui;
+    DevBuf<double> Lx, Ux;
+    void load(const wcb_lu* lu, cudaStream_t s) {
+        n = lu->n;
+        perm_r.alloc(std::max<int64_t>(n, 1));
+        perm_c.alloc(std::max<int64_t>(n, 1));
+        perm_r.upload(lu->perm_r, n, s);
+        perm_c.upload(lu->perm_c, n, s);
+        const int64_t nl = lu->L_indptr[n], nu = lu->U_indptr[n];
+        Lp.alloc(n + 1); Lp.upload(lu->L_indptr, n + 1, s);
+        Up.alloc(n + 1); Up.upload(lu->U_indptr, n + 1, s);
+        Li.alloc(std::max<int64_t>(nl, 1)); Li.upload(lu->L_indices, nl, s);
+        Ui.alloc(std::max<int64_t>(nu, 1)); Ui.upload(lu->U_indices, nu, s);
+        Lx.alloc(std::max<int64_t>(nl, 1)); Lx.upload(lu->L_data, nl, s);
+        Ux.alloc(std::max<int64_t>(nu, 1)); Ux.upload(lu->U_data, nu, s);
+    }
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Sync-free sparse triangular solve (CSR), x = T^-1 b.  `upper` processes rows
+// n-1 .. 0.  done[] must be zero on entry; counter[0] = 0.
+__global__ void k_sptrsv(int64_t n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                         const double* __restrict__ val, const double* __restrict__ b,
+                         double* x, int* done, unsigned long long* counter, int upper) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned long long slot = 0;
+        if (lane == 0) slot = atomicAdd(counter, 1ULL);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (slot >= (unsigned long long)n) break;
+        const int64_t i = upper ? (n - 1 - (int64_t)slot) : (int64_t)slot;
+        double s = 0.0, diag = 0.0;
+        for (int64_t j = ptr[i] + lane; j < ptr[i + 1]; j += 32) {
+            const int64_t c = idx[j];
+            const double a = val[j];
+            if (c == i) {
+                diag = a;
+            } else {
+                while (ld_acquire(done + c) == 0) {
+                }
+                s = fma(a, *((volatile const double*)(x + c)), s);
+            }
+        }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s += __shfl_down_sync(0xffffffffu, s, o);
+            diag += __shfl_down_sync(0xffffffffu, diag, o);
+        }
+        if (lane == 0) {
+            x[i] = (b[i] - s) / diag;
+            st_release(done + i, 1);
+        }
+        __syncwarp();
+    }
+}
+
+// y[perm_r[i]] = b[i]   (row permutation of SuperLU: Pr A Pc = L U)
+__global__ void k_perm_rows(int64_t n, const int64_t* __restrict__ perm_r, const double* __restrict__ b,
+                            double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[perm_r[i]] = b[i];
+}
+
+// c predictor (src/timeint.py:271-274) into the state slots of c, and keep v_pred
+__global__ void k_c_predict(int64_t nc, const int64_t* __restrict__ cs, const double* __restrict__ psi_c,
+                            const double* __restrict__ v_c, const double* __restrict__ a_c, double dt,
+                            double c1, double c2, double* __restrict__ state, double* __restrict__ pred,
+                            double* __restrict__ vpred) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
+        const double p = psi_c[i] + dt * v_c[i] + c1 * a_c[i];
+        pred[i] = p;
+        vpred[i] = v_c[i] + c2 * a_c[i];
+        state[cs[i]] = p;
+    }
+}
+
+// rhs_c = f F_c - Kc
+__global__ void k_c_rhs(int64_t nc, const double* __restrict__ Fc, const double* __restrict__ ft,
+                        int64_t k, const double* __restrict__ Kc, double* __restrict__ rhs) {
+    const double f = ft[k];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
+        rhs[i] = f * Fc[i] - Kc[i];
+}
+
+// corrector (src/timeint.py:279-282); a_c = z[perm_c[i]]; amp over c nodes
+__global__ void k_c_correct(int64_t nc, const int64_t* __restrict__ cs, const int64_t* __restrict__ perm_c,
+                            const double* __restrict__ z, const double* __restrict__ pred,
+                            const double* __restrict__ vpred, double bdt2, double gdt,
+                            double* __restrict__ a_c, double* __restrict__ psi_c, double* __restrict__ v_c,
+                            double* __restrict__ state, unsigned long long* amp_slot) {
+    unsigned long long amp = 0ULL;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
+        const double a = z[perm_c[i]];
+        a_c[i] = a;
+        const double p = pred[i] + bdt2 * a;
+        psi_c[i] = p;
+        v_c[i] = vpred[i] + gdt * a;
+        state[cs[i]] = p;
+        unsigned long long b = amp_bits(p);
+        amp = b > amp ? b : amp;
+    }
+    block_amp_max<256>(amp, amp_slot);
+}
+
+__global__ void k_gather_rows(int64_t n, const int64_t* __restrict__ map, const double* __restrict__ src,
+                              double* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[map[i]];
+}
+
+// bootstrap (src/timeint.py:246-256): prev_d = psi - dt v + dt^2/2 a_d for d slots
+__global__ void k_imex_boot(int64_t ns, const double* __restrict__ psi, const double* __restrict__ v,
+                            const double* __restrict__ Kpsi, const double* __restrict__ m_d_state,
+                            Source F, const double* __restrict__ ft, double dt, double* __restrict__ prev) {
+    const double f0 = ft[0];
+    const double c = 0.5 * dt * dt;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x) {
+        const double md = m_d_state[i];
+        double a = md > 0.0 ? (f0 * source_at(F, i) - Kpsi[i]) / md : 0.0;
+        prev[i] = psi[i] - dt * v[i] + c * a;
+    }
+}
+
+}  // namespace wcb
+
+using namespace wcb;
+
+struct wcb_imex_plan {
+    Operator* op = nullptr;
+    int64_t n_c = 0, n_d = 0;
+    DevBuf<int64_t> c_state;          // state index of each c DOF (c order)
+    DevBuf<int64_t> c_compact;
+    DevBuf<double> minv, m_d_state;   // 1/m_d at d slots (0 at c / non-DOF), m_d at d slots
+    DevBuf<double> Fc;
+    DevBuf<double> F_dense;
+    DevBuf<int64_t> F_idx;
+    DevBuf<double> F_val;
+    Source src;
+    DevLU S, Mcc;
+    int64_t n_obs = 0;
+    DevBuf<int64_t> obs_indptr, obs_idx;
+    DevBuf<double> obs_val;
+    // work
+    DevBuf<double> A, B, T, V;
+    DevBuf<double> psi_c, v_c, a_c, pred, vpred, Kc, rhs, y, z;
+    DevBuf<int> done;
+    DevBuf<unsigned long long> counter;
+    DevBuf<unsigned long long> amp;
+    DevBuf<double> ft_k, ft_new;
+};
+
+namespace wcb {
+static int grid1(Context* ctx, int64_t n) {
+    return (int)std::min<int64_t>(std::max<int64_t>(ceil_div(n, 256), 1), (int64_t)ctx->sm_count * 8);
+}
+
+static void lu_solve(Context* ctx, wcb_imex_plan* P, DevLU& F, const double* b, double* x) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = F.n;
+    if (!n) return;
+    k_perm_rows<<<grid1(ctx, n), 256, 0, s>>>(n, F.perm_r.p, b, P->y.p);
+    // forward: L w = y  (into z), backward: U v = w (into y)
+    WCB_CUDA(cudaMemsetAsync(P->done.p, 0, n * sizeof(int), s));
+    WCB_CUDA(cudaMemsetAsync(P->counter.p, 0, 2 * sizeof(unsigned long long), s));
+    const int blocks = (int)std::min<int64_t>(ceil_div(n, 8), (int64_t)ctx->sm_count * 16);
+    k_sptrsv<<<blocks, 256, 0, s>>>(n, F.Lp.p, F.Li.p, F.Lx.p, P->y.p, P->z.p, P->done.p, P->counter.p, 0);
+    WCB_CUDA(cudaMemsetAsync(P->done.p, 0, n * sizeof(int), s));
+    k_sptrsv<<<blocks, 256, 0, s>>>(n, F.Up.p, F.Ui.p, F.Ux.p, P->z.p, x, P->done.p, P->counter.p + 1, 1);
+    ctx->launches += 3;
+    WCB_CHECK_LAUNCH();
+}
+}  // namespace wcb
+
 extern "C" {
-int wcb_imex_plan_create(wcb_operator*, int64_t, const int64_t*, int64_t, const int64_t*,
-                         const double*, const wcb_lu*, const wcb_lu*, const double*,
-                         const wcb_observer*, wcb_imex_plan**) {
-    wcb::set_error("imex not built yet");
-    return WCB_E_UNSUPPORTED;
+
+int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int64_t n_d,
+                         const int64_t* d_idx, const double* m_d, const wcb_lu* S_cc,
+                         const wcb_lu* M_cc, const double* F_s, const wcb_observer* obs,
+                         wcb_imex_plan** out) {
+    try {
+        WCB_REQUIRE(o && out && F_s, "NULL argument");
+        Operator* op = o->op;
+        Context* ctx = op->ctx;
+        WCB_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const int64_t n = op->n, ns = op->n_state;
+        WCB_REQUIRE(n_c + n_d == n, "c and d index sets must partition the DOFs");
+        std::unique_ptr<wcb_imex_plan> P(new wcb_imex_plan());
+        P->op = op;
+        P->n_c = n_c;
+        P->n_d = n_d;
+        const std::vector<int64_t>& si = op->state_index();
+        std::vector<uint8_t> seen(n, 0);
+        std::vector<double> minv(ns, 0.0), md(ns, 0.0);
+        for (int64_t i = 0; i < n_d; ++i) {
+            const int64_t r = d_idx[i];
+            WCB_REQUIRE(r >= 0 && r < n && !seen[r], "c and d index sets must partition the DOFs");
+            seen[r] = 1;
+            WCB_REQUIRE(m_d[i] > 0.0, "d mass block has non-positive diagonal entries");
+            minv[si[r]] = 1.0 / m_d[i];
+            md[si[r]] = m_d[i];
+        }
+        std::vector<int64_t> cs(std::max<int64_t>(n_c, 1));
+        std::vector<double> Fc(std::max<int64_t>(n_c, 1));
+        for (int64_t i = 0; i < n_c; ++i) {
+            const int64_t r = c_idx[i];
+            WCB_REQUIRE(r >= 0 && r < n && !seen[r], "c and d index sets must partition the DOFs");
+            seen[r] = 1;
+            cs[i] = si[r];
+            Fc[i] = F_s[r];
+        }
+        P->minv.alloc(ns); P->minv.upload(minv.data(), ns, s);
+        P->m_d_state.alloc(ns); P->m_d_state.upload(md.data(), ns, s);
+        P->c_state.alloc(cs.size()); P->c_state.upload(cs.data(), n_c, s);
+        P->Fc.alloc(Fc.size()); P->Fc.upload(Fc.data(), n_c, s);
+        // force vector for the d rows (sparse when possible)
+        std::vector<std::pair<int64_t, double>> nz;
+        for (int64_t i = 0; i < n; ++i)
+            if (F_s[i] != 0.0) nz.emplace_back(si[i], F_s[i]);
+        std::sort(nz.begin(), nz.end());
+        if (nz.size() <= 4096 || (int64_t)nz.size() * 16 <= n) {
+            std::vector<int64_t> idx(nz.size());
+            std::vector<double> val(nz.size());
+            for (size_t i = 0; i < nz.size(); ++i) { idx[i] = nz[i].first; val[i] = nz[i].second; }
+            P->F_idx.alloc(std::max<size_t>(idx.size(), 1)); P->F_idx.upload(idx.data(), idx.size(), s);
+            P->F_val.alloc(std::max<size_t>(val.size(), 1)); P->F_val.upload(val.data(), val.size(), s);
+            P->src.idx = P->F_idx.p; P->src.val = P->F_val.p; P->src.nnz = (int64_t)idx.size();
+            if (!idx.empty()) { P->src.lo = idx.front(); P->src.hi = idx.back(); }
+        } else {
+            std::vector<double> Fd(ns, 0.0);
+            for (auto& q : nz) Fd[q.first] = q.second;
+            P->F_dense.alloc(ns); P->F_dense.upload(Fd.data(), ns, s);
+            P->src.dense = P->F_dense.p;
+        }
+        if (n_c) {
+            WCB_REQUIRE(S_cc && M_cc && S_cc->n == n_c && M_cc->n == n_c, "LU factors of size n_c required");
+            P->S.load(S_cc, s);
+            P->Mcc.load(M_cc, s);
+        }
+        if (obs && obs->n_obs > 0) {
+            P->n_obs = obs->n_obs;
+            const int64_t nnz = obs->indptr[obs->n_obs];
+            std::vector<int64_t> sidx(std::max<int64_t>(nnz, 1));
+            for (int64_t j = 0; j < nnz; ++j) {
+                WCB_REQUIRE(obs->indices[j] >= 0 && obs->indices[j] < n, "observer column out of range");
+                sidx[j] = si[obs->indices[j]];
+            }
+            P->obs_indptr.alloc(obs->n_obs + 1); P->obs_indptr.upload(obs->indptr, obs->n_obs + 1, s);
+            P->obs_idx.alloc(sidx.size()); P->obs_idx.upload(sidx.data(), nnz, s);
+            P->obs_val.alloc(std::max<int64_t>(nnz, 1)); P->obs_val.upload(obs->data, nnz, s);
+        }
+        const int64_t m = std::max<int64_t>(n_c, 1);
+        P->A.alloc(ns); P->B.alloc(ns); P->T.alloc(ns); P->V.alloc(ns);
+        P->psi_c.alloc(m); P->v_c.alloc(m); P->a_c.alloc(m); P->pred.alloc(m); P->vpred.alloc(m);
+        P->Kc.alloc(m); P->rhs.alloc(m); P->y.alloc(m); P->z.alloc(m);
+        P->done.alloc(m);
+        P->counter.alloc(2);
+        WCB_CUDA(cudaStreamSynchronize(s));
+        *out = P.release();
+        return WCB_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
 }
-int wcb_imex_plan_destroy(wcb_imex_plan*) { return WCB_OK; }
-int wcb_imex_plan_run(wcb_imex_plan*, double, const double*, const double*, double, int64_t,
-                      double, double, const double*, const double*, double*, double*, double*,
-                      wcb_divergence*, wcb_timings*) {
-    wcb::set_error("imex not built yet");
-    return WCB_E_UNSUPPORTED;
+
+int wcb_imex_plan_destroy(wcb_imex_plan* plan) {
+    if (!plan) return WCB_OK;
+    cudaSetDevice(plan->op->ctx->device);
+    cudaStreamSynchronize(plan->op->ctx->stream);
+    delete plan;
+    return WCB_OK;
 }
+
+int wcb_imex_plan_run(wcb_imex_plan* P, double f0, const double* ft_k, const double* ft_new,
+                      double dt, int64_t n_t, double beta, double gamma, const double* psi0,
+                      const double* v0, double* psi_out, double* psi_dot_out, double* obs_out,
+                      wcb_divergence* div, wcb_timings* tm) {
+    try {
+        WCB_REQUIRE(P && psi_out, "NULL argument");
+        WCB_REQUIRE(n_t >= 0, "negative n_t");
+        Operator* op = P->op;
+        Context* ctx = op->ctx;
+        WCB_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const int64_t n = op->n, ns = op->n_state, nc = P->n_c;
+        const bool has_c = nc > 0, has_d = P->n_d > 0;
+        if (div) { div->step = -1; div->amplitude = 0.0; }
+        if (tm) { tm->factorization = 0.0; tm->rhs = 0.0; tm->backward_insertion = 0.0; }
+        // force tables: index 0 = f(0) for the bootstrap; ft_k[k], ft_new[k] per step
+        std::vector<double> hk(n_t + 1), hn(std::max<int64_t>(n_t, 1));
+        hk[0] = f0;
+        for (int64_t k = 0; k < n_t; ++k) { hk[k + 1] = ft_k[k]; hn[k] = ft_new[k]; }
+        P->ft_k.alloc(hk.size()); P->ft_k.upload(hk.data(), hk.size(), s);
+        P->ft_new.alloc(hn.size()); P->ft_new.upload(hn.data(), hn.size(), s);
+        P->amp.alloc(n_t + 1);
+        P->amp.zero(s);
+        // initial state
+        DevBuf<double> tmp(std::max<int64_t>(n, 1));
+        P->A.zero(s); P->V.zero(s); P->B.zero(s); P->T.zero(s);
+        if (psi0) { tmp.upload(psi0, n, s); op->scatter(tmp.p, P->A.p); }
+        if (v0) { tmp.upload(v0, n, s); op->scatter(tmp.p, P->V.p); }
+        // bootstrap (src/timeint.py:246-256)
+        op->apply(P->A.p, P->T.p);
+        k_imex_boot<<<grid1(ctx, ns), 256, 0, s>>>(ns, P->A.p, P->V.p, P->T.p, P->m_d_state.p, P->src,
+                                                   P->ft_k.p, dt, P->B.p);
+        ctx->launches++;
+        if (has_c) {
+            // r0_c = f0 F_c - (K psi)_c ; a_c = M_cc^-1 r0_c
+            k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
+            k_c_rhs<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->Fc.p, P->ft_k.p, 0, P->Kc.p, P->rhs.p);
+            ctx->launches += 2;
+            DevBuf<double> w(nc);
+            lu_solve(ctx, P, P->Mcc, P->rhs.p, w.p);
+            // a_c = w[perm_c]
+            k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->Mcc.perm_c.p, w.p, P->a_c.p);
+            k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->A.p, P->psi_c.p);
+            k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->V.p, P->v_c.p);
+            ctx->launches += 3;
+            WCB_CUDA(cudaStreamSynchronize(s));
+        }
+        WCB_CHECK_LAUNCH();
+        const int64_t stride = n_t + 1;
+        StepArgs a;
+        a.minv = P->minv.p;
+        a.F = P->src;
+        a.dt2 = dt * dt;
+        DevBuf<double> dobs;
+        if (P->n_obs && obs_out) dobs.alloc(P->n_obs * stride);
+        auto record = [&](int64_t k, const double* psi) {
+            if (!(P->n_obs && obs_out)) return;
+            StepArgs r;
+            r.cur = psi;
+            r.k = k;
+            r.n_obs = P->n_obs;
+            r.obs_ptr = P->obs_indptr.p;
+            r.obs_idx = P->obs_idx.p;
+            r.obs_val = P->obs_val.p;
+            r.obs_out = dobs.p;
+            r.obs_stride = stride;
+            launch_record_observers(ctx, r);
+        };
+        record(0, P->A.p);
+        double* cur = P->A.p;
+        double* prev = P->B.p;
+        const double c1 = 0.5 * dt * dt * (1.0 - 2.0 * beta);
+        const double c2 = dt * (1.0 - gamma);
+        const double bdt2 = beta * dt * dt;
+        const double gdt = gamma * dt;
+        WCB_CUDA(cudaEventRecord(ctx->ev0, s));
+        std::vector<unsigned long long> h_amp(n_t + 1, 0ULL);
+        int64_t checked = 0;
+        bool diverged = false;
+        auto inspect = [&](int64_t upto) -> bool {
+            if (upto <= checked) return false;
+            WCB_CUDA(cudaMemcpyAsync(h_amp.data() + checked + 1, P->amp.p + checked + 1,
+                                     (upto - checked) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+            WCB_CUDA(cudaStreamSynchronize(s));
+            for (int64_t k = checked + 1; k <= upto; ++k) {
+                double v;
+                std::memcpy(&v, &h_amp[k], sizeof(v));
+                if (!std::isfinite(v) || v > 1.0e12) {
+                    if (div) { div->step = k; div->amplitude = v; }
+                    return true;
+                }
+            }
+            checked = upto;
+            return false;
+        };
+        for (int64_t k = 0; k < n_t; ++k) {
+            // 1. explicit d step into prev (c slots overwritten below)
+            if (has_d) {
+                a.cur = cur;
+                a.prev = prev;
+                a.out = prev;
+                a.ft = P->ft_k.p + 1;   // ft_k[k]
+                a.k = k;
+                a.amp = P->amp.p + (k + 1);
+                op->cdm_step(a);
+            } else {
+                WCB_CUDA(cudaMemcpyAsync(prev, cur, ns * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            }
+            if (has_c) {
+                // 2. c predictor into the new state
+                k_c_predict<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->psi_c.p, P->v_c.p, P->a_c.p,
+                                                           dt, c1, c2, prev, P->pred.p, P->vpred.p);
+                // 3. rhs_c with updated d and predicted c
+                op->apply(prev, P->T.p);
+                k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
+                k_c_rhs<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->Fc.p, P->ft_new.p, k, P->Kc.p, P->rhs.p);
+                ctx->launches += 3;
+                // 4. a_c = S^-1 rhs_c (z permuted) ; 5. corrector
+                lu_solve(ctx, P, P->S, P->rhs.p, P->y.p);   // result in y (column-permuted space)
+                k_c_correct<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->S.perm_c.p, P->y.p, P->pred.p,
+                                                           P->vpred.p, bdt2, gdt, P->a_c.p, P->psi_c.p, P->v_c.p,
+                                                           prev, P->amp.p + (k + 1));
+                ctx->launches++;
+            }
+            std::swap(cur, prev);
+            record(k + 1, cur);
+            if ((k + 1) % 256 == 0) {
+                WCB_CHECK_LAUNCH();
+                if (inspect(k + 1)) { diverged = true; break; }
+            }
+        }
+        WCB_CUDA(cudaEventRecord(ctx->ev1, s));
+        WCB_CHECK_LAUNCH();
+        if (!diverged) diverged = inspect(n_t);
+        WCB_CUDA(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        WCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        if (tm) tm->rhs = ms * 1e-3;
+        if (diverged) throw Error{WCB_E_DIVERGED, "solution diverged"};
+        op->gather(cur, tmp.p);
+        WCB_CUDA(cudaMemcpyAsync(psi_out, tmp.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        // v_c in c order (the caller scatters it when d is empty, src/timeint.py:285-288)
+        if (psi_dot_out && has_c)
+            WCB_CUDA(cudaMemcpyAsync(psi_dot_out, P->v_c.p, nc * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (P->n_obs && obs_out)
+            WCB_CUDA(cudaMemcpyAsync(obs_out, dobs.p, P->n_obs * stride * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s));
+        WCB_CUDA(cudaStreamSynchronize(s));
+        return WCB_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
 }
+
+}  // extern "C"

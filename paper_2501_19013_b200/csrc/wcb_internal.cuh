@@ -216,6 +216,9 @@ Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* indptr,
                             const int32_t* indices, const double* data);
 Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d);
 
+// one-block observer recording (wcb_core.cu)
+void launch_record_observers(Context* ctx, const StepArgs& a);
+
 // generic elementwise kernels (wcb_core.cu)
 void launch_scatter(Context* ctx, int64_t n, const int64_t* d_map, const double* src,
                     double* dst_state);

@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32) k_scm2d(const __grid_con
                 for (int j = 0; j < P; ++j) {
                     if (!edge || Jl + j < g.n1) {
                         a.out[base + j] = v[j];
-                        unsigned long long b = amp_bits(v[j]);
+                        unsigned long long b = mi[j] != 0.0 ? amp_bits(v[j]) : 0ULL;
                         amp = b > amp ? b : amp;
                     }
                 }

@@ -253,10 +253,11 @@ __global__ void __launch_bounds__(Tile3<P>::NWARP * 32) k_scm3d(const __grid_con
                     for (int j = 0; j < P; ++j) {
                         if (Kl + j < g.n1) {
                             const double fF = src ? f * source_at(a.F, base + j) : f * 0.0;
-                            const double v = leapfrog(urow[j], a.prev[base + j], sk * Y[r][b][j],
-                                                      __ldg(a.minv + base + j), fF, a.dt2);
+                            const double mi = __ldg(a.minv + base + j);
+                            const double v = leapfrog(urow[j], a.prev[base + j], sk * Y[r][b][j], mi,
+                                                      fF, a.dt2);
                             a.out[base + j] = v;
-                            unsigned long long bits = amp_bits(v);
+                            unsigned long long bits = mi != 0.0 ? amp_bits(v) : 0ULL;
                             amp = bits > amp ? bits : amp;
                         }
                     }

@@ -57,8 +57,8 @@ class ScmProblem:
               lumping: str = "hrz"):
         if grid.basis.family != "lagrange":
             raise ValueError("ScmProblem needs the Lagrange (GLL) family")
-        if lumping not in ("hrz", "row_sum"):
-            raise ValueError("the explicit device path needs a lumped cut-cell mass")
+        if lumping not in ("hrz", "row_sum", "none"):
+            raise ValueError("lumping must be 'hrz', 'row_sum' or 'none'")
         d, p, h = grid.dim, grid.p, grid.h
         n = p + 1
         L = n ** d
@@ -69,14 +69,17 @@ class ScmProblem:
         cut = grid.cut_lex
         integ = CutCellIntegrator(grid, depth)
         cut_K = np.empty((cut.shape[0], L, L))
-        cut_M = np.empty((cut.shape[0], L))
+        cut_M = np.empty((cut.shape[0], L) if lumping != "none" else (cut.shape[0], L, L))
         shape = (grid.n_e,) * d
         for j, cl in enumerate(cut):
             ijk = np.unravel_index(int(cl), shape)
             Mi, Mo, Ki, Ko = integ.integrate(ijk)
             cut_K[j] = sk * (Ki + alpha * Ko)
             M_o = sm * (Mi + alpha * Mo)
-            cut_M[j] = hrz_lump(M_o) if lumping == "hrz" else row_sum_lump(M_o)
+            if lumping == "none":
+                cut_M[j] = M_o           # consistent cut mass (IMEX, src/assembly.py:591-592)
+            else:
+                cut_M[j] = hrz_lump(M_o) if lumping == "hrz" else row_sum_lump(M_o)
         prob = cls(grid=grid, rho=rho, c=c, alpha=alpha, depth=depth, lumping=lumping,
                    sk=sk, sm=sm, m1=m1, k1=k1, cut_K=cut_K, cut_M=cut_M,
                    m_diag=np.zeros(0))
@@ -103,7 +106,7 @@ class ScmProblem:
         node = node.ravel()
         m = node[g.dofmap.lex_of_compact]
         cut = g.cut_lex
-        if cut.shape[0]:
+        if cut.shape[0] and self.lumping != "none":
             dofs = self.cut_dofs()
             np.add.at(m, dofs.ravel(), self.cut_M.ravel())
         return m
@@ -155,13 +158,27 @@ class ScmProblem:
     def device_operator(self, device=None):
         from ..operators import ScmOperator
         g = self.grid
-        return ScmOperator(dim=g.dim, p=g.p, n_e=(g.n_e,) * g.dim, k1=self.k1, m1=self.m1,
-                           sk=self.sk, cell_class=g.classes.ravel(),
-                           lex_of_compact=g.dofmap.lex_of_compact, cut_cells=g.cut_lex,
-                           cut_K=self.cut_K, device=device)
+        op = ScmOperator(dim=g.dim, p=g.p, n_e=(g.n_e,) * g.dim, k1=self.k1, m1=self.m1,
+                         sk=self.sk, cell_class=g.classes.ravel(),
+                         lex_of_compact=g.dofmap.lex_of_compact, cut_cells=g.cut_lex,
+                         cut_K=self.cut_K, device=device)
+        op.problem = self
+        return op
 
     def mass_matrix(self) -> sp.csr_matrix:
-        return sp.diags(self.m_diag).tocsr()
+        """Global mass: diagonal when lumped; with lumping 'none' the cut cells
+        keep their consistent blocks (the IMEX c-set mass)."""
+        if self.lumping != "none":
+            return sp.diags(self.m_diag).tocsr()
+        L = self.cut_M.shape[-1]
+        dofs = self.cut_dofs()
+        rr, cc = np.divmod(np.arange(L * L), L)
+        rows = np.concatenate([np.arange(self.n_dof)] + [d[rr] for d in dofs])
+        cols = np.concatenate([np.arange(self.n_dof)] + [d[cc] for d in dofs])
+        vals = np.concatenate([self.m_diag] + [Mj.ravel() for Mj in self.cut_M])
+        A = sp.coo_matrix((vals, (rows, cols)), shape=(self.n_dof, self.n_dof)).tocsr()
+        A.eliminate_zeros()
+        return A
 
     # -------------------------------------------------------------- CSR --
     def csr_stiffness(self) -> sp.csr_matrix:

@@ -90,7 +90,8 @@ def imex_critical_time_step(K, M, d_idx, tol: float = 1e-9, seed: int = 0,
     if d_idx.shape[0] == 0:
         raise ValueError("explicit subsystem is empty")
     if isinstance(K, DeviceOperator):
-        K_dd = K.restricted(d_idx)
+        from .imex import _host_stiffness
+        K_dd = _restrict(_host_stiffness(K), d_idx)
     else:
         K_dd = _restrict(K, d_idx)
     M_dd = _restrict(M, d_idx)

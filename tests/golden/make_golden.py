@@ -215,3 +215,4 @@ if __name__ == "__main__":
     gen_cube("cube_p2n4", p=2, n_e=4, alpha=1e-6, depth=2, n_t=300, store_csr=True)
     gen_cube("cube_p3n6", p=3, n_e=6, alpha=1e-8, depth=3, n_t=200, store_csr=False)
     gen_cube_imex("cube_imex_p2n4", p=2, n_e=4, alpha=1e-12, depth=2, n_t=150)
+    gen_cube_imex("cube_imex_p2n4_a4", p=2, n_e=4, alpha=1e-4, depth=2, n_t=150)
