@@ -15,7 +15,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_NAME = "libwavecell_b200.so"
-LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+LIB_PATH = Path(__file__).resolve().parent / os.environ.get("WAVECELL_B200_LIB", LIB_NAME)
 
 WCB_OK = 0
 WCB_E_ARG = 1

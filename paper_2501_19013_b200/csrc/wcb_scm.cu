@@ -38,7 +38,16 @@
 namespace wcb {
 
 // element rows per tile; one compute warp each plus one halo warp
-__host__ __device__ constexpr int rpe_for(int P) { return P <= 4 ? 4 : 2; }
+#ifndef WCB2D_RPE
+#define WCB2D_RPE 4
+#endif
+#ifndef WCB2D_MINB
+#define WCB2D_MINB 3
+#endif
+#ifndef WCB2D_EPI_TMA
+#define WCB2D_EPI_TMA 1      // 1: psi_{k-1} and 1/m also staged by TMA
+#endif
+__host__ __device__ constexpr int rpe_for(int P) { return P <= 4 ? WCB2D_RPE : 2; }
 
 // Tile geometry of the 2D kernel: a tile is 32p node columns x RPE*p node rows;
 // only psi_k (with its halo) is staged in shared memory by TMA.
@@ -54,7 +63,10 @@ struct Tile2 {
     static constexpr int UW = ((TJ + P + 1 + CO) + 1) / 2 * 2;  // cols J0-P-CO..J0+TJ, even
     static constexpr int UH = TI + P + 1;                   // u tile rows (I0-P..I0+TI)
     static constexpr size_t U_BYTES = (size_t)UW * UH * 8;
-    static constexpr size_t OFF_CARRY = (U_BYTES + 127) / 128 * 128;   // [RPE+1][P][32]
+    static constexpr size_t E_BYTES = WCB2D_EPI_TMA ? (size_t)TJ * TI * 8 : 0;  // prev / minv tiles
+    static constexpr size_t OFF_PREV = (U_BYTES + 127) / 128 * 128;
+    static constexpr size_t OFF_MINV = OFF_PREV + (E_BYTES + 127) / 128 * 128;
+    static constexpr size_t OFF_CARRY = OFF_MINV + (E_BYTES + 127) / 128 * 128;   // [RPE+1][P][32]
     static constexpr size_t OFF_BAR = OFF_CARRY + (size_t)(RPE + 1) * P * 32 * 8;
     static constexpr size_t SMEM = OFF_BAR + 8;
 };
@@ -178,9 +190,9 @@ __device__ __forceinline__ void cut_cells_warp(const Scm2DGeo& g, const double* 
 // computes element row ex0 + w.  psi_k arrives by one TMA box; psi_{k-1} and
 // 1/m are read straight from global memory in the epilogue.
 template <int P, int MODE>
-__global__ void __launch_bounds__(Tile2<P>::NWARP * 32) k_scm2d(const __grid_constant__ CUtensorMap tm_u,
-                                                               Scm2DGeo g, Mats2<P> mt, double sk,
-                                                               StepArgs a) {
+__global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
+    const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_prev,
+    const __grid_constant__ CUtensorMap tm_minv, Scm2DGeo g, Mats2<P> mt, double sk, StepArgs a) {
     using T = Tile2<P>;
     constexpr int N = P + 1;
     constexpr int RPE = T::RPE;
@@ -196,8 +208,13 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32) k_scm2d(const __grid_con
     const int64_t J0 = strip * T::TJ, I0 = rtile * T::TI;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        mbar_expect_tx(bar, (uint32_t)T::U_BYTES);
+        const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
+        mbar_expect_tx(bar, (uint32_t)(T::U_BYTES + (epi ? 2 * T::E_BYTES : 0)));
         tma_load_2d(smem, &tm_u, (int32_t)(J0 - P - T::CO + PADJ), (int32_t)I0, bar);
+        if (epi) {
+            tma_load_2d(smem + T::OFF_PREV, &tm_prev, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar);
+            tma_load_2d(smem + T::OFF_MINV, &tm_minv, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar);
+        }
     }
     // cell codes (and the epilogue's psi_{k-1}, 1/m) while the tile is in flight
     const bool halo = (w == RPE);
@@ -210,7 +227,7 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32) k_scm2d(const __grid_con
         mL = __ldg(g.mask + (ex + 1) * ms_ + ey);
     }
     const int64_t Jl = J0 + lane * P;
-    if (MODE == MODE_STEP && !halo) {
+    if (MODE == MODE_STEP && !halo && !WCB2D_EPI_TMA) {
         #pragma unroll
         for (int r = 0; r < P; ++r) {
             const int64_t base = (ex * P + r + P) * g.pitch + Jl + PADJ;
@@ -266,10 +283,19 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32) k_scm2d(const __grid_con
                     if (!edge || Jl + j < g.n1) a.out[base + j] = Y[r][j];
             } else {
                 double up[P], mi[P];
-                #pragma unroll
-                for (int j = 0; j < P; ++j) {
-                    up[j] = a.prev[base + j];
-                    mi[j] = __ldg(a.minv + base + j);
+                if constexpr (WCB2D_EPI_TMA != 0) {
+                    const double* ps = reinterpret_cast<const double*>(smem + T::OFF_PREV) +
+                                       (size_t)(w * P + r) * T::TJ + lane * P;
+                    const double* msm = reinterpret_cast<const double*>(smem + T::OFF_MINV) +
+                                        (size_t)(w * P + r) * T::TJ + lane * P;
+                    #pragma unroll
+                    for (int j = 0; j < P; ++j) { up[j] = ps[j]; mi[j] = msm[j]; }
+                } else {
+                    #pragma unroll
+                    for (int j = 0; j < P; ++j) {
+                        up[j] = a.prev[base + j];
+                        mi[j] = __ldg(a.minv + base + j);
+                    }
                 }
                 const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
                 double v[P];
@@ -315,13 +341,14 @@ struct ScmOperator final : Operator {
     void gather(const double* src, double* dst) override { launch_gather(ctx, n, d_sidx.p, src, dst); }
 
     template <int P>
-    const CUtensorMap& state_map(const double* ptr) {
+    const CUtensorMap& state_map(const double* ptr, int kind = 0) {
         using T = Tile2<P>;
-        return maps.get(ptr, 0, [&] {
+        return maps.get(ptr, kind, [&] {
             const uint64_t dims[2] = {(uint64_t)pitch, (uint64_t)rows};
             const uint64_t strides[1] = {(uint64_t)pitch};
-            const uint32_t box[2] = {(uint32_t)T::UW, (uint32_t)T::UH};
-            return make_map_f64(ptr, 2, dims, strides, box);
+            const uint32_t box_u[2] = {(uint32_t)T::UW, (uint32_t)T::UH};
+            const uint32_t box_e[2] = {(uint32_t)T::TJ, (uint32_t)T::TI};
+            return make_map_f64(ptr, 2, dims, strides, kind == 0 ? box_u : box_e);
         });
     }
     template <int P, int MODE>
@@ -342,7 +369,11 @@ struct ScmOperator final : Operator {
                 }
         Scm2DGeo g{n_e, n1, mask.p, cut_id.p, KT.p, cflags.p, n_strips, n_rtiles, pitch};
         dim3 grid((unsigned)n_strips, (unsigned)n_rtiles);
-        k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(state_map<P>(a.cur), g, mt, sk, a);
+        const CUtensorMap& mu = state_map<P>(a.cur);
+        const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
+        const CUtensorMap& mp = epi ? state_map<P>(a.prev, 1) : mu;
+        const CUtensorMap& mm = epi ? state_map<P>(a.minv, 1) : mu;
+        k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(mu, mp, mm, g, mt, sk, a);
         ctx->launches++;
     }
     template <int MODE>
