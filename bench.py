@@ -130,12 +130,46 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+class IgaCfg:
+    """Config 3 (2D IGA-FCM, B-splines p=3, 1024^2 spans, polygon void)."""
+    name = "config3"
+    n_t = 1000
+    safety = 0.9
+    f_e = 10.0
+    seed = 0
+    alpha = 1e-5
+
+
 def build_workload(name: str):
-    from paper_2501_19013_b200.setup.configs import CONFIGS, build_scm
-    cfg = CONFIGS[name]
     t0 = time.perf_counter()
-    prob = build_scm(cfg)
+    if name == "config3":
+        from paper_2501_19013_b200.setup.iga import build_config3
+        cfg = IgaCfg()
+        prob = build_config3(seed=cfg.seed)
+    else:
+        from paper_2501_19013_b200.setup.configs import CONFIGS, build_scm
+        cfg = CONFIGS[name]
+        prob = build_scm(cfg)
     return cfg, prob, time.perf_counter() - t0
+
+
+def host_csr(prob):
+    """The reference-style CSR of the workload (CPU baseline)."""
+    if hasattr(prob, "K"):
+        return prob.K
+    from oracle import cpu
+    return cpu.scm_csr(prob)
+
+
+def step_bytes(prob):
+    """Algorithmic bytes per time step."""
+    n = prob.n_dof
+    if hasattr(prob, "K"):   # CSR path: 12 B/nnz + int64 row pointers + 4 vectors
+        return 12.0 * prob.K.nnz + 8.0 * (n + 1) + 32.0 * n, "k_csr_cdm<32> (CSR SpMV + fused update)"
+    L = (prob.grid.p + 1) ** prob.grid.dim
+    n_cut = int(prob.grid.cut_lex.shape[0])
+    return (32.0 * n + 8.0 * L * (L + 1) / 2 * n_cut,
+            f"k_scm{prob.grid.dim}d<{prob.grid.p},STEP> (one fused launch per time step)")
 
 
 def cpu_sample(prob, dt, target_s=10.0, threads=0):
@@ -143,7 +177,7 @@ def cpu_sample(prob, dt, target_s=10.0, threads=0):
     from oracle import cpu
     from paper_2501_19013_b200.setup.configs import ricker
     from paper_2501_19013_b200.timeint import force_table
-    K = cpu.scm_csr(prob)
+    K = host_csr(prob)
     f = lambda t: ricker(t, 10.0)  # noqa: E731
     probe = 3
     t0 = time.perf_counter()
@@ -167,7 +201,7 @@ def run_reference(args, world, rank):
     dt = cfg.safety * 2.0 / np.sqrt(lam)
     from paper_2501_19013_b200.setup.configs import ricker
     from paper_2501_19013_b200.timeint import force_table
-    K = cpu.scm_csr(prob)
+    K = host_csr(prob)
     f = lambda t: ricker(t, 10.0)  # noqa: E731
     threads = cpu.max_threads()
     probe = 2
@@ -201,21 +235,28 @@ def run_reference(args, world, rank):
 
 def _host_lambda(prob):
     """Critical step for the CPU arm: oracle power iteration on the CSR."""
-    from oracle import cpu, timeint as O
-    K = cpu.scm_csr(prob)
+    from oracle import timeint as O
+    K = host_csr(prob)
     lam, _ = O.max_gen_eig(K, prob.mass_matrix(), tol=1e-7, seed=0)
     return lam
 
 
 def workload_config(cfg, prob):
     g = prob.grid
-    return {"workload": f"{cfg.name}: {g.dim}D acoustic SCM GLL p={g.p}, {g.n_e}^{g.dim} cells, "
-                        f"{len(prob.grid.geom.radii)} circular voids, alpha={cfg.alpha}, "
-                        f"HRZ cut cells, Ricker point source, {cfg.n_t} CDM steps at 0.9 dt_crit",
+    if hasattr(prob, "K"):
+        desc = (f"{cfg.name}: 2D IGA-FCM B-splines p={g.p}, {g.n_e}^2 spans, 12-vertex polygon "
+                f"void, alpha={cfg.alpha}, row-sum lumped, CSR nnz {prob.K.nnz}, Ricker point "
+                f"source, {cfg.n_t} CDM steps at 0.9 dt_crit")
+    else:
+        desc = (f"{cfg.name}: {g.dim}D acoustic SCM GLL p={g.p}, {g.n_e}^{g.dim} cells, "
+                f"{len(prob.grid.geom.radii)} circular voids, alpha={cfg.alpha}, "
+                f"HRZ cut cells, Ricker point source, {cfg.n_t} CDM steps at 0.9 dt_crit")
+    return {"workload": desc,
             "n_dof": int(prob.n_dof), "n_t": int(cfg.n_t), "n_cut": int(g.cut_lex.shape[0]),
             "seed": cfg.seed,
-            "l2": "flushed (256 MiB write) between bench steps; inside one run the 131 MB "
-                  "working set is re-read every time step as the real loop does"}
+            "l2": f"flushed (256 MiB write) between bench steps; inside one run the "
+                  f"{step_bytes(prob)[0] / 1e6:.0f} MB per-step working set is re-read every "
+                  f"time step as the real loop does"}
 
 
 def main():
@@ -319,9 +360,7 @@ def main():
                                        max(np.linalg.norm(psi), 1e-300))
 
     # roofline of the fused step kernel: algorithmic bytes per time step
-    L = (prob.grid.p + 1) ** prob.grid.dim
-    n_cut = int(prob.grid.cut_lex.shape[0])
-    bytes_step = 32.0 * n + 8.0 * L * (L + 1) / 2 * n_cut
+    bytes_step, kname = step_bytes(prob)
     per_step_s = sum(loop_times) / (args.steps * n_t)
     achieved = bytes_step / per_step_s / 1e9
     peak, peak_kind = measured_peaks()
@@ -336,7 +375,7 @@ def main():
                 "setup_s": round(t_build, 2), "power_iteration_s": round(t_eig, 3)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": f"k_scm{prob.grid.dim}d<{prob.grid.p},STEP> (one fused launch per time step)",
+                         "kernel": kname,
                          "bytes_per_launch": bytes_step,
                          "launch_us": per_step_s * 1e6, "peak_kind": peak_kind},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),

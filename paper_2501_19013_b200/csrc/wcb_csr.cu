@@ -22,7 +22,8 @@ __device__ __forceinline__ double row_dot(const int64_t* __restrict__ indptr,
     double s = 0.0;
     if (valid) {
         const int64_t b = indptr[row], e = indptr[row + 1];
-        for (int64_t j = b + lane; j < e; j += TPR) s += __ldg(data + j) * __ldg(x + __ldg(indices + j));
+        #pragma unroll 4
+        for (int64_t j = b + lane; j < e; j += TPR) s = fma(__ldg(data + j), __ldg(x + __ldg(indices + j)), s);
     }
     #pragma unroll
     for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, TPR);
@@ -50,18 +51,70 @@ __global__ void __launch_bounds__(BLOCK) k_csr_cdm(int64_t n, const int64_t* __r
     const int64_t row = (blockIdx.x * (int64_t)BLOCK + threadIdx.x) / TPR;
     const int lane = threadIdx.x % TPR;
     const bool valid = row < n;
+    // epilogue operands first: their latency overlaps the row's dot product
+    double u = 0.0, up = 0.0, mi = 0.0;
+    if (valid && lane == 0) {
+        u = __ldg(a.cur + row);
+        up = a.prev[row];
+        mi = __ldg(a.minv + row);
+    }
     double Ku = row_dot<TPR>(indptr, indices, data, a.cur, row, lane, valid);
     unsigned long long amp = 0ULL;
     if (valid && lane == 0) {
         const double f = a.ft[a.k];
-        const double u = a.cur[row];
-        const double up = a.prev[row];
-        const double mi = a.minv[row];
         const double v = leapfrog(u, up, Ku, mi, f * source_at(a.F, row), a.dt2);
         a.out[row] = v;
         amp = mi != 0.0 ? amp_bits(v) : 0ULL;
     }
     block_amp_max<BLOCK>(amp, a.amp);
+}
+
+// SELL-32: slices of 32 consecutive rows stored column-major (entry k of row
+// r in slice s at sptr[s] + 32 k + r), one row per thread: every load of a
+// warp is one contiguous 256 B (values) / 128 B (indices) segment.  Padding
+// entries point at the row itself with value 0.  Row sums run in stored
+// order (the CSR order), so results equal the CSR-vector kernel's up to
+// summation order and are bitwise reproducible.
+template <bool STEP>
+__global__ void __launch_bounds__(256) k_sell(int64_t n, const int64_t* __restrict__ sptr,
+                                              const int32_t* __restrict__ swid,
+                                              const int32_t* __restrict__ sidx,
+                                              const double* __restrict__ sval,
+                                              const double* __restrict__ x, double* __restrict__ y,
+                                              StepArgs a) {
+    if (STEP && blockIdx.x == 0) record_observers(a);
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool valid = row < n;
+    const int64_t s = row >> 5;
+    const int r = (int)(row & 31);
+    double u = 0.0, up = 0.0, mi = 0.0;
+    if (STEP && valid) {
+        u = __ldg(a.cur + row);
+        up = a.prev[row];
+        mi = __ldg(a.minv + row);
+    }
+    double acc = 0.0;
+    if (valid) {
+        const int w = __ldg(swid + s);
+        const int64_t base = __ldg(sptr + s) + r;
+        #pragma unroll 8
+        for (int k = 0; k < w; ++k) {
+            const int64_t j = base + 32 * (int64_t)k;
+            acc = fma(__ldg(sval + j), __ldg(x + __ldg(sidx + j)), acc);
+        }
+    }
+    if constexpr (STEP) {
+        unsigned long long amp = 0ULL;
+        if (valid) {
+            const double f = a.ft[a.k];
+            const double v = leapfrog(u, up, acc, mi, f * source_at(a.F, row), a.dt2);
+            a.out[row] = v;
+            amp = mi != 0.0 ? amp_bits(v) : 0ULL;
+        }
+        block_amp_max<256>(amp, a.amp);
+    } else {
+        if (valid) y[row] = acc;
+    }
 }
 
 struct CsrOperator final : Operator {
@@ -72,6 +125,10 @@ struct CsrOperator final : Operator {
     std::vector<int64_t> sidx;
     int64_t nnz = 0;
     int tpr = 8;
+    bool sell = false;
+    DevBuf<int64_t> s_ptr;
+    DevBuf<int32_t> s_wid, s_idx;
+    DevBuf<double> s_val;
 
     const char* name() const override { return "csr"; }
     const std::vector<int64_t>& state_index() const override { return sidx; }
@@ -100,6 +157,14 @@ struct CsrOperator final : Operator {
     }
     void apply(const double* x, double* y) override {
         if (!n) return;
+        if (sell) {
+            StepArgs a;
+            k_sell<false><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(n, s_ptr.p, s_wid.p, s_idx.p,
+                                                                               s_val.p, x, y, a);
+            ctx->launches++;
+            WCB_CHECK_LAUNCH();
+            return;
+        }
         switch (tpr) {
             case 1: apply_t<1>(x, y); break;
             case 2: apply_t<2>(x, y); break;
@@ -112,6 +177,13 @@ struct CsrOperator final : Operator {
     }
     void cdm_step(const StepArgs& a) override {
         if (!n) return;
+        if (sell) {
+            k_sell<true><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(n, s_ptr.p, s_wid.p, s_idx.p,
+                                                                              s_val.p, a.cur, nullptr, a);
+            ctx->launches++;
+            WCB_CHECK_LAUNCH();
+            return;
+        }
         switch (tpr) {
             case 1: step_t<1>(a); break;
             case 2: step_t<2>(a); break;
@@ -152,11 +224,45 @@ Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* h_indptr,
     op->data.upload(h_data, nnz, s);
     op->sidx.resize(n);
     std::iota(op->sidx.begin(), op->sidx.end(), (int64_t)0);
+    // ~6 entries per lane: several rows per warp keep independent load chains
+    // in flight (one row per warp is latency-bound at ~50 nnz/row)
     const double mean = n ? (double)nnz / (double)n : 0.0;
     int t = 1;
-    while (t < 32 && t < mean) t <<= 1;
-    // a few lanes idle is cheaper than a serial tail per lane
+    while (t < 32 && t * 6 < mean) t <<= 1;
     op->tpr = std::max(1, std::min(32, t));
+    // SELL-32 copy when padding stays small (regular stencil rows, e.g. IGA)
+    const int64_t n_sl = ceil_div(n, 32);
+    std::vector<int64_t> sp(n_sl + 1, 0);
+    std::vector<int32_t> sw(std::max<int64_t>(n_sl, 1), 0);
+    for (int64_t sl = 0; sl < n_sl; ++sl) {
+        int64_t w = 0;
+        for (int64_t r = sl * 32; r < std::min(n, sl * 32 + 32); ++r)
+            w = std::max(w, h_indptr[r + 1] - h_indptr[r]);
+        sw[sl] = (int32_t)w;
+        sp[sl + 1] = sp[sl] + 32 * w;
+    }
+    if (n >= 32 && sp[n_sl] <= nnz + nnz / 4 && nnz > 0) {
+        std::vector<int32_t> si(sp[n_sl]);
+        std::vector<double> sv(sp[n_sl], 0.0);
+        for (int64_t sl = 0; sl < n_sl; ++sl)
+            for (int64_t r = sl * 32; r < sl * 32 + 32; ++r)
+                for (int64_t k = 0; k < sw[sl]; ++k) {
+                    const int64_t dst = sp[sl] + 32 * k + (r - sl * 32);
+                    const int64_t src = r < n ? h_indptr[r] + k : -1;
+                    if (r < n && src < h_indptr[r + 1]) {
+                        si[dst] = h_indices[src];
+                        sv[dst] = h_data[src];
+                    } else {
+                        si[dst] = (int32_t)std::min<int64_t>(r, n - 1);
+                        sv[dst] = 0.0;
+                    }
+                }
+        op->s_ptr.alloc(sp.size()); op->s_ptr.upload(sp.data(), sp.size(), s);
+        op->s_wid.alloc(sw.size()); op->s_wid.upload(sw.data(), sw.size(), s);
+        op->s_idx.alloc(si.size()); op->s_idx.upload(si.data(), si.size(), s);
+        op->s_val.alloc(sv.size()); op->s_val.upload(sv.data(), sv.size(), s);
+        op->sell = true;
+    }
     WCB_CUDA(cudaStreamSynchronize(s));
     return op;
 }

@@ -167,6 +167,22 @@ def gen_cube_imex(name, p, n_e, alpha, depth, n_t):
          obs=r.obs)
 
 
+def gen_bspline_cube(name, p, n_e, alpha, depth):
+    """Reference IGA-FCM system (B-splines, row-sum lumping) on the rotated cube."""
+    geom = G.ImmersedGeometry.from_angles(0.3, 0.5, (10.0, 10.0, 10.0))
+    grid = A.Grid.build(geom, B.BasisSpec(family="bspline", p=p, n_e=n_e))
+    cache = A.ElementIntegralCache(grid, octree_depth=depth)
+    params = S.StabilizationParams(alpha=alpha, lumping="row_sum")
+    system = A.assemble(grid, params, source=A.benchmark_source(0.3), cache=cache)
+    lam, it = LA.max_gen_eig(system.K, system.M, tol=1e-7, seed=0)
+    dt = T.select_dt(2.0 / np.sqrt(lam))
+    f = lambda t: A.ricker(t, 10.0)         # noqa: E731
+    r = T.cdm_run(system.M, system.K, system.F_s, f, dt, 200)
+    save(name, **csr_parts("K", system.K), M=system.M.diagonal(), F=system.F_s,
+         lex_of_compact=grid.dofmap.lex_of_compact.astype(np.int64), lam=lam, iters=it,
+         dt=dt, psi=r.psi)
+
+
 def gen_basis():
     """1D ingredients of the spectral-cell / B-spline discretisation."""
     out = {}
@@ -216,3 +232,4 @@ if __name__ == "__main__":
     gen_cube("cube_p3n6", p=3, n_e=6, alpha=1e-8, depth=3, n_t=200, store_csr=False)
     gen_cube_imex("cube_imex_p2n4", p=2, n_e=4, alpha=1e-12, depth=2, n_t=150)
     gen_cube_imex("cube_imex_p2n4_a4", p=2, n_e=4, alpha=1e-4, depth=2, n_t=150)
+    gen_bspline_cube("bspline_cube_p2n5", p=2, n_e=5, alpha=1e-6, depth=2)
