@@ -296,8 +296,21 @@ def main():
     n_t = cfg.n_t if args.nt is None else int(args.nt)
     f = lambda t: ricker(t, cfg.f_e)  # noqa: E731
     ft = force_table(f, dt, n_t)
-    plan = CdmPlan(M, op, prob.F_s, obs_mat=prob.obs_mat, device=local)
-    n = prob.n_dof
+    n_global = prob.n_dof
+    slab_mode = world > 1 and not hasattr(prob, "K")
+    if slab_mode:
+        # strong scaling of the same grid: x slabs, NCCL halo exchange per step
+        from paper_2501_19013_b200 import dist as wdist
+        import scipy.sparse as sp
+        wdist.init_nccl(ctx, rank, world)
+        lo, hi = wdist.partition(prob, world)[rank]
+        slab = wdist.SlabScm(prob, lo, hi)
+        op_run = slab.device_operator(device=local)
+        M_run, F_run, obs_run = sp.diags(slab.m).tocsr(), slab.F, slab.obs
+    else:
+        op_run, M_run, F_run, obs_run = op, M, prob.F_s, prob.obs_mat
+    plan = CdmPlan(M_run, op_run, F_run, obs_mat=obs_run, device=local)
+    n = op_run.n
     dev = torch.device("cuda", local)
     d_ft = torch.from_numpy(ft).to(dev)
     d_psi = torch.empty(n, dtype=torch.float64, device=dev)
@@ -337,7 +350,8 @@ def main():
     barrier(world)
     launches = ctx.launches - launches0
     total = reduce_max(sum(times), world)
-    value = n * n_t * args.steps * world / total
+    # whole-job DOF-updates/s: replicas add up, slabs share one grid
+    value = (n_global if slab_mode else n * world) * n_t * args.steps / total
     psi = d_psi.cpu().numpy()
     assert np.all(np.isfinite(psi)), "non-finite field"
 
@@ -347,30 +361,35 @@ def main():
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
-        r = cdm_run(M, op, prob.F_s, f, dt, n_t, obs_mat=prob.obs_mat, device=local)
+        r = cdm_run(M_run, op_run, F_run, f, dt, n_t, obs_mat=obs_run, device=local)
         e2e_times.append(time.perf_counter() - t0)
     if e2e_times:
         e2e_t = reduce_max(sum(e2e_times) / len(e2e_times), world)
-        e2e_value = n * n_t * world / e2e_t
+        e2e_value = (n_global if slab_mode else n * world) * n_t / e2e_t
     else:
         e2e_value, r = None, None
-    h2d = 8 * (2 * n + max(n_t, 1)) + prob.obs_mat.nnz * 24 + 8 * (plan.n_obs + 1)
+    h2d = 8 * (2 * n + max(n_t, 1)) + (obs_run.nnz if obs_run is not None else 0) * 24 + \
+        8 * (plan.n_obs + 1)
     d2h = 8 * n + 8 * plan.n_obs * (n_t + 1)
     rel = None if r is None else float(np.linalg.norm(r.psi - psi) /
                                        max(np.linalg.norm(psi), 1e-300))
 
     # roofline of the fused step kernel: algorithmic bytes per time step
     bytes_step, kname = step_bytes(prob)
+    if slab_mode:   # this rank's slab (local DOFs and cut cells)
+        L = (prob.grid.p + 1) ** prob.grid.dim
+        bytes_step = 32.0 * n + 8.0 * L * (L + 1) / 2 * len(slab.cut_cells)
     per_step_s = sum(loop_times) / (args.steps * n_t)
     achieved = bytes_step / per_step_s / 1e9
     peak, peak_kind = measured_peaks()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if slab_mode else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded voids and source, BASELINE config shapes)",
             "config": workload_config(cfg, prob) | {
-                "parallelism": f"{world} independent replica(s), one per GPU",
+                "parallelism": (f"{world} x slabs of one grid, NCCL halo exchange per step"
+                                if slab_mode else f"{world} independent replica(s), one per GPU"),
                 "dt": dt, "lambda_max": lam, "power_iterations": iters,
                 "setup_s": round(t_build, 2), "power_iteration_s": round(t_eig, 3)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

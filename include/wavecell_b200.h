@@ -86,6 +86,14 @@ typedef struct {
     int64_t n_cut;               /* number of cut cells                                 */
     const int64_t* cut_cells;    /* n_cut cell lex ids, ascending                       */
     const double* cut_K;         /* n_cut * L * L physical element stiffness, L=(p+1)^dim */
+    /* x slab (multi-GPU); x_cell_hi = 0 means the whole grid.  A
+     * slab owns cell rows [x_cell_lo, x_cell_hi) and node rows
+     * [x_cell_lo*p, x_cell_hi*p) (+ row n_e*p if x_owns_last).  cell_class then
+     * covers the existing cell rows of [x_cell_lo-1, x_cell_hi), lex_of_compact
+     * the owned DOFs (global lex), cut_cells the cut cells of those rows. */
+    int64_t x_cell_lo;
+    int64_t x_cell_hi;
+    int32_t x_owns_last;
 } wcb_scm_desc;
 
 /* ---- library / context ------------------------------------------------- */
@@ -108,6 +116,26 @@ int wcb_operator_destroy(wcb_operator* op);
 int64_t wcb_operator_n(const wcb_operator* op);
 /* y = K @ x on host buffers (K.__matmul__, src/timeint.py:175,182). */
 int wcb_operator_apply(wcb_operator* op, const double* x, double* y);
+/* Halo layout of a slab operator (state rows of xstride doubles):
+ * out[0] xstride, out[1] top halo first row, out[2] top halo rows (p or 0),
+ * out[3] bottom halo row, out[4] bottom halo rows (1 or 0), out[5] first row
+ * sent to the next slab, out[6] rows sent (p or 0), out[7] row sent to the
+ * previous slab (1 row).  Returns 1 for a slab of a larger grid, else 0. */
+int wcb_operator_halo(const wcb_operator* op, int64_t* out8);
+
+/* ---- multi-GPU slabs: NCCL communicator per context -------- */
+/* Halo exchange with the +-1 slab neighbours after every step and all-reduces
+ * of the divergence amplitude / observer partial sums run on the context's
+ * stream.  NCCL is loaded with dlopen("libnccl.so.2"). */
+int wcb_dist_unique_id(char* out128);
+int wcb_dist_init(wcb_context* ctx, int rank, int world, const char* id128);
+int wcb_dist_finalize(wcb_context* ctx);
+/* Single-process emulation of a slab group (all plans on one context): the
+ * same kernels and halo layout, exchanges done by device copies.  Outputs are
+ * per plan (owned DOFs); obs_out receives the sum of the partial observers. */
+int wcb_cdm_group_run(int n_plans, wcb_cdm_plan** plans, const double* ft, double dt,
+                      int64_t n_t, double** psi_out, double* obs_out,
+                      wcb_divergence* div, wcb_timings* tm);
 
 /* ---- critical time step: max_gen_eig, src/linalg.py:89-122 --------------- */
 /* Power iteration on M^-1 K with diagonal M; x0 is the normalised seeded start

@@ -29,10 +29,11 @@ EXPORTS = (
     "wcb_abi_version", "wcb_last_error", "wcb_device_count",
     "wcb_context_create", "wcb_context_destroy", "wcb_context_stream",
     "wcb_context_launches", "wcb_operator_csr_create", "wcb_operator_scm_create",
-    "wcb_operator_destroy", "wcb_operator_n", "wcb_operator_apply",
+    "wcb_operator_destroy", "wcb_operator_n", "wcb_operator_apply", "wcb_operator_halo",
     "wcb_max_gen_eig", "wcb_cdm_plan_create", "wcb_cdm_plan_destroy",
     "wcb_cdm_plan_run", "wcb_cdm_plan_run_device", "wcb_imex_plan_create",
-    "wcb_imex_plan_destroy", "wcb_imex_plan_run",
+    "wcb_imex_plan_destroy", "wcb_imex_plan_run", "wcb_dist_unique_id", "wcb_dist_init",
+    "wcb_dist_finalize", "wcb_cdm_group_run",
 )
 
 _p = C.c_void_p
@@ -61,7 +62,8 @@ class ScmDesc(C.Structure):
     _fields_ = [("dim", _i32), ("p", _i32), ("n_e", _i64 * 3), ("k1", _dp), ("m1", _dp),
                 ("sk", _d), ("cell_class", _i8p), ("n_dof", _i64),
                 ("lex_of_compact", _i64p), ("n_cut", _i64), ("cut_cells", _i64p),
-                ("cut_K", _dp)]
+                ("cut_K", _dp), ("x_cell_lo", _i64), ("x_cell_hi", _i64),
+                ("x_owns_last", _i32)]
 
 
 class LU(C.Structure):
@@ -83,6 +85,7 @@ _SIGS = {
     "wcb_operator_destroy": (C.c_int, [_p]),
     "wcb_operator_n": (_i64, [_p]),
     "wcb_operator_apply": (C.c_int, [_p, _dp, _dp]),
+    "wcb_operator_halo": (C.c_int, [_p, _i64p]),
     "wcb_max_gen_eig": (C.c_int, [_p, _dp, _dp, _d, _i64, _dp, _i64p]),
     "wcb_cdm_plan_create": (C.c_int, [_p, _dp, _dp, C.POINTER(Observer), C.POINTER(_p)]),
     "wcb_cdm_plan_destroy": (C.c_int, [_p]),
@@ -94,6 +97,11 @@ _SIGS = {
                                        C.POINTER(LU), _dp, C.POINTER(Observer),
                                        C.POINTER(_p)]),
     "wcb_imex_plan_destroy": (C.c_int, [_p]),
+    "wcb_dist_unique_id": (C.c_int, [C.c_char_p]),
+    "wcb_dist_init": (C.c_int, [_p, C.c_int, C.c_int, C.c_char_p]),
+    "wcb_dist_finalize": (C.c_int, [_p]),
+    "wcb_cdm_group_run": (C.c_int, [C.c_int, C.POINTER(_p), _dp, _d, _i64, C.POINTER(_dp), _dp,
+                                    C.POINTER(Divergence), C.POINTER(Timings)]),
     "wcb_imex_plan_run": (C.c_int, [_p, _d, _dp, _dp, _d, _i64, _d, _d, _dp, _dp, _dp,
                                     _dp, _dp, C.POINTER(Divergence), C.POINTER(Timings)]),
 }

@@ -408,68 +408,106 @@ struct wcb_cdm_plan {
 
 namespace wcb {
 
-static void run_cdm_device(wcb_cdm_plan* P, const double* d_ft, double dt, int64_t n_t,
-                           const double* d_psi0, const double* d_v0, double* d_psi_out,
-                           double* d_obs_out, wcb_divergence* div, wcb_timings* tm) {
-    Operator* op = P->op;
-    Context* ctx = op->ctx;
+// Halo exchange of state buffers cur[r] between consecutive slabs: device
+// copies for an emulated group (one context), NCCL for one plan per process.
+static void exchange_halos(std::vector<wcb_cdm_plan*>& Ps, std::vector<double*>& cur) {
+    const size_t n = Ps.size();
+    if (n == 1) {
+        int64_t h[8];
+        Context* ctx = Ps[0]->op->ctx;
+        if (ctx->nccl && Ps[0]->op->halo(h)) nccl_exchange_halo(ctx, cur[0], h);
+        return;
+    }
+    cudaStream_t s = Ps[0]->op->ctx->stream;
+    for (size_t r = 0; r + 1 < n; ++r) {
+        int64_t a[8], b[8];
+        Ps[r]->op->halo(a);
+        Ps[r + 1]->op->halo(b);
+        WCB_REQUIRE(a[0] == b[0] && a[6] == b[2] && b[2] > 0 && a[4] == 1,
+                    "plans are not consecutive slabs of one grid");
+        const size_t xs = (size_t)a[0];
+        WCB_CUDA(cudaMemcpyAsync(cur[r + 1] + b[1] * xs, cur[r] + a[5] * xs, a[6] * xs * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, s));
+        WCB_CUDA(cudaMemcpyAsync(cur[r] + a[3] * xs, cur[r + 1] + b[7] * xs, xs * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+// The CDM loop of src/timeint.py:159-193 for one plan or a group of slab
+// plans sharing one context (emulated ranks) or one plan per process with an
+// NCCL communicator on its context.
+static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, double dt, int64_t n_t,
+                          const std::vector<const double*>& d_psi0, const std::vector<const double*>& d_v0,
+                          const std::vector<double*>& d_psi_out, const std::vector<double*>& d_obs_out,
+                          wcb_divergence* div, wcb_timings* tm) {
+    const size_t G = Ps.size();
+    Context* ctx = Ps[0]->op->ctx;
+    for (auto* P : Ps) WCB_REQUIRE(P->op->ctx == ctx, "group plans must share one context");
     cudaStream_t s = ctx->stream;
-    const int64_t n = op->n, ns = op->n_state;
     if (div) { div->step = -1; div->amplitude = 0.0; }
     if (tm) { tm->factorization = 0.0; tm->rhs = 0.0; tm->backward_insertion = 0.0; }
-    if (P->A.n != (size_t)ns) {
-        P->A.alloc(ns); P->B.alloc(ns); P->V.alloc(ns); P->T.alloc(ns);
-        P->A.zero(s); P->B.zero(s); P->V.zero(s); P->T.zero(s);
-    }
-    if (P->amp.n < (size_t)(n_t + 1)) P->amp.alloc(n_t + 1);
-    P->amp.zero(s);
-    // initial state: zeros unless given (src/timeint.py:162-163)
-    P->A.zero(s);
-    P->V.zero(s);
-    if (d_psi0) op->scatter(d_psi0, P->A.p);
-    if (d_v0) op->scatter(d_v0, P->V.p);
-    const int g = grid_for(ctx, ns);
-    // bootstrap a0, psi_{-1}
-    op->apply(P->A.p, P->T.p);
-    k_cdm_bootstrap<<<g, 256, 0, s>>>(ns, P->A.p, P->V.p, P->T.p, P->m_state.p, P->src, d_ft, dt,
-                                      P->B.p);
-    ctx->launches++;
-    WCB_CHECK_LAUNCH();
     const int64_t stride = n_t + 1;
-    auto record = [&](int64_t k, const double* psi) {
-        if (P->n_obs && d_obs_out) {
-            k_obs_record<<<(int)ceil_div(P->n_obs, 64), 64, 0, s>>>(
-                P->n_obs, P->obs_indptr.p, P->obs_idx.p, P->obs_val.p, psi, d_obs_out, stride, k);
-            ctx->launches++;
+    std::vector<double*> cur(G), prev(G);
+    for (size_t r = 0; r < G; ++r) {
+        wcb_cdm_plan* P = Ps[r];
+        Operator* op = P->op;
+        const int64_t ns = op->n_state;
+        if (P->A.n != (size_t)ns) {
+            P->A.alloc(ns); P->B.alloc(ns); P->V.alloc(ns); P->T.alloc(ns);
+            P->B.zero(s); P->T.zero(s);
         }
-    };
-    StepArgs a;
-    a.minv = P->minv.p;
-    a.F = P->src;
-    a.ft = d_ft;
-    a.dt2 = dt * dt;
-    if (P->n_obs && d_obs_out) {
-        a.n_obs = P->n_obs;
-        a.obs_ptr = P->obs_indptr.p;
-        a.obs_idx = P->obs_idx.p;
-        a.obs_val = P->obs_val.p;
-        a.obs_out = d_obs_out;
-        a.obs_stride = stride;
+        if (P->amp.n < (size_t)(n_t + 1)) P->amp.alloc(n_t + 1);
+        P->amp.zero(s);
+        // initial state: zeros unless given (src/timeint.py:162-163)
+        P->A.zero(s);
+        P->V.zero(s);
+        if (d_psi0[r]) op->scatter(d_psi0[r], P->A.p);
+        if (d_v0[r]) op->scatter(d_v0[r], P->V.p);
+        cur[r] = P->A.p;
+        prev[r] = P->B.p;
     }
-    double* cur = P->A.p;
-    double* prev = P->B.p;
-    P->h_amp.assign(n_t + 1, 0ULL);
+    exchange_halos(Ps, cur);   // psi_0 halos for the bootstrap apply
+    std::vector<StepArgs> args(G);
+    for (size_t r = 0; r < G; ++r) {
+        wcb_cdm_plan* P = Ps[r];
+        Operator* op = P->op;
+        const int64_t ns = op->n_state;
+        // bootstrap a0, psi_{-1} (src/timeint.py:175-176)
+        op->apply(P->A.p, P->T.p);
+        k_cdm_bootstrap<<<grid_for(ctx, ns), 256, 0, s>>>(ns, P->A.p, P->V.p, P->T.p, P->m_state.p, P->src,
+                                                          d_ft, dt, P->B.p);
+        ctx->launches++;
+        StepArgs& a = args[r];
+        a.minv = P->minv.p;
+        a.F = P->src;
+        a.ft = d_ft;
+        a.dt2 = dt * dt;
+        if (P->n_obs && d_obs_out[r]) {
+            a.n_obs = P->n_obs;
+            a.obs_ptr = P->obs_indptr.p;
+            a.obs_idx = P->obs_idx.p;
+            a.obs_val = P->obs_val.p;
+            a.obs_out = d_obs_out[r];
+            a.obs_stride = stride;
+        }
+    }
+    WCB_CHECK_LAUNCH();
+    std::vector<unsigned long long> h_amp(G * (n_t + 1), 0ULL);
     const int64_t check_every = 256;
-    int64_t checked = 0;  // amp[1..checked] inspected
+    int64_t checked = 0;   // amp[1..checked] inspected
     auto inspect = [&](int64_t upto) -> bool {
         if (upto <= checked) return false;
-        WCB_CUDA(cudaMemcpyAsync(P->h_amp.data() + checked + 1, P->amp.p + checked + 1,
-                                 (upto - checked) * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
+        const int64_t cnt = upto - checked;
+        for (size_t r = 0; r < G; ++r) {
+            nccl_allreduce_max_u64(ctx, Ps[r]->amp.p + checked + 1, cnt);
+            WCB_CUDA(cudaMemcpyAsync(h_amp.data() + r * (n_t + 1) + checked + 1, Ps[r]->amp.p + checked + 1,
+                                     cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        }
         WCB_CUDA(cudaStreamSynchronize(s));
         for (int64_t k = checked + 1; k <= upto; ++k) {
+            unsigned long long b = 0ULL;
+            for (size_t r = 0; r < G; ++r) b = std::max(b, h_amp[r * (n_t + 1) + k]);
             double v;
-            unsigned long long b = P->h_amp[k];
             std::memcpy(&v, &b, sizeof(v));
             if (!std::isfinite(v) || v > 1.0e12) {
                 if (div) { div->step = k; div->amplitude = v; }
@@ -482,19 +520,30 @@ static void run_cdm_device(wcb_cdm_plan* P, const double* d_ft, double dt, int64
     WCB_CUDA(cudaEventRecord(ctx->ev0, s));
     bool diverged = false;
     for (int64_t k = 0; k < n_t; ++k) {
-        a.cur = cur;
-        a.prev = prev;
-        a.out = prev;  // psi_{k+1} overwrites psi_{k-1} in place
-        a.k = k;
-        a.amp = P->amp.p + (k + 1);
-        op->cdm_step(a);   // also records obs[:, k] from psi_k
-        std::swap(cur, prev);
+        for (size_t r = 0; r < G; ++r) {
+            StepArgs& a = args[r];
+            a.cur = cur[r];
+            a.prev = prev[r];
+            a.out = prev[r];   // psi_{k+1} overwrites psi_{k-1} in place
+            a.k = k;
+            a.amp = Ps[r]->amp.p + (k + 1);
+            Ps[r]->op->cdm_step(a);   // also records obs[:, k] from psi_k
+            std::swap(cur[r], prev[r]);
+        }
+        exchange_halos(Ps, cur);
         if ((k + 1) % check_every == 0) {
             WCB_CHECK_LAUNCH();
             if (inspect(k + 1)) { diverged = true; break; }
         }
     }
-    if (!diverged) record(n_t, cur);
+    if (!diverged)
+        for (size_t r = 0; r < G; ++r)
+            if (Ps[r]->n_obs && d_obs_out[r]) {
+                StepArgs a = args[r];
+                a.cur = cur[r];
+                a.k = n_t;
+                launch_record_observers(ctx, a);
+            }
     WCB_CUDA(cudaEventRecord(ctx->ev1, s));
     WCB_CHECK_LAUNCH();
     if (!diverged) diverged = inspect(n_t);
@@ -505,9 +554,18 @@ static void run_cdm_device(wcb_cdm_plan* P, const double* d_ft, double dt, int64
     // reported under "rhs" (src/timeint.py:181-188 splits them in two).
     if (tm) tm->rhs = ms * 1e-3;
     if (diverged) throw Error{WCB_E_DIVERGED, "solution diverged"};
-    op->gather(cur, d_psi_out);
+    for (size_t r = 0; r < G; ++r) {
+        if (Ps[r]->n_obs && d_obs_out[r]) nccl_allreduce_sum_f64(ctx, d_obs_out[r], Ps[r]->n_obs * stride);
+        Ps[r]->op->gather(cur[r], d_psi_out[r]);
+    }
     WCB_CUDA(cudaStreamSynchronize(s));
-    (void)n;
+}
+
+static void run_cdm_device(wcb_cdm_plan* P, const double* d_ft, double dt, int64_t n_t,
+                           const double* d_psi0, const double* d_v0, double* d_psi_out,
+                           double* d_obs_out, wcb_divergence* div, wcb_timings* tm) {
+    std::vector<wcb_cdm_plan*> Ps{P};
+    run_cdm_group(Ps, d_ft, dt, n_t, {d_psi0}, {d_v0}, {d_psi_out}, {d_obs_out}, div, tm);
 }
 
 }  // namespace wcb
@@ -638,6 +696,56 @@ int wcb_cdm_plan_run(wcb_cdm_plan* P, const double* ft, double dt, int64_t n_t,
         WCB_CUDA(cudaStreamSynchronize(s));
         return WCB_OK;
     });
+}
+
+int wcb_cdm_group_run(int n_plans, wcb_cdm_plan** plans, const double* ft, double dt,
+                      int64_t n_t, double** psi_out, double* obs_out, wcb_divergence* div,
+                      wcb_timings* tm) {
+    return guarded([&] {
+        WCB_REQUIRE(n_plans >= 1 && plans && psi_out && ft, "NULL argument");
+        std::vector<wcb_cdm_plan*> Ps(plans, plans + n_plans);
+        Context* ctx = Ps[0]->op->ctx;
+        WCB_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        DevBuf<double> dft(std::max<int64_t>(n_t, 1));
+        dft.upload(ft, std::max<int64_t>(n_t, 1), s);
+        std::vector<DevBuf<double>> outs(n_plans), obs(n_plans);
+        std::vector<double*> pout(n_plans), pobs(n_plans, nullptr);
+        const int64_t n_obs = Ps[0]->n_obs;
+        for (int r = 0; r < n_plans; ++r) {
+            WCB_REQUIRE(Ps[r]->n_obs == n_obs, "plans must share the observer count");
+            outs[r].alloc(std::max<int64_t>(Ps[r]->op->n, 1));
+            pout[r] = outs[r].p;
+            if (obs_out && n_obs) {
+                obs[r].alloc(n_obs * (n_t + 1));
+                pobs[r] = obs[r].p;
+            }
+        }
+        std::vector<const double*> none(n_plans, nullptr);
+        run_cdm_group(Ps, dft.p, dt, n_t, none, none, pout, pobs, div, tm);
+        for (int r = 0; r < n_plans; ++r)
+            if (Ps[r]->op->n)
+                WCB_CUDA(cudaMemcpyAsync(psi_out[r], pout[r], Ps[r]->op->n * sizeof(double),
+                                         cudaMemcpyDeviceToHost, s));
+        if (obs_out && n_obs) {
+            // sum of the per-slab partial observers, in slab order
+            std::vector<double> acc(n_obs * (n_t + 1), 0.0), part(n_obs * (n_t + 1));
+            for (int r = 0; r < n_plans; ++r) {
+                WCB_CUDA(cudaMemcpyAsync(part.data(), pobs[r], part.size() * sizeof(double),
+                                         cudaMemcpyDeviceToHost, s));
+                WCB_CUDA(cudaStreamSynchronize(s));
+                for (size_t i = 0; i < acc.size(); ++i) acc[i] += part[i];
+            }
+            std::memcpy(obs_out, acc.data(), acc.size() * sizeof(double));
+        }
+        WCB_CUDA(cudaStreamSynchronize(s));
+        return WCB_OK;
+    });
+}
+
+int wcb_operator_halo(const wcb_operator* op, int64_t* out8) {
+    if (!op || !out8) return WCB_E_ARG;
+    return op->op->halo(out8) ? 1 : 0;
 }
 
 }  // extern "C"

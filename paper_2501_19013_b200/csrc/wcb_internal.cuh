@@ -68,7 +68,9 @@ struct DevBuf {
 };
 
 // ---------------------------------------------------------------- context ----
+struct Nccl;
 struct Context {
+    Nccl* nccl = nullptr;   // slab decomposition communicator (wcb_dist_init)
     int device = 0;
     int sm_count = 148;
     cudaStream_t stream = nullptr;
@@ -210,7 +212,20 @@ struct Operator {
     virtual void cdm_step(const StepArgs& a) = 0;
     // algorithmic bytes of one fused step (for the roofline)
     virtual double step_bytes() const = 0;
+    // slab halo layout (state rows of out[0] doubles), see wcb_operator_halo;
+    // false when the operator is not a slab of a larger grid
+    virtual bool halo(int64_t* out8) const {
+        for (int i = 0; i < 8; ++i) out8[i] = 0;
+        return false;
+    }
 };
+
+// NCCL (loaded with dlopen on first use; the library does not link it)
+struct Nccl;
+Nccl* nccl_for(Context* ctx);   // null unless wcb_dist_init was called on ctx
+void nccl_exchange_halo(Context* ctx, double* state, const int64_t* h);  // +-1 neighbours
+void nccl_allreduce_max_u64(Context* ctx, unsigned long long* d, int64_t n);
+void nccl_allreduce_sum_f64(Context* ctx, double* d, int64_t n);
 
 Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* indptr,
                             const int32_t* indices, const double* data);

@@ -71,12 +71,18 @@ struct Tile2 {
     static constexpr size_t SMEM = OFF_BAR + 8;
 };
 
+// Local geometry of a 2D operator.  x (axis 0) may be a slab of the global
+// grid: local cell row 0 is the (possibly phantom) cell row above the first
+// owned one, so every tile can recompute the row above it; owned node rows
+// are [row_lo, row_hi) in local numbering.
 struct Scm2DGeo {
-    int64_t n_e;              // cells per axis
-    int64_t n1;               // nodes per axis
-    const uint8_t* mask;      // (n_e+2)^2 cell codes, one ring of 0 around: 0 out, 1 uncut, 2 cut
-    const int32_t* cut_id;    // n_e^2 -> cut index or -1
-    const double* KT;         // n_cut * L * L, transposed physical cut stiffness
+    int64_t n_ex;             // local cell rows (incl. the halo row 0)
+    int64_t n_ey;             // cells along y (global)
+    int64_t n1y;              // nodes along y
+    int64_t row_lo, row_hi;   // owned local node rows
+    const uint8_t* mask;      // (n_ex+2) x (n_ey+2) cell codes with a zero ring
+    const int32_t* cut_id;    // n_ex x n_ey -> cut index or -1
+    const double* KT;         // n_cut * L * L, transposed physical cut stiffness / sk
     const uint8_t* cflags;    // per tile (strip-major): 1 = owns a DOF
     int64_t n_strips;
     int64_t n_rtiles;
@@ -154,7 +160,7 @@ __device__ __forceinline__ void cut_cells_warp(const Scm2DGeo& g, const double* 
     if (!edge) cut_lanes &= cut_lanes - 1;
     while (src >= -1) {
         const int64_t ecol = ey0 + src;
-        const int32_t id = __ldg(g.cut_id + ex * g.n_e + ecol);
+        const int32_t id = __ldg(g.cut_id + ex * g.n_ey + ecol);
         const double* KT = g.KT + (int64_t)id * L * L;
         const double* corner = rows + CO + P + src * P;
         constexpr int RR = (L + 31) / 32;   // output rows per lane
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
     const int64_t strip = blockIdx.x, rtile = blockIdx.y;
     if (MODE == MODE_STEP && blockIdx.x == 0 && blockIdx.y == 0) record_observers(a);
     if (!g.cflags[strip * g.n_rtiles + rtile]) return;   // tile without DOFs
-    const int64_t J0 = strip * T::TJ, I0 = rtile * T::TI;
+    const int64_t J0 = strip * T::TJ, I0 = g.row_lo + rtile * T::TI;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
@@ -221,8 +227,8 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
     const int64_t ex = halo ? I0 / P - 1 : I0 / P + w;
     const int64_t ey = J0 / P + lane;
     uint8_t mR = 0, mL = 0;
-    if (ex >= 0 && ex < g.n_e && ey <= g.n_e) {
-        const int64_t ms_ = g.n_e + 2;
+    if (ex >= 0 && ex < g.n_ex && ey <= g.n_ey) {
+        const int64_t ms_ = g.n_ey + 2;
         mR = __ldg(g.mask + (ex + 1) * ms_ + (ey + 1));
         mL = __ldg(g.mask + (ex + 1) * ms_ + ey);
     }
@@ -270,17 +276,17 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
             #pragma unroll
             for (int j = 0; j < P; ++j) Y[r][j] *= sk;
         const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
-        const bool edge = (J0 + T::TJ > g.n1);
+        const bool edge = (J0 + T::TJ > g.n1y);
         #pragma unroll
         for (int r = 0; r < P; ++r) {
             const int64_t I = ex * P + r;
-            if (I >= g.n1) break;
+            if (I >= g.row_hi) break;
             const int64_t base = (I + P) * g.pitch + Jl + PADJ;
             const double* urow = us + (size_t)(rbase + r + P) * T::UW + T::CO + P + lane * P;
             if constexpr (MODE == MODE_APPLY) {
                 #pragma unroll
                 for (int j = 0; j < P; ++j)
-                    if (!edge || Jl + j < g.n1) a.out[base + j] = Y[r][j];
+                    if (!edge || Jl + j < g.n1y) a.out[base + j] = Y[r][j];
             } else {
                 double up[P], mi[P];
                 if constexpr (WCB2D_EPI_TMA != 0) {
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
                 }
                 #pragma unroll
                 for (int j = 0; j < P; ++j) {
-                    if (!edge || Jl + j < g.n1) {
+                    if (!edge || Jl + j < g.n1y) {
                         a.out[base + j] = v[j];
                         unsigned long long b = mi[j] != 0.0 ? amp_bits(v[j]) : 0ULL;
                         amp = b > amp ? b : amp;
@@ -322,6 +328,10 @@ struct ScmOperator final : Operator {
     int dim = 2, p = 4;
     int64_t n_e = 0, n1 = 0, pitch = 0, rows = 0;
     int64_t pplane = 0, n_zs = 0, n_xt = 0;   // 3D
+    // x slab (local numbering): cell rows 0..n_ex-1 (0 = halo row above),
+    // node rows 0..n1x-1, owned node rows [row_lo, row_hi)
+    int64_t n_ex = 0, n1x = 0, row_lo = 0, row_hi = 0, xstride = 0;
+    bool has_top = false, owns_last = true;
     std::vector<int64_t> sidx;
     DevBuf<int64_t> d_sidx;
     DevBuf<uint8_t> mask, cflags;
@@ -367,7 +377,7 @@ struct ScmOperator final : Operator {
                     mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
-        Scm2DGeo g{n_e, n1, mask.p, cut_id.p, KT.p, cflags.p, n_strips, n_rtiles, pitch};
+        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, n_strips, n_rtiles, pitch};
         dim3 grid((unsigned)n_strips, (unsigned)n_rtiles);
         const CUtensorMap& mu = state_map<P>(a.cur);
         const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
@@ -392,7 +402,7 @@ struct ScmOperator final : Operator {
     const CUtensorMap& state_map3(const double* ptr) {
         using T = Tile3<P>;
         return maps.get(ptr, 3, [&] {
-            const uint64_t dims[3] = {(uint64_t)pitch, (uint64_t)rows, (uint64_t)rows};
+            const uint64_t dims[3] = {(uint64_t)pitch, (uint64_t)rows, (uint64_t)(n1x + 2 * p)};
             const uint64_t strides[2] = {(uint64_t)pitch, (uint64_t)pplane};
             const uint32_t box[3] = {(uint32_t)T::UW, (uint32_t)T::UR, (uint32_t)T::UP};
             return make_map_f64(ptr, 3, dims, strides, box);
@@ -407,7 +417,7 @@ struct ScmOperator final : Operator {
                     mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
-        Scm3DGeo g{n_e, n1, pitch, pplane, mask.p, cut_id.p, KT.p, cflags.p, n_zs, n_xt};
+        Scm3DGeo g{n_ex, row_lo, row_hi, n_e, n1, pitch, pplane, mask.p, cut_id.p, KT.p, cflags.p, n_zs, n_xt};
         launch_scm3d<P, MODE>(ctx, state_map3<P>(a.cur), g, mt, sk, a);
     }
     template <int MODE>
@@ -432,84 +442,155 @@ struct ScmOperator final : Operator {
         WCB_CHECK_LAUNCH();
     }
     double step_bytes() const override { return bytes_step; }
+    bool halo(int64_t* h) const override {
+        // state row = local node row + p
+        h[0] = xstride;
+        h[1] = has_top ? p : 0;                 // top halo: local rows 0..p-1
+        h[2] = has_top ? p : 0;
+        h[3] = owns_last ? 0 : row_hi + p;      // bottom halo: local row row_hi
+        h[4] = owns_last ? 0 : 1;
+        h[5] = row_hi;                          // last p owned rows (state rows) -> next slab
+        h[6] = owns_last ? 0 : p;
+        h[7] = row_lo + p;                      // first owned row -> previous slab's bottom halo
+        return has_top || !owns_last;
+    }
 };
 
-static Operator* make_scm3d(Context* ctx, const wcb_scm_desc* d);
-
+// Both dimensions: slab preprocessing (cell rows [x_cell_lo-1, x_cell_hi) of
+// the global grid along x, one halo cell row above), state layout, tile flags,
+// cut-cell tables.
 Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
     WCB_REQUIRE(d->dim == 2 || d->dim == 3, "dim must be 2 or 3");
-    if (d->dim == 3) return make_scm3d(ctx, d);
+    const int dim = d->dim;
     const int p = d->p;
-    WCB_REQUIRE(p >= 1 && p <= 6, "p must be in 1..6 for the 2D kernel");
-    WCB_REQUIRE(d->n_e[0] == d->n_e[1] && d->n_e[0] >= 1, "square grids only (n_e[0] == n_e[1])");
+    if (dim == 2) WCB_REQUIRE(p >= 1 && p <= 6, "p must be in 1..6 for the 2D kernel");
+    else WCB_REQUIRE(p >= 1 && p <= 4, "p must be in 1..4 for the 3D kernel");
+    for (int k = 1; k < dim; ++k)
+        WCB_REQUIRE(d->n_e[k] == d->n_e[0], "cubic grids only (n_e equal on all axes)");
+    WCB_REQUIRE(d->n_e[0] >= 1, "n_e must be >= 1");
     WCB_REQUIRE(d->k1 && d->m1 && d->cell_class && (d->n_dof == 0 || d->lex_of_compact),
                 "NULL array in SCM descriptor");
     auto* op = new ScmOperator();
     std::unique_ptr<ScmOperator> guard(op);
     op->ctx = ctx;
-    op->dim = 2;
+    op->dim = dim;
     op->p = p;
     const int64_t n_e = d->n_e[0];
     const int64_t n1 = n_e * p + 1;
     op->n_e = n_e;
     op->n1 = n1;
     op->n = d->n_dof;
-    // columns: PADJ left pad; the last strip's tile reaches n_strips*32p + p + 1
-    const int64_t need_cols = PADJ + ceil_div(n1, 32 * p) * 32 * p + p + 2;
+    // slab
+    const int64_t lo = d->x_cell_lo;
+    const int64_t hi = d->x_cell_hi > 0 ? d->x_cell_hi : n_e;
+    const bool last = d->x_cell_hi > 0 ? (d->x_owns_last != 0) : true;
+    WCB_REQUIRE(lo >= 0 && lo < hi && hi <= n_e, "slab cell range must satisfy 0 <= lo < hi <= n_e");
+    WCB_REQUIRE(!last || hi == n_e, "only the slab ending at n_e can own the last node row");
+    op->has_top = lo > 0;
+    op->owns_last = last;
+    op->n_ex = hi - lo + 1;
+    op->n1x = op->n_ex * p + 1;
+    op->row_lo = p;
+    op->row_hi = last ? op->n1x : op->n1x - 1;
+    const int64_t TJ = 32 * (int64_t)p;
+    const int64_t need_cols = PADJ + ceil_div(n1, TJ) * TJ + p + 2;
     op->pitch = ceil_div(need_cols, 32) * 32;
-    op->rows = n1 + 2 * p;
-    op->n_state = op->rows * op->pitch;
+    const int64_t cells_row = dim == 2 ? n_e : n_e * n_e;    // cells per x cell row
+    const int64_t nodes_row = dim == 2 ? n1 : n1 * n1;       // nodes per x node row
+    if (dim == 2) {
+        op->rows = op->n1x + 2 * p;
+        op->xstride = op->pitch;
+    } else {
+        op->rows = n1 + 2 * p;                                // y rows of a plane
+        op->pplane = op->rows * op->pitch;
+        op->xstride = op->pplane;
+    }
+    const int64_t xrows = op->n1x + 2 * p;
+    op->n_state = xrows * op->xstride;
     const int N = p + 1;
     op->m1.assign(d->m1, d->m1 + N * N);
     op->k1.assign(d->k1, d->k1 + N * N);
     op->sk = d->sk;
-    const int64_t n_cells = n_e * n_e;
-    std::vector<uint8_t> mask((n_e + 2) * (n_e + 2), 0);
-    for (int64_t i = 0; i < n_e; ++i)
-        for (int64_t j = 0; j < n_e; ++j) {
-            const int8_t c = d->cell_class[i * n_e + j];
-            WCB_REQUIRE(c >= 0 && c <= 2, "cell_class values must be 0, 1 or 2");
-            mask[(i + 1) * (n_e + 2) + (j + 1)] = (uint8_t)c;
+    // local cell classes: row 0 = global cell row lo-1 (zeros if lo == 0)
+    const int64_t first_given = op->has_top ? lo - 1 : lo;        // first row present in desc
+    std::vector<int8_t> cls(op->n_ex * cells_row, 0);
+    for (int64_t gx = first_given; gx < hi; ++gx)
+        for (int64_t c = 0; c < cells_row; ++c) {
+            const int8_t v = d->cell_class[(gx - first_given) * cells_row + c];
+            WCB_REQUIRE(v >= 0 && v <= 2, "cell_class values must be 0, 1 or 2");
+            cls[(gx - lo + 1) * cells_row + c] = v;
         }
+    // mask with a zero ring
+    std::vector<uint8_t> mask;
+    if (dim == 2) {
+        const int64_t s_ = n_e + 2;
+        mask.assign((op->n_ex + 2) * s_, 0);
+        for (int64_t i = 0; i < op->n_ex; ++i)
+            for (int64_t j = 0; j < n_e; ++j) mask[(i + 1) * s_ + (j + 1)] = (uint8_t)cls[i * n_e + j];
+    } else {
+        const int64_t s_ = n_e + 2;
+        mask.assign((op->n_ex + 2) * s_ * s_, 0);
+        for (int64_t i = 0; i < op->n_ex; ++i)
+            for (int64_t j = 0; j < n_e; ++j)
+                for (int64_t k = 0; k < n_e; ++k)
+                    mask[((i + 1) * s_ + (j + 1)) * s_ + (k + 1)] = (uint8_t)cls[(i * n_e + j) * n_e + k];
+    }
+    // owned DOFs -> state index; tile flags
+    const int RX = dim == 2 ? rpe_for(p) : rx_for3(p);
+    const int64_t TI = (int64_t)RX * p;
+    const int64_t n_tiles_x = ceil_div(op->row_hi - op->row_lo, TI);
+    std::vector<uint8_t> cf;
+    if (dim == 2) {
+        op->n_strips = ceil_div(n1, TJ);
+        op->n_rtiles = n_tiles_x;
+        cf.assign(op->n_rtiles * op->n_strips, 0);
+    } else {
+        op->n_zs = ceil_div(n1, TJ);
+        op->n_xt = n_tiles_x;
+        cf.assign(op->n_xt * (n_e + 1) * op->n_zs, 0);
+    }
     op->sidx.resize(op->n);
-    std::vector<uint8_t> kept_node(n1 * n1, 0);
+    const int64_t x0 = lo * p - p;   // global node row of local row 0
     for (int64_t i = 0; i < op->n; ++i) {
         const int64_t lex = d->lex_of_compact[i];
-        WCB_REQUIRE(lex >= 0 && lex < n1 * n1, "lex_of_compact out of range");
         if (i) WCB_REQUIRE(d->lex_of_compact[i - 1] < lex, "lex_of_compact must be ascending");
-        const int64_t I = lex / n1, J = lex % n1;
-        op->sidx[i] = (I + p) * op->pitch + J + PADJ;
-        kept_node[lex] = 1;
+        const int64_t I = lex / nodes_row, rest = lex % nodes_row;
+        const int64_t Il = I - x0;
+        WCB_REQUIRE(lex >= 0 && Il >= op->row_lo && Il < op->row_hi, "a DOF lies outside the slab");
+        const int64_t t = (Il - op->row_lo) / TI;
+        if (dim == 2) {
+            op->sidx[i] = (Il + p) * op->xstride + rest + PADJ;
+            cf[(rest / TJ) * op->n_rtiles + t] = 1;
+        } else {
+            const int64_t J = rest / n1, K = rest % n1;
+            op->sidx[i] = (Il + p) * op->xstride + (J + p) * op->pitch + K + PADJ;
+            cf[(t * (n_e + 1) + J / p) * op->n_zs + K / TJ] = 1;
+        }
     }
-    // CTA tiles (32p columns x RPE*p rows) that own at least one DOF
-    const int64_t TI = (int64_t)rpe_for(p) * p, TJ = 32 * (int64_t)p;
-    op->n_strips = ceil_div(n1, TJ);
-    op->n_rtiles = ceil_div(n1, TI);
-    std::vector<uint8_t> cf(op->n_rtiles * op->n_strips, 0);   // tile t = strip*n_rtiles + rtile
-    for (int64_t I = 0; I < n1; ++I)
-        for (int64_t J = 0; J < n1; ++J)
-            if (kept_node[I * n1 + J]) cf[(J / TJ) * op->n_rtiles + I / TI] = 1;
-    // cut cells: id map + transposed stiffness
+    // cut cells (global cell lex) within the local cell rows
     op->n_cut = d->n_cut;
-    op->L = N * N;
+    op->L = dim == 2 ? N * N : N * N * N;
     const int L = op->L;
-    std::vector<int32_t> cid(n_cells, -1);
+    std::vector<int32_t> cid(op->n_ex * cells_row, -1);
     std::vector<double> KT((size_t)std::max<int64_t>(op->n_cut, 1) * L * L, 0.0);
     for (int64_t e = 0; e < op->n_cut; ++e) {
         WCB_REQUIRE(d->cut_cells && d->cut_K, "cut arrays NULL");
         const int64_t c = d->cut_cells[e];
-        WCB_REQUIRE(c >= 0 && c < n_cells && d->cell_class[c] == 2, "cut_cells must list cut cells");
         if (e) WCB_REQUIRE(d->cut_cells[e - 1] < c, "cut_cells must be ascending");
-        cid[c] = (int32_t)e;
+        const int64_t cx = c / cells_row, crest = c % cells_row;
+        const int64_t lx = cx - lo + 1;
+        WCB_REQUIRE(c >= 0 && lx >= 0 && lx < op->n_ex && cls[lx * cells_row + crest] == 2,
+                    "cut_cells must list cut cells of the slab");
+        cid[lx * cells_row + crest] = (int32_t)e;
         const double* K = d->cut_K + e * L * L;
         double* T = KT.data() + e * L * L;
-        // stored transposed and divided by sk: the kernel scales every
+        // stored transposed and divided by sk: the kernels scale every
         // output node by sk once (tensor and cut parts alike)
         for (int r = 0; r < L; ++r)
             for (int m = 0; m < L; ++m) T[m * L + r] = K[r * L + m] / d->sk;
     }
-    for (int64_t c = 0; c < n_cells; ++c)
-        WCB_REQUIRE(d->cell_class[c] != 2 || cid[c] >= 0, "a cut cell is missing from cut_cells");
+    for (size_t c = 0; c < cls.size(); ++c)
+        WCB_REQUIRE(cls[c] != 2 || cid[c] >= 0, "a cut cell is missing from cut_cells");
     cudaStream_t st = ctx->stream;
     op->d_sidx.alloc(std::max<int64_t>(op->n, 1));
     op->d_sidx.upload(op->sidx.data(), op->n, st);
@@ -522,96 +603,6 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
     op->KT.alloc(KT.size());
     op->KT.upload(KT.data(), KT.size(), st);
     // algorithmic bytes per step: 32 B per DOF + packed cut K
-    op->bytes_step = 32.0 * (double)op->n + 8.0 * (double)L * (L + 1) / 2.0 * (double)op->n_cut;
-    WCB_CUDA(cudaStreamSynchronize(st));
-    return guard.release();
-}
-
-
-// 3D: state = planes (x) of rows (y) of columns (z), padded by p planes/rows
-// on each side and PADJ columns on the left.
-static Operator* make_scm3d(Context* ctx, const wcb_scm_desc* d) {
-    const int p = d->p;
-    WCB_REQUIRE(p >= 1 && p <= 4, "p must be in 1..4 for the 3D kernel");
-    WCB_REQUIRE(d->n_e[0] == d->n_e[1] && d->n_e[1] == d->n_e[2] && d->n_e[0] >= 1,
-                "cubic grids only (n_e equal on all axes)");
-    WCB_REQUIRE(d->k1 && d->m1 && d->cell_class && (d->n_dof == 0 || d->lex_of_compact),
-                "NULL array in SCM descriptor");
-    auto* op = new ScmOperator();
-    std::unique_ptr<ScmOperator> guard(op);
-    op->ctx = ctx;
-    op->dim = 3;
-    op->p = p;
-    const int64_t n_e = d->n_e[0];
-    const int64_t n1 = n_e * p + 1;
-    op->n_e = n_e;
-    op->n1 = n1;
-    op->n = d->n_dof;
-    const int64_t TZ = 32 * (int64_t)p;
-    const int64_t need_cols = PADJ + ceil_div(n1, TZ) * TZ + p + 2;
-    op->pitch = ceil_div(need_cols, 32) * 32;
-    op->rows = n1 + 2 * p;
-    op->pplane = op->rows * op->pitch;
-    op->n_state = op->rows * op->pplane;
-    const int N = p + 1;
-    op->m1.assign(d->m1, d->m1 + N * N);
-    op->k1.assign(d->k1, d->k1 + N * N);
-    op->sk = d->sk;
-    const int64_t s_ = n_e + 2;
-    const int64_t n_cells = n_e * n_e * n_e;
-    std::vector<uint8_t> mask(s_ * s_ * s_, 0);
-    for (int64_t i = 0; i < n_e; ++i)
-        for (int64_t j = 0; j < n_e; ++j)
-            for (int64_t k = 0; k < n_e; ++k) {
-                const int8_t c = d->cell_class[(i * n_e + j) * n_e + k];
-                WCB_REQUIRE(c >= 0 && c <= 2, "cell_class values must be 0, 1 or 2");
-                mask[((i + 1) * s_ + (j + 1)) * s_ + (k + 1)] = (uint8_t)c;
-            }
-    // tiles: z strip (32 cells) x one y node-row block (cell row ey) x RX x cell rows
-    const int RX = rx_for3(p);
-    op->n_zs = ceil_div(n1, TZ);
-    op->n_xt = ceil_div(n1, (int64_t)RX * p);
-    std::vector<uint8_t> cf(op->n_xt * (n_e + 1) * op->n_zs, 0);
-    op->sidx.resize(op->n);
-    const int64_t n1sq = n1 * n1;
-    for (int64_t i = 0; i < op->n; ++i) {
-        const int64_t lex = d->lex_of_compact[i];
-        WCB_REQUIRE(lex >= 0 && lex < n1sq * n1, "lex_of_compact out of range");
-        if (i) WCB_REQUIRE(d->lex_of_compact[i - 1] < lex, "lex_of_compact must be ascending");
-        const int64_t I = lex / n1sq, J = (lex / n1) % n1, K = lex % n1;
-        op->sidx[i] = (I + p) * op->pplane + (J + p) * op->pitch + K + PADJ;
-        const int64_t ey = J / p;   // CTA owning node row J (rows ey*p .. ey*p+p-1)
-        cf[((I / (RX * p)) * (n_e + 1) + ey) * op->n_zs + K / TZ] = 1;
-    }
-    op->n_cut = d->n_cut;
-    op->L = N * N * N;
-    const int L = op->L;
-    std::vector<int32_t> cid(n_cells, -1);
-    std::vector<double> KT((size_t)std::max<int64_t>(op->n_cut, 1) * L * L, 0.0);
-    for (int64_t e = 0; e < op->n_cut; ++e) {
-        WCB_REQUIRE(d->cut_cells && d->cut_K, "cut arrays NULL");
-        const int64_t c = d->cut_cells[e];
-        WCB_REQUIRE(c >= 0 && c < n_cells && d->cell_class[c] == 2, "cut_cells must list cut cells");
-        if (e) WCB_REQUIRE(d->cut_cells[e - 1] < c, "cut_cells must be ascending");
-        cid[c] = (int32_t)e;
-        const double* K = d->cut_K + e * L * L;
-        double* T = KT.data() + e * L * L;
-        for (int r = 0; r < L; ++r)
-            for (int m = 0; m < L; ++m) T[m * L + r] = K[r * L + m] / d->sk;
-    }
-    for (int64_t c = 0; c < n_cells; ++c)
-        WCB_REQUIRE(d->cell_class[c] != 2 || cid[c] >= 0, "a cut cell is missing from cut_cells");
-    cudaStream_t st = ctx->stream;
-    op->d_sidx.alloc(std::max<int64_t>(op->n, 1));
-    op->d_sidx.upload(op->sidx.data(), op->n, st);
-    op->mask.alloc(mask.size());
-    op->mask.upload(mask.data(), mask.size(), st);
-    op->cflags.alloc(cf.size());
-    op->cflags.upload(cf.data(), cf.size(), st);
-    op->cut_id.alloc(cid.size());
-    op->cut_id.upload(cid.data(), cid.size(), st);
-    op->KT.alloc(KT.size());
-    op->KT.upload(KT.data(), KT.size(), st);
     op->bytes_step = 32.0 * (double)op->n + 8.0 * (double)L * (L + 1) / 2.0 * (double)op->n_cut;
     WCB_CUDA(cudaStreamSynchronize(st));
     return guard.release();

@@ -49,8 +49,10 @@ struct Mats2 {
 
 // 3D launch description (wcb_scm3d.cu)
 struct Scm3DGeo {
-    int64_t n_e;              // cells per axis
-    int64_t n1;               // nodes per axis
+    int64_t n_ex;             // local x cell rows (incl. the halo row 0)
+    int64_t row_lo, row_hi;   // owned local x node planes
+    int64_t n_e;              // cells along y and z
+    int64_t n1;               // nodes along y and z
     int64_t prow;             // row pitch (doubles, z fastest)
     int64_t pplane;           // plane pitch (doubles)
     const uint8_t* mask;      // (n_e+2)^3 cell codes with a ring of 0: 0 out, 1 uncut, 2 cut

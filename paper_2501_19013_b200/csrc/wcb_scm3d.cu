@@ -71,7 +71,7 @@ __device__ __forceinline__ void cut_cells_warp3(const Scm3DGeo& g, const double*
     if (!edge) cut_lanes &= cut_lanes - 1;
     while (true) {
         const int64_t ecol = ez0 + src;
-        const int32_t id = __ldg(g.cut_id + (ex * g.n_e + eyc) * g.n_e + ecol);
+        const int32_t id = __ldg(g.cut_id + (ex * g.n_e + eyc) * g.n_e + ecol);   // ex local
         const double* KT = g.KT + (int64_t)id * L * L;
         const double* corner = corner0 + src * P;   // node (ex*P, eyc*P, ecol*P) in the tile
         double t[RR];
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(Tile3<P>::NWARP * 32) k_scm3d(const __grid_con
     if (MODE == MODE_STEP && zs == 0 && ey == 0 && xt == 0) record_observers(a);
     if (!g.cflags[(xt * (g.n_e + 1) + ey) * g.n_zs + zs]) return;
     const int64_t K0 = zs * T::TZ;
-    const int64_t ex0 = xt * RX;
+    const int64_t ex0 = g.row_lo / P + xt * RX;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         mbar_expect_tx(bar, (uint32_t)T::U_BYTES);
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(Tile3<P>::NWARP * 32) k_scm3d(const __grid_con
     const int64_t ez = K0 / P + lane;
     // cell codes of the 4 (y, z) neighbours in this x cell row
     uint8_t cRR = 0, cRL = 0, cUR = 0, cUL = 0;   // (ey, ez), (ey, ez-1), (ey-1, ez), (ey-1, ez-1)
-    if (ex >= 0 && ex < g.n_e && ez <= g.n_e) {
+    if (ex >= 0 && ex < g.n_ex && ez <= g.n_e) {
         const int64_t s_ = g.n_e + 2;
         const uint8_t* mrow = g.mask + ((ex + 1) * s_ + (ey + 1)) * s_;
         if (ey < g.n_e) { cRR = __ldg(mrow + ez + 1); cRL = __ldg(mrow + ez); }
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(Tile3<P>::NWARP * 32) k_scm3d(const __grid_con
         #pragma unroll
         for (int r = 0; r < P; ++r) {
             const int64_t I = ex * P + r;
-            if (I >= g.n1) break;
+            if (I >= g.row_hi) break;
             #pragma unroll
             for (int b = 0; b < P; ++b) {
                 const int64_t J = ey * P + b;

@@ -102,7 +102,7 @@ class ScmOperator(DeviceOperator):
     kind = "scm"
 
     def __init__(self, dim: int, p: int, n_e, k1, m1, sk: float, cell_class,
-                 lex_of_compact, cut_cells, cut_K, device: int | None = None):
+                 lex_of_compact, cut_cells, cut_K, device: int | None = None, slab=None):
         dim = int(dim)
         p = int(p)
         n_e = tuple(int(v) for v in n_e)
@@ -112,8 +112,11 @@ class ScmOperator(DeviceOperator):
         self._k1 = np.ascontiguousarray(k1, dtype=np.float64).reshape(p + 1, p + 1)
         self._m1 = np.ascontiguousarray(m1, dtype=np.float64).reshape(p + 1, p + 1)
         self._cls = np.ascontiguousarray(cell_class, dtype=np.int8).reshape(-1)
-        if self._cls.shape[0] != int(np.prod(n_e)):
-            raise ValueError("cell_class must have prod(n_e) entries")
+        lo, hi, last = (0, n_e[0], True) if slab is None else (int(slab[0]), int(slab[1]),
+                                                               bool(slab[2]))
+        rows = hi - (lo - 1 if lo > 0 else lo)
+        if self._cls.shape[0] != rows * int(np.prod(n_e[1:])):
+            raise ValueError("cell_class must cover the cell rows of the operator")
         self._lex = np.ascontiguousarray(lex_of_compact, dtype=np.int64)
         self._cut = np.ascontiguousarray(cut_cells, dtype=np.int64).reshape(-1)
         self._cutK = np.ascontiguousarray(cut_K, dtype=np.float64).reshape(-1)
@@ -133,6 +136,9 @@ class ScmOperator(DeviceOperator):
         desc.n_cut = self._cut.shape[0]
         desc.cut_cells = _lib.i64ptr(self._cut) if self._cut.size else None
         desc.cut_K = _lib.dptr(self._cutK) if self._cutK.size else None
+        desc.x_cell_lo = lo
+        desc.x_cell_hi = hi
+        desc.x_owns_last = 1 if last else 0
         ctx = _lib.context(device)
         h = _lib.C.c_void_p()
         _lib.check(_lib.load().wcb_operator_scm_create(ctx.handle, _lib.C.byref(desc),
