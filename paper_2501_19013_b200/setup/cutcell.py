@@ -69,7 +69,8 @@ class CutCellIntegrator:
         n = grid.p + 1
         Ld = n ** d
         lo, hi = grid.cell_box(ijk)
-        llo, lhi, lcls, ldep = tree_partition(grid.geom, lo, hi, self.depth)
+        geom = grid.geom.restricted(lo, hi) if hasattr(grid.geom, "restricted") else grid.geom
+        llo, lhi, lcls, ldep = tree_partition(geom, lo, hi, self.depth)
         tabs = [self.tables(e) for e in ijk]
         A = 2.0 * (llo - lo) / (hi - lo) - 1.0
         pos = np.rint((A + 1.0) / 2.0 * (2.0 ** ldep[:, None])).astype(np.int64)
@@ -108,7 +109,7 @@ class CutCellIntegrator:
             for k in range(d):
                 g = lo[k] + (xd[k] + 1.0) / 2.0 * (hi[k] - lo[k])      # (Lc, q)
                 pts[..., k] = _broadcast_axis(g, k, d, q)
-            inside = grid.geom.contains(pts.reshape(-1, d))
+            inside = geom.contains(pts.reshape(-1, d))
             wt = _tensor_weights(wd)
             w_in = np.where(inside, wt, 0.0)
             V = _tensor_rows(Vd)

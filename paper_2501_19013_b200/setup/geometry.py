@@ -240,6 +240,13 @@ class BallVoids:
         self.domain_lo = np.zeros(self.dim)
         self.domain_hi = np.ones(self.dim)
 
+    def restricted(self, lo, hi):
+        """Same geometry inside the box [lo, hi]: only the voids that reach it."""
+        near = np.clip(self.centers, lo, hi) - self.centers
+        sel = np.sum(near * near, axis=1) < self.radii ** 2
+        out = BallVoids(self.dim, self.centers[sel], self.radii[sel])
+        return out
+
     def contains(self, x):
         x = np.asarray(x, dtype=float)
         flat = x.reshape(-1, self.dim)

@@ -157,6 +157,7 @@ def _discard_slivers(geom, classes, origin, h, min_volume_fraction):
     ijk = np.stack(np.unravel_index(cut, classes.shape), axis=1)
     lo = origin + ijk * h
     for s in geom.sliver_candidates(lo, h):
-        frac = geom.volume_fraction(lo[s], lo[s] + h, stop_above=min_volume_fraction)
+        local = geom.restricted(lo[s], lo[s] + h) if hasattr(geom, "restricted") else geom
+        frac = local.volume_fraction(lo[s], lo[s] + h, stop_above=min_volume_fraction)
         if frac < min_volume_fraction:
             flat[cut[s]] = OUTSIDE

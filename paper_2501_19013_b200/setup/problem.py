@@ -32,6 +32,68 @@ def _kron_list(mats):
     return out
 
 
+def _cut_chunk(args):
+    grid, depth, cells, alpha, sk, sm, lumping = args
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(1)
+    except ImportError:
+        lim = None
+    d = grid.dim
+    L = (grid.p + 1) ** d
+    integ = CutCellIntegrator(grid, depth)
+    K = np.empty((cells.shape[0], L, L))
+    M = np.empty((cells.shape[0], L) if lumping != "none" else (cells.shape[0], L, L))
+    shape = (grid.n_e,) * d
+    for j, cl in enumerate(cells):
+        Mi, Mo, Ki, Ko = integ.integrate(np.unravel_index(int(cl), shape))
+        K[j] = sk * (Ki + alpha * Ko)
+        M_o = sm * (Mi + alpha * Mo)
+        if lumping == "none":
+            M[j] = M_o           # consistent cut mass (IMEX, src/assembly.py:591-592)
+        else:
+            M[j] = hrz_lump(M_o) if lumping == "hrz" else row_sum_lump(M_o)
+    if lim is not None:
+        lim.unregister()
+    return K, M
+
+
+def integrate_cut_cells(grid, depth, cut, alpha, sk, sm, lumping, n_jobs=None):
+    """Physical cut-cell stiffness and (lumped) mass for every cut cell;
+    large sets are spread over host processes (each cell is independent)."""
+    import os
+    n_jobs = n_jobs or min(32, os.cpu_count() or 1)
+    if cut.shape[0] < 256 or n_jobs <= 1:
+        return _cut_chunk((grid, depth, cut, alpha, sk, sm, lumping))
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    chunks = np.array_split(cut, n_jobs * 4)
+    light = _LightGrid(grid)
+    with ProcessPoolExecutor(max_workers=n_jobs, mp_context=mp.get_context("fork")) as ex:
+        parts = list(ex.map(_cut_chunk, [(light, depth, c, alpha, sk, sm, lumping)
+                                         for c in chunks if c.shape[0]]))
+    return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
+
+
+class _LightGrid:
+    """What the cut-cell integrator needs from a Grid (cheap to pickle)."""
+
+    def __init__(self, g):
+        self.geom, self.basis, self.dim, self.origin, self.h = g.geom, g.basis, g.dim, g.origin, g.h
+
+    @property
+    def p(self):
+        return self.basis.p
+
+    @property
+    def n_e(self):
+        return self.basis.n_e
+
+    def cell_box(self, ijk):
+        lo = self.origin + np.asarray(ijk, dtype=float) * self.h
+        return lo, lo + self.h
+
+
 @dataclass
 class ScmProblem:
     grid: Grid
@@ -67,19 +129,7 @@ class ScmProblem:
         sm = rho * (h / 2.0) ** d
         m1, k1 = uncut_1d(grid.basis, 0)
         cut = grid.cut_lex
-        integ = CutCellIntegrator(grid, depth)
-        cut_K = np.empty((cut.shape[0], L, L))
-        cut_M = np.empty((cut.shape[0], L) if lumping != "none" else (cut.shape[0], L, L))
-        shape = (grid.n_e,) * d
-        for j, cl in enumerate(cut):
-            ijk = np.unravel_index(int(cl), shape)
-            Mi, Mo, Ki, Ko = integ.integrate(ijk)
-            cut_K[j] = sk * (Ki + alpha * Ko)
-            M_o = sm * (Mi + alpha * Mo)
-            if lumping == "none":
-                cut_M[j] = M_o           # consistent cut mass (IMEX, src/assembly.py:591-592)
-            else:
-                cut_M[j] = hrz_lump(M_o) if lumping == "hrz" else row_sum_lump(M_o)
+        cut_K, cut_M = integrate_cut_cells(grid, depth, cut, alpha, sk, sm, lumping)
         prob = cls(grid=grid, rho=rho, c=c, alpha=alpha, depth=depth, lumping=lumping,
                    sk=sk, sm=sm, m1=m1, k1=k1, cut_K=cut_K, cut_M=cut_M,
                    m_diag=np.zeros(0))
