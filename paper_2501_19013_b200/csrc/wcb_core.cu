@@ -393,9 +393,7 @@ int wcb_max_gen_eig(wcb_operator* o, const double* m_diag, const double* x0, dou
 struct wcb_cdm_plan {
     Operator* op = nullptr;
     DevBuf<double> m_state, minv;
-    DevBuf<double> F_dense;
-    DevBuf<int64_t> F_idx;
-    DevBuf<double> F_val;
+    DevBuf<double> F_win;
     Source src;
     int64_t n_obs = 0;
     DevBuf<int64_t> obs_indptr, obs_idx;
@@ -598,31 +596,12 @@ int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s
         if (n) k_mass_state<<<grid_for(ctx, n), 256, 0, s>>>(n, map.p, dm.p, P->m_state.p, P->minv.p);
         ctx->launches += 2;
         WCB_CHECK_LAUNCH();
-        // source: sparse when it has few nonzeros
-        std::vector<std::pair<int64_t, double>> nz;
-        for (int64_t i = 0; i < n; ++i)
-            if (F_s[i] != 0.0) nz.emplace_back(si[i], F_s[i]);
-        if ((int64_t)nz.size() * 16 <= n || nz.size() <= 4096) {
-            std::sort(nz.begin(), nz.end());
-            std::vector<int64_t> idx(nz.size());
-            std::vector<double> val(nz.size());
-            for (size_t i = 0; i < nz.size(); ++i) { idx[i] = nz[i].first; val[i] = nz[i].second; }
-            P->F_idx.alloc(idx.size());
-            P->F_val.alloc(val.size());
-            P->F_idx.upload(idx.data(), idx.size(), s);
-            P->F_val.upload(val.data(), val.size(), s);
-            P->src.idx = P->F_idx.p;
-            P->src.val = P->F_val.p;
-            P->src.nnz = (int64_t)idx.size();
-            if (!idx.empty()) { P->src.lo = idx.front(); P->src.hi = idx.back(); }
-        } else {
-            DevBuf<double> dF(n);
-            dF.upload(F_s, n, s);
-            P->F_dense.alloc(ns);
-            P->F_dense.zero(s);
-            op->scatter(dF.p, P->F_dense.p);
-            P->src.dense = P->F_dense.p;
-            WCB_CUDA(cudaStreamSynchronize(s));
+        // source: dense window over its nonzeros' state-index range
+        {
+            std::vector<std::pair<int64_t, double>> nz;
+            for (int64_t i = 0; i < n; ++i)
+                if (F_s[i] != 0.0) nz.emplace_back(si[i], F_s[i]);
+            P->src = make_source(std::move(nz), P->F_win, s);
         }
         if (obs && obs->n_obs > 0) {
             P->n_obs = obs->n_obs;

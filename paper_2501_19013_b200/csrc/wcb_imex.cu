@@ -174,9 +174,7 @@ struct wcb_imex_plan {
     DevBuf<int64_t> c_compact;
     DevBuf<double> minv, m_d_state;   // 1/m_d at d slots (0 at c / non-DOF), m_d at d slots
     DevBuf<double> Fc;
-    DevBuf<double> F_dense;
-    DevBuf<int64_t> F_idx;
-    DevBuf<double> F_val;
+    DevBuf<double> F_win;
     Source src;
     DevLU S, Mcc;
     int64_t n_obs = 0;
@@ -255,24 +253,12 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
         P->m_d_state.alloc(ns); P->m_d_state.upload(md.data(), ns, s);
         P->c_state.alloc(cs.size()); P->c_state.upload(cs.data(), n_c, s);
         P->Fc.alloc(Fc.size()); P->Fc.upload(Fc.data(), n_c, s);
-        // force vector for the d rows (sparse when possible)
-        std::vector<std::pair<int64_t, double>> nz;
-        for (int64_t i = 0; i < n; ++i)
-            if (F_s[i] != 0.0) nz.emplace_back(si[i], F_s[i]);
-        std::sort(nz.begin(), nz.end());
-        if (nz.size() <= 4096 || (int64_t)nz.size() * 16 <= n) {
-            std::vector<int64_t> idx(nz.size());
-            std::vector<double> val(nz.size());
-            for (size_t i = 0; i < nz.size(); ++i) { idx[i] = nz[i].first; val[i] = nz[i].second; }
-            P->F_idx.alloc(std::max<size_t>(idx.size(), 1)); P->F_idx.upload(idx.data(), idx.size(), s);
-            P->F_val.alloc(std::max<size_t>(val.size(), 1)); P->F_val.upload(val.data(), val.size(), s);
-            P->src.idx = P->F_idx.p; P->src.val = P->F_val.p; P->src.nnz = (int64_t)idx.size();
-            if (!idx.empty()) { P->src.lo = idx.front(); P->src.hi = idx.back(); }
-        } else {
-            std::vector<double> Fd(ns, 0.0);
-            for (auto& q : nz) Fd[q.first] = q.second;
-            P->F_dense.alloc(ns); P->F_dense.upload(Fd.data(), ns, s);
-            P->src.dense = P->F_dense.p;
+        // force vector for the d rows: dense window over its nonzeros
+        {
+            std::vector<std::pair<int64_t, double>> nz;
+            for (int64_t i = 0; i < n; ++i)
+                if (F_s[i] != 0.0) nz.emplace_back(si[i], F_s[i]);
+            P->src = make_source(std::move(nz), P->F_win, s);
         }
         if (n_c) {
             WCB_REQUIRE(S_cc && M_cc && S_cc->n == n_c && M_cc->n == n_c, "LU factors of size n_c required");

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/wavecell_b200.h"
@@ -83,26 +84,33 @@ struct Context {
 };
 
 // ----------------------------------------------------------- step inputs ----
-// Sparse or dense spatial load F_s in the operator's state layout.
+// Spatial load F_s in the operator's state layout, stored as a dense window
+// over the state-index range [lo, hi] of its nonzeros (a point source spans
+// a few rows; a distributed load spans the state), so a lookup is one load.
 struct Source {
-    const double* dense = nullptr;   // state-layout dense F_s, or null
-    const int64_t* idx = nullptr;    // sorted state indices of nonzeros
-    const double* val = nullptr;
-    int64_t nnz = 0;
-    int64_t lo = 1, hi = 0;          // idx range (empty when lo > hi)
+    const double* win = nullptr;     // win[i - lo] = F_s at state index i
+    int64_t lo = 1, hi = 0;          // window range (empty when lo > hi)
 };
 
 __device__ __forceinline__ double source_at(const Source& s, int64_t i) {
-    if (s.dense) return s.dense[i];
-    if (i < s.lo || i > s.hi) return 0.0;
-    int64_t a = 0, b = s.nnz - 1;
-    while (a <= b) {
-        int64_t m = (a + b) >> 1;
-        int64_t v = s.idx[m];
-        if (v == i) return s.val[m];
-        if (v < i) a = m + 1; else b = m - 1;
-    }
-    return 0.0;
+    return (i < s.lo || i > s.hi) ? 0.0 : s.win[i - s.lo];
+}
+
+// Host: build the window from (state index, value) pairs.
+inline Source make_source(std::vector<std::pair<int64_t, double>> nz, DevBuf<double>& buf,
+                          cudaStream_t s) {
+    Source src;
+    if (nz.empty()) return src;
+    std::sort(nz.begin(), nz.end());
+    src.lo = nz.front().first;
+    src.hi = nz.back().first;
+    std::vector<double> w((size_t)(src.hi - src.lo + 1), 0.0);
+    for (auto& q : nz) w[(size_t)(q.first - src.lo)] = q.second;
+    buf.alloc(w.size());
+    buf.upload(w.data(), w.size(), s);
+    WCB_CUDA(cudaStreamSynchronize(s));
+    src.win = buf.p;
+    return src;
 }
 
 // One explicit CDM step, src/timeint.py:179-190, fused:

@@ -31,11 +31,13 @@
 #include "wcb_scm.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
 
 namespace wcb {
+__device__ __forceinline__ int smid() { int r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
 
 // element rows per tile; one compute warp each plus one halo warp
 #ifndef WCB2D_RPE
@@ -84,10 +86,28 @@ struct Scm2DGeo {
     const int32_t* cut_id;    // n_ex x n_ey -> cut index or -1
     const double* KT;         // n_cut * L * L, transposed physical cut stiffness / sk
     const uint8_t* cflags;    // per tile (strip-major): 1 = owns a DOF
+    const int32_t* order;     // live tiles (strip-major ids), most expensive first
     int64_t n_strips;
     int64_t n_rtiles;
     int64_t pitch;            // row pitch of the state (doubles)
 };
+
+// P consecutive doubles of a lane from shared memory (16-byte loads for
+// even P: the row starts are 16-byte aligned in every tile layout)
+template <int P>
+__device__ __forceinline__ void lds_row(const double* p, double (&v)[P]) {
+    if constexpr ((P % 2) == 0) {
+        #pragma unroll
+        for (int j = 0; j < P; j += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(p + j);
+            v[j] = t.x;
+            v[j + 1] = t.y;
+        }
+    } else {
+        #pragma unroll
+        for (int j = 0; j < P; ++j) v[j] = p[j];
+    }
+}
 
 // One node row of the smem tile: y contraction (masked) then x contraction
 // accumulated into Y.  `row` points at tile column 0 of that row.
@@ -153,14 +173,15 @@ __device__ __forceinline__ void row_contract(const double (&mc)[orb_count(P)],
 template <int P, int UW, int CO>
 __device__ __forceinline__ void cut_cells_warp(const Scm2DGeo& g, const double* rows, int64_t ex,
                                                int64_t ey0, int lane, unsigned cut_lanes,
-                                               bool edge, double (&Y)[P + 1][P]) {
+                                               bool edge, int32_t cid, int32_t cidL,
+                                               double (&Y)[P + 1][P]) {
     constexpr int N = P + 1;
     constexpr int L = N * N;
     int src = edge ? -1 : (__ffs(cut_lanes) - 1);
     if (!edge) cut_lanes &= cut_lanes - 1;
     while (src >= -1) {
-        const int64_t ecol = ey0 + src;
-        const int32_t id = __ldg(g.cut_id + ex * g.n_ey + ecol);
+        // cut ids were fetched by their lanes in the prologue
+        const int32_t id = src >= 0 ? __shfl_sync(0xffffffffu, cid, src) : __shfl_sync(0xffffffffu, cidL, 0);
         const double* KT = g.KT + (int64_t)id * L * L;
         const double* corner = rows + CO + P + src * P;
         constexpr int RR = (L + 31) / 32;   // output rows per lane
@@ -208,9 +229,18 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
-    const int64_t strip = blockIdx.x, rtile = blockIdx.y;
-    if (MODE == MODE_STEP && blockIdx.x == 0 && blockIdx.y == 0) record_observers(a);
-    if (!g.cflags[strip * g.n_rtiles + rtile]) return;   // tile without DOFs
+    // tiles are dispatched longest-first (cut-cell tiles lead) so the last
+    // wave is made of cheap interior tiles
+#ifdef WCB2D_EMPTY
+    return;
+#endif
+#ifdef WCB2D_TRACE
+    unsigned long long t_0, t_1, t_2, t_3, t_4;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_0));
+#endif
+    const int32_t tid = __ldg(g.order + blockIdx.x);
+    const int64_t strip = tid / g.n_rtiles, rtile = tid % g.n_rtiles;
+    if (MODE == MODE_STEP && blockIdx.x == 0) record_observers(a);
     const int64_t J0 = strip * T::TJ, I0 = g.row_lo + rtile * T::TI;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
@@ -232,6 +262,8 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
         mR = __ldg(g.mask + (ex + 1) * ms_ + (ey + 1));
         mL = __ldg(g.mask + (ex + 1) * ms_ + ey);
     }
+    const int32_t cid = mR == 2 ? __ldg(g.cut_id + ex * g.n_ey + ey) : -1;
+    const int32_t cidL = (lane == 0 && mL == 2) ? __ldg(g.cut_id + ex * g.n_ey + ey - 1) : -1;
     const int64_t Jl = J0 + lane * P;
     if (MODE == MODE_STEP && !halo && !WCB2D_EPI_TMA) {
         #pragma unroll
@@ -242,7 +274,13 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
         }
     }
     __syncthreads();   // barrier init visible
+#ifdef WCB2D_TRACE
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_1));
+#endif
     mbar_wait(bar, 0);
+#ifdef WCB2D_TRACE
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_2));
+#endif
 
     double mc[orb_count(P)], kc[orb_count(P)];
     #pragma unroll
@@ -257,15 +295,22 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
         const double chiR = mR == 1 ? 1.0 : 0.0;
         const double chiL = mL == 1 ? 1.0 : 0.0;
         const double* rows = us + (size_t)(rbase + P) * T::UW;
+#ifndef WCB2D_NOTENSOR
         #pragma unroll
         for (int c = 0; c < N; ++c) row_contract<P>(mc, kc, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
+#endif
         const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
         const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
-        if (cl || ed) cut_cells_warp<P, T::UW, T::CO>(g, rows, ex, J0 / P, lane, cl, ed, Y);
+#ifndef WCB2D_NOCUT
+        if (cl || ed) cut_cells_warp<P, T::UW, T::CO>(g, rows, ex, J0 / P, lane, cl, ed, cid, cidL, Y);
+#endif
     }
     // row a = P of element row ex is row a = 0 of element row ex+1
     #pragma unroll
     for (int j = 0; j < P; ++j) carry[((halo ? 0 : w + 1) * P + j) * 32 + lane] = Y[P][j];
+#ifdef WCB2D_TRACE
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_3));
+#endif
     __syncthreads();
     unsigned long long amp = 0ULL;
     if (!halo) {
@@ -294,8 +339,8 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
                                        (size_t)(w * P + r) * T::TJ + lane * P;
                     const double* msm = reinterpret_cast<const double*>(smem + T::OFF_MINV) +
                                         (size_t)(w * P + r) * T::TJ + lane * P;
-                    #pragma unroll
-                    for (int j = 0; j < P; ++j) { up[j] = ps[j]; mi[j] = msm[j]; }
+                    lds_row<P>(ps, up);
+                    lds_row<P>(msm, mi);
                 } else {
                     #pragma unroll
                     for (int j = 0; j < P; ++j) {
@@ -304,11 +349,25 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
                     }
                 }
                 const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
-                double v[P];
+                double v[P], uu[P];
+                lds_row<P>(urow, uu);
                 #pragma unroll
                 for (int j = 0; j < P; ++j) {
                     const double fF = src ? f * source_at(a.F, base + j) : f * 0.0;
-                    v[j] = leapfrog(urow[j], up[j], Y[r][j], mi[j], fF, a.dt2);
+                    v[j] = leapfrog(uu[j], up[j], Y[r][j], mi[j], fF, a.dt2);
+                }
+                if constexpr (P == 4) {
+                    if (!edge) {
+                        // one 32-byte store per lane: every sector written exactly once
+                        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(a.out + base),
+                                     "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]) : "memory");
+                        #pragma unroll
+                        for (int j = 0; j < P; ++j) {
+                            unsigned long long b = mi[j] != 0.0 ? amp_bits(v[j]) : 0ULL;
+                            amp = b > amp ? b : amp;
+                        }
+                        continue;
+                    }
                 }
                 #pragma unroll
                 for (int j = 0; j < P; ++j) {
@@ -321,8 +380,17 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
             }
         }
     }
+#ifndef WCB2D_NOAMP
     if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
+#endif
+#ifdef WCB2D_TRACE
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_4));
+    if (MODE == MODE_STEP && a.k == 100 && threadIdx.x == 0)
+        printf("TRACE blk %d w %d sm %d start %llu pre %llu tma %llu comp %llu end %llu\n", blockIdx.x, threadIdx.x >> 5,
+               smid(), t_0, t_1 - t_0, t_2 - t_0, t_3 - t_0, t_4 - t_0);
+#endif
 }
+
 
 struct ScmOperator final : Operator {
     int dim = 2, p = 4;
@@ -338,6 +406,8 @@ struct ScmOperator final : Operator {
     DevBuf<int32_t> cut_id;
     MapCache maps;
     DevBuf<double> KT;
+    DevBuf<int32_t> order;        // 2D tile kernel: live tiles, most expensive first
+    int64_t n_order = 0;
     int64_t n_strips = 0, n_rtiles = 0;
     std::vector<double> m1, k1;
     double sk = 1.0;
@@ -377,8 +447,9 @@ struct ScmOperator final : Operator {
                     mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
-        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, n_strips, n_rtiles, pitch};
-        dim3 grid((unsigned)n_strips, (unsigned)n_rtiles);
+        if (!n_order) return;
+        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, order.p, n_strips, n_rtiles, pitch};
+        dim3 grid((unsigned)n_order);
         const CUtensorMap& mu = state_map<P>(a.cur);
         const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
         const CUtensorMap& mp = epi ? state_map<P>(a.prev, 1) : mu;
@@ -591,6 +662,31 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
     }
     for (size_t c = 0; c < cls.size(); ++c)
         WCB_REQUIRE(cls[c] != 2 || cid[c] >= 0, "a cut cell is missing from cut_cells");
+    if (dim == 2) {
+        // dispatch order of the tile kernel: live tiles by decreasing cost
+        // (one unit per tile + CUT_COST per cut cell it integrates, the halo
+        // row above included), ties in strip-major order
+        constexpr double CUT_COST = 0.15;
+        const int64_t TI_cells = RX;
+        std::vector<std::pair<double, int32_t>> w;
+        for (int64_t t = 0; t < (int64_t)cf.size(); ++t) {
+            if (!cf[t]) continue;
+            const int64_t strip = t / op->n_rtiles, rt = t % op->n_rtiles;
+            const int64_t ex0 = (op->row_lo + rt * TI) / p - 1, ey0 = strip * (TJ / p) - 1;
+            int n_c = 0;
+            for (int64_t ex = std::max<int64_t>(ex0, 0); ex < std::min<int64_t>(ex0 + 1 + TI_cells, op->n_ex); ++ex)
+                for (int64_t ey = std::max<int64_t>(ey0, 0); ey < std::min<int64_t>(ey0 + 1 + TJ / p, n_e); ++ey)
+                    n_c += cid[ex * cells_row + ey] >= 0;
+            w.emplace_back(-(1.0 + CUT_COST * n_c), (int32_t)t);
+        }
+        std::stable_sort(w.begin(), w.end(),
+                         [](const auto& a, const auto& b) { return a.first < b.first; });
+        std::vector<int32_t> ord(w.size());
+        for (size_t i = 0; i < w.size(); ++i) ord[i] = w[i].second;
+        op->n_order = (int64_t)ord.size();
+        op->order.alloc(std::max<int64_t>(op->n_order, 1));
+        op->order.upload(ord.data(), ord.size(), ctx->stream);
+    }
     cudaStream_t st = ctx->stream;
     op->d_sidx.alloc(std::max<int64_t>(op->n, 1));
     op->d_sidx.upload(op->sidx.data(), op->n, st);

@@ -62,7 +62,7 @@ def integrate_cut_cells(grid, depth, cut, alpha, sk, sm, lumping, n_jobs=None):
     """Physical cut-cell stiffness and (lumped) mass for every cut cell;
     large sets are spread over host processes (each cell is independent)."""
     import os
-    n_jobs = n_jobs or min(32, os.cpu_count() or 1)
+    n_jobs = n_jobs or int(os.environ.get("WAVECELL_B200_JOBS", 0)) or min(32, os.cpu_count() or 1)
     if cut.shape[0] < 256 or n_jobs <= 1:
         return _cut_chunk((grid, depth, cut, alpha, sk, sm, lumping))
     from concurrent.futures import ProcessPoolExecutor
