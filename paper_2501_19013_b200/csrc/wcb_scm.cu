@@ -41,10 +41,10 @@ __device__ __forceinline__ int smid() { int r; asm volatile("mov.u32 %0, %%smid;
 
 // element rows per tile; one compute warp each plus one halo warp
 #ifndef WCB2D_RPE
-#define WCB2D_RPE 4
+#define WCB2D_RPE 3
 #endif
 #ifndef WCB2D_MINB
-#define WCB2D_MINB 3
+#define WCB2D_MINB 4
 #endif
 #ifndef WCB2D_EPI_TMA
 #define WCB2D_EPI_TMA 1      // 1: psi_{k-1} and 1/m also staged by TMA
