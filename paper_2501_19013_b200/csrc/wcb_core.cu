@@ -228,6 +228,12 @@ int wcb_context_create(int device, wcb_context** out) {
                         "capability major " + std::to_string(major)};
         WCB_CUDA(cudaDeviceGetAttribute(&x.sm_count, cudaDevAttrMultiProcessorCount, device));
         WCB_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
+        {   // keep freed run buffers in the device pool (no release to the OS)
+            cudaMemPool_t pool;
+            WCB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t keep = ~0ULL;
+            WCB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        }
         WCB_CUDA(cudaEventCreate(&x.ev0));
         WCB_CUDA(cudaEventCreate(&x.ev1));
         WCB_CUDA(cudaEventCreate(&x.ev2));
@@ -451,10 +457,10 @@ static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, do
         Operator* op = P->op;
         const int64_t ns = op->n_state;
         if (P->A.n != (size_t)ns) {
-            P->A.alloc(ns); P->B.alloc(ns); P->V.alloc(ns); P->T.alloc(ns);
+            P->A.alloc(ns, s); P->B.alloc(ns, s); P->V.alloc(ns, s); P->T.alloc(ns, s);
             P->B.zero(s); P->T.zero(s);
         }
-        if (P->amp.n < (size_t)(n_t + 1)) P->amp.alloc(n_t + 1);
+        if (P->amp.n < (size_t)(n_t + 1)) P->amp.alloc(n_t + 1, s);
         P->amp.zero(s);
         // initial state: zeros unless given (src/timeint.py:162-163)
         P->A.zero(s);
@@ -585,12 +591,14 @@ int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s
         std::unique_ptr<wcb_cdm_plan> P(new wcb_cdm_plan());
         P->op = op;
         const std::vector<int64_t>& si = op->state_index();
-        DevBuf<int64_t> map(n);
+        DevBuf<int64_t> map;
+        map.alloc(n, s);
         map.upload(si.data(), n, s);
-        DevBuf<double> dm(n);
+        DevBuf<double> dm;
+        dm.alloc(n, s);
         dm.upload(m_diag, n, s);
-        P->m_state.alloc(ns);
-        P->minv.alloc(ns);
+        P->m_state.alloc(ns, s);
+        P->minv.alloc(ns, s);
         k_fill<<<grid_for(ctx, ns), 256, 0, s>>>(ns, 1.0, P->m_state.p);
         P->minv.zero(s);
         if (n) k_mass_state<<<grid_for(ctx, n), 256, 0, s>>>(n, map.p, dm.p, P->m_state.p, P->minv.p);
@@ -612,11 +620,11 @@ int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s
                 WCB_REQUIRE(c >= 0 && c < n, "observer column out of range");
                 sidx[j] = si[c];
             }
-            P->obs_indptr.alloc(obs->n_obs + 1);
+            P->obs_indptr.alloc(obs->n_obs + 1, s);
             P->obs_indptr.upload(obs->indptr, obs->n_obs + 1, s);
-            P->obs_idx.alloc(std::max<int64_t>(nnz, 1));
+            P->obs_idx.alloc(std::max<int64_t>(nnz, 1), s);
             P->obs_idx.upload(sidx.data(), nnz, s);
-            P->obs_val.alloc(std::max<int64_t>(nnz, 1));
+            P->obs_val.alloc(std::max<int64_t>(nnz, 1), s);
             P->obs_val.upload(obs->data, nnz, s);
         }
         WCB_CUDA(cudaStreamSynchronize(s));
@@ -659,13 +667,14 @@ int wcb_cdm_plan_run(wcb_cdm_plan* P, const double* ft, double dt, int64_t n_t,
         WCB_CUDA(cudaSetDevice(ctx->device));
         cudaStream_t s = ctx->stream;
         const int64_t n = op->n;
-        DevBuf<double> dft(std::max<int64_t>(n_t, 1)), dpsi0, dv0, dout(std::max<int64_t>(n, 1)),
-            dobs;
+        DevBuf<double> dft, dpsi0, dv0, dout, dobs;
+        dft.alloc(std::max<int64_t>(n_t, 1), s);
+        dout.alloc(std::max<int64_t>(n, 1), s);
         WCB_REQUIRE(ft, "force table is NULL (it holds max(n_t,1) entries, ft[0] = f_t(0.0))");
         dft.upload(ft, std::max<int64_t>(n_t, 1), s);
-        if (psi0) { dpsi0.alloc(n); dpsi0.upload(psi0, n, s); }
-        if (v0) { dv0.alloc(n); dv0.upload(v0, n, s); }
-        if (obs_out && P->n_obs) dobs.alloc(P->n_obs * (n_t + 1));
+        if (psi0) { dpsi0.alloc(n, s); dpsi0.upload(psi0, n, s); }
+        if (v0) { dv0.alloc(n, s); dv0.upload(v0, n, s); }
+        if (obs_out && P->n_obs) dobs.alloc(P->n_obs * (n_t + 1), s);
         run_cdm_device(P, dft.p, dt, n_t, dpsi0.p, dv0.p, dout.p, dobs.p, div, tm);
         if (n) WCB_CUDA(cudaMemcpyAsync(psi_out, dout.p, n * sizeof(double),
                                         cudaMemcpyDeviceToHost, s));

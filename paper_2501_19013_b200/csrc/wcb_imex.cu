@@ -36,17 +36,17 @@ struct DevLU {
     DevBuf<double> Lx, Ux;
     void load(const wcb_lu* lu, cudaStream_t s) {
         n = lu->n;
-        perm_r.alloc(std::max<int64_t>(n, 1));
-        perm_c.alloc(std::max<int64_t>(n, 1));
+        perm_r.alloc(std::max<int64_t>(n, 1), s);
+        perm_c.alloc(std::max<int64_t>(n, 1), s);
         perm_r.upload(lu->perm_r, n, s);
         perm_c.upload(lu->perm_c, n, s);
         const int64_t nl = lu->L_indptr[n], nu = lu->U_indptr[n];
-        Lp.alloc(n + 1); Lp.upload(lu->L_indptr, n + 1, s);
-        Up.alloc(n + 1); Up.upload(lu->U_indptr, n + 1, s);
-        Li.alloc(std::max<int64_t>(nl, 1)); Li.upload(lu->L_indices, nl, s);
-        Ui.alloc(std::max<int64_t>(nu, 1)); Ui.upload(lu->U_indices, nu, s);
-        Lx.alloc(std::max<int64_t>(nl, 1)); Lx.upload(lu->L_data, nl, s);
-        Ux.alloc(std::max<int64_t>(nu, 1)); Ux.upload(lu->U_data, nu, s);
+        Lp.alloc(n + 1, s); Lp.upload(lu->L_indptr, n + 1, s);
+        Up.alloc(n + 1, s); Up.upload(lu->U_indptr, n + 1, s);
+        Li.alloc(std::max<int64_t>(nl, 1), s); Li.upload(lu->L_indices, nl, s);
+        Ui.alloc(std::max<int64_t>(nu, 1), s); Ui.upload(lu->U_indices, nu, s);
+        Lx.alloc(std::max<int64_t>(nl, 1), s); Lx.upload(lu->L_data, nl, s);
+        Ux.alloc(std::max<int64_t>(nu, 1), s); Ux.upload(lu->U_data, nu, s);
     }
 };
 
@@ -249,10 +249,10 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
             cs[i] = si[r];
             Fc[i] = F_s[r];
         }
-        P->minv.alloc(ns); P->minv.upload(minv.data(), ns, s);
-        P->m_d_state.alloc(ns); P->m_d_state.upload(md.data(), ns, s);
-        P->c_state.alloc(cs.size()); P->c_state.upload(cs.data(), n_c, s);
-        P->Fc.alloc(Fc.size()); P->Fc.upload(Fc.data(), n_c, s);
+        P->minv.alloc(ns, s); P->minv.upload(minv.data(), ns, s);
+        P->m_d_state.alloc(ns, s); P->m_d_state.upload(md.data(), ns, s);
+        P->c_state.alloc(cs.size(), s); P->c_state.upload(cs.data(), n_c, s);
+        P->Fc.alloc(Fc.size(), s); P->Fc.upload(Fc.data(), n_c, s);
         // force vector for the d rows: dense window over its nonzeros
         {
             std::vector<std::pair<int64_t, double>> nz;
@@ -273,16 +273,16 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
                 WCB_REQUIRE(obs->indices[j] >= 0 && obs->indices[j] < n, "observer column out of range");
                 sidx[j] = si[obs->indices[j]];
             }
-            P->obs_indptr.alloc(obs->n_obs + 1); P->obs_indptr.upload(obs->indptr, obs->n_obs + 1, s);
-            P->obs_idx.alloc(sidx.size()); P->obs_idx.upload(sidx.data(), nnz, s);
-            P->obs_val.alloc(std::max<int64_t>(nnz, 1)); P->obs_val.upload(obs->data, nnz, s);
+            P->obs_indptr.alloc(obs->n_obs + 1, s); P->obs_indptr.upload(obs->indptr, obs->n_obs + 1, s);
+            P->obs_idx.alloc(sidx.size(), s); P->obs_idx.upload(sidx.data(), nnz, s);
+            P->obs_val.alloc(std::max<int64_t>(nnz, 1), s); P->obs_val.upload(obs->data, nnz, s);
         }
         const int64_t m = std::max<int64_t>(n_c, 1);
-        P->A.alloc(ns); P->B.alloc(ns); P->T.alloc(ns); P->V.alloc(ns);
-        P->psi_c.alloc(m); P->v_c.alloc(m); P->a_c.alloc(m); P->pred.alloc(m); P->vpred.alloc(m);
-        P->Kc.alloc(m); P->rhs.alloc(m); P->y.alloc(m); P->z.alloc(m);
-        P->done.alloc(m);
-        P->counter.alloc(2);
+        P->A.alloc(ns, s); P->B.alloc(ns, s); P->T.alloc(ns, s); P->V.alloc(ns, s);
+        P->psi_c.alloc(m, s); P->v_c.alloc(m, s); P->a_c.alloc(m, s); P->pred.alloc(m, s); P->vpred.alloc(m, s);
+        P->Kc.alloc(m, s); P->rhs.alloc(m, s); P->y.alloc(m, s); P->z.alloc(m, s);
+        P->done.alloc(m, s);
+        P->counter.alloc(2, s);
         WCB_CUDA(cudaStreamSynchronize(s));
         *out = P.release();
         return WCB_OK;
@@ -319,9 +319,9 @@ int wcb_imex_plan_run(wcb_imex_plan* P, double f0, const double* ft_k, const dou
         std::vector<double> hk(n_t + 1), hn(std::max<int64_t>(n_t, 1));
         hk[0] = f0;
         for (int64_t k = 0; k < n_t; ++k) { hk[k + 1] = ft_k[k]; hn[k] = ft_new[k]; }
-        P->ft_k.alloc(hk.size()); P->ft_k.upload(hk.data(), hk.size(), s);
-        P->ft_new.alloc(hn.size()); P->ft_new.upload(hn.data(), hn.size(), s);
-        P->amp.alloc(n_t + 1);
+        P->ft_k.alloc(hk.size(), s); P->ft_k.upload(hk.data(), hk.size(), s);
+        P->ft_new.alloc(hn.size(), s); P->ft_new.upload(hn.data(), hn.size(), s);
+        P->amp.alloc(n_t + 1, s);
         P->amp.zero(s);
         // initial state
         DevBuf<double> tmp(std::max<int64_t>(n, 1));
@@ -354,7 +354,7 @@ int wcb_imex_plan_run(wcb_imex_plan* P, double f0, const double* ft_k, const dou
         a.F = P->src;
         a.dt2 = dt * dt;
         DevBuf<double> dobs;
-        if (P->n_obs && obs_out) dobs.alloc(P->n_obs * stride);
+        if (P->n_obs && obs_out) dobs.alloc(P->n_obs * stride, s);
         auto record = [&](int64_t k, const double* psi) {
             if (!(P->n_obs && obs_out)) return;
             StepArgs r;

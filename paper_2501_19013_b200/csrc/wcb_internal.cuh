@@ -44,20 +44,39 @@ struct DevBuf {
     explicit DevBuf(size_t count) { alloc(count); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; o.st = nullptr; }
     DevBuf& operator=(DevBuf&& o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; st = o.st;
+            o.p = nullptr; o.n = 0; o.st = nullptr;
+        }
         return *this;
     }
     ~DevBuf() { release(); }
+    cudaStream_t st = nullptr;   // stream-ordered allocation (pool) when set
     void alloc(size_t count) {
         release();
         n = count;
         if (count) WCB_CUDA(cudaMalloc(&p, count * sizeof(T)));
     }
+    // Stream-ordered allocation from the device's memory pool: per-run
+    // buffers are recycled without the device-wide sync of cudaFree.
+    void alloc(size_t count, cudaStream_t s) {
+        release();
+        n = count;
+        st = s;
+        if (count) WCB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (!st || cudaFreeAsync(p, st) != cudaSuccess) {
+                cudaGetLastError();
+                cudaFree(p);
+            }
+        }
         p = nullptr;
+        st = nullptr;
         n = 0;
     }
     void upload(const T* h, size_t count, cudaStream_t s) {
@@ -106,7 +125,7 @@ inline Source make_source(std::vector<std::pair<int64_t, double>> nz, DevBuf<dou
     src.hi = nz.back().first;
     std::vector<double> w((size_t)(src.hi - src.lo + 1), 0.0);
     for (auto& q : nz) w[(size_t)(q.first - src.lo)] = q.second;
-    buf.alloc(w.size());
+    buf.alloc(w.size(), s);
     buf.upload(w.data(), w.size(), s);
     WCB_CUDA(cudaStreamSynchronize(s));
     src.win = buf.p;

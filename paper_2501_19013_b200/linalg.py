@@ -30,11 +30,24 @@ def is_structurally_diagonal(A) -> bool:
     return bool(np.all(coo.row[mask] == coo.col[mask]))
 
 
+def _csr_identity_pattern(M) -> bool:
+    """Fast path: a CSR matrix storing exactly its diagonal, in order."""
+    if not sp.issparse(M) or M.format != "csr" or M.shape[0] != M.shape[1]:
+        return False
+    n = M.shape[0]
+    if M.nnz != n:
+        return False
+    ar = np.arange(n + 1, dtype=M.indptr.dtype)
+    return bool(np.array_equal(M.indptr, ar) and np.array_equal(M.indices, ar[:n]))
+
+
 def diagonal_mass(M) -> np.ndarray:
     """The diagonal of a structurally diagonal SPD mass, with the checks of
     ``factorize``'s fast path (src/linalg.py:63-69)."""
     if isinstance(M, np.ndarray) and M.ndim == 1:
         d = np.ascontiguousarray(M, dtype=np.float64)
+    elif _csr_identity_pattern(M):
+        d = np.ascontiguousarray(M.data, dtype=np.float64)
     else:
         A = sp.csr_matrix(M)
         if A.shape[0] != A.shape[1]:
