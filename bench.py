@@ -91,6 +91,9 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        from paper_2501_19013_b200.setup.problem import _under_profiler
+        if _under_profiler():   # under ncu: no child processes
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",

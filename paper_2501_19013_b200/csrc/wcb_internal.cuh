@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <string>
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/wavecell_b200.h"
@@ -36,6 +37,15 @@ struct Error {
     } while (0)
 
 // ------------------------------------------------------------ device buf ----
+// WAVECELL_B200_NO_POOL=1 turns the stream-ordered pool off (plain cudaMalloc)
+inline bool use_pool() {
+    static const bool on = [] {
+        const char* e = getenv("WAVECELL_B200_NO_POOL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -63,6 +73,7 @@ struct DevBuf {
     // Stream-ordered allocation from the device's memory pool: per-run
     // buffers are recycled without the device-wide sync of cudaFree.
     void alloc(size_t count, cudaStream_t s) {
+        if (!use_pool()) { alloc(count); return; }
         release();
         n = count;
         st = s;

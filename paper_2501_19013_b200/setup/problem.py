@@ -58,11 +58,20 @@ def _cut_chunk(args):
     return K, M
 
 
+def _under_profiler() -> bool:
+    import os
+    if any(k.startswith(("CUDA_INJECTION", "NV_TPS", "NV_NSIGHT")) for k in os.environ):
+        return True
+    return "TreeLauncher" in os.environ.get("LD_PRELOAD", "")
+
+
 def integrate_cut_cells(grid, depth, cut, alpha, sk, sm, lumping, n_jobs=None):
     """Physical cut-cell stiffness and (lumped) mass for every cut cell;
     large sets are spread over host processes (each cell is independent)."""
     import os
     n_jobs = n_jobs or int(os.environ.get("WAVECELL_B200_JOBS", 0)) or min(32, os.cpu_count() or 1)
+    if _under_profiler():
+        n_jobs = 1   # under ncu: forked workers crash the injected tool
     if cut.shape[0] < 256 or n_jobs <= 1:
         return _cut_chunk((grid, depth, cut, alpha, sk, sm, lumping))
     from concurrent.futures import ProcessPoolExecutor
