@@ -79,6 +79,19 @@ def barrier(world):
         dist.barrier()
 
 
+def measured_traffic(cfg_name: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/*/traffic.json, newest round first), else None."""
+    for f in sorted(Path(__file__).resolve().parent.glob("profiles/r*/traffic.json"), reverse=True):
+        try:
+            ent = json.loads(f.read_text()).get(cfg_name)
+        except (OSError, ValueError):
+            continue
+        if ent:
+            return ent["bytes"]
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -402,7 +415,7 @@ def main():
                 "dt": dt, "lambda_max": lam, "power_iterations": iters,
                 "setup_s": round(t_build, 2), "power_iteration_s": round(t_eig, 3)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": None if slab_mode else measured_traffic(args.config),
                          "kernel": kname,
                          "bytes_per_launch": bytes_step,
                          "launch_us": per_step_s * 1e6, "peak_kind": peak_kind},
