@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define WCB_ABI_VERSION 1
+#define WCB_ABI_VERSION 2
 
 enum wcb_status {
     WCB_OK = 0,
@@ -96,6 +96,29 @@ typedef struct {
     int32_t x_owns_last;
 } wcb_scm_desc;
 
+/* Matrix-free plane-strain elastic stiffness on the SCM node grid (BASELINE
+ * config 4; the reference has no vector operator).  DOFs are
+ * component major: dof = comp * n_node + node (node = scalar compact id).
+ * Uncut cells: [[(l+2m) k1(x)m1 + m m1(x)k1, l g1(x)g1^T + m (g1(x)g1^T)^T],
+ * [.^T, m k1(x)m1 + (l+2m) m1(x)k1]] by sum factorisation, g1[a][b] =
+ * int phi_a' phi_b.  Cut cells: dense physical matrices, L = 2 (p+1)^2,
+ * local order (comp, x-node, y-node), src/assembly.py:575-583 applied to
+ * each derivative pairing. */
+typedef struct {
+    int32_t p;                   /* 1..5                                                */
+    int64_t n_e[2];              /* cells per axis (equal)                              */
+    double lam, mu;              /* Lame parameters (plane strain)                      */
+    const double* m1;            /* (p+1)^2 GL-exact 1D mass                             */
+    const double* k1;            /* (p+1)^2 GL-exact 1D stiffness                        */
+    const double* g1;            /* (p+1)^2 GL-exact int phi_a' phi_b                    */
+    const int8_t* cell_class;    /* n_e^2 ElementClass, lex                              */
+    int64_t n_node;              /* compact nodes (DOFs = 2 n_node)                      */
+    const int64_t* lex_of_compact; /* n_node node lex ids, ascending                     */
+    int64_t n_cut;
+    const int64_t* cut_cells;    /* n_cut cell lex ids, ascending                        */
+    const double* cut_K;         /* n_cut * L * L, L = 2 (p+1)^2                          */
+} wcb_elastic_desc;
+
 /* ---- library / context ------------------------------------------------- */
 int wcb_abi_version(void);
 const char* wcb_last_error(void);
@@ -112,6 +135,8 @@ int wcb_operator_csr_create(wcb_context* ctx, int64_t n, const int64_t* indptr,
                             wcb_operator** out);
 /* Matrix-free SCM K (replaces the CSR K of Lagrange systems, src/assembly.py:554-583). */
 int wcb_operator_scm_create(wcb_context* ctx, const wcb_scm_desc* desc, wcb_operator** out);
+/* Matrix-free plane-strain K (config 4; used by imex_run / cdm_run as any K). */
+int wcb_operator_elastic_create(wcb_context* ctx, const wcb_elastic_desc* desc, wcb_operator** out);
 int wcb_operator_destroy(wcb_operator* op);
 int64_t wcb_operator_n(const wcb_operator* op);
 /* y = K @ x on host buffers (K.__matmul__, src/timeint.py:175,182). */
@@ -142,6 +167,13 @@ int wcb_cdm_group_run(int n_plans, wcb_cdm_plan** plans, const double* ft, doubl
  * vector (src/linalg.py:103-105).  Returns WCB_E_NOCONV after max_iter. */
 int wcb_max_gen_eig(wcb_operator* K, const double* m_diag, const double* x0,
                     double tol, int64_t max_iter, double* lam, int64_t* n_iter);
+/* Power iteration on the principal sub-problem (K_ss, M_ss), s = sub_idx
+ * (ascending compact ids): imex_critical_time_step's d subsystem,
+ * src/timeint.py:80-88, without forming K_dd.  m_diag holds n entries (only
+ * the sub entries are read), x0_sub the n_sub-long start vector. */
+int wcb_max_gen_eig_sub(wcb_operator* op, const double* m_diag, int64_t n_sub,
+                        const int64_t* sub_idx, const double* x0_sub, double tol,
+                        int64_t max_iter, double* out_lambda, int64_t* out_iters);
 
 /* ---- central difference method: cdm_run, src/timeint.py:159-193 ---------- */
 /* Diagonal M only (the factorize() fast path, src/linalg.py:63-69).  F_s may be

@@ -29,8 +29,9 @@ EXPORTS = (
     "wcb_abi_version", "wcb_last_error", "wcb_device_count",
     "wcb_context_create", "wcb_context_destroy", "wcb_context_stream",
     "wcb_context_launches", "wcb_operator_csr_create", "wcb_operator_scm_create",
+    "wcb_operator_elastic_create",
     "wcb_operator_destroy", "wcb_operator_n", "wcb_operator_apply", "wcb_operator_halo",
-    "wcb_max_gen_eig", "wcb_cdm_plan_create", "wcb_cdm_plan_destroy",
+    "wcb_max_gen_eig", "wcb_max_gen_eig_sub", "wcb_cdm_plan_create", "wcb_cdm_plan_destroy",
     "wcb_cdm_plan_run", "wcb_cdm_plan_run_device", "wcb_imex_plan_create",
     "wcb_imex_plan_destroy", "wcb_imex_plan_run", "wcb_dist_unique_id", "wcb_dist_init",
     "wcb_dist_finalize", "wcb_cdm_group_run",
@@ -66,6 +67,13 @@ class ScmDesc(C.Structure):
                 ("x_owns_last", _i32)]
 
 
+class ElasticDesc(C.Structure):
+    _fields_ = [("p", _i32), ("n_e", _i64 * 2), ("lam", _d), ("mu", _d), ("m1", _dp),
+                ("k1", _dp), ("g1", _dp), ("cell_class", _i8p), ("n_node", _i64),
+                ("lex_of_compact", _i64p), ("n_cut", _i64), ("cut_cells", _i64p),
+                ("cut_K", _dp)]
+
+
 class LU(C.Structure):
     _fields_ = [("n", _i64), ("perm_r", _i64p), ("perm_c", _i64p),
                 ("L_indptr", _i64p), ("L_indices", _i32p), ("L_data", _dp),
@@ -82,11 +90,13 @@ _SIGS = {
     "wcb_context_launches": (_i64, [_p]),
     "wcb_operator_csr_create": (C.c_int, [_p, _i64, _i64p, _i32p, _dp, C.POINTER(_p)]),
     "wcb_operator_scm_create": (C.c_int, [_p, C.POINTER(ScmDesc), C.POINTER(_p)]),
+    "wcb_operator_elastic_create": (C.c_int, [_p, C.POINTER(ElasticDesc), C.POINTER(_p)]),
     "wcb_operator_destroy": (C.c_int, [_p]),
     "wcb_operator_n": (_i64, [_p]),
     "wcb_operator_apply": (C.c_int, [_p, _dp, _dp]),
     "wcb_operator_halo": (C.c_int, [_p, _i64p]),
     "wcb_max_gen_eig": (C.c_int, [_p, _dp, _dp, _d, _i64, _dp, _i64p]),
+    "wcb_max_gen_eig_sub": (C.c_int, [_p, _dp, _i64, _i64p, _dp, _d, _i64, _dp, _i64p]),
     "wcb_cdm_plan_create": (C.c_int, [_p, _dp, _dp, C.POINTER(Observer), C.POINTER(_p)]),
     "wcb_cdm_plan_destroy": (C.c_int, [_p]),
     "wcb_cdm_plan_run": (C.c_int, [_p, _dp, _d, _i64, _dp, _dp, _dp, _dp,

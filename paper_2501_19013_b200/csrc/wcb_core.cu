@@ -161,7 +161,7 @@ __global__ void k_pow_dots(int64_t ns, const double* __restrict__ x, const doubl
     for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < ns; i += (int64_t)gridDim.x * RB) {
         double xi = x[i];
         a += xi * Kx[i];
-        b += xi * (m[i] * xi);
+        b += xi == 0.0 ? 0.0 : xi * (m[i] * xi);   // frozen DOFs carry m = inf
     }
     double sa = block_sum<RB>(a);
     double sb = block_sum<RB>(b);
@@ -290,6 +290,17 @@ int wcb_operator_scm_create(wcb_context* ctx, const wcb_scm_desc* desc, wcb_oper
     });
 }
 
+int wcb_operator_elastic_create(wcb_context* ctx, const wcb_elastic_desc* desc, wcb_operator** out) {
+    return guarded([&] {
+        WCB_REQUIRE(ctx && desc && out, "NULL argument");
+        WCB_CUDA(cudaSetDevice(ctx->c.device));
+        std::unique_ptr<wcb_operator> o(new wcb_operator());
+        o->op = make_elastic_operator(&ctx->c, desc);
+        *out = o.release();
+        return WCB_OK;
+    });
+}
+
 int wcb_operator_destroy(wcb_operator* op) {
     if (!op) return WCB_OK;
     return guarded([&] {
@@ -325,8 +336,10 @@ int wcb_operator_apply(wcb_operator* o, const double* x, double* y) {
 }
 
 // ---------------------------------------------------------- max_gen_eig ----
-int wcb_max_gen_eig(wcb_operator* o, const double* m_diag, const double* x0, double tol,
-                    int64_t max_iter, double* lam, int64_t* n_iter) {
+// Power iteration of M^-1 K on the state; DOFs with m = +inf are frozen at
+// zero (principal sub-problem, see wcb_max_gen_eig_sub).
+static int max_gen_eig_impl(wcb_operator* o, const double* m_diag, const double* x0, double tol,
+                            int64_t max_iter, double* lam, int64_t* n_iter) {
     return guarded([&] {
         WCB_REQUIRE(o && m_diag && x0 && lam && n_iter, "NULL argument");
         Operator* op = o->op;
@@ -391,6 +404,33 @@ int wcb_max_gen_eig(wcb_operator* o, const double* m_diag, const double* x0, dou
         *n_iter = (int64_t)ctx->h_scalars[4];
         return WCB_OK;
     });
+}
+
+int wcb_max_gen_eig(wcb_operator* o, const double* m_diag, const double* x0, double tol,
+                    int64_t max_iter, double* lam, int64_t* n_iter) {
+    return max_gen_eig_impl(o, m_diag, x0, tol, max_iter, lam, n_iter);
+}
+
+int wcb_max_gen_eig_sub(wcb_operator* o, const double* m_diag, int64_t n_sub,
+                        const int64_t* sub_idx, const double* x0_sub, double tol,
+                        int64_t max_iter, double* lam, int64_t* n_iter) {
+    int64_t n = 0;
+    int code = guarded([&] {
+        WCB_REQUIRE(o && m_diag && sub_idx && x0_sub, "NULL argument");
+        n = o->op->n;
+        WCB_REQUIRE(n_sub >= 1 && n_sub <= n, "sub-problem size must be in 1..n");
+        return WCB_OK;
+    });
+    if (code != WCB_OK) return code;
+    std::vector<double> m(n, INFINITY), x(n, 0.0);
+    for (int64_t k = 0; k < n_sub; ++k) {
+        const int64_t i = sub_idx[k];
+        if (i < 0 || i >= n || (k && sub_idx[k - 1] >= i))
+            return guarded([&] { throw Error{WCB_E_ARG, "sub_idx must be ascending DOF ids"}; return 0; });
+        m[i] = m_diag[i];
+        x[i] = x0_sub[k];
+    }
+    return max_gen_eig_impl(o, m.data(), x.data(), tol, max_iter, lam, n_iter);
 }
 
 }  // extern "C"

@@ -268,6 +268,7 @@ void nccl_allreduce_sum_f64(Context* ctx, double* d, int64_t n);
 Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* indptr,
                             const int32_t* indices, const double* data);
 Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d);
+Operator* make_elastic_operator(Context* ctx, const wcb_elastic_desc* d);
 
 // one-block observer recording (wcb_core.cu)
 void launch_record_observers(Context* ctx, const StepArgs& a);

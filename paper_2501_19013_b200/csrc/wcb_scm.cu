@@ -392,6 +392,8 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
 }
 
 
+#include "wcb_ela2d.cuh"
+
 struct ScmOperator final : Operator {
     int dim = 2, p = 4;
     int64_t n_e = 0, n1 = 0, pitch = 0, rows = 0;
@@ -411,6 +413,11 @@ struct ScmOperator final : Operator {
     int64_t n_strips = 0, n_rtiles = 0;
     std::vector<double> m1, k1;
     double sk = 1.0;
+    // plane-strain elasticity (ncomp = 2): component planes `plane` apart
+    int ncomp = 1;
+    std::vector<double> g1;
+    double lam = 0.0, mu = 0.0;
+    int64_t plane = 0;
     int64_t n_cut = 0;
     int L = 0;
     double bytes_step = 0.0;
@@ -457,8 +464,70 @@ struct ScmOperator final : Operator {
         k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(mu, mp, mm, g, mt, sk, a);
         ctx->launches++;
     }
+    template <int P>
+    const CUtensorMap& state_map_e(const double* ptr, int kind) {
+        using T = Tile2E<P>;
+        return maps.get(ptr, 20 + kind, [&] {
+            const uint64_t dims[2] = {(uint64_t)pitch, (uint64_t)(2 * rows)};
+            const uint64_t strides[1] = {(uint64_t)pitch};
+            const uint32_t box[2] = {(uint32_t)(kind ? T::TJ : T::UW), (uint32_t)(kind ? T::TI : T::UH)};
+            return make_map_f64(ptr, 2, dims, strides, box);
+        });
+    }
+    template <int P, int MODE>
+    void launch2e(const StepArgs& a) {
+        using T = Tile2E<P>;
+        static bool attr_set = false;
+        if (!attr_set) {
+            WCB_CUDA(cudaFuncSetAttribute(k_ela2d<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)T::SMEM));
+            attr_set = true;
+        }
+        if (!n_order) return;
+        constexpr int N = P + 1;
+        EMats<P> mt;
+        const double l2m = lam + 2.0 * mu;
+        for (int r = 0; r < N; ++r)
+            for (int c = 0; c < N; ++c) {
+                const int rc = r * N + c, cr = c * N + r;
+                mt.ym[rc] = m1[rc];
+                mt.yk[rc] = k1[rc];
+                mt.yg[rc] = g1[rc];
+                mt.xa[0][0][rc] = l2m * k1[rc];
+                mt.xa[0][1][rc] = mu * m1[rc];
+                mt.xa[0][2][rc] = lam * g1[rc];
+                mt.xa[0][3][rc] = mu * g1[cr];
+                mt.xa[1][0][rc] = mu * k1[rc];
+                mt.xa[1][1][rc] = l2m * m1[rc];
+                mt.xa[1][2][rc] = lam * g1[cr];
+                mt.xa[1][3][rc] = mu * g1[rc];
+            }
+        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, order.p, n_strips, n_rtiles, pitch};
+        const CUtensorMap& mu_ = state_map_e<P>(a.cur, 0);
+        const bool epi = MODE == MODE_STEP;
+        const CUtensorMap& mp = epi ? state_map_e<P>(a.prev, 1) : mu_;
+        const CUtensorMap& mm = epi ? state_map_e<P>(a.minv, 1) : mu_;
+        k_ela2d<P, MODE><<<(unsigned)n_order, T::NWARP * 32, T::SMEM, ctx->stream>>>(
+            mu_, mp, mm, g, mt, plane, (int32_t)rows, a);
+        ctx->launches++;
+    }
+    template <int MODE>
+    void dispatch2e(const StepArgs& a) {
+        switch (p) {
+            case 1: launch2e<1, MODE>(a); break;
+            case 2: launch2e<2, MODE>(a); break;
+            case 3: launch2e<3, MODE>(a); break;
+            case 4: launch2e<4, MODE>(a); break;
+            case 5: launch2e<5, MODE>(a); break;
+            default: throw Error{WCB_E_UNSUPPORTED, "2D elastic kernel built for p = 1..5"};
+        }
+    }
     template <int MODE>
     void dispatch2d(const StepArgs& a) {
+        if (ncomp == 2) {
+            dispatch2e<MODE>(a);
+            return;
+        }
         switch (p) {
             case 1: launch2d<1, MODE>(a); break;
             case 2: launch2d<2, MODE>(a); break;
@@ -530,12 +599,45 @@ struct ScmOperator final : Operator {
 // Both dimensions: slab preprocessing (cell rows [x_cell_lo-1, x_cell_hi) of
 // the global grid along x, one halo cell row above), state layout, tile flags,
 // cut-cell tables.
+static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int ncomp, double lam,
+                                    double mu, const double* g1);
+
 Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
+    return build_scm_operator(ctx, d, 1, 0.0, 0.0, nullptr);
+}
+
+// Plane strain: the node grid of the scalar descriptor carries two
+// displacement components (compact DOF = comp * n_node + node).
+Operator* make_elastic_operator(Context* ctx, const wcb_elastic_desc* e) {
+    WCB_REQUIRE(e && e->m1 && e->k1 && e->g1, "NULL array in elastic descriptor");
+    WCB_REQUIRE(e->p >= 1 && e->p <= 5, "p must be in 1..5 for the elastic kernel");
+    WCB_REQUIRE(e->lam + 2.0 * e->mu > 0.0 && e->mu > 0.0, "Lame parameters must give a positive operator");
+    wcb_scm_desc d{};
+    d.dim = 2;
+    d.p = e->p;
+    d.n_e[0] = e->n_e[0];
+    d.n_e[1] = e->n_e[1];
+    d.n_e[2] = 1;
+    d.k1 = e->k1;
+    d.m1 = e->m1;
+    d.sk = 1.0;
+    d.cell_class = e->cell_class;
+    d.n_dof = e->n_node;
+    d.lex_of_compact = e->lex_of_compact;
+    d.n_cut = e->n_cut;
+    d.cut_cells = e->cut_cells;
+    d.cut_K = e->cut_K;
+    return build_scm_operator(ctx, &d, 2, e->lam, e->mu, e->g1);
+}
+
+static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int ncomp, double lam,
+                                    double mu, const double* g1) {
     WCB_REQUIRE(d->dim == 2 || d->dim == 3, "dim must be 2 or 3");
     const int dim = d->dim;
     const int p = d->p;
     if (dim == 2) WCB_REQUIRE(p >= 1 && p <= 6, "p must be in 1..6 for the 2D kernel");
     else WCB_REQUIRE(p >= 1 && p <= 4, "p must be in 1..4 for the 3D kernel");
+    WCB_REQUIRE(ncomp == 1 || (dim == 2 && d->x_cell_hi == 0), "elastic operator: 2D, single slab");
     for (int k = 1; k < dim; ++k)
         WCB_REQUIRE(d->n_e[k] == d->n_e[0], "cubic grids only (n_e equal on all axes)");
     WCB_REQUIRE(d->n_e[0] >= 1, "n_e must be >= 1");
@@ -550,7 +652,11 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
     const int64_t n1 = n_e * p + 1;
     op->n_e = n_e;
     op->n1 = n1;
-    op->n = d->n_dof;
+    op->n = ncomp * d->n_dof;
+    op->ncomp = ncomp;
+    op->lam = lam;
+    op->mu = mu;
+    if (ncomp == 2) op->g1.assign(g1, g1 + (p + 1) * (p + 1));
     // slab
     const int64_t lo = d->x_cell_lo;
     const int64_t hi = d->x_cell_hi > 0 ? d->x_cell_hi : n_e;
@@ -577,7 +683,8 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
         op->xstride = op->pplane;
     }
     const int64_t xrows = op->n1x + 2 * p;
-    op->n_state = xrows * op->xstride;
+    op->plane = xrows * op->xstride;
+    op->n_state = ncomp * op->plane;
     const int N = p + 1;
     op->m1.assign(d->m1, d->m1 + N * N);
     op->k1.assign(d->k1, d->k1 + N * N);
@@ -607,7 +714,7 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
                     mask[((i + 1) * s_ + (j + 1)) * s_ + (k + 1)] = (uint8_t)cls[(i * n_e + j) * n_e + k];
     }
     // owned DOFs -> state index; tile flags
-    const int RX = dim == 2 ? rpe_for(p) : rx_for3(p);
+    const int RX = ncomp == 2 ? rpe_e(p) : dim == 2 ? rpe_for(p) : rx_for3(p);
     const int64_t TI = (int64_t)RX * p;
     const int64_t n_tiles_x = ceil_div(op->row_hi - op->row_lo, TI);
     std::vector<uint8_t> cf;
@@ -622,7 +729,7 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
     }
     op->sidx.resize(op->n);
     const int64_t x0 = lo * p - p;   // global node row of local row 0
-    for (int64_t i = 0; i < op->n; ++i) {
+    for (int64_t i = 0; i < d->n_dof; ++i) {
         const int64_t lex = d->lex_of_compact[i];
         if (i) WCB_REQUIRE(d->lex_of_compact[i - 1] < lex, "lex_of_compact must be ascending");
         const int64_t I = lex / nodes_row, rest = lex % nodes_row;
@@ -638,9 +745,10 @@ Operator* make_scm_operator(Context* ctx, const wcb_scm_desc* d) {
             cf[(t * (n_e + 1) + J / p) * op->n_zs + K / TJ] = 1;
         }
     }
+    for (int64_t i = 0; i < (ncomp - 1) * d->n_dof; ++i) op->sidx[d->n_dof + i] = op->plane + op->sidx[i];
     // cut cells (global cell lex) within the local cell rows
     op->n_cut = d->n_cut;
-    op->L = dim == 2 ? N * N : N * N * N;
+    op->L = ncomp * (dim == 2 ? N * N : N * N * N);
     const int L = op->L;
     std::vector<int32_t> cid(op->n_ex * cells_row, -1);
     std::vector<double> KT((size_t)std::max<int64_t>(op->n_cut, 1) * L * L, 0.0);

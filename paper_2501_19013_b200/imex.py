@@ -106,9 +106,12 @@ def imex_run(M, K, F_s, f_t, dt: float, n_t: int, c_idx, d_idx, obs_mat=None,
             raise ValueError("d mass block has non-positive diagonal entries")
     S_lu = M_lu = None
     if has_c:
-        Kh = _host_stiffness(K)
         M_cc = M[c_idx][:, c_idx]
-        K_cc = Kh[c_idx][:, c_idx]
+        prob = getattr(K, "problem", None)
+        if isinstance(K, DeviceOperator) and hasattr(prob, "stiffness_block"):
+            K_cc = prob.stiffness_block(c_idx)       # from the cells touching c only
+        else:
+            K_cc = _host_stiffness(K)[c_idx][:, c_idx]
         S_lu = _LU(_splu((M_cc + (beta * dt * dt) * K_cc).tocsr()))
         M_lu = _LU(_splu(M_cc))
     timings.factorization = time.perf_counter() - t0

@@ -93,6 +93,30 @@ def max_gen_eig(K, M, tol=1e-9, max_iter=50000, seed=0, device: int | None = Non
     return float(lam.value), int(it.value)
 
 
+def max_gen_eig_sub(op, m_diag, sub_idx, tol=1e-9, max_iter=50000, seed=0):
+    """``max_gen_eig(K[s][:, s], diag(m)[s])`` on the device without forming
+    the sub-matrix: the other DOFs are frozen at zero inside the operator's
+    own apply.  The start vector is the reference's for size ``len(s)``."""
+    sub = np.ascontiguousarray(sub_idx, dtype=np.int64)
+    m = np.ascontiguousarray(m_diag, dtype=np.float64)
+    if m.shape[0] != op.n:
+        raise ValueError("K and M sizes differ")
+    ms = m[sub]
+    if np.any(ms <= 0.0) or not np.all(np.isfinite(ms)):
+        raise IndefiniteMatrixError("diagonal matrix has non-positive entries; "
+                                    "check the stabilization and lumping settings")
+    x0 = start_vector(sub.shape[0], seed)
+    lam = _lib.C.c_double(0.0)
+    it = _lib.C.c_int64(0)
+    code = _lib.load().wcb_max_gen_eig_sub(op.handle, _lib.dptr(m), sub.shape[0],
+                                           _lib.i64ptr(sub), _lib.dptr(x0), float(tol),
+                                           int(max_iter), _lib.C.byref(lam), _lib.C.byref(it))
+    if code == _lib.WCB_E_NOCONV:
+        raise RuntimeError(_lib.last_error())
+    _lib.check(code)
+    return float(lam.value), int(it.value)
+
+
 def dt_crit(K, M, tol=1e-9, seed=0, device: int | None = None) -> float:
     """Critical time step of central differences, ``2 / sqrt(lam_max(K, M))``
     (src/linalg.py:125-130)."""
@@ -103,4 +127,4 @@ def dt_crit(K, M, tol=1e-9, seed=0, device: int | None = None) -> float:
 
 
 __all__ = ["IndefiniteMatrixError", "is_structurally_diagonal", "diagonal_mass",
-           "start_vector", "max_gen_eig", "dt_crit", "DeviceOperator"]
+           "start_vector", "max_gen_eig", "max_gen_eig_sub", "dt_crit", "DeviceOperator"]

@@ -148,6 +148,51 @@ class ScmOperator(DeviceOperator):
         self.n_cut = int(self._cut.shape[0])
 
 
+class ElasticOperator(DeviceOperator):
+    """Matrix-free plane-strain stiffness on the SCM node grid (BASELINE
+    config 4; setup/elastic.py documents the operator).  DOFs are component
+    major: ``dof = comp * n_node + node``."""
+
+    kind = "elastic"
+
+    def __init__(self, p: int, n_e: int, lam: float, mu: float, m1, k1, g1, cell_class,
+                 lex_of_compact, cut_cells, cut_K, device: int | None = None):
+        p = int(p)
+        n_e = int(n_e)
+        N = p + 1
+        L = 2 * N * N
+        self._m1 = np.ascontiguousarray(m1, dtype=np.float64).reshape(N, N)
+        self._k1 = np.ascontiguousarray(k1, dtype=np.float64).reshape(N, N)
+        self._g1 = np.ascontiguousarray(g1, dtype=np.float64).reshape(N, N)
+        self._cls = np.ascontiguousarray(cell_class, dtype=np.int8).reshape(-1)
+        if self._cls.shape[0] != n_e * n_e:
+            raise ValueError("cell_class must hold n_e^2 entries")
+        self._lex = np.ascontiguousarray(lex_of_compact, dtype=np.int64)
+        self._cut = np.ascontiguousarray(cut_cells, dtype=np.int64).reshape(-1)
+        self._cutK = np.ascontiguousarray(cut_K, dtype=np.float64).reshape(-1)
+        if self._cutK.shape[0] != self._cut.shape[0] * L * L:
+            raise ValueError("cut_K must hold n_cut * L * L values, L = 2 (p+1)^2")
+        desc = _lib.ElasticDesc()
+        desc.p = p
+        desc.n_e[0] = desc.n_e[1] = n_e
+        desc.lam, desc.mu = float(lam), float(mu)
+        desc.m1, desc.k1, desc.g1 = _lib.dptr(self._m1), _lib.dptr(self._k1), _lib.dptr(self._g1)
+        desc.cell_class = _lib.i8ptr(self._cls)
+        desc.n_node = self._lex.shape[0]
+        desc.lex_of_compact = _lib.i64ptr(self._lex)
+        desc.n_cut = self._cut.shape[0]
+        desc.cut_cells = _lib.i64ptr(self._cut) if self._cut.size else None
+        desc.cut_K = _lib.dptr(self._cutK) if self._cutK.size else None
+        ctx = _lib.context(device)
+        h = _lib.C.c_void_p()
+        _lib.check(_lib.load().wcb_operator_elastic_create(ctx.handle, _lib.C.byref(desc),
+                                                           _lib.C.byref(h)))
+        super().__init__(h, 2 * self._lex.shape[0], ctx)
+        self.dim, self.p, self.n_e = 2, p, (n_e, n_e)
+        self.lam, self.mu = float(lam), float(mu)
+        self.n_cut = int(self._cut.shape[0])
+
+
 _cache: dict[int, tuple] = {}
 
 

@@ -184,6 +184,15 @@ def uncut_1d(basis: Basis1D, e: int, q: int | None = None):
     return (V * w[:, None]).T @ V, (D * w[:, None]).T @ D
 
 
+def uncut_g1(basis: Basis1D, e: int, q: int | None = None):
+    """Exact 1D reference "gradient-mass" G[a][b] = int phi_a' phi_b of cell e
+    (the mixed-derivative factor of the plane-strain operator)."""
+    q = basis.p + 1 if q is None else q
+    x, w = gl_rule(q)
+    V, D = basis.eval(e, x)
+    return (D * w[:, None]).T @ V
+
+
 def dyadic_intervals(max_depth: int):
     """Start, length and id offset of every dyadic subinterval of [-1, 1]
     up to max_depth (src/assembly.py:447-459)."""
@@ -212,4 +221,5 @@ def dyadic_tables(basis: Basis1D, e: int, max_depth: int, q: int | None = None):
     wq = w[None, :] * (lengths[:, None] / 2.0)
     m1 = np.einsum("lqa,lq,lqb->lab", V, wq, V)
     k1 = np.einsum("lqa,lq,lqb->lab", D, wq, D)
-    return {"xi": xi, "w": wq, "V": V, "D": D, "m1": m1, "k1": k1, "offsets": offsets}
+    g1 = np.einsum("lqa,lq,lqb->lab", D, wq, V)     # int phi_a' phi_b (elasticity)
+    return {"xi": xi, "w": wq, "V": V, "D": D, "m1": m1, "k1": k1, "g1": g1, "offsets": offsets}

@@ -127,6 +127,67 @@ class CutCellIntegrator:
         return M_in, M_out, K_in, K_out
 
 
+class ElasticCutIntegrator(CutCellIntegrator):
+    """2D cut-cell integrals for plane-strain elasticity: mass and the three
+    derivative pairings, physical ("in") and fictitious ("out") parts
+    separate.  Kxy[a][b] = int dN_a/dx dN_b/dy; Kyx = Kxy^T."""
+
+    def integrate_elastic(self, ij):
+        grid = self.grid
+        if grid.dim != 2:
+            raise ValueError("elastic cut integration is 2D")
+        n = grid.p + 1
+        Ld = n * n
+        lo, hi = grid.cell_box(ij)
+        geom = grid.geom.restricted(lo, hi) if hasattr(grid.geom, "restricted") else grid.geom
+        llo, lhi, lcls, ldep = tree_partition(geom, lo, hi, self.depth)
+        tabs = [self.tables(e) for e in ij]
+        A = 2.0 * (llo - lo) / (hi - lo) - 1.0
+        pos = np.rint((A + 1.0) / 2.0 * (2.0 ** ldep[:, None])).astype(np.int64)
+        ids = tabs[0]["offsets"][ldep][:, None] + pos
+        names = ("M", "Kxx", "Kyy", "Kxy")
+        acc = {(nm, part): np.zeros((Ld, Ld)) for nm in names for part in ("in", "out")}
+
+        def settled(sel):
+            t = [{key: tabs[k][key][ids[sel, k]] for key in ("m1", "k1", "g1")} for k in range(2)]
+            return {"M": kron_sum([t[0]["m1"], t[1]["m1"]]),
+                    "Kxx": kron_sum([t[0]["k1"], t[1]["m1"]]),
+                    "Kyy": kron_sum([t[0]["m1"], t[1]["k1"]]),
+                    "Kxy": kron_sum([t[0]["g1"], np.swapaxes(t[1]["g1"], 1, 2)])}
+
+        for klass, part in ((INSIDE, "in"), (OUTSIDE, "out")):
+            sel = np.flatnonzero(lcls == klass)
+            if sel.shape[0]:
+                for nm, v in settled(sel).items():
+                    acc[(nm, part)] += v
+        sel = np.flatnonzero(lcls == CUT)
+        if sel.shape[0]:
+            full = settled(sel)
+            Vd = [tabs[k]["V"][ids[sel, k]] for k in range(2)]
+            Dd = [tabs[k]["D"][ids[sel, k]] for k in range(2)]
+            xd = [tabs[k]["xi"][ids[sel, k]] for k in range(2)]
+            wd = [tabs[k]["w"][ids[sel, k]] for k in range(2)]
+            q = self.q
+            Lc = sel.shape[0]
+            pts = np.empty((Lc, q, q, 2))
+            for k in range(2):
+                g = lo[k] + (xd[k] + 1.0) / 2.0 * (hi[k] - lo[k])
+                pts[..., k] = _broadcast_axis(g, k, 2, q)
+            inside = geom.contains(pts.reshape(-1, 2))
+            w_in = np.where(inside, _tensor_weights(wd), 0.0)
+            V = _tensor_rows(Vd)
+            DX = _tensor_rows([Dd[0], Vd[1]])
+            DY = _tensor_rows([Vd[0], Dd[1]])
+            ins = {"M": (V * w_in[:, None]).T @ V,
+                   "Kxx": (DX * w_in[:, None]).T @ DX,
+                   "Kyy": (DY * w_in[:, None]).T @ DY,
+                   "Kxy": (DX * w_in[:, None]).T @ DY}
+            for nm in names:
+                acc[(nm, "in")] += ins[nm]
+                acc[(nm, "out")] += full[nm] - ins[nm]
+        return acc
+
+
 def _broadcast_axis(g, k, d, q):
     """(Lc, q) per-axis coordinates broadcast to (Lc, q, ..., q) along axis k."""
     shape = [g.shape[0]] + [1] * d

@@ -90,10 +90,18 @@ def imex_critical_time_step(K, M, d_idx, tol: float = 1e-9, seed: int = 0,
     if d_idx.shape[0] == 0:
         raise ValueError("explicit subsystem is empty")
     if isinstance(K, DeviceOperator):
-        from .imex import _host_stiffness
-        K_dd = _restrict(_host_stiffness(K), d_idx)
-    else:
-        K_dd = _restrict(K, d_idx)
+        # power iteration on the d block inside the operator's own apply
+        from .linalg import max_gen_eig_sub
+        M_dd = _restrict(M, d_idx)
+        if not is_structurally_diagonal(M_dd):
+            raise NotImplementedError("the d mass block must be diagonal")
+        m = np.ones(K.n)
+        m[np.asarray(d_idx, dtype=np.int64)] = sp.csr_matrix(M_dd).diagonal()
+        lam, _ = max_gen_eig_sub(K, m, d_idx, tol=tol, seed=seed)
+        if lam <= 0.0:
+            raise ValueError("largest generalized eigenvalue must be positive")
+        return 2.0 / np.sqrt(lam)
+    K_dd = _restrict(K, d_idx)
     M_dd = _restrict(M, d_idx)
     return _dt_crit(K_dd, M_dd, tol=tol, seed=seed, device=device)
 

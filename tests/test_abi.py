@@ -23,7 +23,7 @@ def test_library_exports_every_symbol():
     lib = _lib.load()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.wcb_abi_version() == 1
+    assert lib.wcb_abi_version() == 2
 
 
 def test_no_device_here_is_reported_not_faked():
