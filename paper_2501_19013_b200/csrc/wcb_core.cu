@@ -2,6 +2,8 @@
 // (src/timeint.py:159-193) and the power iteration (src/linalg.py:89-130).
 #include "wcb_internal.cuh"
 
+#include <mutex>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -245,20 +247,52 @@ int wcb_context_create(int device, wcb_context** out) {
     });
 }
 
+static std::mutex g_ctx_mutex;
+
+static void ctx_teardown(wcb_context* ctx) {
+    Context& x = ctx->c;
+    cudaSetDevice(x.device);
+    cudaStreamSynchronize(x.stream);
+    x.partials.release();
+    x.scalars.release();
+    if (x.h_scalars) cudaFreeHost(x.h_scalars);
+    cudaEventDestroy(x.ev0);
+    cudaEventDestroy(x.ev1);
+    cudaEventDestroy(x.ev2);
+    cudaStreamDestroy(x.stream);
+    delete ctx;
+}
+
+}  // extern "C"
+
+namespace wcb {
+void ctx_retain(Context* ctx) {
+    std::lock_guard<std::mutex> g(g_ctx_mutex);
+    ++ctx->refs;
+}
+void ctx_release(Context* ctx) {
+    bool last = false;
+    {
+        std::lock_guard<std::mutex> g(g_ctx_mutex);
+        last = --ctx->refs == 0 && ctx->closing;
+    }
+    // wcb_context's first member is the Context
+    if (last) ctx_teardown(reinterpret_cast<wcb_context*>(ctx));
+}
+}  // namespace wcb
+
+extern "C" {
+
 int wcb_context_destroy(wcb_context* ctx) {
     if (!ctx) return WCB_OK;
     return guarded([&] {
-        Context& x = ctx->c;
-        cudaSetDevice(x.device);
-        cudaStreamSynchronize(x.stream);
-        x.partials.release();
-        x.scalars.release();
-        if (x.h_scalars) cudaFreeHost(x.h_scalars);
-        cudaEventDestroy(x.ev0);
-        cudaEventDestroy(x.ev1);
-        cudaEventDestroy(x.ev2);
-        cudaStreamDestroy(x.stream);
-        delete ctx;
+        bool now = false;
+        {
+            std::lock_guard<std::mutex> g(g_ctx_mutex);
+            ctx->c.closing = true;
+            now = ctx->c.refs == 0;
+        }
+        if (now) ctx_teardown(ctx);
         return WCB_OK;
     });
 }
@@ -274,6 +308,7 @@ int wcb_operator_csr_create(wcb_context* ctx, int64_t n, const int64_t* indptr,
         WCB_CUDA(cudaSetDevice(ctx->c.device));
         std::unique_ptr<wcb_operator> o(new wcb_operator());
         o->op = make_csr_operator(&ctx->c, n, indptr, indices, data);
+        ctx_retain(o->op->ctx);
         *out = o.release();
         return WCB_OK;
     });
@@ -285,6 +320,7 @@ int wcb_operator_scm_create(wcb_context* ctx, const wcb_scm_desc* desc, wcb_oper
         WCB_CUDA(cudaSetDevice(ctx->c.device));
         std::unique_ptr<wcb_operator> o(new wcb_operator());
         o->op = make_scm_operator(&ctx->c, desc);
+        ctx_retain(o->op->ctx);
         *out = o.release();
         return WCB_OK;
     });
@@ -296,6 +332,7 @@ int wcb_operator_elastic_create(wcb_context* ctx, const wcb_elastic_desc* desc, 
         WCB_CUDA(cudaSetDevice(ctx->c.device));
         std::unique_ptr<wcb_operator> o(new wcb_operator());
         o->op = make_elastic_operator(&ctx->c, desc);
+        ctx_retain(o->op->ctx);
         *out = o.release();
         return WCB_OK;
     });
@@ -304,10 +341,12 @@ int wcb_operator_elastic_create(wcb_context* ctx, const wcb_elastic_desc* desc, 
 int wcb_operator_destroy(wcb_operator* op) {
     if (!op) return WCB_OK;
     return guarded([&] {
-        cudaSetDevice(op->op->ctx->device);
-        cudaStreamSynchronize(op->op->ctx->stream);
+        Context* cx = op->op->ctx;
+        cudaSetDevice(cx->device);
+        cudaStreamSynchronize(cx->stream);
         delete op->op;
         delete op;
+        ctx_release(cx);
         return WCB_OK;
     });
 }
@@ -438,6 +477,7 @@ int wcb_max_gen_eig_sub(wcb_operator* o, const double* m_diag, int64_t n_sub,
 // ============================================================= CDM plan ====
 struct wcb_cdm_plan {
     Operator* op = nullptr;
+    Context* ctx = nullptr;   // retained
     DevBuf<double> m_state, minv;
     DevBuf<double> F_win;
     Source src;
@@ -630,6 +670,7 @@ int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s
                         "diagonal mass has non-positive entries");
         std::unique_ptr<wcb_cdm_plan> P(new wcb_cdm_plan());
         P->op = op;
+        P->ctx = ctx;
         const std::vector<int64_t>& si = op->state_index();
         DevBuf<int64_t> map;
         map.alloc(n, s);
@@ -668,6 +709,7 @@ int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s
             P->obs_val.upload(obs->data, nnz, s);
         }
         WCB_CUDA(cudaStreamSynchronize(s));
+        ctx_retain(ctx);
         *out = P.release();
         return WCB_OK;
     });
@@ -676,9 +718,11 @@ int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s
 int wcb_cdm_plan_destroy(wcb_cdm_plan* plan) {
     if (!plan) return WCB_OK;
     return guarded([&] {
-        cudaSetDevice(plan->op->ctx->device);
-        cudaStreamSynchronize(plan->op->ctx->stream);
+        Context* cx = plan->ctx;
+        cudaSetDevice(cx->device);
+        cudaStreamSynchronize(cx->stream);
         delete plan;
+        ctx_release(cx);
         return WCB_OK;
     });
 }

@@ -155,12 +155,19 @@ __device__ __forceinline__ void cut_cells_warp_e(const Scm2DGeo& g, const double
             const int r = lane + 32 * q;
             if (r < LN) {
                 const double* kt = KT + O * LN + r;
-                #pragma unroll
-                for (int m = 0; m < LN; ++m)
-                    t[q] = fma(__ldg(kt + (int64_t)m * L), c0[(m / N) * UW + (m % N)], t[q]);
-                #pragma unroll
-                for (int m = 0; m < LN; ++m)
-                    t[q] = fma(__ldg(kt + (int64_t)(LN + m) * L), c1[(m / N) * UW + (m % N)], t[q]);
+                // bounded unroll: at most N loads in flight per lane (registers)
+                #pragma unroll 1
+                for (int a0 = 0; a0 < N; ++a0) {
+                    #pragma unroll
+                    for (int b0 = 0; b0 < N; ++b0)
+                        t[q] = fma(__ldg(kt + (int64_t)(a0 * N + b0) * L), c0[a0 * UW + b0], t[q]);
+                }
+                #pragma unroll 1
+                for (int a0 = 0; a0 < N; ++a0) {
+                    #pragma unroll
+                    for (int b0 = 0; b0 < N; ++b0)
+                        t[q] = fma(__ldg(kt + (int64_t)(LN + a0 * N + b0) * L), c1[a0 * UW + b0], t[q]);
+                }
             }
         }
         #pragma unroll
@@ -268,7 +275,7 @@ __device__ __forceinline__ void ela2d_warp(const Scm2DGeo& g, const EMats<P>& mt
 // One CTA per tile (order[] = live tiles, most expensive first).  The state
 // tensor maps cover both component planes: plane 1 is `rows` TMA rows below.
 template <int P, int MODE>
-__global__ void __launch_bounds__(Tile2E<P>::NWARP * 32, (P >= 5 ? 1 : 2)) k_ela2d(
+__global__ void __launch_bounds__(Tile2E<P>::NWARP * 32, 2) k_ela2d(
     const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_prev,
     const __grid_constant__ CUtensorMap tm_minv, Scm2DGeo g, const __grid_constant__ EMats<P> mt,
     int64_t plane, int32_t rows, StepArgs a) {

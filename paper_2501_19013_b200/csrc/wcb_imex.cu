@@ -28,12 +28,149 @@
 
 namespace wcb {
 
+// Level schedule of a triangular factor split by connected component: the
+// c-set of an immersed grid is a union of independent patches (one ring of cut
+// cells per void), and SuperLU keeps them independent, so every component is
+// solved by one CTA with its unknowns in shared memory and one barrier per
+// elimination level -- instead of a device-wide chain of global-memory
+// handshakes.  Entries of a row are visited in the same lane-strided order and
+// reduced by the same shuffle tree as the sync-free kernel (bitwise equal).
+struct TriSched {
+    bool ok = false;
+    int64_t n_comp = 0, max_size = 0, n_levels = 0, max_levels = 0;
+    DevBuf<int32_t> comp_rows;   // n_comp + 1: offsets into rows
+    DevBuf<int32_t> comp_lvl;    // n_comp + 1: offsets into lvl_off
+    DevBuf<int32_t> lvl_off;     // n_levels + 1: offsets into rows
+    DevBuf<int32_t> lvl_ent;     // n_levels + 1: offsets into the packed entries
+    DevBuf<int32_t> rows;        // n: row ids grouped by component, then level
+    DevBuf<int32_t> pos;         // n: local slot of each row in its component
+    // off-diagonal entries packed in schedule order (a level's rows are
+    // contiguous, so the next level can be prefetched with coalesced loads)
+    DevBuf<int32_t> sptr;        // n + 1
+    DevBuf<int32_t> slcol;       // local slot of the column
+    DevBuf<double> sval;
+    DevBuf<double> sdiag;        // n, schedule order
+    size_t smem_bytes() const;
+};
+
+__device__ __forceinline__ uint32_t smem_u32_imex(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+static int64_t uf_find(std::vector<int64_t>& p, int64_t a) {
+    while (p[a] != a) { p[a] = p[p[a]]; a = p[a]; }
+    return a;
+}
+
+// components of the union of both factors' patterns
+static std::vector<int64_t> factor_components(int64_t n, const wcb_lu* lu, int64_t* n_comp) {
+    std::vector<int64_t> par(n);
+    for (int64_t i = 0; i < n; ++i) par[i] = i;
+    for (int f = 0; f < 2; ++f) {
+        const int64_t* ptr = f ? lu->U_indptr : lu->L_indptr;
+        const int32_t* idx = f ? lu->U_indices : lu->L_indices;
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = ptr[i]; j < ptr[i + 1]; ++j) {
+                const int64_t a = uf_find(par, i), b = uf_find(par, idx[j]);
+                if (a != b) par[std::max(a, b)] = std::min(a, b);
+            }
+    }
+    std::vector<int64_t> comp(n), label(n, -1);
+    int64_t nc = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t r = uf_find(par, i);
+        if (label[r] < 0) label[r] = nc++;
+        comp[i] = label[r];
+    }
+    *n_comp = nc;
+    return comp;
+}
+
+static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_t* idx,
+                        const double* val, bool upper,
+                        const std::vector<int64_t>& comp, int64_t n_comp, cudaStream_t s) {
+    std::vector<int32_t> lev(n, 0);
+    auto visit = [&](int64_t i) {
+        int32_t l = 0;
+        for (int64_t j = ptr[i]; j < ptr[i + 1]; ++j)
+            if (idx[j] != i) l = std::max(l, lev[idx[j]] + 1);
+        lev[i] = l;
+    };
+    if (upper) for (int64_t i = n - 1; i >= 0; --i) visit(i);
+    else for (int64_t i = 0; i < n; ++i) visit(i);
+    // order rows by (component, level, row)
+    std::vector<int32_t> order(n);
+    for (int64_t i = 0; i < n; ++i) order[i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+        return comp[a] != comp[b] ? comp[a] < comp[b] : lev[a] < lev[b];
+    });
+    std::vector<int32_t> comp_rows(n_comp + 1, 0), comp_lvl(n_comp + 1, 0), lvl_off, pos(n);
+    int64_t k = 0;
+    T.max_size = 0;
+    for (int64_t c = 0; c < n_comp; ++c) {
+        comp_rows[c] = (int32_t)k;
+        comp_lvl[c] = (int32_t)lvl_off.size();
+        const int64_t start = k;
+        int32_t cur = -1;
+        while (k < n && comp[order[k]] == c) {
+            if (lev[order[k]] != cur) {
+                cur = lev[order[k]];
+                lvl_off.push_back((int32_t)k);
+            }
+            pos[order[k]] = (int32_t)(k - start);
+            ++k;
+        }
+        T.max_size = std::max<int64_t>(T.max_size, k - start);
+    }
+    comp_rows[n_comp] = (int32_t)k;
+    comp_lvl[n_comp] = (int32_t)lvl_off.size();
+    T.max_levels = 0;
+    for (int64_t c = 0; c < n_comp; ++c)
+        T.max_levels = std::max<int64_t>(T.max_levels, comp_lvl[c + 1] - comp_lvl[c]);
+    lvl_off.push_back((int32_t)n);
+    std::vector<int32_t> sptr(n + 1, 0), slcol;
+    std::vector<double> sval, sdiag(n, 0.0);
+    slcol.reserve(ptr[n]);
+    sval.reserve(ptr[n]);
+    for (int64_t k2 = 0; k2 < n; ++k2) {
+        const int64_t i = order[k2];
+        sptr[k2] = (int32_t)slcol.size();
+        for (int64_t j = ptr[i]; j < ptr[i + 1]; ++j) {
+            if (idx[j] == i) {
+                sdiag[k2] = val[j];
+            } else {
+                slcol.push_back(pos[idx[j]]);
+                sval.push_back(val[j]);
+            }
+        }
+    }
+    sptr[n] = (int32_t)slcol.size();
+    if (slcol.empty()) { slcol.push_back(0); sval.push_back(0.0); }
+    T.n_comp = n_comp;
+    T.n_levels = (int64_t)lvl_off.size() - 1;
+    T.comp_rows.alloc(comp_rows.size(), s); T.comp_rows.upload(comp_rows.data(), comp_rows.size(), s);
+    T.comp_lvl.alloc(comp_lvl.size(), s); T.comp_lvl.upload(comp_lvl.data(), comp_lvl.size(), s);
+    T.lvl_off.alloc(lvl_off.size(), s); T.lvl_off.upload(lvl_off.data(), lvl_off.size(), s);
+    T.rows.alloc(n, s); T.rows.upload(order.data(), n, s);
+    T.pos.alloc(n, s); T.pos.upload(pos.data(), n, s);
+    std::vector<int32_t> lvl_ent(lvl_off.size());
+    for (size_t l = 0; l < lvl_off.size(); ++l) lvl_ent[l] = sptr[lvl_off[l]];
+    T.lvl_ent.alloc(lvl_ent.size(), s); T.lvl_ent.upload(lvl_ent.data(), lvl_ent.size(), s);
+    T.sptr.alloc(sptr.size(), s); T.sptr.upload(sptr.data(), sptr.size(), s);
+    T.slcol.alloc(slcol.size(), s); T.slcol.upload(slcol.data(), slcol.size(), s);
+    T.sval.alloc(sval.size(), s); T.sval.upload(sval.data(), sval.size(), s);
+    T.sdiag.alloc(n, s); T.sdiag.upload(sdiag.data(), n, s);
+    WCB_CUDA(cudaStreamSynchronize(s));   // host vectors die here
+    T.ok = T.smem_bytes() <= 220 * 1024;
+}
+
 struct DevLU {
     int64_t n = 0;
     DevBuf<int64_t> perm_r, perm_c;
     DevBuf<int64_t> Lp, Up;
     DevBuf<int32_t> Li, Ui;
     DevBuf<double> Lx, Ux;
+    TriSched Ls, Us;
     void load(const wcb_lu* lu, cudaStream_t s) {
         n = lu->n;
         perm_r.alloc(std::max<int64_t>(n, 1), s);
@@ -47,6 +184,12 @@ struct DevLU {
         Ui.alloc(std::max<int64_t>(nu, 1), s); Ui.upload(lu->U_indices, nu, s);
         Lx.alloc(std::max<int64_t>(nl, 1), s); Lx.upload(lu->L_data, nl, s);
         Ux.alloc(std::max<int64_t>(nu, 1), s); Ux.upload(lu->U_data, nu, s);
+        if (n > 0 && !getenv("WAVECELL_B200_SYNCFREE_TRSV")) {
+            int64_t nc = 0;
+            const std::vector<int64_t> comp = factor_components(n, lu, &nc);
+            build_sched(Ls, n, lu->L_indptr, lu->L_indices, lu->L_data, false, comp, nc, s);
+            build_sched(Us, n, lu->U_indptr, lu->U_indices, lu->U_data, true, comp, nc, s);
+        }
     }
 };
 
@@ -94,6 +237,108 @@ __global__ void k_sptrsv(int64_t n, const int64_t* __restrict__ ptr, const int32
         }
         __syncwarp();
     }
+}
+
+// Component-local level-scheduled solve (see TriSched): one CTA per
+// component, unknowns in shared memory (b read in place of x).  While a level
+// is solved, every warp already holds its row of the next level in registers
+// (values and column slots do not depend on x), so a level costs one barrier
+// plus shared-memory FMAs.  Fixed lane order and shuffle tree: deterministic.
+// Level data staged into a shared-memory ring by cp.async, TRSV_D levels
+// ahead: a level's rows are contiguous in schedule order, so its packed
+// entries (values, column slots), row starts and diagonals are four
+// contiguous ranges.  Levels too large for a ring slot read global memory.
+constexpr int TRSV_D = 4;               // ring depth (levels in flight)
+constexpr int TRSV_SLOT_E = 1536;       // entries per slot
+constexpr int TRSV_SLOT_R = 256;        // rows per slot
+
+struct TrsvSlot {
+    double v[TRSV_SLOT_E];
+    double d[TRSV_SLOT_R];
+    int c[TRSV_SLOT_E];
+    int p[TRSV_SLOT_R + 1];
+};
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32_imex(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32_imex(dst)), "l"(src) : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_trsv_comp(
+    const int32_t* __restrict__ comp_rows, const int32_t* __restrict__ comp_lvl,
+    const int32_t* __restrict__ lvl_off, const int32_t* __restrict__ lvl_ent, const int32_t* __restrict__ rows,
+    const int32_t* __restrict__ sptr, const int32_t* __restrict__ slcol,
+    const double* __restrict__ sval, const double* __restrict__ sdiag, const double* __restrict__ b,
+    double* __restrict__ x, int max_size, int max_levels) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    TrsvSlot* ring = reinterpret_cast<TrsvSlot*>(smraw);
+    double* xl = reinterpret_cast<double*>(smraw + sizeof(TrsvSlot) * TRSV_D);
+    int* lo = reinterpret_cast<int*>(xl + max_size);   // this component's level offsets
+    int* le = lo + max_levels + 1;                     // and entry offsets
+    const int c = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
+    const int l0 = comp_lvl[c], nl = comp_lvl[c + 1] - l0;
+    for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) xl[k - r0] = b[rows[k]];
+    for (int l = threadIdx.x; l <= nl; l += blockDim.x) {
+        lo[l] = lvl_off[l0 + l];
+        le[l] = lvl_ent[l0 + l];
+    }
+    __syncthreads();
+    auto fits = [&](int l) {
+        return lo[l + 1] - lo[l] <= TRSV_SLOT_R && le[l + 1] - le[l] <= TRSV_SLOT_E;
+    };
+    auto stage = [&](int l) {
+        if (l < nl && fits(l)) {
+            TrsvSlot& S = ring[l % TRSV_D];
+            const int a = lo[l], e = lo[l + 1];
+            const int pa = le[l], pe = le[l + 1];
+            for (int k = threadIdx.x; k <= e - a; k += blockDim.x) cp_async4(&S.p[k], sptr + a + k);
+            for (int k = threadIdx.x; k < e - a; k += blockDim.x) cp_async8(&S.d[k], sdiag + a + k);
+            for (int j = threadIdx.x; j < pe - pa; j += blockDim.x) {
+                cp_async8(&S.v[j], sval + pa + j);
+                cp_async4(&S.c[j], slcol + pa + j);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    #pragma unroll
+    for (int l = 0; l < TRSV_D - 1; ++l) stage(l);
+    for (int l = 0; l < nl; ++l) {
+        stage(l + TRSV_D - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(TRSV_D - 1) : "memory");
+        __syncthreads();
+        const int a = lo[l], e = lo[l + 1];
+        if (fits(l)) {
+            const TrsvSlot& S = ring[l % TRSV_D];
+            const int base = S.p[0];
+            for (int k = warp; k < e - a; k += nw) {
+                const int p0 = S.p[k] - base, p1 = S.p[k + 1] - base;
+                double sacc = 0.0;
+                for (int j = p0 + lane; j < p1; j += 32) sacc = fma(S.v[j], xl[S.c[j]], sacc);
+                #pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
+                if (lane == 0) xl[a + k - r0] = (xl[a + k - r0] - sacc) / S.d[k];
+            }
+        } else {
+            for (int k = a + warp; k < e; k += nw) {
+                double sacc = 0.0;
+                for (int j = sptr[k] + lane; j < sptr[k + 1]; j += 32) sacc = fma(sval[j], xl[slcol[j]], sacc);
+                #pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
+                if (lane == 0) xl[k - r0] = (xl[k - r0] - sacc) / sdiag[k];
+            }
+        }
+        __syncthreads();   // level done; its ring slot may be refilled next iteration
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) x[rows[k]] = xl[k - r0];
+}
+
+size_t TriSched::smem_bytes() const {
+    return sizeof(TrsvSlot) * TRSV_D + (size_t)max_size * 8 + (size_t)(max_levels + 1) * 8;
 }
 
 // y[perm_r[i]] = b[i]   (row permutation of SuperLU: Pr A Pc = L U)
@@ -169,6 +414,7 @@ using namespace wcb;
 
 struct wcb_imex_plan {
     Operator* op = nullptr;
+    Context* ctx = nullptr;   // retained
     int64_t n_c = 0, n_d = 0;
     DevBuf<int64_t> c_state;          // state index of each c DOF (c order)
     DevBuf<int64_t> c_compact;
@@ -200,6 +446,24 @@ static void lu_solve(Context* ctx, wcb_imex_plan* P, DevLU& F, const double* b, 
     if (!n) return;
     k_perm_rows<<<grid1(ctx, n), 256, 0, s>>>(n, F.perm_r.p, b, P->y.p);
     // forward: L w = y  (into z), backward: U v = w (into y)
+    if (F.Ls.ok && F.Us.ok) {
+        static bool attr = false;
+        if (!attr) {
+            WCB_CUDA(cudaFuncSetAttribute(k_trsv_comp, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            attr = true;
+        }
+        k_trsv_comp<<<(unsigned)F.Ls.n_comp, 256, F.Ls.smem_bytes(), s>>>(
+            F.Ls.comp_rows.p, F.Ls.comp_lvl.p, F.Ls.lvl_off.p, F.Ls.lvl_ent.p, F.Ls.rows.p, F.Ls.sptr.p,
+            F.Ls.slcol.p, F.Ls.sval.p, F.Ls.sdiag.p, P->y.p, P->z.p, (int)F.Ls.max_size,
+            (int)F.Ls.max_levels);
+        k_trsv_comp<<<(unsigned)F.Us.n_comp, 256, F.Us.smem_bytes(), s>>>(
+            F.Us.comp_rows.p, F.Us.comp_lvl.p, F.Us.lvl_off.p, F.Us.lvl_ent.p, F.Us.rows.p, F.Us.sptr.p,
+            F.Us.slcol.p, F.Us.sval.p, F.Us.sdiag.p, P->z.p, x, (int)F.Us.max_size,
+            (int)F.Us.max_levels);
+        ctx->launches += 3;
+        WCB_CHECK_LAUNCH();
+        return;
+    }
     WCB_CUDA(cudaMemsetAsync(P->done.p, 0, n * sizeof(int), s));
     WCB_CUDA(cudaMemsetAsync(P->counter.p, 0, 2 * sizeof(unsigned long long), s));
     const int blocks = (int)std::min<int64_t>(ceil_div(n, 8), (int64_t)ctx->sm_count * 16);
@@ -227,6 +491,7 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
         WCB_REQUIRE(n_c + n_d == n, "c and d index sets must partition the DOFs");
         std::unique_ptr<wcb_imex_plan> P(new wcb_imex_plan());
         P->op = op;
+        P->ctx = ctx;
         P->n_c = n_c;
         P->n_d = n_d;
         const std::vector<int64_t>& si = op->state_index();
@@ -284,6 +549,7 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
         P->done.alloc(m, s);
         P->counter.alloc(2, s);
         WCB_CUDA(cudaStreamSynchronize(s));
+        ctx_retain(ctx);
         *out = P.release();
         return WCB_OK;
     } catch (const Error& e) {
@@ -294,9 +560,11 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
 
 int wcb_imex_plan_destroy(wcb_imex_plan* plan) {
     if (!plan) return WCB_OK;
-    cudaSetDevice(plan->op->ctx->device);
-    cudaStreamSynchronize(plan->op->ctx->stream);
+    Context* cx = plan->ctx;
+    cudaSetDevice(cx->device);
+    cudaStreamSynchronize(cx->stream);
     delete plan;
+    ctx_release(cx);
     return WCB_OK;
 }
 

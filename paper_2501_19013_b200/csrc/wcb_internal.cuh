@@ -101,6 +101,10 @@ struct DevBuf {
 // ---------------------------------------------------------------- context ----
 struct Nccl;
 struct Context {
+    // lifetime: operators and plans retain their context; wcb_context_destroy
+    // only marks it closing while they live (the last release tears it down)
+    int refs = 0;
+    bool closing = false;
     Nccl* nccl = nullptr;   // slab decomposition communicator (wcb_dist_init)
     int device = 0;
     int sm_count = 148;
@@ -257,6 +261,9 @@ struct Operator {
         return false;
     }
 };
+
+void ctx_retain(Context* ctx);
+void ctx_release(Context* ctx);
 
 // NCCL (loaded with dlopen on first use; the library does not link it)
 struct Nccl;

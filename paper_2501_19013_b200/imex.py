@@ -76,86 +76,121 @@ def _host_stiffness(K):
     return sp.csr_matrix(K)
 
 
-def imex_run(M, K, F_s, f_t, dt: float, n_t: int, c_idx, d_idx, obs_mat=None,
-             beta: float = 0.25, gamma: float = 0.5, psi0=None, v0=None,
-             device: int | None = None) -> RunResult:
-    """Implicit-explicit split integration, src/timeint.py:196-292, on the device."""
-    M = sp.csr_matrix(M)
-    n = M.shape[0]
-    c_idx = np.asarray(c_idx, dtype=np.int64)
-    d_idx = np.asarray(d_idx, dtype=np.int64)
-    if c_idx.shape[0] + d_idx.shape[0] != n:
-        raise ValueError("c and d index sets must partition the DOFs")
-    dt = float(dt)
-    n_t = int(n_t)
-    has_d, has_c = d_idx.shape[0] > 0, c_idx.shape[0] > 0
-    timings = StageTimings()
-    t0 = time.perf_counter()
-    m_d = np.zeros(0)
-    if has_d:
-        M_drows = M[d_idx]
-        if M_drows[:, c_idx].nnz != 0:
-            raise ValueError("d mass rows couple into the implicit set; the basis/lumping "
-                             "choice does not support the implicit-explicit split")
-        M_dd = M_drows[:, d_idx]
-        if not is_structurally_diagonal(M_dd):
-            raise ValueError("d mass block is not diagonal; the basis/lumping choice does not "
-                             "support the implicit-explicit split")
-        m_d = np.ascontiguousarray(M_dd.diagonal(), dtype=np.float64)
-        if np.any(m_d <= 0.0):
-            raise ValueError("d mass block has non-positive diagonal entries")
-    S_lu = M_lu = None
-    if has_c:
-        M_cc = M[c_idx][:, c_idx]
-        prob = getattr(K, "problem", None)
-        if isinstance(K, DeviceOperator) and hasattr(prob, "stiffness_block"):
-            K_cc = prob.stiffness_block(c_idx)       # from the cells touching c only
-        else:
-            K_cc = _host_stiffness(K)[c_idx][:, c_idx]
-        S_lu = _LU(_splu((M_cc + (beta * dt * dt) * K_cc).tocsr()))
-        M_lu = _LU(_splu(M_cc))
-    timings.factorization = time.perf_counter() - t0
-    op = as_device_operator(K, device=device)
-    if op.n != n:
-        raise ValueError("K and M sizes differ")
-    F = np.ascontiguousarray(np.asarray(F_s, dtype=np.float64).reshape(-1))
-    obs, keep = _observer(obs_mat, n)
-    lib = _lib.load()
-    h = _lib.C.c_void_p()
-    ci = np.ascontiguousarray(c_idx)
-    di = np.ascontiguousarray(d_idx)
-    _lib.check(lib.wcb_imex_plan_create(
-        op.handle, ci.shape[0], _lib.i64ptr(ci) if has_c else None, di.shape[0],
-        _lib.i64ptr(di) if has_d else None, _lib.dptr(m_d) if has_d else None,
-        _lib.C.byref(S_lu.struct) if has_c else None,
-        _lib.C.byref(M_lu.struct) if has_c else None, _lib.dptr(F),
-        _lib.C.byref(obs) if obs is not None else None, _lib.C.byref(h)))
-    try:
+class ImexPlan:
+    """Device-resident IMEX split for repeated runs at one ``(dt, beta)``:
+    validation and SuperLU factorisation of ``S_cc`` / ``M_cc`` happen once
+    (src/timeint.py:210-245), ``run`` is the stepping loop (:246-292)."""
+
+    def __init__(self, M, K, F_s, dt: float, c_idx, d_idx, obs_mat=None, beta: float = 0.25,
+                 device: int | None = None):
+        M = sp.csr_matrix(M)
+        n = M.shape[0]
+        c_idx = np.asarray(c_idx, dtype=np.int64)
+        d_idx = np.asarray(d_idx, dtype=np.int64)
+        if c_idx.shape[0] + d_idx.shape[0] != n:
+            raise ValueError("c and d index sets must partition the DOFs")
+        self.dt = float(dt)
+        self.beta = float(beta)
+        self.n = n
+        has_d, has_c = d_idx.shape[0] > 0, c_idx.shape[0] > 0
+        self.has_c, self.has_d = has_c, has_d
+        self.c_idx = c_idx
+        t0 = time.perf_counter()
+        m_d = np.zeros(0)
+        if has_d:
+            M_drows = M[d_idx]
+            if M_drows[:, c_idx].nnz != 0:
+                raise ValueError("d mass rows couple into the implicit set; the basis/lumping "
+                                 "choice does not support the implicit-explicit split")
+            M_dd = M_drows[:, d_idx]
+            if not is_structurally_diagonal(M_dd):
+                raise ValueError("d mass block is not diagonal; the basis/lumping choice does "
+                                 "not support the implicit-explicit split")
+            m_d = np.ascontiguousarray(M_dd.diagonal(), dtype=np.float64)
+            if np.any(m_d <= 0.0):
+                raise ValueError("d mass block has non-positive diagonal entries")
+        S_lu = M_lu = None
+        if has_c:
+            M_cc = M[c_idx][:, c_idx]
+            prob = getattr(K, "problem", None)
+            if isinstance(K, DeviceOperator) and hasattr(prob, "stiffness_block"):
+                K_cc = prob.stiffness_block(c_idx)       # from the cells touching c only
+            else:
+                K_cc = _host_stiffness(K)[c_idx][:, c_idx]
+            S_lu = _LU(_splu((M_cc + (self.beta * self.dt * self.dt) * K_cc).tocsr()))
+            M_lu = _LU(_splu(M_cc))
+        self.factorization = time.perf_counter() - t0
+        self.fact_nnz = 0 if S_lu is None else int(S_lu.keep[4].shape[0] + S_lu.keep[7].shape[0])
+        op = as_device_operator(K, device=device)
+        if op.n != n:
+            raise ValueError("K and M sizes differ")
+        self.op = op
+        F = np.ascontiguousarray(np.asarray(F_s, dtype=np.float64).reshape(-1))
+        obs, self._obs_keep = _observer(obs_mat, n)
+        self.n_obs = 0 if obs is None else int(obs.n_obs)
+        ci = np.ascontiguousarray(c_idx)
+        di = np.ascontiguousarray(d_idx)
+        h = _lib.C.c_void_p()
+        _lib.check(_lib.load().wcb_imex_plan_create(
+            op.handle, ci.shape[0], _lib.i64ptr(ci) if has_c else None, di.shape[0],
+            _lib.i64ptr(di) if has_d else None, _lib.dptr(m_d) if has_d else None,
+            _lib.C.byref(S_lu.struct) if has_c else None,
+            _lib.C.byref(M_lu.struct) if has_c else None, _lib.dptr(F),
+            _lib.C.byref(obs) if obs is not None else None, _lib.C.byref(h)))
+        self._h = h
+        del S_lu, M_lu    # uploaded; the host factors are not needed any more
+
+    def run(self, f_t, n_t: int, gamma: float = 0.5, psi0=None, v0=None,
+            record: bool = True) -> RunResult:
+        n_t = int(n_t)
+        dt = self.dt
+        n = self.n
         f0 = float(f_t(0.0))
         ft_k = np.array([float(f_t(k * dt)) for k in range(n_t)] or [0.0])
         ft_new = np.array([float(f_t(k * dt + dt)) for k in range(n_t)] or [0.0])
         p0 = None if psi0 is None else np.ascontiguousarray(np.array(psi0, dtype=float).reshape(-1))
         q0 = None if v0 is None else np.ascontiguousarray(np.array(v0, dtype=float).reshape(-1))
         psi = np.empty(n)
-        vc = np.empty(max(ci.shape[0], 1))
-        n_obs = 0 if obs is None else int(obs.n_obs)
-        obs_out = np.empty((n_obs, n_t + 1)) if n_obs else None
+        nc = self.c_idx.shape[0]
+        vc = np.empty(max(nc, 1))
+        obs_out = np.empty((self.n_obs, n_t + 1)) if (self.n_obs and record) else None
         div = _lib.Divergence()
         tm = _lib.Timings()
-        code = lib.wcb_imex_plan_run(h, f0, _lib.dptr(ft_k), _lib.dptr(ft_new), dt, n_t,
-                                     float(beta), float(gamma), _lib.dptr(p0), _lib.dptr(q0),
-                                     _lib.dptr(psi), _lib.dptr(vc) if has_c else None,
-                                     _lib.dptr(obs_out) if obs_out is not None else None,
-                                     _lib.C.byref(div), _lib.C.byref(tm))
+        code = _lib.load().wcb_imex_plan_run(
+            self._h, f0, _lib.dptr(ft_k), _lib.dptr(ft_new), dt, n_t, self.beta, float(gamma),
+            _lib.dptr(p0), _lib.dptr(q0), _lib.dptr(psi), _lib.dptr(vc) if self.has_c else None,
+            _lib.dptr(obs_out) if obs_out is not None else None,
+            _lib.C.byref(div), _lib.C.byref(tm))
         if code == _lib.WCB_E_DIVERGED:
             raise DivergenceError(int(div.step), float(div.amplitude))
         _lib.check(code)
+        v_out = None
+        if self.has_c and not self.has_d:
+            v_out = np.zeros(n)
+            v_out[self.c_idx] = vc[:nc]
+        timings = StageTimings(factorization=self.factorization, rhs=float(tm.rhs),
+                               backward_insertion=float(tm.backward_insertion))
+        return RunResult(method="imex", dt=dt, t=np.arange(n_t + 1) * dt, obs=obs_out, psi=psi,
+                         psi_dot=v_out, timings=timings, fact_dim=int(nc))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().wcb_imex_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def imex_run(M, K, F_s, f_t, dt: float, n_t: int, c_idx, d_idx, obs_mat=None,
+             beta: float = 0.25, gamma: float = 0.5, psi0=None, v0=None,
+             device: int | None = None) -> RunResult:
+    """Implicit-explicit split integration, src/timeint.py:196-292, on the device."""
+    plan = ImexPlan(M, K, F_s, dt, c_idx, d_idx, obs_mat=obs_mat, beta=beta, device=device)
+    try:
+        return plan.run(f_t, n_t, gamma=gamma, psi0=psi0, v0=v0)
     finally:
-        lib.wcb_imex_plan_destroy(h)
-    v_out = None
-    if has_c and not has_d:
-        v_out = np.zeros(n)
-        v_out[c_idx] = vc[:c_idx.shape[0]]
-    timings.rhs = float(tm.rhs)
-    return RunResult(method="imex", dt=dt, t=np.arange(n_t + 1) * dt, obs=obs_out, psi=psi,
-                     psi_dot=v_out, timings=timings, fact_dim=int(c_idx.shape[0]))
+        plan.close()
