@@ -35,9 +35,15 @@ namespace wcb {
 // elimination level -- instead of a device-wide chain of global-memory
 // handshakes.  Entries of a row are visited in the same lane-strided order and
 // reduced by the same shuffle tree as the sync-free kernel (bitwise equal).
+constexpr int TRSV_D = 3;                 // ring depth (levels in flight)
+constexpr int TRSV_SMEM = 220 * 1024;     // dynamic shared memory budget
+constexpr int TRSV_THREADS = 512;
+
 struct TriSched {
     bool ok = false;
     int64_t n_comp = 0, max_size = 0, n_levels = 0, max_levels = 0;
+    int64_t max_lvl_rows = 0, max_lvl_ent = 0;   // widest level
+    int slot_e = 0, slot_r = 0;                  // ring slot capacities (entries, rows)
     DevBuf<int32_t> comp_rows;   // n_comp + 1: offsets into rows
     DevBuf<int32_t> comp_lvl;    // n_comp + 1: offsets into lvl_off
     DevBuf<int32_t> lvl_off;     // n_levels + 1: offsets into rows
@@ -155,13 +161,24 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
     T.pos.alloc(n, s); T.pos.upload(pos.data(), n, s);
     std::vector<int32_t> lvl_ent(lvl_off.size());
     for (size_t l = 0; l < lvl_off.size(); ++l) lvl_ent[l] = sptr[lvl_off[l]];
+    T.max_lvl_rows = T.max_lvl_ent = 0;
+    for (size_t l = 0; l + 1 < lvl_off.size(); ++l) {
+        T.max_lvl_rows = std::max<int64_t>(T.max_lvl_rows, lvl_off[l + 1] - lvl_off[l]);
+        T.max_lvl_ent = std::max<int64_t>(T.max_lvl_ent, lvl_ent[l + 1] - lvl_ent[l]);
+    }
     T.lvl_ent.alloc(lvl_ent.size(), s); T.lvl_ent.upload(lvl_ent.data(), lvl_ent.size(), s);
     T.sptr.alloc(sptr.size(), s); T.sptr.upload(sptr.data(), sptr.size(), s);
     T.slcol.alloc(slcol.size(), s); T.slcol.upload(slcol.data(), slcol.size(), s);
     T.sval.alloc(sval.size(), s); T.sval.upload(sval.data(), sval.size(), s);
     T.sdiag.alloc(n, s); T.sdiag.upload(sdiag.data(), n, s);
     WCB_CUDA(cudaStreamSynchronize(s));   // host vectors die here
-    T.ok = T.smem_bytes() <= 220 * 1024;
+    // ring slots as large as the widest level allows within the smem budget
+    const int64_t fixed = T.max_size * 8 + (T.max_levels + 1) * 8 + 64;
+    const int64_t avail = (int64_t)TRSV_SMEM - fixed;
+    T.slot_r = (int)std::min<int64_t>(std::max<int64_t>(T.max_lvl_rows, 1), 1024);
+    const int64_t per = avail / TRSV_D - (int64_t)T.slot_r * 12 - 32;
+    T.slot_e = (int)std::max<int64_t>(0, std::min<int64_t>(std::max<int64_t>(T.max_lvl_ent, 1), per / 12));
+    T.ok = avail > 0 && T.slot_e >= 256;
 }
 
 struct DevLU {
@@ -248,16 +265,6 @@ __global__ void k_sptrsv(int64_t n, const int64_t* __restrict__ ptr, const int32
 // ahead: a level's rows are contiguous in schedule order, so its packed
 // entries (values, column slots), row starts and diagonals are four
 // contiguous ranges.  Levels too large for a ring slot read global memory.
-constexpr int TRSV_D = 4;               // ring depth (levels in flight)
-constexpr int TRSV_SLOT_E = 1536;       // entries per slot
-constexpr int TRSV_SLOT_R = 256;        // rows per slot
-
-struct TrsvSlot {
-    double v[TRSV_SLOT_E];
-    double d[TRSV_SLOT_R];
-    int c[TRSV_SLOT_E];
-    int p[TRSV_SLOT_R + 1];
-};
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32_imex(dst)), "l"(src) : "memory");
@@ -266,17 +273,23 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32_imex(dst)), "l"(src) : "memory");
 }
 
-__global__ void __launch_bounds__(256) k_trsv_comp(
+static __host__ __device__ inline size_t trsv_slot_bytes(int e, int r);
+
+__global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
     const int32_t* __restrict__ comp_rows, const int32_t* __restrict__ comp_lvl,
     const int32_t* __restrict__ lvl_off, const int32_t* __restrict__ lvl_ent, const int32_t* __restrict__ rows,
     const int32_t* __restrict__ sptr, const int32_t* __restrict__ slcol,
     const double* __restrict__ sval, const double* __restrict__ sdiag, const double* __restrict__ b,
-    double* __restrict__ x, int max_size, int max_levels) {
+    double* __restrict__ x, int max_size, int max_levels, int slot_e, int slot_r) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    TrsvSlot* ring = reinterpret_cast<TrsvSlot*>(smraw);
-    double* xl = reinterpret_cast<double*>(smraw + sizeof(TrsvSlot) * TRSV_D);
+    const size_t sb = trsv_slot_bytes(slot_e, slot_r);
+    double* xl = reinterpret_cast<double*>(smraw + sb * TRSV_D);
     int* lo = reinterpret_cast<int*>(xl + max_size);   // this component's level offsets
     int* le = lo + max_levels + 1;                     // and entry offsets
+    auto sv = [&](int l) { return reinterpret_cast<double*>(smraw + sb * (l % TRSV_D)); };
+    auto sd = [&](int l) { return sv(l) + slot_e; };
+    auto sc = [&](int l) { return reinterpret_cast<int*>(sd(l) + slot_r); };
+    auto sp = [&](int l) { return sc(l) + slot_e; };
     const int c = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
@@ -287,19 +300,20 @@ __global__ void __launch_bounds__(256) k_trsv_comp(
         le[l] = lvl_ent[l0 + l];
     }
     __syncthreads();
-    auto fits = [&](int l) {
-        return lo[l + 1] - lo[l] <= TRSV_SLOT_R && le[l + 1] - le[l] <= TRSV_SLOT_E;
-    };
+    auto fits = [&](int l) { return lo[l + 1] - lo[l] <= slot_r && le[l + 1] - le[l] <= slot_e; };
     auto stage = [&](int l) {
         if (l < nl && fits(l)) {
-            TrsvSlot& S = ring[l % TRSV_D];
             const int a = lo[l], e = lo[l + 1];
             const int pa = le[l], pe = le[l + 1];
-            for (int k = threadIdx.x; k <= e - a; k += blockDim.x) cp_async4(&S.p[k], sptr + a + k);
-            for (int k = threadIdx.x; k < e - a; k += blockDim.x) cp_async8(&S.d[k], sdiag + a + k);
+            int* P = sp(l);
+            double* D = sd(l);
+            double* V = sv(l);
+            int* C = sc(l);
+            for (int k = threadIdx.x; k <= e - a; k += blockDim.x) cp_async4(P + k, sptr + a + k);
+            for (int k = threadIdx.x; k < e - a; k += blockDim.x) cp_async8(D + k, sdiag + a + k);
             for (int j = threadIdx.x; j < pe - pa; j += blockDim.x) {
-                cp_async8(&S.v[j], sval + pa + j);
-                cp_async4(&S.c[j], slcol + pa + j);
+                cp_async8(V + j, sval + pa + j);
+                cp_async4(C + j, slcol + pa + j);
             }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -312,15 +326,18 @@ __global__ void __launch_bounds__(256) k_trsv_comp(
         __syncthreads();
         const int a = lo[l], e = lo[l + 1];
         if (fits(l)) {
-            const TrsvSlot& S = ring[l % TRSV_D];
-            const int base = S.p[0];
+            const int* P = sp(l);
+            const double* D = sd(l);
+            const double* V = sv(l);
+            const int* C = sc(l);
+            const int base = P[0];
             for (int k = warp; k < e - a; k += nw) {
-                const int p0 = S.p[k] - base, p1 = S.p[k + 1] - base;
+                const int p0 = P[k] - base, p1 = P[k + 1] - base;
                 double sacc = 0.0;
-                for (int j = p0 + lane; j < p1; j += 32) sacc = fma(S.v[j], xl[S.c[j]], sacc);
+                for (int j = p0 + lane; j < p1; j += 32) sacc = fma(V[j], xl[C[j]], sacc);
                 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
-                if (lane == 0) xl[a + k - r0] = (xl[a + k - r0] - sacc) / S.d[k];
+                if (lane == 0) xl[a + k - r0] = (xl[a + k - r0] - sacc) / D[k];
             }
         } else {
             for (int k = a + warp; k < e; k += nw) {
@@ -337,8 +354,11 @@ __global__ void __launch_bounds__(256) k_trsv_comp(
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) x[rows[k]] = xl[k - r0];
 }
 
+static __host__ __device__ inline size_t trsv_slot_bytes(int e, int r) {
+    return (((size_t)e * 12 + (size_t)r * 8 + (size_t)(r + 1) * 4) + 15) / 16 * 16;
+}
 size_t TriSched::smem_bytes() const {
-    return sizeof(TrsvSlot) * TRSV_D + (size_t)max_size * 8 + (size_t)(max_levels + 1) * 8;
+    return trsv_slot_bytes(slot_e, slot_r) * TRSV_D + (size_t)max_size * 8 + (size_t)(max_levels + 1) * 8;
 }
 
 // y[perm_r[i]] = b[i]   (row permutation of SuperLU: Pr A Pc = L U)
@@ -449,17 +469,17 @@ static void lu_solve(Context* ctx, wcb_imex_plan* P, DevLU& F, const double* b, 
     if (F.Ls.ok && F.Us.ok) {
         static bool attr = false;
         if (!attr) {
-            WCB_CUDA(cudaFuncSetAttribute(k_trsv_comp, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            WCB_CUDA(cudaFuncSetAttribute(k_trsv_comp, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSV_SMEM));
             attr = true;
         }
-        k_trsv_comp<<<(unsigned)F.Ls.n_comp, 256, F.Ls.smem_bytes(), s>>>(
+        k_trsv_comp<<<(unsigned)F.Ls.n_comp, TRSV_THREADS, F.Ls.smem_bytes(), s>>>(
             F.Ls.comp_rows.p, F.Ls.comp_lvl.p, F.Ls.lvl_off.p, F.Ls.lvl_ent.p, F.Ls.rows.p, F.Ls.sptr.p,
             F.Ls.slcol.p, F.Ls.sval.p, F.Ls.sdiag.p, P->y.p, P->z.p, (int)F.Ls.max_size,
-            (int)F.Ls.max_levels);
-        k_trsv_comp<<<(unsigned)F.Us.n_comp, 256, F.Us.smem_bytes(), s>>>(
+            (int)F.Ls.max_levels, F.Ls.slot_e, F.Ls.slot_r);
+        k_trsv_comp<<<(unsigned)F.Us.n_comp, TRSV_THREADS, F.Us.smem_bytes(), s>>>(
             F.Us.comp_rows.p, F.Us.comp_lvl.p, F.Us.lvl_off.p, F.Us.lvl_ent.p, F.Us.rows.p, F.Us.sptr.p,
             F.Us.slcol.p, F.Us.sval.p, F.Us.sdiag.p, P->z.p, x, (int)F.Us.max_size,
-            (int)F.Us.max_levels);
+            (int)F.Us.max_levels, F.Us.slot_e, F.Us.slot_r);
         ctx->launches += 3;
         WCB_CHECK_LAUNCH();
         return;
@@ -518,6 +538,7 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
         P->m_d_state.alloc(ns, s); P->m_d_state.upload(md.data(), ns, s);
         P->c_state.alloc(cs.size(), s); P->c_state.upload(cs.data(), n_c, s);
         P->Fc.alloc(Fc.size(), s); P->Fc.upload(Fc.data(), n_c, s);
+        if (n_c) op->set_apply_subset(c_idx, n_c);   // K rows of c only, per step
         // force vector for the d rows: dense window over its nonzeros
         {
             std::vector<std::pair<int64_t, double>> nz;
@@ -681,7 +702,7 @@ int wcb_imex_plan_run(wcb_imex_plan* P, double f0, const double* ft_k, const dou
                 k_c_predict<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->psi_c.p, P->v_c.p, P->a_c.p,
                                                            dt, c1, c2, prev, P->pred.p, P->vpred.p);
                 // 3. rhs_c with updated d and predicted c
-                op->apply(prev, P->T.p);
+                op->apply_subset(prev, P->T.p);   // tiles owning c rows only
                 k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
                 k_c_rhs<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->Fc.p, P->ft_new.p, k, P->Kc.p, P->rhs.p);
                 ctx->launches += 3;

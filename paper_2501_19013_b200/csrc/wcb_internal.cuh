@@ -252,6 +252,10 @@ struct Operator {
     virtual void apply(const double* d_x, double* d_y) = 0;
     // fused explicit step
     virtual void cdm_step(const StepArgs& a) = 0;
+    // y = K x at (at least) the rows of a DOF subset fixed beforehand by
+    // set_apply_subset (other rows of y are unspecified); default: full apply
+    virtual bool set_apply_subset(const int64_t* /*compact_ids*/, int64_t /*n*/) { return false; }
+    virtual void apply_subset(const double* x, double* y) { apply(x, y); }
     // algorithmic bytes of one fused step (for the roofline)
     virtual double step_bytes() const = 0;
     // slab halo layout (state rows of out[0] doubles), see wcb_operator_halo;

@@ -410,6 +410,10 @@ struct ScmOperator final : Operator {
     DevBuf<double> KT;
     DevBuf<int32_t> order;        // 2D tile kernel: live tiles, most expensive first
     int64_t n_order = 0;
+    // apply restricted to the tiles owning a given DOF subset (IMEX c rows)
+    DevBuf<int32_t> order_sub;
+    int64_t n_order_sub = 0;
+    bool sub_ready = false, sub_active = false;
     int64_t n_strips = 0, n_rtiles = 0;
     std::vector<double> m1, k1;
     double sk = 1.0;
@@ -454,9 +458,11 @@ struct ScmOperator final : Operator {
                     mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
-        if (!n_order) return;
-        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, order.p, n_strips, n_rtiles, pitch};
-        dim3 grid((unsigned)n_order);
+        const int32_t* ord = sub_active ? order_sub.p : order.p;
+        const int64_t n_ord = sub_active ? n_order_sub : n_order;
+        if (!n_ord) return;
+        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, ord, n_strips, n_rtiles, pitch};
+        dim3 grid((unsigned)n_ord);
         const CUtensorMap& mu = state_map<P>(a.cur);
         const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
         const CUtensorMap& mp = epi ? state_map<P>(a.prev, 1) : mu;
@@ -483,7 +489,9 @@ struct ScmOperator final : Operator {
                                           (int)T::SMEM));
             attr_set = true;
         }
-        if (!n_order) return;
+        const int32_t* ord = sub_active ? order_sub.p : order.p;
+        const int64_t n_ord = sub_active ? n_order_sub : n_order;
+        if (!n_ord) return;
         constexpr int N = P + 1;
         EMats<P> mt;
         const double l2m = lam + 2.0 * mu;
@@ -502,12 +510,12 @@ struct ScmOperator final : Operator {
                 mt.xa[1][2][rc] = lam * g1[cr];
                 mt.xa[1][3][rc] = mu * g1[rc];
             }
-        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, order.p, n_strips, n_rtiles, pitch};
+        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, ord, n_strips, n_rtiles, pitch};
         const CUtensorMap& mu_ = state_map_e<P>(a.cur, 0);
         const bool epi = MODE == MODE_STEP;
         const CUtensorMap& mp = epi ? state_map_e<P>(a.prev, 1) : mu_;
         const CUtensorMap& mm = epi ? state_map_e<P>(a.minv, 1) : mu_;
-        k_ela2d<P, MODE><<<(unsigned)n_order, T::NWARP * 32, T::SMEM, ctx->stream>>>(
+        k_ela2d<P, MODE><<<(unsigned)n_ord, T::NWARP * 32, T::SMEM, ctx->stream>>>(
             mu_, mp, mm, g, mt, plane, (int32_t)rows, a);
         ctx->launches++;
     }
@@ -579,6 +587,36 @@ struct ScmOperator final : Operator {
     }
     void cdm_step(const StepArgs& a) override {
         if (dim == 3) dispatch3d<MODE_STEP>(a); else dispatch2d<MODE_STEP>(a);
+        WCB_CHECK_LAUNCH();
+    }
+    bool set_apply_subset(const int64_t* ids, int64_t n_ids) override {
+        if (dim != 2) return false;
+        const int RX = ncomp == 2 ? rpe_e(p) : rpe_for(p);
+        const int64_t TI = (int64_t)RX * p, TJ = 32 * (int64_t)p;
+        std::vector<uint8_t> mark(n_strips * n_rtiles, 0);
+        for (int64_t k = 0; k < n_ids; ++k) {
+            const int64_t sidx_k = sidx[ids[k]] % plane;   // same tile in both planes
+            const int64_t row = sidx_k / pitch - p, col = sidx_k % pitch - PADJ;
+            mark[(col / TJ) * n_rtiles + (row - row_lo) / TI] = 1;
+        }
+        std::vector<int32_t> ord;
+        for (int64_t t = 0; t < (int64_t)mark.size(); ++t)
+            if (mark[t]) ord.push_back((int32_t)t);
+        n_order_sub = (int64_t)ord.size();
+        order_sub.alloc(std::max<int64_t>(n_order_sub, 1));
+        if (n_order_sub) order_sub.upload(ord.data(), ord.size(), ctx->stream);
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        sub_ready = true;
+        return true;
+    }
+    void apply_subset(const double* x, double* y) override {
+        if (!sub_ready) { apply(x, y); return; }
+        sub_active = true;
+        StepArgs a;
+        a.cur = x;
+        a.out = y;
+        dispatch2d<MODE_APPLY>(a);
+        sub_active = false;
         WCB_CHECK_LAUNCH();
     }
     double step_bytes() const override { return bytes_step; }
