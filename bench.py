@@ -281,6 +281,161 @@ def workload_config(cfg, prob):
                   f"time step as the real loop does"}
 
 
+# --------------------------------------------------------------- config 4 --
+def _cpu_imex_sample(n_e_small: int, target_s: float):
+    """Reference-arithmetic IMEX loop (oracle port of src/timeint.py:196-292:
+    SciPy CSR matvec + SuperLU solves, one host thread) on config 4 reduced to
+    n_e_small^2 cells -- the global CSR of the full grid (~60-80 GB) does not
+    fit host memory.  Returns (DOF-updates/s, steps, seconds,
+    n_dof); factorisation excluded (timed as T(n) - T(0))."""
+    from oracle import timeint as O
+    from paper_2501_19013_b200.setup.configs import ElasticConfig, build_elastic, ricker
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(1)
+    except ImportError:
+        lim = None
+    cfg = ElasticConfig().scaled(n_e_small)
+    prob = build_elastic(cfg)
+    K = prob.csr_stiffness()
+    M = prob.mass_matrix()
+    c, d = prob.c_idx, prob.d_idx
+    lam, _ = O.max_gen_eig(K[d][:, d], M[d][:, d], tol=1e-7, seed=cfg.seed)
+    dt = cfg.safety * 2.0 / np.sqrt(lam)
+    f = lambda t: ricker(t, cfg.f_e)  # noqa: E731
+    t0 = time.perf_counter()
+    O.imex_run(M, K, prob.F_s, f, dt, 0, c, d)
+    t_fixed = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.imex_run(M, K, prob.F_s, f, dt, 3, c, d)
+    per = max((time.perf_counter() - t0 - t_fixed) / 3, 1e-6)
+    n_s = int(max(3, min(cfg.n_t, target_s / per)))
+    t0 = time.perf_counter()
+    O.imex_run(M, K, prob.F_s, f, dt, n_s, c, d)
+    el = max(time.perf_counter() - t0 - t_fixed, 1e-9)
+    if lim is not None:
+        lim.unregister()
+    return prob.n_dof * n_s / el, n_s, el, prob.n_dof
+
+
+def run_config4(args, world, rank, local):
+    """Config 4: plane-strain SCM p=5 IMEX.  One bench step = one full
+    ImexPlan.run (n_t steps) on device-resident operator, mass, factors and
+    state; the loop time is CUDA-event timed inside the run (tm.rhs).  N > 1
+    runs independent replicas (IMEX slab sharding is not built yet)."""
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2501_19013_b200 import _lib, imex_critical_time_step
+    from paper_2501_19013_b200.imex import ImexPlan
+    from paper_2501_19013_b200.setup.configs import ElasticConfig, build_elastic, ricker
+    cfg = ElasticConfig()
+    t0 = time.perf_counter()
+    prob = build_elastic(cfg)
+    t_build = time.perf_counter() - t0
+    ctx = _lib.context(local)
+    op = prob.device_operator(device=local)
+    M = prob.mass_matrix()
+    c, d = prob.c_idx, prob.d_idx
+    t0 = time.perf_counter()
+    dtd = imex_critical_time_step(op, M, d, tol=1e-7, seed=cfg.seed)
+    t_eig = time.perf_counter() - t0
+    dt = cfg.safety * dtd
+    n_t = cfg.n_t if args.nt is None else int(args.nt)
+    f = lambda t: ricker(t, cfg.f_e)  # noqa: E731
+    plan = ImexPlan(M, op, prob.F_s, dt, c, d, obs_mat=prob.obs_mat, beta=cfg.beta, device=local)
+    n = prob.n_dof
+    for _ in range(args.warmup):
+        plan.run(f, n_t, gamma=cfg.gamma)
+    barrier(world)
+    launches0 = ctx.launches
+    loops, walls = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            r = plan.run(f, n_t, gamma=cfg.gamma)
+            walls.append(time.perf_counter() - t0)
+            loops.append(r.timings.rhs)
+    launches = ctx.launches - launches0
+    assert np.all(np.isfinite(r.psi)), "non-finite field"
+    total = reduce_max(sum(loops), world)
+    value = n * world * n_t * args.steps / total
+    e2e_t = reduce_max(sum(walls), world)
+    e2e_value = n * world * n_t * args.steps / e2e_t
+    fact_nnz = plan.fact_nnz
+    L = 2 * (cfg.p + 1) ** 2
+    n_cut = int(prob.grid.cut_lex.shape[0])
+    nc = int(c.shape[0])
+    bytes_step = 32.0 * n + 8.0 * L * (L + 1) / 2 * n_cut + 12.0 * fact_nnz + 48.0 * nc
+    per_step_s = sum(loops) / (args.steps * n_t)
+    achieved = bytes_step / per_step_s / 1e9
+    peak, peak_kind = measured_peaks()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded voids and source, BASELINE config shapes)",
+            "config": {"workload": (f"config4: 2D plane-strain SCM GLL p={cfg.p}, {cfg.n_e}^2 cells, "
+                                    f"E={cfg.E}, nu={cfg.nu}, {cfg.n_random} random voids r in "
+                                    f"{list(cfg.r_range)}, alpha={cfg.alpha}, IMEX: CDM on d, Newmark "
+                                    f"beta={cfg.beta} gamma={cfg.gamma} on c (SuperLU factors), "
+                                    f"x point force (Ricker), {cfg.n_t} steps at 0.9 dt_crit(d)"),
+                       "n_dof": n, "n_c": nc, "n_cut": n_cut, "n_t": n_t, "seed": cfg.seed,
+                       "factor_nnz": fact_nnz, "dt": dt,
+                       "parallelism": f"{world} independent replica(s), one per GPU",
+                       "setup_s": round(t_build, 2), "dt_crit_s": round(t_eig, 3),
+                       "factorization_s": round(plan.factorization, 2),
+                       "l2": f"working set {bytes_step / 1e9:.2f} GB per time step (> L2)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "IMEX step: k_ela2d<5,STEP> + c-row k_ela2d<5,APPLY> + 2 k_trsv_comp",
+                         "bytes_per_launch": bytes_step, "launch_us": per_step_s * 1e6,
+                         "peak_kind": peak_kind},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(16 * n_t + 8),
+                    "d2h_bytes_per_step": int(8 * n + 8 * plan.n_obs * (n_t + 1)),
+                    "note": "ImexPlan.run with host arrays; factorisation once per plan, reported "
+                            "in config.factorization_s"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary()}
+    plan.close()
+    if rank == 0 and not args.no_cpu:
+        from oracle import cpu
+        cv, n_s, el, nd = _cpu_imex_sample(128, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": cv, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{n_s} IMEX steps of config 4 reduced to 128^2 cells ({nd} DOFs; the full CSR "
+                      f"exceeds host RAM), oracle port of src/timeint.py:196-292 (SciPy CSR + SuperLU, "
+                      f"1 thread, {el:.1f} s); host {cpu.host_cpu_model()}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    barrier(world)
+
+
+def run_reference_config4(args, world, rank):
+    if rank != 0:
+        return
+    from oracle import cpu
+    times, vals = [], []
+    for _ in range(args.warmup):
+        _cpu_imex_sample(64, 1.0)
+    for _ in range(args.steps):
+        cv, n_s, el, nd = _cpu_imex_sample(128, args.cpu_seconds / max(args.steps, 1))
+        vals.append(cv)
+        times.append(el)
+    value = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config4 reduced to 128^2 cells (full CSR exceeds host RAM)",
+                       "n_dof": nd},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"{n_s} IMEX steps per bench step at 128^2 cells, oracle port "
+                                       f"(SciPy CSR + SuperLU, 1 thread); host {cpu.host_cpu_model()}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -295,8 +450,14 @@ def main():
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
-        run_reference(args, world, rank)
+        if args.config == "config4":
+            run_reference_config4(args, world, rank)
+        else:
+            run_reference(args, world, rank)
         barrier(world)
+        return
+    if args.config == "config4":
+        run_config4(args, world, rank, local)
         return
 
     import torch
