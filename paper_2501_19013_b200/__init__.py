@@ -9,7 +9,9 @@ include/wavecell_b200.h); there is no CPU fallback.
 """
 
 from .linalg import IndefiniteMatrixError, dt_crit, max_gen_eig
-from .operators import CsrOperator, DeviceOperator, ScmOperator, as_device_operator
+from .imex import ImexPlan
+from .operators import (CsrOperator, DeviceOperator, ElasticOperator, ScmOperator,
+                        as_device_operator)
 from .timeint import (DIVERGENCE_LIMIT, CdmPlan, DivergenceError, RunResult,
                       StageTimings, cdm_run, imex_critical_time_step, imex_run,
                       sample_history, select_dt)
@@ -18,7 +20,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "CdmPlan", "CsrOperator", "DIVERGENCE_LIMIT", "DeviceOperator", "DivergenceError",
-    "IndefiniteMatrixError", "RunResult", "ScmOperator", "StageTimings",
+    "ElasticOperator", "ImexPlan", "IndefiniteMatrixError", "RunResult", "ScmOperator",
+    "StageTimings",
     "as_device_operator", "cdm_run", "dt_crit", "imex_critical_time_step", "imex_run",
     "max_gen_eig", "sample_history", "select_dt",
 ]
