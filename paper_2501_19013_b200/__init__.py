@@ -2,14 +2,14 @@
 
 Drop-in for the integrator / critical-step API of the reference package
 ``wavecell`` (src/__init__.py:5-20): ``cdm_run``, ``imex_run``,
-``max_gen_eig``, ``dt_crit``, ``imex_critical_time_step``, ``select_dt``,
+``newmark_run``, ``max_gen_eig``, ``dt_crit``, ``imex_critical_time_step``, ``select_dt``,
 ``RunResult``, ``StageTimings``, ``DivergenceError``.  Every step runs in HBM
 through hand-written CUDA kernels in ``libwavecell_b200.so`` (C ABI:
 include/wavecell_b200.h); there is no CPU fallback.
 """
 
 from .linalg import IndefiniteMatrixError, dt_crit, max_gen_eig
-from .imex import ImexPlan
+from .imex import ImexPlan, newmark_run
 from .operators import (CsrOperator, DeviceOperator, ElasticOperator, ScmOperator,
                         as_device_operator)
 from .timeint import (DIVERGENCE_LIMIT, CdmPlan, DivergenceError, RunResult,
@@ -23,5 +23,5 @@ __all__ = [
     "ElasticOperator", "ImexPlan", "IndefiniteMatrixError", "RunResult", "ScmOperator",
     "StageTimings",
     "as_device_operator", "cdm_run", "dt_crit", "imex_critical_time_step", "imex_run",
-    "max_gen_eig", "sample_history", "select_dt",
+    "max_gen_eig", "newmark_run", "sample_history", "select_dt",
 ]

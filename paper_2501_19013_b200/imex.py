@@ -194,3 +194,30 @@ def imex_run(M, K, F_s, f_t, dt: float, n_t: int, c_idx, d_idx, obs_mat=None,
         return plan.run(f_t, n_t, gamma=gamma, psi0=psi0, v0=v0)
     finally:
         plan.close()
+
+
+def newmark_run(M, K, F_s, f_t, dt: float, n_t: int, obs_mat=None, beta: float = 0.25,
+                gamma: float = 0.5, psi0=None, v0=None, s_factory=None,
+                device: int | None = None) -> RunResult:
+    """Newmark-beta on the device, src/timeint.py:109-156.
+
+    Every DOF is implicit: ``S = M + beta dt^2 K`` and ``M`` are factorised
+    once with SuperLU in the reference configuration (for ``beta = 0``,
+    ``S = M`` as in the reference) and each step runs predictor, ``K``
+    apply, the two triangular solves and the corrector on the B200 -- the
+    IMEX plan with an empty explicit set, whose per-step arithmetic is the
+    reference's Newmark loop line by line.  ``s_factory`` (a host
+    factorisation object called every step) has no device form.
+    """
+    if s_factory is not None:
+        raise NotImplementedError("newmark_run(s_factory=...) solves through a host object every "
+                                  "step; the device path factorises S itself (omit s_factory)")
+    n = sp.csr_matrix(M).shape[0]
+    plan = ImexPlan(M, K, F_s, dt, np.arange(n, dtype=np.int64), np.zeros(0, dtype=np.int64),
+                    obs_mat=obs_mat, beta=beta, device=device)
+    try:
+        r = plan.run(f_t, n_t, gamma=gamma, psi0=psi0, v0=v0)
+    finally:
+        plan.close()
+    return RunResult(method="newmark", dt=r.dt, t=r.t, obs=r.obs, psi=r.psi, psi_dot=r.psi_dot,
+                     timings=r.timings, fact_dim=n)

@@ -11,7 +11,7 @@ from oracle import timeint as O
 
 pytestmark = pytest.mark.gpu
 
-from paper_2501_19013_b200 import cdm_run, imex_run  # noqa: E402
+from paper_2501_19013_b200 import cdm_run, imex_run, newmark_run  # noqa: E402
 
 
 def rel(a, b):
@@ -128,3 +128,37 @@ def test_imex_scm_operator_2d_voids():
     assert rel(r.psi, psi_ref) <= 1e-10
     r2 = imex_run(M, K, prob.F_s, f, dt, 200, dm.c_idx, dm.d_idx)
     assert rel(r2.psi, psi_ref) <= 1e-10
+
+
+def test_newmark_run_matches_reference_golden():
+    """newmark_run drop-in (src/timeint.py:109-156) vs the reference's own output."""
+    M, K, g = bar()
+    f = lambda t: np.sin(6.0 * t)
+    r = newmark_run(M, K, g["F"], f, float(g["dt"]), int(g["n_t"]),
+                    obs_mat=sp.identity(4, format="csr"))
+    assert np.abs(r.obs - g["nm_obs"]).max() <= 1e-12 * np.abs(g["nm_obs"]).max()
+    assert r.method == "newmark" and r.fact_dim == 4 and r.psi_dot.shape == (4,)
+    r0 = newmark_run(M, K, g["F"], f, float(g["dt"]), 50, beta=0.0)
+    psi_ref, v_ref, _ = O.newmark_run(M, K, g["F"], f, float(g["dt"]), 50, beta=0.0)
+    assert rel(r0.psi, psi_ref) <= 1e-12 and rel(r0.psi_dot, v_ref) <= 1e-12
+    with pytest.raises(NotImplementedError):
+        newmark_run(M, K, g["F"], f, 1e-3, 3, s_factory=lambda: None)
+
+
+def test_newmark_scm_operator_matches_oracle():
+    """Whole-system Newmark with the matrix-free SCM K on a 2D void problem."""
+    from paper_2501_19013_b200.setup.configs import ricker
+    from paper_2501_19013_b200.setup.geometry import BallVoids
+    from paper_2501_19013_b200.setup.grid import Grid
+    from paper_2501_19013_b200.setup.problem import ScmProblem
+    geom = BallVoids(2, [[0.5, 0.5]], [0.21])
+    prob = ScmProblem.build(Grid.build(geom, "lagrange", 3, 12), 1e-3, 2)
+    prob.set_point_source([0.15, 0.2])
+    M = prob.mass_matrix()
+    K = prob.csr_stiffness()
+    op = prob.device_operator()
+    f = lambda t: ricker(t, 10.0)
+    dt = 2e-3
+    psi_ref, v_ref, _ = O.newmark_run(M, K, prob.F_s, f, dt, 120)
+    r = newmark_run(M, op, prob.F_s, f, dt, 120)
+    assert rel(r.psi, psi_ref) <= 1e-10 and rel(r.psi_dot, v_ref) <= 1e-10
