@@ -408,6 +408,8 @@ struct ScmOperator final : Operator {
     DevBuf<int32_t> cut_id;
     MapCache maps;
     DevBuf<double> KT;
+    DevBuf<double> KP, cut_out;      // 3D: packed cut matrices, per-step products
+    DevBuf<int64_t> cut_base;        // 3D: state index of each cut cell's first node
     DevBuf<int32_t> order;        // 2D tile kernel: live tiles, most expensive first
     int64_t n_order = 0;
     // apply restricted to the tiles owning a given DOF subset (IMEX c rows)
@@ -565,7 +567,9 @@ struct ScmOperator final : Operator {
                     mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
-        Scm3DGeo g{n_ex, row_lo, row_hi, n_e, n1, pitch, pplane, mask.p, cut_id.p, KT.p, cflags.p, n_zs, n_xt};
+        launch_cut_pre<P>(ctx, n_cut, KP.p, cut_base.p, pplane, pitch, a.cur, cut_out.p);
+        Scm3DGeo g{n_ex, row_lo, row_hi, n_e, n1, pitch, pplane, mask.p, cut_id.p, KT.p, cut_out.p, cflags.p,
+                   n_zs, n_xt};
         launch_scm3d<P, MODE>(ctx, state_map3<P>(a.cur), g, mt, sk, a);
     }
     template <int MODE>
@@ -789,7 +793,11 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
     op->L = ncomp * (dim == 2 ? N * N : N * N * N);
     const int L = op->L;
     std::vector<int32_t> cid(op->n_ex * cells_row, -1);
-    std::vector<double> KT((size_t)std::max<int64_t>(op->n_cut, 1) * L * L, 0.0);
+    // 2D: full transposed matrices; 3D: packed lower triangles (k_cut_pre)
+    const int64_t LP = (int64_t)L * (L + 1) / 2;
+    std::vector<double> KT(dim == 2 ? (size_t)std::max<int64_t>(op->n_cut, 1) * L * L : 1, 0.0);
+    std::vector<double> KP(dim == 3 ? (size_t)std::max<int64_t>(op->n_cut, 1) * LP : 1, 0.0);
+    std::vector<int64_t> cbase(std::max<int64_t>(op->n_cut, 1), 0);
     for (int64_t e = 0; e < op->n_cut; ++e) {
         WCB_REQUIRE(d->cut_cells && d->cut_K, "cut arrays NULL");
         const int64_t c = d->cut_cells[e];
@@ -800,11 +808,19 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
                     "cut_cells must list cut cells of the slab");
         cid[lx * cells_row + crest] = (int32_t)e;
         const double* K = d->cut_K + e * L * L;
-        double* T = KT.data() + e * L * L;
-        // stored transposed and divided by sk: the kernels scale every
-        // output node by sk once (tensor and cut parts alike)
-        for (int r = 0; r < L; ++r)
-            for (int m = 0; m < L; ++m) T[m * L + r] = K[r * L + m] / d->sk;
+        // divided by sk: the kernels scale every output node by sk once
+        // (tensor and cut parts alike)
+        if (dim == 2) {
+            double* T = KT.data() + e * L * L;   // transposed: lane r reads column r
+            for (int r = 0; r < L; ++r)
+                for (int m = 0; m < L; ++m) T[m * L + r] = K[r * L + m] / d->sk;
+        } else {
+            double* T = KP.data() + e * LP;      // row r, columns m <= r
+            for (int r = 0; r < L; ++r)
+                for (int m = 0; m <= r; ++m) T[(int64_t)r * (r + 1) / 2 + m] = K[r * L + m] / d->sk;
+            const int64_t cy = crest / n_e, cz = crest % n_e;
+            cbase[e] = (lx * p + p) * op->xstride + (cy * p + p) * op->pitch + cz * p + PADJ;
+        }
     }
     for (size_t c = 0; c < cls.size(); ++c)
         WCB_REQUIRE(cls[c] != 2 || cid[c] >= 0, "a cut cell is missing from cut_cells");
@@ -844,6 +860,13 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
     op->cut_id.upload(cid.data(), cid.size(), st);
     op->KT.alloc(KT.size());
     op->KT.upload(KT.data(), KT.size(), st);
+    if (dim == 3) {
+        op->KP.alloc(KP.size());
+        op->KP.upload(KP.data(), KP.size(), st);
+        op->cut_base.alloc(cbase.size());
+        op->cut_base.upload(cbase.data(), cbase.size(), st);
+        op->cut_out.alloc((size_t)std::max<int64_t>(op->n_cut, 1) * L);
+    }
     // algorithmic bytes per step: 32 B per DOF + packed cut K
     op->bytes_step = 32.0 * (double)op->n + 8.0 * (double)L * (L + 1) / 2.0 * (double)op->n_cut;
     WCB_CUDA(cudaStreamSynchronize(st));

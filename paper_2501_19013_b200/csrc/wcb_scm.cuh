@@ -57,7 +57,8 @@ struct Scm3DGeo {
     int64_t pplane;           // plane pitch (doubles)
     const uint8_t* mask;      // (n_e+2)^3 cell codes with a ring of 0: 0 out, 1 uncut, 2 cut
     const int32_t* cut_id;    // n_e^3 -> cut index or -1
-    const double* KT;         // n_cut * L * L transposed cut stiffness / sk
+    const double* KT;         // unused in 3D (cut products come from cut_out)
+    const double* cut_out;    // n_cut * L: K_o u_e / sk of every cut cell (k_cut_pre)
     const uint8_t* cflags;    // per CTA tile (z strip, y row, x tile): owns a DOF
     int64_t n_zs;             // z strips
     int64_t n_xt;             // x tiles
@@ -84,5 +85,9 @@ struct Tile3 {
 template <int P, int MODE>
 void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const Scm3DGeo& g, const Mats2<P>& mt,
                   double sk, const StepArgs& a);
+// dense cut-cell products u_e -> K_o u_e / sk (packed symmetric K), before the stencil
+template <int P>
+void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t* cut_base,
+                    int64_t pplane, int64_t prow, const double* u, double* out);
 
 }  // namespace wcb

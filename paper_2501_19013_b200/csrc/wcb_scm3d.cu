@@ -55,50 +55,36 @@ __device__ __forceinline__ void zpass_row(const double (&mc)[orb_count(P)],
     zkL = l2;
 }
 
-// Dense cut cells of one x cell row, cooperatively per warp.  `up` selects the
-// y-up cell row (only its y-local row P is routed, to our y row 0); z routing
-// as in 2D: z-local j < P -> the cell's lane, j = P -> the next lane.
+// Cut cells of one x cell row: the products K_o u_e / sk were computed by
+// k_cut_pre; the lanes owning the outputs add them in ascending cell order.
+// `up` selects the y-up cell row (only its y-local row P is routed, to our y
+// row 0); z routing as in 2D: z-local j < P -> the cell's lane, j = P -> the
+// next lane.
 template <int P>
-__device__ __forceinline__ void cut_cells_warp3(const Scm3DGeo& g, const double* corner0,
-                                                int64_t ex, int64_t eyc, int64_t ez0, int lane,
-                                                unsigned cut_lanes, bool edge, bool up,
-                                                double (&Y)[P + 1][P][P]) {
-    using T = Tile3<P>;
+__device__ __forceinline__ void cut_cells_warp3(const Scm3DGeo& g, int64_t ex, int64_t eyc,
+                                                int64_t ez0, int lane, unsigned cut_lanes,
+                                                bool edge, bool up, double (&Y)[P + 1][P][P]) {
     constexpr int N = P + 1;
     constexpr int L = N * N * N;
-    constexpr int RR = (L + 31) / 32;
     int src = edge ? -1 : (__ffs(cut_lanes) - 1);
     if (!edge) cut_lanes &= cut_lanes - 1;
     while (true) {
         const int64_t ecol = ez0 + src;
-        const int32_t id = __ldg(g.cut_id + (ex * g.n_e + eyc) * g.n_e + ecol);   // ex local
-        const double* KT = g.KT + (int64_t)id * L * L;
-        const double* corner = corner0 + src * P;   // node (ex*P, eyc*P, ecol*P) in the tile
-        double t[RR];
-        #pragma unroll
-        for (int q = 0; q < RR; ++q) {
-            t[q] = 0.0;
-            const int r = lane + 32 * q;
-            if (r < L) {
-                #pragma unroll 8
-                for (int m = 0; m < L; ++m) {
-                    const int mc_ = m / (N * N), me = (m / N) % N, md = m % N;
-                    t[q] = fma(__ldg(KT + m * L + r),
-                               corner[((size_t)mc_ * T::UR + me) * T::UW + md], t[q]);
-                }
-            }
-        }
-        #pragma unroll
-        for (int r = 0; r < L; ++r) {
-            const double v = __shfl_sync(0xffffffffu, t[r / 32], r % 32);
-            const int a = r / (N * N), b = (r / N) % N, j = r % N;
-            const bool yok = up ? (b == P) : (b < P);
-            if (yok) {
-                const int bb = up ? 0 : (b % P);
-                if (j < P) {
-                    if (lane == src) Y[a][bb][j % P] += v;
-                } else {
-                    if (lane == src + 1) Y[a][bb][0] += v;
+        const bool mine = lane == src || lane == src + 1;
+        if (mine) {
+            const int32_t id = __ldg(g.cut_id + (ex * g.n_e + eyc) * g.n_e + ecol);   // ex local
+            const double* o = g.cut_out + (int64_t)id * L;
+            #pragma unroll
+            for (int r = 0; r < L; ++r) {
+                const int a = r / (N * N), b = (r / N) % N, j = r % N;
+                const bool yok = up ? (b == P) : (b < P);
+                if (yok) {
+                    const int bb = up ? 0 : (b % P);
+                    if (j < P) {
+                        if (lane == src) Y[a][bb][j % P] += __ldcg(o + r);
+                    } else {
+                        if (lane == src + 1) Y[a][bb][0] += __ldcg(o + r);
+                    }
                 }
             }
         }
@@ -106,6 +92,67 @@ __device__ __forceinline__ void cut_cells_warp3(const Scm3DGeo& g, const double*
         src = __ffs(cut_lanes) - 1;
         cut_lanes &= cut_lanes - 1;
     }
+}
+
+// One warp per cut cell: gather u_e (64 nodes for p = 3) from the state, stage
+// the packed lower triangle of K_o / sk in shared memory (one coalesced read
+// of L(L+1)/2 doubles -- half the full matrix), lane r forms row r in
+// ascending column order.
+template <int P>
+__host__ __device__ constexpr int cut_pre_warps() {
+    return (int)(200 * 1024 / (((P + 1) * (P + 1) * (P + 1)) * (((P + 1) * (P + 1) * (P + 1)) + 3) / 2 * 8)) > 4
+               ? 4
+               : (int)(200 * 1024 / (((P + 1) * (P + 1) * (P + 1)) * (((P + 1) * (P + 1) * (P + 1)) + 3) / 2 * 8));
+}
+
+template <int P>
+__global__ void __launch_bounds__(128) k_cut_pre(int64_t n_cut, const double* __restrict__ KP,
+                                                 const int64_t* __restrict__ cut_base, int64_t pplane,
+                                                 int64_t prow, const double* __restrict__ u,
+                                                 double* __restrict__ out) {
+    constexpr int N = P + 1;
+    constexpr int L = N * N * N;
+    constexpr int LP = L * (L + 1) / 2;
+    extern __shared__ double smc[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* kp = smc + (size_t)w * (LP + L);
+    double* uu = kp + LP;
+    const int64_t e = (int64_t)blockIdx.x * cut_pre_warps<P>() + w;
+    if (e >= n_cut) return;
+    const double* src = KP + e * LP;
+    for (int i = lane; i < LP; i += 32) kp[i] = __ldg(src + i);
+    const int64_t base = cut_base[e];
+    for (int m = lane; m < L; m += 32) {
+        const int a = m / (N * N), b = (m / N) % N, j = m % N;
+        uu[m] = u[base + a * pplane + b * prow + j];
+    }
+    __syncwarp();
+    for (int r = lane; r < L; r += 32) {
+        double t = 0.0;
+        #pragma unroll 8
+        for (int m = 0; m < L; ++m) {
+            const int hi = r >= m ? r : m, lo = r >= m ? m : r;
+            t = fma(kp[hi * (hi + 1) / 2 + lo], uu[m], t);
+        }
+        out[e * L + r] = t;
+    }
+}
+
+template <int P>
+void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t* cut_base,
+                    int64_t pplane, int64_t prow, const double* u, double* out) {
+    if (!n_cut) return;
+    constexpr int L = (P + 1) * (P + 1) * (P + 1);
+    constexpr int W = cut_pre_warps<P>();
+    const size_t smem = (size_t)W * (L * (L + 1) / 2 + L) * 8;
+    static bool attr_set = false;
+    if (!attr_set) {
+        WCB_CUDA(cudaFuncSetAttribute(k_cut_pre<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    k_cut_pre<P><<<(unsigned)ceil_div(n_cut, W), 32 * W, smem, ctx->stream>>>(n_cut, KP, cut_base, pplane, prow,
+                                                                         u, out);
+    ctx->launches++;
 }
 
 template <int P, int MODE>
@@ -208,14 +255,16 @@ __global__ void __launch_bounds__(Tile3<P>::NWARP * 32) k_scm3d(const __grid_con
                         Y[r][b][j] = fma(kc[orb(P, r, c)], Au[b][j], fma(mc[orb(P, r, c)], Bu[b][j], Y[r][b][j]));
         }
         // dense cut cells: own y row (ey) and the y-up row (ey-1)
-        const double* corner_own = us + ((size_t)po * T::UR + P) * T::UW + T::CO + P;
-        const double* corner_up = us + ((size_t)po * T::UR + 0) * T::UW + T::CO + P;
         const unsigned clR = __ballot_sync(0xffffffffu, cRR == 2);
         const bool edR = __shfl_sync(0xffffffffu, cRL == 2, 0);
-        if (clR || edR) cut_cells_warp3<P>(g, corner_own, ex, ey, K0 / P, lane, clR, edR, false, Y);
+#ifndef WCB3D_NOCUT
+        if (clR || edR) cut_cells_warp3<P>(g, ex, ey, K0 / P, lane, clR, edR, false, Y);
+#endif
         const unsigned clU = __ballot_sync(0xffffffffu, cUR == 2);
         const bool edU = __shfl_sync(0xffffffffu, cUL == 2, 0);
-        if (clU || edU) cut_cells_warp3<P>(g, corner_up, ex, ey - 1, K0 / P, lane, clU, edU, true, Y);
+#ifndef WCB3D_NOCUT
+        if (clU || edU) cut_cells_warp3<P>(g, ex, ey - 1, K0 / P, lane, clU, edU, true, Y);
+#endif
     }
     // x plane a = P of cell row ex is plane a = 0 of cell row ex+1
     #pragma unroll
@@ -288,6 +337,13 @@ void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const Scm3DGeo& g, con
                                              const Mats2<P>&, double, const StepArgs&);        \
     template void launch_scm3d<P, MODE_APPLY>(Context*, const CUtensorMap&, const Scm3DGeo&,   \
                                               const Mats2<P>&, double, const StepArgs&);
+#define WCB_INSTC(P) \
+    template void launch_cut_pre<P>(Context*, int64_t, const double*, const int64_t*, int64_t, int64_t, \
+                                    const double*, double*);
+WCB_INSTC(1)
+WCB_INSTC(2)
+WCB_INSTC(3)
+WCB_INSTC(4)
 WCB_INST3(1)
 WCB_INST3(2)
 WCB_INST3(3)

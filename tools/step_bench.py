@@ -12,7 +12,9 @@ from paper_2501_19013_b200.setup.configs import CONFIGS, build_scm, ricker
 name = sys.argv[1] if len(sys.argv) > 1 else "config2"
 n_t = int(sys.argv[2]) if len(sys.argv) > 2 else 500
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-prob = build_scm(CONFIGS[name])
+base, _, scale = name.partition("@")
+cfg = CONFIGS[base] if not scale else CONFIGS[base].scaled(int(scale))
+prob = build_scm(cfg)
 op = prob.device_operator()
 plan = CdmPlan(prob.mass_matrix(), op, prob.F_s)
 dt = 1e-7
