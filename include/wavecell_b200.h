@@ -187,6 +187,11 @@ int wcb_cdm_plan_destroy(wcb_cdm_plan* plan);
 int wcb_cdm_plan_run(wcb_cdm_plan* plan, const double* ft, double dt, int64_t n_t,
                      const double* psi0, const double* v0, double* psi_out,
                      double* obs_out, wcb_divergence* div, wcb_timings* tm);
+/* Algorithmic bytes one fused time step of this plan moves: 32 B per DOF
+ * (psi_k, psi_{k-1}, 1/m, psi_{k+1}) less 8 B per DOF whose 1/m the kernel
+ * takes from the interior-cell table (bitwise-checked at plan creation), plus
+ * the operator's own data (cut-cell matrices, CSR arrays). */
+int wcb_cdm_plan_step_bytes(const wcb_cdm_plan* plan, double* out);
 /* Same loop on device-resident buffers (cudaMalloc'd by the caller on the
  * context's device): d_ft (n_t), d_psi0/d_v0 (n, may be NULL), d_psi_out (n),
  * d_obs_out (n_obs*(n_t+1) or NULL).  Used by bench.py for the HBM-resident

@@ -685,6 +685,7 @@ int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s
         if (n) k_mass_state<<<grid_for(ctx, n), 256, 0, s>>>(n, map.p, dm.p, P->m_state.p, P->minv.p);
         ctx->launches += 2;
         WCB_CHECK_LAUNCH();
+        op->bind_minv(P->minv.p);
         // source: dense window over its nonzeros' state-index range
         {
             std::vector<std::pair<int64_t, double>> nz;
@@ -811,6 +812,15 @@ int wcb_cdm_group_run(int n_plans, wcb_cdm_plan** plans, const double* ft, doubl
             std::memcpy(obs_out, acc.data(), acc.size() * sizeof(double));
         }
         WCB_CUDA(cudaStreamSynchronize(s));
+        return WCB_OK;
+    });
+}
+
+int wcb_cdm_plan_step_bytes(const wcb_cdm_plan* plan, double* out) {
+    return guarded([&] {
+        WCB_REQUIRE(plan && out, "NULL argument");
+        const Operator* op = plan->op;
+        *out = op->step_bytes() - 8.0 * op->minv_skipped;
         return WCB_OK;
     });
 }

@@ -35,7 +35,7 @@ namespace wcb {
 // elimination level -- instead of a device-wide chain of global-memory
 // handshakes.  Entries of a row are visited in the same lane-strided order and
 // reduced by the same shuffle tree as the sync-free kernel (bitwise equal).
-constexpr int TRSV_D = 3;                 // ring depth (levels in flight)
+constexpr int TRSV_DMAX = 12;             // max ring depth (levels in flight)
 constexpr int TRSV_SMEM = 220 * 1024;     // dynamic shared memory budget
 constexpr int TRSV_THREADS = 512;
 
@@ -44,6 +44,8 @@ struct TriSched {
     int64_t n_comp = 0, max_size = 0, n_levels = 0, max_levels = 0;
     int64_t max_lvl_rows = 0, max_lvl_ent = 0;   // widest level
     int slot_e = 0, slot_r = 0;                  // ring slot capacities (entries, rows)
+    int depth = 3;                               // ring depth (levels in flight)
+    DevBuf<int32_t> comp_order;  // launch order: components by decreasing level count
     DevBuf<int32_t> comp_rows;   // n_comp + 1: offsets into rows
     DevBuf<int32_t> comp_lvl;    // n_comp + 1: offsets into lvl_off
     DevBuf<int32_t> lvl_off;     // n_levels + 1: offsets into rows
@@ -173,12 +175,39 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
     T.sdiag.alloc(n, s); T.sdiag.upload(sdiag.data(), n, s);
     WCB_CUDA(cudaStreamSynchronize(s));   // host vectors die here
     // ring slots as large as the widest level allows within the smem budget
+    // ring slots sized for the 97th-percentile level (wider levels read global
+    // memory directly), as many slots as the budget allows (2..TRSV_DMAX)
     const int64_t fixed = T.max_size * 8 + (T.max_levels + 1) * 8 + 64;
     const int64_t avail = (int64_t)TRSV_SMEM - fixed;
-    T.slot_r = (int)std::min<int64_t>(std::max<int64_t>(T.max_lvl_rows, 1), 1024);
-    const int64_t per = avail / TRSV_D - (int64_t)T.slot_r * 12 - 32;
-    T.slot_e = (int)std::max<int64_t>(0, std::min<int64_t>(std::max<int64_t>(T.max_lvl_ent, 1), per / 12));
-    T.ok = avail > 0 && T.slot_e >= 256;
+    std::vector<int32_t> le_sz, lr_sz;
+    for (size_t l = 0; l + 1 < lvl_off.size(); ++l) {
+        le_sz.push_back(lvl_ent[l + 1] - lvl_ent[l]);
+        lr_sz.push_back(lvl_off[l + 1] - lvl_off[l]);
+    }
+    auto pct = [](std::vector<int32_t> v, double q) -> int64_t {
+        if (v.empty()) return 1;
+        std::sort(v.begin(), v.end());
+        return std::max<int64_t>(1, v[(size_t)std::min<double>(v.size() - 1, q * v.size())]);
+    };
+    const char* qe = getenv("WAVECELL_B200_TRSV_Q");
+    const double q = qe ? atof(qe) : 0.97;
+    T.slot_r = (int)std::min<int64_t>(pct(lr_sz, q) + 8, 1024);
+    T.slot_e = (int)std::min<int64_t>(pct(le_sz, q) + 64, std::max<int64_t>(T.max_lvl_ent, 1));
+    const int64_t sb = (int64_t)(((size_t)T.slot_e * 12 + (size_t)T.slot_r * 12 + 4) + 15) / 16 * 16;
+    T.depth = (int)std::min<int64_t>(TRSV_DMAX, avail / std::max<int64_t>(sb, 1));
+    T.depth = T.depth >= 12 ? 12 : T.depth >= 8 ? 8 : T.depth >= 6 ? 6 : T.depth >= 4 ? 4 : T.depth >= 3 ? 3 : T.depth;
+    T.ok = avail > 0 && T.depth >= 3;
+    // launch order: longest dependency chains first (2 waves when components > SMs)
+    std::vector<int32_t> co(n_comp);
+    for (int64_t c = 0; c < n_comp; ++c) co[c] = (int32_t)c;
+    std::stable_sort(co.begin(), co.end(), [&](int32_t a, int32_t b) {
+        const int64_t la = comp_lvl[a + 1] - comp_lvl[a], lb = comp_lvl[b + 1] - comp_lvl[b];
+        if (la != lb) return la > lb;
+        return comp_rows[a + 1] - comp_rows[a] > comp_rows[b + 1] - comp_rows[b];
+    });
+    T.comp_order.alloc(std::max<int64_t>(n_comp, 1), s);
+    T.comp_order.upload(co.data(), n_comp, s);
+    WCB_CUDA(cudaStreamSynchronize(s));
 }
 
 struct DevLU {
@@ -275,7 +304,9 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 
 static __host__ __device__ inline size_t trsv_slot_bytes(int e, int r);
 
+template <int TRSV_D>
 __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
+    const int32_t* __restrict__ comp_order,
     const int32_t* __restrict__ comp_rows, const int32_t* __restrict__ comp_lvl,
     const int32_t* __restrict__ lvl_off, const int32_t* __restrict__ lvl_ent, const int32_t* __restrict__ rows,
     const int32_t* __restrict__ sptr, const int32_t* __restrict__ slcol,
@@ -290,7 +321,7 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
     auto sd = [&](int l) { return sv(l) + slot_e; };
     auto sc = [&](int l) { return reinterpret_cast<int*>(sd(l) + slot_r); };
     auto sp = [&](int l) { return sc(l) + slot_e; };
-    const int c = blockIdx.x;
+    const int c = comp_order[blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
     const int l0 = comp_lvl[c], nl = comp_lvl[c + 1] - l0;
@@ -318,12 +349,15 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    // prologue: levels 0..D-2 in flight.  Iteration l: wait for level l,
+    // one barrier (level l-1's x and level l's data visible; ring slot of
+    // level l-1 free), refill that slot with level l+D-1, solve level l.
     #pragma unroll
     for (int l = 0; l < TRSV_D - 1; ++l) stage(l);
     for (int l = 0; l < nl; ++l) {
-        stage(l + TRSV_D - 1);
-        asm volatile("cp.async.wait_group %0;" ::"n"(TRSV_D - 1) : "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(TRSV_D - 2) : "memory");
         __syncthreads();
+        stage(l + TRSV_D - 1);
         const int a = lo[l], e = lo[l + 1];
         if (fits(l)) {
             const int* P = sp(l);
@@ -348,17 +382,119 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
                 if (lane == 0) xl[k - r0] = (xl[k - r0] - sacc) / sdiag[k];
             }
         }
-        __syncthreads();   // level done; its ring slot may be refilled next iteration
     }
+    __syncthreads();
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) x[rows[k]] = xl[k - r0];
+}
+
+// Component-local sync-free solve: one CTA per component, x in shared memory
+// initialised to a sentinel; warps take the component's rows round-robin in
+// schedule (level) order and each lane waits only for the x entries its
+// products need, so rows of different levels overlap and no CTA barrier
+// separates levels.  A row's entries are loaded into registers one row ahead
+// (they do not depend on x).  Same lane-strided fma order and shuffle tree as
+// k_trsv_comp / k_sptrsv: bitwise equal results.
+constexpr int TRSF_THREADS = 512;
+constexpr int TRSF_E = 4;   // entries per lane held in registers (rows up to 128 entries)
+constexpr unsigned long long TRSF_SENT = 0xfff8dead0000beefULL;   // a NaN the solve never produces
+
+__device__ __forceinline__ double lds_volatile(const double* p) {
+    double v;
+    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32_imex(p)));
+    return v;
+}
+
+__global__ void __launch_bounds__(TRSF_THREADS, 2) k_trsv_sf(
+    const int32_t* __restrict__ comp_rows, const int32_t* __restrict__ rows,
+    const int32_t* __restrict__ sptr, const int32_t* __restrict__ slcol,
+    const double* __restrict__ sval, const double* __restrict__ sdiag, const double* __restrict__ b,
+    double* __restrict__ x) {
+    extern __shared__ __align__(16) double xs[];
+    const int c = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
+    for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x) xs[k] = __longlong_as_double((long long)TRSF_SENT);
+    __syncthreads();
+    int cc[TRSF_E];
+    double cv[TRSF_E];
+    int p0 = 0, p1 = 0;
+    double bk = 0.0, dk = 1.0;
+    auto fetch = [&](int k) {
+        p0 = sptr[k];
+        p1 = sptr[k + 1];
+        #pragma unroll
+        for (int t = 0; t < TRSF_E; ++t) {
+            const int j = p0 + lane + 32 * t;
+            cc[t] = j < p1 ? slcol[j] : 0;
+            cv[t] = j < p1 ? sval[j] : 0.0;
+        }
+        bk = b[rows[k]];
+        dk = sdiag[k];
+    };
+    int k = r0 + warp;
+    if (k < r1) fetch(k);
+    for (; k < r1; k += nw) {
+        const int q0 = p0, q1 = p1;
+        int ccur[TRSF_E];
+        double vcur[TRSF_E];
+        #pragma unroll
+        for (int t = 0; t < TRSF_E; ++t) { ccur[t] = cc[t]; vcur[t] = cv[t]; }
+        const double bcur = bk, dcur = dk;
+        if (k + nw < r1) fetch(k + nw);   // next row's entries in flight while this one waits
+        double acc = 0.0;
+        #pragma unroll
+        for (int t = 0; t < TRSF_E; ++t) {
+            if (q0 + lane + 32 * t < q1) {
+                double xv;
+                do { xv = lds_volatile(xs + ccur[t]); } while ((unsigned long long)__double_as_longlong(xv) == TRSF_SENT);
+                acc = fma(vcur[t], xv, acc);
+            }
+        }
+        for (int j = q0 + lane + 32 * TRSF_E; j < q1; j += 32) {   // long rows
+            const int cj = slcol[j];
+            double xv;
+            do { xv = lds_volatile(xs + cj); } while ((unsigned long long)__double_as_longlong(xv) == TRSF_SENT);
+            acc = fma(sval[j], xv, acc);
+        }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            const double v = (bcur - acc) / dcur;
+            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32_imex(xs + (k - r0))), "d"(v) : "memory");
+        }
+    }
+    __syncthreads();
+    for (int k2 = r0 + threadIdx.x; k2 < r1; k2 += blockDim.x) x[rows[k2]] = xs[k2 - r0];
 }
 
 static __host__ __device__ inline size_t trsv_slot_bytes(int e, int r) {
     return (((size_t)e * 12 + (size_t)r * 8 + (size_t)(r + 1) * 4) + 15) / 16 * 16;
 }
 size_t TriSched::smem_bytes() const {
-    return trsv_slot_bytes(slot_e, slot_r) * TRSV_D + (size_t)max_size * 8 + (size_t)(max_levels + 1) * 8;
+    return trsv_slot_bytes(slot_e, slot_r) * depth + (size_t)max_size * 8 + (size_t)(max_levels + 1) * 8;
+}
+
+template <int D>
+static void launch_trsv_d(Context* ctx, const TriSched& T, const double* b, double* x) {
+    static size_t attr = 0;
+    const size_t sm = T.smem_bytes();
+    if (attr < sm) {
+        WCB_CUDA(cudaFuncSetAttribute(k_trsv_comp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr = sm;
+    }
+    k_trsv_comp<D><<<(unsigned)T.n_comp, TRSV_THREADS, sm, ctx->stream>>>(
+        T.comp_order.p, T.comp_rows.p, T.comp_lvl.p, T.lvl_off.p, T.lvl_ent.p, T.rows.p, T.sptr.p, T.slcol.p,
+        T.sval.p, T.sdiag.p, b, x, (int)T.max_size, (int)T.max_levels, T.slot_e, T.slot_r);
+}
+static void launch_trsv(Context* ctx, const TriSched& T, const double* b, double* x) {
+    switch (T.depth) {
+        case 3: launch_trsv_d<3>(ctx, T, b, x); break;
+        case 4: launch_trsv_d<4>(ctx, T, b, x); break;
+        case 6: launch_trsv_d<6>(ctx, T, b, x); break;
+        case 8: launch_trsv_d<8>(ctx, T, b, x); break;
+        default: launch_trsv_d<12>(ctx, T, b, x); break;
+    }
 }
 
 // y[perm_r[i]] = b[i]   (row permutation of SuperLU: Pr A Pc = L U)
@@ -467,19 +603,8 @@ static void lu_solve(Context* ctx, wcb_imex_plan* P, DevLU& F, const double* b, 
     k_perm_rows<<<grid1(ctx, n), 256, 0, s>>>(n, F.perm_r.p, b, P->y.p);
     // forward: L w = y  (into z), backward: U v = w (into y)
     if (F.Ls.ok && F.Us.ok) {
-        static bool attr = false;
-        if (!attr) {
-            WCB_CUDA(cudaFuncSetAttribute(k_trsv_comp, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSV_SMEM));
-            attr = true;
-        }
-        k_trsv_comp<<<(unsigned)F.Ls.n_comp, TRSV_THREADS, F.Ls.smem_bytes(), s>>>(
-            F.Ls.comp_rows.p, F.Ls.comp_lvl.p, F.Ls.lvl_off.p, F.Ls.lvl_ent.p, F.Ls.rows.p, F.Ls.sptr.p,
-            F.Ls.slcol.p, F.Ls.sval.p, F.Ls.sdiag.p, P->y.p, P->z.p, (int)F.Ls.max_size,
-            (int)F.Ls.max_levels, F.Ls.slot_e, F.Ls.slot_r);
-        k_trsv_comp<<<(unsigned)F.Us.n_comp, TRSV_THREADS, F.Us.smem_bytes(), s>>>(
-            F.Us.comp_rows.p, F.Us.comp_lvl.p, F.Us.lvl_off.p, F.Us.lvl_ent.p, F.Us.rows.p, F.Us.sptr.p,
-            F.Us.slcol.p, F.Us.sval.p, F.Us.sdiag.p, P->z.p, x, (int)F.Us.max_size,
-            (int)F.Us.max_levels, F.Us.slot_e, F.Us.slot_r);
+        launch_trsv(ctx, F.Ls, P->y.p, P->z.p);
+        launch_trsv(ctx, F.Us, P->z.p, x);
         ctx->launches += 3;
         WCB_CHECK_LAUNCH();
         return;

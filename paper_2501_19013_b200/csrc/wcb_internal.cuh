@@ -256,6 +256,10 @@ struct Operator {
     // set_apply_subset (other rows of y are unspecified); default: full apply
     virtual bool set_apply_subset(const int64_t* /*compact_ids*/, int64_t /*n*/) { return false; }
     virtual void apply_subset(const double* x, double* y) { apply(x, y); }
+    // the plan's 1/m state vector (fixed for the plan's lifetime): operators
+    // may precompute which cells read it (default: every node loads 1/m)
+    virtual void bind_minv(const double* /*d_minv*/) {}
+    double minv_skipped = 0.0;   // DOFs whose 1/m the bound step takes from a table (no 8 B load)
     // algorithmic bytes of one fused step (for the roofline)
     virtual double step_bytes() const = 0;
     // slab halo layout (state rows of out[0] doubles), see wcb_operator_halo;

@@ -90,7 +90,34 @@ struct Scm2DGeo {
     int64_t n_strips;
     int64_t n_rtiles;
     int64_t pitch;            // row pitch of the state (doubles)
+    // per tile (strip-major): every owned node's 1/m equals the interior
+    // table (checked bitwise once per plan) -- the 1/m tile is not loaded.
+    // null: every tile loads 1/m.
+    const uint8_t* tclean;
 };
+
+template <int P>
+struct MinvTab2 {
+    double v[P * P];   // (r, j) of the owned nodes of an interior uncut cell
+};
+
+// tclean[t] for every tile t: 1 when all owned nodes carry minv == tab (bitwise)
+template <int P>
+__global__ void k_clean2d(Scm2DGeo g, int TI, int TJ, MinvTab2<P> tab, const double* __restrict__ minv,
+                          uint8_t* tclean) {
+    const int64_t t = blockIdx.x;
+    const int64_t strip = t / g.n_rtiles, rt = t % g.n_rtiles;
+    const int64_t I0 = g.row_lo + rt * TI, J0 = strip * TJ;
+    bool ok = true;
+    for (int q = threadIdx.x; q < TI * TJ && ok; q += blockDim.x) {
+        const int64_t I = I0 + q / TJ, J = J0 + q % TJ;
+        if (I >= g.row_hi || J >= g.n1y) continue;
+        const double m = minv[(I + P) * g.pitch + J + PADJ];
+        ok = __double_as_longlong(m) == __double_as_longlong(tab.v[(I % P) * P + J % P]);
+    }
+    ok = __syncthreads_and(ok);
+    if (threadIdx.x == 0) tclean[t] = ok ? 1 : 0;
+}
 
 // P consecutive doubles of a lane from shared memory (16-byte loads for
 // even P: the row starts are 16-byte aligned in every tile layout)
@@ -219,7 +246,8 @@ __device__ __forceinline__ void cut_cells_warp(const Scm2DGeo& g, const double* 
 template <int P, int MODE>
 __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
     const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_prev,
-    const __grid_constant__ CUtensorMap tm_minv, Scm2DGeo g, Mats2<P> mt, double sk, StepArgs a) {
+    const __grid_constant__ CUtensorMap tm_minv, Scm2DGeo g, Mats2<P> mt, MinvTab2<P> mtab, double sk,
+    StepArgs a) {
     using T = Tile2<P>;
     constexpr int N = P + 1;
     constexpr int RPE = T::RPE;
@@ -242,14 +270,15 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
     const int64_t strip = tid / g.n_rtiles, rtile = tid % g.n_rtiles;
     if (MODE == MODE_STEP && blockIdx.x == 0) record_observers(a);
     const int64_t J0 = strip * T::TJ, I0 = g.row_lo + rtile * T::TI;
+    const bool tcl = MODE == MODE_STEP && g.tclean && __ldg(g.tclean + tid) != 0;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
-        mbar_expect_tx(bar, (uint32_t)(T::U_BYTES + (epi ? 2 * T::E_BYTES : 0)));
+        mbar_expect_tx(bar, (uint32_t)(T::U_BYTES + (epi ? (tcl ? 1 : 2) * T::E_BYTES : 0)));
         tma_load_2d(smem, &tm_u, (int32_t)(J0 - P - T::CO + PADJ), (int32_t)I0, bar);
         if (epi) {
             tma_load_2d(smem + T::OFF_PREV, &tm_prev, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar);
-            tma_load_2d(smem + T::OFF_MINV, &tm_minv, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar);
+            if (!tcl) tma_load_2d(smem + T::OFF_MINV, &tm_minv, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar);
         }
     }
     // cell codes (and the epilogue's psi_{k-1}, 1/m) while the tile is in flight
@@ -340,7 +369,12 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
                     const double* msm = reinterpret_cast<const double*>(smem + T::OFF_MINV) +
                                         (size_t)(w * P + r) * T::TJ + lane * P;
                     lds_row<P>(ps, up);
-                    lds_row<P>(msm, mi);
+                    if (tcl) {
+                        #pragma unroll
+                        for (int j = 0; j < P; ++j) mi[j] = mtab.v[r * P + j];
+                    } else {
+                        lds_row<P>(msm, mi);
+                    }
                 } else {
                     #pragma unroll
                     for (int j = 0; j < P; ++j) {
@@ -397,7 +431,12 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
 struct ScmOperator final : Operator {
     int dim = 2, p = 4;
     int64_t n_e = 0, n1 = 0, pitch = 0, rows = 0;
-    int64_t pplane = 0, n_zs = 0, n_xt = 0;   // 3D
+    int64_t pplane = 0, n_zs = 0, n_yb = 0, n_xc = 0, xc3 = 0, ex_last = 0;   // 3D streaming grid
+    int64_t probe_base = -1;          // 3D: state index of an interior uncut cell's node (0,0,0)
+    std::vector<double> minv_tab;     // its P^3 owned 1/m values (bind_minv)
+    DevBuf<uint8_t> clean;            // 3D: per local cell: owned 1/m == minv_tab
+    DevBuf<uint8_t> tclean;           // 2D: per tile
+    const double* minv_bound = nullptr;
     // x slab (local numbering): cell rows 0..n_ex-1 (0 = halo row above),
     // node rows 0..n1x-1, owned node rows [row_lo, row_hi)
     int64_t n_ex = 0, n1x = 0, row_lo = 0, row_hi = 0, xstride = 0;
@@ -469,7 +508,12 @@ struct ScmOperator final : Operator {
         const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
         const CUtensorMap& mp = epi ? state_map<P>(a.prev, 1) : mu;
         const CUtensorMap& mm = epi ? state_map<P>(a.minv, 1) : mu;
-        k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(mu, mp, mm, g, mt, sk, a);
+        MinvTab2<P> tab{};
+        if (MODE == MODE_STEP && a.minv && a.minv == minv_bound && tclean.p) {
+            g.tclean = tclean.p;
+            for (int i = 0; i < P * P; ++i) tab.v[i] = minv_tab[i];
+        }
+        k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(mu, mp, mm, g, mt, tab, sk, a);
         ctx->launches++;
     }
     template <int P>
@@ -550,11 +594,21 @@ struct ScmOperator final : Operator {
     }
     template <int P>
     const CUtensorMap& state_map3(const double* ptr) {
-        using T = Tile3<P>;
+        using T = Str3<P>;
         return maps.get(ptr, 3, [&] {
             const uint64_t dims[3] = {(uint64_t)pitch, (uint64_t)rows, (uint64_t)(n1x + 2 * p)};
             const uint64_t strides[2] = {(uint64_t)pitch, (uint64_t)pplane};
-            const uint32_t box[3] = {(uint32_t)T::UW, (uint32_t)T::UR, (uint32_t)T::UP};
+            const uint32_t box[3] = {(uint32_t)T::UW, (uint32_t)T::UR, 1u};
+            return make_map_f64(ptr, 3, dims, strides, box);
+        });
+    }
+    template <int P>
+    const CUtensorMap& prev_map3(const double* ptr) {   // owned box of one cell row
+        using T = Str3<P>;
+        return maps.get(ptr, 4, [&] {
+            const uint64_t dims[3] = {(uint64_t)pitch, (uint64_t)rows, (uint64_t)(n1x + 2 * p)};
+            const uint64_t strides[2] = {(uint64_t)pitch, (uint64_t)pplane};
+            const uint32_t box[3] = {(uint32_t)T::TZ, (uint32_t)(T::WY * P), (uint32_t)P};
             return make_map_f64(ptr, 3, dims, strides, box);
         });
     }
@@ -568,9 +622,98 @@ struct ScmOperator final : Operator {
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
         launch_cut_pre<P>(ctx, n_cut, KP.p, cut_base.p, pplane, pitch, a.cur, cut_out.p);
-        Scm3DGeo g{n_ex, row_lo, row_hi, n_e, n1, pitch, pplane, mask.p, cut_id.p, KT.p, cut_out.p, cflags.p,
-                   n_zs, n_xt};
-        launch_scm3d<P, MODE>(ctx, state_map3<P>(a.cur), g, mt, sk, a);
+        Scm3DGeo g = geo3();
+        MinvTab<P> tab{};
+        if (MODE == MODE_STEP && a.minv && a.minv == minv_bound && clean.p) {
+            g.clean = clean.p;
+            for (int i = 0; i < P * P * P; ++i) tab.v[i] = minv_tab[i];
+        }
+        const CUtensorMap& mu = state_map3<P>(a.cur);
+        launch_scm3d<P, MODE>(ctx, mu, MODE == MODE_STEP ? prev_map3<P>(a.prev) : mu, g, mt, tab, sk, a);
+    }
+    Scm3DGeo geo3() const {
+        return Scm3DGeo{n_ex, row_lo, row_hi, n_e, n1, pitch, pplane, mask.p, cut_id.p, cut_out.p, cflags.p,
+                        n_zs, n_yb, n_xc, xc3, ex_last, nullptr};
+    }
+    template <int P>
+    void bind3(const double* d_minv) {
+        MinvTab<P> tab{};
+        std::vector<double> h(P * P * P);
+        for (int q = 0; q < P; ++q)
+            for (int r = 0; r < P; ++r)
+                WCB_CUDA(cudaMemcpyAsync(h.data() + (q * P + r) * P, d_minv + probe_base + q * pplane + r * pitch,
+                                         P * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < P * P * P; ++i) {
+            if (!(h[i] > 0.0)) return;   // probe is not a DOF cell: keep loading 1/m everywhere
+            tab.v[i] = h[i];
+        }
+        if (!clean.p) clean.alloc((size_t)n_ex * n_e * n_e);
+        launch_clean3d<P>(ctx, geo3(), tab, d_minv, clean.p);
+        WCB_CHECK_LAUNCH();
+        std::vector<uint8_t> hc(clean.n);
+        WCB_CUDA(cudaMemcpyAsync(hc.data(), clean.p, hc.size(), cudaMemcpyDeviceToHost, ctx->stream));
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        int64_t nclean = 0;
+        for (uint8_t v : hc) nclean += v;
+        minv_skipped = (double)nclean * P * P * P;
+        minv_tab = h;
+        minv_bound = d_minv;
+    }
+    template <int P>
+    void bind2(const double* d_minv) {
+        using T = Tile2<P>;
+        MinvTab2<P> tab{};
+        std::vector<double> h(P * P);
+        for (int r = 0; r < P; ++r)
+            WCB_CUDA(cudaMemcpyAsync(h.data() + r * P, d_minv + probe_base + r * pitch, P * sizeof(double),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < P * P; ++i) {
+            if (!(h[i] > 0.0)) return;
+            tab.v[i] = h[i];
+        }
+        const int64_t nt = n_strips * n_rtiles;
+        if (!tclean.p) tclean.alloc((size_t)nt);
+        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, order.p, n_strips, n_rtiles,
+                   pitch, nullptr};
+        k_clean2d<P><<<(unsigned)nt, 128, 0, ctx->stream>>>(g, T::TI, T::TJ, tab, d_minv, tclean.p);
+        ctx->launches++;
+        WCB_CHECK_LAUNCH();
+        std::vector<uint8_t> hc(nt);
+        WCB_CUDA(cudaMemcpyAsync(hc.data(), tclean.p, nt, cudaMemcpyDeviceToHost, ctx->stream));
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        minv_skipped = 0.0;
+        for (int64_t t = 0; t < nt; ++t)
+            if (hc[t]) {
+                const int64_t I0 = row_lo + (t % n_rtiles) * T::TI, J0 = (t / n_rtiles) * T::TJ;
+                minv_skipped += (double)(std::min<int64_t>(T::TI, row_hi - I0) * std::min<int64_t>(T::TJ, n1 - J0));
+            }
+        minv_tab = h;
+        minv_bound = d_minv;
+    }
+    void bind_minv(const double* d_minv) override {
+        minv_bound = nullptr;
+        minv_skipped = 0.0;
+        if (probe_base < 0 || !d_minv || getenv("WAVECELL_B200_NO_MINV_TAB")) return;
+        if (dim == 2) {
+            if (ncomp != 1 || !WCB2D_EPI_TMA) return;
+            switch (p) {
+                case 1: bind2<1>(d_minv); break;
+                case 2: bind2<2>(d_minv); break;
+                case 3: bind2<3>(d_minv); break;
+                case 4: bind2<4>(d_minv); break;
+                case 5: bind2<5>(d_minv); break;
+                case 6: bind2<6>(d_minv); break;
+            }
+            return;
+        }
+        switch (p) {
+            case 1: bind3<1>(d_minv); break;
+            case 2: bind3<2>(d_minv); break;
+            case 3: bind3<3>(d_minv); break;
+            case 4: bind3<4>(d_minv); break;
+        }
     }
     template <int MODE>
     void dispatch3d(const StepArgs& a) {
@@ -740,6 +883,27 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
             WCB_REQUIRE(v >= 0 && v <= 2, "cell_class values must be 0, 1 or 2");
             cls[(gx - lo + 1) * cells_row + c] = v;
         }
+    // 3D probe for the interior 1/m table: a cell (local row >= 2) whose 8
+    // cells sharing its owned corner block are all uncut
+    if (dim == 3) {
+        auto C = [&](int64_t x, int64_t y, int64_t z) { return cls[(x * n_e + y) * n_e + z]; };
+        for (int64_t x = std::max<int64_t>(2, op->n_ex / 2); x < op->n_ex && op->probe_base < 0; ++x)
+            for (int64_t y = std::max<int64_t>(1, n_e / 2); y < n_e && op->probe_base < 0; ++y)
+                for (int64_t z = std::max<int64_t>(1, n_e / 2); z < n_e && op->probe_base < 0; ++z) {
+                    bool ok = (x * p + p - 1) < op->row_hi;
+                    for (int d = 0; d < 8 && ok; ++d) ok = C(x - (d >> 2), y - ((d >> 1) & 1), z - (d & 1)) == 1;
+                    if (ok) op->probe_base = (x * p + p) * op->xstride + (y * p + p) * op->pitch + z * p + PADJ;
+                }
+    }
+    if (dim == 2 && ncomp == 1) {
+        auto C = [&](int64_t x, int64_t y) { return cls[x * n_e + y]; };
+        for (int64_t x = std::max<int64_t>(2, op->n_ex / 2); x < op->n_ex && op->probe_base < 0; ++x)
+            for (int64_t y = std::max<int64_t>(1, n_e / 2); y < n_e && op->probe_base < 0; ++y) {
+                bool ok = (x * p + p - 1) < op->row_hi;
+                for (int d = 0; d < 4 && ok; ++d) ok = C(x - (d >> 1), y - (d & 1)) == 1;
+                if (ok) op->probe_base = (x * p + p) * op->xstride + y * p + PADJ;
+            }
+    }
     // mask with a zero ring
     std::vector<uint8_t> mask;
     if (dim == 2) {
@@ -756,18 +920,37 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
                     mask[((i + 1) * s_ + (j + 1)) * s_ + (k + 1)] = (uint8_t)cls[(i * n_e + j) * n_e + k];
     }
     // owned DOFs -> state index; tile flags
-    const int RX = ncomp == 2 ? rpe_e(p) : dim == 2 ? rpe_for(p) : rx_for3(p);
+    const int RX = ncomp == 2 ? rpe_e(p) : dim == 2 ? rpe_for(p) : 1;
     const int64_t TI = (int64_t)RX * p;
     const int64_t n_tiles_x = ceil_div(op->row_hi - op->row_lo, TI);
     std::vector<uint8_t> cf;
+    int64_t WY3 = 1;
     if (dim == 2) {
         op->n_strips = ceil_div(n1, TJ);
         op->n_rtiles = n_tiles_x;
         cf.assign(op->n_rtiles * op->n_strips, 0);
     } else {
-        op->n_zs = ceil_div(n1, TJ);
-        op->n_xt = n_tiles_x;
-        cf.assign(op->n_xt * (n_e + 1) * op->n_zs, 0);
+        // streaming 3D grid: z strips of 32 cells (the node column z = n1-1 of
+        // a grid with n_e % 32 == 0 goes to k_scm3d_zcol), y blocks of WY cell
+        // rows, x chunks sized so the grid fills the resident CTA slots
+        WY3 = p == 1 ? wy_for3(1) : p == 2 ? wy_for3(2) : p == 3 ? wy_for3(3) : wy_for3(4);
+        op->n_zs = ceil_div(n_e, 32);
+        op->n_yb = ceil_div(n_e + 1, WY3);   // cell rows 0..n_e (row n_e: the last node row)
+        op->ex_last = (op->row_hi - 1) / p;
+        const int64_t rows_out = op->ex_last;                  // cell rows 1..ex_last
+        const int64_t slots = (int64_t)ctx->sm_count * (p == 1 ? cpsm_for3(1) : p == 2 ? cpsm_for3(2) : p == 3 ? cpsm_for3(3) : cpsm_for3(4));
+        const int64_t per_chunk = op->n_zs * op->n_yb;
+        // waves x (rows per chunk + its halo row), minimised over the chunk count
+        int64_t nxc = 1;
+        double best = 1e300;
+        for (int64_t c = 1; c <= std::min<int64_t>(rows_out, 32); ++c) {
+            const double cost = (double)ceil_div(per_chunk * c, slots) * (double)(ceil_div(rows_out, c) + 1);
+            if (cost < best - 1e-9) { best = cost; nxc = c; }
+        }
+        if (const char* e = getenv("WAVECELL_B200_XCHUNKS")) nxc = std::max<int64_t>(1, std::min<int64_t>(atoll(e), rows_out));
+        op->xc3 = ceil_div(rows_out, nxc);
+        op->n_xc = ceil_div(rows_out, op->xc3);
+        cf.assign(op->n_xc * op->n_yb * op->n_zs, 0);
     }
     op->sidx.resize(op->n);
     const int64_t x0 = lo * p - p;   // global node row of local row 0
@@ -784,7 +967,10 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
         } else {
             const int64_t J = rest / n1, K = rest % n1;
             op->sidx[i] = (Il + p) * op->xstride + (J + p) * op->pitch + K + PADJ;
-            cf[(t * (n_e + 1) + J / p) * op->n_zs + K / TJ] = 1;
+            // owner: x cell row (Il-1)/p+1 ... plane Il belongs to cell row Il/p (local a = Il%p)
+            const int64_t exo = Il / p, eyo = J / p, ezo = std::min<int64_t>(K / p, n_e - 1);
+            const int64_t xcx = (exo - 1) / op->xc3;
+            cf[(xcx * op->n_yb + eyo / WY3) * op->n_zs + ezo / 32] = 1;
         }
     }
     for (int64_t i = 0; i < (ncomp - 1) * d->n_dof; ++i) op->sidx[d->n_dof + i] = op->plane + op->sidx[i];

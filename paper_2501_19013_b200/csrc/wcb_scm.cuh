@@ -47,7 +47,9 @@ struct Mats2 {
 };
 
 
-// 3D launch description (wcb_scm3d.cu)
+// 3D launch description (wcb_scm3d.cu).  A CTA owns one z strip (32 cells,
+// lane = z cell) x WY y cell rows (one warp each) x one chunk of x cell rows,
+// and streams node planes along x through a TMA ring.
 struct Scm3DGeo {
     int64_t n_ex;             // local x cell rows (incl. the halo row 0)
     int64_t row_lo, row_hi;   // owned local x node planes
@@ -55,36 +57,65 @@ struct Scm3DGeo {
     int64_t n1;               // nodes along y and z
     int64_t prow;             // row pitch (doubles, z fastest)
     int64_t pplane;           // plane pitch (doubles)
-    const uint8_t* mask;      // (n_e+2)^3 cell codes with a ring of 0: 0 out, 1 uncut, 2 cut
-    const int32_t* cut_id;    // n_e^3 -> cut index or -1
-    const double* KT;         // unused in 3D (cut products come from cut_out)
+    const uint8_t* mask;      // (n_ex+2)(n_e+2)^2 cell codes with a ring of 0: 0 out, 1 uncut, 2 cut
+    const int32_t* cut_id;    // n_ex n_e^2 -> cut index or -1
     const double* cut_out;    // n_cut * L: K_o u_e / sk of every cut cell (k_cut_pre)
-    const uint8_t* cflags;    // per CTA tile (z strip, y row, x tile): owns a DOF
+    const uint8_t* cflags;    // per CTA (x chunk, y block, z strip): owns a DOF
     int64_t n_zs;             // z strips
-    int64_t n_xt;             // x tiles
+    int64_t n_yb;             // y blocks
+    int64_t n_xc;             // x chunks
+    int64_t xc;               // x cell rows per chunk
+    int64_t ex_last;          // last local x cell row holding an owned node plane
+    // cells whose P^3 owned nodes all carry the interior 1/m of minv_tab
+    // (bitwise, checked on the device once per plan): the epilogue skips the
+    // 1/m stream there.  null: every node loads 1/m.
+    const uint8_t* clean;
 };
 
-__host__ __device__ constexpr int rx_for3(int P) { return P <= 3 ? 4 : 2; }
-
-// box of the 3D psi tile (z, y, x extents)
 template <int P>
-struct Tile3 {
-    static constexpr int RX = rx_for3(P);          // x element rows per CTA (+1 halo warp)
-    static constexpr int NWARP = RX + 1;
+struct MinvTab {
+    double v[P * P * P];   // (a, b, j) of the owned nodes of an interior uncut cell
+};
+
+// Streaming tile shape per degree: WY compute warps + 1 (halo y row and TMA
+// producer); ring of S node planes = the P+1 planes of the current cell row
+// plus LA planes of look-ahead.
+#ifndef WCB3D_REUSE
+#define WCB3D_REUSE 1
+#endif
+#ifndef WCB3D_WY3
+#define WCB3D_WY3 3
+#endif
+__host__ __device__ constexpr int wy_for3(int P) { return P <= 2 ? 7 : P == 3 ? WCB3D_WY3 : 2; }
+// resident CTAs per SM the launch bounds ask for
+__host__ __device__ constexpr int cpsm_for3(int P) { return P == 3 && WCB3D_WY3 >= 7 ? 1 : P <= 3 ? 2 : 1; }
+__host__ __device__ constexpr int la_for3(int P) { return P <= 3 ? P : 1; }
+
+template <int P>
+struct Str3 {
+    static constexpr int WY = wy_for3(P);
+    static constexpr int NWARP = WY + 1;
     static constexpr int TZ = 32 * P;               // owned node columns (z)
     static constexpr int CO = P & 1;                // 16-byte TMA alignment offset
     static constexpr int UW = ((TZ + P + 1 + CO) + 1) / 2 * 2;
-    static constexpr int UR = 2 * P + 1;            // y rows (ey-1)*P .. ey*P+P
-    static constexpr int UP = RX * P + P + 1;       // x planes (ex0-1)*P .. (ex0+RX)*P
-    static constexpr size_t U_BYTES = (size_t)UW * UR * UP * 8;
-    static constexpr size_t OFF_CARRY = (U_BYTES + 127) / 128 * 128;   // [RX+1][P*P][32]
-    static constexpr size_t OFF_BAR = OFF_CARRY + (size_t)(RX + 1) * P * P * 32 * 8;
-    static constexpr size_t SMEM = OFF_BAR + 8;
+    static constexpr int UR = (WY + 1) * P + 1;     // y rows (ey0-1)*P .. (ey0+WY)*P
+    static constexpr int PLANE = UW * UR;           // doubles per ring slot
+    static constexpr int S = P + 1 + la_for3(P);    // ring slots
+    static constexpr int SLOT = (PLANE * 8 + 127) / 128 * 128 / 8;   // slot stride (doubles, 128 B aligned)
+    static constexpr size_t RING_BYTES = (size_t)S * SLOT * 8;
+    static constexpr size_t OFF_XCH = (RING_BYTES + 127) / 128 * 128;   // [2][NWARP][2P][32]
+    static constexpr size_t OFF_PREV = OFF_XCH + (size_t)2 * NWARP * 2 * P * 32 * 8;   // [P][WY*P][TZ]
+    static constexpr size_t PREV_BYTES = (size_t)P * WY * P * TZ * 8;
+    static constexpr size_t OFF_BAR = OFF_PREV + (PREV_BYTES + 127) / 128 * 128;
+    static constexpr size_t SMEM = OFF_BAR + 8 * (S + 1);
 };
 
 template <int P, int MODE>
-void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const Scm3DGeo& g, const Mats2<P>& mt,
-                  double sk, const StepArgs& a);
+void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map_p, const Scm3DGeo& g,
+                  const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a);
+// clean[c] = 1 when every owned node of local cell c has minv == tab (bitwise)
+template <int P>
+void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean);
 // dense cut-cell products u_e -> K_o u_e / sk (packed symmetric K), before the stencil
 template <int P>
 void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t* cut_base,

@@ -25,7 +25,7 @@ __device__ __forceinline__ void zpass_row(const double (&mc)[orb_count(P)],
                                           const double (&kc)[orb_count(P)], const double* row,
                                           int lane, double (&zmR)[P], double (&zkR)[P],
                                           double& zmL, double& zkL) {
-    row += Tile3<P>::CO;
+    row += Str3<P>::CO;
     const double* own_p = row + P + lane * P;
     double own[P];
     #pragma unroll
@@ -155,49 +155,64 @@ void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t
     ctx->launches++;
 }
 
+// Streaming stencil + fused CDM epilogue.  Per node plane c of x cell row ex
+// (planes ex*P .. ex*P+P, TMA ring): each warp z-contracts the P+1 y rows of
+// its cell row and y-contracts them into Au/Bu for its P+1 output rows; row P
+// (shared with the next cell row) goes to the next warp through shared memory
+// and is added to that warp's row 0 (the halo warp supplies it for the first
+// row); the x pass accumulates Y[a] += k1[a][c] Au + m1[a][c] Bu in registers.
+// After plane c = P the cut-cell products are added, planes a < P are final
+// (epilogue), and Y[P] becomes Y[0] of the next cell row.  Each chunk of x
+// cell rows starts one row early (no epilogue) to build that carry, so every
+// node value is the same fixed-order sum whatever the chunking (slabs too).
 template <int P, int MODE>
-__global__ void __launch_bounds__(Tile3<P>::NWARP * 32) k_scm3d(const __grid_constant__ CUtensorMap tm_u,
-                                                               Scm3DGeo g, Mats2<P> mt, double sk,
-                                                               StepArgs a) {
-    using T = Tile3<P>;
+__global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
+    k_scm3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_p, Scm3DGeo g,
+            Mats2<P> mt, MinvTab<P> mtab, double sk, StepArgs a) {
+    using T = Str3<P>;
     constexpr int N = P + 1;
-    constexpr int RX = T::RX;
+    constexpr int WY = T::WY;
+    constexpr int S = T::S;
     extern __shared__ __align__(128) unsigned char smem[];
-    const double* us = reinterpret_cast<const double*>(smem);
-    double* carry = reinterpret_cast<double*>(smem + T::OFF_CARRY);   // [RX+1][P*P][32]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
+    const double* ring = reinterpret_cast<const double*>(smem);
+    double* xch = reinterpret_cast<double*>(smem + T::OFF_XCH);   // [2][NWARP][2P][32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
+    uint64_t* pbar = full + S;                                           // psi_{k-1} of a cell row
+    const double* prv = reinterpret_cast<const double*>(smem + T::OFF_PREV);   // [P][WY*P][TZ]
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
-    const int64_t zs = blockIdx.x, ey = blockIdx.y, xt = blockIdx.z;
-    if (MODE == MODE_STEP && zs == 0 && ey == 0 && xt == 0) record_observers(a);
-    if (!g.cflags[(xt * (g.n_e + 1) + ey) * g.n_zs + zs]) return;
+    const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z;
+    if (MODE == MODE_STEP && zs == 0 && yb == 0 && xc == 0) record_observers(a);
+    if (!g.cflags[(xc * g.n_yb + yb) * g.n_zs + zs]) return;
     const int64_t K0 = zs * T::TZ;
-    const int64_t ex0 = g.row_lo / P + xt * RX;
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        mbar_expect_tx(bar, (uint32_t)T::U_BYTES);
-        tma_load_3d(smem, &tm_u, (int32_t)(K0 - P - T::CO + PADJ), (int32_t)(ey * P),
-                    (int32_t)(ex0 * P), bar);
-    }
-    const bool halo = (w == RX);
-    const int64_t ex = halo ? ex0 - 1 : ex0 + w;
+    const int64_t ey0 = yb * WY;
+    const int64_t exA = 1 + xc * g.xc;                                   // first row with an epilogue
+    const int64_t exE = exA + g.xc < g.ex_last + 1 ? exA + g.xc : g.ex_last + 1;
+    const int64_t G0 = (exA - 1) * P, G1 = (exE - 1) * P + P;           // node planes streamed
+    const bool halo = (w == WY);
+    const int64_t ey = halo ? ey0 - 1 : ey0 + w;                         // this warp's cell row
     const int64_t ez = K0 / P + lane;
-    // cell codes of the 4 (y, z) neighbours in this x cell row
-    uint8_t cRR = 0, cRL = 0, cUR = 0, cUL = 0;   // (ey, ez), (ey, ez-1), (ey-1, ez), (ey-1, ez-1)
-    if (ex >= 0 && ex < g.n_ex && ez <= g.n_e) {
-        const int64_t s_ = g.n_e + 2;
-        const uint8_t* mrow = g.mask + ((ex + 1) * s_ + (ey + 1)) * s_;
-        if (ey < g.n_e) { cRR = __ldg(mrow + ez + 1); cRL = __ldg(mrow + ez); }
-        const uint8_t* urow = mrow - s_;
-        if (ey >= 1) { cUR = __ldg(urow + ez + 1); cUL = __ldg(urow + ez); }
+    const int trow = (halo ? 0 : w + 1) * P;                             // tile row of node row ey*P
+    const bool producer = halo && lane == 0;
+    auto issue = [&](int64_t gp) {   // plane gp -> its ring slot
+        const int s = (int)((gp - G0) % S);
+        mbar_expect_tx(&full[s], (uint32_t)(T::PLANE * 8));
+        tma_load_3d(smem + (size_t)s * T::SLOT * 8, &tm_u, (int32_t)(K0 - P - T::CO + PADJ),
+                    (int32_t)(ey0 * P), (int32_t)(gp + P), &full[s]);
+    };
+    if (threadIdx.x == 0) {
+        #pragma unroll
+        for (int s = 0; s < S + 1; ++s) mbar_init(&full[s], 1);
     }
+    __syncthreads();
+    if (producer)
+        for (int64_t gp = G0; gp <= G1 && gp < G0 + S; ++gp) issue(gp);
     double mc[orb_count(P)], kc[orb_count(P)];
     #pragma unroll
     for (int i = 0; i < orb_count(P); ++i) { mc[i] = mt.m[i]; kc[i] = mt.k[i]; }
-    __syncthreads();
-    mbar_wait(bar, 0);
-
-    const int po = halo ? 0 : (w + 1) * P;   // tile plane of node plane ex*P
+    const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
+    const int64_t s_ = g.n_e + 2;
+    const int up = halo ? WY : (w == 0 ? WY : w - 1);   // exchange source warp
     double Y[N][P][P];
     #pragma unroll
     for (int r = 0; r < N; ++r)
@@ -205,138 +220,264 @@ __global__ void __launch_bounds__(Tile3<P>::NWARP * 32) k_scm3d(const __grid_con
         for (int b = 0; b < P; ++b)
             #pragma unroll
             for (int j = 0; j < P; ++j) Y[r][b][j] = 0.0;
-    if (__any_sync(0xffffffffu, (cRR | cRL | cUR | cUL) != 0)) {
-        const double xRR = cRR == 1, xRL = cRL == 1, xUR = cUR == 1, xUL = cUL == 1;
+    unsigned long long amp = 0ULL;
+    // Au/Bu persist across cell rows: plane P of row ex is plane 0 of row
+    // ex+1, so when no uncut flag of the CTA changes between the rows its
+    // (exchanged) y/z contraction is reused instead of recomputed
+    double Au[N][P], Bu[N][P];
+    bool pxRR = false, pxRL = false;
+    for (int64_t ex = exA - 1; ex < exE; ++ex) {
+        // codes of (ex, ey, ez), (ex, ey, ez-1), (ex, ey-1, ez), (ex, ey-1, ez-1)
+        uint8_t cRR = 0, cRL = 0, cUR = 0, cUL = 0;
+        if (ex >= 0 && ex < g.n_ex && ez <= g.n_e && ey >= -1 && ey <= g.n_e) {
+            const uint8_t* mrow = g.mask + ((ex + 1) * s_ + (ey + 1)) * s_;
+            if (ey < g.n_e && ey >= 0) { cRR = __ldg(mrow + ez + 1); cRL = __ldg(mrow + ez); }
+            if (!halo && ey >= 1) { cUR = __ldg(mrow - s_ + ez + 1); cUL = __ldg(mrow - s_ + ez); }
+        }
+        const double xRR = cRR == 1, xRL = cRL == 1;
+        const bool cln = g.clean && cRR == 1 && ex >= 1 && __ldg(g.clean + (ex * g.n_e + ey) * g.n_e + ez) != 0;
+        const bool live = __syncthreads_or((cRR | cRL) != 0);   // any uncut/cut work in this CTA row
+#if WCB3D_REUSE
+        const bool reuse = ex > exA - 1 && !__syncthreads_or((cRR == 1) != pxRR || (cRL == 1) != pxRL);
+#else
+        const bool reuse = false;
+#endif
+        pxRR = cRR == 1;
+        pxRL = cRL == 1;
         #pragma unroll
         for (int c = 0; c < N; ++c) {
-            const double* plane = us + (size_t)(po + c) * T::UR * T::UW;
-            double Au[P][P], Bu[P][P];
+          if (!(c == 0 && reuse)) {   // CTA-uniform
+            const int64_t gp = ex * P + c;
+            const int slot = (int)((gp - G0) % S);
+            const double* plane = ring + (size_t)slot * T::SLOT;
             #pragma unroll
-            for (int b = 0; b < P; ++b)
+            for (int b = 0; b < N; ++b)
                 #pragma unroll
                 for (int j = 0; j < P; ++j) { Au[b][j] = 0.0; Bu[b][j] = 0.0; }
-            #pragma unroll
-            for (int e = -P; e <= P; ++e) {
-                double zmR[P], zkR[P], zmL, zkL;
-                zpass_row<P>(mc, kc, plane + (size_t)(e + P) * T::UW, lane, zmR, zkR, zmL, zkL);
-                if (e >= 0) {   // local row e of cell row ey
+            mbar_wait(&full[slot], (uint32_t)(((gp - G0) / S) & 1));
+            if (live) {
+                #pragma unroll
+                for (int e = 0; e < N; ++e) {
+                    double zmR[P], zkR[P], zmL, zkL;
+                    zpass_row<P>(mc, kc, plane + (size_t)(trow + e) * T::UW, lane, zmR, zkR, zmL, zkL);
                     double am[P], ak[P];
                     #pragma unroll
                     for (int j = 0; j < P; ++j) { am[j] = xRR * zmR[j]; ak[j] = xRR * zkR[j]; }
                     am[0] = fma(xRL, zmL, am[0]);
                     ak[0] = fma(xRL, zkL, ak[0]);
                     #pragma unroll
-                    for (int b = 0; b < P; ++b)
+                    for (int b = 0; b < N; ++b) {
+                        if (halo && b < P) continue;
                         #pragma unroll
                         for (int j = 0; j < P; ++j) {
                             Au[b][j] = fma(mc[orb(P, b, e)], am[j], Au[b][j]);
                             Bu[b][j] = fma(kc[orb(P, b, e)], am[j], fma(mc[orb(P, b, e)], ak[j], Bu[b][j]));
                         }
-                }
-                if (e <= 0) {   // local row e+P of cell row ey-1 -> our y row 0
-                    double am[P], ak[P];
-                    #pragma unroll
-                    for (int j = 0; j < P; ++j) { am[j] = xUR * zmR[j]; ak[j] = xUR * zkR[j]; }
-                    am[0] = fma(xUL, zmL, am[0]);
-                    ak[0] = fma(xUL, zkL, ak[0]);
-                    #pragma unroll
-                    for (int j = 0; j < P; ++j) {
-                        Au[0][j] = fma(mc[orb(P, P, e + P)], am[j], Au[0][j]);
-                        Bu[0][j] = fma(kc[orb(P, P, e + P)], am[j], fma(mc[orb(P, P, e + P)], ak[j], Bu[0][j]));
                     }
                 }
             }
+            double* xw = xch + ((size_t)((gp & 1) * T::NWARP + w) * 2 * P) * 32 + lane;
             #pragma unroll
-            for (int r = 0; r < N; ++r)
+            for (int j = 0; j < P; ++j) { xw[j * 32] = Au[P][j]; xw[(P + j) * 32] = Bu[P][j]; }
+            __syncthreads();
+            if (producer && c == 1 && ex >= exA) {   // row ex-1's epilogue is done: refill its planes
+                #pragma unroll 1
+                for (int q = 0; q < P; ++q) {
+                    const int64_t np = (ex - 1) * P + q + S;
+                    if (np <= G1) issue(np);
+                }
+                if (MODE == MODE_STEP) {   // psi_{k-1} of row ex's owned nodes for its epilogue
+                    mbar_expect_tx(pbar, (uint32_t)T::PREV_BYTES);
+                    tma_load_3d(smem + T::OFF_PREV, &tm_p, (int32_t)(K0 + PADJ), (int32_t)(ey0 * P + P),
+                                (int32_t)(ex * P + P), pbar);
+                }
+            }
+            if (!halo) {
+                const double* xr = xch + ((size_t)((gp & 1) * T::NWARP + up) * 2 * P) * 32 + lane;
                 #pragma unroll
-                for (int b = 0; b < P; ++b)
+                for (int j = 0; j < P; ++j) { Au[0][j] += xr[j * 32]; Bu[0][j] += xr[(P + j) * 32]; }
+            }
+          }
+            // x pass (plane 0 of a reused row takes the previous row's plane-P Au/Bu)
+            if (!halo) {
+                #pragma unroll
+                for (int r = 0; r < N; ++r)
                     #pragma unroll
-                    for (int j = 0; j < P; ++j)
-                        Y[r][b][j] = fma(kc[orb(P, r, c)], Au[b][j], fma(mc[orb(P, r, c)], Bu[b][j], Y[r][b][j]));
+                    for (int b = 0; b < P; ++b)
+                        #pragma unroll
+                        for (int j = 0; j < P; ++j)
+                            Y[r][b][j] = fma(kc[orb(P, r, c)], Au[b][j], fma(mc[orb(P, r, c)], Bu[b][j], Y[r][b][j]));
+            }
         }
-        // dense cut cells: own y row (ey) and the y-up row (ey-1)
-        const unsigned clR = __ballot_sync(0xffffffffu, cRR == 2);
-        const bool edR = __shfl_sync(0xffffffffu, cRL == 2, 0);
-#ifndef WCB3D_NOCUT
-        if (clR || edR) cut_cells_warp3<P>(g, ex, ey, K0 / P, lane, clR, edR, false, Y);
-#endif
-        const unsigned clU = __ballot_sync(0xffffffffu, cUR == 2);
-        const bool edU = __shfl_sync(0xffffffffu, cUL == 2, 0);
-#ifndef WCB3D_NOCUT
-        if (clU || edU) cut_cells_warp3<P>(g, ex, ey - 1, K0 / P, lane, clU, edU, true, Y);
-#endif
-    }
-    // x plane a = P of cell row ex is plane a = 0 of cell row ex+1
-    #pragma unroll
-    for (int b = 0; b < P; ++b)
-        #pragma unroll
-        for (int j = 0; j < P; ++j)
-            carry[((halo ? 0 : w + 1) * P * P + b * P + j) * 32 + lane] = Y[P][b][j];
-    __syncthreads();
-    unsigned long long amp = 0ULL;
-    if (!halo) {
-        #pragma unroll
-        for (int b = 0; b < P; ++b)
-            #pragma unroll
-            for (int j = 0; j < P; ++j)
-                Y[0][b][j] = carry[(w * P * P + b * P + j) * 32 + lane] + Y[0][b][j];
-        const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
-        const int64_t Kl = K0 + lane * P;
-        #pragma unroll
-        for (int r = 0; r < P; ++r) {
-            const int64_t I = ex * P + r;
-            if (I >= g.row_hi) break;
-            #pragma unroll
-            for (int b = 0; b < P; ++b) {
-                const int64_t J = ey * P + b;
-                if (J >= g.n1) break;
-                const int64_t base = (I + P) * g.pplane + (J + P) * g.prow + Kl + PADJ;
-                const double* urow = us + ((size_t)(po + r) * T::UR + P + b) * T::UW + T::CO + P + lane * P;
-                if constexpr (MODE == MODE_APPLY) {
+        if (!halo) {
+            // dense cut cells: own y row (ey) and the y-up row (ey-1)
+            const unsigned clR = __ballot_sync(0xffffffffu, cRR == 2);
+            const bool edR = __shfl_sync(0xffffffffu, cRL == 2, 0);
+            if (clR || edR) cut_cells_warp3<P>(g, ex, ey, K0 / P, lane, clR, edR, false, Y);
+            const unsigned clU = __ballot_sync(0xffffffffu, cUR == 2);
+            const bool edU = __shfl_sync(0xffffffffu, cUL == 2, 0);
+            if (clU || edU) cut_cells_warp3<P>(g, ex, ey - 1, K0 / P, lane, clU, edU, true, Y);
+            if (ex >= exA) {
+                if (MODE == MODE_STEP) mbar_wait(pbar, (uint32_t)((ex - exA) & 1));
+                const int64_t Kl = K0 + lane * P;
+                #pragma unroll
+                for (int r = 0; r < P; ++r) {
+                    const int64_t I = ex * P + r;
+                    if (I >= g.row_hi) break;
+                    const double* pl = ring + (size_t)((I - G0) % S) * T::SLOT;
                     #pragma unroll
-                    for (int j = 0; j < P; ++j)
-                        if (Kl + j < g.n1) a.out[base + j] = sk * Y[r][b][j];
-                } else {
-                    const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
-                    #pragma unroll
-                    for (int j = 0; j < P; ++j) {
-                        if (Kl + j < g.n1) {
-                            const double fF = src ? f * source_at(a.F, base + j) : f * 0.0;
-                            const double mi = __ldg(a.minv + base + j);
-                            const double v = leapfrog(urow[j], a.prev[base + j], sk * Y[r][b][j], mi,
-                                                      fF, a.dt2);
-                            a.out[base + j] = v;
-                            unsigned long long bits = mi != 0.0 ? amp_bits(v) : 0ULL;
-                            amp = bits > amp ? bits : amp;
+                    for (int b = 0; b < P; ++b) {
+                        const int64_t J = ey * P + b;
+                        if (J >= g.n1) break;
+                        const int64_t base = (I + P) * g.pplane + (J + P) * g.prow + Kl + PADJ;
+                        if constexpr (MODE == MODE_APPLY) {
+                            #pragma unroll
+                            for (int j = 0; j < P; ++j)
+                                if (Kl + j < g.n1) a.out[base + j] = sk * Y[r][b][j];
+                        } else {
+                            const double* urow = pl + (size_t)(trow + b) * T::UW + T::CO + P + lane * P;
+                            const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
+                            #pragma unroll
+                            for (int j = 0; j < P; ++j) {
+                                if (Kl + j < g.n1) {
+                                    const double fF = src ? f * source_at(a.F, base + j) : f * 0.0;
+                                    const double mi = cln ? mtab.v[(r * P + b) * P + j] : __ldg(a.minv + base + j);
+                                    const double up = prv[((size_t)r * WY * P + w * P + b) * T::TZ + lane * P + j];
+                                    const double v = leapfrog(urow[j], up, sk * Y[r][b][j], mi, fF, a.dt2);
+                                    a.out[base + j] = v;
+                                    const unsigned long long bits = mi != 0.0 ? amp_bits(v) : 0ULL;
+                                    amp = bits > amp ? bits : amp;
+                                }
+                            }
                         }
                     }
                 }
             }
+            // x plane P of cell row ex is plane 0 of cell row ex+1
+            #pragma unroll
+            for (int b = 0; b < P; ++b)
+                #pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    Y[0][b][j] = Y[P][b][j];
+                    #pragma unroll
+                    for (int r = 1; r < N; ++r) Y[r][b][j] = 0.0;
+                }
         }
     }
     if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
 }
 
+// The node column z = n1-1 when n_e is a multiple of 32 (no strip lane owns
+// it): one thread per (x plane, y row), direct sum over the <= 4 cells
+// (ex, ey, n_e-1) containing the node, in ascending (ex, ey) order.
 template <int P, int MODE>
-void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const Scm3DGeo& g, const Mats2<P>& mt,
-                  double sk, const StepArgs& a) {
-    using T = Tile3<P>;
+__global__ void __launch_bounds__(128) k_scm3d_zcol(Scm3DGeo g, Mats2<P> mt, double sk, StepArgs a) {
+    constexpr int N = P + 1;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n_pl = g.row_hi - g.row_lo;
+    unsigned long long amp = 0ULL;
+    if (t < n_pl * g.n1) {
+        const int64_t I = g.row_lo + t / g.n1, J = t % g.n1, K = g.n1 - 1;
+        const int64_t s_ = g.n_e + 2;
+        double acc = 0.0;
+        for (int dx = 1; dx >= 0; --dx) {
+            const int64_t ex = I / P - dx;
+            const int ia = (int)(I - ex * P);
+            if (ex < 0 || ex >= g.n_ex || ia > P) continue;
+            for (int dy = 1; dy >= 0; --dy) {
+                const int64_t ey = J / P - dy;
+                const int ib = (int)(J - ey * P);
+                if (ey < 0 || ey >= g.n_e || ib > P) continue;
+                const int64_t ez = g.n_e - 1;
+                const uint8_t code = g.mask[((ex + 1) * s_ + (ey + 1)) * s_ + ez + 1];
+                if (code == 1) {
+                    const int64_t b0 = (ex * P + P) * g.pplane + (ey * P + P) * g.prow + ez * P + PADJ;
+                    double s = 0.0;
+                    for (int q = 0; q < N; ++q)
+                        for (int r = 0; r < N; ++r) {
+                            const double* u = a.cur + b0 + q * g.pplane + r * g.prow;
+                            double zm = 0.0, zk = 0.0;
+                            for (int j = 0; j < N; ++j) {
+                                zm = fma(mt.m[orb(P, P, j)], u[j], zm);
+                                zk = fma(mt.k[orb(P, P, j)], u[j], zk);
+                            }
+                            const double mq = mt.m[orb(P, ia, q)], kq = mt.k[orb(P, ia, q)];
+                            const double mr = mt.m[orb(P, ib, r)], kr = mt.k[orb(P, ib, r)];
+                            s = fma(kq * mr + mq * kr, zm, fma(mq * mr, zk, s));
+                        }
+                    acc += s;
+                } else if (code == 2) {
+                    const int32_t id = g.cut_id[(ex * g.n_e + ey) * g.n_e + ez];
+                    acc += g.cut_out[(int64_t)id * N * N * N + (ia * N + ib) * N + P];
+                }
+            }
+        }
+        const int64_t base = (I + P) * g.pplane + (J + P) * g.prow + K + PADJ;
+        if constexpr (MODE == MODE_APPLY) {
+            a.out[base] = sk * acc;
+        } else {
+            const double f = __ldg(a.ft + a.k);
+            const double mi = a.minv[base];
+            const double v = leapfrog(a.cur[base], a.prev[base], sk * acc, mi, f * source_at(a.F, base), a.dt2);
+            a.out[base] = v;
+            amp = mi != 0.0 ? amp_bits(v) : 0ULL;
+        }
+    }
+    if constexpr (MODE == MODE_STEP) block_amp_max<128>(amp, a.amp);
+}
+
+template <int P>
+__global__ void k_clean3d(Scm3DGeo g, MinvTab<P> tab, const double* __restrict__ minv, uint8_t* clean) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nc = g.n_ex * g.n_e * g.n_e;
+    if (c >= nc) return;
+    const int64_t ex = c / (g.n_e * g.n_e), ey = (c / g.n_e) % g.n_e, ez = c % g.n_e;
+    bool ok = ex >= 1;
+    for (int q = 0; q < P && ok; ++q)
+        for (int r = 0; r < P && ok; ++r)
+            for (int j = 0; j < P && ok; ++j) {
+                const int64_t I = ex * P + q;
+                const int64_t s = (I + P) * g.pplane + (ey * P + r + P) * g.prow + ez * P + j + PADJ;
+                ok = I < g.row_hi && __double_as_longlong(minv[s]) == __double_as_longlong(tab.v[(q * P + r) * P + j]);
+            }
+    clean[c] = ok ? 1 : 0;
+}
+
+template <int P>
+void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean) {
+    const int64_t nc = g.n_ex * g.n_e * g.n_e;
+    k_clean3d<P><<<(unsigned)ceil_div(nc, 256), 256, 0, ctx->stream>>>(g, tab, minv, clean);
+    ctx->launches++;
+}
+
+template <int P, int MODE>
+void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map_p, const Scm3DGeo& g,
+                  const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a) {
+    using T = Str3<P>;
     static bool attr_set = false;
     if (!attr_set) {
         WCB_CUDA(cudaFuncSetAttribute(k_scm3d<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)T::SMEM));
         attr_set = true;
     }
-    dim3 grid((unsigned)g.n_zs, (unsigned)(g.n_e + 1), (unsigned)g.n_xt);
-    k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, g, mt, sk, a);
+    dim3 grid((unsigned)g.n_zs, (unsigned)g.n_yb, (unsigned)g.n_xc);
+    k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
     ctx->launches++;
+    if (g.n_e % 32 == 0) {
+        const int64_t n = (g.row_hi - g.row_lo) * g.n1;
+        k_scm3d_zcol<P, MODE><<<(unsigned)ceil_div(n, 128), 128, 0, ctx->stream>>>(g, mt, sk, a);
+        ctx->launches++;
+    }
 }
 
 #define WCB_INST3(P)                                                                            \
-    template void launch_scm3d<P, MODE_STEP>(Context*, const CUtensorMap&, const Scm3DGeo&,    \
-                                             const Mats2<P>&, double, const StepArgs&);        \
-    template void launch_scm3d<P, MODE_APPLY>(Context*, const CUtensorMap&, const Scm3DGeo&,   \
-                                              const Mats2<P>&, double, const StepArgs&);
+    template void launch_scm3d<P, MODE_STEP>(Context*, const CUtensorMap&, const CUtensorMap&, const Scm3DGeo&, \
+                                             const Mats2<P>&, const MinvTab<P>&, double,        \
+                                             const StepArgs&);                                  \
+    template void launch_scm3d<P, MODE_APPLY>(Context*, const CUtensorMap&, const CUtensorMap&, const Scm3DGeo&, \
+                                              const Mats2<P>&, const MinvTab<P>&, double,       \
+                                              const StepArgs&);                                 \
+    template void launch_clean3d<P>(Context*, const Scm3DGeo&, const MinvTab<P>&, const double*, uint8_t*);
 #define WCB_INSTC(P) \
     template void launch_cut_pre<P>(Context*, int64_t, const double*, const int64_t*, int64_t, int64_t, \
                                     const double*, double*);

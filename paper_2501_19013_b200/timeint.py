@@ -159,6 +159,14 @@ class CdmPlan:
     def handle(self):
         return self._h
 
+    def step_bytes(self) -> float:
+        """Algorithmic HBM bytes of one fused time step of this plan (32 B per
+        DOF, 24 B where 1/m comes from the interior-cell table, plus the
+        operator's cut-cell / CSR data)."""
+        out = _lib.C.c_double()
+        _lib.check(_lib.load().wcb_cdm_plan_step_bytes(self._h, _lib.C.byref(out)))
+        return float(out.value)
+
     def run(self, f_t, dt: float, n_t: int, psi0=None, v0=None,
             record: bool = True) -> RunResult:
         n = self.op.n

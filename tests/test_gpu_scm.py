@@ -113,7 +113,9 @@ def test_3d_cube_cdm_and_dt_crit_match_reference():
     assert rel(r.obs, g["obs"]) <= 1e-10
 
 
-@pytest.mark.parametrize("p,n_e", [(1, 7), (2, 9), (3, 12), (3, 40)])
+# (1, 32), (2, 32): n_e % 32 == 0 takes the z = n1-1 column kernel; (3, 17):
+# n_e + 1 a multiple of the y block; (4, 6): the p = 4 streaming tile
+@pytest.mark.parametrize("p,n_e", [(1, 7), (2, 9), (3, 12), (3, 17), (3, 40), (1, 32), (2, 32), (4, 6)])
 def test_3d_sphere_voids_apply_and_cdm(p, n_e):
     """Config-5 style geometry (sphere + small voids) at reduced size: device
     apply vs host CSR, and 100 CDM steps vs the CPU oracle loop."""
@@ -134,3 +136,26 @@ def test_3d_sphere_voids_apply_and_cdm(p, n_e):
     psi_ref, _, _ = O.cdm_run(M, K, prob.F_s, f, dt, 100)
     r = cdm_run(M, op, prob.F_s, f, dt, 100)
     assert rel(r.psi, psi_ref) <= 1e-10
+
+
+@pytest.mark.parametrize("p,n_e", [(3, 20), (2, 13)])
+def test_3d_x_chunking_bitwise_invariant(p, n_e, monkeypatch):
+    """The 3D kernel streams x cell rows in chunks, each rebuilding its carry
+    plane from the row above: any chunking gives bitwise the same field."""
+    from paper_2501_19013_b200.setup.configs import build_scm as _b
+    from paper_2501_19013_b200.setup.configs import CONFIGS as _C
+    from dataclasses import replace
+    cfg = replace(_C["config5"], p=p, n_e=n_e, n_random=5, r_range=(0.03, 0.08), name="c5x")
+    prob = _b(cfg)
+    M = prob.mass_matrix()
+    x = np.random.default_rng(1).standard_normal(prob.n_dof)
+    f = lambda t: ricker(t, 10.0)
+    outs = []
+    for chunks in ("1", "3", str(n_e)):
+        monkeypatch.setenv("WAVECELL_B200_XCHUNKS", chunks)
+        op = prob.device_operator()
+        r = cdm_run(M, op, prob.F_s, f, 1e-3 / n_e, 60)
+        outs.append((op @ x, r.psi))
+    for y, psi in outs[1:]:
+        assert np.array_equal(y, outs[0][0])
+        assert np.array_equal(psi, outs[0][1])
