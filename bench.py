@@ -18,9 +18,12 @@ Arms
 * ``reference``: the reference CPU path (oracle C port of the CSR CDM loop,
   all host threads) on the same configuration; bounded sample per step.
 
-N>1 (torchrun): every rank runs an independent replica of the workload on its
-own GPU (config 2 is a single-GPU configuration; weak scaling, no data-path
-collective); timing is the max over ranks.
+N>1 (torchrun): configs 1-3 are single-GPU configurations: every
+rank runs an independent replica of the workload on its own GPU (weak scaling,
+no data-path collective).  Config 5 (``--config config5``) is the sharded
+configuration: N x slabs of the one 192^3 grid with an NCCL halo exchange per
+time step (strong scaling); ``--slabs`` forces slabs for config 2 as well.
+Timing is the max over ranks.
 """
 
 from __future__ import annotations
@@ -447,6 +450,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--nt", type=int, default=None, help="override the time-step count (profiling)")
+    ap.add_argument("--slabs", action="store_true", help="N>1: x slabs of one 2D grid instead of replicas")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
@@ -480,7 +484,7 @@ def main():
     f = lambda t: ricker(t, cfg.f_e)  # noqa: E731
     ft = force_table(f, dt, n_t)
     n_global = prob.n_dof
-    slab_mode = world > 1 and not hasattr(prob, "K")
+    slab_mode = world > 1 and not hasattr(prob, "K") and (args.slabs or prob.grid.dim == 3)
     if slab_mode:
         # strong scaling of the same grid: x slabs, NCCL halo exchange per step
         from paper_2501_19013_b200 import dist as wdist

@@ -37,7 +37,8 @@ namespace wcb {
 // reduced by the same shuffle tree as the sync-free kernel (bitwise equal).
 constexpr int TRSV_DMAX = 12;             // max ring depth (levels in flight)
 constexpr int TRSV_SMEM = 220 * 1024;     // dynamic shared memory budget
-constexpr int TRSV_THREADS = 512;
+constexpr int TRSV_THREADS = 512;      // launch bound
+constexpr int TRSV_THREADS_DEF = 512;
 
 struct TriSched {
     bool ok = false;
@@ -483,7 +484,12 @@ static void launch_trsv_d(Context* ctx, const TriSched& T, const double* b, doub
         WCB_CUDA(cudaFuncSetAttribute(k_trsv_comp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = sm;
     }
-    k_trsv_comp<D><<<(unsigned)T.n_comp, TRSV_THREADS, sm, ctx->stream>>>(
+    static const int threads = [] {
+        const char* e = getenv("WAVECELL_B200_TRSV_THREADS");
+        const int t = e ? atoi(e) : TRSV_THREADS_DEF;
+        return t >= 32 && t <= TRSV_THREADS && t % 32 == 0 ? t : TRSV_THREADS_DEF;
+    }();
+    k_trsv_comp<D><<<(unsigned)T.n_comp, threads, sm, ctx->stream>>>(
         T.comp_order.p, T.comp_rows.p, T.comp_lvl.p, T.lvl_off.p, T.lvl_ent.p, T.rows.p, T.sptr.p, T.slcol.p,
         T.sval.p, T.sdiag.p, b, x, (int)T.max_size, (int)T.max_levels, T.slot_e, T.slot_r);
 }
@@ -664,6 +670,7 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
         P->c_state.alloc(cs.size(), s); P->c_state.upload(cs.data(), n_c, s);
         P->Fc.alloc(Fc.size(), s); P->Fc.upload(Fc.data(), n_c, s);
         if (n_c) op->set_apply_subset(c_idx, n_c);   // K rows of c only, per step
+        op->bind_minv(P->minv.p);                      // interior 1/m table for the d step
         // force vector for the d rows: dense window over its nonzeros
         {
             std::vector<std::pair<int64_t, double>> nz;

@@ -101,6 +101,25 @@ struct MinvTab2 {
     double v[P * P];   // (r, j) of the owned nodes of an interior uncut cell
 };
 
+// clean[c] for every local cell c of a plane-strain operator: both
+// components of all P x P owned nodes carry minv == tab (bitwise)
+template <int P>
+__global__ void k_clean2e(int64_t n_ex, int64_t n_ey, int64_t row_hi, int64_t pitch, int64_t plane,
+                          MinvTab2<P> tab, const double* __restrict__ minv, uint8_t* clean) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_ex * n_ey) return;
+    const int64_t ex = c / n_ey, ey = c % n_ey;
+    bool ok = ex >= 1;
+    for (int r = 0; r < P && ok; ++r)
+        for (int j = 0; j < P && ok; ++j) {
+            const int64_t I = ex * P + r;
+            const int64_t s = (I + P) * pitch + ey * P + j + PADJ;
+            const long long t = __double_as_longlong(tab.v[r * P + j]);
+            ok = I < row_hi && __double_as_longlong(minv[s]) == t && __double_as_longlong(minv[s + plane]) == t;
+        }
+    clean[c] = ok ? 1 : 0;
+}
+
 // tclean[t] for every tile t: 1 when all owned nodes carry minv == tab (bitwise)
 template <int P>
 __global__ void k_clean2d(Scm2DGeo g, int TI, int TJ, MinvTab2<P> tab, const double* __restrict__ minv,
@@ -436,6 +455,8 @@ struct ScmOperator final : Operator {
     std::vector<double> minv_tab;     // its P^3 owned 1/m values (bind_minv)
     DevBuf<uint8_t> clean;            // 3D: per local cell: owned 1/m == minv_tab
     DevBuf<uint8_t> tclean;           // 2D: per tile
+    DevBuf<uint8_t> sflags;           // elastic streaming step: per (x chunk, strip) owns a DOF
+    int64_t n_xs = 0, xs_len = 0;     // elastic streaming step: x chunks, cell rows per chunk
     const double* minv_bound = nullptr;
     // x slab (local numbering): cell rows 0..n_ex-1 (0 = halo row above),
     // node rows 0..n1x-1, owned node rows [row_lo, row_hi)
@@ -526,18 +547,8 @@ struct ScmOperator final : Operator {
             return make_map_f64(ptr, 2, dims, strides, box);
         });
     }
-    template <int P, int MODE>
-    void launch2e(const StepArgs& a) {
-        using T = Tile2E<P>;
-        static bool attr_set = false;
-        if (!attr_set) {
-            WCB_CUDA(cudaFuncSetAttribute(k_ela2d<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)T::SMEM));
-            attr_set = true;
-        }
-        const int32_t* ord = sub_active ? order_sub.p : order.p;
-        const int64_t n_ord = sub_active ? n_order_sub : n_order;
-        if (!n_ord) return;
+    template <int P>
+    EMats<P> emats() const {
         constexpr int N = P + 1;
         EMats<P> mt;
         const double l2m = lam + 2.0 * mu;
@@ -556,6 +567,58 @@ struct ScmOperator final : Operator {
                 mt.xa[1][2][rc] = lam * g1[cr];
                 mt.xa[1][3][rc] = mu * g1[rc];
             }
+        return mt;
+    }
+    // streaming elastic step (k_ela2s): maps with boxes (UW, P) and (TJ, P)
+    template <int P>
+    const CUtensorMap& stream_map_e(const double* ptr, int kind) {
+        using T = Str2E<P>;
+        return maps.get(ptr, 30 + kind, [&] {
+            const uint64_t dims[2] = {(uint64_t)pitch, (uint64_t)(2 * rows)};
+            const uint64_t strides[1] = {(uint64_t)pitch};
+            const uint32_t box[2] = {(uint32_t)(kind ? T::TJ : T::UW), (uint32_t)P};
+            return make_map_f64(ptr, 2, dims, strides, box);
+        });
+    }
+    template <int P>
+    void launch2s(const StepArgs& a) {
+        using T = Str2E<P>;
+        static bool attr_set = false;
+        if (!attr_set) {
+            WCB_CUDA(cudaFuncSetAttribute(k_ela2s<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
+            attr_set = true;
+        }
+        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, sflags.p, nullptr, n_strips, n_rtiles,
+                   pitch, nullptr};
+        MinvTabE<P> tab{};
+        const uint8_t* cl = nullptr;
+        if (a.minv && a.minv == minv_bound && clean.p) {
+            cl = clean.p;
+            for (int i = 0; i < P * P; ++i) tab.v[i] = minv_tab[i];
+        }
+        const EMats<P> mt = emats<P>();
+        dim3 grid((unsigned)n_strips, (unsigned)n_xs);
+        k_ela2s<P><<<grid, 64, T::SMEM, ctx->stream>>>(stream_map_e<P>(a.cur, 0), stream_map_e<P>(a.prev, 1), g, mt,
+                                                      plane, (int32_t)rows, xs_len, ex_last, cl, tab, a);
+        ctx->launches++;
+    }
+    template <int P, int MODE>
+    void launch2e(const StepArgs& a) {
+        using T = Tile2E<P>;
+        if (MODE == MODE_STEP && n_xs > 0 && getenv("WAVECELL_B200_STREAM_ELASTIC")) {   // experimental
+            launch2s<P>(a);
+            return;
+        }
+        static bool attr_set = false;
+        if (!attr_set) {
+            WCB_CUDA(cudaFuncSetAttribute(k_ela2d<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)T::SMEM));
+            attr_set = true;
+        }
+        const int32_t* ord = sub_active ? order_sub.p : order.p;
+        const int64_t n_ord = sub_active ? n_order_sub : n_order;
+        if (!n_ord) return;
+        const EMats<P> mt = emats<P>();
         Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, ord, n_strips, n_rtiles, pitch};
         const CUtensorMap& mu_ = state_map_e<P>(a.cur, 0);
         const bool epi = MODE == MODE_STEP;
@@ -692,10 +755,47 @@ struct ScmOperator final : Operator {
         minv_tab = h;
         minv_bound = d_minv;
     }
+    template <int P>
+    void bind2e(const double* d_minv) {
+        MinvTab2<P> tab{};
+        std::vector<double> h(P * P);
+        for (int r = 0; r < P; ++r)
+            WCB_CUDA(cudaMemcpyAsync(h.data() + r * P, d_minv + probe_base + r * pitch, P * sizeof(double),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < P * P; ++i) {
+            if (!(h[i] > 0.0)) return;
+            tab.v[i] = h[i];
+        }
+        const int64_t nc = n_ex * n_e;
+        if (!clean.p) clean.alloc((size_t)nc);
+        k_clean2e<P><<<(unsigned)ceil_div(nc, 256), 256, 0, ctx->stream>>>(n_ex, n_e, row_hi, pitch, plane, tab,
+                                                                          d_minv, clean.p);
+        ctx->launches++;
+        WCB_CHECK_LAUNCH();
+        std::vector<uint8_t> hc(nc);
+        WCB_CUDA(cudaMemcpyAsync(hc.data(), clean.p, nc, cudaMemcpyDeviceToHost, ctx->stream));
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        int64_t ncl = 0;
+        for (uint8_t v : hc) ncl += v;
+        minv_skipped = 2.0 * (double)ncl * P * P;   // both components
+        minv_tab = h;
+        minv_bound = d_minv;
+    }
     void bind_minv(const double* d_minv) override {
         minv_bound = nullptr;
         minv_skipped = 0.0;
         if (probe_base < 0 || !d_minv || getenv("WAVECELL_B200_NO_MINV_TAB")) return;
+        if (dim == 2 && ncomp == 2) {
+            switch (p) {
+                case 1: bind2e<1>(d_minv); break;
+                case 2: bind2e<2>(d_minv); break;
+                case 3: bind2e<3>(d_minv); break;
+                case 4: bind2e<4>(d_minv); break;
+                case 5: bind2e<5>(d_minv); break;
+            }
+            return;
+        }
         if (dim == 2) {
             if (ncomp != 1 || !WCB2D_EPI_TMA) return;
             switch (p) {
@@ -780,6 +880,23 @@ struct ScmOperator final : Operator {
         return has_top || !owns_last;
     }
 };
+
+template <int P>
+static int ela2s_occ() {
+    int nb = 0;
+    WCB_CUDA(cudaFuncSetAttribute(k_ela2s<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Str2E<P>::SMEM));
+    WCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_ela2s<P>, 64, Str2E<P>::SMEM));
+    return nb;
+}
+static int ela2s_ctas_per_sm(int p) {
+    switch (p) {
+        case 1: return ela2s_occ<1>();
+        case 2: return ela2s_occ<2>();
+        case 3: return ela2s_occ<3>();
+        case 4: return ela2s_occ<4>();
+        default: return ela2s_occ<5>();
+    }
+}
 
 // Both dimensions: slab preprocessing (cell rows [x_cell_lo-1, x_cell_hi) of
 // the global grid along x, one halo cell row above), state layout, tile flags,
@@ -895,7 +1012,7 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
                     if (ok) op->probe_base = (x * p + p) * op->xstride + (y * p + p) * op->pitch + z * p + PADJ;
                 }
     }
-    if (dim == 2 && ncomp == 1) {
+    if (dim == 2) {
         auto C = [&](int64_t x, int64_t y) { return cls[x * n_e + y]; };
         for (int64_t x = std::max<int64_t>(2, op->n_ex / 2); x < op->n_ex && op->probe_base < 0; ++x)
             for (int64_t y = std::max<int64_t>(1, n_e / 2); y < n_e && op->probe_base < 0; ++y) {
@@ -953,6 +1070,24 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
         cf.assign(op->n_xc * op->n_yb * op->n_zs, 0);
     }
     op->sidx.resize(op->n);
+    // elastic streaming step: x chunks of cell rows x strips, sized so the
+    // grid fills the resident CTA slots (waves x (rows + halo row) minimal)
+    std::vector<uint8_t> sf;
+    if (ncomp == 2) {
+        op->ex_last = (op->row_hi - 1) / p;
+        const int64_t rows_out = op->ex_last;
+        const int64_t slots = (int64_t)ctx->sm_count * std::max(1, ela2s_ctas_per_sm(p));
+        const int64_t per_chunk = ceil_div(n1, TJ);
+        int64_t nxc = 1;
+        double best = 1e300;
+        for (int64_t c = 1; c <= std::min<int64_t>(rows_out, 256); ++c) {
+            const double cost = (double)ceil_div(per_chunk * c, slots) * (double)(ceil_div(rows_out, c) + 1);
+            if (cost < best - 1e-9) { best = cost; nxc = c; }
+        }
+        op->xs_len = ceil_div(rows_out, nxc);
+        op->n_xs = ceil_div(rows_out, op->xs_len);
+        sf.assign(op->n_xs * per_chunk, 0);
+    }
     const int64_t x0 = lo * p - p;   // global node row of local row 0
     for (int64_t i = 0; i < d->n_dof; ++i) {
         const int64_t lex = d->lex_of_compact[i];
@@ -964,6 +1099,7 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
         if (dim == 2) {
             op->sidx[i] = (Il + p) * op->xstride + rest + PADJ;
             cf[(rest / TJ) * op->n_rtiles + t] = 1;
+            if (ncomp == 2) sf[((Il / p - 1) / op->xs_len) * op->n_strips + rest / TJ] = 1;
         } else {
             const int64_t J = rest / n1, K = rest % n1;
             op->sidx[i] = (Il + p) * op->xstride + (J + p) * op->pitch + K + PADJ;
@@ -1042,6 +1178,10 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
     op->mask.upload(mask.data(), mask.size(), st);
     op->cflags.alloc(cf.size());
     op->cflags.upload(cf.data(), cf.size(), st);
+    if (!sf.empty()) {
+        op->sflags.alloc(sf.size());
+        op->sflags.upload(sf.data(), sf.size(), st);
+    }
     op->cut_id.alloc(cid.size());
     op->cut_id.upload(cid.data(), cid.size(), st);
     op->KT.alloc(KT.size());

@@ -84,7 +84,7 @@ struct MinvTab {
 #define WCB3D_REUSE 1
 #endif
 #ifndef WCB3D_WY3
-#define WCB3D_WY3 3
+#define WCB3D_WY3 7
 #endif
 __host__ __device__ constexpr int wy_for3(int P) { return P <= 2 ? 7 : P == 3 ? WCB3D_WY3 : 2; }
 // resident CTAs per SM the launch bounds ask for

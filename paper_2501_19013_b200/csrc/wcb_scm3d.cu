@@ -27,11 +27,12 @@ __device__ __forceinline__ void zpass_row(const double (&mc)[orb_count(P)],
                                           double& zmL, double& zkL) {
     row += Str3<P>::CO;
     const double* own_p = row + P + lane * P;
+    // own nodes, the right neighbour's first node and the left cell's nodes
+    // straight from shared memory (no shuffles: uniform, no warp collectives)
     double own[P];
     #pragma unroll
     for (int j = 0; j < P; ++j) own[j] = own_p[j];
-    double right = __shfl_down_sync(0xffffffffu, own[0], 1);
-    if (lane == 31) right = own_p[P];
+    const double right = own_p[P];
     #pragma unroll
     for (int j = 0; j < P; ++j) {
         double s1 = mc[orb(P, j, P)] * right, s2 = kc[orb(P, j, P)] * right;
@@ -46,8 +47,7 @@ __device__ __forceinline__ void zpass_row(const double (&mc)[orb_count(P)],
     double l1 = mc[orb(P, P, P)] * own[0], l2 = kc[orb(P, P, P)] * own[0];
     #pragma unroll
     for (int d = 0; d < P; ++d) {
-        double ud = __shfl_up_sync(0xffffffffu, own[d], 1);
-        if (lane == 0) ud = row[d];
+        const double ud = own_p[d - P];
         l1 = fma(mc[orb(P, P, d)], ud, l1);
         l2 = fma(kc[orb(P, P, d)], ud, l2);
     }
