@@ -206,10 +206,16 @@ __device__ __forceinline__ void cut_cells_warp_e(const Scm2DGeo& g, const double
     }
 }
 
+template <int P>
+struct MinvTabE {
+    double v[P * P];
+};
+
 template <int P, int MODE, int O>
 __device__ __forceinline__ void ela2d_warp(const Scm2DGeo& g, const EMats<P>& mt, const StepArgs& a,
                                            int64_t plane, unsigned char* smem, int wi, int lane,
-                                           int64_t J0, int64_t I0, unsigned long long& amp) {
+                                           int64_t J0, int64_t I0, unsigned long long& amp, bool tcl,
+                                           const MinvTabE<P>& mtab) {
     using T = Tile2E<P>;
     constexpr int N = P + 1;
     constexpr int RPE = T::RPE;
@@ -275,7 +281,12 @@ __device__ __forceinline__ void ela2d_warp(const Scm2DGeo& g, const EMats<P>& mt
                                 (size_t)(wi * P + r) * T::TJ + lane * P;
             double up[P], mi[P], uu[P];
             lds_row<P>(ps, up);
-            lds_row<P>(msm, mi);
+            if (tcl) {
+                #pragma unroll
+                for (int j = 0; j < P; ++j) mi[j] = mtab.v[r * P + j];
+            } else {
+                lds_row<P>(msm, mi);
+            }
             lds_row<P>(urow, uu);
             const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
             #pragma unroll
@@ -298,7 +309,7 @@ template <int P, int MODE>
 __global__ void __launch_bounds__(Tile2E<P>::NWARP * 32, 2) k_ela2d(
     const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_prev,
     const __grid_constant__ CUtensorMap tm_minv, Scm2DGeo g, const __grid_constant__ EMats<P> mt,
-    int64_t plane, int32_t rows, StepArgs a) {
+    int64_t plane, int32_t rows, const __grid_constant__ MinvTabE<P> mtab, StepArgs a) {
     using T = Tile2E<P>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
@@ -308,24 +319,26 @@ __global__ void __launch_bounds__(Tile2E<P>::NWARP * 32, 2) k_ela2d(
     const int64_t strip = tid / g.n_rtiles, rtile = tid % g.n_rtiles;
     if (MODE == MODE_STEP && blockIdx.x == 0) record_observers(a);
     const int64_t J0 = strip * T::TJ, I0 = g.row_lo + rtile * T::TI;
+    const bool tcl = MODE == MODE_STEP && g.tclean && __ldg(g.tclean + tid) != 0;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         const bool epi = MODE == MODE_STEP;
-        mbar_expect_tx(bar, (uint32_t)(2 * T::U_BYTES + (epi ? 4 * T::E_BYTES : 0)));
+        mbar_expect_tx(bar, (uint32_t)(2 * T::U_BYTES + (epi ? (tcl ? 2 : 4) * T::E_BYTES : 0)));
         const int32_t xu = (int32_t)(J0 - P - T::CO + PADJ), xe = (int32_t)(J0 + PADJ);
         tma_load_2d(smem, &tm_u, xu, (int32_t)I0, bar);
         tma_load_2d(smem + T::OFF_U1, &tm_u, xu, (int32_t)I0 + rows, bar);
         if (epi) {
             for (int o = 0; o < 2; ++o) {
                 tma_load_2d(smem + T::OFF_PREV + o * T::E_R, &tm_prev, xe, (int32_t)(I0 + P) + o * rows, bar);
-                tma_load_2d(smem + T::OFF_MINV + o * T::E_R, &tm_minv, xe, (int32_t)(I0 + P) + o * rows, bar);
+                if (!tcl)
+                    tma_load_2d(smem + T::OFF_MINV + o * T::E_R, &tm_minv, xe, (int32_t)(I0 + P) + o * rows, bar);
             }
         }
     }
     __syncthreads();
     unsigned long long amp = 0ULL;
-    if (w < T::NWB) ela2d_warp<P, MODE, 0>(g, mt, a, plane, smem, w, lane, J0, I0, amp);
-    else ela2d_warp<P, MODE, 1>(g, mt, a, plane, smem, w - T::NWB, lane, J0, I0, amp);
+    if (w < T::NWB) ela2d_warp<P, MODE, 0>(g, mt, a, plane, smem, w, lane, J0, I0, amp, tcl, mtab);
+    else ela2d_warp<P, MODE, 1>(g, mt, a, plane, smem, w - T::NWB, lane, J0, I0, amp, tcl, mtab);
     if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
 }
 
@@ -355,11 +368,6 @@ struct Str2E {
     static constexpr size_t OFF_PREV = 2 * SLOT;
     static constexpr size_t OFF_BAR = OFF_PREV + 2 * PCOMP;
     static constexpr size_t SMEM = OFF_BAR + 8 * 3;
-};
-
-template <int P>
-struct MinvTabE {
-    double v[P * P];
 };
 
 template <int P>

@@ -35,7 +35,8 @@ namespace wcb {
 // elimination level -- instead of a device-wide chain of global-memory
 // handshakes.  Entries of a row are visited in the same lane-strided order and
 // reduced by the same shuffle tree as the sync-free kernel (bitwise equal).
-constexpr int TRSV_DMAX = 12;             // max ring depth (levels in flight)
+constexpr int TRSV_DMAX = 12;
+static __host__ __device__ inline size_t trsv_slot_bytes(int e, int r);             // max ring depth (levels in flight)
 constexpr int TRSV_SMEM = 220 * 1024;     // dynamic shared memory budget
 constexpr int TRSV_THREADS = 512;      // launch bound
 constexpr int TRSV_THREADS_DEF = 512;
@@ -175,29 +176,27 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
     T.sval.alloc(sval.size(), s); T.sval.upload(sval.data(), sval.size(), s);
     T.sdiag.alloc(n, s); T.sdiag.upload(sdiag.data(), n, s);
     WCB_CUDA(cudaStreamSynchronize(s));   // host vectors die here
-    // ring slots as large as the widest level allows within the smem budget
-    // ring slots sized for the 97th-percentile level (wider levels read global
-    // memory directly), as many slots as the budget allows (2..TRSV_DMAX)
     const int64_t fixed = T.max_size * 8 + (T.max_levels + 1) * 8 + 64;
     const int64_t avail = (int64_t)TRSV_SMEM - fixed;
-    std::vector<int32_t> le_sz, lr_sz;
-    for (size_t l = 0; l + 1 < lvl_off.size(); ++l) {
-        le_sz.push_back(lvl_ent[l + 1] - lvl_ent[l]);
-        lr_sz.push_back(lvl_off[l + 1] - lvl_off[l]);
+    // ring slots: as deep as the budget allows with every level fitting a
+    // slot (cap TRSV_DMAX); if fewer than 3 such slots fit, 3 slots as large
+    // as the budget allows (wider levels read global memory directly)
+    const int64_t full_r = std::min<int64_t>(std::max<int64_t>(T.max_lvl_rows, 1), 1024);
+    const int64_t full_e = std::max<int64_t>(T.max_lvl_ent, 1);
+    const int64_t sb_full = (int64_t)trsv_slot_bytes((int)full_e, (int)full_r);
+    const int64_t d_full = avail > 0 ? avail / sb_full : 0;
+    if (d_full >= 3) {
+        T.slot_r = (int)full_r;
+        T.slot_e = (int)full_e;
+        T.depth = (int)std::min<int64_t>(TRSV_DMAX, d_full);
+    } else {
+        T.slot_r = (int)full_r;
+        const int64_t per = avail / 3 - full_r * 12 - 32;
+        T.slot_e = (int)std::max<int64_t>(0, std::min<int64_t>(full_e, per / 12));
+        T.depth = 3;
     }
-    auto pct = [](std::vector<int32_t> v, double q) -> int64_t {
-        if (v.empty()) return 1;
-        std::sort(v.begin(), v.end());
-        return std::max<int64_t>(1, v[(size_t)std::min<double>(v.size() - 1, q * v.size())]);
-    };
-    const char* qe = getenv("WAVECELL_B200_TRSV_Q");
-    const double q = qe ? atof(qe) : 0.97;
-    T.slot_r = (int)std::min<int64_t>(pct(lr_sz, q) + 8, 1024);
-    T.slot_e = (int)std::min<int64_t>(pct(le_sz, q) + 64, std::max<int64_t>(T.max_lvl_ent, 1));
-    const int64_t sb = (int64_t)(((size_t)T.slot_e * 12 + (size_t)T.slot_r * 12 + 4) + 15) / 16 * 16;
-    T.depth = (int)std::min<int64_t>(TRSV_DMAX, avail / std::max<int64_t>(sb, 1));
-    T.depth = T.depth >= 12 ? 12 : T.depth >= 8 ? 8 : T.depth >= 6 ? 6 : T.depth >= 4 ? 4 : T.depth >= 3 ? 3 : T.depth;
-    T.ok = avail > 0 && T.depth >= 3;
+    T.depth = T.depth >= 12 ? 12 : T.depth >= 8 ? 8 : T.depth >= 6 ? 6 : T.depth >= 4 ? 4 : 3;
+    T.ok = avail > 0 && T.slot_e >= 256;
     // launch order: longest dependency chains first (2 waves when components > SMs)
     std::vector<int32_t> co(n_comp);
     for (int64_t c = 0; c < n_comp; ++c) co[c] = (int32_t)c;

@@ -624,8 +624,13 @@ struct ScmOperator final : Operator {
         const bool epi = MODE == MODE_STEP;
         const CUtensorMap& mp = epi ? state_map_e<P>(a.prev, 1) : mu_;
         const CUtensorMap& mm = epi ? state_map_e<P>(a.minv, 1) : mu_;
+        MinvTabE<P> tab{};
+        if (MODE == MODE_STEP && a.minv && a.minv == minv_bound && tclean.p) {
+            g.tclean = tclean.p;
+            for (int i = 0; i < P * P; ++i) tab.v[i] = minv_tab[i];
+        }
         k_ela2d<P, MODE><<<(unsigned)n_ord, T::NWARP * 32, T::SMEM, ctx->stream>>>(
-            mu_, mp, mm, g, mt, plane, (int32_t)rows, a);
+            mu_, mp, mm, g, mt, plane, (int32_t)rows, tab, a);
         ctx->launches++;
     }
     template <int MODE>
@@ -778,7 +783,29 @@ struct ScmOperator final : Operator {
         WCB_CUDA(cudaStreamSynchronize(ctx->stream));
         int64_t ncl = 0;
         for (uint8_t v : hc) ncl += v;
-        minv_skipped = 2.0 * (double)ncl * P * P;   // both components
+        minv_skipped = 2.0 * (double)ncl * P * P;   // both components (streaming kernel)
+        // tile kernel: a tile is clean when all its cells are
+        {
+            using TE = Tile2E<P>;
+            const int64_t nt = n_strips * n_rtiles;
+            std::vector<uint8_t> tc(nt, 0);
+            double skipped_tiles = 0.0;
+            for (int64_t t = 0; t < nt; ++t) {
+                const int64_t strip = t / n_rtiles, rt = t % n_rtiles;
+                const int64_t ex0 = (row_lo + rt * TE::TI) / P, ey0 = strip * 32;
+                bool ok = ey0 + 32 <= n_e && ex0 + TE::RPE <= n_ex;
+                for (int64_t ex = ex0; ok && ex < ex0 + TE::RPE; ++ex)
+                    for (int64_t ey = ey0; ok && ey < ey0 + 32; ++ey) ok = hc[ex * n_e + ey] != 0;
+                if (ok) {
+                    tc[t] = 1;
+                    skipped_tiles += 2.0 * (double)(std::min<int64_t>(TE::TI, row_hi - (row_lo + rt * TE::TI)) * TE::TJ);
+                }
+            }
+            if (!tclean.p) tclean.alloc((size_t)nt);
+            tclean.upload(tc.data(), nt, ctx->stream);
+            WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (!n_xs || !getenv("WAVECELL_B200_STREAM_ELASTIC")) minv_skipped = skipped_tiles;
+        }
         minv_tab = h;
         minv_bound = d_minv;
     }
