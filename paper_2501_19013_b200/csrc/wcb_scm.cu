@@ -470,6 +470,7 @@ struct ScmOperator final : Operator {
     DevBuf<double> KT;
     DevBuf<double> KP, cut_out;      // 3D: packed cut matrices, per-step products
     DevBuf<int64_t> cut_base;        // 3D: state index of each cut cell's first node
+    DevBuf<double2> zline;           // 3D, n_e % 32 == 0: z-lines of the last cell column
     DevBuf<int32_t> order;        // 2D tile kernel: live tiles, most expensive first
     int64_t n_order = 0;
     // apply restricted to the tiles owning a given DOF subset (IMEX c rows)
@@ -701,7 +702,7 @@ struct ScmOperator final : Operator {
     }
     Scm3DGeo geo3() const {
         return Scm3DGeo{n_ex, row_lo, row_hi, n_e, n1, pitch, pplane, mask.p, cut_id.p, cut_out.p, cflags.p,
-                        n_zs, n_yb, n_xc, xc3, ex_last, nullptr};
+                        n_zs, n_yb, n_xc, xc3, ex_last, nullptr, zline.p};
     }
     template <int P>
     void bind3(const double* d_minv) {
@@ -1143,7 +1144,7 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
     const int L = op->L;
     std::vector<int32_t> cid(op->n_ex * cells_row, -1);
     // 2D: full transposed matrices; 3D: packed lower triangles (k_cut_pre)
-    const int64_t LP = (int64_t)L * (L + 1) / 2;
+    const int64_t LP = dim == 3 ? (int64_t)cut_lp_stride(p) : (int64_t)L * (L + 1) / 2;   // packed stride
     std::vector<double> KT(dim == 2 ? (size_t)std::max<int64_t>(op->n_cut, 1) * L * L : 1, 0.0);
     std::vector<double> KP(dim == 3 ? (size_t)std::max<int64_t>(op->n_cut, 1) * LP : 1, 0.0);
     std::vector<int64_t> cbase(std::max<int64_t>(op->n_cut, 1), 0);
@@ -1219,6 +1220,7 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
         op->cut_base.alloc(cbase.size());
         op->cut_base.upload(cbase.data(), cbase.size(), st);
         op->cut_out.alloc((size_t)std::max<int64_t>(op->n_cut, 1) * L);
+        if (n_e % 32 == 0) op->zline.alloc((size_t)(op->n_ex * p + 1) * n1);
     }
     // algorithmic bytes per step: 32 B per DOF + packed cut K
     op->bytes_step = 32.0 * (double)op->n + 8.0 * (double)L * (L + 1) / 2.0 * (double)op->n_cut;

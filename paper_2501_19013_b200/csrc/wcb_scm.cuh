@@ -70,6 +70,7 @@ struct Scm3DGeo {
     // (bitwise, checked on the device once per plan): the epilogue skips the
     // 1/m stream there.  null: every node loads 1/m.
     const uint8_t* clean;
+    double2* zline;           // (n_ex P + 1) x n1 z-lines of the last cell column (n_e % 32 == 0)
 };
 
 template <int P>
@@ -103,8 +104,8 @@ struct Str3 {
     static constexpr int S = P + 1 + la_for3(P);    // ring slots
     static constexpr int SLOT = (PLANE * 8 + 127) / 128 * 128 / 8;   // slot stride (doubles, 128 B aligned)
     static constexpr size_t RING_BYTES = (size_t)S * SLOT * 8;
-    static constexpr size_t OFF_XCH = (RING_BYTES + 127) / 128 * 128;   // [2][NWARP][2P][32]
-    static constexpr size_t OFF_PREV = OFF_XCH + (size_t)2 * NWARP * 2 * P * 32 * 8;   // [P][WY*P][TZ]
+    static constexpr size_t OFF_XCH = (RING_BYTES + 127) / 128 * 128;   // [NWARP][P+1][P][32]
+    static constexpr size_t OFF_PREV = OFF_XCH + (size_t)NWARP * (P + 1) * P * 32 * 8;   // [P][WY*P][TZ]
     static constexpr size_t PREV_BYTES = (size_t)P * WY * P * TZ * 8;
     static constexpr size_t OFF_BAR = OFF_PREV + (PREV_BYTES + 127) / 128 * 128;
     static constexpr size_t SMEM = OFF_BAR + 8 * (S + 1);
@@ -116,6 +117,10 @@ void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map
 // clean[c] = 1 when every owned node of local cell c has minv == tab (bitwise)
 template <int P>
 void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean);
+// packed lower triangle of a cut cell's K_o / sk, stride padded to 16 bytes
+__host__ __device__ constexpr int cut_lp_stride(int P) {
+    return (((P + 1) * (P + 1) * (P + 1)) * (((P + 1) * (P + 1) * (P + 1)) + 1) / 2 + 1) / 2 * 2;
+}
 // dense cut-cell products u_e -> K_o u_e / sk (packed symmetric K), before the stencil
 template <int P>
 void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t* cut_base,

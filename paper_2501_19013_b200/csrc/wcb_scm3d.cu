@@ -94,47 +94,98 @@ __device__ __forceinline__ void cut_cells_warp3(const Scm3DGeo& g, int64_t ex, i
     }
 }
 
-// One warp per cut cell: gather u_e (64 nodes for p = 3) from the state, stage
-// the packed lower triangle of K_o / sk in shared memory (one coalesced read
-// of L(L+1)/2 doubles -- half the full matrix), lane r forms row r in
-// ascending column order.
+// Cut-cell products u_e -> K_o u_e / sk.  Persistent warps walk the cut
+// cells with a two-deep pipeline: the packed lower triangle of the next
+// cell's K_o / sk (L(L+1)/2 doubles, one 1D bulk copy) and its u_e (cp.async
+// gather from the state) land in shared memory while the current cell is
+// multiplied.  Lane r forms row r in ascending column order (running packed
+// indices: m <= r along row r, m > r down column r) -- the same sums as a
+// dense symmetric row.
 template <int P>
-__host__ __device__ constexpr int cut_pre_warps() {
-    return (int)(200 * 1024 / (((P + 1) * (P + 1) * (P + 1)) * (((P + 1) * (P + 1) * (P + 1)) + 3) / 2 * 8)) > 4
-               ? 4
-               : (int)(200 * 1024 / (((P + 1) * (P + 1) * (P + 1)) * (((P + 1) * (P + 1) * (P + 1)) + 3) / 2 * 8));
+struct CutPre {
+    static constexpr int N = P + 1;
+    static constexpr int L = N * N * N;
+    static constexpr int LP = L * (L + 1) / 2;
+    static constexpr int LPS = cut_lp_stride(P);                        // 16-byte multiple
+    static constexpr int W = P <= 2 ? 8 : P == 3 ? 6 : 1;               // warps per CTA
+    static constexpr int NS = 2;                                        // pipeline stages per warp (6 warps x 2 beat 4 x 3)
+    static constexpr size_t KB = ((size_t)LPS * 8 + 127) / 128 * 128;   // packed matrix buffer
+    static constexpr size_t UB = ((size_t)L * 8 + 127) / 128 * 128;     // u_e buffer
+    static constexpr size_t PER_WARP = NS * (KB + UB);
+    static constexpr size_t OFF_BAR = W * PER_WARP;
+    static constexpr size_t SMEM = OFF_BAR + W * NS * 8;
+};
+
+__device__ __forceinline__ void cp_async8_g(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
 template <int P>
-__global__ void __launch_bounds__(128) k_cut_pre(int64_t n_cut, const double* __restrict__ KP,
+__global__ void __launch_bounds__(256) k_cut_pre(int64_t n_cut, const double* __restrict__ KP,
                                                  const int64_t* __restrict__ cut_base, int64_t pplane,
                                                  int64_t prow, const double* __restrict__ u,
                                                  double* __restrict__ out) {
-    constexpr int N = P + 1;
-    constexpr int L = N * N * N;
-    constexpr int LP = L * (L + 1) / 2;
-    extern __shared__ double smc[];
+    using C = CutPre<P>;
+    constexpr int N = C::N, L = C::L;
+    extern __shared__ __align__(128) unsigned char smc[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double* kp = smc + (size_t)w * (LP + L);
-    double* uu = kp + LP;
-    const int64_t e = (int64_t)blockIdx.x * cut_pre_warps<P>() + w;
-    if (e >= n_cut) return;
-    const double* src = KP + e * LP;
-    for (int i = lane; i < LP; i += 32) kp[i] = __ldg(src + i);
-    const int64_t base = cut_base[e];
-    for (int m = lane; m < L; m += 32) {
-        const int a = m / (N * N), b = (m / N) % N, j = m % N;
-        uu[m] = u[base + a * pplane + b * prow + j];
+    unsigned char* mine = smc + (size_t)w * C::PER_WARP;
+    constexpr int NS = C::NS;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smc + C::OFF_BAR) + NS * w;
+    const int64_t stride = (int64_t)gridDim.x * C::W;
+    const int64_t e0 = (int64_t)blockIdx.x * C::W + w;
+    if (lane == 0) {
+        #pragma unroll
+        for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
     }
     __syncwarp();
-    for (int r = lane; r < L; r += 32) {
-        double t = 0.0;
-        #pragma unroll 8
-        for (int m = 0; m < L; ++m) {
-            const int hi = r >= m ? r : m, lo = r >= m ? m : r;
-            t = fma(kp[hi * (hi + 1) / 2 + lo], uu[m], t);
+    auto fetch = [&](int64_t e, int buf) {   // K_o by bulk copy, u_e by cp.async
+        double* kp = reinterpret_cast<double*>(mine + buf * (C::KB + C::UB));
+        double* uu = reinterpret_cast<double*>(mine + buf * (C::KB + C::UB) + C::KB);
+        if (lane == 0) {
+            mbar_expect_tx(&bar[buf], (uint32_t)(C::LPS * 8));
+            bulk_load(kp, KP + e * C::LPS, (uint32_t)(C::LPS * 8), &bar[buf]);
         }
-        out[e * L + r] = t;
+        const int64_t base = cut_base[e];
+        for (int m = lane; m < L; m += 32) {
+            const int a = m / (N * N), b = (m / N) % N, j = m % N;
+            cp_async8_g(uu + m, u + base + a * pplane + b * prow + j);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // NS-1 cells in flight ahead of the one being multiplied (one cp.async
+    // group per fetch slot, empty groups past the end keep the count uniform)
+    #pragma unroll
+    for (int q = 0; q < NS - 1; ++q) {
+        const int64_t eq = e0 + q * stride;
+        if (eq < n_cut) fetch(eq, q);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    int it = 0;
+    for (int64_t e = e0; e < n_cut; e += stride, ++it) {
+        const int buf = it % NS;
+        const int64_t en = e + (NS - 1) * stride;
+        if (en < n_cut) fetch(en, (it + NS - 1) % NS);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1) : "memory");
+        __syncwarp();   // every lane's u_e gather of this cell is visible
+        mbar_wait(&bar[buf], (uint32_t)((it / NS) & 1));
+        const double* kp = reinterpret_cast<const double*>(mine + buf * (C::KB + C::UB));
+        const double* uu = reinterpret_cast<const double*>(mine + buf * (C::KB + C::UB) + C::KB);
+        for (int r = lane; r < L; r += 32) {
+            double t = 0.0;
+            int idx = r * (r + 1) / 2;   // (r, 0)
+            #pragma unroll 8
+            for (int m = 0; m <= r; ++m) t = fma(kp[idx + m], uu[m], t);
+            idx = (r + 1) * (r + 2) / 2 + r;   // (r+1, r)
+            #pragma unroll 8
+            for (int m = r + 1; m < L; ++m) {
+                t = fma(kp[idx], uu[m], t);
+                idx += m + 1;
+            }
+            out[e * L + r] = t;
+        }
+        __syncwarp();   // buffer reused NS cells later
     }
 }
 
@@ -142,16 +193,14 @@ template <int P>
 void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t* cut_base,
                     int64_t pplane, int64_t prow, const double* u, double* out) {
     if (!n_cut) return;
-    constexpr int L = (P + 1) * (P + 1) * (P + 1);
-    constexpr int W = cut_pre_warps<P>();
-    const size_t smem = (size_t)W * (L * (L + 1) / 2 + L) * 8;
+    using C = CutPre<P>;
     static bool attr_set = false;
     if (!attr_set) {
-        WCB_CUDA(cudaFuncSetAttribute(k_cut_pre<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        WCB_CUDA(cudaFuncSetAttribute(k_cut_pre<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
         attr_set = true;
     }
-    k_cut_pre<P><<<(unsigned)ceil_div(n_cut, W), 32 * W, smem, ctx->stream>>>(n_cut, KP, cut_base, pplane, prow,
-                                                                         u, out);
+    const int64_t blocks = std::min<int64_t>(ceil_div(n_cut, C::W), (int64_t)ctx->sm_count * std::max<int64_t>(1, (int64_t)(220 * 1024 / C::SMEM)));
+    k_cut_pre<P><<<(unsigned)blocks, 32 * C::W, C::SMEM, ctx->stream>>>(n_cut, KP, cut_base, pplane, prow, u, out);
     ctx->launches++;
 }
 
@@ -223,8 +272,11 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     unsigned long long amp = 0ULL;
     // Au/Bu persist across cell rows: plane P of row ex is plane 0 of row
     // ex+1, so when no uncut flag of the CTA changes between the rows its
-    // (exchanged) y/z contraction is reused instead of recomputed
+    // y/z contraction is reused instead of recomputed.  YP accumulates this
+    // warp's contribution to the next warp's node row 0 (y-local row P) for
+    // every x plane of the row; it is exchanged once per cell row.
     double Au[N][P], Bu[N][P];
+    double YP[N][P];
     bool pxRR = false, pxRL = false;
     for (int64_t ex = exA - 1; ex < exE; ++ex) {
         // codes of (ex, ey, ez), (ex, ey, ez-1), (ex, ey-1, ez), (ex, ey-1, ez-1)
@@ -236,6 +288,7 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
         }
         const double xRR = cRR == 1, xRL = cRL == 1;
         const bool cln = g.clean && cRR == 1 && ex >= 1 && __ldg(g.clean + (ex * g.n_e + ey) * g.n_e + ez) != 0;
+        // row-start barrier: every warp is past row ex-1's epilogue
         const bool live = __syncthreads_or((cRR | cRL) != 0);   // any uncut/cut work in this CTA row
 #if WCB3D_REUSE
         const bool reuse = ex > exA - 1 && !__syncthreads_or((cRR == 1) != pxRR || (cRL == 1) != pxRL);
@@ -244,6 +297,22 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
 #endif
         pxRR = cRR == 1;
         pxRL = cRL == 1;
+        if (producer && ex >= exA) {   // refill row ex-1's planes (a full row of look-ahead)
+            #pragma unroll 1
+            for (int q = 0; q < P; ++q) {
+                const int64_t np = (ex - 1) * P + q + S;
+                if (np <= G1) issue(np);
+            }
+            if (MODE == MODE_STEP) {   // psi_{k-1} of row ex's owned nodes for its epilogue
+                mbar_expect_tx(pbar, (uint32_t)T::PREV_BYTES);
+                tma_load_3d(smem + T::OFF_PREV, &tm_p, (int32_t)(K0 + PADJ), (int32_t)(ey0 * P + P),
+                            (int32_t)(ex * P + P), pbar);
+            }
+        }
+        #pragma unroll
+        for (int a2 = 0; a2 < N; ++a2)
+            #pragma unroll
+            for (int j = 0; j < P; ++j) YP[a2][j] = 0.0;
         #pragma unroll
         for (int c = 0; c < N; ++c) {
           if (!(c == 0 && reuse)) {   // CTA-uniform
@@ -276,40 +345,37 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
                     }
                 }
             }
-            double* xw = xch + ((size_t)((gp & 1) * T::NWARP + w) * 2 * P) * 32 + lane;
-            #pragma unroll
-            for (int j = 0; j < P; ++j) { xw[j * 32] = Au[P][j]; xw[(P + j) * 32] = Bu[P][j]; }
-            __syncthreads();
-            if (producer && c == 1 && ex >= exA) {   // row ex-1's epilogue is done: refill its planes
-                #pragma unroll 1
-                for (int q = 0; q < P; ++q) {
-                    const int64_t np = (ex - 1) * P + q + S;
-                    if (np <= G1) issue(np);
-                }
-                if (MODE == MODE_STEP) {   // psi_{k-1} of row ex's owned nodes for its epilogue
-                    mbar_expect_tx(pbar, (uint32_t)T::PREV_BYTES);
-                    tma_load_3d(smem + T::OFF_PREV, &tm_p, (int32_t)(K0 + PADJ), (int32_t)(ey0 * P + P),
-                                (int32_t)(ex * P + P), pbar);
-                }
-            }
-            if (!halo) {
-                const double* xr = xch + ((size_t)((gp & 1) * T::NWARP + up) * 2 * P) * 32 + lane;
-                #pragma unroll
-                for (int j = 0; j < P; ++j) { Au[0][j] += xr[j * 32]; Bu[0][j] += xr[(P + j) * 32]; }
-            }
           }
             // x pass (plane 0 of a reused row takes the previous row's plane-P Au/Bu)
-            if (!halo) {
+            #pragma unroll
+            for (int r = 0; r < N; ++r) {
                 #pragma unroll
-                for (int r = 0; r < N; ++r)
+                for (int j = 0; j < P; ++j)
+                    YP[r][j] = fma(kc[orb(P, r, c)], Au[P][j], fma(mc[orb(P, r, c)], Bu[P][j], YP[r][j]));
+                if (!halo) {
                     #pragma unroll
                     for (int b = 0; b < P; ++b)
                         #pragma unroll
                         for (int j = 0; j < P; ++j)
                             Y[r][b][j] = fma(kc[orb(P, r, c)], Au[b][j], fma(mc[orb(P, r, c)], Bu[b][j], Y[r][b][j]));
+                }
             }
         }
+        // y exchange of the shared node row: own + row above's contribution
+        {
+            double* xw = xch + (size_t)w * N * P * 32 + lane;
+            #pragma unroll
+            for (int r = 0; r < N; ++r)
+                #pragma unroll
+                for (int j = 0; j < P; ++j) xw[(r * P + j) * 32] = YP[r][j];
+        }
+        __syncthreads();
         if (!halo) {
+            const double* xr = xch + (size_t)up * N * P * 32 + lane;
+            #pragma unroll
+            for (int r = 0; r < N; ++r)
+                #pragma unroll
+                for (int j = 0; j < P; ++j) Y[r][0][j] += xr[(r * P + j) * 32];
             // dense cut cells: own y row (ey) and the y-up row (ey-1)
             const unsigned clR = __ballot_sync(0xffffffffu, cRR == 2);
             const bool edR = __shfl_sync(0xffffffffu, cRL == 2, 0);
@@ -368,10 +434,32 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
 }
 
 // The node column z = n1-1 when n_e is a multiple of 32 (no strip lane owns
-// it): one thread per (x plane, y row), direct sum over the <= 4 cells
-// (ex, ey, n_e-1) containing the node, in ascending (ex, ey) order.
+// it).  Stage 1: the z contraction of the last cell column onto its node
+// z = n1-1 for every (x plane, y row): zline = (m1[P] . u, k1[P] . u).
+// Stage 2: one thread per (x plane, y row) sums its <= 4 cells (ex, ey, n_e-1)
+// in ascending (ex, ey) order from those lines (coalesced in y).
+template <int P>
+__global__ void __launch_bounds__(256) k_scm3d_zline(Scm3DGeo g, Mats2<P> mt, const double* __restrict__ u,
+                                                    double2* __restrict__ zl) {
+    constexpr int N = P + 1;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t npl = g.n_ex * P + 1;
+    if (t >= npl * g.n1) return;
+    const int64_t I = t / g.n1, J = t % g.n1;
+    const double* row = u + (I + P) * g.pplane + (J + P) * g.prow + (g.n1 - 1 - P) + PADJ;
+    double zm = 0.0, zk = 0.0;
+    #pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double v = row[j];
+        zm = fma(mt.m[orb(P, P, j)], v, zm);
+        zk = fma(mt.k[orb(P, P, j)], v, zk);
+    }
+    zl[t] = make_double2(zm, zk);
+}
+
 template <int P, int MODE>
-__global__ void __launch_bounds__(128) k_scm3d_zcol(Scm3DGeo g, Mats2<P> mt, double sk, StepArgs a) {
+__global__ void __launch_bounds__(128) k_scm3d_zcol(Scm3DGeo g, Mats2<P> mt, double sk, const double2* __restrict__ zl,
+                                                   StepArgs a) {
     constexpr int N = P + 1;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n_pl = g.row_hi - g.row_lo;
@@ -391,19 +479,15 @@ __global__ void __launch_bounds__(128) k_scm3d_zcol(Scm3DGeo g, Mats2<P> mt, dou
                 const int64_t ez = g.n_e - 1;
                 const uint8_t code = g.mask[((ex + 1) * s_ + (ey + 1)) * s_ + ez + 1];
                 if (code == 1) {
-                    const int64_t b0 = (ex * P + P) * g.pplane + (ey * P + P) * g.prow + ez * P + PADJ;
                     double s = 0.0;
+                    #pragma unroll
                     for (int q = 0; q < N; ++q)
+                        #pragma unroll
                         for (int r = 0; r < N; ++r) {
-                            const double* u = a.cur + b0 + q * g.pplane + r * g.prow;
-                            double zm = 0.0, zk = 0.0;
-                            for (int j = 0; j < N; ++j) {
-                                zm = fma(mt.m[orb(P, P, j)], u[j], zm);
-                                zk = fma(mt.k[orb(P, P, j)], u[j], zk);
-                            }
+                            const double2 z = zl[(ex * P + q) * g.n1 + ey * P + r];
                             const double mq = mt.m[orb(P, ia, q)], kq = mt.k[orb(P, ia, q)];
                             const double mr = mt.m[orb(P, ib, r)], kr = mt.k[orb(P, ib, r)];
-                            s = fma(kq * mr + mq * kr, zm, fma(mq * mr, zk, s));
+                            s = fma(kq * mr + mq * kr, z.x, fma(mq * mr, z.y, s));
                         }
                     acc += s;
                 } else if (code == 2) {
@@ -464,9 +548,12 @@ void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map
     k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
     ctx->launches++;
     if (g.n_e % 32 == 0) {
+        WCB_REQUIRE(g.zline, "z-line buffer missing");
+        const int64_t nl = (g.n_ex * P + 1) * g.n1;
+        k_scm3d_zline<P><<<(unsigned)ceil_div(nl, 256), 256, 0, ctx->stream>>>(g, mt, a.cur, g.zline);
         const int64_t n = (g.row_hi - g.row_lo) * g.n1;
-        k_scm3d_zcol<P, MODE><<<(unsigned)ceil_div(n, 128), 128, 0, ctx->stream>>>(g, mt, sk, a);
-        ctx->launches++;
+        k_scm3d_zcol<P, MODE><<<(unsigned)ceil_div(n, 128), 128, 0, ctx->stream>>>(g, mt, sk, g.zline, a);
+        ctx->launches += 2;
     }
 }
 
