@@ -325,7 +325,9 @@ def run_config4(args, world, rank, local):
     """Config 4: plane-strain SCM p=5 IMEX.  One bench step = one full
     ImexPlan.run (n_t steps) on device-resident operator, mass, factors and
     state; the loop time is CUDA-event timed inside the run (tm.rhs).  N > 1
-    runs independent replicas (IMEX slab sharding is not built yet)."""
+    runs x slabs of the one grid (``dist.partition_imex``: cuts avoid cut
+    cells, NCCL halo exchange per step; strong scaling); ``--replicas`` runs
+    independent replicas instead."""
     import torch
     torch.cuda.set_device(local)
     from paper_2501_19013_b200 import _lib, imex_critical_time_step
@@ -345,8 +347,18 @@ def run_config4(args, world, rank, local):
     dt = cfg.safety * dtd
     n_t = cfg.n_t if args.nt is None else int(args.nt)
     f = lambda t: ricker(t, cfg.f_e)  # noqa: E731
-    plan = ImexPlan(M, op, prob.F_s, dt, c, d, obs_mat=prob.obs_mat, beta=cfg.beta, device=local)
-    n = prob.n_dof
+    slab_mode = world > 1 and not args.replicas
+    n_global = prob.n_dof
+    if slab_mode:
+        from paper_2501_19013_b200 import dist as wdist
+        del op
+        slab, plan = wdist.dist_imex_plan(prob, dt, beta=cfg.beta, device=local)
+        c = slab.c_idx
+        n = slab.n
+        parts = wdist.partition_imex(prob, world)
+    else:
+        plan = ImexPlan(M, op, prob.F_s, dt, c, d, obs_mat=prob.obs_mat, beta=cfg.beta, device=local)
+        n = prob.n_dof
     for _ in range(args.warmup):
         plan.run(f, n_t, gamma=cfg.gamma)
     barrier(world)
@@ -361,12 +373,13 @@ def run_config4(args, world, rank, local):
     launches = ctx.launches - launches0
     assert np.all(np.isfinite(r.psi)), "non-finite field"
     total = reduce_max(sum(loops), world)
-    value = n * world * n_t * args.steps / total
+    units = n_global if slab_mode else n * world
+    value = units * n_t * args.steps / total
     e2e_t = reduce_max(sum(walls), world)
-    e2e_value = n * world * n_t * args.steps / e2e_t
+    e2e_value = units * n_t * args.steps / e2e_t
     fact_nnz = plan.fact_nnz
     L = 2 * (cfg.p + 1) ** 2
-    n_cut = int(prob.grid.cut_lex.shape[0])
+    n_cut = int(slab.cut_cells.shape[0]) if slab_mode else int(prob.grid.cut_lex.shape[0])
     nc = int(c.shape[0])
     bytes_step = 32.0 * n + 8.0 * L * (L + 1) / 2 * n_cut + 12.0 * fact_nnz + 48.0 * nc
     per_step_s = sum(loops) / (args.steps * n_t)
@@ -375,16 +388,18 @@ def run_config4(args, world, rank, local):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if slab_mode else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded voids and source, BASELINE config shapes)",
             "config": {"workload": (f"config4: 2D plane-strain SCM GLL p={cfg.p}, {cfg.n_e}^2 cells, "
                                     f"E={cfg.E}, nu={cfg.nu}, {cfg.n_random} random voids r in "
                                     f"{list(cfg.r_range)}, alpha={cfg.alpha}, IMEX: CDM on d, Newmark "
                                     f"beta={cfg.beta} gamma={cfg.gamma} on c (SuperLU factors), "
                                     f"x point force (Ricker), {cfg.n_t} steps at 0.9 dt_crit(d)"),
-                       "n_dof": n, "n_c": nc, "n_cut": n_cut, "n_t": n_t, "seed": cfg.seed,
+                       "n_dof": n_global, "n_c": nc, "n_cut": n_cut, "n_t": n_t, "seed": cfg.seed,
                        "factor_nnz": fact_nnz, "dt": dt,
-                       "parallelism": f"{world} independent replica(s), one per GPU",
+                       "parallelism": (f"{world} x slabs of one grid (cell rows {parts}), NCCL halo "
+                                       f"exchange per step; rank-0 slab figures for n_c/n_cut/roofline"
+                                       if slab_mode else f"{world} independent replica(s), one per GPU"),
                        "setup_s": round(t_build, 2), "dt_crit_s": round(t_eig, 3),
                        "factorization_s": round(plan.factorization, 2),
                        "l2": f"working set {bytes_step / 1e9:.2f} GB per time step (> L2)"},
@@ -451,6 +466,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--nt", type=int, default=None, help="override the time-step count (profiling)")
     ap.add_argument("--slabs", action="store_true", help="N>1: x slabs of one 2D grid instead of replicas")
+    ap.add_argument("--replicas", action="store_true", help="config 4 at N>1: replicas instead of slabs")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

@@ -117,6 +117,12 @@ typedef struct {
     int64_t n_cut;
     const int64_t* cut_cells;    /* n_cut cell lex ids, ascending                        */
     const double* cut_K;         /* n_cut * L * L, L = 2 (p+1)^2                          */
+    /* x slab as in wcb_scm_desc (x_cell_hi == 0: the whole grid); n_node,
+     * lex_of_compact, cell_class and cut_cells then describe the slab's nodes
+     * and the cell rows [x_cell_lo-1, x_cell_hi) */
+    int64_t x_cell_lo;
+    int64_t x_cell_hi;
+    int32_t x_owns_last;
 } wcb_elastic_desc;
 
 /* ---- library / context ------------------------------------------------- */
@@ -149,6 +155,14 @@ int wcb_operator_apply(wcb_operator* op, const double* x, double* y);
 int wcb_operator_halo(const wcb_operator* op, int64_t* out8);
 
 /* ---- multi-GPU slabs: NCCL communicator per context -------- */
+/* imex_run over consecutive x slabs of one plane-strain grid emulated in one
+ * process (plans share one context; halos by device copies after every step).
+ * Per plan: psi_out (its DOFs), psi_dot_out (its v_c, may be NULL), obs_out
+ * (its observer partial sums, n_obs x (n_t+1), may be NULL). */
+int wcb_imex_group_run(int n_plans, wcb_imex_plan** plans, double f0, const double* ft_k,
+                       const double* ft_new, double dt, int64_t n_t, double beta, double gamma,
+                       double** psi_out, double** psi_dot_out, double** obs_out,
+                       wcb_divergence* div, wcb_timings* tm);
 /* Halo exchange with the +-1 slab neighbours after every step and all-reduces
  * of the divergence amplitude / observer partial sums run on the context's
  * stream.  NCCL is loaded with dlopen("libnccl.so.2"). */

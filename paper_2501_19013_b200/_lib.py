@@ -34,7 +34,7 @@ EXPORTS = (
     "wcb_max_gen_eig", "wcb_max_gen_eig_sub", "wcb_cdm_plan_create", "wcb_cdm_plan_destroy",
     "wcb_cdm_plan_run", "wcb_cdm_plan_run_device", "wcb_imex_plan_create",
     "wcb_imex_plan_destroy", "wcb_imex_plan_run", "wcb_dist_unique_id", "wcb_dist_init",
-    "wcb_dist_finalize", "wcb_cdm_group_run", "wcb_cdm_plan_step_bytes",
+    "wcb_dist_finalize", "wcb_cdm_group_run", "wcb_cdm_plan_step_bytes", "wcb_imex_group_run",
 )
 
 _p = C.c_void_p
@@ -71,7 +71,8 @@ class ElasticDesc(C.Structure):
     _fields_ = [("p", _i32), ("n_e", _i64 * 2), ("lam", _d), ("mu", _d), ("m1", _dp),
                 ("k1", _dp), ("g1", _dp), ("cell_class", _i8p), ("n_node", _i64),
                 ("lex_of_compact", _i64p), ("n_cut", _i64), ("cut_cells", _i64p),
-                ("cut_K", _dp)]
+                ("cut_K", _dp), ("x_cell_lo", _i64), ("x_cell_hi", _i64),
+                ("x_owns_last", _i32)]
 
 
 class LU(C.Structure):
@@ -115,6 +116,9 @@ _SIGS = {
                                     C.POINTER(Divergence), C.POINTER(Timings)]),
     "wcb_imex_plan_run": (C.c_int, [_p, _d, _dp, _dp, _d, _i64, _d, _d, _dp, _dp, _dp,
                                     _dp, _dp, C.POINTER(Divergence), C.POINTER(Timings)]),
+    "wcb_imex_group_run": (C.c_int, [C.c_int, C.POINTER(_p), _d, _dp, _dp, _d, _i64, _d, _d,
+                                     C.POINTER(_dp), C.POINTER(_dp), C.POINTER(_dp),
+                                     C.POINTER(Divergence), C.POINTER(Timings)]),
 }
 
 _lock = threading.Lock()

@@ -500,23 +500,14 @@ static void exchange_halos(std::vector<wcb_cdm_plan*>& Ps, std::vector<double*>&
     const size_t n = Ps.size();
     if (n == 1) {
         int64_t h[8];
-        Context* ctx = Ps[0]->op->ctx;
-        if (ctx->nccl && Ps[0]->op->halo(h)) nccl_exchange_halo(ctx, cur[0], h);
+        Operator* op = Ps[0]->op;
+        Context* ctx = op->ctx;
+        if (ctx->nccl && op->halo(h)) nccl_exchange_halo(ctx, cur[0], h, op->halo_nplanes, op->halo_pstride);
         return;
     }
-    cudaStream_t s = Ps[0]->op->ctx->stream;
-    for (size_t r = 0; r + 1 < n; ++r) {
-        int64_t a[8], b[8];
-        Ps[r]->op->halo(a);
-        Ps[r + 1]->op->halo(b);
-        WCB_REQUIRE(a[0] == b[0] && a[6] == b[2] && b[2] > 0 && a[4] == 1,
-                    "plans are not consecutive slabs of one grid");
-        const size_t xs = (size_t)a[0];
-        WCB_CUDA(cudaMemcpyAsync(cur[r + 1] + b[1] * xs, cur[r] + a[5] * xs, a[6] * xs * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, s));
-        WCB_CUDA(cudaMemcpyAsync(cur[r] + a[3] * xs, cur[r + 1] + b[7] * xs, xs * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, s));
-    }
+    std::vector<Operator*> ops;
+    for (auto* P : Ps) ops.push_back(P->op);
+    copy_exchange_halo(ops, cur, Ps[0]->op->ctx->stream);
 }
 
 // The CDM loop of src/timeint.py:159-193 for one plan or a group of slab

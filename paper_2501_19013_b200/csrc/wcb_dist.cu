@@ -56,23 +56,45 @@ static F sym(void* h, const char* name) {
 
 Nccl* nccl_for(Context* ctx) { return ctx->nccl; }
 
-void nccl_exchange_halo(Context* ctx, double* state, const int64_t* h) {
+void nccl_exchange_halo(Context* ctx, double* state, const int64_t* h, int nplanes, int64_t pstride) {
     Nccl* N = ctx->nccl;
     if (!N || N->world == 1) return;
     const int64_t xs = h[0];
     const int up = N->rank + 1, down = N->rank - 1;
     NCCL_CHECK(N, N->gstart());
-    if (h[2] > 0 && down >= 0) {
-        // top halo (p rows) <- previous slab's last p rows; our first row -> its bottom halo
-        NCCL_CHECK(N, N->recv(state + h[1] * xs, (size_t)(h[2] * xs), ncclDouble, down, N->comm, ctx->stream));
-        NCCL_CHECK(N, N->send(state + h[7] * xs, (size_t)xs, ncclDouble, down, N->comm, ctx->stream));
-    }
-    if (h[4] > 0 && up < N->world) {
-        // our last p rows -> next slab's top halo; its first row -> our bottom halo
-        NCCL_CHECK(N, N->send(state + h[5] * xs, (size_t)(h[6] * xs), ncclDouble, up, N->comm, ctx->stream));
-        NCCL_CHECK(N, N->recv(state + h[3] * xs, (size_t)(h[4] * xs), ncclDouble, up, N->comm, ctx->stream));
+    for (int pl = 0; pl < nplanes; ++pl) {
+        double* st = state + pl * pstride;
+        if (h[2] > 0 && down >= 0) {
+            // top halo (p rows) <- previous slab's last p rows; our first row -> its bottom halo
+            NCCL_CHECK(N, N->recv(st + h[1] * xs, (size_t)(h[2] * xs), ncclDouble, down, N->comm, ctx->stream));
+            NCCL_CHECK(N, N->send(st + h[7] * xs, (size_t)xs, ncclDouble, down, N->comm, ctx->stream));
+        }
+        if (h[4] > 0 && up < N->world) {
+            // our last p rows -> next slab's top halo; its first row -> our bottom halo
+            NCCL_CHECK(N, N->send(st + h[5] * xs, (size_t)(h[6] * xs), ncclDouble, up, N->comm, ctx->stream));
+            NCCL_CHECK(N, N->recv(st + h[3] * xs, (size_t)(h[4] * xs), ncclDouble, up, N->comm, ctx->stream));
+        }
     }
     NCCL_CHECK(N, N->gend());
+}
+
+void copy_exchange_halo(const std::vector<Operator*>& ops, const std::vector<double*>& st, cudaStream_t s) {
+    for (size_t r = 0; r + 1 < ops.size(); ++r) {
+        int64_t a[8], b[8];
+        ops[r]->halo(a);
+        ops[r + 1]->halo(b);
+        WCB_REQUIRE(a[0] == b[0] && a[6] == b[2] && b[2] > 0 && a[4] == 1,
+                    "plans are not consecutive slabs of one grid");
+        const size_t xs = (size_t)a[0];
+        for (int pl = 0; pl < ops[r]->halo_nplanes; ++pl) {
+            double* A = st[r] + pl * ops[r]->halo_pstride;
+            double* B = st[r + 1] + pl * ops[r + 1]->halo_pstride;
+            WCB_CUDA(cudaMemcpyAsync(B + b[1] * xs, A + a[5] * xs, a[6] * xs * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+            WCB_CUDA(cudaMemcpyAsync(A + a[3] * xs, B + b[7] * xs, xs * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+        }
+    }
 }
 
 void nccl_allreduce_max_u64(Context* ctx, unsigned long long* d, int64_t n) {

@@ -720,40 +720,73 @@ int wcb_imex_plan_destroy(wcb_imex_plan* plan) {
     return WCB_OK;
 }
 
-int wcb_imex_plan_run(wcb_imex_plan* P, double f0, const double* ft_k, const double* ft_new,
-                      double dt, int64_t n_t, double beta, double gamma, const double* psi0,
-                      const double* v0, double* psi_out, double* psi_dot_out, double* obs_out,
-                      wcb_divergence* div, wcb_timings* tm) {
-    try {
-        WCB_REQUIRE(P && psi_out, "NULL argument");
-        WCB_REQUIRE(n_t >= 0, "negative n_t");
+}  // extern "C"
+
+namespace wcb {
+
+// The IMEX loop (src/timeint.py:196-292) for one plan, or for consecutive x
+// slabs of one grid: plans sharing one context (emulated ranks, halos by
+// device copies) or one plan per process with an NCCL communicator on its
+// context.  The slab cuts leave every c patch and the cells around it inside
+// one slab, so only the explicit d rows need the neighbours' halo rows: one
+// exchange per step, after the corrector, exactly as in the CDM loop.
+static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const double* ft_k,
+                           const double* ft_new, double dt, int64_t n_t, double beta, double gamma,
+                           const std::vector<const double*>& psi0, const std::vector<const double*>& v0,
+                           const std::vector<double*>& psi_out, const std::vector<double*>& psi_dot_out,
+                           const std::vector<double*>& obs_out, wcb_divergence* div, wcb_timings* tm) {
+    const size_t G = Ps.size();
+    Context* ctx = Ps[0]->op->ctx;
+    for (auto* P : Ps) WCB_REQUIRE(P->op->ctx == ctx, "group plans must share one context");
+    WCB_REQUIRE(n_t >= 0, "negative n_t");
+    WCB_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    if (div) { div->step = -1; div->amplitude = 0.0; }
+    if (tm) { tm->factorization = 0.0; tm->rhs = 0.0; tm->backward_insertion = 0.0; }
+    std::vector<Operator*> ops;
+    for (auto* P : Ps) ops.push_back(P->op);
+    auto exchange = [&](const std::vector<double*>& st) {
+        if (G == 1) {
+            int64_t h[8];
+            if (ctx->nccl && ops[0]->halo(h))
+                nccl_exchange_halo(ctx, st[0], h, ops[0]->halo_nplanes, ops[0]->halo_pstride);
+        } else {
+            copy_exchange_halo(ops, st, s);
+        }
+    };
+    // force tables: index 0 = f(0) for the bootstrap; ft_k[k], ft_new[k] per step
+    std::vector<double> hk(n_t + 1), hn(std::max<int64_t>(n_t, 1));
+    hk[0] = f0;
+    for (int64_t k = 0; k < n_t; ++k) { hk[k + 1] = ft_k[k]; hn[k] = ft_new[k]; }
+    std::vector<DevBuf<double>> tmp(G), dobs(G);
+    const int64_t stride = n_t + 1;
+    std::vector<double*> cur(G), prev(G);
+    for (size_t r = 0; r < G; ++r) {
+        wcb_imex_plan* P = Ps[r];
         Operator* op = P->op;
-        Context* ctx = op->ctx;
-        WCB_CUDA(cudaSetDevice(ctx->device));
-        cudaStream_t s = ctx->stream;
-        const int64_t n = op->n, ns = op->n_state, nc = P->n_c;
-        const bool has_c = nc > 0, has_d = P->n_d > 0;
-        if (div) { div->step = -1; div->amplitude = 0.0; }
-        if (tm) { tm->factorization = 0.0; tm->rhs = 0.0; tm->backward_insertion = 0.0; }
-        // force tables: index 0 = f(0) for the bootstrap; ft_k[k], ft_new[k] per step
-        std::vector<double> hk(n_t + 1), hn(std::max<int64_t>(n_t, 1));
-        hk[0] = f0;
-        for (int64_t k = 0; k < n_t; ++k) { hk[k + 1] = ft_k[k]; hn[k] = ft_new[k]; }
         P->ft_k.alloc(hk.size(), s); P->ft_k.upload(hk.data(), hk.size(), s);
         P->ft_new.alloc(hn.size(), s); P->ft_new.upload(hn.data(), hn.size(), s);
         P->amp.alloc(n_t + 1, s);
         P->amp.zero(s);
-        // initial state
-        DevBuf<double> tmp(std::max<int64_t>(n, 1));
+        tmp[r].alloc(std::max<int64_t>(op->n, 1));
         P->A.zero(s); P->V.zero(s); P->B.zero(s); P->T.zero(s);
-        if (psi0) { tmp.upload(psi0, n, s); op->scatter(tmp.p, P->A.p); }
-        if (v0) { tmp.upload(v0, n, s); op->scatter(tmp.p, P->V.p); }
+        if (psi0[r]) { tmp[r].upload(psi0[r], op->n, s); op->scatter(tmp[r].p, P->A.p); }
+        if (v0[r]) { tmp[r].upload(v0[r], op->n, s); op->scatter(tmp[r].p, P->V.p); }
+        if (P->n_obs && obs_out[r]) dobs[r].alloc(P->n_obs * stride, s);
+        cur[r] = P->A.p;
+        prev[r] = P->B.p;
+    }
+    exchange(cur);   // psi_0 halos for the bootstrap apply
+    for (size_t r = 0; r < G; ++r) {
+        wcb_imex_plan* P = Ps[r];
+        Operator* op = P->op;
+        const int64_t ns = op->n_state, nc = P->n_c;
         // bootstrap (src/timeint.py:246-256)
         op->apply(P->A.p, P->T.p);
         k_imex_boot<<<grid1(ctx, ns), 256, 0, s>>>(ns, P->A.p, P->V.p, P->T.p, P->m_d_state.p, P->src,
                                                    P->ft_k.p, dt, P->B.p);
         ctx->launches++;
-        if (has_c) {
+        if (nc > 0) {
             // r0_c = f0 F_c - (K psi)_c ; a_c = M_cc^-1 r0_c
             k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
             k_c_rhs<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->Fc.p, P->ft_k.p, 0, P->Kc.p, P->rhs.p);
@@ -767,73 +800,80 @@ int wcb_imex_plan_run(wcb_imex_plan* P, double f0, const double* ft_k, const dou
             ctx->launches += 3;
             WCB_CUDA(cudaStreamSynchronize(s));
         }
-        WCB_CHECK_LAUNCH();
-        const int64_t stride = n_t + 1;
-        StepArgs a;
-        a.minv = P->minv.p;
-        a.F = P->src;
-        a.dt2 = dt * dt;
-        DevBuf<double> dobs;
-        if (P->n_obs && obs_out) dobs.alloc(P->n_obs * stride, s);
-        auto record = [&](int64_t k, const double* psi) {
-            if (!(P->n_obs && obs_out)) return;
-            StepArgs r;
-            r.cur = psi;
-            r.k = k;
-            r.n_obs = P->n_obs;
-            r.obs_ptr = P->obs_indptr.p;
-            r.obs_idx = P->obs_idx.p;
-            r.obs_val = P->obs_val.p;
-            r.obs_out = dobs.p;
-            r.obs_stride = stride;
-            launch_record_observers(ctx, r);
-        };
-        record(0, P->A.p);
-        double* cur = P->A.p;
-        double* prev = P->B.p;
-        const double c1 = 0.5 * dt * dt * (1.0 - 2.0 * beta);
-        const double c2 = dt * (1.0 - gamma);
-        const double bdt2 = beta * dt * dt;
-        const double gdt = gamma * dt;
-        WCB_CUDA(cudaEventRecord(ctx->ev0, s));
-        std::vector<unsigned long long> h_amp(n_t + 1, 0ULL);
-        int64_t checked = 0;
-        bool diverged = false;
-        auto inspect = [&](int64_t upto) -> bool {
-            if (upto <= checked) return false;
-            WCB_CUDA(cudaMemcpyAsync(h_amp.data() + checked + 1, P->amp.p + checked + 1,
-                                     (upto - checked) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-            WCB_CUDA(cudaStreamSynchronize(s));
-            for (int64_t k = checked + 1; k <= upto; ++k) {
-                double v;
-                std::memcpy(&v, &h_amp[k], sizeof(v));
-                if (!std::isfinite(v) || v > 1.0e12) {
-                    if (div) { div->step = k; div->amplitude = v; }
-                    return true;
-                }
+    }
+    WCB_CHECK_LAUNCH();
+    auto record = [&](size_t r, int64_t k, const double* psi) {
+        wcb_imex_plan* P = Ps[r];
+        if (!(P->n_obs && obs_out[r])) return;
+        StepArgs o;
+        o.cur = psi;
+        o.k = k;
+        o.n_obs = P->n_obs;
+        o.obs_ptr = P->obs_indptr.p;
+        o.obs_idx = P->obs_idx.p;
+        o.obs_val = P->obs_val.p;
+        o.obs_out = dobs[r].p;
+        o.obs_stride = stride;
+        launch_record_observers(ctx, o);
+    };
+    for (size_t r = 0; r < G; ++r) record(r, 0, Ps[r]->A.p);
+    const double c1 = 0.5 * dt * dt * (1.0 - 2.0 * beta);
+    const double c2 = dt * (1.0 - gamma);
+    const double bdt2 = beta * dt * dt;
+    const double gdt = gamma * dt;
+    WCB_CUDA(cudaEventRecord(ctx->ev0, s));
+    std::vector<unsigned long long> h_amp(G * (n_t + 1), 0ULL);
+    int64_t checked = 0;
+    bool diverged = false;
+    auto inspect = [&](int64_t upto) -> bool {
+        if (upto <= checked) return false;
+        const int64_t cnt = upto - checked;
+        for (size_t r = 0; r < G; ++r) {
+            nccl_allreduce_max_u64(ctx, Ps[r]->amp.p + checked + 1, cnt);
+            WCB_CUDA(cudaMemcpyAsync(h_amp.data() + r * (n_t + 1) + checked + 1, Ps[r]->amp.p + checked + 1,
+                                     cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        }
+        WCB_CUDA(cudaStreamSynchronize(s));
+        for (int64_t k = checked + 1; k <= upto; ++k) {
+            unsigned long long bb = 0ULL;
+            for (size_t r = 0; r < G; ++r) bb = std::max(bb, h_amp[r * (n_t + 1) + k]);
+            double v;
+            std::memcpy(&v, &bb, sizeof(v));
+            if (!std::isfinite(v) || v > 1.0e12) {
+                if (div) { div->step = k; div->amplitude = v; }
+                return true;
             }
-            checked = upto;
-            return false;
-        };
-        for (int64_t k = 0; k < n_t; ++k) {
+        }
+        checked = upto;
+        return false;
+    };
+    for (int64_t k = 0; k < n_t; ++k) {
+        for (size_t r = 0; r < G; ++r) {
+            wcb_imex_plan* P = Ps[r];
+            Operator* op = P->op;
+            const int64_t ns = op->n_state, nc = P->n_c;
             // 1. explicit d step into prev (c slots overwritten below)
-            if (has_d) {
-                a.cur = cur;
-                a.prev = prev;
-                a.out = prev;
+            if (P->n_d > 0) {
+                StepArgs a;
+                a.minv = P->minv.p;
+                a.F = P->src;
+                a.dt2 = dt * dt;
+                a.cur = cur[r];
+                a.prev = prev[r];
+                a.out = prev[r];
                 a.ft = P->ft_k.p + 1;   // ft_k[k]
                 a.k = k;
                 a.amp = P->amp.p + (k + 1);
                 op->cdm_step(a);
             } else {
-                WCB_CUDA(cudaMemcpyAsync(prev, cur, ns * sizeof(double), cudaMemcpyDeviceToDevice, s));
+                WCB_CUDA(cudaMemcpyAsync(prev[r], cur[r], ns * sizeof(double), cudaMemcpyDeviceToDevice, s));
             }
-            if (has_c) {
+            if (nc > 0) {
                 // 2. c predictor into the new state
                 k_c_predict<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->psi_c.p, P->v_c.p, P->a_c.p,
-                                                           dt, c1, c2, prev, P->pred.p, P->vpred.p);
+                                                           dt, c1, c2, prev[r], P->pred.p, P->vpred.p);
                 // 3. rhs_c with updated d and predicted c
-                op->apply_subset(prev, P->T.p);   // tiles owning c rows only
+                op->apply_subset(prev[r], P->T.p);   // tiles owning c rows only
                 k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
                 k_c_rhs<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->Fc.p, P->ft_new.p, k, P->Kc.p, P->rhs.p);
                 ctx->launches += 3;
@@ -841,38 +881,82 @@ int wcb_imex_plan_run(wcb_imex_plan* P, double f0, const double* ft_k, const dou
                 lu_solve(ctx, P, P->S, P->rhs.p, P->y.p);   // result in y (column-permuted space)
                 k_c_correct<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->S.perm_c.p, P->y.p, P->pred.p,
                                                            P->vpred.p, bdt2, gdt, P->a_c.p, P->psi_c.p, P->v_c.p,
-                                                           prev, P->amp.p + (k + 1));
+                                                           prev[r], P->amp.p + (k + 1));
                 ctx->launches++;
             }
-            std::swap(cur, prev);
-            record(k + 1, cur);
-            if ((k + 1) % 256 == 0) {
-                WCB_CHECK_LAUNCH();
-                if (inspect(k + 1)) { diverged = true; break; }
-            }
+            std::swap(cur[r], prev[r]);
         }
-        WCB_CUDA(cudaEventRecord(ctx->ev1, s));
-        WCB_CHECK_LAUNCH();
-        if (!diverged) diverged = inspect(n_t);
-        WCB_CUDA(cudaEventSynchronize(ctx->ev1));
-        float ms = 0.f;
-        WCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-        if (tm) tm->rhs = ms * 1e-3;
-        if (diverged) throw Error{WCB_E_DIVERGED, "solution diverged"};
-        op->gather(cur, tmp.p);
-        WCB_CUDA(cudaMemcpyAsync(psi_out, tmp.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        exchange(cur);
+        for (size_t r = 0; r < G; ++r) record(r, k + 1, cur[r]);
+        if ((k + 1) % 256 == 0) {
+            WCB_CHECK_LAUNCH();
+            if (inspect(k + 1)) { diverged = true; break; }
+        }
+    }
+    WCB_CUDA(cudaEventRecord(ctx->ev1, s));
+    WCB_CHECK_LAUNCH();
+    if (!diverged) diverged = inspect(n_t);
+    WCB_CUDA(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    WCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    if (tm) tm->rhs = ms * 1e-3;
+    if (diverged) throw Error{WCB_E_DIVERGED, "solution diverged"};
+    for (size_t r = 0; r < G; ++r) {
+        wcb_imex_plan* P = Ps[r];
+        Operator* op = P->op;
+        op->gather(cur[r], tmp[r].p);
+        WCB_CUDA(cudaMemcpyAsync(psi_out[r], tmp[r].p, op->n * sizeof(double), cudaMemcpyDeviceToHost, s));
         // v_c in c order (the caller scatters it when d is empty, src/timeint.py:285-288)
-        if (psi_dot_out && has_c)
-            WCB_CUDA(cudaMemcpyAsync(psi_dot_out, P->v_c.p, nc * sizeof(double), cudaMemcpyDeviceToHost, s));
-        if (P->n_obs && obs_out)
-            WCB_CUDA(cudaMemcpyAsync(obs_out, dobs.p, P->n_obs * stride * sizeof(double),
+        if (psi_dot_out[r] && P->n_c > 0)
+            WCB_CUDA(cudaMemcpyAsync(psi_dot_out[r], P->v_c.p, P->n_c * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (P->n_obs && obs_out[r]) {
+            nccl_allreduce_sum_f64(ctx, dobs[r].p, P->n_obs * stride);
+            WCB_CUDA(cudaMemcpyAsync(obs_out[r], dobs[r].p, P->n_obs * stride * sizeof(double),
                                      cudaMemcpyDeviceToHost, s));
-        WCB_CUDA(cudaStreamSynchronize(s));
+        }
+    }
+    WCB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace wcb
+
+extern "C" {
+
+int wcb_imex_plan_run(wcb_imex_plan* P, double f0, const double* ft_k, const double* ft_new,
+                      double dt, int64_t n_t, double beta, double gamma, const double* psi0,
+                      const double* v0, double* psi_out, double* psi_dot_out, double* obs_out,
+                      wcb_divergence* div, wcb_timings* tm) {
+    try {
+        WCB_REQUIRE(P && psi_out, "NULL argument");
+        std::vector<wcb_imex_plan*> Ps{P};
+        imex_run_group(Ps, f0, ft_k, ft_new, dt, n_t, beta, gamma, {psi0}, {v0}, {psi_out}, {psi_dot_out},
+                       {obs_out}, div, tm);
         return WCB_OK;
     } catch (const Error& e) {
         set_error(e.msg);
         return e.code;
     }
 }
+
+int wcb_imex_group_run(int n_plans, wcb_imex_plan** plans, double f0, const double* ft_k,
+                       const double* ft_new, double dt, int64_t n_t, double beta, double gamma,
+                       double** psi_out, double** psi_dot_out, double** obs_out,
+                       wcb_divergence* div, wcb_timings* tm) {
+    try {
+        WCB_REQUIRE(n_plans >= 1 && plans && psi_out, "NULL argument");
+        std::vector<wcb_imex_plan*> Ps(plans, plans + n_plans);
+        for (auto* P : Ps) WCB_REQUIRE(P, "NULL plan");
+        std::vector<const double*> none(n_plans, nullptr);
+        std::vector<double*> po(psi_out, psi_out + n_plans), pd(n_plans, nullptr), ob(n_plans, nullptr);
+        if (psi_dot_out) pd.assign(psi_dot_out, psi_dot_out + n_plans);
+        if (obs_out) ob.assign(obs_out, obs_out + n_plans);
+        imex_run_group(Ps, f0, ft_k, ft_new, dt, n_t, beta, gamma, none, none, po, pd, ob, div, tm);
+        return WCB_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
+}
+
 
 }  // extern "C"

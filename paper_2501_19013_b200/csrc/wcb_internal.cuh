@@ -260,6 +260,8 @@ struct Operator {
     // may precompute which cells read it (default: every node loads 1/m)
     virtual void bind_minv(const double* /*d_minv*/) {}
     double minv_skipped = 0.0;   // DOFs whose 1/m the bound step takes from a table (no 8 B load)
+    int halo_nplanes = 1;        // component planes of the state (slab halo exchange)
+    int64_t halo_pstride = 0;    // doubles between component planes
     // algorithmic bytes of one fused step (for the roofline)
     virtual double step_bytes() const = 0;
     // slab halo layout (state rows of out[0] doubles), see wcb_operator_halo;
@@ -276,7 +278,11 @@ void ctx_release(Context* ctx);
 // NCCL (loaded with dlopen on first use; the library does not link it)
 struct Nccl;
 Nccl* nccl_for(Context* ctx);   // null unless wcb_dist_init was called on ctx
-void nccl_exchange_halo(Context* ctx, double* state, const int64_t* h);  // +-1 neighbours
+// +-1 neighbours; nplanes component planes `pstride` doubles apart
+void nccl_exchange_halo(Context* ctx, double* state, const int64_t* h, int nplanes = 1, int64_t pstride = 0);
+// the same exchange between consecutive slab states of one process (device copies)
+struct Operator;
+void copy_exchange_halo(const std::vector<Operator*>& ops, const std::vector<double*>& states, cudaStream_t s);
 void nccl_allreduce_max_u64(Context* ctx, unsigned long long* d, int64_t n);
 void nccl_allreduce_sum_f64(Context* ctx, double* d, int64_t n);
 

@@ -957,6 +957,9 @@ Operator* make_elastic_operator(Context* ctx, const wcb_elastic_desc* e) {
     d.n_cut = e->n_cut;
     d.cut_cells = e->cut_cells;
     d.cut_K = e->cut_K;
+    d.x_cell_lo = e->x_cell_lo;
+    d.x_cell_hi = e->x_cell_hi;
+    d.x_owns_last = e->x_owns_last;
     return build_scm_operator(ctx, &d, 2, e->lam, e->mu, e->g1);
 }
 
@@ -967,7 +970,7 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
     const int p = d->p;
     if (dim == 2) WCB_REQUIRE(p >= 1 && p <= 6, "p must be in 1..6 for the 2D kernel");
     else WCB_REQUIRE(p >= 1 && p <= 4, "p must be in 1..4 for the 3D kernel");
-    WCB_REQUIRE(ncomp == 1 || (dim == 2 && d->x_cell_hi == 0), "elastic operator: 2D, single slab");
+    WCB_REQUIRE(ncomp == 1 || dim == 2, "elastic operator: 2D");
     for (int k = 1; k < dim; ++k)
         WCB_REQUIRE(d->n_e[k] == d->n_e[0], "cubic grids only (n_e equal on all axes)");
     WCB_REQUIRE(d->n_e[0] >= 1, "n_e must be >= 1");
@@ -1015,6 +1018,8 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
     const int64_t xrows = op->n1x + 2 * p;
     op->plane = xrows * op->xstride;
     op->n_state = ncomp * op->plane;
+    op->halo_nplanes = ncomp;
+    op->halo_pstride = op->plane;
     const int N = p + 1;
     op->m1.assign(d->m1, d->m1 + N * N);
     op->k1.assign(d->k1, d->k1 + N * N);

@@ -163,3 +163,171 @@ def dist_cdm_run(prob, f_t, dt: float, n_t: int, device=None, gather: bool = Tru
         if rank == 0:
             full = np.concatenate(pieces)
     return slab, res, full
+
+
+# --------------------------------------------------------------------------
+# Plane-strain IMEX (BASELINE config 4) over x slabs.  The c set is a union of
+# independent patches (the nodes of the cut cells around each void); a slab
+# cut at cell row c is admissible when cell rows c-2, c-1 and c hold no cut
+# cell, so every patch, every cell touching a patch node, and hence every c
+# row of K lie inside one slab's owned rows.  The explicit d step is the slab kernel of the CDM
+# path (p halo rows above, one below, exchanged once per step after the
+# corrector); the c predictor / solve / corrector are slab-local.  Each slab
+# factorises its own S_cc and M_cc blocks with SuperLU in the reference
+# configuration (a block of independent patches: the same matrices, a
+# per-slab ordering), so sharded fields agree with the single-GPU run to
+# rounding (tested at 1e-12), not bitwise.
+
+def partition_imex(prob, world: int):
+    """Balanced cell-row ranges whose cuts avoid cut cells (see above)."""
+    g = prob.grid
+    n_e = g.n_e
+    cut_rows = np.zeros(n_e, dtype=bool)
+    cut_rows[np.asarray(g.cut_lex, dtype=np.int64) // n_e] = True
+    # cut c admissible: no cut cell in rows c-2, c-1 (the upper slab's c rows
+    # then never reach its bottom halo row c*p) nor in row c (the lower
+    # slab's c rows never reach the cell row it recomputes from its top halo)
+    ok = np.zeros(n_e + 1, dtype=bool)
+    for c in range(2, n_e):
+        ok[c] = not (cut_rows[c - 2] or cut_rows[c - 1] or cut_rows[c])
+    base = partition(prob, world)
+    cuts = [0]
+    for r in range(1, world):
+        want = base[r][0]
+        cand = np.flatnonzero(ok)
+        cand = cand[cand > cuts[-1]]
+        if cand.size == 0:
+            raise ValueError("no admissible slab cut (every cell row pair holds a cut cell)")
+        c = int(cand[np.argmin(np.abs(cand - want))])
+        cuts.append(c)
+    cuts.append(n_e)
+    if any(b <= a for a, b in zip(cuts[:-1], cuts[1:])):
+        raise ValueError(f"cannot cut {n_e} cell rows into {world} admissible slabs")
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+class _SlabBlockK:
+    """Stiffness blocks of a slab's DOFs from the global problem (ImexPlan's
+    K_cc source when the global CSR does not fit host memory)."""
+
+    def __init__(self, prob, gdofs):
+        self.prob, self.gdofs = prob, gdofs
+
+    def stiffness_block(self, idx):
+        return self.prob.stiffness_block(self.gdofs[np.asarray(idx, dtype=np.int64)])
+
+
+class SlabElastic:
+    """Slab [lo, hi) of an ElasticProblem: local DOFs (component major), mass,
+    load, observers, c/d sets and the slab operator."""
+
+    def __init__(self, prob, lo: int, hi: int, M=None):
+        g = prob.grid
+        self.prob, self.lo, self.hi = prob, int(lo), int(hi)
+        p, n_e = g.p, g.n_e
+        n1 = n_e * p + 1
+        self.last = self.hi == n_e
+        lex = g.dofmap.lex_of_compact
+        row_end = self.hi * p + (1 if self.last else 0)
+        self.d_lo = int(np.searchsorted(lex, self.lo * p * n1))
+        self.d_hi = int(np.searchsorted(lex, row_end * n1))
+        nn = prob.n_node
+        nodes = np.arange(self.d_lo, self.d_hi, dtype=np.int64)
+        self.gdofs = np.concatenate([nodes, nodes + nn])         # local dof -> global dof
+        self.n_node_local = nodes.shape[0]
+        first = self.lo - 1 if self.lo > 0 else 0
+        self.cell_class = np.ascontiguousarray(g.classes.reshape(n_e, n_e)[first:self.hi].ravel(),
+                                               dtype=np.int8)
+        cut = np.asarray(g.cut_lex, dtype=np.int64)
+        crow = cut // n_e
+        sel = np.flatnonzero((crow >= self.lo - 1) & (crow < self.hi))
+        self.cut_cells = np.ascontiguousarray(cut[sel])
+        self.cut_K = np.ascontiguousarray(prob.cut_K[sel])
+        self.lex = np.ascontiguousarray(lex[self.d_lo:self.d_hi])
+        M = prob.mass_matrix() if M is None else M
+        self.M = sp.csr_matrix(M)[self.gdofs][:, self.gdofs]
+        self.F = np.ascontiguousarray(prob.F_s[self.gdofs])
+        self.obs = (sp.csr_matrix(prob.obs_mat)[:, self.gdofs] if prob.obs_mat is not None else None)
+        loc = np.full(prob.n_dof, -1, dtype=np.int64)
+        loc[self.gdofs] = np.arange(self.gdofs.shape[0])
+        c = loc[prob.c_idx]
+        self.c_idx = np.sort(c[c >= 0])
+        d = loc[prob.d_idx]
+        self.d_idx = np.sort(d[d >= 0])
+
+    @property
+    def n(self) -> int:
+        return self.gdofs.shape[0]
+
+    def device_operator(self, device=None):
+        from .operators import ElasticOperator
+        g, pr = self.prob.grid, self.prob
+        op = ElasticOperator(p=g.p, n_e=g.n_e, lam=pr.lam, mu=pr.mu, m1=pr.m1, k1=pr.k1, g1=pr.g1,
+                             cell_class=self.cell_class, lex_of_compact=self.lex,
+                             cut_cells=self.cut_cells, cut_K=self.cut_K, device=device,
+                             slab=(self.lo, self.hi, self.last))
+        op.problem = _SlabBlockK(self.prob, self.gdofs)
+        return op
+
+    def plan(self, dt: float, beta: float = 0.25, device=None):
+        from .imex import ImexPlan
+        return ImexPlan(self.M, self.device_operator(device=device), self.F, dt, self.c_idx, self.d_idx,
+                        obs_mat=self.obs, beta=beta, device=device)
+
+
+def _imex_tables(f_t, dt: float, n_t: int):
+    f0 = float(f_t(0.0))
+    ft_k = np.array([float(f_t(k * dt)) for k in range(n_t)] or [0.0])
+    ft_new = np.array([float(f_t(k * dt + dt)) for k in range(n_t)] or [0.0])
+    return f0, ft_k, ft_new
+
+
+def group_imex_run(prob, f_t, dt: float, n_t: int, world: int, beta: float = 0.25,
+                   gamma: float = 0.5, device=None) -> RunResult:
+    """imex_run over `world` slabs emulated in one process on one GPU (halo
+    exchange by device copies); returns the global field and observers."""
+    parts = partition_imex(prob, world)
+    M = prob.mass_matrix()
+    slabs = [SlabElastic(prob, lo, hi, M=M) for lo, hi in parts]
+    plans = [s.plan(dt, beta=beta, device=device) for s in slabs]
+    n_t = int(n_t)
+    f0, ft_k, ft_new = _imex_tables(f_t, float(dt), n_t)
+    outs = [np.empty(max(s.n, 1)) for s in slabs]
+    n_obs = plans[0].n_obs
+    obs_parts = [np.zeros((n_obs, n_t + 1)) for _ in slabs] if n_obs else None
+    lib = _lib.load()
+    parr = (_lib.C.c_void_p * world)(*[pl._h.value for pl in plans])
+    oarr = (_lib.C.POINTER(_lib.C.c_double) * world)(*[_lib.dptr(o) for o in outs])
+    barr = ((_lib.C.POINTER(_lib.C.c_double) * world)(*[_lib.dptr(o) for o in obs_parts])
+            if obs_parts else None)
+    div = _lib.Divergence()
+    tm = _lib.Timings()
+    code = lib.wcb_imex_group_run(world, parr, f0, _lib.dptr(ft_k), _lib.dptr(ft_new), float(dt), n_t,
+                                  float(beta), float(gamma), oarr, None, barr,
+                                  _lib.C.byref(div), _lib.C.byref(tm))
+    if code == _lib.WCB_E_DIVERGED:
+        raise DivergenceError(int(div.step), float(div.amplitude))
+    _lib.check(code)
+    psi = np.zeros(prob.n_dof)
+    for s, o in zip(slabs, outs):
+        psi[s.gdofs] = o[:s.n]
+    obs = sum(obs_parts) if obs_parts else None
+    return RunResult(method="imex", dt=float(dt), t=np.arange(n_t + 1) * float(dt), obs=obs,
+                     psi=psi, psi_dot=None,
+                     timings=StageTimings(factorization=sum(p.factorization for p in plans), rhs=float(tm.rhs)),
+                     fact_dim=0)
+
+
+def dist_imex_plan(prob, dt: float, beta: float = 0.25, device=None):
+    """One slab per torchrun rank (NCCL halos on the library context): this
+    rank's SlabElastic and ImexPlan; ImexPlan.run then exchanges halos and
+    all-reduces the divergence amplitude and observer partials."""
+    import torch.distributed as tdist
+    rank, world = tdist.get_rank(), tdist.get_world_size()
+    ctx = _lib.context(device)
+    if not getattr(ctx, "_nccl", False):
+        init_nccl(ctx, rank, world)
+        ctx._nccl = True
+    lo, hi = partition_imex(prob, world)[rank]
+    slab = SlabElastic(prob, lo, hi)
+    return slab, slab.plan(dt, beta=beta, device=device)

@@ -156,7 +156,7 @@ class ElasticOperator(DeviceOperator):
     kind = "elastic"
 
     def __init__(self, p: int, n_e: int, lam: float, mu: float, m1, k1, g1, cell_class,
-                 lex_of_compact, cut_cells, cut_K, device: int | None = None):
+                 lex_of_compact, cut_cells, cut_K, device: int | None = None, slab=None):
         p = int(p)
         n_e = int(n_e)
         N = p + 1
@@ -165,7 +165,7 @@ class ElasticOperator(DeviceOperator):
         self._k1 = np.ascontiguousarray(k1, dtype=np.float64).reshape(N, N)
         self._g1 = np.ascontiguousarray(g1, dtype=np.float64).reshape(N, N)
         self._cls = np.ascontiguousarray(cell_class, dtype=np.int8).reshape(-1)
-        if self._cls.shape[0] != n_e * n_e:
+        if slab is None and self._cls.shape[0] != n_e * n_e:
             raise ValueError("cell_class must hold n_e^2 entries")
         self._lex = np.ascontiguousarray(lex_of_compact, dtype=np.int64)
         self._cut = np.ascontiguousarray(cut_cells, dtype=np.int64).reshape(-1)
@@ -183,6 +183,9 @@ class ElasticOperator(DeviceOperator):
         desc.n_cut = self._cut.shape[0]
         desc.cut_cells = _lib.i64ptr(self._cut) if self._cut.size else None
         desc.cut_K = _lib.dptr(self._cutK) if self._cutK.size else None
+        if slab is not None:
+            lo, hi, last = slab
+            desc.x_cell_lo, desc.x_cell_hi, desc.x_owns_last = int(lo), int(hi), 1 if last else 0
         ctx = _lib.context(device)
         h = _lib.C.c_void_p()
         _lib.check(_lib.load().wcb_operator_elastic_create(ctx.handle, _lib.C.byref(desc),

@@ -114,3 +114,25 @@ def test_slab_halo_exchange_reproduces_serial_cdm(kind, world):
     ref, _, _ = O.cdm_run(sp.diags(prob.m_diag).tocsr(), K, prob.F_s,
                           lambda t: ricker(t, 10.0), 2e-5, n_t)
     assert np.array_equal(psi, ref)
+
+
+def test_imex_slab_host_sets():
+    """Slab c/d sets and DOF maps of the plane-strain IMEX partition (host only)."""
+    from paper_2501_19013_b200.dist import SlabElastic, partition_imex
+    from paper_2501_19013_b200.setup.elastic import ElasticProblem, lame
+    from paper_2501_19013_b200.setup.geometry import BallVoids
+    from paper_2501_19013_b200.setup.grid import Grid
+    lam, mu = lame(1.0, 0.3)
+    geom = BallVoids(2, [[0.22, 0.5], [0.7, 0.3]], [0.08, 0.09])
+    prob = ElasticProblem.build(Grid.build(geom, "lagrange", 2, 20), lam, mu, 1e-4, 2)
+    prob.set_point_source([0.1, 0.9])
+    parts = partition_imex(prob, 3)
+    assert parts[0][0] == 0 and parts[-1][1] == 20
+    slabs = [SlabElastic(prob, lo, hi) for lo, hi in parts]
+    g = np.concatenate([s.gdofs for s in slabs])
+    assert np.array_equal(np.sort(g), np.arange(prob.n_dof))
+    c_all = np.sort(np.concatenate([s.gdofs[s.c_idx] for s in slabs]))
+    assert np.array_equal(c_all, np.sort(prob.c_idx))
+    for s in slabs:
+        assert s.c_idx.shape[0] + s.d_idx.shape[0] == s.n
+        assert s.M[s.d_idx][:, s.c_idx].nnz == 0
