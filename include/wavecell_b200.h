@@ -189,6 +189,15 @@ int wcb_max_gen_eig_sub(wcb_operator* op, const double* m_diag, int64_t n_sub,
                         const int64_t* sub_idx, const double* x0_sub, double tol,
                         int64_t max_iter, double* out_lambda, int64_t* out_iters);
 
+/* Host-side check of factorize()'s diagonal fast path (src/linalg.py:63-69)
+ * for a CSR mass matrix, multi-threaded: returns 1 when the pattern is exactly
+ * the diagonal in order and every stored value is positive and finite, 0 when
+ * the pattern is the diagonal but a value is not positive/finite, -1 when the
+ * pattern is not the identity (the caller falls back to a general check).
+ * index_bytes = 4 or 8 for indptr / indices. */
+int wcb_csr_diagonal_check(int64_t n, const void* indptr, const void* indices, int index_bytes,
+                           const double* data);
+
 /* ---- central difference method: cdm_run, src/timeint.py:159-193 ---------- */
 /* Diagonal M only (the factorize() fast path, src/linalg.py:63-69).  F_s may be
  * sparse: only its nonzeros are kept on the device. */

@@ -35,6 +35,7 @@ EXPORTS = (
     "wcb_cdm_plan_run", "wcb_cdm_plan_run_device", "wcb_imex_plan_create",
     "wcb_imex_plan_destroy", "wcb_imex_plan_run", "wcb_dist_unique_id", "wcb_dist_init",
     "wcb_dist_finalize", "wcb_cdm_group_run", "wcb_cdm_plan_step_bytes", "wcb_imex_group_run",
+    "wcb_csr_diagonal_check",
 )
 
 _p = C.c_void_p
@@ -100,6 +101,7 @@ _SIGS = {
     "wcb_max_gen_eig_sub": (C.c_int, [_p, _dp, _i64, _i64p, _dp, _d, _i64, _dp, _i64p]),
     "wcb_cdm_plan_create": (C.c_int, [_p, _dp, _dp, C.POINTER(Observer), C.POINTER(_p)]),
     "wcb_cdm_plan_destroy": (C.c_int, [_p]),
+    "wcb_csr_diagonal_check": (C.c_int, [_i64, _p, _p, C.c_int, _dp]),
     "wcb_cdm_plan_step_bytes": (C.c_int, [_p, _dp]),
     "wcb_cdm_plan_run": (C.c_int, [_p, _dp, _d, _i64, _dp, _dp, _dp, _dp,
                                    C.POINTER(Divergence), C.POINTER(Timings)]),

@@ -2,6 +2,9 @@
 // (src/timeint.py:159-193) and the power iteration (src/linalg.py:89-130).
 #include "wcb_internal.cuh"
 
+#include <atomic>
+#include <thread>
+
 #include <mutex>
 
 #include <algorithm>
@@ -10,6 +13,22 @@
 #include <memory>
 
 namespace wcb {
+
+// Host loop split over up to 16 threads in chunks of >= 256k iterations.
+template <class F>
+static void host_par_for(int64_t n, F&& f) {
+    const int64_t min_chunk = 1 << 18;
+    int nt = (int)std::min<int64_t>(std::max<int64_t>(1, n / min_chunk),
+                                    std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    if (nt <= 1) { f(0, n); return; }
+    std::vector<std::thread> th;
+    const int64_t chunk = (n + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t) {
+        const int64_t a = t * chunk, b = std::min<int64_t>(n, a + chunk);
+        if (a < b) th.emplace_back([&f, a, b] { f(a, b); });
+    }
+    for (auto& x : th) x.join();
+}
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -74,6 +93,16 @@ __global__ void k_mass_state(int64_t n, const int64_t* __restrict__ map,
         int64_t s = map[i];
         m_state[s] = m[i];
         minv[s] = 1.0 / m[i];
+    }
+}
+// in: minv holds m at DOF slots and 0 elsewhere; out: m_state = m (1 at
+// non-DOF slots), minv = 1/m (0 at non-DOF slots)
+__global__ void k_mass_from_state(int64_t ns, double* __restrict__ minv, double* __restrict__ m_state) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double m = minv[i];
+        m_state[i] = m != 0.0 ? m : 1.0;
+        minv[i] = m != 0.0 ? 1.0 / m : 0.0;
     }
 }
 __global__ void k_fill(int64_t n, double v, double* __restrict__ x) {
@@ -681,6 +710,31 @@ static void run_cdm_device(wcb_cdm_plan* P, const double* d_ft, double dt, int64
 
 extern "C" {
 
+int wcb_csr_diagonal_check(int64_t n, const void* indptr, const void* indices, int index_bytes,
+                           const double* data) {
+    if (n < 0 || !indptr || !indices || !data || (index_bytes != 4 && index_bytes != 8)) return -1;
+    std::atomic<int> pattern_ok{1}, values_ok{1};
+    host_par_for(n, [&](int64_t a, int64_t b) {
+        bool pat = true, val = true;
+        if (index_bytes == 4) {
+            const int32_t* ip = static_cast<const int32_t*>(indptr);
+            const int32_t* ix = static_cast<const int32_t*>(indices);
+            for (int64_t i = a; i < b && pat; ++i) pat = ip[i] == i && ix[i] == i;
+            if (b == n) pat = pat && ip[n] == n;
+        } else {
+            const int64_t* ip = static_cast<const int64_t*>(indptr);
+            const int64_t* ix = static_cast<const int64_t*>(indices);
+            for (int64_t i = a; i < b && pat; ++i) pat = ip[i] == i && ix[i] == i;
+            if (b == n) pat = pat && ip[n] == n;
+        }
+        for (int64_t i = a; i < b && val; ++i) val = data[i] > 0.0 && std::isfinite(data[i]);
+        if (!pat) pattern_ok = 0;
+        if (!val) values_ok = 0;
+    });
+    if (!pattern_ok) return -1;
+    return values_ok ? 1 : 0;
+}
+
 int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s,
                         const wcb_observer* obs, wcb_cdm_plan** out) {
     return guarded([&] {
@@ -690,33 +744,43 @@ int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s
         WCB_CUDA(cudaSetDevice(ctx->device));
         cudaStream_t s = ctx->stream;
         const int64_t n = op->n, ns = op->n_state;
-        for (int64_t i = 0; i < n; ++i)
-            WCB_REQUIRE(m_diag[i] > 0.0 && std::isfinite(m_diag[i]),
-                        "diagonal mass has non-positive entries");
+        std::atomic<int> m_ok{1};
+        host_par_for(n, [&](int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; ++i)
+                if (!(m_diag[i] > 0.0 && std::isfinite(m_diag[i]))) { m_ok = 0; return; }
+        });
+        WCB_REQUIRE(m_ok, "diagonal mass has non-positive entries");
         std::unique_ptr<wcb_cdm_plan> P(new wcb_cdm_plan());
         P->op = op;
         P->ctx = ctx;
         const std::vector<int64_t>& si = op->state_index();
-        DevBuf<int64_t> map;
-        map.alloc(n, s);
-        map.upload(si.data(), n, s);
+        // m into the state layout through the operator's own device map
+        // (scatter), then m_state = m / 1 and minv = 1/m / 0 at DOF / other slots
         DevBuf<double> dm;
         dm.alloc(n, s);
         dm.upload(m_diag, n, s);
         P->m_state.alloc(ns, s);
         P->minv.alloc(ns, s);
-        k_fill<<<grid_for(ctx, ns), 256, 0, s>>>(ns, 1.0, P->m_state.p);
         P->minv.zero(s);
-        if (n) k_mass_state<<<grid_for(ctx, n), 256, 0, s>>>(n, map.p, dm.p, P->m_state.p, P->minv.p);
+        if (n) op->scatter(dm.p, P->minv.p);
+        k_mass_from_state<<<grid_for(ctx, ns), 256, 0, s>>>(ns, P->minv.p, P->m_state.p);
         ctx->launches += 2;
         WCB_CHECK_LAUNCH();
         op->bind_minv(P->minv.p);
         // source: dense window over its nonzeros' state-index range
         {
+            std::mutex mu;
             std::vector<std::pair<int64_t, double>> nz;
-            for (int64_t i = 0; i < n; ++i)
-                if (F_s[i] != 0.0) nz.emplace_back(si[i], F_s[i]);
-            P->src = make_source(std::move(nz), P->F_win, s);
+            host_par_for(n, [&](int64_t a, int64_t b) {
+                std::vector<std::pair<int64_t, double>> loc;
+                for (int64_t i = a; i < b; ++i)
+                    if (F_s[i] != 0.0) loc.emplace_back(si[i], F_s[i]);
+                if (!loc.empty()) {
+                    std::lock_guard<std::mutex> g(mu);
+                    nz.insert(nz.end(), loc.begin(), loc.end());
+                }
+            });
+            P->src = make_source(std::move(nz), P->F_win, s);   // sorts by state index
         }
         if (obs && obs->n_obs > 0) {
             P->n_obs = obs->n_obs;

@@ -41,11 +41,38 @@ def _csr_identity_pattern(M) -> bool:
     return bool(np.array_equal(M.indptr, ar) and np.array_equal(M.indices, ar[:n]))
 
 
+def _native_diag(M):
+    """Threaded native check of a CSR diagonal (wcb_csr_diagonal_check): the
+    diagonal, or None when the pattern is not the identity; raises like
+    factorize when a value is not positive/finite."""
+    if not (sp.issparse(M) and M.format == "csr" and M.shape[0] == M.shape[1] and M.nnz == M.shape[0]):
+        return None
+    ip, ix = M.indptr, M.indices
+    if ip.dtype != ix.dtype or ip.dtype not in (np.int32, np.int64) or M.data.dtype != np.float64:
+        return None
+    from . import _lib
+    try:
+        lib = _lib.load()
+    except ImportError:
+        return None
+    d = np.ascontiguousarray(M.data)
+    r = lib.wcb_csr_diagonal_check(M.shape[0], ip.ctypes.data, ix.ctypes.data, ip.dtype.itemsize,
+                                   _lib.dptr(d))
+    if r < 0:
+        return None
+    if r == 0:
+        raise IndefiniteMatrixError("diagonal matrix has non-positive entries; "
+                                    "check the stabilization and lumping settings")
+    return d
+
+
 def diagonal_mass(M) -> np.ndarray:
     """The diagonal of a structurally diagonal SPD mass, with the checks of
     ``factorize``'s fast path (src/linalg.py:63-69)."""
     if isinstance(M, np.ndarray) and M.ndim == 1:
         d = np.ascontiguousarray(M, dtype=np.float64)
+    elif (d := _native_diag(M)) is not None:
+        return d
     elif _csr_identity_pattern(M):
         d = np.ascontiguousarray(M.data, dtype=np.float64)
     else:

@@ -17,7 +17,7 @@ prob = build_scm(CONFIGS[name])
 op = prob.device_operator()
 M = prob.mass_matrix()
 F = prob.F_s
-obs = prob.observer_matrix() if hasattr(prob, "observer_matrix") else None
+obs = prob.obs_mat
 dt = 1e-7
 f = lambda t: ricker(t, 10.0)
 torch.cuda.synchronize()
