@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <numeric>
+#include <cstring>
 
 namespace wcb {
 
@@ -70,16 +71,24 @@ __global__ void __launch_bounds__(BLOCK) k_csr_cdm(int64_t n, const int64_t* __r
 }
 
 // SELL-32: slices of 32 consecutive rows stored column-major (entry k of row
-// r in slice s at sptr[s] + 32 k + r), one row per thread: every load of a
-// warp is one contiguous 256 B (values) / 128 B (indices) segment.  Padding
-// entries point at the row itself with value 0.  Row sums run in stored
-// order (the CSR order), so results equal the CSR-vector kernel's up to
-// summation order and are bitwise reproducible.
+// r in slice s at e_ptr[s] + 32 k + r), one row per thread (one slice per
+// warp).  A slice whose 32 rows have the same width and the same column
+// offsets relative to their row (translation-invariant stencil rows: the
+// B-spline interior) keeps one offset vector (type 1); if the values are also
+// bitwise the same across the 32 rows it keeps one value vector too (type 2:
+// no per-entry bytes at all, x is read at row + offset -- coalesced).  Other
+// slices store every index and value (type 0; padding entries point at the
+// row with value 0).  Row sums run in stored (CSR) order in every type, so
+// results are bitwise those of the plain SELL layout.
 template <bool STEP>
-__global__ void __launch_bounds__(256) k_sell(int64_t n, const int64_t* __restrict__ sptr,
+__global__ void __launch_bounds__(256) k_sell(int64_t n, const uint8_t* __restrict__ stype,
                                               const int32_t* __restrict__ swid,
-                                              const int32_t* __restrict__ sidx,
-                                              const double* __restrict__ sval,
+                                              const int64_t* __restrict__ e_ptr,
+                                              const int32_t* __restrict__ e_idx,
+                                              const double* __restrict__ e_val,
+                                              const int64_t* __restrict__ p_ptr,
+                                              const int32_t* __restrict__ p_off,
+                                              const double* __restrict__ p_val,
                                               const double* __restrict__ x, double* __restrict__ y,
                                               StepArgs a) {
     if (STEP && blockIdx.x == 0) record_observers(a);
@@ -96,11 +105,25 @@ __global__ void __launch_bounds__(256) k_sell(int64_t n, const int64_t* __restri
     double acc = 0.0;
     if (valid) {
         const int w = __ldg(swid + s);
-        const int64_t base = __ldg(sptr + s) + r;
-        #pragma unroll 8
-        for (int k = 0; k < w; ++k) {
-            const int64_t j = base + 32 * (int64_t)k;
-            acc = fma(__ldg(sval + j), __ldg(x + __ldg(sidx + j)), acc);
+        const int t = __ldg(stype + s);
+        if (t == 2) {
+            const int64_t pb = __ldg(p_ptr + s);
+            #pragma unroll 8
+            for (int k = 0; k < w; ++k)
+                acc = fma(__ldg(p_val + pb + k), __ldg(x + row + __ldg(p_off + pb + k)), acc);
+        } else if (t == 1) {
+            const int64_t pb = __ldg(p_ptr + s);
+            const int64_t eb = __ldg(e_ptr + s) + r;
+            #pragma unroll 8
+            for (int k = 0; k < w; ++k)
+                acc = fma(__ldg(e_val + eb + 32 * (int64_t)k), __ldg(x + row + __ldg(p_off + pb + k)), acc);
+        } else {
+            const int64_t eb = __ldg(e_ptr + s) + r;
+            #pragma unroll 8
+            for (int k = 0; k < w; ++k) {
+                const int64_t j = eb + 32 * (int64_t)k;
+                acc = fma(__ldg(e_val + j), __ldg(x + __ldg(e_idx + j)), acc);
+            }
         }
     }
     if constexpr (STEP) {
@@ -126,9 +149,12 @@ struct CsrOperator final : Operator {
     int64_t nnz = 0;
     int tpr = 8;
     bool sell = false;
-    DevBuf<int64_t> s_ptr;
-    DevBuf<int32_t> s_wid, s_idx;
-    DevBuf<double> s_val;
+    DevBuf<uint8_t> s_type;
+    DevBuf<int32_t> s_wid;
+    DevBuf<int64_t> e_ptr, p_ptr;
+    DevBuf<int32_t> e_idx, p_off;
+    DevBuf<double> e_val, p_val;
+    double sell_bytes = 0.0;   // matrix bytes per apply in the SELL layout
 
     const char* name() const override { return "csr"; }
     const std::vector<int64_t>& state_index() const override { return sidx; }
@@ -159,8 +185,8 @@ struct CsrOperator final : Operator {
         if (!n) return;
         if (sell) {
             StepArgs a;
-            k_sell<false><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(n, s_ptr.p, s_wid.p, s_idx.p,
-                                                                               s_val.p, x, y, a);
+            k_sell<false><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(
+                n, s_type.p, s_wid.p, e_ptr.p, e_idx.p, e_val.p, p_ptr.p, p_off.p, p_val.p, x, y, a);
             ctx->launches++;
             WCB_CHECK_LAUNCH();
             return;
@@ -178,8 +204,8 @@ struct CsrOperator final : Operator {
     void cdm_step(const StepArgs& a) override {
         if (!n) return;
         if (sell) {
-            k_sell<true><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(n, s_ptr.p, s_wid.p, s_idx.p,
-                                                                              s_val.p, a.cur, nullptr, a);
+            k_sell<true><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(
+                n, s_type.p, s_wid.p, e_ptr.p, e_idx.p, e_val.p, p_ptr.p, p_off.p, p_val.p, a.cur, nullptr, a);
             ctx->launches++;
             WCB_CHECK_LAUNCH();
             return;
@@ -195,8 +221,11 @@ struct CsrOperator final : Operator {
         WCB_CHECK_LAUNCH();
     }
     // 12 B/nnz (fp64 value + int32 index) + 8 B indptr (int64 here)
-    // + psi_k, psi_{k-1} read, psi_{k+1} write, 1/m read.
-    double step_bytes() const override { return 12.0 * nnz + 8.0 * (n + 1) + 32.0 * n; }
+    // + psi_k, psi_{k-1} read, psi_{k+1} write, 1/m read.  In the SELL layout
+    // the matrix bytes are those of the stored slices (shared stencils once).
+    double step_bytes() const override {
+        return (sell ? sell_bytes : 12.0 * nnz + 8.0 * (n + 1)) + 32.0 * n;
+    }
 };
 
 Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* h_indptr,
@@ -241,26 +270,71 @@ Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* h_indptr,
         sw[sl] = (int32_t)w;
         sp[sl + 1] = sp[sl] + 32 * w;
     }
-    if (n >= 32 && sp[n_sl] <= nnz + nnz / 4 && nnz > 0) {
-        std::vector<int32_t> si(sp[n_sl]);
-        std::vector<double> sv(sp[n_sl], 0.0);
-        for (int64_t sl = 0; sl < n_sl; ++sl)
-            for (int64_t r = sl * 32; r < sl * 32 + 32; ++r)
-                for (int64_t k = 0; k < sw[sl]; ++k) {
-                    const int64_t dst = sp[sl] + 32 * k + (r - sl * 32);
-                    const int64_t src = r < n ? h_indptr[r] + k : -1;
-                    if (r < n && src < h_indptr[r + 1]) {
-                        si[dst] = h_indices[src];
-                        sv[dst] = h_data[src];
-                    } else {
-                        si[dst] = (int32_t)std::min<int64_t>(r, n - 1);
-                        sv[dst] = 0.0;
+    if (n >= 32 && sp[n_sl] <= nnz + nnz / 4 && nnz > 0 && !getenv("WAVECELL_B200_NO_SELL")) {
+        const bool share = !getenv("WAVECELL_B200_NO_SHARED_STENCIL");
+        std::vector<uint8_t> st(n_sl, 0);
+        std::vector<int64_t> ep(n_sl, 0), pp(n_sl, 0);
+        std::vector<int32_t> ei, po;
+        std::vector<double> ev, pv;
+        for (int64_t sl = 0; sl < n_sl; ++sl) {
+            const int64_t r0 = sl * 32, w = sw[sl];
+            int type = 0;
+            if (share && r0 + 32 <= n && w > 0) {
+                bool same_idx = true, same_val = true;
+                for (int64_t r = r0; r < r0 + 32 && same_idx; ++r) {
+                    if (h_indptr[r + 1] - h_indptr[r] != w) { same_idx = false; break; }
+                    for (int64_t k = 0; k < w; ++k) {
+                        const int64_t jr = h_indptr[r] + k, j0 = h_indptr[r0] + k;
+                        if ((int64_t)h_indices[jr] - r != (int64_t)h_indices[j0] - r0) { same_idx = false; break; }
+                        if (std::memcmp(&h_data[jr], &h_data[j0], sizeof(double)) != 0) same_val = false;
                     }
                 }
-        op->s_ptr.alloc(sp.size()); op->s_ptr.upload(sp.data(), sp.size(), s);
+                type = same_idx ? (same_val ? 2 : 1) : 0;
+            }
+            st[sl] = (uint8_t)type;
+            if (type >= 1) {
+                pp[sl] = (int64_t)po.size();
+                for (int64_t k = 0; k < w; ++k) {
+                    po.push_back((int32_t)((int64_t)h_indices[h_indptr[r0] + k] - r0));
+                    if (type == 2) pv.push_back(h_data[h_indptr[r0] + k]);
+                    else pv.push_back(0.0);
+                }
+            }
+            if (type <= 1) {
+                ep[sl] = (int64_t)ev.size();
+                const bool with_idx = type == 0;
+                if (with_idx && ei.size() < ev.size()) ei.resize(ev.size(), 0);
+                for (int64_t k = 0; k < w; ++k)
+                    for (int64_t r = r0; r < r0 + 32; ++r) {
+                        const int64_t src = r < n ? h_indptr[r] + k : -1;
+                        const bool real = r < n && src < h_indptr[r + 1];
+                        ev.push_back(real ? h_data[src] : 0.0);
+                        if (with_idx) ei.push_back(real ? h_indices[src] : (int32_t)std::min<int64_t>(r, n - 1));
+                    }
+                if (!with_idx) ei.resize(ev.size(), 0);   // keep e_idx aligned with e_val
+            }
+        }
+        // bytes one apply reads from the matrix: per-entry arrays of type 0/1
+        // slices + one pattern per type 1/2 slice + slice headers
+        double mb = 0.0;
+        for (int64_t sl = 0; sl < n_sl; ++sl) {
+            const double w = sw[sl];
+            mb += st[sl] == 0 ? 32.0 * w * 12.0 : st[sl] == 1 ? 32.0 * w * 8.0 + w * 4.0 : w * 12.0;
+            mb += 1.0 + 4.0 + 16.0;
+        }
+        op->sell_bytes = mb;
+        if (ei.empty()) ei.push_back(0);
+        if (ev.empty()) ev.push_back(0.0);
+        if (po.empty()) po.push_back(0);
+        if (pv.empty()) pv.push_back(0.0);
+        op->s_type.alloc(st.size()); op->s_type.upload(st.data(), st.size(), s);
         op->s_wid.alloc(sw.size()); op->s_wid.upload(sw.data(), sw.size(), s);
-        op->s_idx.alloc(si.size()); op->s_idx.upload(si.data(), si.size(), s);
-        op->s_val.alloc(sv.size()); op->s_val.upload(sv.data(), sv.size(), s);
+        op->e_ptr.alloc(ep.size()); op->e_ptr.upload(ep.data(), ep.size(), s);
+        op->p_ptr.alloc(pp.size()); op->p_ptr.upload(pp.data(), pp.size(), s);
+        op->e_idx.alloc(ei.size()); op->e_idx.upload(ei.data(), ei.size(), s);
+        op->e_val.alloc(ev.size()); op->e_val.upload(ev.data(), ev.size(), s);
+        op->p_off.alloc(po.size()); op->p_off.upload(po.data(), po.size(), s);
+        op->p_val.alloc(pv.size()); op->p_val.upload(pv.data(), pv.size(), s);
         op->sell = true;
     }
     WCB_CUDA(cudaStreamSynchronize(s));

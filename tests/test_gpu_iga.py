@@ -44,3 +44,24 @@ def test_config3_reduced_cdm_parity():
     r = cdm_run(M, op, prob.F_s, f, dt, 400, obs_mat=prob.obs_mat)
     assert rel(r.psi, psi_ref) <= 1e-10
     assert rel(r.obs, obs_ref) <= 1e-10
+
+
+def test_shared_stencil_slices_bitwise(monkeypatch):
+    """SELL slices with translation-invariant rows keep one offset/value
+    vector; the field equals the plain SELL layout's bitwise (same stored
+    order of every row sum)."""
+    from paper_2501_19013_b200.operators import CsrOperator
+    prob = build_config3(n_e=96)
+    M = prob.mass_matrix()
+    f = lambda t: ricker(t, 10.0)  # noqa: E731
+    x = np.random.default_rng(3).standard_normal(prob.n_dof)
+    outs = []
+    for flag in ("1", None):
+        if flag:
+            monkeypatch.setenv("WAVECELL_B200_NO_SHARED_STENCIL", flag)
+        else:
+            monkeypatch.delenv("WAVECELL_B200_NO_SHARED_STENCIL", raising=False)
+        op = CsrOperator(prob.K)
+        outs.append((op @ x, cdm_run(M, op, prob.F_s, f, 1e-4, 200).psi))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
