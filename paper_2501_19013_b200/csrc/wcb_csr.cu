@@ -91,6 +91,10 @@ __global__ void __launch_bounds__(256) k_sell(int64_t n, const uint8_t* __restri
                                               const double* __restrict__ p_val,
                                               const double* __restrict__ x, double* __restrict__ y,
                                               StepArgs a) {
+    if (STEP) {
+        pdl_trigger();
+        pdl_wait();   // the previous step's psi is complete from here on
+    }
     if (STEP && blockIdx.x == 0) record_observers(a);
     const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid = row < n;
@@ -204,8 +208,20 @@ struct CsrOperator final : Operator {
     void cdm_step(const StepArgs& a) override {
         if (!n) return;
         if (sell) {
-            k_sell<true><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(
-                n, s_type.p, s_wid.p, e_ptr.p, e_idx.p, e_val.p, p_ptr.p, p_off.p, p_val.p, a.cur, nullptr, a);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)ceil_div(n, 256));
+            cfg.blockDim = dim3(256);
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = pdl_enabled() ? 1 : 0;
+            const double* none = nullptr;
+            WCB_CUDA(cudaLaunchKernelEx(&cfg, k_sell<true>, n, (const uint8_t*)s_type.p, (const int32_t*)s_wid.p,
+                                        (const int64_t*)e_ptr.p, (const int32_t*)e_idx.p, (const double*)e_val.p,
+                                        (const int64_t*)p_ptr.p, (const int32_t*)p_off.p, (const double*)p_val.p,
+                                        a.cur, (double*)none, a));
             ctx->launches++;
             WCB_CHECK_LAUNCH();
             return;

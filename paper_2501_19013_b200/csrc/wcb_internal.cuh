@@ -181,6 +181,19 @@ __device__ __forceinline__ void record_observers(const StepArgs& a) {
     }
 }
 
+// Programmatic dependent launch (time-step chains): a step kernel lets the
+// next one launch as soon as all its CTAs are resident, and waits for the
+// previous grid's completion (and memory) before touching any state.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("WAVECELL_B200_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // Reference arithmetic order of src/timeint.py:185:
 //   psi_new = 2.0*psi - psi_prev + (dt*dt) * (rhs / m)
 // with rhs = f*F - K psi; 1/m is precomputed (<= 1 ulp from the division).

@@ -285,11 +285,13 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
     unsigned long long t_0, t_1, t_2, t_3, t_4;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_0));
 #endif
+    if (MODE == MODE_STEP) pdl_trigger();
     const int32_t tid = __ldg(g.order + blockIdx.x);
     const int64_t strip = tid / g.n_rtiles, rtile = tid % g.n_rtiles;
-    if (MODE == MODE_STEP && blockIdx.x == 0) record_observers(a);
     const int64_t J0 = strip * T::TJ, I0 = g.row_lo + rtile * T::TI;
     const bool tcl = MODE == MODE_STEP && g.tclean && __ldg(g.tclean + tid) != 0;
+    if (MODE == MODE_STEP) pdl_wait();   // the previous step's psi is complete from here on
+    if (MODE == MODE_STEP && blockIdx.x == 0) record_observers(a);
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
@@ -535,7 +537,21 @@ struct ScmOperator final : Operator {
             g.tclean = tclean.p;
             for (int i = 0; i < P * P; ++i) tab.v[i] = minv_tab[i];
         }
-        k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(mu, mp, mm, g, mt, tab, sk, a);
+        if (MODE == MODE_STEP && pdl_enabled()) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = grid;
+            cfg.blockDim = dim3(T::NWARP * 32);
+            cfg.dynamicSmemBytes = T::SMEM;
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            WCB_CUDA(cudaLaunchKernelEx(&cfg, k_scm2d<P, MODE>, mu, mp, mm, g, mt, tab, sk, a));
+        } else {
+            k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(mu, mp, mm, g, mt, tab, sk, a);
+        }
         ctx->launches++;
     }
     template <int P>
