@@ -18,7 +18,13 @@
 #pragma once
 // (included inside namespace wcb by wcb_scm.cu)
 
-__host__ __device__ constexpr int rpe_e(int P) { return P <= 3 ? 3 : 2; }
+#ifndef WCB_ELA_RPE5
+#define WCB_ELA_RPE5 2
+#endif
+#ifndef WCB_ELA_MINB
+#define WCB_ELA_MINB 2
+#endif
+__host__ __device__ constexpr int rpe_e(int P) { return P <= 3 ? 3 : P == 5 ? WCB_ELA_RPE5 : 2; }
 
 template <int P>
 struct Tile2E {
@@ -306,7 +312,7 @@ __device__ __forceinline__ void ela2d_warp(const Scm2DGeo& g, const EMats<P>& mt
 // One CTA per tile (order[] = live tiles, most expensive first).  The state
 // tensor maps cover both component planes: plane 1 is `rows` TMA rows below.
 template <int P, int MODE>
-__global__ void __launch_bounds__(Tile2E<P>::NWARP * 32, 2) k_ela2d(
+__global__ void __launch_bounds__(Tile2E<P>::NWARP * 32, WCB_ELA_MINB) k_ela2d(
     const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_prev,
     const __grid_constant__ CUtensorMap tm_minv, Scm2DGeo g, const __grid_constant__ EMats<P> mt,
     int64_t plane, int32_t rows, const __grid_constant__ MinvTabE<P> mtab, StepArgs a) {

@@ -47,6 +47,7 @@ struct TriSched {
     int64_t max_lvl_rows = 0, max_lvl_ent = 0;   // widest level
     int slot_e = 0, slot_r = 0;                  // ring slot capacities (entries, rows)
     int depth = 3;                               // ring depth (levels in flight)
+    bool recip = false;                          // sdiag holds 1/diag
     DevBuf<int32_t> comp_order;  // launch order: components by decreasing level count
     DevBuf<int32_t> comp_rows;   // n_comp + 1: offsets into rows
     DevBuf<int32_t> comp_lvl;    // n_comp + 1: offsets into lvl_off
@@ -138,6 +139,11 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
     for (int64_t c = 0; c < n_comp; ++c)
         T.max_levels = std::max<int64_t>(T.max_levels, comp_lvl[c + 1] - comp_lvl[c]);
     lvl_off.push_back((int32_t)n);
+    // the level kernel multiplies by 1/diag (one correctly rounded reciprocal
+    // per row, host-side) instead of dividing on the critical path of every
+    // level; WAVECELL_B200_TRSV_DIV=1 restores the division
+    const bool recip = !(getenv("WAVECELL_B200_TRSV_DIV") && getenv("WAVECELL_B200_TRSV_DIV")[0] == '1');
+    T.recip = recip;
     std::vector<int32_t> sptr(n + 1, 0), slcol;
     std::vector<double> sval, sdiag(n, 0.0);
     slcol.reserve(ptr[n]);
@@ -147,7 +153,7 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
         sptr[k2] = (int32_t)slcol.size();
         for (int64_t j = ptr[i]; j < ptr[i + 1]; ++j) {
             if (idx[j] == i) {
-                sdiag[k2] = val[j];
+                sdiag[k2] = recip ? 1.0 / val[j] : val[j];
             } else {
                 slcol.push_back(pos[idx[j]]);
                 sval.push_back(val[j]);
@@ -311,7 +317,7 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
     const int32_t* __restrict__ lvl_off, const int32_t* __restrict__ lvl_ent, const int32_t* __restrict__ rows,
     const int32_t* __restrict__ sptr, const int32_t* __restrict__ slcol,
     const double* __restrict__ sval, const double* __restrict__ sdiag, const double* __restrict__ b,
-    double* __restrict__ x, int max_size, int max_levels, int slot_e, int slot_r) {
+    double* __restrict__ x, int max_size, int max_levels, int slot_e, int slot_r, int recip) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const size_t sb = trsv_slot_bytes(slot_e, slot_r);
     double* xl = reinterpret_cast<double*>(smraw + sb * TRSV_D);
@@ -371,7 +377,7 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
                 for (int j = p0 + lane; j < p1; j += 32) sacc = fma(V[j], xl[C[j]], sacc);
                 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
-                if (lane == 0) xl[a + k - r0] = (xl[a + k - r0] - sacc) / D[k];
+                if (lane == 0) xl[a + k - r0] = recip ? (xl[a + k - r0] - sacc) * D[k] : (xl[a + k - r0] - sacc) / D[k];
             }
         } else {
             for (int k = a + warp; k < e; k += nw) {
@@ -379,7 +385,7 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
                 for (int j = sptr[k] + lane; j < sptr[k + 1]; j += 32) sacc = fma(sval[j], xl[slcol[j]], sacc);
                 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
-                if (lane == 0) xl[k - r0] = (xl[k - r0] - sacc) / sdiag[k];
+                if (lane == 0) xl[k - r0] = recip ? (xl[k - r0] - sacc) * sdiag[k] : (xl[k - r0] - sacc) / sdiag[k];
             }
         }
     }
@@ -460,7 +466,7 @@ __global__ void __launch_bounds__(TRSF_THREADS, 2) k_trsv_sf(
         #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
         if (lane == 0) {
-            const double v = (bcur - acc) / dcur;
+            const double v = (bcur - acc) / dcur;   // (unlaunched variant: expects sdiag = diag)
             asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32_imex(xs + (k - r0))), "d"(v) : "memory");
         }
     }
@@ -490,7 +496,7 @@ static void launch_trsv_d(Context* ctx, const TriSched& T, const double* b, doub
     }();
     k_trsv_comp<D><<<(unsigned)T.n_comp, threads, sm, ctx->stream>>>(
         T.comp_order.p, T.comp_rows.p, T.comp_lvl.p, T.lvl_off.p, T.lvl_ent.p, T.rows.p, T.sptr.p, T.slcol.p,
-        T.sval.p, T.sdiag.p, b, x, (int)T.max_size, (int)T.max_levels, T.slot_e, T.slot_r);
+        T.sval.p, T.sdiag.p, b, x, (int)T.max_size, (int)T.max_levels, T.slot_e, T.slot_r, T.recip ? 1 : 0);
 }
 static void launch_trsv(Context* ctx, const TriSched& T, const double* b, double* x) {
     switch (T.depth) {

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_scm.py tests/test_gpu_timeint.py tests/test_gpu_dist.py -x -q > gpurun_out/t16.log 2>&1; echo "exit $?" >> gpurun_out/t16.log
+timeout 300 python tools/step_bench.py config2 1000 3 > gpurun_out/t16_steps.log 2>&1
