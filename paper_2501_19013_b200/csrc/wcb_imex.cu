@@ -35,6 +35,9 @@ namespace wcb {
 // elimination level -- instead of a device-wide chain of global-memory
 // handshakes.  Entries of a row are visited in the same lane-strided order and
 // reduced by the same shuffle tree as the sync-free kernel (bitwise equal).
+#ifndef WCB_TRSV_STAGE_LATE
+#define WCB_TRSV_STAGE_LATE 1
+#endif
 constexpr int TRSV_DMAX = 12;
 static __host__ __device__ inline size_t trsv_slot_bytes(int e, int r);             // max ring depth (levels in flight)
 constexpr int TRSV_SMEM = 220 * 1024;     // dynamic shared memory budget
@@ -363,7 +366,9 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
     for (int l = 0; l < nl; ++l) {
         asm volatile("cp.async.wait_group %0;" ::"n"(TRSV_D - 2) : "memory");
         __syncthreads();
+#if !WCB_TRSV_STAGE_LATE
         stage(l + TRSV_D - 1);
+#endif
         const int a = lo[l], e = lo[l + 1];
         if (fits(l)) {
             const int* P = sp(l);
@@ -388,6 +393,9 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
                 if (lane == 0) xl[k - r0] = recip ? (xl[k - r0] - sacc) * sdiag[k] : (xl[k - r0] - sacc) / sdiag[k];
             }
         }
+#if WCB_TRSV_STAGE_LATE
+        stage(l + TRSV_D - 1);   // after the level's rows: off the critical path
+#endif
     }
     __syncthreads();
     asm volatile("cp.async.wait_group 0;" ::: "memory");
