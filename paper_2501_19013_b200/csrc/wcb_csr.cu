@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256) k_sell(int64_t n, const uint8_t* __restri
             a.out[row] = v;
             amp = mi != 0.0 ? amp_bits(v) : 0ULL;
         }
-        block_amp_max<256>(amp, a.amp);
+        warp_amp_max(amp, a.amp);
     } else {
         if (valid) y[row] = acc;
     }

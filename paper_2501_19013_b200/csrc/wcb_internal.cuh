@@ -209,6 +209,17 @@ __device__ __forceinline__ unsigned long long amp_bits(double v) {
     return b;
 }
 
+// Warp-wide max of per-thread amp bits, one atomic per warp (no block
+// barrier: warps that finish early leave at once).
+__device__ __forceinline__ void warp_amp_max(unsigned long long v, unsigned long long* slot) {
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(slot, v);
+}
+
 // Block-wide max of per-thread amp bits, one atomic per block.
 template <int BLOCK>
 __device__ __forceinline__ void block_amp_max(unsigned long long v, unsigned long long* slot) {
