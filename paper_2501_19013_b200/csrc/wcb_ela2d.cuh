@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(Tile2E<P>::NWARP * 32, WCB_ELA_MINB) k_ela2d(
     unsigned long long amp = 0ULL;
     if (w < T::NWB) ela2d_warp<P, MODE, 0>(g, mt, a, plane, smem, w, lane, J0, I0, amp, tcl, mtab);
     else ela2d_warp<P, MODE, 1>(g, mt, a, plane, smem, w - T::NWB, lane, J0, I0, amp, tcl, mtab);
-    if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
+    if constexpr (MODE == MODE_STEP) warp_amp_max(amp, a.amp);
 }
 
 

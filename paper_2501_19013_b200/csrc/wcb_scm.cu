@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
         }
     }
 #ifndef WCB2D_NOAMP
-    if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
+    if constexpr (MODE == MODE_STEP) warp_amp_max(amp, a.amp);
 #endif
 #ifdef WCB2D_TRACE
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_4));
