@@ -258,7 +258,10 @@ int wcb_context_create(int device, wcb_context** out) {
                         "wavecell_b200 is built for sm_100a (B200); device has compute "
                         "capability major " + std::to_string(major)};
         WCB_CUDA(cudaDeviceGetAttribute(&x.sm_count, cudaDevAttrMultiProcessorCount, device));
-        WCB_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
+        // highest priority: helper streams (IMEX far tiles) yield to it
+        int lo_prio = 0, hi_prio = 0;
+        WCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+        WCB_CUDA(cudaStreamCreateWithPriority(&x.stream, cudaStreamNonBlocking, hi_prio));
         {   // keep freed run buffers in the device pool (no release to the OS)
             cudaMemPool_t pool;
             WCB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));

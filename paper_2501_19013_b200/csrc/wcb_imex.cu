@@ -591,6 +591,16 @@ struct wcb_imex_plan {
     Operator* op = nullptr;
     Context* ctx = nullptr;   // retained
     int64_t n_c = 0, n_d = 0;
+    // overlap of step k+1's far tiles (second stream) with step k's c solve
+    bool split = false;
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t e_near = nullptr, e_far = nullptr, e_boot = nullptr;
+    ~wcb_imex_plan() {
+        if (s2) { cudaStreamSynchronize(s2); cudaStreamDestroy(s2); }
+        if (e_near) cudaEventDestroy(e_near);
+        if (e_far) cudaEventDestroy(e_far);
+        if (e_boot) cudaEventDestroy(e_boot);
+    }
     DevBuf<int64_t> c_state;          // state index of each c DOF (c order)
     DevBuf<int64_t> c_compact;
     DevBuf<double> minv, m_d_state;   // 1/m_d at d slots (0 at c / non-DOF), m_d at d slots
@@ -683,6 +693,15 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
         P->c_state.alloc(cs.size(), s); P->c_state.upload(cs.data(), n_c, s);
         P->Fc.alloc(Fc.size(), s); P->Fc.upload(Fc.data(), n_c, s);
         if (n_c) op->set_apply_subset(c_idx, n_c);   // K rows of c only, per step
+        if (n_c && n_d && !getenv("WAVECELL_B200_NO_IMEX_OVERLAP") && op->set_step_split(c_idx, n_c)) {
+            int lo_prio = 0, hi_prio = 0;
+            WCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+            WCB_CUDA(cudaStreamCreateWithPriority(&P->s2, cudaStreamNonBlocking, lo_prio));   // lowest
+            WCB_CUDA(cudaEventCreateWithFlags(&P->e_near, cudaEventDisableTiming));
+            WCB_CUDA(cudaEventCreateWithFlags(&P->e_far, cudaEventDisableTiming));
+            WCB_CUDA(cudaEventCreateWithFlags(&P->e_boot, cudaEventDisableTiming));
+            P->split = true;
+        }
         op->bind_minv(P->minv.p);                      // interior 1/m table for the d step
         // force vector for the d rows: dense window over its nonzeros
         {
@@ -861,24 +880,58 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
         checked = upto;
         return false;
     };
+    // Single plan, no NCCL: the explicit step is split into far tiles (input
+    // footprint free of c DOFs) on a second stream and near tiles on the main
+    // one; far(k+1) only needs step k's d values, so it runs while the c
+    // chain of step k (c-row apply, triangular solves, corrector) runs:
+    //   S0: near(k) -> [rec e_near] -> [wait e_far = far(k)] -> c chain(k)
+    //   S1: [wait e_near(k)] -> far(k+1) -> [rec e_far]
+    // far(k+1) writes psi_{k+2} over psi_k, read only by step k's explicit
+    // tiles (done: e_near) -- the c chain reads and writes the other buffer.
+    const bool overlap = G == 1 && !ctx->nccl && Ps[0]->split;
+    auto d_args = [&](wcb_imex_plan* P, int64_t k, double* c_, double* p_) {
+        StepArgs a;
+        a.minv = P->minv.p;
+        a.F = P->src;
+        a.dt2 = dt * dt;
+        a.cur = c_;
+        a.prev = p_;
+        a.out = p_;
+        a.ft = P->ft_k.p + 1;   // ft_k[k]
+        a.k = k;
+        a.amp = P->amp.p + (k + 1);
+        return a;
+    };
+    auto launch_far = [&](wcb_imex_plan* P, const StepArgs& a) {
+        cudaStream_t save = ctx->stream;
+        ctx->stream = P->s2;
+        try {
+            P->op->cdm_step_part(a, 0);
+        } catch (...) {
+            ctx->stream = save;
+            throw;
+        }
+        ctx->stream = save;
+    };
+    if (overlap && n_t > 0) {
+        wcb_imex_plan* P = Ps[0];
+        WCB_CUDA(cudaEventRecord(P->e_boot, s));
+        WCB_CUDA(cudaStreamWaitEvent(P->s2, P->e_boot, 0));
+        launch_far(P, d_args(P, 0, cur[0], prev[0]));
+        WCB_CUDA(cudaEventRecord(P->e_far, P->s2));
+    }
     for (int64_t k = 0; k < n_t; ++k) {
         for (size_t r = 0; r < G; ++r) {
             wcb_imex_plan* P = Ps[r];
             Operator* op = P->op;
             const int64_t ns = op->n_state, nc = P->n_c;
             // 1. explicit d step into prev (c slots overwritten below)
-            if (P->n_d > 0) {
-                StepArgs a;
-                a.minv = P->minv.p;
-                a.F = P->src;
-                a.dt2 = dt * dt;
-                a.cur = cur[r];
-                a.prev = prev[r];
-                a.out = prev[r];
-                a.ft = P->ft_k.p + 1;   // ft_k[k]
-                a.k = k;
-                a.amp = P->amp.p + (k + 1);
-                op->cdm_step(a);
+            if (overlap) {
+                op->cdm_step_part(d_args(P, k, cur[r], prev[r]), 1);
+                WCB_CUDA(cudaEventRecord(P->e_near, s));
+                WCB_CUDA(cudaStreamWaitEvent(s, P->e_far, 0));   // far(k) complete
+            } else if (P->n_d > 0) {
+                op->cdm_step(d_args(P, k, cur[r], prev[r]));
             } else {
                 WCB_CUDA(cudaMemcpyAsync(prev[r], cur[r], ns * sizeof(double), cudaMemcpyDeviceToDevice, s));
             }
@@ -893,6 +946,13 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
                 ctx->launches += 3;
                 // 4. a_c = S^-1 rhs_c (z permuted) ; 5. corrector
                 lu_solve(ctx, P, P->S, P->rhs.p, P->y.p);   // result in y (column-permuted space)
+                if (overlap && k + 1 < n_t) {
+                    // far(k+1) enqueued behind the solves (their CTAs claim the
+                    // SMs first; far tiles fill SMs the short patches free)
+                    WCB_CUDA(cudaStreamWaitEvent(P->s2, P->e_near, 0));
+                    launch_far(P, d_args(P, k + 1, prev[r], cur[r]));
+                    WCB_CUDA(cudaEventRecord(P->e_far, P->s2));
+                }
                 k_c_correct<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->S.perm_c.p, P->y.p, P->pred.p,
                                                            P->vpred.p, bdt2, gdt, P->a_c.p, P->psi_c.p, P->v_c.p,
                                                            prev[r], P->amp.p + (k + 1));
@@ -907,6 +967,7 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
             if (inspect(k + 1)) { diverged = true; break; }
         }
     }
+    if (overlap) WCB_CUDA(cudaStreamSynchronize(Ps[0]->s2));   // no far step left in flight
     WCB_CUDA(cudaEventRecord(ctx->ev1, s));
     WCB_CHECK_LAUNCH();
     if (!diverged) diverged = inspect(n_t);

@@ -280,6 +280,12 @@ struct Operator {
     // set_apply_subset (other rows of y are unspecified); default: full apply
     virtual bool set_apply_subset(const int64_t* /*compact_ids*/, int64_t /*n*/) { return false; }
     virtual void apply_subset(const double* x, double* y) { apply(x, y); }
+    // split of the fused step into tiles whose input footprint holds none of
+    // the given DOFs (part 0, "far") and the rest (part 1, "near"), so the far
+    // part of step k+1 can overlap the implicit solve of step k; false when
+    // the operator cannot split (then only cdm_step is used)
+    virtual bool set_step_split(const int64_t* /*ids*/, int64_t /*n*/) { return false; }
+    virtual void cdm_step_part(const StepArgs& a, int part) { if (part == 1) cdm_step(a); }
     // the plan's 1/m state vector (fixed for the plan's lifetime): operators
     // may precompute which cells read it (default: every node loads 1/m)
     virtual void bind_minv(const double* /*d_minv*/) {}

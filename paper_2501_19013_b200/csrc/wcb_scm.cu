@@ -479,6 +479,10 @@ struct ScmOperator final : Operator {
     DevBuf<int32_t> order_sub;
     int64_t n_order_sub = 0;
     bool sub_ready = false, sub_active = false;
+    std::vector<int32_t> order_h;            // host copy of the dispatch order
+    DevBuf<int32_t> order_part[2];           // step split: far / near tiles (dispatch order kept)
+    int64_t n_order_part[2] = {0, 0};
+    int part_active = -1;
     int64_t n_strips = 0, n_rtiles = 0;
     std::vector<double> m1, k1;
     double sk = 1.0;
@@ -523,8 +527,8 @@ struct ScmOperator final : Operator {
                     mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
-        const int32_t* ord = sub_active ? order_sub.p : order.p;
-        const int64_t n_ord = sub_active ? n_order_sub : n_order;
+        const int32_t* ord = part_active >= 0 ? order_part[part_active].p : sub_active ? order_sub.p : order.p;
+        const int64_t n_ord = part_active >= 0 ? n_order_part[part_active] : sub_active ? n_order_sub : n_order;
         if (!n_ord) return;
         Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, ord, n_strips, n_rtiles, pitch};
         dim3 grid((unsigned)n_ord);
@@ -537,7 +541,7 @@ struct ScmOperator final : Operator {
             g.tclean = tclean.p;
             for (int i = 0; i < P * P; ++i) tab.v[i] = minv_tab[i];
         }
-        if (MODE == MODE_STEP && pdl_enabled()) {
+        if (MODE == MODE_STEP && pdl_enabled() && part_active < 0) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = grid;
             cfg.blockDim = dim3(T::NWARP * 32);
@@ -632,8 +636,8 @@ struct ScmOperator final : Operator {
                                           (int)T::SMEM));
             attr_set = true;
         }
-        const int32_t* ord = sub_active ? order_sub.p : order.p;
-        const int64_t n_ord = sub_active ? n_order_sub : n_order;
+        const int32_t* ord = part_active >= 0 ? order_part[part_active].p : sub_active ? order_sub.p : order.p;
+        const int64_t n_ord = part_active >= 0 ? n_order_part[part_active] : sub_active ? n_order_sub : n_order;
         if (!n_ord) return;
         const EMats<P> mt = emats<P>();
         Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, ord, n_strips, n_rtiles, pitch};
@@ -899,6 +903,46 @@ struct ScmOperator final : Operator {
         WCB_CUDA(cudaStreamSynchronize(ctx->stream));
         sub_ready = true;
         return true;
+    }
+    bool set_step_split(const int64_t* ids, int64_t n_ids) override {
+        if (dim != 2 || order_h.empty()) return false;
+        const int RX = ncomp == 2 ? rpe_e(p) : rpe_for(p);
+        const int64_t TI = (int64_t)RX * p, TJ = 32 * (int64_t)p;
+        std::vector<uint8_t> near(n_strips * n_rtiles, 0);
+        for (int64_t k = 0; k < n_ids; ++k) {
+            const int64_t sk_ = sidx[ids[k]] % plane;
+            const int64_t row = sk_ / pitch - p, col = sk_ % pitch - PADJ;   // local node coordinates
+            // tiles whose input footprint [I0-p, I0+TI] x [J0-p-1, J0+TJ+1] holds the node
+            const int64_t rt_lo = std::max<int64_t>(0, (row - TI - row_lo) / TI - 1);
+            const int64_t rt_hi = std::min<int64_t>(n_rtiles - 1, (row + p - row_lo) / TI + 1);
+            const int64_t st_lo = std::max<int64_t>(0, (col - TJ - 1) / TJ - 1);
+            const int64_t st_hi = std::min<int64_t>(n_strips - 1, (col + p + 1) / TJ + 1);
+            for (int64_t rt = rt_lo; rt <= rt_hi; ++rt)
+                for (int64_t st = st_lo; st <= st_hi; ++st) {
+                    const int64_t I0 = row_lo + rt * TI, J0 = st * TJ;
+                    if (row >= I0 - p && row <= I0 + TI && col >= J0 - p - 1 && col <= J0 + TJ + 1)
+                        near[st * n_rtiles + rt] = 1;
+                }
+        }
+        std::vector<int32_t> part[2];
+        for (int32_t t : order_h) part[near[t] ? 1 : 0].push_back(t);
+        for (int q = 0; q < 2; ++q) {
+            n_order_part[q] = (int64_t)part[q].size();
+            order_part[q].alloc(std::max<int64_t>(n_order_part[q], 1));
+            if (n_order_part[q]) order_part[q].upload(part[q].data(), part[q].size(), ctx->stream);
+        }
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+        return true;
+    }
+    void cdm_step_part(const StepArgs& a, int part) override {
+        if (dim != 2 || n_order_part[0] + n_order_part[1] == 0) {
+            if (part == 1) cdm_step(a);
+            return;
+        }
+        part_active = part;
+        dispatch2d<MODE_STEP>(a);
+        part_active = -1;
+        WCB_CHECK_LAUNCH();
     }
     void apply_subset(const double* x, double* y) override {
         if (!sub_ready) { apply(x, y); return; }
@@ -1219,6 +1263,7 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
         op->n_order = (int64_t)ord.size();
         op->order.alloc(std::max<int64_t>(op->n_order, 1));
         op->order.upload(ord.data(), ord.size(), ctx->stream);
+        op->order_h = ord;
     }
     cudaStream_t st = ctx->stream;
     op->d_sidx.alloc(std::max<int64_t>(op->n, 1));
