@@ -35,6 +35,9 @@ namespace wcb {
 // elimination level -- instead of a device-wide chain of global-memory
 // handshakes.  Entries of a row are visited in the same lane-strided order and
 // reduced by the same shuffle tree as the sync-free kernel (bitwise equal).
+#ifndef WCB_TRSV_GW
+#define WCB_TRSV_GW 16
+#endif
 #ifndef WCB_TRSV_STAGE_LATE
 #define WCB_TRSV_STAGE_LATE 1
 #endif
@@ -332,6 +335,9 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
     auto sp = [&](int l) { return sc(l) + slot_e; };
     const int c = comp_order[blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    constexpr int GW = WCB_TRSV_GW;                 // lanes per row
+    const int hw = lane / GW, l16 = lane % GW;      // row slot in the warp, lane in the row group
+    const unsigned hmask = (GW == 32 ? 0xffffffffu : ((1u << GW) - 1u)) << (hw * GW);
     const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
     const int l0 = comp_lvl[c], nl = comp_lvl[c + 1] - l0;
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) xl[k - r0] = b[rows[k]];
@@ -375,22 +381,24 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
             const double* D = sd(l);
             const double* V = sv(l);
             const int* C = sc(l);
+            // GW lanes per row (levels are narrow: median 3 rows of ~47
+            // entries): GW-strided entries, log2(GW)-step shuffle tree
             const int base = P[0];
-            for (int k = warp; k < e - a; k += nw) {
+            for (int k = (32 / GW) * warp + hw; k < e - a; k += (32 / GW) * nw) {
                 const int p0 = P[k] - base, p1 = P[k + 1] - base;
                 double sacc = 0.0;
-                for (int j = p0 + lane; j < p1; j += 32) sacc = fma(V[j], xl[C[j]], sacc);
+                for (int j = p0 + l16; j < p1; j += GW) sacc = fma(V[j], xl[C[j]], sacc);
                 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
-                if (lane == 0) xl[a + k - r0] = recip ? (xl[a + k - r0] - sacc) * D[k] : (xl[a + k - r0] - sacc) / D[k];
+                for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
+                if (l16 == 0) xl[a + k - r0] = recip ? (xl[a + k - r0] - sacc) * D[k] : (xl[a + k - r0] - sacc) / D[k];
             }
         } else {
-            for (int k = a + warp; k < e; k += nw) {
+            for (int k = a + (32 / GW) * warp + hw; k < e; k += (32 / GW) * nw) {
                 double sacc = 0.0;
-                for (int j = sptr[k] + lane; j < sptr[k + 1]; j += 32) sacc = fma(sval[j], xl[slcol[j]], sacc);
+                for (int j = sptr[k] + l16; j < sptr[k + 1]; j += GW) sacc = fma(sval[j], xl[slcol[j]], sacc);
                 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, o);
-                if (lane == 0) xl[k - r0] = recip ? (xl[k - r0] - sacc) * sdiag[k] : (xl[k - r0] - sacc) / sdiag[k];
+                for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
+                if (l16 == 0) xl[k - r0] = recip ? (xl[k - r0] - sacc) * sdiag[k] : (xl[k - r0] - sacc) / sdiag[k];
             }
         }
 #if WCB_TRSV_STAGE_LATE
