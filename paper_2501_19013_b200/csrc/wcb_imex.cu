@@ -44,8 +44,8 @@ namespace wcb {
 constexpr int TRSV_DMAX = 12;
 static __host__ __device__ inline size_t trsv_slot_bytes(int e, int r);             // max ring depth (levels in flight)
 constexpr int TRSV_SMEM = 220 * 1024;     // dynamic shared memory budget
-constexpr int TRSV_THREADS = 512;      // launch bound
-constexpr int TRSV_THREADS_DEF = 512;
+constexpr int TRSV_THREADS = 1024;     // launch bound
+constexpr int TRSV_THREADS_DEF = 768;  // measured: 256 2770, 384 2485, 512 2329, 768 2253, 1024 2295 us per config-4 step
 
 struct TriSched {
     bool ok = false;
