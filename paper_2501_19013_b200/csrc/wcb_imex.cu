@@ -410,86 +410,6 @@ __global__ void __launch_bounds__(TRSV_THREADS) k_trsv_comp(
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) x[rows[k]] = xl[k - r0];
 }
 
-// Component-local sync-free solve: one CTA per component, x in shared memory
-// initialised to a sentinel; warps take the component's rows round-robin in
-// schedule (level) order and each lane waits only for the x entries its
-// products need, so rows of different levels overlap and no CTA barrier
-// separates levels.  A row's entries are loaded into registers one row ahead
-// (they do not depend on x).  Same lane-strided fma order and shuffle tree as
-// k_trsv_comp / k_sptrsv: bitwise equal results.
-constexpr int TRSF_THREADS = 512;
-constexpr int TRSF_E = 4;   // entries per lane held in registers (rows up to 128 entries)
-constexpr unsigned long long TRSF_SENT = 0xfff8dead0000beefULL;   // a NaN the solve never produces
-
-__device__ __forceinline__ double lds_volatile(const double* p) {
-    double v;
-    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32_imex(p)));
-    return v;
-}
-
-__global__ void __launch_bounds__(TRSF_THREADS, 2) k_trsv_sf(
-    const int32_t* __restrict__ comp_rows, const int32_t* __restrict__ rows,
-    const int32_t* __restrict__ sptr, const int32_t* __restrict__ slcol,
-    const double* __restrict__ sval, const double* __restrict__ sdiag, const double* __restrict__ b,
-    double* __restrict__ x) {
-    extern __shared__ __align__(16) double xs[];
-    const int c = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
-    for (int k = threadIdx.x; k < r1 - r0; k += blockDim.x) xs[k] = __longlong_as_double((long long)TRSF_SENT);
-    __syncthreads();
-    int cc[TRSF_E];
-    double cv[TRSF_E];
-    int p0 = 0, p1 = 0;
-    double bk = 0.0, dk = 1.0;
-    auto fetch = [&](int k) {
-        p0 = sptr[k];
-        p1 = sptr[k + 1];
-        #pragma unroll
-        for (int t = 0; t < TRSF_E; ++t) {
-            const int j = p0 + lane + 32 * t;
-            cc[t] = j < p1 ? slcol[j] : 0;
-            cv[t] = j < p1 ? sval[j] : 0.0;
-        }
-        bk = b[rows[k]];
-        dk = sdiag[k];
-    };
-    int k = r0 + warp;
-    if (k < r1) fetch(k);
-    for (; k < r1; k += nw) {
-        const int q0 = p0, q1 = p1;
-        int ccur[TRSF_E];
-        double vcur[TRSF_E];
-        #pragma unroll
-        for (int t = 0; t < TRSF_E; ++t) { ccur[t] = cc[t]; vcur[t] = cv[t]; }
-        const double bcur = bk, dcur = dk;
-        if (k + nw < r1) fetch(k + nw);   // next row's entries in flight while this one waits
-        double acc = 0.0;
-        #pragma unroll
-        for (int t = 0; t < TRSF_E; ++t) {
-            if (q0 + lane + 32 * t < q1) {
-                double xv;
-                do { xv = lds_volatile(xs + ccur[t]); } while ((unsigned long long)__double_as_longlong(xv) == TRSF_SENT);
-                acc = fma(vcur[t], xv, acc);
-            }
-        }
-        for (int j = q0 + lane + 32 * TRSF_E; j < q1; j += 32) {   // long rows
-            const int cj = slcol[j];
-            double xv;
-            do { xv = lds_volatile(xs + cj); } while ((unsigned long long)__double_as_longlong(xv) == TRSF_SENT);
-            acc = fma(sval[j], xv, acc);
-        }
-        #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-            const double v = (bcur - acc) / dcur;   // (unlaunched variant: expects sdiag = diag)
-            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32_imex(xs + (k - r0))), "d"(v) : "memory");
-        }
-    }
-    __syncthreads();
-    for (int k2 = r0 + threadIdx.x; k2 < r1; k2 += blockDim.x) x[rows[k2]] = xs[k2 - r0];
-}
-
 static __host__ __device__ inline size_t trsv_slot_bytes(int e, int r) {
     return (((size_t)e * 12 + (size_t)r * 8 + (size_t)(r + 1) * 4) + 15) / 16 * 16;
 }
