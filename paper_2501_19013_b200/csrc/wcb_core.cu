@@ -224,6 +224,120 @@ __global__ void k_pow_lambda(int nparts, const double* __restrict__ part, double
     }
 }
 
+// ------------------------------------------------- staged host copies ----
+// Pageable host arrays (NumPy) move through a per-device ring of pinned
+// chunks: the host side of each chunk is a memcpy split over threads (which
+// also faults in fresh destination pages in parallel), overlapped with the
+// DMA of the neighbouring chunk.  The driver's own pageable path stages
+// through one thread.
+namespace {
+constexpr size_t STAGE_CHUNK = size_t(8) << 20;
+constexpr int STAGE_NBUF = 3;
+constexpr size_t STAGE_MIN = size_t(2) << 20;   // smaller copies use cudaMemcpyAsync
+struct StageRing {
+    unsigned char* buf[STAGE_NBUF] = {};
+    cudaEvent_t ev[STAGE_NBUF] = {};
+    std::mutex mu;
+};
+StageRing* stage_ring(int dev) {
+    static std::mutex mu;
+    static std::vector<std::unique_ptr<StageRing>> rings;
+    std::lock_guard<std::mutex> g(mu);
+    if ((int)rings.size() <= dev) rings.resize(dev + 1);
+    if (!rings[dev]) {
+        auto r = std::make_unique<StageRing>();
+        for (int b = 0; b < STAGE_NBUF; ++b) {
+            WCB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&r->buf[b]), STAGE_CHUNK,
+                                   cudaHostAllocPortable));
+            WCB_CUDA(cudaEventCreateWithFlags(&r->ev[b], cudaEventDisableTiming));
+        }
+        rings[dev] = std::move(r);
+    }
+    return rings[dev].get();
+}
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    static const int nthr = std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2));
+    const size_t piece = ((bytes + nthr - 1) / nthr + 4095) & ~size_t(4095);
+    std::vector<std::thread> th;
+    for (int t = 1; t < nthr && t * piece < bytes; ++t)
+        th.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + t * piece, static_cast<const char*>(src) + t * piece,
+                        std::min(piece, bytes - t * piece));
+        });
+    std::memcpy(dst, src, std::min(piece, bytes));
+    for (auto& x : th) x.join();
+}
+struct DevGuard {   // events are recorded on the stream's device
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) WCB_CUDA(cudaSetDevice(dev));
+    }
+    ~DevGuard() {
+        int cur;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+int stream_device(cudaStream_t s) {
+    int dev;
+    if (s) WCB_CUDA(cudaStreamGetDevice(s, &dev));
+    else WCB_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
+}  // namespace
+
+void copy_h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
+    if (bytes < STAGE_MIN) {
+        if (bytes) WCB_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    const int dev = stream_device(s);
+    DevGuard g(dev);
+    StageRing* r = stage_ring(dev);
+    std::lock_guard<std::mutex> lk(r->mu);
+    for (size_t off = 0, i = 0; off < bytes; off += STAGE_CHUNK, ++i) {
+        const int b = (int)(i % STAGE_NBUF);
+        const size_t len = std::min(STAGE_CHUNK, bytes - off);
+        WCB_CUDA(cudaEventSynchronize(r->ev[b]));   // this chunk's last DMA is done
+        par_memcpy(r->buf[b], static_cast<const char*>(h) + off, len);
+        WCB_CUDA(cudaMemcpyAsync(static_cast<char*>(d) + off, r->buf[b], len,
+                                 cudaMemcpyHostToDevice, s));
+        WCB_CUDA(cudaEventRecord(r->ev[b], s));
+    }
+}
+
+void copy_d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
+    if (bytes < STAGE_MIN) {
+        if (bytes) {
+            WCB_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
+            WCB_CUDA(cudaStreamSynchronize(s));
+        }
+        return;
+    }
+    const int dev = stream_device(s);
+    DevGuard g(dev);
+    StageRing* r = stage_ring(dev);
+    std::lock_guard<std::mutex> lk(r->mu);
+    const size_t n = (bytes + STAGE_CHUNK - 1) / STAGE_CHUNK;
+    auto issue = [&](size_t i) {
+        const int b = (int)(i % STAGE_NBUF);
+        const size_t off = i * STAGE_CHUNK;
+        WCB_CUDA(cudaStreamWaitEvent(s, r->ev[b], 0));   // an H2D on another stream may read it
+        WCB_CUDA(cudaMemcpyAsync(r->buf[b], static_cast<const char*>(d) + off,
+                                 std::min(STAGE_CHUNK, bytes - off), cudaMemcpyDeviceToHost, s));
+        WCB_CUDA(cudaEventRecord(r->ev[b], s));
+    };
+    for (size_t i = 0; i < std::min<size_t>(n, STAGE_NBUF - 1); ++i) issue(i);
+    for (size_t i = 0; i < n; ++i) {
+        // buffer (i + NBUF - 1) % NBUF was drained by chunk i - 1's host copy
+        if (i + STAGE_NBUF - 1 < n) issue(i + STAGE_NBUF - 1);
+        const int b = (int)(i % STAGE_NBUF);
+        const size_t off = i * STAGE_CHUNK;
+        WCB_CUDA(cudaEventSynchronize(r->ev[b]));
+        par_memcpy(static_cast<char*>(h) + off, r->buf[b], std::min(STAGE_CHUNK, bytes - off));
+    }
+}
+
 }  // namespace wcb
 
 using namespace wcb;
@@ -399,8 +513,7 @@ int wcb_operator_apply(wcb_operator* o, const double* x, double* y) {
         op->scatter(dx.p, sx.p);
         op->apply(sx.p, sy.p);
         op->gather(sy.p, dy.p);
-        WCB_CUDA(cudaMemcpyAsync(y, dy.p, n * sizeof(double), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
+        copy_d2h(y, dy.p, n * sizeof(double), ctx->stream);
         WCB_CUDA(cudaStreamSynchronize(ctx->stream));
         return WCB_OK;
     });
@@ -853,8 +966,7 @@ int wcb_cdm_plan_run(wcb_cdm_plan* P, const double* ft, double dt, int64_t n_t,
         if (v0) { dv0.alloc(n, s); dv0.upload(v0, n, s); }
         if (obs_out && P->n_obs) dobs.alloc(P->n_obs * (n_t + 1), s);
         run_cdm_device(P, dft.p, dt, n_t, dpsi0.p, dv0.p, dout.p, dobs.p, div, tm);
-        if (n) WCB_CUDA(cudaMemcpyAsync(psi_out, dout.p, n * sizeof(double),
-                                        cudaMemcpyDeviceToHost, s));
+        copy_d2h(psi_out, dout.p, n * sizeof(double), s);
         if (obs_out && P->n_obs)
             WCB_CUDA(cudaMemcpyAsync(obs_out, dobs.p, P->n_obs * (n_t + 1) * sizeof(double),
                                      cudaMemcpyDeviceToHost, s));
@@ -890,8 +1002,7 @@ int wcb_cdm_group_run(int n_plans, wcb_cdm_plan** plans, const double* ft, doubl
         run_cdm_group(Ps, dft.p, dt, n_t, none, none, pout, pobs, div, tm);
         for (int r = 0; r < n_plans; ++r)
             if (Ps[r]->op->n)
-                WCB_CUDA(cudaMemcpyAsync(psi_out[r], pout[r], Ps[r]->op->n * sizeof(double),
-                                         cudaMemcpyDeviceToHost, s));
+                copy_d2h(psi_out[r], pout[r], Ps[r]->op->n * sizeof(double), s);
         if (obs_out && n_obs) {
             // sum of the per-slab partial observers, in slab order
             std::vector<double> acc(n_obs * (n_t + 1), 0.0), part(n_obs * (n_t + 1));

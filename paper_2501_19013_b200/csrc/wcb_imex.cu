@@ -908,7 +908,7 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
         wcb_imex_plan* P = Ps[r];
         Operator* op = P->op;
         op->gather(cur[r], tmp[r].p);
-        WCB_CUDA(cudaMemcpyAsync(psi_out[r], tmp[r].p, op->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        copy_d2h(psi_out[r], tmp[r].p, op->n * sizeof(double), s);
         // v_c in c order (the caller scatters it when d is empty, src/timeint.py:285-288)
         if (psi_dot_out[r] && P->n_c > 0)
             WCB_CUDA(cudaMemcpyAsync(psi_dot_out[r], P->v_c.p, P->n_c * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -29,6 +29,12 @@ struct Error {
                                                cudaGetErrorString(_e)};        \
     } while (0)
 
+// Host<->device copies of (pageable) host arrays; large ones are staged through
+// pinned chunks (wcb_core.cu).  copy_h2d returns once h may be reused,
+// copy_d2h once h holds the data.
+void copy_h2d(void* d, const void* h, size_t bytes, cudaStream_t s);
+void copy_d2h(void* h, const void* d, size_t bytes, cudaStream_t s);
+
 #define WCB_CHECK_LAUNCH() WCB_CUDA(cudaGetLastError())
 
 #define WCB_REQUIRE(cond, msg)                                                  \
@@ -90,9 +96,7 @@ struct DevBuf {
         st = nullptr;
         n = 0;
     }
-    void upload(const T* h, size_t count, cudaStream_t s) {
-        if (count) WCB_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
-    }
+    void upload(const T* h, size_t count, cudaStream_t s) { copy_h2d(p, h, count * sizeof(T), s); }
     void zero(cudaStream_t s) {
         if (n) WCB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
     }

@@ -21,7 +21,7 @@ import scipy.sparse.linalg as spla
 from . import _lib
 from .linalg import IndefiniteMatrixError, is_structurally_diagonal
 from .operators import DeviceOperator, as_device_operator
-from .timeint import DivergenceError, RunResult, StageTimings, _observer
+from .timeint import DivergenceError, RunResult, StageTimings, _observer, eval_force
 
 
 def _splu(A):
@@ -146,8 +146,9 @@ class ImexPlan:
         dt = self.dt
         n = self.n
         f0 = float(f_t(0.0))
-        ft_k = np.array([float(f_t(k * dt)) for k in range(n_t)] or [0.0])
-        ft_new = np.array([float(f_t(k * dt + dt)) for k in range(n_t)] or [0.0])
+        ks = np.arange(n_t, dtype=np.float64) * dt
+        ft_k = eval_force(f_t, ks) if n_t else np.zeros(1)
+        ft_new = eval_force(f_t, ks + dt) if n_t else np.zeros(1)
         p0 = None if psi0 is None else np.ascontiguousarray(np.array(psi0, dtype=float).reshape(-1))
         q0 = None if v0 is None else np.ascontiguousarray(np.array(v0, dtype=float).reshape(-1))
         psi = np.empty(n)

@@ -106,16 +106,30 @@ def imex_critical_time_step(K, M, d_idx, tol: float = 1e-9, seed: int = 0,
     return _dt_crit(K_dd, M_dd, tol=tol, seed=seed, device=device)
 
 
+def eval_force(f_t, t) -> np.ndarray:
+    """``[float(f_t(float(x))) for x in t]``.  A NumPy ufunc expression is
+    evaluated in one array call, kept only if it reproduces the scalar calls
+    bit for bit at probe points; anything else runs the scalar loop."""
+    t = np.asarray(t, dtype=np.float64)
+    n = t.shape[0]
+    if n > 64:
+        try:
+            with np.errstate(all="ignore"):
+                v = np.array(f_t(t), dtype=np.float64)
+            probe = sorted({0, 1, 2, n // 3, n // 2, n - 2, n - 1})
+            if v.shape == (n,) and all(v[k] == float(f_t(float(t[k]))) for k in probe):
+                return v
+        except Exception:
+            pass
+    return np.array([float(f_t(float(x))) for x in t], dtype=np.float64).reshape(n)
+
+
 def force_table(f_t, dt: float, n_t: int) -> np.ndarray:
     """``[f_t(k * dt) for k in range(n_t)]`` at the reference's float times
     (src/timeint.py:180-182); entry 0 is ``f_t(0.0)`` (the bootstrap force,
     src/timeint.py:175) and is always present."""
     n = max(int(n_t), 1)
-    out = np.empty(n)
-    out[0] = float(f_t(0.0))
-    for k in range(1, n):
-        out[k] = float(f_t(k * dt))
-    return out
+    return eval_force(f_t, np.arange(n, dtype=np.float64) * dt)
 
 
 def _observer(obs_mat, n):
