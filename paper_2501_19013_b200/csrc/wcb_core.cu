@@ -234,6 +234,13 @@ namespace {
 constexpr size_t STAGE_CHUNK = size_t(8) << 20;
 constexpr int STAGE_NBUF = 3;
 constexpr size_t STAGE_MIN = size_t(2) << 20;   // smaller copies use cudaMemcpyAsync
+bool stage_off() {   // WAVECELL_B200_NO_STAGE=1: plain cudaMemcpyAsync (A/B runs)
+    static const bool off = [] {
+        const char* e = getenv("WAVECELL_B200_NO_STAGE");
+        return e && e[0] == '1';
+    }();
+    return off;
+}
 struct StageRing {
     unsigned char* buf[STAGE_NBUF] = {};
     cudaEvent_t ev[STAGE_NBUF] = {};
@@ -287,7 +294,7 @@ int stream_device(cudaStream_t s) {
 }  // namespace
 
 void copy_h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
-    if (bytes < STAGE_MIN) {
+    if (bytes < STAGE_MIN || stage_off()) {
         if (bytes) WCB_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
         return;
     }
@@ -307,7 +314,7 @@ void copy_h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
 }
 
 void copy_d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
-    if (bytes < STAGE_MIN) {
+    if (bytes < STAGE_MIN || stage_off()) {
         if (bytes) {
             WCB_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
             WCB_CUDA(cudaStreamSynchronize(s));

@@ -21,7 +21,7 @@ obs = prob.obs_mat
 dt = 1e-7
 f = lambda t: ricker(t, 10.0)
 torch.cuda.synchronize()
-for rep in range(3):
+for rep in range(int(sys.argv[3]) if len(sys.argv) > 3 else 3):
     T = {}
     t0 = time.perf_counter()
     m = diagonal_mass(M); T["diagonal_mass"] = time.perf_counter() - t0
