@@ -231,7 +231,13 @@ __global__ void k_pow_lambda(int nparts, const double* __restrict__ part, double
 // DMA of the neighbouring chunk.  The driver's own pageable path stages
 // through one thread.
 namespace {
-constexpr size_t STAGE_CHUNK = size_t(8) << 20;
+size_t env_size(const char* name, size_t dflt, size_t lo, size_t hi) {
+    const char* e = getenv(name);
+    const long long v = e ? atoll(e) : 0;
+    return v > 0 ? std::min(hi, std::max(lo, (size_t)v)) : dflt;
+}
+// chunk MiB / host threads: WAVECELL_B200_STAGE_MB, WAVECELL_B200_STAGE_THREADS
+const size_t STAGE_CHUNK = env_size("WAVECELL_B200_STAGE_MB", 32, 1, 256) << 20;
 constexpr int STAGE_NBUF = 3;
 constexpr size_t STAGE_MIN = size_t(2) << 20;   // smaller copies use cudaMemcpyAsync
 bool stage_off() {   // WAVECELL_B200_NO_STAGE=1: plain cudaMemcpyAsync (A/B runs)
@@ -263,7 +269,8 @@ StageRing* stage_ring(int dev) {
     return rings[dev].get();
 }
 void par_memcpy(void* dst, const void* src, size_t bytes) {
-    static const int nthr = std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2));
+    static const int nthr = (int)env_size("WAVECELL_B200_STAGE_THREADS",
+                                          std::max(1u, std::min(16u, std::thread::hardware_concurrency())), 1, 64);
     const size_t piece = ((bytes + nthr - 1) / nthr + 4095) & ~size_t(4095);
     std::vector<std::thread> th;
     for (int t = 1; t < nthr && t * piece < bytes; ++t)
