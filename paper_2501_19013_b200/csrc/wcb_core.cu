@@ -320,6 +320,21 @@ void copy_h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
     }
 }
 
+Prefault::Prefault(void* p, size_t bytes) {
+    if (!p || bytes < STAGE_MIN || stage_off()) return;
+    const int nt = std::max(1, std::min(8, (int)std::thread::hardware_concurrency() / 2));
+    const size_t piece = ((bytes + nt - 1) / nt + 4095) & ~size_t(4095);
+    for (int t = 0; t < nt && t * piece < bytes; ++t)
+        th.emplace_back([=] {
+            std::memset(static_cast<char*>(p) + t * piece, 0, std::min(piece, bytes - t * piece));
+        });
+}
+Prefault::~Prefault() { join(); }
+void Prefault::join() {
+    for (auto& x : th) x.join();
+    th.clear();
+}
+
 void copy_d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
     if (bytes < STAGE_MIN || stage_off()) {
         if (bytes) {
@@ -979,7 +994,9 @@ int wcb_cdm_plan_run(wcb_cdm_plan* P, const double* ft, double dt, int64_t n_t,
         if (psi0) { dpsi0.alloc(n, s); dpsi0.upload(psi0, n, s); }
         if (v0) { dv0.alloc(n, s); dv0.upload(v0, n, s); }
         if (obs_out && P->n_obs) dobs.alloc(P->n_obs * (n_t + 1), s);
+        Prefault pf(psi_out, n * sizeof(double));   // fault the output in while the loop runs
         run_cdm_device(P, dft.p, dt, n_t, dpsi0.p, dv0.p, dout.p, dobs.p, div, tm);
+        pf.join();
         copy_d2h(psi_out, dout.p, n * sizeof(double), s);
         if (obs_out && P->n_obs)
             WCB_CUDA(cudaMemcpyAsync(obs_out, dobs.p, P->n_obs * (n_t + 1) * sizeof(double),
@@ -1013,7 +1030,11 @@ int wcb_cdm_group_run(int n_plans, wcb_cdm_plan** plans, const double* ft, doubl
             }
         }
         std::vector<const double*> none(n_plans, nullptr);
+        std::vector<std::unique_ptr<Prefault>> pfs;
+        for (int r = 0; r < n_plans; ++r)
+            pfs.emplace_back(new Prefault(psi_out[r], Ps[r]->op->n * sizeof(double)));
         run_cdm_group(Ps, dft.p, dt, n_t, none, none, pout, pobs, div, tm);
+        for (auto& pf : pfs) pf->join();
         for (int r = 0; r < n_plans; ++r)
             if (Ps[r]->op->n)
                 copy_d2h(psi_out[r], pout[r], Ps[r]->op->n * sizeof(double), s);

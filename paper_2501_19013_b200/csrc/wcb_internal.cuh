@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
+#include <thread>
 
 #include "../../include/wavecell_b200.h"
 
@@ -34,6 +35,14 @@ struct Error {
 // copy_d2h once h holds the data.
 void copy_h2d(void* d, const void* h, size_t bytes, cudaStream_t s);
 void copy_d2h(void* h, const void* d, size_t bytes, cudaStream_t s);
+// Writes zeros over a large host output buffer on background threads (its
+// pages are faulted in while the device works); join() before copy_d2h.
+struct Prefault {
+    std::vector<std::thread> th;
+    Prefault(void* p, size_t bytes);
+    ~Prefault();
+    void join();
+};
 
 #define WCB_CHECK_LAUNCH() WCB_CUDA(cudaGetLastError())
 
