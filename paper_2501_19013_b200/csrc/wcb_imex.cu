@@ -737,6 +737,10 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
         cur[r] = P->A.p;
         prev[r] = P->B.p;
     }
+    // fault the outputs in while the loop runs (inputs are uploaded above)
+    std::vector<std::unique_ptr<Prefault>> pfs;
+    for (size_t r = 0; r < G; ++r)
+        pfs.emplace_back(new Prefault(psi_out[r], Ps[r]->op->n * sizeof(double)));
     exchange(cur);   // psi_0 halos for the bootstrap apply
     for (size_t r = 0; r < G; ++r) {
         wcb_imex_plan* P = Ps[r];
@@ -904,6 +908,7 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
     WCB_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     if (tm) tm->rhs = ms * 1e-3;
     if (diverged) throw Error{WCB_E_DIVERGED, "solution diverged"};
+    for (auto& pf : pfs) pf->join();
     for (size_t r = 0; r < G; ++r) {
         wcb_imex_plan* P = Ps[r];
         Operator* op = P->op;
