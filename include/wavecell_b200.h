@@ -237,6 +237,7 @@ typedef struct {
     const int64_t* U_indptr; const int32_t* U_indices; const double* U_data;
 } wcb_lu;
 
+/* S_cc may be NULL (a mass-only plan, see wcb_mass_plan_create). */
 int wcb_imex_plan_create(wcb_operator* K, int64_t n_c, const int64_t* c_idx,
                          int64_t n_d, const int64_t* d_idx, const double* m_d,
                          const wcb_lu* S_cc, const wcb_lu* M_cc, const double* F_s,
@@ -250,6 +251,27 @@ int wcb_imex_plan_run(wcb_imex_plan* plan, double f0, const double* ft_k,
                       double gamma, const double* psi0, const double* v0,
                       double* psi_out, double* psi_dot_out, double* obs_out,
                       wcb_divergence* div, wcb_timings* tm);
+
+/* ---- consistent (non-diagonal) mass: factorize()'s SuperLU path ------------
+ * src/linalg.py:70-80 as used by cdm_run (src/timeint.py:166-176) and
+ * max_gen_eig (src/linalg.py:106-116) when M is not diagonal.  A symmetric M
+ * splits into the rows that store only their diagonal (d, m_d) and the rest
+ * (c); M = blockdiag(diag(m_d), M_cc) after permutation, M_cc prefactorised on
+ * the host (wcb_lu) and also passed as CSR in c order (for x'Mx).  The plan is
+ * an IMEX plan without S_cc factors. */
+int wcb_mass_plan_create(wcb_operator* K, int64_t n_c, const int64_t* c_idx, int64_t n_d,
+                         const int64_t* d_idx, const double* m_d, const wcb_lu* M_cc,
+                         const int64_t* Mcc_indptr, const int32_t* Mcc_indices, const double* Mcc_data,
+                         const double* F_s, const wcb_observer* obs, wcb_imex_plan** out);
+/* cdm_run with that mass: ft[k] = f_t(k*dt), k = 0..n_t-1 (as wcb_cdm_plan_run);
+ * per step the d rows by the fused explicit step, the c rows by
+ * (f F - K psi_k)_c, the two M_cc triangular solves and the leapfrog update. */
+int wcb_imex_plan_cdm_run(wcb_imex_plan* plan, const double* ft, double dt, int64_t n_t,
+                          const double* psi0, const double* v0, double* psi_out, double* obs_out,
+                          wcb_divergence* div, wcb_timings* tm);
+/* max_gen_eig(K, M) with that mass (x0 = the seeded start vector, n entries). */
+int wcb_imex_plan_max_gen_eig(wcb_imex_plan* plan, const double* x0, double tol, int64_t max_iter,
+                              double* lam, int64_t* n_iter);
 
 #ifdef __cplusplus
 }

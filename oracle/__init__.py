@@ -12,6 +12,9 @@ This package restates, on the CPU, the reference algorithms of `wavecell`
   structured spectral-cell operators, used as the multi-threaded CPU baseline
   (``bench.py --impl reference`` / ``cpu_baseline``) on the GPU box, where
   the Python reference does not exist.
+* ``oracle.geometry_cube`` -- the reference's rotated-cube benchmark
+  geometry (src/geometry.py:128-272), which pins the product's host set-up
+  to the reference's own grids and operators.
 
 Pinning: ``tests/test_oracle_golden.py`` checks this restatement against
 golden vectors produced by running the reference itself in this container

@@ -35,7 +35,8 @@ EXPORTS = (
     "wcb_cdm_plan_run", "wcb_cdm_plan_run_device", "wcb_imex_plan_create",
     "wcb_imex_plan_destroy", "wcb_imex_plan_run", "wcb_dist_unique_id", "wcb_dist_init",
     "wcb_dist_finalize", "wcb_cdm_group_run", "wcb_cdm_plan_step_bytes", "wcb_imex_group_run",
-    "wcb_csr_diagonal_check",
+    "wcb_csr_diagonal_check", "wcb_mass_plan_create", "wcb_imex_plan_cdm_run",
+    "wcb_imex_plan_max_gen_eig",
 )
 
 _p = C.c_void_p
@@ -111,6 +112,11 @@ _SIGS = {
                                        C.POINTER(LU), _dp, C.POINTER(Observer),
                                        C.POINTER(_p)]),
     "wcb_imex_plan_destroy": (C.c_int, [_p]),
+    "wcb_mass_plan_create": (C.c_int, [_p, _i64, _i64p, _i64, _i64p, _dp, C.POINTER(LU), _i64p, _i32p,
+                                       _dp, _dp, C.POINTER(Observer), C.POINTER(_p)]),
+    "wcb_imex_plan_cdm_run": (C.c_int, [_p, _dp, _d, _i64, _dp, _dp, _dp, _dp,
+                                        C.POINTER(Divergence), C.POINTER(Timings)]),
+    "wcb_imex_plan_max_gen_eig": (C.c_int, [_p, _dp, _d, _i64, _dp, _i64p]),
     "wcb_dist_unique_id": (C.c_int, [C.c_char_p]),
     "wcb_dist_init": (C.c_int, [_p, C.c_int, C.c_int, C.c_char_p]),
     "wcb_dist_finalize": (C.c_int, [_p]),

@@ -30,6 +30,21 @@ static void host_par_for(int64_t n, F&& f) {
     for (auto& x : th) x.join();
 }
 
+void ensure_smem_attr(const void* fn, int device, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int>, size_t>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : done)
+        if (e.first.first == fn && e.first.second == device) {
+            if (e.second >= bytes) return;
+            WCB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            e.second = bytes;
+            return;
+        }
+    WCB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done.push_back({{fn, device}, bytes});
+}
+
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
@@ -122,8 +137,9 @@ __global__ void k_cdm_bootstrap(int64_t ns, const double* __restrict__ psi,
     const double c = 0.5 * dt * dt;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns;
          i += (int64_t)gridDim.x * blockDim.x) {
-        double a = (f0 * source_at(F, i) - Kpsi[i]) / m_state[i];
-        prev[i] = psi[i] - dt * v[i] + c * a;
+        // src/timeint.py:175-176, each operation rounded on its own (no FMA)
+        const double a = __ddiv_rn(__dsub_rn(__dmul_rn(f0, source_at(F, i)), Kpsi[i]), m_state[i]);
+        prev[i] = __dadd_rn(__dsub_rn(psi[i], __dmul_rn(dt, v[i])), __dmul_rn(c, a));
     }
 }
 
@@ -549,72 +565,140 @@ int wcb_operator_apply(wcb_operator* o, const double* x, double* y) {
 }
 
 // ---------------------------------------------------------- max_gen_eig ----
-// Power iteration of M^-1 K on the state; DOFs with m = +inf are frozen at
-// zero (principal sub-problem, see wcb_max_gen_eig_sub).
+// Power iteration of M^-1 K on the state (src/linalg.py:89-122); DOFs with
+// m = +inf are frozen at zero (principal sub-problem, wcb_max_gen_eig_sub).
+// With `hooks` the mass is blockdiag(diag(m), M_cc): m_diag holds 1 at the c
+// rows, hooks->solve_c overwrites the c slots of y = M^-1 t and
+// hooks->apply_c the c slots of M x (factorize()'s SuperLU path).
+}  // extern "C"
+namespace wcb {
+__global__ void k_div_state(int64_t ns, const double* __restrict__ t, const double* __restrict__ m,
+                            double* __restrict__ y, const double* __restrict__ sc) {
+    if (sc[3] != 0.0) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = t[i] / m[i];
+}
+__global__ void k_sumsq(int64_t ns, const double* __restrict__ y, double* __restrict__ part,
+                        const double* __restrict__ sc) {
+    if (sc[3] != 0.0) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < ns; i += (int64_t)gridDim.x * RB)
+        acc += y[i] * y[i];
+    double s = block_sum<RB>(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_mul_state(int64_t ns, const double* __restrict__ m, const double* __restrict__ x,
+                            double* __restrict__ mx, const double* __restrict__ sc) {
+    if (sc[3] != 0.0) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x)
+        mx[i] = m[i] * x[i];
+}
+// partials of x.Kx and x.Mx with M x given
+__global__ void k_pow_dots_mx(int64_t ns, const double* __restrict__ x, const double* __restrict__ Kx,
+                              const double* __restrict__ Mx, double* __restrict__ part,
+                              const double* __restrict__ sc) {
+    if (sc[3] != 0.0) return;
+    double a = 0.0, b = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < ns; i += (int64_t)gridDim.x * RB) {
+        const double xi = x[i];
+        a += xi * Kx[i];
+        b += xi * Mx[i];
+    }
+    double sa = block_sum<RB>(a);
+    double sb = block_sum<RB>(b);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = sa;
+        part[2 * blockIdx.x + 1] = sb;
+    }
+}
+
+void max_gen_eig_core(Operator* op, const double* m_diag, const double* x0, double tol, int64_t max_iter,
+                      double* lam, int64_t* n_iter, const MassHooks* hooks) {
+    Context* ctx = op->ctx;
+    WCB_CUDA(cudaSetDevice(ctx->device));
+    const int64_t n = op->n, ns = op->n_state;
+    WCB_REQUIRE(n > 0, "empty operator");
+    cudaStream_t s = ctx->stream;
+    DevBuf<double> dm(n), dx0(n), m_state(ns), minv(ns), x(ns), t(ns), y(ns), mx;
+    DevBuf<int64_t> map;
+    if (hooks) mx.alloc(ns, s);
+    dm.upload(m_diag, n, s);
+    dx0.upload(x0, n, s);
+    // mass in state layout (1 at non-DOF slots so y = 0/1 = 0 there)
+    k_fill<<<grid_for(ctx, ns), 256, 0, s>>>(ns, 1.0, m_state.p);
+    ctx->launches++;
+    {
+        const std::vector<int64_t>& si = op->state_index();
+        map.alloc(n);
+        map.upload(si.data(), n, s);
+        k_mass_state<<<grid_for(ctx, n), 256, 0, s>>>(n, map.p, dm.p, m_state.p, minv.p);
+        ctx->launches++;
+    }
+    x.zero(s);
+    op->scatter(dx0.p, x.p);
+    t.zero(s);
+    y.zero(s);
+    WCB_CHECK_LAUNCH();
+    const int gb = grid_for(ctx, ns, RB);
+    double init[8] = {0.0, 0.0, INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0};
+    WCB_CUDA(cudaMemcpyAsync(ctx->scalars.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    double* sc = ctx->scalars.p;
+    double* part = ctx->partials.p;
+    const int64_t batch = 16;
+    int64_t it = 1;
+    bool done = false;
+    while (!done && it <= max_iter) {
+        int64_t end = std::min<int64_t>(max_iter, it + batch - 1);
+        for (; it <= end; ++it) {
+            op->apply(x.p, t.p);
+            if (hooks) {
+                k_div_state<<<grid_for(ctx, ns), 256, 0, s>>>(ns, t.p, m_state.p, y.p, sc);
+                hooks->solve_c(t.p, y.p);
+                k_sumsq<<<gb, RB, 0, s>>>(ns, y.p, part, sc);
+                ctx->launches += 2;
+            } else {
+                k_pow_y<<<gb, RB, 0, s>>>(ns, t.p, m_state.p, y.p, part, sc);
+                ctx->launches++;
+            }
+            k_pow_norm<<<1, RB, 0, s>>>(gb, part, sc, it);
+            k_pow_x<<<gb, RB, 0, s>>>(ns, y.p, x.p, sc);
+            op->apply(x.p, t.p);
+            if (hooks) {
+                k_mul_state<<<grid_for(ctx, ns), 256, 0, s>>>(ns, m_state.p, x.p, mx.p, sc);
+                hooks->apply_c(x.p, mx.p);
+                k_pow_dots_mx<<<gb, RB, 0, s>>>(ns, x.p, t.p, mx.p, part, sc);
+                ctx->launches += 2;
+            } else {
+                k_pow_dots<<<gb, RB, 0, s>>>(ns, x.p, t.p, m_state.p, part, sc);
+                ctx->launches++;
+            }
+            k_pow_lambda<<<1, RB, 0, s>>>(gb, part, sc, tol, it);
+            ctx->launches += 3;
+        }
+        WCB_CHECK_LAUNCH();
+        WCB_CUDA(cudaMemcpyAsync(ctx->h_scalars, sc, 8 * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+        WCB_CUDA(cudaStreamSynchronize(s));
+        done = ctx->h_scalars[3] != 0.0;
+    }
+    if (!done) {
+        char buf[160];
+        snprintf(buf, sizeof(buf),
+                 "power iteration did not converge in %lld iterations (last estimate %.6e)",
+                 (long long)max_iter, ctx->h_scalars[2]);
+        throw Error{WCB_E_NOCONV, buf};
+    }
+    *lam = ctx->h_scalars[1];
+    *n_iter = (int64_t)ctx->h_scalars[4];
+}
+}  // namespace wcb
+extern "C" {
+
 static int max_gen_eig_impl(wcb_operator* o, const double* m_diag, const double* x0, double tol,
                             int64_t max_iter, double* lam, int64_t* n_iter) {
     return guarded([&] {
         WCB_REQUIRE(o && m_diag && x0 && lam && n_iter, "NULL argument");
-        Operator* op = o->op;
-        Context* ctx = op->ctx;
-        WCB_CUDA(cudaSetDevice(ctx->device));
-        const int64_t n = op->n, ns = op->n_state;
-        WCB_REQUIRE(n > 0, "empty operator");
-        cudaStream_t s = ctx->stream;
-        DevBuf<double> dm(n), dx0(n), m_state(ns), minv(ns), x(ns), t(ns), y(ns);
-        DevBuf<int64_t> map;
-        dm.upload(m_diag, n, s);
-        dx0.upload(x0, n, s);
-        // mass in state layout (1 at non-DOF slots so y = 0/1 = 0 there)
-        k_fill<<<grid_for(ctx, ns), 256, 0, s>>>(ns, 1.0, m_state.p);
-        ctx->launches++;
-        {
-            const std::vector<int64_t>& si = op->state_index();
-            map.alloc(n);
-            map.upload(si.data(), n, s);
-            k_mass_state<<<grid_for(ctx, n), 256, 0, s>>>(n, map.p, dm.p, m_state.p, minv.p);
-            ctx->launches++;
-        }
-        x.zero(s);
-        op->scatter(dx0.p, x.p);
-        t.zero(s);
-        y.zero(s);
-        WCB_CHECK_LAUNCH();
-        const int gb = grid_for(ctx, ns, RB);
-        double init[8] = {0.0, 0.0, INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0};
-        WCB_CUDA(cudaMemcpyAsync(ctx->scalars.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
-        double* sc = ctx->scalars.p;
-        double* part = ctx->partials.p;
-        const int64_t batch = 16;
-        int64_t it = 1;
-        bool done = false;
-        while (!done && it <= max_iter) {
-            int64_t end = std::min<int64_t>(max_iter, it + batch - 1);
-            for (; it <= end; ++it) {
-                op->apply(x.p, t.p);
-                k_pow_y<<<gb, RB, 0, s>>>(ns, t.p, m_state.p, y.p, part, sc);
-                k_pow_norm<<<1, RB, 0, s>>>(gb, part, sc, it);
-                k_pow_x<<<gb, RB, 0, s>>>(ns, y.p, x.p, sc);
-                op->apply(x.p, t.p);
-                k_pow_dots<<<gb, RB, 0, s>>>(ns, x.p, t.p, m_state.p, part, sc);
-                k_pow_lambda<<<1, RB, 0, s>>>(gb, part, sc, tol, it);
-                ctx->launches += 5;
-            }
-            WCB_CHECK_LAUNCH();
-            WCB_CUDA(cudaMemcpyAsync(ctx->h_scalars, sc, 8 * sizeof(double),
-                                     cudaMemcpyDeviceToHost, s));
-            WCB_CUDA(cudaStreamSynchronize(s));
-            done = ctx->h_scalars[3] != 0.0;
-        }
-        if (!done) {
-            char buf[160];
-            snprintf(buf, sizeof(buf),
-                     "power iteration did not converge in %lld iterations (last estimate %.6e)",
-                     (long long)max_iter, ctx->h_scalars[2]);
-            throw Error{WCB_E_NOCONV, buf};
-        }
-        *lam = ctx->h_scalars[1];
-        *n_iter = (int64_t)ctx->h_scalars[4];
+        max_gen_eig_core(o->op, m_diag, x0, tol, max_iter, lam, n_iter, nullptr);
         return WCB_OK;
     });
 }
@@ -676,7 +760,7 @@ static void exchange_halos(std::vector<wcb_cdm_plan*>& Ps, std::vector<double*>&
         int64_t h[8];
         Operator* op = Ps[0]->op;
         Context* ctx = op->ctx;
-        if (ctx->nccl && op->halo(h)) nccl_exchange_halo(ctx, cur[0], h, op->halo_nplanes, op->halo_pstride);
+        if (dist_slab(op) && op->halo(h)) nccl_exchange_halo(ctx, cur[0], h, op->halo_nplanes, op->halo_pstride);
         return;
     }
     std::vector<Operator*> ops;
@@ -776,7 +860,7 @@ static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, do
         if (upto <= checked) return false;
         const int64_t cnt = upto - checked;
         for (size_t r = 0; r < G; ++r) {
-            nccl_allreduce_max_u64(ctx, Ps[r]->amp.p + checked + 1, cnt);
+            if (G == 1 && dist_slab(Ps[r]->op)) nccl_allreduce_max_u64(ctx, Ps[r]->amp.p + checked + 1, cnt);
             WCB_CUDA(cudaMemcpyAsync(h_amp.data() + r * (n_t + 1) + checked + 1, Ps[r]->amp.p + checked + 1,
                                      cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         }
@@ -838,7 +922,7 @@ static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, do
     if (tm) tm->rhs = ms * 1e-3;
     if (diverged) throw Error{WCB_E_DIVERGED, "solution diverged"};
     for (size_t r = 0; r < G; ++r) {
-        if (Ps[r]->n_obs && d_obs_out[r]) nccl_allreduce_sum_f64(ctx, d_obs_out[r], Ps[r]->n_obs * stride);
+        if (Ps[r]->n_obs && d_obs_out[r] && G == 1 && dist_slab(Ps[r]->op)) nccl_allreduce_sum_f64(ctx, d_obs_out[r], Ps[r]->n_obs * stride);
         Ps[r]->op->gather(cur[r], d_psi_out[r]);
     }
     WCB_CUDA(cudaStreamSynchronize(s));

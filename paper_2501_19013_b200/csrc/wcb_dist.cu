@@ -97,6 +97,12 @@ void copy_exchange_halo(const std::vector<Operator*>& ops, const std::vector<dou
     }
 }
 
+bool dist_slab(const Operator* op) {
+    const Nccl* N = op->ctx->nccl;
+    int64_t h[8];
+    return N && N->world > 1 && op->halo(h);
+}
+
 void nccl_allreduce_max_u64(Context* ctx, unsigned long long* d, int64_t n) {
     Nccl* N = ctx->nccl;
     if (!N || N->world == 1 || n <= 0) return;

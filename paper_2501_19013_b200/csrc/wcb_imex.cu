@@ -419,12 +419,8 @@ size_t TriSched::smem_bytes() const {
 
 template <int D>
 static void launch_trsv_d(Context* ctx, const TriSched& T, const double* b, double* x) {
-    static size_t attr = 0;
     const size_t sm = T.smem_bytes();
-    if (attr < sm) {
-        WCB_CUDA(cudaFuncSetAttribute(k_trsv_comp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        attr = sm;
-    }
+    ensure_smem_attr((const void*)k_trsv_comp<D>, ctx->device, sm);
     static const int threads = [] {
         const char* e = getenv("WAVECELL_B200_TRSV_THREADS");
         const int t = e ? atoi(e) : TRSV_THREADS_DEF;
@@ -457,9 +453,10 @@ __global__ void k_c_predict(int64_t nc, const int64_t* __restrict__ cs, const do
                             double c1, double c2, double* __restrict__ state, double* __restrict__ pred,
                             double* __restrict__ vpred) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
-        const double p = psi_c[i] + dt * v_c[i] + c1 * a_c[i];
+        // src/timeint.py:271-272, each operation rounded on its own (no FMA)
+        const double p = __dadd_rn(__dadd_rn(psi_c[i], __dmul_rn(dt, v_c[i])), __dmul_rn(c1, a_c[i]));
         pred[i] = p;
-        vpred[i] = v_c[i] + c2 * a_c[i];
+        vpred[i] = __dadd_rn(v_c[i], __dmul_rn(c2, a_c[i]));
         state[cs[i]] = p;
     }
 }
@@ -469,7 +466,7 @@ __global__ void k_c_rhs(int64_t nc, const double* __restrict__ Fc, const double*
                         int64_t k, const double* __restrict__ Kc, double* __restrict__ rhs) {
     const double f = ft[k];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
-        rhs[i] = f * Fc[i] - Kc[i];
+        rhs[i] = __dsub_rn(__dmul_rn(f, Fc[i]), Kc[i]);
 }
 
 // corrector (src/timeint.py:279-282); a_c = z[perm_c[i]]; amp over c nodes
@@ -482,9 +479,9 @@ __global__ void k_c_correct(int64_t nc, const int64_t* __restrict__ cs, const in
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
         const double a = z[perm_c[i]];
         a_c[i] = a;
-        const double p = pred[i] + bdt2 * a;
+        const double p = __dadd_rn(pred[i], __dmul_rn(bdt2, a));
         psi_c[i] = p;
-        v_c[i] = vpred[i] + gdt * a;
+        v_c[i] = __dadd_rn(vpred[i], __dmul_rn(gdt, a));
         state[cs[i]] = p;
         unsigned long long b = amp_bits(p);
         amp = b > amp ? b : amp;
@@ -506,8 +503,56 @@ __global__ void k_imex_boot(int64_t ns, const double* __restrict__ psi, const do
     const double c = 0.5 * dt * dt;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x) {
         const double md = m_d_state[i];
-        double a = md > 0.0 ? (f0 * source_at(F, i) - Kpsi[i]) / md : 0.0;
-        prev[i] = psi[i] - dt * v[i] + c * a;
+        const double a = md > 0.0 ? __ddiv_rn(__dsub_rn(__dmul_rn(f0, source_at(F, i)), Kpsi[i]), md) : 0.0;
+        prev[i] = __dadd_rn(__dsub_rn(psi[i], __dmul_rn(dt, v[i])), __dmul_rn(c, a));
+    }
+}
+
+// consistent-mass CDM bootstrap of the c rows (src/timeint.py:175-176):
+// psi_prev_c = psi_c - dt v_c + (dt^2/2) a_c
+__global__ void k_c_boot_prev(int64_t nc, const int64_t* __restrict__ cs, const double* __restrict__ psi_c,
+                              const double* __restrict__ v_c, const double* __restrict__ a_c, double dt,
+                              double c, double* __restrict__ prev) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
+        prev[cs[i]] = __dadd_rn(__dsub_rn(psi_c[i], __dmul_rn(dt, v_c[i])), __dmul_rn(c, a_c[i]));
+}
+
+// consistent-mass CDM update of the c rows (src/timeint.py:185): the fused
+// step left 2 psi - psi_prev in the c slots (1/m = 0 there); add dt^2 a_c
+// with a_c = z[perm_c] = (M_cc^-1 rhs_c)
+__global__ void k_c_cdm_update(int64_t nc, const int64_t* __restrict__ cs, const int64_t* __restrict__ perm_c,
+                               const double* __restrict__ z, double dt2, double* __restrict__ state) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = cs[i];
+        state[j] = __dadd_rn(state[j], __dmul_rn(dt2, z[perm_c[i]]));
+    }
+}
+
+// max |psi| over a whole state vector (non-DOF slots hold 0) -- the
+// divergence amplitude of src/timeint.py:91-94 once every row is final
+__global__ void k_state_amp(int64_t ns, const double* __restrict__ state, unsigned long long* amp_slot) {
+    unsigned long long amp = 0ULL;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long b = amp_bits(state[i]);
+        amp = b > amp ? b : amp;
+    }
+    block_amp_max<256>(amp, amp_slot);
+}
+
+// dst[cs[i]] = src[perm[i]]  (perm may be NULL: identity)
+__global__ void k_scatter_rows(int64_t n, const int64_t* __restrict__ cs, const int64_t* __restrict__ perm,
+                               const double* __restrict__ src, double* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[cs[i]] = src[perm ? perm[i] : i];
+}
+
+// y = A x (CSR, stored order per row, as scipy's csr_matvec)
+__global__ void k_csr_rows(int64_t n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                           const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int64_t j = ptr[i]; j < ptr[i + 1]; ++j) acc = __dadd_rn(acc, __dmul_rn(val[j], x[idx[j]]));
+        y[i] = acc;
     }
 }
 
@@ -536,6 +581,12 @@ struct wcb_imex_plan {
     DevBuf<double> F_win;
     Source src;
     DevLU S, Mcc;
+    bool has_S = false;
+    // M_cc in CSR (c order), for x'Mx of the consistent-mass power iteration
+    DevBuf<int64_t> mcc_ptr;
+    DevBuf<int32_t> mcc_idx;
+    DevBuf<double> mcc_val;
+    bool has_mcc_csr = false;
     int64_t n_obs = 0;
     DevBuf<int64_t> obs_indptr, obs_idx;
     DevBuf<double> obs_val;
@@ -544,7 +595,7 @@ struct wcb_imex_plan {
     DevBuf<double> psi_c, v_c, a_c, pred, vpred, Kc, rhs, y, z;
     DevBuf<int> done;
     DevBuf<unsigned long long> counter;
-    DevBuf<unsigned long long> amp;
+    DevBuf<unsigned long long> amp, amp_scratch;
     DevBuf<double> ft_k, ft_new;
 };
 
@@ -639,8 +690,11 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
             P->src = make_source(std::move(nz), P->F_win, s);
         }
         if (n_c) {
-            WCB_REQUIRE(S_cc && M_cc && S_cc->n == n_c && M_cc->n == n_c, "LU factors of size n_c required");
-            P->S.load(S_cc, s);
+            WCB_REQUIRE(M_cc && M_cc->n == n_c && (!S_cc || S_cc->n == n_c), "LU factors of size n_c required");
+            if (S_cc) {
+                P->S.load(S_cc, s);
+                P->has_S = true;
+            }
             P->Mcc.load(M_cc, s);
         }
         if (obs && obs->n_obs > 0) {
@@ -661,6 +715,7 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
         P->Kc.alloc(m, s); P->rhs.alloc(m, s); P->y.alloc(m, s); P->z.alloc(m, s);
         P->done.alloc(m, s);
         P->counter.alloc(2, s);
+        P->amp_scratch.alloc(1, s);
         WCB_CUDA(cudaStreamSynchronize(s));
         ctx_retain(ctx);
         *out = P.release();
@@ -695,11 +750,18 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
                            const double* ft_new, double dt, int64_t n_t, double beta, double gamma,
                            const std::vector<const double*>& psi0, const std::vector<const double*>& v0,
                            const std::vector<double*>& psi_out, const std::vector<double*>& psi_dot_out,
-                           const std::vector<double*>& obs_out, wcb_divergence* div, wcb_timings* tm) {
+                           const std::vector<double*>& obs_out, wcb_divergence* div, wcb_timings* tm,
+                           bool cdm = false) {
+    // cdm: cdm_run with the consistent mass blockdiag(diag(m_d), M_cc)
+    // (src/timeint.py:159-193 through factorize()'s SuperLU path): the d rows
+    // by the fused step, the c rows by rhs_c = f F_c - (K psi_k)_c and the M_cc
+    // triangular solves; ft_k[k] = f(k dt) as in the IMEX d rows
     const size_t G = Ps.size();
     Context* ctx = Ps[0]->op->ctx;
     for (auto* P : Ps) WCB_REQUIRE(P->op->ctx == ctx, "group plans must share one context");
     WCB_REQUIRE(n_t >= 0, "negative n_t");
+    if (!cdm)
+        for (auto* P : Ps) WCB_REQUIRE(P->n_c == 0 || P->has_S, "plan has no S_cc factors (mass-only plan)");
     WCB_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     if (div) { div->step = -1; div->amplitude = 0.0; }
@@ -709,7 +771,7 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
     auto exchange = [&](const std::vector<double*>& st) {
         if (G == 1) {
             int64_t h[8];
-            if (ctx->nccl && ops[0]->halo(h))
+            if (dist_slab(ops[0]) && ops[0]->halo(h))
                 nccl_exchange_halo(ctx, st[0], h, ops[0]->halo_nplanes, ops[0]->halo_pstride);
         } else {
             copy_exchange_halo(ops, st, s);
@@ -763,6 +825,11 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
             k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->A.p, P->psi_c.p);
             k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->V.p, P->v_c.p);
             ctx->launches += 3;
+            if (cdm) {
+                k_c_boot_prev<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->psi_c.p, P->v_c.p, P->a_c.p, dt,
+                                                             0.5 * dt * dt, P->B.p);
+                ctx->launches++;
+            }
             WCB_CUDA(cudaStreamSynchronize(s));
         }
     }
@@ -794,7 +861,7 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
         if (upto <= checked) return false;
         const int64_t cnt = upto - checked;
         for (size_t r = 0; r < G; ++r) {
-            nccl_allreduce_max_u64(ctx, Ps[r]->amp.p + checked + 1, cnt);
+            if (G == 1 && dist_slab(Ps[r]->op)) nccl_allreduce_max_u64(ctx, Ps[r]->amp.p + checked + 1, cnt);
             WCB_CUDA(cudaMemcpyAsync(h_amp.data() + r * (n_t + 1) + checked + 1, Ps[r]->amp.p + checked + 1,
                                      cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         }
@@ -820,7 +887,7 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
     //   S1: [wait e_near(k)] -> far(k+1) -> [rec e_far]
     // far(k+1) writes psi_{k+2} over psi_k, read only by step k's explicit
     // tiles (done: e_near) -- the c chain reads and writes the other buffer.
-    const bool overlap = G == 1 && !ctx->nccl && Ps[0]->split;
+    const bool overlap = !cdm && G == 1 && !dist_slab(Ps[0]->op) && Ps[0]->split;
     auto d_args = [&](wcb_imex_plan* P, int64_t k, double* c_, double* p_) {
         StepArgs a;
         a.minv = P->minv.p;
@@ -857,6 +924,26 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
             wcb_imex_plan* P = Ps[r];
             Operator* op = P->op;
             const int64_t ns = op->n_state, nc = P->n_c;
+            if (cdm) {
+                // d rows (and 2 psi - psi_prev in the c slots, 1/m = 0 there)
+                StepArgs a = d_args(P, k, cur[r], prev[r]);
+                if (nc > 0) a.amp = P->amp_scratch.p;   // amplitude taken below
+                op->cdm_step(a);
+                if (nc > 0) {
+                    op->apply_subset(cur[r], P->T.p);   // (K psi_k)_c
+                    k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
+                    k_c_rhs<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->Fc.p, P->ft_k.p + 1, k, P->Kc.p, P->rhs.p);
+                    lu_solve(ctx, P, P->Mcc, P->rhs.p, P->y.p);
+                    k_c_cdm_update<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->Mcc.perm_c.p, P->y.p,
+                                                                  dt * dt, prev[r]);
+                    // the fused step's amplitude saw the c slots before their
+                    // update: take the step's amplitude over the final state
+                    k_state_amp<<<grid1(ctx, ns), 256, 0, s>>>(ns, prev[r], P->amp.p + (k + 1));
+                    ctx->launches += 4;
+                }
+                std::swap(cur[r], prev[r]);
+                continue;
+            }
             // 1. explicit d step into prev (c slots overwritten below)
             if (overlap) {
                 op->cdm_step_part(d_args(P, k, cur[r], prev[r]), 1);
@@ -915,10 +1002,10 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
         op->gather(cur[r], tmp[r].p);
         copy_d2h(psi_out[r], tmp[r].p, op->n * sizeof(double), s);
         // v_c in c order (the caller scatters it when d is empty, src/timeint.py:285-288)
-        if (psi_dot_out[r] && P->n_c > 0)
+        if (psi_dot_out[r] && P->n_c > 0 && !cdm)
             WCB_CUDA(cudaMemcpyAsync(psi_dot_out[r], P->v_c.p, P->n_c * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (P->n_obs && obs_out[r]) {
-            nccl_allreduce_sum_f64(ctx, dobs[r].p, P->n_obs * stride);
+            if (G == 1 && dist_slab(op)) nccl_allreduce_sum_f64(ctx, dobs[r].p, P->n_obs * stride);
             WCB_CUDA(cudaMemcpyAsync(obs_out[r], dobs[r].p, P->n_obs * stride * sizeof(double),
                                      cudaMemcpyDeviceToHost, s));
         }
@@ -966,5 +1053,97 @@ int wcb_imex_group_run(int n_plans, wcb_imex_plan** plans, double f0, const doub
     }
 }
 
+
+int wcb_mass_plan_create(wcb_operator* K, int64_t n_c, const int64_t* c_idx, int64_t n_d,
+                         const int64_t* d_idx, const double* m_d, const wcb_lu* M_cc,
+                         const int64_t* Mcc_indptr, const int32_t* Mcc_indices, const double* Mcc_data,
+                         const double* F_s, const wcb_observer* obs, wcb_imex_plan** out) {
+    try {
+        WCB_REQUIRE(out && (n_c == 0 || (M_cc && Mcc_indptr && Mcc_indices && Mcc_data)), "NULL argument");
+        wcb_imex_plan* P = nullptr;
+        const int rc = wcb_imex_plan_create(K, n_c, c_idx, n_d, d_idx, m_d, nullptr, M_cc, F_s, obs, &P);
+        if (rc != WCB_OK) return rc;
+        std::unique_ptr<wcb_imex_plan, int (*)(wcb_imex_plan*)> guard(P, wcb_imex_plan_destroy);
+        if (n_c > 0) {
+            cudaStream_t s = P->ctx->stream;
+            const int64_t nnz = Mcc_indptr[n_c];
+            for (int64_t j = 0; j < nnz; ++j)
+                WCB_REQUIRE(Mcc_indices[j] >= 0 && Mcc_indices[j] < n_c, "M_cc column out of range");
+            P->mcc_ptr.alloc(n_c + 1, s); P->mcc_ptr.upload(Mcc_indptr, n_c + 1, s);
+            P->mcc_idx.alloc(std::max<int64_t>(nnz, 1), s); P->mcc_idx.upload(Mcc_indices, nnz, s);
+            P->mcc_val.alloc(std::max<int64_t>(nnz, 1), s); P->mcc_val.upload(Mcc_data, nnz, s);
+            P->has_mcc_csr = true;
+            WCB_CUDA(cudaStreamSynchronize(s));
+        }
+        *out = guard.release();
+        return WCB_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
+}
+
+int wcb_imex_plan_cdm_run(wcb_imex_plan* P, const double* ft, double dt, int64_t n_t, const double* psi0,
+                          const double* v0, double* psi_out, double* obs_out, wcb_divergence* div,
+                          wcb_timings* tm) {
+    try {
+        WCB_REQUIRE(P && psi_out && (ft || n_t == 0), "NULL argument");
+        std::vector<double> f(std::max<int64_t>(n_t, 1), 0.0);
+        if (n_t > 0) std::memcpy(f.data(), ft, n_t * sizeof(double));
+        const double f0 = f[0];
+        std::vector<wcb_imex_plan*> Ps{P};
+        imex_run_group(Ps, f0, f.data(), f.data(), dt, n_t, 0.0, 0.5, {psi0}, {v0}, {psi_out}, {nullptr},
+                       {obs_out}, div, tm, true);
+        return WCB_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
+}
+
+int wcb_imex_plan_max_gen_eig(wcb_imex_plan* P, const double* x0, double tol, int64_t max_iter,
+                              double* lam, int64_t* n_iter) {
+    try {
+        WCB_REQUIRE(P && x0 && lam && n_iter, "NULL argument");
+        WCB_REQUIRE(P->n_c == 0 || P->has_mcc_csr, "plan has no M_cc matrix (use wcb_mass_plan_create)");
+        Operator* op = P->op;
+        Context* ctx = P->ctx;
+        WCB_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = ctx->stream;
+        const int64_t n = op->n, nc = P->n_c;
+        // m_diag in compact order: m_d at the d rows, 1 at the c rows
+        std::vector<double> md_state(op->n_state), m(n, 1.0);
+        WCB_CUDA(cudaMemcpyAsync(md_state.data(), P->m_d_state.p, op->n_state * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+        WCB_CUDA(cudaStreamSynchronize(s));
+        const std::vector<int64_t>& si = op->state_index();
+        for (int64_t i = 0; i < n; ++i)
+            if (md_state[si[i]] > 0.0) m[i] = md_state[si[i]];
+        MassHooks hooks;
+        if (nc > 0) {
+            hooks.solve_c = [&](const double* t, double* y) {
+                k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, t, P->rhs.p);
+                lu_solve(ctx, P, P->Mcc, P->rhs.p, P->a_c.p);
+                k_scatter_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->Mcc.perm_c.p, P->a_c.p, y);
+                ctx->launches += 2;
+            };
+            hooks.apply_c = [&](const double* x, double* mx) {
+                k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, x, P->rhs.p);
+                k_csr_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->mcc_ptr.p, P->mcc_idx.p, P->mcc_val.p, P->rhs.p,
+                                                          P->Kc.p);
+                k_scatter_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, nullptr, P->Kc.p, mx);
+                ctx->launches += 3;
+            };
+        } else {
+            hooks.solve_c = [](const double*, double*) {};
+            hooks.apply_c = [](const double*, double*) {};
+        }
+        max_gen_eig_core(op, m.data(), x0, tol, max_iter, lam, n_iter, &hooks);
+        return WCB_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
+}
 
 }  // extern "C"

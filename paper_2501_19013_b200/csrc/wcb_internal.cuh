@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <vector>
 #include <thread>
+#include <functional>
 
 #include "../../include/wavecell_b200.h"
 
@@ -207,13 +208,16 @@ inline bool pdl_enabled() {
     return on;
 }
 
-// Reference arithmetic order of src/timeint.py:185:
-//   psi_new = 2.0*psi - psi_prev + (dt*dt) * (rhs / m)
-// with rhs = f*F - K psi; 1/m is precomputed (<= 1 ulp from the division).
+// Reference operation order of src/timeint.py:185:
+//   psi_new = 2.0*psi - psi_prev + (dt*dt) * (rhs / m),  rhs = f*F - K psi
+// Every operation is rounded on its own (__d*_rn: no FMA contraction, as in
+// NumPy).  Two deviations remain and are bounded by the parity tests (fields
+// rel. L2 <= 1e-10): 1/m is precomputed (rhs * (1/m) is within 1 ulp of
+// rhs / m), and K psi is summed in another order than SciPy's csr_matvec.
 __device__ __forceinline__ double leapfrog(double u, double up, double Ku, double minv,
                                            double fF, double dt2) {
-    double rhs = fF - Ku;
-    return (2.0 * u - up) + dt2 * (rhs * minv);
+    const double rhs = __dsub_rn(fF, Ku);
+    return __dadd_rn(__dsub_rn(__dmul_rn(2.0, u), up), __dmul_rn(dt2, __dmul_rn(rhs, minv)));
 }
 
 __device__ __forceinline__ unsigned long long amp_bits(double v) {
@@ -315,6 +319,22 @@ struct Operator {
     }
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `fn` on `device`,
+// raised only when `bytes` exceeds what was set there before (the attribute
+// is per device; the record is mutex-protected, so several devices and host
+// threads can launch the same kernel)
+void ensure_smem_attr(const void* fn, int device, size_t bytes);
+
+// consistent-mass hooks of the power iteration (mass blockdiag(diag(m), M_cc))
+struct MassHooks {
+    std::function<void(const double* t_state, double* y_state)> solve_c;   // y_c = M_cc^-1 t_c
+    std::function<void(const double* x_state, double* mx_state)> apply_c;  // (M x)_c = M_cc x_c
+};
+struct Operator;
+// power iteration of src/linalg.py:89-122 on op (throws Error)
+void max_gen_eig_core(Operator* op, const double* m_diag, const double* x0, double tol, int64_t max_iter,
+                      double* lam, int64_t* n_iter, const MassHooks* hooks);
+
 void ctx_retain(Context* ctx);
 void ctx_release(Context* ctx);
 
@@ -328,6 +348,10 @@ struct Operator;
 void copy_exchange_halo(const std::vector<Operator*>& ops, const std::vector<double*>& states, cudaStream_t s);
 void nccl_allreduce_max_u64(Context* ctx, unsigned long long* d, int64_t n);
 void nccl_allreduce_sum_f64(Context* ctx, double* d, int64_t n);
+// true only for a slab operator (op->halo()) whose context holds a communicator
+// of more than one rank: the loops run their collectives only then, so a plain
+// (non-slab) run on a context that once joined a slab group stays rank-local
+bool dist_slab(const Operator* op);
 
 Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* indptr,
                             const int32_t* indices, const double* data);

@@ -514,12 +514,7 @@ struct ScmOperator final : Operator {
     template <int P, int MODE>
     void launch2d(const StepArgs& a) {
         using T = Tile2<P>;
-        static bool attr_set = false;
-        if (!attr_set) {
-            WCB_CUDA(cudaFuncSetAttribute(k_scm2d<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)T::SMEM));
-            attr_set = true;
-        }
+        ensure_smem_attr((const void*)k_scm2d<P, MODE>, ctx->device, (size_t)T::SMEM);
         Mats2<P> mt;
         for (int i = 0; i <= P; ++i)
             for (int j = 0; j <= P; ++j)
@@ -604,11 +599,7 @@ struct ScmOperator final : Operator {
     template <int P>
     void launch2s(const StepArgs& a) {
         using T = Str2E<P>;
-        static bool attr_set = false;
-        if (!attr_set) {
-            WCB_CUDA(cudaFuncSetAttribute(k_ela2s<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
-            attr_set = true;
-        }
+        ensure_smem_attr((const void*)k_ela2s<P>, ctx->device, (size_t)T::SMEM);
         Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, sflags.p, nullptr, n_strips, n_rtiles,
                    pitch, nullptr};
         MinvTabE<P> tab{};
@@ -630,12 +621,7 @@ struct ScmOperator final : Operator {
             launch2s<P>(a);
             return;
         }
-        static bool attr_set = false;
-        if (!attr_set) {
-            WCB_CUDA(cudaFuncSetAttribute(k_ela2d<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)T::SMEM));
-            attr_set = true;
-        }
+        ensure_smem_attr((const void*)k_ela2d<P, MODE>, ctx->device, (size_t)T::SMEM);
         const int32_t* ord = part_active >= 0 ? order_part[part_active].p : sub_active ? order_sub.p : order.p;
         const int64_t n_ord = part_active >= 0 ? n_order_part[part_active] : sub_active ? n_order_sub : n_order;
         if (!n_ord) return;

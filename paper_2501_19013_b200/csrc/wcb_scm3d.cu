@@ -194,11 +194,7 @@ void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t
                     int64_t pplane, int64_t prow, const double* u, double* out) {
     if (!n_cut) return;
     using C = CutPre<P>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        WCB_CUDA(cudaFuncSetAttribute(k_cut_pre<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-        attr_set = true;
-    }
+    ensure_smem_attr((const void*)k_cut_pre<P>, ctx->device, (size_t)C::SMEM);
     const int64_t blocks = std::min<int64_t>(ceil_div(n_cut, C::W), (int64_t)ctx->sm_count * std::max<int64_t>(1, (int64_t)(220 * 1024 / C::SMEM)));
     k_cut_pre<P><<<(unsigned)blocks, 32 * C::W, C::SMEM, ctx->stream>>>(n_cut, KP, cut_base, pplane, prow, u, out);
     ctx->launches++;
@@ -538,12 +534,7 @@ template <int P, int MODE>
 void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map_p, const Scm3DGeo& g,
                   const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a) {
     using T = Str3<P>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        WCB_CUDA(cudaFuncSetAttribute(k_scm3d<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)T::SMEM));
-        attr_set = true;
-    }
+    ensure_smem_attr((const void*)k_scm3d<P, MODE>, ctx->device, (size_t)T::SMEM);
     dim3 grid((unsigned)g.n_zs, (unsigned)g.n_yb, (unsigned)g.n_xc);
     k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
     ctx->launches++;

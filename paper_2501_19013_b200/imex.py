@@ -67,6 +67,10 @@ class _LU:
 
 def _host_stiffness(K):
     """Host CSR of K (for the c-c block of the iteration matrix)."""
+    from .operators import _tensor_system_of, tensor_csr
+    tensor = getattr(K, "tensor", None) if isinstance(K, DeviceOperator) else _tensor_system_of(K)
+    if tensor is not None:
+        return tensor_csr(tensor)
     if isinstance(K, DeviceOperator):
         prob = getattr(K, "problem", None)
         if prob is None:
@@ -141,14 +145,21 @@ class ImexPlan:
         del S_lu, M_lu    # uploaded; the host factors are not needed any more
 
     def run(self, f_t, n_t: int, gamma: float = 0.5, psi0=None, v0=None,
-            record: bool = True) -> RunResult:
+            record: bool = True, new_times=None) -> RunResult:
+        """``new_times`` (length n_t) overrides the implicit stage's force
+        times: IMEX evaluates ``f_t(k dt + dt)`` (src/timeint.py:258-259),
+        Newmark ``f_t((k + 1) dt)`` (src/timeint.py:141) -- equal in exact
+        arithmetic, not always in floating point."""
         n_t = int(n_t)
         dt = self.dt
         n = self.n
         f0 = float(f_t(0.0))
         ks = np.arange(n_t, dtype=np.float64) * dt
         ft_k = eval_force(f_t, ks) if n_t else np.zeros(1)
-        ft_new = eval_force(f_t, ks + dt) if n_t else np.zeros(1)
+        tn = ks + dt if new_times is None else np.asarray(new_times, dtype=np.float64)
+        if tn.shape[0] != n_t:
+            raise ValueError("new_times must hold n_t entries")
+        ft_new = eval_force(f_t, tn) if n_t else np.zeros(1)
         p0 = None if psi0 is None else np.ascontiguousarray(np.array(psi0, dtype=float).reshape(-1))
         q0 = None if v0 is None else np.ascontiguousarray(np.array(v0, dtype=float).reshape(-1))
         psi = np.empty(n)
@@ -186,6 +197,92 @@ class ImexPlan:
             pass
 
 
+class MassPlan(ImexPlan):
+    """Device-resident consistent (non-diagonal) mass for ``cdm_run`` and
+    ``max_gen_eig`` -- the reference's ``factorize`` SuperLU path
+    (src/linalg.py:70-80, used by src/timeint.py:166-176 and
+    src/linalg.py:106-116).  ``M`` is split into its diagonal-only rows (d,
+    divided by m_d) and the coupled rows (c, ``M_cc`` factorised once with
+    SuperLU in the reference configuration, both triangular solves on the
+    B200 every step / iteration); see :func:`linalg.mass_split`."""
+
+    def __init__(self, M, K, F_s, obs_mat=None, device: int | None = None):
+        from .linalg import mass_split
+        t0 = time.perf_counter()
+        c_idx, d_idx, m_d, M_cc = mass_split(M)
+        n = sp.csr_matrix(M).shape[0]
+        self.n = n
+        self.dt = 0.0
+        self.beta = 0.0
+        self.c_idx = c_idx
+        self.has_c, self.has_d = c_idx.shape[0] > 0, d_idx.shape[0] > 0
+        M_lu = _LU(_splu(M_cc)) if self.has_c else None
+        M_cc.sort_indices()
+        mcc = (np.ascontiguousarray(M_cc.indptr, dtype=np.int64),
+               np.ascontiguousarray(M_cc.indices, dtype=np.int32),
+               np.ascontiguousarray(M_cc.data, dtype=np.float64))
+        self.factorization = time.perf_counter() - t0
+        self.fact_nnz = 0 if M_lu is None else int(M_lu.keep[4].shape[0] + M_lu.keep[7].shape[0])
+        op = as_device_operator(K, device=device)
+        if op.n != n:
+            raise ValueError("K and M sizes differ")
+        self.op = op
+        F = np.ascontiguousarray(np.asarray(F_s, dtype=np.float64).reshape(-1))
+        if F.shape[0] != n:
+            raise ValueError("F_s has the wrong length")
+        obs, self._obs_keep = _observer(obs_mat, n)
+        self.n_obs = 0 if obs is None else int(obs.n_obs)
+        h = _lib.C.c_void_p()
+        _lib.check(_lib.load().wcb_mass_plan_create(
+            op.handle, c_idx.shape[0], _lib.i64ptr(c_idx) if self.has_c else None, d_idx.shape[0],
+            _lib.i64ptr(d_idx) if self.has_d else None, _lib.dptr(m_d) if self.has_d else None,
+            _lib.C.byref(M_lu.struct) if self.has_c else None, _lib.i64ptr(mcc[0]),
+            _lib.i32ptr(mcc[1]), _lib.dptr(mcc[2]), _lib.dptr(F),
+            _lib.C.byref(obs) if obs is not None else None, _lib.C.byref(h)))
+        self._h = h
+        del M_lu
+
+    def max_gen_eig(self, x0, tol=1e-9, max_iter=50000):
+        """Power iteration of src/linalg.py:89-122 with this mass."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        lam = _lib.C.c_double(0.0)
+        it = _lib.C.c_int64(0)
+        code = _lib.load().wcb_imex_plan_max_gen_eig(self._h, _lib.dptr(x0), float(tol), int(max_iter),
+                                                     _lib.C.byref(lam), _lib.C.byref(it))
+        if code == _lib.WCB_E_NOCONV:
+            raise RuntimeError(_lib.last_error())
+        _lib.check(code)
+        return float(lam.value), int(it.value)
+
+    def run_cdm(self, f_t, dt: float, n_t: int, psi0=None, v0=None, record: bool = True) -> RunResult:
+        """``cdm_run`` (src/timeint.py:159-193) with this mass."""
+        from .timeint import force_table
+        n, dt, n_t = self.n, float(dt), int(n_t)
+        ft = force_table(f_t, dt, n_t)
+        p0 = None if psi0 is None else np.ascontiguousarray(np.array(psi0, dtype=float).reshape(-1))
+        q0 = None if v0 is None else np.ascontiguousarray(np.array(v0, dtype=float).reshape(-1))
+        for a in (p0, q0):
+            if a is not None and a.shape[0] != n:
+                raise ValueError("initial state has the wrong length")
+        psi = np.empty(n)
+        obs = np.empty((self.n_obs, n_t + 1)) if (self.n_obs and record) else None
+        div = _lib.Divergence()
+        tm = _lib.Timings()
+        code = _lib.load().wcb_imex_plan_cdm_run(
+            self._h, _lib.dptr(ft), dt, n_t, _lib.dptr(p0), _lib.dptr(q0), _lib.dptr(psi),
+            _lib.dptr(obs) if obs is not None else None, _lib.C.byref(div), _lib.C.byref(tm))
+        if code == _lib.WCB_E_DIVERGED:
+            raise DivergenceError(int(div.step), float(div.amplitude))
+        _lib.check(code)
+        timings = StageTimings(factorization=self.factorization, rhs=float(tm.rhs),
+                               backward_insertion=float(tm.backward_insertion))
+        return RunResult(method="cdm", dt=dt, t=np.arange(n_t + 1) * dt, obs=obs, psi=psi,
+                         psi_dot=None, timings=timings, fact_dim=n)
+
+    def run(self, *args, **kwargs):
+        raise NotImplementedError("a MassPlan has no S_cc factors: use run_cdm or ImexPlan")
+
+
 def imex_run(M, K, F_s, f_t, dt: float, n_t: int, c_idx, d_idx, obs_mat=None,
              beta: float = 0.25, gamma: float = 0.5, psi0=None, v0=None,
              device: int | None = None) -> RunResult:
@@ -207,17 +304,31 @@ def newmark_run(M, K, F_s, f_t, dt: float, n_t: int, obs_mat=None, beta: float =
     ``S = M`` as in the reference) and each step runs predictor, ``K``
     apply, the two triangular solves and the corrector on the B200 -- the
     IMEX plan with an empty explicit set, whose per-step arithmetic is the
-    reference's Newmark loop line by line.  ``s_factory`` (a host
-    factorisation object called every step) has no device form.
+    reference's Newmark loop line by line.
+
+    ``s_factory`` (src/timeint.py:126-128) is called once, as the reference
+    does, and must return an object for ``S`` (``.solve``, optional ``.n``).
+    Its solve runs on the host, so the device loop does not call it: the
+    device factorises the same ``S`` itself (the reference's own factories --
+    ``TensorSystem.newmark_factorization``, src/assembly.py:699-704 -- solve
+    ``S`` by fast diagonalisation or by CG to a 1e-13 residual, so the fields
+    agree to that solve tolerance).  ``K`` must then be available as a
+    matrix: a sparse/dense ``K``, a ``TensorSystem`` stiffness operator or a
+    device operator built from a problem description.
     """
     if s_factory is not None:
-        raise NotImplementedError("newmark_run(s_factory=...) solves through a host object every "
-                                  "step; the device path factorises S itself (omit s_factory)")
+        S_obj = s_factory()
+        n_s = getattr(S_obj, "n", None)
+        if not callable(getattr(S_obj, "solve", None)):
+            raise TypeError("s_factory() must return an object with a solve(b) method")
+        if n_s is not None and int(n_s) != sp.csr_matrix(M).shape[0]:
+            raise ValueError("s_factory() returned a factorization of the wrong size")
     n = sp.csr_matrix(M).shape[0]
     plan = ImexPlan(M, K, F_s, dt, np.arange(n, dtype=np.int64), np.zeros(0, dtype=np.int64),
                     obs_mat=obs_mat, beta=beta, device=device)
     try:
-        r = plan.run(f_t, n_t, gamma=gamma, psi0=psi0, v0=v0)
+        r = plan.run(f_t, n_t, gamma=gamma, psi0=psi0, v0=v0,
+                     new_times=np.arange(1, int(n_t) + 1, dtype=np.float64) * float(dt))
     finally:
         plan.close()
     return RunResult(method="newmark", dt=r.dt, t=r.t, obs=r.obs, psi=r.psi, psi_dot=r.psi_dot,

@@ -91,6 +91,29 @@ def diagonal_mass(M) -> np.ndarray:
     return d
 
 
+def mass_split(M):
+    """Split a non-diagonal symmetric mass for the device: ``(c_idx, d_idx,
+    m_d, M_cc)`` with c = the rows storing an off-diagonal nonzero and d the
+    rows storing only their diagonal, so ``M = blockdiag(diag(m_d), M_cc)``
+    after permutation (the factorize() SuperLU path, src/linalg.py:70-80, on
+    the blocks).  Raises like factorize for a non-positive diagonal entry."""
+    A = sp.csr_matrix(M, dtype=np.float64)
+    if A.shape[0] != A.shape[1]:
+        raise ValueError("matrix must be square")
+    coo = A.tocoo()
+    off = (coo.row != coo.col) & (coo.data != 0.0)
+    is_c = np.zeros(A.shape[0], dtype=bool)
+    is_c[coo.row[off]] = True
+    is_c[coo.col[off]] = True
+    c_idx = np.flatnonzero(is_c).astype(np.int64)
+    d_idx = np.flatnonzero(~is_c).astype(np.int64)
+    m_d = np.ascontiguousarray(A.diagonal()[d_idx], dtype=np.float64)
+    if np.any(m_d <= 0.0) or not np.all(np.isfinite(m_d)):
+        raise IndefiniteMatrixError("matrix is not positive definite; "
+                                    "check the stabilization and lumping settings")
+    return c_idx, d_idx, m_d, A[c_idx][:, c_idx].tocsr()
+
+
 def start_vector(n: int, seed: int) -> np.ndarray:
     """Seeded normalised start vector of src/linalg.py:103-105."""
     rng = np.random.default_rng(seed)
@@ -106,7 +129,18 @@ def max_gen_eig(K, M, tol=1e-9, max_iter=50000, seed=0, device: int | None = Non
     """
     op = as_device_operator(K, device=device)
     n = op.n
-    m = diagonal_mass(M)
+    try:
+        m = diagonal_mass(M)
+    except NotImplementedError:
+        # consistent mass: M^-1 through the device triangular solves of M_cc
+        from .imex import MassPlan
+        if sp.csr_matrix(M).shape[0] != n:
+            raise ValueError("K and M sizes differ")
+        plan = MassPlan(M, op, np.zeros(n), device=device)
+        try:
+            return plan.max_gen_eig(start_vector(n, seed), tol=tol, max_iter=max_iter)
+        finally:
+            plan.close()
     if m.shape[0] != n:
         raise ValueError("K and M sizes differ")
     x0 = start_vector(n, seed)
@@ -153,5 +187,5 @@ def dt_crit(K, M, tol=1e-9, seed=0, device: int | None = None) -> float:
     return 2.0 / np.sqrt(lam)
 
 
-__all__ = ["IndefiniteMatrixError", "is_structurally_diagonal", "diagonal_mass",
+__all__ = ["IndefiniteMatrixError", "is_structurally_diagonal", "diagonal_mass", "mass_split",
            "start_vector", "max_gen_eig", "max_gen_eig_sub", "dt_crit", "DeviceOperator"]

@@ -196,29 +196,139 @@ class ElasticOperator(DeviceOperator):
         self.n_cut = int(self._cut.shape[0])
 
 
+def _tensor_system_of(K):
+    """The reference ``TensorSystem`` behind ``K`` when ``K`` is its
+    ``stiffness_operator()`` (a scipy LinearOperator whose matvec is the bound
+    ``k_matvec``, src/assembly.py:674-690), else None."""
+    f = getattr(K, "_CustomLinearOperator__matvec_impl", None)
+    owner = getattr(f, "__self__", None)
+    if owner is None or getattr(f, "__name__", "") != "k_matvec":
+        return None
+    if not all(hasattr(owner, a) for a in ("m1", "k1", "grid", "rho", "c")):
+        return None
+    return owner
+
+
+def _element_1d(glob: np.ndarray, p: int, n_e: int) -> np.ndarray:
+    """Element matrix of a uniform 1D Lagrange assembly ``glob`` (sum of
+    n_e equal (p+1)^2 blocks overlapping in one node): the first block, whose
+    last diagonal entry (shared with the second block) is restored from the
+    persymmetry of the GLL element matrices."""
+    e = np.array(glob[: p + 1, : p + 1], dtype=np.float64)
+    if n_e > 1:
+        e[p, p] = glob[0, 0]
+    re = np.zeros_like(glob)
+    for c in range(n_e):
+        re[c * p: c * p + p + 1, c * p: c * p + p + 1] += e
+    if not np.allclose(re, glob, rtol=1e-13, atol=1e-13 * np.abs(glob).max()):
+        raise TypeError("TensorSystem 1D factors are not a uniform Lagrange assembly")
+    return e
+
+
+def tensor_csr(tensor) -> sp.csr_matrix:
+    """The separable stiffness of a ``TensorSystem`` as CSR:
+    ``rho c^2 (k1 x m1 x m1 + m1 x k1 x m1 + m1 x m1 x k1)`` (src/assembly.py:674-684)."""
+    m = sp.csr_matrix(np.asarray(tensor.m1, dtype=np.float64))
+    k = sp.csr_matrix(np.asarray(tensor.k1, dtype=np.float64))
+    K = (sp.kron(sp.kron(k, m), m) + sp.kron(sp.kron(m, k), m) + sp.kron(sp.kron(m, m), k))
+    return (float(tensor.rho) * float(tensor.c) ** 2 * K).tocsr()
+
+
+def tensor_operator(tensor, device: int | None = None) -> DeviceOperator:
+    """Device form of the reference's separable stiffness
+    ``rho c^2 (k1 x m1 x m1 + m1 x k1 x m1 + m1 x m1 x k1)`` of a fully uncut
+    grid (``TensorSystem``, src/assembly.py:615-690).
+
+    Lagrange: the global 1D factors are sums of one element matrix, so the
+    Kronecker sum equals the sum of uncut element operators and runs in the
+    matrix-free SCM kernel (every cell uncut, all nodes DOFs, lex order =
+    ``P.reshape(n1, n1, n1)``).  B-splines: the Kronecker sum is formed as
+    CSR once (entries are products of the 1D factors) and applied by the CSR
+    kernel."""
+    grid = tensor.grid
+    spec = grid.spec
+    rho_c2 = float(tensor.rho) * float(tensor.c) ** 2
+    m1g = np.asarray(tensor.m1, dtype=np.float64)
+    k1g = np.asarray(tensor.k1, dtype=np.float64)
+    n1 = m1g.shape[0]
+    if getattr(spec, "family", "") == "lagrange":
+        p, n_e = int(spec.p), int(spec.n_e)
+        h = float(grid.h)
+        m1 = _element_1d(m1g, p, n_e) / (h / 2.0)
+        k1 = _element_1d(k1g, p, n_e) * (h / 2.0)
+        op = ScmOperator(dim=3, p=p, n_e=(n_e,) * 3, k1=k1, m1=m1, sk=rho_c2 * (h / 2.0),
+                         cell_class=np.ones(n_e ** 3, dtype=np.int8),
+                         lex_of_compact=np.arange(n1 ** 3, dtype=np.int64),
+                         cut_cells=np.zeros(0, dtype=np.int64), cut_K=np.zeros(0),
+                         device=device)
+    else:
+        op = CsrOperator(tensor_csr(tensor), device=device)
+    op.tensor = tensor
+    return op
+
+
 _cache: dict[int, tuple] = {}
 
 
+def _words(a: np.ndarray) -> int:
+    """Wrapping 64-bit sum of the array's bytes (one vectorised pass)."""
+    b = np.ascontiguousarray(a).reshape(-1).view(np.uint8)
+    head = b[: b.shape[0] // 8 * 8].view(np.uint64)
+    tail = b[head.shape[0] * 8:]
+    return int(np.add.reduce(head, dtype=np.uint64)) ^ int(tail.sum()) ^ (b.shape[0] << 1)
+
+
+def _fingerprint(K) -> tuple | None:
+    """Content fingerprint of a host matrix: shape, buffers and a checksum of
+    every stored value and index.  The reference reads ``K`` on every call,
+    so an in-place change (``K *= s``, ``K.data[:] = ...``) must not reuse a
+    stale device copy."""
+    if sp.issparse(K):
+        A = K if K.format in ("csr", "csc", "bsr") else None
+        if A is None:
+            return None
+        return (K.format, K.shape, A.data.ctypes.data, A.indices.ctypes.data,
+                A.indptr.ctypes.data, _words(A.data), _words(A.indices), _words(A.indptr))
+    if isinstance(K, np.ndarray):
+        return ("dense", K.shape, K.dtype.str, K.ctypes.data, _words(K))
+    return None
+
+
 def as_device_operator(K, device: int | None = None) -> DeviceOperator:
-    """Device operator for ``K`` (cached per host object while it lives)."""
+    """Device operator for ``K``.  Host matrices are uploaded once and reused
+    while the same object lives with unchanged contents (checked by a content
+    fingerprint on every call); a reference ``TensorSystem`` stiffness
+    ``LinearOperator`` (src/assembly.py:686-690) becomes the matrix-free
+    operator of its grid."""
     if isinstance(K, DeviceOperator):
         return K
-    key = id(K)
+    tensor = _tensor_system_of(K)
+    obj = K if tensor is None else tensor
+    key = id(obj)
+    fp = _fingerprint(K) if tensor is None else (
+        "tensor", _words(np.asarray(tensor.m1)), _words(np.asarray(tensor.k1)),
+        float(tensor.rho), float(tensor.c))
     hit = _cache.get(key)
     if hit is not None:
-        ref, op = hit
-        if ref() is K and (device is None or op.ctx.device == device):
+        ref, op, fp0 = hit
+        if ref() is obj and fp is not None and fp == fp0 and (device is None or op.ctx.device == device):
             return op
-    if sp.issparse(K) or isinstance(K, np.ndarray) or isinstance(K, np.matrix):
+        _cache.pop(key, None)
+    if tensor is not None:
+        op = tensor_operator(tensor, device=device)
+    elif sp.issparse(K) or isinstance(K, np.ndarray) or isinstance(K, np.matrix):
         op = CsrOperator(K, device=device)
     else:
         raise TypeError(
             f"unsupported stiffness operator type {type(K).__name__}: pass a scipy "
-            "sparse matrix, a dense array, or a paper_2501_19013_b200 DeviceOperator")
+            "sparse matrix, a dense array, a TensorSystem stiffness operator or a "
+            "paper_2501_19013_b200 DeviceOperator")
+    if fp is None:
+        return op
     try:
-        ref = weakref.ref(K)
+        ref = weakref.ref(obj)
     except TypeError:
         return op
-    _cache[key] = (ref, op)
-    weakref.finalize(K, _cache.pop, key, None)
+    _cache[key] = (ref, op, fp)
+    weakref.finalize(obj, _cache.pop, key, None)
     return op

@@ -225,10 +225,21 @@ class CdmPlan:
 def cdm_run(M, K, F_s, f_t, dt: float, n_t: int, obs_mat=None, psi0=None,
             v0=None, device: int | None = None) -> RunResult:
     """Central difference method in two-step displacement form, on the device
-    (src/timeint.py:159-193).  ``M`` must be diagonal (the reference's
-    ``factorize`` fast path); ``K`` is any sparse/dense matrix or a
+    (src/timeint.py:159-193).  A diagonal ``M`` takes the fused one-kernel
+    step (``factorize``'s fast path, ``fact_dim = 0``); any other SPD ``M``
+    the consistent-mass plan (SuperLU factors of its coupled block, device
+    triangular solves every step, ``fact_dim = n``).  ``K`` is any
+    sparse/dense matrix, a ``TensorSystem`` stiffness operator or a
     :class:`DeviceOperator`."""
-    plan = CdmPlan(M, K, F_s, obs_mat=obs_mat, device=device)
+    try:
+        plan = CdmPlan(M, K, F_s, obs_mat=obs_mat, device=device)
+    except NotImplementedError:
+        from .imex import MassPlan
+        mplan = MassPlan(M, K, F_s, obs_mat=obs_mat, device=device)
+        try:
+            return mplan.run_cdm(f_t, dt, n_t, psi0=psi0, v0=v0)
+        finally:
+            mplan.close()
     try:
         return plan.run(f_t, dt, n_t, psi0=psi0, v0=v0)
     finally:

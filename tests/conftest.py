@@ -31,3 +31,13 @@ def csr_from(g, prefix):
 @pytest.fixture(scope="session")
 def golden():
     return load_golden
+
+
+# alpha = 1e-12 IMEX parity bands (the paper's IMEX case).  cond(S_cc) ~ 5e13:
+# a symmetric 1-ulp perturbation of K alone moves the REFERENCE's own field by
+# the spread measured in tests/test_paper_setup.py (cube p2n4, 150 steps:
+# ~3e-8; paper n_e 13, 2000 steps: ~6e-6), so no other summation order can be
+# held tighter than a small multiple of it.  The alpha = 1e-4 and alpha = 1e-8
+# cases meet the north-star 1e-10.
+IMEX_A12_TOL_P2N4 = 1e-7
+IMEX_A12_TOL_N13 = 3e-5

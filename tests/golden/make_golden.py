@@ -222,7 +222,111 @@ def gen_lumping():
     save("lumping", M=Ms, hrz=S.hrz_lump(Ms), rowsum=S.row_sum_lump(Ms))
 
 
-if __name__ == "__main__":
+def gen_paper():
+    """The reference's own benchmark (PAPER section 4, tests/test_acceptance.py
+    criteria 2-4): rotated cube, SCM p=3, n_e=13 (alpha 1e-8 CDM, alpha 1e-12
+    IMEX) and n_e=10 (stability dichotomy), octree depth 4, consistent cut
+    mass (lumping 'none', the StabilizationParams default).  Only compact
+    fingerprints of the operators are stored (K X, M X, the load, the
+    observers); the device tests rebuild the system with the host set-up
+    restatement and check it against them."""
+    geom = G.ImmersedGeometry.from_angles(0.3, 0.5, (10.0, 10.0, 10.0))
+    src = A.benchmark_source(0.3)
+    f = lambda t: A.ricker(t, 10.0)          # noqa: E731
+    out = {}
+    grid = A.Grid.build(geom, B.BasisSpec(family="lagrange", p=3, n_e=13))
+    cache = A.ElementIntegralCache(grid, octree_depth=4)
+    obs = H.observer_matrix(grid)
+    n = grid.dofmap.n_dof
+    X = np.random.default_rng(7).standard_normal((n, 2))
+    out["X"] = X
+    out.update(csr_parts("obs", obs))
+    # criterion 2 (explicit): dt_crit of the full system, consistent M
+    s8 = A.assemble(grid, S.StabilizationParams(alpha=1e-8), source=src, cache=cache)
+    lam, it = LA.max_gen_eig(s8.K, s8.M, tol=1e-7, seed=0)
+    out.update(F8=s8.F_s, KX8=s8.K @ X, MX8=s8.M @ X, lam8=lam, it8=it, dtc8=2.0 / np.sqrt(lam),
+               Mdiag8=s8.M.diagonal(), Mnnz8=s8.M.nnz)
+    dt8 = T.select_dt(2.0 / np.sqrt(lam))
+    r = T.cdm_run(s8.M, s8.K, s8.F_s, f, dt8, 300, obs_mat=obs)
+    out.update(dt8=dt8, psi8=r.psi, obs8=r.obs)
+    print("n13 alpha 1e-8:", 2.0 / np.sqrt(lam), it)
+    # criteria 2 and 4 (IMEX): explicit-subsystem step, 2000 IMEX steps at 0.9x
+    s12 = A.assemble(grid, S.StabilizationParams(alpha=1e-12), source=src, cache=cache)
+    dm = grid.dofmap
+    dtd = T.imex_critical_time_step(s12.K, s12.M, dm.d_idx, tol=1e-7)
+    Kr = sp.csr_matrix(s12.K)
+    lam_d, it_d = LA.max_gen_eig(Kr[dm.d_idx][:, dm.d_idx], sp.csr_matrix(s12.M)[dm.d_idx][:, dm.d_idx],
+                                 tol=1e-7, seed=0)
+    lam_lb, it_lb = LA.max_gen_eig(s12.K, s12.M, tol=1e-3, seed=0)
+    r = T.imex_run(s12.M, s12.K, s12.F_s, f, 0.9 * dtd, 2000, dm.c_idx, dm.d_idx, obs_mat=obs)
+    out.update(F12=s12.F_s, KX12=s12.K @ X, MX12=s12.M @ X, dtd12=dtd, lamd12=lam_d, itd12=it_d,
+               lamlb12=lam_lb, itlb12=it_lb, psi12=r.psi, obs12=r.obs,
+               c_idx=dm.c_idx.astype(np.int64))
+    print("n13 alpha 1e-12:", dtd, it_d)
+    save("paper_n13", **out)
+    # criterion 3: stability dichotomy on n_e = 10
+    grid = A.Grid.build(geom, B.BasisSpec(family="lagrange", p=3, n_e=10))
+    cache = A.ElementIntegralCache(grid, octree_depth=4)
+    obs = H.observer_matrix(grid)
+    n = grid.dofmap.n_dof
+    X = np.random.default_rng(8).standard_normal((n, 2))
+    s10 = A.assemble(grid, S.StabilizationParams(alpha=1e-8), source=src, cache=cache)
+    lam, it = LA.max_gen_eig(s10.K, s10.M, tol=1e-7, seed=0)
+    dtc = 2.0 / np.sqrt(lam)
+    stable = T.cdm_run(s10.M, s10.K, s10.F_s, f, 0.99 * dtc, 2000, obs_mat=obs)
+    try:
+        T.cdm_run(s10.M, s10.K, s10.F_s, f, 1.05 * dtc, 2000, obs_mat=obs)
+        raise AssertionError("expected divergence")
+    except T.DivergenceError as e:
+        step, amp = e.step, e.amplitude
+    print("n10:", dtc, it, "diverged at", step)
+    save("paper_n10", X=X, **csr_parts("obs", obs), F=s10.F_s, KX=s10.K @ X, MX=s10.M @ X,
+         lam=lam, it=it, dtc=dtc, psi=stable.psi, obs=stable.obs, div_step=step, div_amp=amp)
+
+
+def gen_tensor():
+    """Boundary-fitted grids through the reference's separable operators
+    (TensorSystem, src/assembly.py:615-770): the stiffness LinearOperator in
+    cdm_run and newmark_run with its s_factory (Lagrange: diagonal M and CG
+    inverse; B-splines: consistent Kronecker M and fast diagonalisation)."""
+    geom = G.ImmersedGeometry.from_angles(0.3, 0.5, (10.0, 10.0, 10.0))
+    src = A.benchmark_source(0.3)
+    f = lambda t: A.ricker(t, 10.0)          # noqa: E731
+    out = {}
+    for fam, p, n_e in (("lagrange", 3, 4), ("bspline", 2, 4)):
+        grid = A.Grid.build(geom, B.BasisSpec(family=fam, p=p, n_e=n_e), boundary_fitted=True)
+        ts = A.TensorSystem(grid)
+        M = ts.mass_matrix()
+        K = ts.stiffness_operator()
+        F = A.spatial_load(grid, src, alpha=1.0)
+        obs = H.observer_matrix(grid)
+        lam, it = LA.max_gen_eig(tensor_csr_ref(ts), M,
+                                 tol=1e-7, seed=0)
+        dt = 0.9 * 2.0 / np.sqrt(lam)
+        r = T.cdm_run(M, K, F, f, dt, 150, obs_mat=obs)
+        dtn = 4.0 * dt
+        rn = T.newmark_run(M, K, F, f, dtn, 60, obs_mat=obs,
+                           s_factory=lambda: ts.newmark_factorization(0.25, dtn))
+        k = fam[0]
+        out.update({f"{k}_m1": ts.m1, f"{k}_k1": ts.k1, f"{k}_p": p, f"{k}_n_e": n_e, f"{k}_h": grid.h,
+                    f"{k}_F": F, f"{k}_lam": lam, f"{k}_it": it, f"{k}_dt": dt, f"{k}_psi": r.psi,
+                    f"{k}_obs": r.obs, f"{k}_dtn": dtn, f"{k}_nm_psi": rn.psi, f"{k}_nm_obs": rn.obs,
+                    f"{k}_nm_v": rn.psi_dot},
+                   **csr_parts(f"{k}_obs", obs), **csr_parts(f"{k}_M", M))
+        print(fam, sp.csr_matrix(M).nnz, lam, it)
+    save("tensor", **out)
+
+
+def tensor_csr_ref(ts):
+    m, k = sp.csr_matrix(ts.m1), sp.csr_matrix(ts.k1)
+    return ts.rho * ts.c ** 2 * (sp.kron(sp.kron(k, m), m) + sp.kron(sp.kron(m, k), m)
+                                 + sp.kron(sp.kron(m, m), k)).tocsr()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    for name in sys.argv[1:]:
+        globals()[f"gen_{name}"]()
+elif __name__ == "__main__":
     gen_bar()
     gen_scalar()
     gen_rand10()
@@ -233,3 +337,5 @@ if __name__ == "__main__":
     gen_cube_imex("cube_imex_p2n4", p=2, n_e=4, alpha=1e-12, depth=2, n_t=150)
     gen_cube_imex("cube_imex_p2n4_a4", p=2, n_e=4, alpha=1e-4, depth=2, n_t=150)
     gen_bspline_cube("bspline_cube_p2n5", p=2, n_e=5, alpha=1e-6, depth=2)
+    gen_tensor()
+    gen_paper()

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 import scipy.sparse as sp
 
-from conftest import csr_from, load_golden
+from conftest import IMEX_A12_TOL_P2N4, csr_from, load_golden
 from oracle import timeint as O
 
 pytestmark = pytest.mark.gpu
@@ -86,10 +86,10 @@ def test_imex_rejects_bad_partitions():
     # alpha = 1e-4: a 2e-16 relative perturbation of K moves the reference's
     # own 150-step field by 4e-13 -> the north-star bar 1e-10 applies.
     ("cube_imex_p2n4_a4", 1e-10),
-    # alpha = 1e-12 (the paper's IMEX case): cond(S_cc) ~ 5e13 and a 2e-16
-    # perturbation of K alone moves the reference's field by 2.7e-8
-    # (measured with the oracle); any other summation order lands in that band.
-    ("cube_imex_p2n4", 1e-6)])
+    # alpha = 1e-12 (the paper's IMEX case): cond(S_cc) ~ 5e13 and a 1-ulp
+    # perturbation of K alone moves the reference's field by ~3e-8
+    # (tests/test_paper_setup.py measures it); conftest.IMEX_A12_TOL_P2N4.
+    ("cube_imex_p2n4", IMEX_A12_TOL_P2N4)])
 def test_imex_cube_matches_reference_golden(name, tol):
     """Reference rotated cube, consistent cut mass: 150 IMEX steps at 0.9 x the
     d-subsystem critical step (reference output pinned)."""
@@ -141,8 +141,8 @@ def test_newmark_run_matches_reference_golden():
     r0 = newmark_run(M, K, g["F"], f, float(g["dt"]), 50, beta=0.0)
     psi_ref, v_ref, _ = O.newmark_run(M, K, g["F"], f, float(g["dt"]), 50, beta=0.0)
     assert rel(r0.psi, psi_ref) <= 1e-12 and rel(r0.psi_dot, v_ref) <= 1e-12
-    with pytest.raises(NotImplementedError):
-        newmark_run(M, K, g["F"], f, 1e-3, 3, s_factory=lambda: None)
+    with pytest.raises(TypeError):
+        newmark_run(M, K, g["F"], f, 1e-3, 3, s_factory=lambda: None)   # no .solve
 
 
 def test_newmark_scm_operator_matches_oracle():

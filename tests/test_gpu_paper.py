@@ -1,0 +1,108 @@
+"""The paper's own benchmark through the device: the reference acceptance
+criteria 2-4 (tests/test_acceptance.py:119-179) on the
+rotated cube, SCM p=3, octree depth 4, consistent cut-cell mass (lumping
+'none', the StabilizationParams default):
+
+* criterion 2: dt_crit(K, M) = 3.826625e-4 (alpha 1e-8, n_e 13) and the
+  explicit-subsystem step 5.846924e-3 (alpha 1e-12) -- the device power
+  iteration stops at the reference's iteration with the same estimate;
+* criterion 3: 0.99 dt_crit stays finite for 2000 steps, 1.05 dt_crit
+  diverges at the reference's step (n_e 10);
+* criterion 4: the global step is below half the IMEX step and 2000 IMEX
+  steps at 0.9x stay finite and match the reference's field.
+
+Goldens: tests/golden/make_golden.py ``gen_paper`` (the reference itself).
+The operators are rebuilt here by the host set-up restatement; CPU test
+tests/test_paper_setup.py pins them to the reference's (K X, M X)."""
+
+import numpy as np
+import pytest
+
+from conftest import IMEX_A12_TOL_N13, csr_from, load_golden
+from oracle.geometry_cube import RotatedCube
+
+pytestmark = pytest.mark.gpu
+
+from paper_2501_19013_b200 import (DivergenceError, cdm_run, dt_crit,  # noqa: E402
+                                   imex_critical_time_step, imex_run, max_gen_eig)
+from paper_2501_19013_b200.setup.configs import ricker  # noqa: E402
+from paper_2501_19013_b200.setup.grid import Grid  # noqa: E402
+from paper_2501_19013_b200.setup.problem import ScmProblem  # noqa: E402
+
+# alpha = 1e-12 IMEX over 2000 steps: the reference's own field moves by
+# ~6e-6 under a 1-ulp perturbation of K (tests/test_paper_setup.py measures
+# it), so the device field is held to a small multiple of that spread.
+IMEX_A12_TOL = IMEX_A12_TOL_N13
+
+
+def f(t):
+    return ricker(t, 10.0)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def n13():
+    g = load_golden("paper_n13")
+    grid = Grid.build(RotatedCube(), "lagrange", 3, 13)
+    p8 = ScmProblem.build(grid, 1e-8, 4, lumping="none")
+    p12 = ScmProblem.build(grid, 1e-12, 4, lumping="none")
+    return g, grid, p8, p12
+
+
+def test_criterion2_dt_crit_and_cdm_consistent_mass(n13):
+    g, grid, p8, _ = n13
+    M = p8.mass_matrix()
+    op = p8.device_operator()
+    assert rel(op @ g["X"][:, 0], g["KX8"][:, 0]) <= 1e-13
+    lam, it = max_gen_eig(op, M, tol=1e-7, seed=0)
+    assert it == int(g["it8"])                           # same stopping iteration
+    assert abs(lam - float(g["lam8"])) <= 1e-12 * float(g["lam8"])
+    dtc = dt_crit(op, M, tol=1e-7, seed=0)
+    assert abs(dtc - float(g["dtc8"])) <= 1e-12 * float(g["dtc8"])
+    assert round(dtc, 10) == 3.826625e-4                  # PAPER.md:1396 (0.38268e-3)
+    r = cdm_run(M, op, g["F8"], f, float(g["dt8"]), 300, obs_mat=csr_from(g, "obs"))
+    assert r.fact_dim == grid.n_dof                       # factorize() of a consistent M
+    assert rel(r.psi, g["psi8"]) <= 1e-10
+    assert rel(r.obs, g["obs8"]) <= 1e-10
+
+
+def test_criteria2_4_imex_step_and_2000_steps(n13):
+    g, grid, _, p12 = n13
+    M = p12.mass_matrix()
+    op = p12.device_operator()
+    dm = grid.dofmap
+    dtd = imex_critical_time_step(op, M, dm.d_idx, tol=1e-7)
+    assert abs(dtd - float(g["dtd12"])) <= 1e-12 * float(g["dtd12"])
+    assert round(dtd, 9) == 5.846924e-3                   # PAPER.md:1389 (5.84696e-3)
+    lam_lb, it_lb = max_gen_eig(op, M, tol=1e-3, seed=0)  # consistent-mass power iteration
+    assert it_lb == int(g["itlb12"])
+    assert abs(lam_lb - float(g["lamlb12"])) <= 1e-12 * float(g["lamlb12"])
+    assert 2.0 / np.sqrt(lam_lb) <= 0.5 * dtd
+    r = imex_run(M, op, g["F12"], f, 0.9 * float(g["dtd12"]), 2000, dm.c_idx, dm.d_idx,
+                 obs_mat=csr_from(g, "obs"))
+    assert np.isfinite(r.psi).all() and np.isfinite(r.obs).all()
+    assert r.fact_dim == dm.c_idx.shape[0]
+    assert rel(r.psi, g["psi12"]) <= IMEX_A12_TOL
+    assert rel(r.obs, g["obs12"]) <= IMEX_A12_TOL
+
+
+def test_criterion3_stability_dichotomy():
+    g = load_golden("paper_n10")
+    grid = Grid.build(RotatedCube(), "lagrange", 3, 10)
+    prob = ScmProblem.build(grid, 1e-8, 4, lumping="none")
+    M = prob.mass_matrix()
+    op = prob.device_operator()
+    assert rel(op @ g["X"][:, 0], g["KX"][:, 0]) <= 1e-13
+    lam, it = max_gen_eig(op, M, tol=1e-7, seed=0)
+    assert it == int(g["it"]) and abs(lam - float(g["lam"])) <= 1e-12 * float(g["lam"])
+    dtc = float(g["dtc"])
+    obs = csr_from(g, "obs")
+    r = cdm_run(M, op, g["F"], f, 0.99 * dtc, 2000, obs_mat=obs)
+    assert np.isfinite(r.psi).all() and np.isfinite(r.obs).all()
+    assert rel(r.psi, g["psi"]) <= 1e-10
+    with pytest.raises(DivergenceError) as e:
+        cdm_run(M, op, g["F"], f, 1.05 * dtc, 2000, obs_mat=obs)
+    assert e.value.step == int(g["div_step"])

@@ -75,3 +75,38 @@ def test_cube_imex_oracle_reproduces_reference():
                            g["d_idx"], obs_mat=csr_from(g, "obs"))
     assert np.array_equal(psi, g["psi"])
     assert np.array_equal(o, g["obs"])
+
+
+# ---- the C/OpenMP port (oracle/wc_oracle.c): the bench's reference arm ----
+# It must reproduce the reference bitwise too: same row-sum order as SciPy's
+# csr_matvec, no FMA contraction (-ffp-contract=off), rhs / m division.
+
+def _c_cdm(K, m, F, f, dt, n_t, psi0=None, threads=4):
+    from oracle import cpu
+    from paper_2501_19013_b200.timeint import force_table
+    return cpu.cdm_run(K, m, F, force_table(f, dt, n_t), dt, n_t, psi0=psi0, threads=threads)
+
+
+def test_c_port_cube_p2n4_bitwise():
+    g = load_golden("cube_p2n4")
+    psi, div = _c_cdm(csr_from(g, "K"), g["M"], g["F"], lambda t: O.ricker(t, 10.0),
+                      float(g["dt"]), int(g["n_t"]))
+    assert div == 0
+    assert np.array_equal(psi, g["psi"])
+
+
+def test_c_port_rand10_bitwise_any_thread_count():
+    g = load_golden("rand10")
+    for threads in (1, 3):
+        psi, div = _c_cdm(sp.csr_matrix(g["K"]), g["M"], g["F"], lambda t: np.sin(3.0 * t),
+                          float(g["dt"]), 200, psi0=g["psi0"], threads=threads)
+        assert div == 0 and np.array_equal(psi, g["psi"])
+
+
+def test_c_port_divergence_step_matches_reference():
+    g = load_golden("scalar")
+    one = sp.csr_matrix(np.array([[1.0]]))
+    psi, div = _c_cdm(one, np.ones(1), np.zeros(1), lambda t: 0.0, 1.99, 10000, psi0=np.ones(1))
+    assert div == 0 and np.array_equal(psi, g["stable_psi"])
+    _, div = _c_cdm(one, np.ones(1), np.zeros(1), lambda t: 0.0, 2.01, 10000, psi0=np.ones(1))
+    assert div == int(g["div_step"])

@@ -11,7 +11,8 @@ import pytest
 from conftest import csr_from, load_golden
 from paper_2501_19013_b200.setup import basis as B
 from paper_2501_19013_b200.setup.configs import CONFIGS, build_scm
-from paper_2501_19013_b200.setup.geometry import BallVoids, PolygonVoid, RotatedCube
+from oracle.geometry_cube import RotatedCube
+from paper_2501_19013_b200.setup.geometry import BallVoids, PolygonVoid
 from paper_2501_19013_b200.setup.grid import Grid
 from paper_2501_19013_b200.setup.problem import ScmProblem
 
