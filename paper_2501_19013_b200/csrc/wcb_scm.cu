@@ -94,6 +94,7 @@ struct Scm2DGeo {
     // table (checked bitwise once per plan) -- the 1/m tile is not loaded.
     // null: every tile loads 1/m.
     const uint8_t* tclean;
+    int32_t chunk_nt;         // streaming kernel (k_scm2s): row tiles per chunk
 };
 
 template <int P>
@@ -157,7 +158,7 @@ __device__ __forceinline__ void lds_row(const double* p, double (&v)[P]) {
 
 // One node row of the smem tile: y contraction (masked) then x contraction
 // accumulated into Y.  `row` points at tile column 0 of that row.
-template <int P>
+template <int P, bool MASK = true>
 __device__ __forceinline__ void row_contract(const double (&mc)[orb_count(P)],
                                              const double (&kc)[orb_count(P)], const double* row,
                                              int lane, double chiR, double chiL, int c,
@@ -188,8 +189,8 @@ __device__ __forceinline__ void row_contract(const double (&mc)[orb_count(P)],
             s1 = fma(mc[orb(P, j, d)], own[d], s1);
             s2 = fma(kc[orb(P, j, d)], own[d], s2);
         }
-        W1[j] = chiR * s1;
-        W2[j] = chiR * s2;
+        W1[j] = MASK ? chiR * s1 : s1;
+        W2[j] = MASK ? chiR * s2 : s2;
     }
     // left cell: its local column P is our column 0
     double l1 = mc[orb(P, P, P)] * own[0], l2 = kc[orb(P, P, P)] * own[0];
@@ -200,8 +201,8 @@ __device__ __forceinline__ void row_contract(const double (&mc)[orb_count(P)],
         l1 = fma(mc[orb(P, P, d)], ud, l1);
         l2 = fma(kc[orb(P, P, d)], ud, l2);
     }
-    W1[0] = fma(chiL, l1, W1[0]);
-    W2[0] = fma(chiL, l2, W2[0]);
+    W1[0] = MASK ? fma(chiL, l1, W1[0]) : W1[0] + l1;
+    W2[0] = MASK ? fma(chiL, l2, W2[0]) : W2[0] + l2;
     #pragma unroll
     for (int r = 0; r < N; ++r)
         #pragma unroll
@@ -447,6 +448,205 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
 }
 
 
+// ---------------------------------------------------------------------------
+// Streaming 2D step (default for scalar SCM operators): a CTA owns one strip
+// of 32 cell columns and a chunk of NT consecutive row tiles, and walks down
+// the chunk tile by tile.  Per tile every warp computes one cell row (no halo
+// warp: the shared node row above a tile is carried from the previous tile's
+// bottom warp; only the chunk's first tile recomputes the cell row above, in
+// a prologue).  psi_k (TI+1 node rows) and psi_{k-1} (TI rows) of tile t+1
+// stream into the other half of a double-buffered TMA stage while tile t is
+// computed.  Same fixed-order sums as k_scm2d (carry + own), bitwise equal.
+__host__ __device__ constexpr int minb_2s(int P) { return P <= 4 ? 3 : 2; }
+__host__ __device__ constexpr size_t al128(size_t b) { return (b + 127) / 128 * 128; }
+template <int P>
+struct Tile2S {
+    static constexpr int RPE = Tile2<P>::RPE;   // same row tiles as k_scm2d (cflags, tclean)
+    static constexpr int NWARP = RPE;
+    static constexpr int TJ = 32 * P;
+    static constexpr int TI = RPE * P;
+    static constexpr int CO = P & 1;
+    static constexpr int UW = Tile2<P>::UW;
+    static constexpr int UH = TI + 1;       // node rows I0 .. I0+TI
+    static constexpr int HH = P + 1;        // chunk halo rows I0-P .. I0
+    static constexpr size_t U_BYTES = (size_t)UW * UH * 8;
+    static constexpr size_t H_BYTES = (size_t)UW * HH * 8;
+    static constexpr size_t E_BYTES = (size_t)TJ * TI * 8;
+    static constexpr size_t STAGE = al128(U_BYTES) + al128(E_BYTES);
+    static constexpr int NS = 2;
+    static constexpr size_t OFF_HALO = NS * STAGE;
+    static constexpr size_t OFF_CARRY = OFF_HALO + al128(H_BYTES);               // [2][RPE+1][P][32]
+    static constexpr size_t OFF_BAR = OFF_CARRY + (size_t)2 * (RPE + 1) * P * 32 * 8;
+    static constexpr size_t SMEM = OFF_BAR + 8 * (NS + 1);
+};
+
+// the cell row whose node rows start at `rows` (stride UW): y/x contraction
+// (unmasked fast path when the warp's cells are all uncut) and cut cells
+template <int P, int UW, int CO>
+__device__ __forceinline__ void cell_row2(const Scm2DGeo& g, const double (&mc)[orb_count(P)],
+                                          const double (&kc)[orb_count(P)], const double* rows, int64_t ex,
+                                          int64_t ey, int lane, double (&Y)[P + 1][P]) {
+    constexpr int N = P + 1;
+    uint8_t mR = 0, mL = 0;
+    if (ex >= 0 && ex < g.n_ex && ey <= g.n_ey) {
+        const int64_t ms_ = g.n_ey + 2;
+        mR = __ldg(g.mask + (ex + 1) * ms_ + (ey + 1));
+        mL = __ldg(g.mask + (ex + 1) * ms_ + ey);
+    }
+    const int32_t cid = mR == 2 ? __ldg(g.cut_id + ex * g.n_ey + ey) : -1;
+    const int32_t cidL = (lane == 0 && mL == 2) ? __ldg(g.cut_id + ex * g.n_ey + ey - 1) : -1;
+    #pragma unroll
+    for (int r = 0; r < N; ++r)
+        #pragma unroll
+        for (int j = 0; j < P; ++j) Y[r][j] = 0.0;
+    if (!__any_sync(0xffffffffu, (mR | mL) != 0)) return;
+    if (__all_sync(0xffffffffu, mR == 1 && mL == 1)) {
+        #pragma unroll
+        for (int c = 0; c < N; ++c) row_contract<P, false>(mc, kc, rows + (size_t)c * UW, lane, 1.0, 1.0, c, Y);
+        return;
+    }
+    const double chiR = mR == 1 ? 1.0 : 0.0;
+    const double chiL = mL == 1 ? 1.0 : 0.0;
+    #pragma unroll
+    for (int c = 0; c < N; ++c) row_contract<P, true>(mc, kc, rows + (size_t)c * UW, lane, chiR, chiL, c, Y);
+    const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
+    const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
+    if (cl || ed) cut_cells_warp<P, UW, CO>(g, rows, ex, ey - lane, lane, cl, ed, cid, cidL, Y);
+}
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(Tile2S<P>::NWARP * 32, minb_2s(P)) k_scm2s(
+    const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_h,
+    const __grid_constant__ CUtensorMap tm_prev, Scm2DGeo g, Mats2<P> mt, MinvTab2<P> mtab, double sk,
+    StepArgs a) {
+    using T = Tile2S<P>;
+    constexpr int N = P + 1;
+    constexpr int RPE = T::RPE;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* carry = reinterpret_cast<double*>(smem + T::OFF_CARRY);   // [2][RPE+1][P][32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);  // [NS] stages, [NS] halo
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    if (MODE == MODE_STEP) pdl_trigger();
+    const int32_t chunk = __ldg(g.order + blockIdx.x);
+    const int64_t strip = chunk / g.n_rtiles, rt0 = chunk % g.n_rtiles;
+    const int nt = (int)min((int64_t)g.chunk_nt, g.n_rtiles - rt0);
+    const int64_t J0 = strip * T::TJ;
+    const int64_t I00 = g.row_lo + rt0 * T::TI;
+    if (MODE == MODE_STEP) pdl_wait();
+    if (MODE == MODE_STEP && blockIdx.x == 0) record_observers(a);
+    auto issue = [&](int t) {   // tile t of the chunk into stage t % NS
+        const int b = t % T::NS;
+        unsigned char* st = smem + (size_t)b * T::STAGE;
+        const int64_t I0 = I00 + (int64_t)t * T::TI;
+        mbar_expect_tx(&full[b], (uint32_t)(T::U_BYTES + (MODE == MODE_STEP ? T::E_BYTES : 0)));
+        tma_load_2d(st, &tm_u, (int32_t)(J0 - P - T::CO + PADJ), (int32_t)(I0 + P), &full[b]);
+        if (MODE == MODE_STEP)
+            tma_load_2d(st + al128(T::U_BYTES), &tm_prev, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), &full[b]);
+    };
+    if (threadIdx.x == 0) {
+        #pragma unroll
+        for (int q = 0; q < T::NS + 1; ++q) mbar_init(&full[q], 1);
+        mbar_expect_tx(&full[T::NS], (uint32_t)T::H_BYTES);
+        tma_load_2d(smem + T::OFF_HALO, &tm_h, (int32_t)(J0 - P - T::CO + PADJ), (int32_t)I00, &full[T::NS]);
+        issue(0);
+    }
+    double mc[orb_count(P)], kc[orb_count(P)];
+    #pragma unroll
+    for (int i = 0; i < orb_count(P); ++i) { mc[i] = mt.m[i]; kc[i] = mt.k[i]; }
+    const int64_t ey = J0 / P + lane;
+    const int64_t Jl = J0 + lane * P;
+    const bool edge = (J0 + T::TJ > g.n1y);
+    const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
+    __syncthreads();   // barrier init visible
+    double Y[N][P];
+    if (w == 0) {      // the cell row above the chunk: its bottom row feeds tile 0's top row
+        mbar_wait(&full[T::NS], 0);
+        cell_row2<P, T::UW, T::CO>(g, mc, kc, reinterpret_cast<const double*>(smem + T::OFF_HALO),
+                                   I00 / P - 1, ey, lane, Y);
+        #pragma unroll
+        for (int j = 0; j < P; ++j) carry[((1 * (RPE + 1) + RPE) * P + j) * 32 + lane] = Y[P][j];
+    }
+    unsigned long long amp = 0ULL;
+    for (int t = 0; t < nt; ++t) {
+        const int b = t % T::NS, par = t & 1;
+        if (threadIdx.x == 0 && t + 1 < nt) issue(t + 1);
+        const unsigned char* st = smem + (size_t)b * T::STAGE;
+        const double* us = reinterpret_cast<const double*>(st);
+        const int64_t I0 = I00 + (int64_t)t * T::TI;
+        const int64_t rt = rt0 + t;
+        const bool tcl = MODE == MODE_STEP && g.tclean && __ldg(g.tclean + strip * g.n_rtiles + rt) != 0;
+        mbar_wait(&full[b], (uint32_t)((t / T::NS) & 1));
+        const int64_t ex = I0 / P + w;
+        cell_row2<P, T::UW, T::CO>(g, mc, kc, us + (size_t)(w * P) * T::UW, ex, ey, lane, Y);
+        #pragma unroll
+        for (int j = 0; j < P; ++j) carry[((par * (RPE + 1) + w + 1) * P + j) * 32 + lane] = Y[P][j];
+        __syncthreads();
+        {
+            const double* cin = carry + (size_t)(w == 0 ? ((par ^ 1) * (RPE + 1) + RPE) : (par * (RPE + 1) + w)) * P * 32;
+            #pragma unroll
+            for (int j = 0; j < P; ++j) Y[0][j] = cin[j * 32 + lane] + Y[0][j];
+        }
+        #pragma unroll
+        for (int r = 0; r < P; ++r)
+            #pragma unroll
+            for (int j = 0; j < P; ++j) Y[r][j] *= sk;
+        #pragma unroll
+        for (int r = 0; r < P; ++r) {
+            const int64_t I = ex * P + r;
+            if (I >= g.row_hi) break;
+            const int64_t base = (I + P) * g.pitch + Jl + PADJ;
+            const double* urow = us + (size_t)(w * P + r) * T::UW + T::CO + P + lane * P;
+            if constexpr (MODE == MODE_APPLY) {
+                #pragma unroll
+                for (int j = 0; j < P; ++j)
+                    if (!edge || Jl + j < g.n1y) a.out[base + j] = Y[r][j];
+            } else {
+                double up[P], mi[P], uu[P], v[P];
+                lds_row<P>(reinterpret_cast<const double*>(st + al128(T::U_BYTES)) +
+                               (size_t)(w * P + r) * T::TJ + lane * P, up);
+                if (tcl) {
+                    #pragma unroll
+                    for (int j = 0; j < P; ++j) mi[j] = mtab.v[r * P + j];
+                } else {
+                    #pragma unroll
+                    for (int j = 0; j < P; ++j) mi[j] = (!edge || Jl + j < g.n1y) ? __ldg(a.minv + base + j) : 0.0;
+                }
+                lds_row<P>(urow, uu);
+                const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
+                #pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    const double fF = src ? f * source_at(a.F, base + j) : f * 0.0;
+                    v[j] = leapfrog(uu[j], up[j], Y[r][j], mi[j], fF, a.dt2);
+                }
+                if constexpr (P == 4) {
+                    if (!edge) {
+                        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(a.out + base),
+                                     "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]) : "memory");
+                        #pragma unroll
+                        for (int j = 0; j < P; ++j) {
+                            const unsigned long long bb = mi[j] != 0.0 ? amp_bits(v[j]) : 0ULL;
+                            amp = bb > amp ? bb : amp;
+                        }
+                        continue;
+                    }
+                }
+                #pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    if (!edge || Jl + j < g.n1y) {
+                        a.out[base + j] = v[j];
+                        const unsigned long long bb = mi[j] != 0.0 ? amp_bits(v[j]) : 0ULL;
+                        amp = bb > amp ? bb : amp;
+                    }
+                }
+            }
+        }
+        __syncthreads();   // stage b and this parity's carry are free again
+    }
+    if constexpr (MODE == MODE_STEP) warp_amp_max(amp, a.amp);
+}
+
+
 #include "wcb_ela2d.cuh"
 
 struct ScmOperator final : Operator {
@@ -475,6 +675,9 @@ struct ScmOperator final : Operator {
     DevBuf<double2> zline;           // 3D, n_e % 32 == 0: z-lines of the last cell column
     DevBuf<int32_t> order;        // 2D tile kernel: live tiles, most expensive first
     int64_t n_order = 0;
+    std::vector<double> tile_cost;           // 2D: per tile (strip-major), for the chunk order
+    DevBuf<int32_t> chunks;                  // streaming kernel: live chunks, most expensive first
+    int64_t n_chunks = 0, chunk_nt = 0;
     // apply restricted to the tiles owning a given DOF subset (IMEX c rows)
     DevBuf<int32_t> order_sub;
     int64_t n_order_sub = 0;
@@ -511,6 +714,87 @@ struct ScmOperator final : Operator {
             return make_map_f64(ptr, 2, dims, strides, kind == 0 ? box_u : box_e);
         });
     }
+    // streaming step / apply of scalar 2D operators (k_scm2s): chunks of
+    // chunk_nt row tiles per CTA; WAVECELL_B200_TILE2D=1 keeps the tile kernel
+    bool stream2d_off = getenv("WAVECELL_B200_TILE2D") && getenv("WAVECELL_B200_TILE2D")[0] == '1';
+    bool use_stream2d() const {
+        return !stream2d_off && ncomp == 1 && part_active < 0 && !sub_active && !tile_cost.empty();
+    }
+    template <int P>
+    void build_chunks() {
+        using T = Tile2S<P>;
+        int per_sm = 0;
+        ensure_smem_attr((const void*)k_scm2s<P, MODE_STEP>, ctx->device, (size_t)T::SMEM);
+        WCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scm2s<P, MODE_STEP>, T::NWARP * 32,
+                                                               T::SMEM));
+        const int64_t slots = std::max(1, per_sm) * (int64_t)ctx->sm_count;
+        int64_t live = 0;
+        for (double c : tile_cost) live += c > 0.0;
+        // about WAVES waves of chunks (load balance) unless overridden
+        const char* e = getenv("WAVECELL_B200_CHUNK_NT");
+        const double waves = getenv("WAVECELL_B200_CHUNK_WAVES") ? atof(getenv("WAVECELL_B200_CHUNK_WAVES")) : 2.0;
+        chunk_nt = e ? std::max(1, atoi(e)) : std::max<int64_t>(1, (int64_t)std::llround(live / (waves * slots)));
+        std::vector<std::pair<double, int32_t>> w;
+        for (int64_t st = 0; st < n_strips; ++st)
+            for (int64_t rt = 0; rt < n_rtiles; rt += chunk_nt) {
+                double c = 0.0;
+                for (int64_t q = rt; q < std::min<int64_t>(rt + chunk_nt, n_rtiles); ++q) c += tile_cost[st * n_rtiles + q];
+                if (c > 0.0) w.emplace_back(-c, (int32_t)(st * n_rtiles + rt));
+            }
+        std::stable_sort(w.begin(), w.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        std::vector<int32_t> ord(w.size());
+        for (size_t i = 0; i < w.size(); ++i) ord[i] = w[i].second;
+        n_chunks = (int64_t)ord.size();
+        chunks.alloc(std::max<int64_t>(n_chunks, 1));
+        if (n_chunks) chunks.upload(ord.data(), ord.size(), ctx->stream);
+        WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    template <int P>
+    const CUtensorMap& stream_map2(const double* ptr, int kind) {
+        using T = Tile2S<P>;
+        return maps.get(ptr, 40 + kind, [&] {
+            const uint64_t dims[2] = {(uint64_t)pitch, (uint64_t)rows};
+            const uint64_t strides[1] = {(uint64_t)pitch};
+            const uint32_t box_u[2] = {(uint32_t)T::UW, (uint32_t)T::UH};
+            const uint32_t box_h[2] = {(uint32_t)T::UW, (uint32_t)T::HH};
+            const uint32_t box_e[2] = {(uint32_t)T::TJ, (uint32_t)T::TI};
+            return make_map_f64(ptr, 2, dims, strides, kind == 0 ? box_u : kind == 1 ? box_h : box_e);
+        });
+    }
+    template <int P, int MODE>
+    void launch2st(const StepArgs& a, const Mats2<P>& mt) {
+        using T = Tile2S<P>;
+        if (!chunk_nt) build_chunks<P>();
+        if (!n_chunks) return;
+        ensure_smem_attr((const void*)k_scm2s<P, MODE>, ctx->device, (size_t)T::SMEM);
+        Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, chunks.p, n_strips, n_rtiles,
+                   pitch, nullptr, (int32_t)chunk_nt};
+        MinvTab2<P> tab{};
+        if (MODE == MODE_STEP && a.minv && a.minv == minv_bound && tclean.p) {
+            g.tclean = tclean.p;
+            for (int i = 0; i < P * P; ++i) tab.v[i] = minv_tab[i];
+        }
+        const CUtensorMap& mu = stream_map2<P>(a.cur, 0);
+        const CUtensorMap& mh = stream_map2<P>(a.cur, 1);
+        const CUtensorMap& mp = MODE == MODE_STEP ? stream_map2<P>(a.prev, 2) : mu;
+        dim3 grid((unsigned)n_chunks);
+        if (MODE == MODE_STEP && pdl_enabled()) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = grid;
+            cfg.blockDim = dim3(T::NWARP * 32);
+            cfg.dynamicSmemBytes = T::SMEM;
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            WCB_CUDA(cudaLaunchKernelEx(&cfg, k_scm2s<P, MODE>, mu, mh, mp, g, mt, tab, sk, a));
+        } else {
+            k_scm2s<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(mu, mh, mp, g, mt, tab, sk, a);
+        }
+        ctx->launches++;
+    }
     template <int P, int MODE>
     void launch2d(const StepArgs& a) {
         using T = Tile2<P>;
@@ -522,6 +806,10 @@ struct ScmOperator final : Operator {
                     mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
+        if (use_stream2d()) {
+            launch2st<P, MODE>(a, mt);
+            return;
+        }
         const int32_t* ord = part_active >= 0 ? order_part[part_active].p : sub_active ? order_sub.p : order.p;
         const int64_t n_ord = part_active >= 0 ? n_order_part[part_active] : sub_active ? n_order_sub : n_order;
         if (!n_ord) return;
@@ -1242,6 +1530,8 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
                     n_c += cid[ex * cells_row + ey] >= 0;
             w.emplace_back(-(1.0 + CUT_COST * n_c), (int32_t)t);
         }
+        op->tile_cost.assign(cf.size(), 0.0);
+        for (const auto& x : w) op->tile_cost[x.second] = -x.first;
         std::stable_sort(w.begin(), w.end(),
                          [](const auto& a, const auto& b) { return a.first < b.first; });
         std::vector<int32_t> ord(w.size());

@@ -159,3 +159,33 @@ def test_3d_x_chunking_bitwise_invariant(p, n_e, monkeypatch):
     for y, psi in outs[1:]:
         assert np.array_equal(y, outs[0][0])
         assert np.array_equal(psi, outs[0][1])
+
+
+@pytest.mark.parametrize("p,n_e", [(4, 96), (3, 40), (2, 33), (5, 20), (1, 64)])
+def test_2d_streaming_kernel_bitwise_vs_tile_kernel(p, n_e, monkeypatch):
+    """k_scm2s (chunks of row tiles per CTA, carried top row, double-buffered
+    TMA stages) against k_scm2d (one tile per CTA, halo warp): the same
+    fixed-order sums, so apply and 200 CDM steps are bitwise equal for any
+    chunk length."""
+    from dataclasses import replace
+    cfg = replace(CONFIGS["config2"], p=p, n_e=n_e, name="c2s")
+    prob = build_scm(cfg)
+    M = prob.mass_matrix()
+    x = np.random.default_rng(p).standard_normal(prob.n_dof)
+    f = lambda t: ricker(t, 10.0)  # noqa: E731
+    outs = []
+    for env, nt in (("1", None), (None, "1"), (None, "3"), (None, "100000")):
+        monkeypatch.delenv("WAVECELL_B200_TILE2D", raising=False)
+        if env:
+            monkeypatch.setenv("WAVECELL_B200_TILE2D", env)
+        if nt:
+            monkeypatch.setenv("WAVECELL_B200_CHUNK_NT", nt)
+        op = prob.device_operator()
+        r = cdm_run(M, op, prob.F_s, f, 0.2 / (n_e * p * p), 200)
+        outs.append((op @ x, r.psi))
+        op.close()
+    K = prob.csr_stiffness()
+    assert rel(outs[0][0], K @ x) <= 1e-13
+    for y, psi in outs[1:]:
+        assert np.array_equal(y, outs[0][0])
+        assert np.array_equal(psi, outs[0][1])

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 import scipy.sparse as sp
 
-from conftest import IMEX_A12_TOL_N13, IMEX_A12_TOL_P2N4, csr_from, load_golden
+from conftest import IMEX_A12_TOL_N13, IMEX_A12_TOL_P2N4, NEAR_CRITICAL_TOL, csr_from, load_golden
 from oracle import timeint as O
 from oracle.geometry_cube import RotatedCube
 from paper_2501_19013_b200.setup.configs import ricker
@@ -88,3 +88,18 @@ def test_imex_alpha12_sensitivity_paper_n13(n13):
     spread = rel(O.imex_run(M, perturbed(K, 5), *args)[0], base)
     assert setup_dev <= IMEX_A12_TOL_N13 and 1e-7 <= spread <= IMEX_A12_TOL_N13 <= 10.0 * spread, \
         (setup_dev, spread)
+
+
+def test_near_critical_cdm_sensitivity_paper_n10():
+    """2000 consistent-mass CDM steps at 0.99 dt_crit (criterion 3, n_e 10):
+    the reference arithmetic moves by ~2e-10 under a 1-ulp perturbation of
+    K, which is why the device check of this case uses NEAR_CRITICAL_TOL."""
+    g = load_golden("paper_n10")
+    grid = Grid.build(RotatedCube(), "lagrange", 3, 10)
+    p = ScmProblem.build(grid, 1e-8, 4, lumping="none")
+    K, M = p.csr_stiffness(), p.mass_matrix()
+    args = (g["F"], f, 0.99 * float(g["dtc"]), 2000)
+    base, _, _ = O.cdm_run(M, K, *args)
+    assert rel(base, g["psi"]) <= NEAR_CRITICAL_TOL
+    spread = rel(O.cdm_run(M, perturbed(K, 1), *args)[0], base)
+    assert 1e-11 <= spread <= NEAR_CRITICAL_TOL <= 10.0 * spread, spread
