@@ -54,6 +54,7 @@ struct TriSched {
     int slot_e = 0, slot_r = 0;                  // ring slot capacities (entries, rows)
     int depth = 3;                               // ring depth (levels in flight)
     bool recip = false;                          // sdiag holds 1/diag
+    bool pf_ok = false;                          // k_trsv_pf fits (unknowns + level offsets in smem)
     DevBuf<int32_t> comp_order;  // launch order: components by decreasing level count
     DevBuf<int32_t> comp_rows;   // n_comp + 1: offsets into rows
     DevBuf<int32_t> comp_lvl;    // n_comp + 1: offsets into lvl_off
@@ -209,6 +210,7 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
     }
     T.depth = T.depth >= 12 ? 12 : T.depth >= 8 ? 8 : T.depth >= 6 ? 6 : T.depth >= 4 ? 4 : 3;
     T.ok = avail > 0 && T.slot_e >= 256;
+    T.pf_ok = T.max_size * 8 + (T.max_levels + 1) * 8 <= (int64_t)TRSV_SMEM;
     // launch order: longest dependency chains first (2 waves when components > SMs)
     std::vector<int32_t> co(n_comp);
     for (int64_t c = 0; c < n_comp; ++c) co[c] = (int32_t)c;
@@ -430,7 +432,137 @@ static void launch_trsv_d(Context* ctx, const TriSched& T, const double* b, doub
         T.comp_order.p, T.comp_rows.p, T.comp_lvl.p, T.lvl_off.p, T.lvl_ent.p, T.rows.p, T.sptr.p, T.slcol.p,
         T.sval.p, T.sdiag.p, b, x, (int)T.max_size, (int)T.max_levels, T.slot_e, T.slot_r, T.recip ? 1 : 0);
 }
+
+// Level-scheduled component solve with register prefetch (default):
+// one CTA per component (unknowns in shared memory), NW warps in row groups
+// of GW lanes.  A level costs one barrier plus its rows: every group loads
+// the values / column slots / pivot of its next row while the current
+// level is solved (they do not depend on x), so after the barrier only the
+// shared-memory gathers of x, the FMAs and the shuffle tree remain on the
+// critical path; levels further ahead are prefetched into L2 by bulk
+// prefetches.  Entries are visited in the same lane-strided order and reduced
+// by the same tree as k_trsv_comp / k_sptrsv (bitwise equal).
+constexpr int TRSV_KPF = 4;     // entries per lane held in registers
+constexpr int TRSV_PFD = 8;     // L2 prefetch distance (levels)
+
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~(uintptr_t)15;
+    if (e > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_trsv_pf(
+    const int32_t* __restrict__ comp_order, const int32_t* __restrict__ comp_rows,
+    const int32_t* __restrict__ comp_lvl, const int32_t* __restrict__ lvl_off, const int32_t* __restrict__ lvl_ent,
+    const int32_t* __restrict__ rows, const int32_t* __restrict__ sptr, const int32_t* __restrict__ slcol,
+    const double* __restrict__ sval, const double* __restrict__ sdiag, const double* __restrict__ b,
+    double* __restrict__ x, int max_size, int max_levels, int recip) {
+    constexpr int GW = WCB_TRSV_GW;
+    constexpr int G = NW * 32 / GW;                 // row groups
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* xl = reinterpret_cast<double*>(smraw);
+    int* lo = reinterpret_cast<int*>(xl + max_size);
+    int* le = lo + max_levels + 1;
+    const int c = comp_order[blockIdx.x];
+    const int lane = threadIdx.x & 31;
+    const int grp = threadIdx.x / GW, l16 = lane % GW;
+    const unsigned hmask = (GW == 32 ? 0xffffffffu : ((1u << GW) - 1u)) << ((lane / GW) * GW);
+    const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
+    const int l0 = comp_lvl[c], nl = comp_lvl[c + 1] - l0;
+    for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) xl[k - r0] = b[rows[k]];
+    for (int l = threadIdx.x; l <= nl; l += blockDim.x) {
+        lo[l] = lvl_off[l0 + l];
+        le[l] = lvl_ent[l0 + l];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int l = 0; l < TRSV_PFD && l < nl; ++l) {
+            l2_prefetch(sval + le[l], (size_t)(le[l + 1] - le[l]) * 8);
+            l2_prefetch(slcol + le[l], (size_t)(le[l + 1] - le[l]) * 4);
+        }
+    // this group's first row of a level: (row, entry range, pivot, first entries)
+    int rk = -1, p0 = 0, p1 = 0;
+    double dg = 0.0, pv[TRSV_KPF];
+    int pc[TRSV_KPF];
+    auto preload = [&](int l) {
+        rk = -1;
+        if (l >= nl) return;
+        const int k = lo[l] + grp;
+        if (k >= lo[l + 1]) return;
+        rk = k;
+        p0 = sptr[k];
+        p1 = sptr[k + 1];
+        dg = sdiag[k];
+        #pragma unroll
+        for (int q = 0; q < TRSV_KPF; ++q) {
+            const int j = p0 + l16 + q * GW;
+            pv[q] = j < p1 ? sval[j] : 0.0;
+            pc[q] = j < p1 ? slcol[j] : 0;
+        }
+    };
+    auto finish = [&](int k, double sacc) {
+        #pragma unroll
+        for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
+        if (l16 == 0) {
+            const int i = k - r0;
+            xl[i] = recip ? (xl[i] - sacc) * sdiag[k] : (xl[i] - sacc) / sdiag[k];
+        }
+    };
+    preload(0);
+    for (int l = 0; l < nl; ++l) {
+        __syncthreads();   // level l-1 solved
+        if (threadIdx.x == 0 && l + TRSV_PFD < nl) {
+            const int lp = l + TRSV_PFD;
+            l2_prefetch(sval + le[lp], (size_t)(le[lp + 1] - le[lp]) * 8);
+            l2_prefetch(slcol + le[lp], (size_t)(le[lp + 1] - le[lp]) * 4);
+            l2_prefetch(sptr + lo[lp], (size_t)(lo[lp + 1] - lo[lp] + 1) * 4);
+            l2_prefetch(sdiag + lo[lp], (size_t)(lo[lp + 1] - lo[lp]) * 8);
+        }
+        if (rk >= 0) {
+            double sacc = 0.0;
+            #pragma unroll
+            for (int q = 0; q < TRSV_KPF; ++q)
+                if (p0 + l16 + q * GW < p1) sacc = fma(pv[q], xl[pc[q]], sacc);
+            for (int j = p0 + l16 + TRSV_KPF * GW; j < p1; j += GW) sacc = fma(sval[j], xl[slcol[j]], sacc);
+            (void)dg;
+            finish(rk, sacc);
+        }
+        // further rows of a wide level
+        for (int k = lo[l] + grp + G; k < lo[l + 1]; k += G) {
+            double sacc = 0.0;
+            for (int j = sptr[k] + l16; j < sptr[k + 1]; j += GW) sacc = fma(sval[j], xl[slcol[j]], sacc);
+            finish(k, sacc);
+        }
+        preload(l + 1);
+    }
+    __syncthreads();
+    for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) x[rows[k]] = xl[k - r0];
+}
+
+template <int NW>
+static void launch_trsv_pf(Context* ctx, const TriSched& T, const double* b, double* x) {
+    const size_t sm = (size_t)T.max_size * 8 + (size_t)(T.max_levels + 1) * 8;
+    ensure_smem_attr((const void*)k_trsv_pf<NW>, ctx->device, sm);
+    k_trsv_pf<NW><<<(unsigned)T.n_comp, NW * 32, sm, ctx->stream>>>(
+        T.comp_order.p, T.comp_rows.p, T.comp_lvl.p, T.lvl_off.p, T.lvl_ent.p, T.rows.p, T.sptr.p, T.slcol.p,
+        T.sval.p, T.sdiag.p, b, x, (int)T.max_size, (int)T.max_levels, T.recip ? 1 : 0);
+}
+
 static void launch_trsv(Context* ctx, const TriSched& T, const double* b, double* x) {
+    static const int nw = [] {
+        const char* e = getenv("WAVECELL_B200_TRSV_NW");
+        return e ? atoi(e) : 16;
+    }();
+    if (T.pf_ok && (nw > 0 || !T.ok)) {
+        switch (nw) {
+            case 4: launch_trsv_pf<4>(ctx, T, b, x); return;
+            case 8: launch_trsv_pf<8>(ctx, T, b, x); return;
+            case 32: launch_trsv_pf<32>(ctx, T, b, x); return;
+            default: launch_trsv_pf<16>(ctx, T, b, x); return;
+        }
+    }
     switch (T.depth) {
         case 3: launch_trsv_d<3>(ctx, T, b, x); break;
         case 4: launch_trsv_d<4>(ctx, T, b, x); break;
@@ -610,7 +742,7 @@ static void lu_solve(Context* ctx, wcb_imex_plan* P, DevLU& F, const double* b, 
     if (!n) return;
     k_perm_rows<<<grid1(ctx, n), 256, 0, s>>>(n, F.perm_r.p, b, P->y.p);
     // forward: L w = y  (into z), backward: U v = w (into y)
-    if (F.Ls.ok && F.Us.ok) {
+    if ((F.Ls.ok || F.Ls.pf_ok) && (F.Us.ok || F.Us.pf_ok)) {
         launch_trsv(ctx, F.Ls, P->y.p, P->z.p);
         launch_trsv(ctx, F.Us, P->z.p, x);
         ctx->launches += 3;

@@ -158,7 +158,7 @@ __device__ __forceinline__ void lds_row(const double* p, double (&v)[P]) {
 
 // One node row of the smem tile: y contraction (masked) then x contraction
 // accumulated into Y.  `row` points at tile column 0 of that row.
-template <int P, bool MASK = true>
+template <int P, bool MASK = true, bool HALO = false>
 __device__ __forceinline__ void row_contract(const double (&mc)[orb_count(P)],
                                              const double (&kc)[orb_count(P)], const double* row,
                                              int lane, double chiR, double chiL, int c,
@@ -204,7 +204,7 @@ __device__ __forceinline__ void row_contract(const double (&mc)[orb_count(P)],
     W1[0] = MASK ? fma(chiL, l1, W1[0]) : W1[0] + l1;
     W2[0] = MASK ? fma(chiL, l2, W2[0]) : W2[0] + l2;
     #pragma unroll
-    for (int r = 0; r < N; ++r)
+    for (int r = HALO ? P : 0; r < N; ++r)   // the halo warp only needs output row P
         #pragma unroll
         for (int j = 0; j < P; ++j)
             Y[r][j] = fma(kc[orb(P, r, c)], W1[j], fma(mc[orb(P, r, c)], W2[j], Y[r][j]));
@@ -346,10 +346,20 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
         const double chiR = mR == 1 ? 1.0 : 0.0;
         const double chiL = mL == 1 ? 1.0 : 0.0;
         const double* rows = us + (size_t)(rbase + P) * T::UW;
-#ifndef WCB2D_NOTENSOR
-        #pragma unroll
-        for (int c = 0; c < N; ++c) row_contract<P>(mc, kc, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
+        // warp-uniform variants: every cell uncut (no masks); halo warp
+        // (output row P only) -- the same sums as the masked general path
+#ifdef WCB2D_NOFAST
+        const bool clean_row = false;
+#else
+        const bool clean_row = __all_sync(0xffffffffu, mR == 1 && mL == 1);
 #endif
+        if (clean_row) {
+            #pragma unroll
+            for (int c = 0; c < N; ++c) row_contract<P, false, false>(mc, kc, rows + (size_t)c * T::UW, lane, 1.0, 1.0, c, Y);
+        } else {
+            #pragma unroll
+            for (int c = 0; c < N; ++c) row_contract<P>(mc, kc, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
+        }
         const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
         const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
 #ifndef WCB2D_NOCUT
@@ -457,7 +467,13 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
 // a prologue).  psi_k (TI+1 node rows) and psi_{k-1} (TI rows) of tile t+1
 // stream into the other half of a double-buffered TMA stage while tile t is
 // computed.  Same fixed-order sums as k_scm2d (carry + own), bitwise equal.
-__host__ __device__ constexpr int minb_2s(int P) { return P <= 4 ? 3 : 2; }
+#ifndef WCB2S_MINB
+#define WCB2S_MINB 3
+#endif
+#ifndef WCB2S_PREV_TMA
+#define WCB2S_PREV_TMA 1     // psi_{k-1} staged by TMA (0: loaded in the epilogue)
+#endif
+__host__ __device__ constexpr int minb_2s(int P) { return P <= 4 ? WCB2S_MINB : 2; }
 __host__ __device__ constexpr size_t al128(size_t b) { return (b + 127) / 128 * 128; }
 template <int P>
 struct Tile2S {
@@ -471,7 +487,7 @@ struct Tile2S {
     static constexpr int HH = P + 1;        // chunk halo rows I0-P .. I0
     static constexpr size_t U_BYTES = (size_t)UW * UH * 8;
     static constexpr size_t H_BYTES = (size_t)UW * HH * 8;
-    static constexpr size_t E_BYTES = (size_t)TJ * TI * 8;
+    static constexpr size_t E_BYTES = WCB2S_PREV_TMA ? (size_t)TJ * TI * 8 : 0;
     static constexpr size_t STAGE = al128(U_BYTES) + al128(E_BYTES);
     static constexpr int NS = 2;
     static constexpr size_t OFF_HALO = NS * STAGE;
@@ -541,7 +557,7 @@ __global__ void __launch_bounds__(Tile2S<P>::NWARP * 32, minb_2s(P)) k_scm2s(
         const int64_t I0 = I00 + (int64_t)t * T::TI;
         mbar_expect_tx(&full[b], (uint32_t)(T::U_BYTES + (MODE == MODE_STEP ? T::E_BYTES : 0)));
         tma_load_2d(st, &tm_u, (int32_t)(J0 - P - T::CO + PADJ), (int32_t)(I0 + P), &full[b]);
-        if (MODE == MODE_STEP)
+        if (MODE == MODE_STEP && WCB2S_PREV_TMA)
             tma_load_2d(st + al128(T::U_BYTES), &tm_prev, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), &full[b]);
     };
     if (threadIdx.x == 0) {
@@ -603,8 +619,13 @@ __global__ void __launch_bounds__(Tile2S<P>::NWARP * 32, minb_2s(P)) k_scm2s(
                     if (!edge || Jl + j < g.n1y) a.out[base + j] = Y[r][j];
             } else {
                 double up[P], mi[P], uu[P], v[P];
-                lds_row<P>(reinterpret_cast<const double*>(st + al128(T::U_BYTES)) +
-                               (size_t)(w * P + r) * T::TJ + lane * P, up);
+                if constexpr (WCB2S_PREV_TMA != 0) {
+                    lds_row<P>(reinterpret_cast<const double*>(st + al128(T::U_BYTES)) +
+                                   (size_t)(w * P + r) * T::TJ + lane * P, up);
+                } else {
+                    #pragma unroll
+                    for (int j = 0; j < P; ++j) up[j] = (!edge || Jl + j < g.n1y) ? a.prev[base + j] : 0.0;
+                }
                 if (tcl) {
                     #pragma unroll
                     for (int j = 0; j < P; ++j) mi[j] = mtab.v[r * P + j];
@@ -716,7 +737,9 @@ struct ScmOperator final : Operator {
     }
     // streaming step / apply of scalar 2D operators (k_scm2s): chunks of
     // chunk_nt row tiles per CTA; WAVECELL_B200_TILE2D=1 keeps the tile kernel
-    bool stream2d_off = getenv("WAVECELL_B200_TILE2D") && getenv("WAVECELL_B200_TILE2D")[0] == '1';
+    // measured slower than the tile kernel on config 2 (41-44 vs 25.5 us per
+    // step): opt-in with WAVECELL_B200_STREAM2D=1
+    bool stream2d_off = !(getenv("WAVECELL_B200_STREAM2D") && getenv("WAVECELL_B200_STREAM2D")[0] == '1');
     bool use_stream2d() const {
         return !stream2d_off && ncomp == 1 && part_active < 0 && !sub_active && !tile_cost.empty();
     }

@@ -87,15 +87,30 @@ struct MinvTab {
 #ifndef WCB3D_WY3
 #define WCB3D_WY3 7
 #endif
-__host__ __device__ constexpr int wy_for3(int P) { return P <= 2 ? 7 : P == 3 ? WCB3D_WY3 : 2; }
+// P = 3 runs the z-node-split kernel (k_scm3j, P warps per y cell row) by
+// default; WCB3D_JSPLIT=0 restores the one-warp-per-row kernel (k_scm3d)
+#ifndef WCB3D_JSPLIT
+#define WCB3D_JSPLIT 1
+#endif
+#ifndef WCB3D_WYJ
+#define WCB3D_WYJ 4
+#endif
+__host__ __device__ constexpr bool jsplit3(int P) { return WCB3D_JSPLIT && P == 3; }
+__host__ __device__ constexpr int wy_for3(int P) {
+    return jsplit3(P) ? WCB3D_WYJ : P <= 2 ? 7 : P == 3 ? WCB3D_WY3 : 2;
+}
 // resident CTAs per SM the launch bounds ask for
-__host__ __device__ constexpr int cpsm_for3(int P) { return P == 3 && WCB3D_WY3 >= 7 ? 1 : P <= 3 ? 2 : 1; }
+__host__ __device__ constexpr int cpsm_for3(int P) {
+    return jsplit3(P) ? 1 : P == 3 && WCB3D_WY3 >= 7 ? 1 : P <= 3 ? 2 : 1;
+}
 __host__ __device__ constexpr int la_for3(int P) { return P <= 3 ? P : 1; }
 
 template <int P>
 struct Str3 {
     static constexpr int WY = wy_for3(P);
-    static constexpr int NWARP = WY + 1;
+    // k_scm3d: one warp per y cell row (+ halo warp); k_scm3j: P warps per
+    // row, warp j owning the cell-local z node j of its lane's cell
+    static constexpr int NWARP = jsplit3(P) ? (WY + 1) * P : WY + 1;
     static constexpr int TZ = 32 * P;               // owned node columns (z)
     static constexpr int CO = P & 1;                // 16-byte TMA alignment offset
     static constexpr int UW = ((TZ + P + 1 + CO) + 1) / 2 * 2;
@@ -104,8 +119,8 @@ struct Str3 {
     static constexpr int S = P + 1 + la_for3(P);    // ring slots
     static constexpr int SLOT = (PLANE * 8 + 127) / 128 * 128 / 8;   // slot stride (doubles, 128 B aligned)
     static constexpr size_t RING_BYTES = (size_t)S * SLOT * 8;
-    static constexpr size_t OFF_XCH = (RING_BYTES + 127) / 128 * 128;   // [NWARP][P+1][P][32]
-    static constexpr size_t OFF_PREV = OFF_XCH + (size_t)NWARP * (P + 1) * P * 32 * 8;   // [P][WY*P][TZ]
+    static constexpr size_t OFF_XCH = (RING_BYTES + 127) / 128 * 128;   // [NWARP][P+1][P or 1][32]
+    static constexpr size_t OFF_PREV = OFF_XCH + (size_t)NWARP * (P + 1) * (jsplit3(P) ? 1 : P) * 32 * 8;   // [P][WY*P][TZ]
     static constexpr size_t PREV_BYTES = (size_t)P * WY * P * TZ * 8;
     static constexpr size_t OFF_BAR = OFF_PREV + (PREV_BYTES + 127) / 128 * 128;
     static constexpr size_t SMEM = OFF_BAR + 8 * (S + 1);

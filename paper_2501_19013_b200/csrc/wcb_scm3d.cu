@@ -429,6 +429,234 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
 }
 
+// z-node-split variant of k_scm3d (default for P = 3): the P warps of a y cell
+// row share its lanes' cells, warp j owning cell-local z node j (warp j = 0
+// also takes the left neighbour cell's node P).  Per thread the x pass keeps
+// Y[P+1][P] (x plane, y node) of one z node instead of all P, which cuts the
+// registers enough for P x (WY+1) warps per SM (15 vs 8 for P = 3).  Same
+// streaming scheme: TMA ring of node planes, a full cell row of look-ahead,
+// plane-P reuse, one exchange of the shared y node row per cell row, cut-cell
+// products from k_cut_pre, carry of x plane P, chunking-invariant sums.
+template <int P, int MODE>
+__global__ void __launch_bounds__(Str3<P>::NWARP * 32, 1)
+    k_scm3j(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_p, Scm3DGeo g,
+            Mats2<P> mt, MinvTab<P> mtab, double sk, StepArgs a) {
+    using T = Str3<P>;
+    constexpr int N = P + 1;
+    constexpr int WY = T::WY;
+    constexpr int S = T::S;
+    constexpr int L = N * N * N;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const double* ring = reinterpret_cast<const double*>(smem);
+    double* xch = reinterpret_cast<double*>(smem + T::OFF_XCH);   // [NWARP][N][32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
+    uint64_t* pbar = full + S;
+    const double* prv = reinterpret_cast<const double*>(smem + T::OFF_PREV);   // [P][WY*P][TZ]
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int yw = w / P, jz = w % P;   // y cell row slot (WY = halo), cell-local z node
+    const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z;
+    if (MODE == MODE_STEP && zs == 0 && yb == 0 && xc == 0) record_observers(a);
+    if (!g.cflags[(xc * g.n_yb + yb) * g.n_zs + zs]) return;
+    const int64_t K0 = zs * T::TZ;
+    const int64_t ey0 = yb * WY;
+    const int64_t exA = 1 + xc * g.xc;
+    const int64_t exE = exA + g.xc < g.ex_last + 1 ? exA + g.xc : g.ex_last + 1;
+    const int64_t G0 = (exA - 1) * P, G1 = (exE - 1) * P + P;
+    const bool halo = (yw == WY);
+    const int64_t ey = halo ? ey0 - 1 : ey0 + yw;
+    const int64_t ez = K0 / P + lane;
+    const int trow = (halo ? 0 : yw + 1) * P;
+    const bool producer = halo && jz == 0 && lane == 0;
+    auto issue = [&](int64_t gp) {
+        const int s = (int)((gp - G0) % S);
+        mbar_expect_tx(&full[s], (uint32_t)(T::PLANE * 8));
+        tma_load_3d(smem + (size_t)s * T::SLOT * 8, &tm_u, (int32_t)(K0 - P - T::CO + PADJ),
+                    (int32_t)(ey0 * P), (int32_t)(gp + P), &full[s]);
+    };
+    if (threadIdx.x == 0) {
+        #pragma unroll
+        for (int s = 0; s < S + 1; ++s) mbar_init(&full[s], 1);
+    }
+    __syncthreads();
+    if (producer)
+        for (int64_t gp = G0; gp <= G1 && gp < G0 + S; ++gp) issue(gp);
+    // z pass coefficients of this thread's node: m1[jz][d], k1[jz][d] (own
+    // cell, d = 0..P) and m1[P][d], k1[P][d] (left cell, jz = 0 only)
+    double zm[N], zk[N];
+    #pragma unroll
+    for (int d = 0; d < N; ++d) {
+        zm[d] = 0.0;
+        zk[d] = 0.0;
+        #pragma unroll
+        for (int q = 0; q < P; ++q)
+            if (q == jz) { zm[d] = mt.m[orb(P, q, d)]; zk[d] = mt.k[orb(P, q, d)]; }
+    }
+    const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
+    const int64_t s_ = g.n_e + 2;
+    const int up = halo ? WY : (yw == 0 ? WY : yw - 1);   // exchange source row slot
+    double Y[N][P];
+    #pragma unroll
+    for (int r = 0; r < N; ++r)
+        #pragma unroll
+        for (int b = 0; b < P; ++b) Y[r][b] = 0.0;
+    unsigned long long amp = 0ULL;
+    double Au[N], Bu[N], YP[N];
+    bool pxRR = false, pxRL = false;
+    for (int64_t ex = exA - 1; ex < exE; ++ex) {
+        uint8_t cRR = 0, cRL = 0, cUR = 0, cUL = 0;
+        if (ex >= 0 && ex < g.n_ex && ez <= g.n_e && ey >= -1 && ey <= g.n_e) {
+            const uint8_t* mrow = g.mask + ((ex + 1) * s_ + (ey + 1)) * s_;
+            if (ey < g.n_e && ey >= 0) { cRR = __ldg(mrow + ez + 1); cRL = __ldg(mrow + ez); }
+            if (!halo && ey >= 1) { cUR = __ldg(mrow - s_ + ez + 1); cUL = __ldg(mrow - s_ + ez); }
+        }
+        const double xRR = cRR == 1, xRL = (jz == 0 && cRL == 1) ? 1.0 : 0.0;
+        const bool cln = g.clean && cRR == 1 && ex >= 1 && __ldg(g.clean + (ex * g.n_e + ey) * g.n_e + ez) != 0;
+        const bool live = __syncthreads_or((cRR | cRL) != 0);
+        const bool reuse = ex > exA - 1 && !__syncthreads_or((cRR == 1) != pxRR || (cRL == 1) != pxRL);
+        pxRR = cRR == 1;
+        pxRL = cRL == 1;
+        if (producer && ex >= exA) {
+            #pragma unroll 1
+            for (int q = 0; q < P; ++q) {
+                const int64_t np = (ex - 1) * P + q + S;
+                if (np <= G1) issue(np);
+            }
+            if (MODE == MODE_STEP) {
+                mbar_expect_tx(pbar, (uint32_t)T::PREV_BYTES);
+                tma_load_3d(smem + T::OFF_PREV, &tm_p, (int32_t)(K0 + PADJ), (int32_t)(ey0 * P + P),
+                            (int32_t)(ex * P + P), pbar);
+            }
+        }
+        #pragma unroll
+        for (int r = 0; r < N; ++r) YP[r] = 0.0;
+        #pragma unroll
+        for (int c = 0; c < N; ++c) {
+            if (!(c == 0 && reuse)) {
+                const int64_t gp = ex * P + c;
+                const int slot = (int)((gp - G0) % S);
+                const double* plane = ring + (size_t)slot * T::SLOT;
+                #pragma unroll
+                for (int b = 0; b < N; ++b) { Au[b] = 0.0; Bu[b] = 0.0; }
+                mbar_wait(&full[slot], (uint32_t)(((gp - G0) / S) & 1));
+                if (live) {
+                    #pragma unroll
+                    for (int e = 0; e < N; ++e) {
+                        const double* own = plane + (size_t)(trow + e) * T::UW + T::CO + P + lane * P;
+                        // own cell: node jz from nodes 0..P (the right one is the next cell's node 0)
+                        double s1 = zm[P] * own[P], s2 = zk[P] * own[P];
+                        #pragma unroll
+                        for (int d = 0; d < P; ++d) {
+                            s1 = fma(zm[d], own[d], s1);
+                            s2 = fma(zk[d], own[d], s2);
+                        }
+                        double am = xRR * s1, ak = xRR * s2;
+                        if (jz == 0) {   // left cell: its node P is our node 0
+                            double l1 = mt.m[orb(P, P, P)] * own[0], l2 = mt.k[orb(P, P, P)] * own[0];
+                            #pragma unroll
+                            for (int d = 0; d < P; ++d) {
+                                l1 = fma(mt.m[orb(P, P, d)], own[d - P], l1);
+                                l2 = fma(mt.k[orb(P, P, d)], own[d - P], l2);
+                            }
+                            am = fma(xRL, l1, am);
+                            ak = fma(xRL, l2, ak);
+                        }
+                        #pragma unroll
+                        for (int b = 0; b < N; ++b) {
+                            if (halo && b < P) continue;
+                            Au[b] = fma(mt.m[orb(P, b, e)], am, Au[b]);
+                            Bu[b] = fma(mt.k[orb(P, b, e)], am, fma(mt.m[orb(P, b, e)], ak, Bu[b]));
+                        }
+                    }
+                }
+            }
+            #pragma unroll
+            for (int r = 0; r < N; ++r) {
+                YP[r] = fma(mt.k[orb(P, r, c)], Au[P], fma(mt.m[orb(P, r, c)], Bu[P], YP[r]));
+                if (!halo) {
+                    #pragma unroll
+                    for (int b = 0; b < P; ++b)
+                        Y[r][b] = fma(mt.k[orb(P, r, c)], Au[b], fma(mt.m[orb(P, r, c)], Bu[b], Y[r][b]));
+                }
+            }
+        }
+        {
+            double* xw = xch + (size_t)w * N * 32 + lane;
+            #pragma unroll
+            for (int r = 0; r < N; ++r) xw[r * 32] = YP[r];
+        }
+        __syncthreads();
+        if (!halo) {
+            const double* xr = xch + (size_t)(up * P + jz) * N * 32 + lane;
+            #pragma unroll
+            for (int r = 0; r < N; ++r) Y[r][0] += xr[r * 32];
+            // cut cells (K_o u_e / sk from k_cut_pre): own row, then the y-up
+            // row's local row P (our node row 0); left cell before own cell
+            const int64_t cbase = (ex * g.n_e + ey) * g.n_e + ez;
+            if (jz == 0 && cRL == 2) {
+                const double* o = g.cut_out + (int64_t)__ldg(g.cut_id + cbase - 1) * L;
+                #pragma unroll
+                for (int a2 = 0; a2 < N; ++a2)
+                    #pragma unroll
+                    for (int b = 0; b < P; ++b) Y[a2][b] += __ldcg(o + (a2 * N + b) * N + P);
+            }
+            if (cRR == 2) {
+                const double* o = g.cut_out + (int64_t)__ldg(g.cut_id + cbase) * L;
+                #pragma unroll
+                for (int a2 = 0; a2 < N; ++a2)
+                    #pragma unroll
+                    for (int b = 0; b < P; ++b) Y[a2][b] += __ldcg(o + (a2 * N + b) * N + jz);
+            }
+            if (jz == 0 && cUL == 2) {
+                const double* o = g.cut_out + (int64_t)__ldg(g.cut_id + cbase - g.n_e - 1) * L;
+                #pragma unroll
+                for (int a2 = 0; a2 < N; ++a2) Y[a2][0] += __ldcg(o + (a2 * N + P) * N + P);
+            }
+            if (cUR == 2) {
+                const double* o = g.cut_out + (int64_t)__ldg(g.cut_id + cbase - g.n_e) * L;
+                #pragma unroll
+                for (int a2 = 0; a2 < N; ++a2) Y[a2][0] += __ldcg(o + (a2 * N + P) * N + jz);
+            }
+            if (ex >= exA) {
+                if (MODE == MODE_STEP) mbar_wait(pbar, (uint32_t)((ex - exA) & 1));
+                const int64_t Kn = K0 + lane * P + jz;
+                #pragma unroll
+                for (int r = 0; r < P; ++r) {
+                    const int64_t I = ex * P + r;
+                    if (I >= g.row_hi) break;
+                    const double* pl = ring + (size_t)((I - G0) % S) * T::SLOT;
+                    #pragma unroll
+                    for (int b = 0; b < P; ++b) {
+                        const int64_t J = ey * P + b;
+                        if (J >= g.n1 || Kn >= g.n1) break;
+                        const int64_t base = (I + P) * g.pplane + (J + P) * g.prow + Kn + PADJ;
+                        if constexpr (MODE == MODE_APPLY) {
+                            a.out[base] = sk * Y[r][b];
+                        } else {
+                            const double u = pl[(size_t)(trow + b) * T::UW + T::CO + P + lane * P + jz];
+                            const bool src = base >= a.F.lo && base <= a.F.hi;
+                            const double fF = src ? f * source_at(a.F, base) : f * 0.0;
+                            const double mi = cln ? mtab.v[(r * P + b) * P + jz] : __ldg(a.minv + base);
+                            const double upv = prv[((size_t)r * WY * P + yw * P + b) * T::TZ + lane * P + jz];
+                            const double v = leapfrog(u, upv, sk * Y[r][b], mi, fF, a.dt2);
+                            a.out[base] = v;
+                            const unsigned long long bits = mi != 0.0 ? amp_bits(v) : 0ULL;
+                            amp = bits > amp ? bits : amp;
+                        }
+                    }
+                }
+            }
+            #pragma unroll
+            for (int b = 0; b < P; ++b) {
+                Y[0][b] = Y[P][b];
+                #pragma unroll
+                for (int r = 1; r < N; ++r) Y[r][b] = 0.0;
+            }
+        }
+    }
+    if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
+}
+
 // The node column z = n1-1 when n_e is a multiple of 32 (no strip lane owns
 // it).  Stage 1: the z contraction of the last cell column onto its node
 // z = n1-1 for every (x plane, y row): zline = (m1[P] . u, k1[P] . u).
@@ -534,9 +762,14 @@ template <int P, int MODE>
 void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map_p, const Scm3DGeo& g,
                   const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a) {
     using T = Str3<P>;
-    ensure_smem_attr((const void*)k_scm3d<P, MODE>, ctx->device, (size_t)T::SMEM);
     dim3 grid((unsigned)g.n_zs, (unsigned)g.n_yb, (unsigned)g.n_xc);
-    k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
+    if constexpr (jsplit3(P)) {
+        ensure_smem_attr((const void*)k_scm3j<P, MODE>, ctx->device, (size_t)T::SMEM);
+        k_scm3j<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
+    } else {
+        ensure_smem_attr((const void*)k_scm3d<P, MODE>, ctx->device, (size_t)T::SMEM);
+        k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
+    }
     ctx->launches++;
     if (g.n_e % 32 == 0) {
         WCB_REQUIRE(g.zline, "z-line buffer missing");

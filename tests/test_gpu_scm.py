@@ -173,15 +173,17 @@ def test_2d_streaming_kernel_bitwise_vs_tile_kernel(p, n_e, monkeypatch):
     M = prob.mass_matrix()
     x = np.random.default_rng(p).standard_normal(prob.n_dof)
     f = lambda t: ricker(t, 10.0)  # noqa: E731
+    lam, _ = max_gen_eig(prob.device_operator(), M, tol=1e-7, seed=0)
+    dt = 0.9 * 2.0 / np.sqrt(lam)
     outs = []
-    for env, nt in (("1", None), (None, "1"), (None, "3"), (None, "100000")):
-        monkeypatch.delenv("WAVECELL_B200_TILE2D", raising=False)
+    for env, nt in ((None, None), ("1", "1"), ("1", "3"), ("1", "100000")):
+        monkeypatch.delenv("WAVECELL_B200_STREAM2D", raising=False)
         if env:
-            monkeypatch.setenv("WAVECELL_B200_TILE2D", env)
+            monkeypatch.setenv("WAVECELL_B200_STREAM2D", env)
         if nt:
             monkeypatch.setenv("WAVECELL_B200_CHUNK_NT", nt)
         op = prob.device_operator()
-        r = cdm_run(M, op, prob.F_s, f, 0.2 / (n_e * p * p), 200)
+        r = cdm_run(M, op, prob.F_s, f, dt, 200)
         outs.append((op @ x, r.psi))
         op.close()
     K = prob.csr_stiffness()
