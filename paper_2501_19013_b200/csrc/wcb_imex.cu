@@ -20,6 +20,7 @@
 // depend on, sum in a fixed lane order and publish (release) their row -- one
 // launch per solve, deterministic results.
 #include "wcb_internal.cuh"
+#include "wcb_tma.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -55,6 +56,16 @@ struct TriSched {
     int depth = 3;                               // ring depth (levels in flight)
     bool recip = false;                          // sdiag holds 1/diag
     bool pf_ok = false;                          // k_trsv_pf fits (unknowns + level offsets in smem)
+    // k_trsv_ring: every level (split into pieces of <= PIECE_BYTES) packed as
+    // one 16-byte aligned segment [hdr | row ptrs | pivots | values | column
+    // slots], streamed by one producer warp into a shared-memory ring
+    bool ring_ok = false;
+    int ring_depth = 0;
+    int64_t max_pieces = 0;
+    DevBuf<unsigned char> blob;
+    DevBuf<int64_t> piece_off;   // byte offset of each piece's segment
+    DevBuf<int32_t> piece_bytes;
+    DevBuf<int32_t> comp_piece;  // n_comp + 1: offsets into the pieces
     DevBuf<int32_t> comp_order;  // launch order: components by decreasing level count
     DevBuf<int32_t> comp_rows;   // n_comp + 1: offsets into rows
     DevBuf<int32_t> comp_lvl;    // n_comp + 1: offsets into lvl_off
@@ -102,6 +113,76 @@ static std::vector<int64_t> factor_components(int64_t n, const wcb_lu* lu, int64
     }
     *n_comp = nc;
     return comp;
+}
+
+// Segment layout of one piece (rows [k0, k1) of one level, every offset a
+// multiple of 16 bytes): int32 hdr[4] = {nrow, k0, ne, 0}; int32 rptr[nrow+1]
+// (entry offsets within the piece); double pivot[nrow]; double val[ne];
+// int32 col[ne].  The whole piece is one bulk copy.
+constexpr int64_t TRSV_PIECE_BYTES = 24 * 1024;
+static inline int64_t pad16(int64_t b) { return (b + 15) / 16 * 16; }
+static inline int64_t piece_size(int64_t nrow, int64_t ne) {
+    return 16 + pad16(4 * (nrow + 1)) + pad16(8 * nrow) + pad16(8 * ne) + pad16(4 * ne);
+}
+static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp_rows,
+                        const std::vector<int32_t>& comp_lvl, const std::vector<int32_t>& lvl_off,
+                        const std::vector<int32_t>& sptr, const std::vector<double>& sdiag,
+                        const std::vector<double>& sval, const std::vector<int32_t>& slcol, cudaStream_t s) {
+    std::vector<int64_t> off;
+    std::vector<int32_t> bytes, cpiece(T.n_comp + 1, 0);
+    std::vector<unsigned char> blob;
+    int64_t maxp = 0;
+    bool ok = true;
+    for (int64_t c = 0; c < T.n_comp; ++c) {
+        cpiece[c] = (int32_t)off.size();
+        for (int32_t l = comp_lvl[c]; l < comp_lvl[c + 1]; ++l) {
+            int64_t k = lvl_off[l];
+            const int64_t e = lvl_off[l + 1];
+            while (k < e) {
+                // grow the piece row by row while it fits the slot
+                int64_t k1 = k + 1;
+                if (piece_size(1, sptr[k + 1] - sptr[k]) > TRSV_PIECE_BYTES) { ok = false; break; }
+                while (k1 < e && piece_size(k1 + 1 - k, sptr[k1 + 1] - sptr[k]) <= TRSV_PIECE_BYTES) ++k1;
+                const int64_t nrow = k1 - k, ne = sptr[k1] - sptr[k];
+                const int64_t sz = piece_size(nrow, ne);
+                const int64_t base = (int64_t)blob.size();
+                blob.resize(base + sz, 0);
+                unsigned char* p = blob.data() + base;
+                int32_t* hdr = reinterpret_cast<int32_t*>(p);
+                hdr[0] = (int32_t)nrow;
+                hdr[1] = (int32_t)k;
+                hdr[2] = (int32_t)ne;
+                int32_t* rp = reinterpret_cast<int32_t*>(p + 16);
+                for (int64_t q = 0; q <= nrow; ++q) rp[q] = sptr[k + q] - sptr[k];
+                double* dg = reinterpret_cast<double*>(p + 16 + pad16(4 * (nrow + 1)));
+                for (int64_t q = 0; q < nrow; ++q) dg[q] = sdiag[k + q];
+                double* vv = dg + pad16(8 * nrow) / 8;
+                std::memcpy(vv, sval.data() + sptr[k], 8 * ne);
+                int32_t* cc = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(vv) + pad16(8 * ne));
+                std::memcpy(cc, slcol.data() + sptr[k], 4 * ne);
+                off.push_back(base);
+                bytes.push_back((int32_t)sz);
+                k = k1;
+            }
+            if (!ok) break;
+        }
+        if (!ok) break;
+        maxp = std::max<int64_t>(maxp, (int64_t)off.size() - cpiece[c]);
+    }
+    T.ring_ok = false;
+    if (!ok || off.empty()) return;
+    cpiece[T.n_comp] = (int32_t)off.size();
+    const int64_t avail = (int64_t)TRSV_SMEM - T.max_size * 8 - 256;
+    T.ring_depth = (int)std::min<int64_t>(4, avail / TRSV_PIECE_BYTES);
+    if (T.ring_depth < 2) return;
+    T.max_pieces = maxp;
+    T.blob.alloc(blob.size(), s); T.blob.upload(blob.data(), blob.size(), s);
+    T.piece_off.alloc(off.size(), s); T.piece_off.upload(off.data(), off.size(), s);
+    T.piece_bytes.alloc(bytes.size(), s); T.piece_bytes.upload(bytes.data(), bytes.size(), s);
+    T.comp_piece.alloc(cpiece.size(), s); T.comp_piece.upload(cpiece.data(), cpiece.size(), s);
+    WCB_CUDA(cudaStreamSynchronize(s));
+    T.ring_ok = true;
+    (void)n;
 }
 
 static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_t* idx,
@@ -222,6 +303,7 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
     T.comp_order.alloc(std::max<int64_t>(n_comp, 1), s);
     T.comp_order.upload(co.data(), n_comp, s);
     WCB_CUDA(cudaStreamSynchronize(s));
+    pack_pieces(T, n, comp_rows, comp_lvl, lvl_off, sptr, sdiag, sval, slcol, s);
 }
 
 struct DevLU {
@@ -541,6 +623,101 @@ __global__ void __launch_bounds__(NW * 32) k_trsv_pf(
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) x[rows[k]] = xl[k - r0];
 }
 
+// Producer / consumer level solve (default): one CTA per component, the
+// unknowns in shared memory.  Warp 0 (one lane) streams the component's level
+// pieces into a ring of DEPTH slots with one bulk copy each (mbarrier
+// complete_tx), gated by "slot free" mbarriers; NC consumer warps solve a
+// piece (row groups of GW lanes, rows strided over the groups), meet at a
+// named barrier (x of the piece visible) and release the slot.  A level
+// costs one consumer barrier plus its rows; the staging never occupies the
+// consumers.  Same lane order and shuffle tree as k_trsv_comp (bitwise equal).
+template <int NC, int DEPTH>
+__global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
+    const int32_t* __restrict__ comp_order, const int32_t* __restrict__ comp_rows,
+    const int32_t* __restrict__ comp_piece, const int64_t* __restrict__ piece_off,
+    const int32_t* __restrict__ piece_bytes, const unsigned char* __restrict__ blob,
+    const int32_t* __restrict__ rows, const double* __restrict__ b, double* __restrict__ x, int max_size,
+    int recip) {
+    constexpr int GW = WCB_TRSV_GW;
+    constexpr int G = NC * 32 / GW;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+    uint64_t* empty = full + DEPTH;
+    unsigned char* ring = smraw + 128;
+    double* xl = reinterpret_cast<double*>(ring + (size_t)DEPTH * TRSV_PIECE_BYTES);
+    const int c = comp_order[blockIdx.x];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
+    const int q0 = comp_piece[c], nq = comp_piece[c + 1] - q0;
+    if (threadIdx.x == 0) {
+        for (int d = 0; d < DEPTH; ++d) {
+            mbar_init(&full[d], 1);
+            mbar_init(&empty[d], 1);
+        }
+    }
+    for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) xl[k - r0] = b[rows[k]];
+    __syncthreads();
+    if (warp == 0) {   // producer
+        if (lane == 0)
+            for (int q = 0; q < nq; ++q) {
+                const int d = q % DEPTH;
+                mbar_wait(&empty[d], (uint32_t)(((q / DEPTH) & 1) ^ 1));
+                const uint32_t nb = (uint32_t)piece_bytes[q0 + q];
+                mbar_expect_tx(&full[d], nb);
+                bulk_load(ring + (size_t)d * TRSV_PIECE_BYTES, blob + piece_off[q0 + q], nb, &full[d]);
+            }
+        __syncwarp();
+    } else {
+        const int ct = threadIdx.x - 32;
+        const int grp = ct / GW, l16 = lane % GW;
+        const unsigned hmask = (GW == 32 ? 0xffffffffu : ((1u << GW) - 1u)) << ((lane / GW) * GW);
+        for (int q = 0; q < nq; ++q) {
+            const int d = q % DEPTH;
+            mbar_wait(&full[d], (uint32_t)((q / DEPTH) & 1));
+            const unsigned char* pc = ring + (size_t)d * TRSV_PIECE_BYTES;
+            const int32_t* hdr = reinterpret_cast<const int32_t*>(pc);
+            const int nrow = hdr[0], k0 = hdr[1], ne = hdr[2];
+            const int32_t* rp = reinterpret_cast<const int32_t*>(pc + 16);
+            const double* dg = reinterpret_cast<const double*>(pc + 16 + ((4 * (nrow + 1) + 15) / 16) * 16);
+            const double* vv = dg + ((8 * nrow + 15) / 16) * 2;
+            const int32_t* cc = reinterpret_cast<const int32_t*>(reinterpret_cast<const unsigned char*>(vv) +
+                                                                 ((8 * (int64_t)ne + 15) / 16) * 16);
+            for (int k = grp; k < nrow; k += G) {
+                double sacc = 0.0;
+                const int p1 = rp[k + 1];
+                for (int j = rp[k] + l16; j < p1; j += GW) sacc = fma(vv[j], xl[cc[j]], sacc);
+                #pragma unroll
+                for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
+                if (l16 == 0) {
+                    const int i = k0 + k - r0;
+                    xl[i] = recip ? (xl[i] - sacc) * dg[k] : (xl[i] - sacc) / dg[k];
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");   // piece solved by every consumer
+            if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32_imex(&empty[d])) : "memory");
+        }
+    }
+    __syncthreads();
+    for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) x[rows[k]] = xl[k - r0];
+}
+
+template <int NC, int DEPTH>
+static void launch_trsv_ring(Context* ctx, const TriSched& T, const double* b, double* x) {
+    const size_t sm = 128 + (size_t)DEPTH * TRSV_PIECE_BYTES + (size_t)T.max_size * 8;
+    ensure_smem_attr((const void*)k_trsv_ring<NC, DEPTH>, ctx->device, sm);
+    k_trsv_ring<NC, DEPTH><<<(unsigned)T.n_comp, (NC + 1) * 32, sm, ctx->stream>>>(
+        T.comp_order.p, T.comp_rows.p, T.comp_piece.p, T.piece_off.p, T.piece_bytes.p, T.blob.p, T.rows.p, b, x,
+        (int)T.max_size, T.recip ? 1 : 0);
+}
+template <int NC>
+static void launch_trsv_ring_d(Context* ctx, const TriSched& T, const double* b, double* x) {
+    switch (T.ring_depth) {
+        case 2: launch_trsv_ring<NC, 2>(ctx, T, b, x); break;
+        case 3: launch_trsv_ring<NC, 3>(ctx, T, b, x); break;
+        default: launch_trsv_ring<NC, 4>(ctx, T, b, x); break;
+    }
+}
+
 template <int NW>
 static void launch_trsv_pf(Context* ctx, const TriSched& T, const double* b, double* x) {
     const size_t sm = (size_t)T.max_size * 8 + (size_t)(T.max_levels + 1) * 8;
@@ -551,10 +728,22 @@ static void launch_trsv_pf(Context* ctx, const TriSched& T, const double* b, dou
 }
 
 static void launch_trsv(Context* ctx, const TriSched& T, const double* b, double* x) {
-    static const int nw = [] {
+    static const int nw = [] {   // > 0: k_trsv_pf with nw warps (experimental)
         const char* e = getenv("WAVECELL_B200_TRSV_NW");
+        return e ? atoi(e) : 0;
+    }();
+    static const int nc = [] {   // consumer warps of k_trsv_ring; 0: level kernel k_trsv_comp
+        const char* e = getenv("WAVECELL_B200_TRSV_NC");
         return e ? atoi(e) : 16;
     }();
+    if (nw <= 0 && nc > 0 && T.ring_ok) {
+        switch (nc) {
+            case 4: launch_trsv_ring_d<4>(ctx, T, b, x); return;
+            case 8: launch_trsv_ring_d<8>(ctx, T, b, x); return;
+            case 24: launch_trsv_ring_d<24>(ctx, T, b, x); return;
+            default: launch_trsv_ring_d<16>(ctx, T, b, x); return;
+        }
+    }
     if (T.pf_ok && (nw > 0 || !T.ok)) {
         switch (nw) {
             case 4: launch_trsv_pf<4>(ctx, T, b, x); return;
@@ -742,7 +931,7 @@ static void lu_solve(Context* ctx, wcb_imex_plan* P, DevLU& F, const double* b, 
     if (!n) return;
     k_perm_rows<<<grid1(ctx, n), 256, 0, s>>>(n, F.perm_r.p, b, P->y.p);
     // forward: L w = y  (into z), backward: U v = w (into y)
-    if ((F.Ls.ok || F.Ls.pf_ok) && (F.Us.ok || F.Us.pf_ok)) {
+    if ((F.Ls.ok || F.Ls.pf_ok || F.Ls.ring_ok) && (F.Us.ok || F.Us.pf_ok || F.Us.ring_ok)) {
         launch_trsv(ctx, F.Ls, P->y.p, P->z.p);
         launch_trsv(ctx, F.Us, P->z.p, x);
         ctx->launches += 3;
@@ -804,6 +993,7 @@ int wcb_imex_plan_create(wcb_operator* o, int64_t n_c, const int64_t* c_idx, int
         P->c_state.alloc(cs.size(), s); P->c_state.upload(cs.data(), n_c, s);
         P->Fc.alloc(Fc.size(), s); P->Fc.upload(Fc.data(), n_c, s);
         if (n_c) op->set_apply_subset(c_idx, n_c);   // K rows of c only, per step
+        if (n_c && !getenv("WAVECELL_B200_NO_ROW_APPLY")) op->set_row_subset(c_idx, n_c);
         if (n_c && n_d && !getenv("WAVECELL_B200_NO_IMEX_OVERLAP") && op->set_step_split(c_idx, n_c)) {
             int lo_prio = 0, hi_prio = 0;
             WCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
@@ -1062,8 +1252,10 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
                 if (nc > 0) a.amp = P->amp_scratch.p;   // amplitude taken below
                 op->cdm_step(a);
                 if (nc > 0) {
-                    op->apply_subset(cur[r], P->T.p);   // (K psi_k)_c
-                    k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
+                    if (!op->apply_rows(cur[r], P->Kc.p)) {   // (K psi_k)_c
+                        op->apply_subset(cur[r], P->T.p);
+                        k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
+                    }
                     k_c_rhs<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->Fc.p, P->ft_k.p + 1, k, P->Kc.p, P->rhs.p);
                     lu_solve(ctx, P, P->Mcc, P->rhs.p, P->y.p);
                     k_c_cdm_update<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->Mcc.perm_c.p, P->y.p,
@@ -1091,8 +1283,10 @@ static void imex_run_group(std::vector<wcb_imex_plan*>& Ps, double f0, const dou
                 k_c_predict<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->psi_c.p, P->v_c.p, P->a_c.p,
                                                            dt, c1, c2, prev[r], P->pred.p, P->vpred.p);
                 // 3. rhs_c with updated d and predicted c
-                op->apply_subset(prev[r], P->T.p);   // tiles owning c rows only
-                k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
+                if (!op->apply_rows(prev[r], P->Kc.p)) {   // cells touching c rows only
+                    op->apply_subset(prev[r], P->T.p);   // tiles owning c rows
+                    k_gather_rows<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->c_state.p, P->T.p, P->Kc.p);
+                }
                 k_c_rhs<<<grid1(ctx, nc), 256, 0, s>>>(nc, P->Fc.p, P->ft_new.p, k, P->Kc.p, P->rhs.p);
                 ctx->launches += 3;
                 // 4. a_c = S^-1 rhs_c (z permuted) ; 5. corrector

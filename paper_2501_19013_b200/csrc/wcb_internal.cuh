@@ -297,6 +297,11 @@ struct Operator {
     // set_apply_subset (other rows of y are unspecified); default: full apply
     virtual bool set_apply_subset(const int64_t* /*compact_ids*/, int64_t /*n*/) { return false; }
     virtual void apply_subset(const double* x, double* y) { apply(x, y); }
+    // (K x) at a fixed set of DOF rows, in the order given (IMEX c rows): the
+    // operator may restrict the work to the cells touching those rows.
+    // apply_rows returns false when not supported (caller: apply_subset + gather)
+    virtual bool set_row_subset(const int64_t* /*compact_ids*/, int64_t /*n*/) { return false; }
+    virtual bool apply_rows(const double* /*x_state*/, double* /*out_rows*/) { return false; }
     // split of the fused step into tiles whose input footprint holds none of
     // the given DOFs (part 0, "far") and the rest (part 1, "near"), so the far
     // part of step k+1 can overlap the implicit solve of step k; false when

@@ -667,6 +667,53 @@ __global__ void __launch_bounds__(Tile2S<P>::NWARP * 32, minb_2s(P)) k_scm2s(
     if constexpr (MODE == MODE_STEP) warp_amp_max(amp, a.amp);
 }
 
+// ---------------------------------------------------------------------------
+// K x at a set of DOF rows (IMEX c rows) from the cells touching them only:
+// one warp per cell computes the dense element product y_e = K_e u_e (the
+// shared uncut element matrix in shared memory, or the cell's cut matrix),
+// then every row sums its cells' contributions in ascending cell order.
+template <int L>
+__global__ void __launch_bounds__(256) k_rc_cells(int64_t n_cells, const int64_t* __restrict__ base,
+                                                  const int32_t* __restrict__ cutid, const double* __restrict__ Kref,
+                                                  const double* __restrict__ KT, int64_t pitch, int64_t plane,
+                                                  int P, int ncomp, double sk, const double* __restrict__ x,
+                                                  double* __restrict__ out) {
+    __shared__ double Ks[L * L];
+    __shared__ double us[8][L];
+    for (int i = threadIdx.x; i < L * L; i += blockDim.x) Ks[i] = Kref[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int N = P + 1;
+    for (int64_t c = (int64_t)blockIdx.x * 8 + w; c < n_cells; c += (int64_t)gridDim.x * 8) {
+        const int64_t b0 = base[c];
+        for (int m = lane; m < L; m += 32) {
+            const int comp = m / (N * N), a = (m / N) % N, bb = m % N;
+            us[w][m] = x[b0 + comp * plane + a * pitch + bb];
+        }
+        __syncwarp();
+        const int32_t id = cutid[c];
+        for (int r = lane; r < L; r += 32) {
+            double t = 0.0;
+            if (id < 0) {
+                for (int m = 0; m < L; ++m) t = fma(Ks[r * L + m], us[w][m], t);
+            } else {
+                const double* K = KT + (int64_t)id * L * L;
+                for (int m = 0; m < L; ++m) t = fma(__ldg(K + m * L + r), us[w][m], t);
+            }
+            out[c * L + r] = sk * t;
+        }
+        __syncwarp();
+    }
+}
+__global__ void k_rc_rows(int64_t n_rows, const int32_t* __restrict__ ptr, const int64_t* __restrict__ src,
+                          const double* __restrict__ cell_out, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = ptr[i]; j < ptr[i + 1]; ++j) s += cell_out[src[j]];
+        y[i] = s;
+    }
+}
+
 
 #include "wcb_ela2d.cuh"
 
@@ -1250,6 +1297,129 @@ struct ScmOperator final : Operator {
         dispatch2d<MODE_APPLY>(a);
         sub_active = false;
         WCB_CHECK_LAUNCH();
+    }
+    // IMEX c rows by cells (set_row_subset / apply_rows)
+    int64_t rc_n_cells = 0, rc_n_rows = 0;
+    DevBuf<int64_t> rc_base, rc_src;
+    DevBuf<int32_t> rc_cutid, rc_ptr;
+    DevBuf<double> rc_Kref, rc_out;
+    bool set_row_subset(const int64_t* ids, int64_t n_ids) override {
+        if (dim != 2) return false;
+        const int P = p, N = p + 1;
+        const int Lr = ncomp * N * N;
+        if (Lr != 25 && Lr != 72 && Lr != 16 && Lr != 9 && Lr != 4 && Lr != 36 && Lr != 49 && Lr != 8 &&
+            Lr != 18 && Lr != 32 && Lr != 50)
+            return false;
+        // cells touching each row's node: local (ex, ey) with ex*P <= I <= ex*P+P
+        std::vector<std::pair<int64_t, int>> contrib;   // (cell key, local row) per row, flattened
+        std::vector<int32_t> ptr(n_ids + 1, 0);
+        std::vector<int64_t> cells;
+        std::vector<std::vector<std::pair<int64_t, int>>> per(n_ids);
+        const int64_t ms_ = n_e + 2;
+        std::vector<uint8_t> hmask;
+        {
+            hmask.resize(mask.n);
+            WCB_CUDA(cudaMemcpy(hmask.data(), mask.p, mask.n, cudaMemcpyDeviceToHost));
+        }
+        for (int64_t k = 0; k < n_ids; ++k) {
+            const int64_t st = sidx[ids[k]];
+            const int comp = (int)(st / (plane ? plane : INT64_MAX));
+            const int64_t s0 = st - comp * plane;
+            const int64_t I = s0 / pitch - P, J = s0 % pitch - PADJ;   // local node coordinates
+            for (int64_t ex = I / P - 1; ex <= I / P; ++ex) {
+                if (ex < 0 || ex >= n_ex || I < ex * P || I > ex * P + P) continue;
+                for (int64_t ey = J / P - 1; ey <= J / P; ++ey) {
+                    if (ey < 0 || ey >= n_e || J < ey * P || J > ey * P + P) continue;
+                    if (hmask[(ex + 1) * ms_ + ey + 1] == 0) continue;
+                    const int a = (int)(I - ex * P), b = (int)(J - ey * P);
+                    per[k].emplace_back(ex * n_e + ey, comp * N * N + a * N + b);
+                    cells.push_back(ex * n_e + ey);
+                }
+            }
+        }
+        std::sort(cells.begin(), cells.end());
+        cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
+        std::vector<int64_t> src, cbase(cells.size());
+        std::vector<int32_t> cid(cells.size(), -1);
+        std::vector<int32_t> hcid(cut_id.n);
+        WCB_CUDA(cudaMemcpy(hcid.data(), cut_id.p, cut_id.n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        for (size_t q = 0; q < cells.size(); ++q) {
+            const int64_t ex = cells[q] / n_e, ey = cells[q] % n_e;
+            cbase[q] = (ex * P + P) * pitch + ey * P + PADJ;
+            cid[q] = hcid[cells[q]];
+        }
+        for (int64_t k = 0; k < n_ids; ++k) {
+            std::sort(per[k].begin(), per[k].end());
+            for (auto& e : per[k]) {
+                const int64_t q = std::lower_bound(cells.begin(), cells.end(), e.first) - cells.begin();
+                src.push_back(q * Lr + e.second);
+            }
+            ptr[k + 1] = (int32_t)src.size();
+        }
+        // uncut element matrix / sk (the kernels scale by sk, as the cut KT)
+        std::vector<double> Kr((size_t)Lr * Lr, 0.0);
+        const double l2m = lam + 2.0 * mu;
+        for (int r = 0; r < Lr; ++r)
+            for (int m = 0; m < Lr; ++m) {
+                const int cr = r / (N * N), ar = (r / N) % N, br = r % N;
+                const int cm = m / (N * N), am = (m / N) % N, bm = m % N;
+                const double Kxx = k1[ar * N + am] * m1[br * N + bm];   // x derivatives
+                const double Kyy = m1[ar * N + am] * k1[br * N + bm];
+                double v;
+                if (ncomp == 1) {
+                    v = Kxx + Kyy;
+                } else {
+                    // Kxy[(a,b),(c,d)] = g1[a][c] g1[d][b]; Kuv = lam Kxy + mu Kxy^T
+                    const double Kxy = g1[ar * N + am] * g1[bm * N + br];
+                    const double KxyT = g1[am * N + ar] * g1[br * N + bm];
+                    if (cr == 0 && cm == 0) v = l2m * Kxx + mu * Kyy;
+                    else if (cr == 1 && cm == 1) v = mu * Kxx + l2m * Kyy;
+                    else if (cr == 0) v = lam * Kxy + mu * KxyT;
+                    else v = lam * KxyT + mu * Kxy;   // (Kuv)^T
+                }
+                Kr[(size_t)r * Lr + m] = v;
+            }
+        cudaStream_t st = ctx->stream;
+        rc_n_cells = (int64_t)cells.size();
+        rc_n_rows = n_ids;
+        rc_base.alloc(std::max<int64_t>(rc_n_cells, 1), st); rc_base.upload(cbase.data(), cbase.size(), st);
+        rc_cutid.alloc(std::max<int64_t>(rc_n_cells, 1), st); rc_cutid.upload(cid.data(), cid.size(), st);
+        rc_ptr.alloc(ptr.size(), st); rc_ptr.upload(ptr.data(), ptr.size(), st);
+        rc_src.alloc(std::max<size_t>(src.size(), 1), st); rc_src.upload(src.data(), src.size(), st);
+        rc_Kref.alloc(Kr.size(), st); rc_Kref.upload(Kr.data(), Kr.size(), st);
+        rc_out.alloc(std::max<int64_t>(rc_n_cells, 1) * Lr, st);
+        WCB_CUDA(cudaStreamSynchronize(st));
+        return true;
+    }
+    template <int L>
+    void launch_rc(const double* x, double* out) {
+        const int64_t blocks = std::min<int64_t>(ceil_div(rc_n_cells, 8), (int64_t)ctx->sm_count * 8);
+        if (rc_n_cells)
+            k_rc_cells<L><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, ctx->stream>>>(
+                rc_n_cells, rc_base.p, rc_cutid.p, rc_Kref.p, KT.p, pitch, plane, p, ncomp, ncomp == 1 ? sk : 1.0, x,
+                rc_out.p);
+        k_rc_rows<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rc_n_rows, 256), (int64_t)ctx->sm_count * 8)),
+                    256, 0, ctx->stream>>>(rc_n_rows, rc_ptr.p, rc_src.p, rc_out.p, out);
+        ctx->launches += 2;
+    }
+    bool apply_rows(const double* x, double* out) override {
+        if (!rc_n_rows) return false;
+        switch (ncomp * (p + 1) * (p + 1)) {
+            case 4: launch_rc<4>(x, out); break;
+            case 8: launch_rc<8>(x, out); break;
+            case 9: launch_rc<9>(x, out); break;
+            case 16: launch_rc<16>(x, out); break;
+            case 18: launch_rc<18>(x, out); break;
+            case 25: launch_rc<25>(x, out); break;
+            case 32: launch_rc<32>(x, out); break;
+            case 36: launch_rc<36>(x, out); break;
+            case 49: launch_rc<49>(x, out); break;
+            case 50: launch_rc<50>(x, out); break;
+            case 72: launch_rc<72>(x, out); break;
+            default: return false;
+        }
+        WCB_CHECK_LAUNCH();
+        return true;
     }
     double step_bytes() const override { return bytes_step; }
     bool halo(int64_t* h) const override {
