@@ -153,6 +153,9 @@ int wcb_operator_apply(wcb_operator* op, const double* x, double* y);
  * sent to the next slab, out[6] rows sent (p or 0), out[7] row sent to the
  * previous slab (1 row).  Returns 1 for a slab of a larger grid, else 0. */
 int wcb_operator_halo(const wcb_operator* op, int64_t* out8);
+/* Name of the kernel(s) one fused time step of this operator launches
+ * (NUL-terminated, truncated to cap bytes) -- for bench and profile labels. */
+int wcb_operator_step_kernel(const wcb_operator* op, char* out, int64_t cap);
 
 /* ---- multi-GPU slabs: NCCL communicator per context -------- */
 /* imex_run over consecutive x slabs of one plane-strain grid emulated in one

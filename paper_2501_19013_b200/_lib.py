@@ -36,7 +36,7 @@ EXPORTS = (
     "wcb_imex_plan_destroy", "wcb_imex_plan_run", "wcb_dist_unique_id", "wcb_dist_init",
     "wcb_dist_finalize", "wcb_cdm_group_run", "wcb_cdm_plan_step_bytes", "wcb_imex_group_run",
     "wcb_csr_diagonal_check", "wcb_mass_plan_create", "wcb_imex_plan_cdm_run",
-    "wcb_imex_plan_max_gen_eig",
+    "wcb_imex_plan_max_gen_eig", "wcb_operator_step_kernel",
 )
 
 _p = C.c_void_p
@@ -98,6 +98,7 @@ _SIGS = {
     "wcb_operator_n": (_i64, [_p]),
     "wcb_operator_apply": (C.c_int, [_p, _dp, _dp]),
     "wcb_operator_halo": (C.c_int, [_p, _i64p]),
+    "wcb_operator_step_kernel": (C.c_int, [_p, C.c_char_p, _i64]),
     "wcb_max_gen_eig": (C.c_int, [_p, _dp, _dp, _d, _i64, _dp, _i64p]),
     "wcb_max_gen_eig_sub": (C.c_int, [_p, _dp, _i64, _i64p, _dp, _d, _i64, _dp, _i64p]),
     "wcb_cdm_plan_create": (C.c_int, [_p, _dp, _dp, C.POINTER(Observer), C.POINTER(_p)]),

@@ -754,19 +754,51 @@ namespace wcb {
 
 // Halo exchange of state buffers cur[r] between consecutive slabs: device
 // copies for an emulated group (one context), NCCL for one plan per process.
-static void exchange_halos(std::vector<wcb_cdm_plan*>& Ps, std::vector<double*>& cur) {
+static void exchange_halos(std::vector<wcb_cdm_plan*>& Ps, std::vector<double*>& cur,
+                           cudaStream_t on = nullptr) {
     const size_t n = Ps.size();
+    Context* ctx = Ps[0]->op->ctx;
+    cudaStream_t s = on ? on : ctx->stream;
     if (n == 1) {
         int64_t h[8];
         Operator* op = Ps[0]->op;
-        Context* ctx = op->ctx;
-        if (dist_slab(op) && op->halo(h)) nccl_exchange_halo(ctx, cur[0], h, op->halo_nplanes, op->halo_pstride);
+        if (dist_slab(op) && op->halo(h)) {
+            cudaStream_t save = ctx->stream;
+            ctx->stream = s;
+            try {
+                nccl_exchange_halo(ctx, cur[0], h, op->halo_nplanes, op->halo_pstride);
+            } catch (...) {
+                ctx->stream = save;
+                throw;
+            }
+            ctx->stream = save;
+        }
         return;
     }
     std::vector<Operator*> ops;
     for (auto* P : Ps) ops.push_back(P->op);
-    copy_exchange_halo(ops, cur, Ps[0]->op->ctx->stream);
+    copy_exchange_halo(ops, cur, s);
 }
+
+// RAII second stream + events for the halo exchange overlapped with the
+// interior part of a slab step
+struct HaloOverlap {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t e_b = nullptr, e_x = nullptr;
+    explicit HaloOverlap(int device) {
+        WCB_CUDA(cudaSetDevice(device));
+        int lo = 0, hi = 0;
+        WCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        WCB_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi));   // the exchange first
+        WCB_CUDA(cudaEventCreateWithFlags(&e_b, cudaEventDisableTiming));
+        WCB_CUDA(cudaEventCreateWithFlags(&e_x, cudaEventDisableTiming));
+    }
+    ~HaloOverlap() {
+        if (s2) { cudaStreamSynchronize(s2); cudaStreamDestroy(s2); }
+        if (e_b) cudaEventDestroy(e_b);
+        if (e_x) cudaEventDestroy(e_x);
+    }
+};
 
 // The CDM loop of src/timeint.py:159-193 for one plan or a group of slab
 // plans sharing one context (emulated ranks) or one plan per process with an
@@ -878,9 +910,42 @@ static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, do
         checked = upto;
         return false;
     };
+    // slab steps: the node rows the neighbours need first, their exchange on a
+    // second stream while the interior rows are computed (north star (d));
+    // WAVECELL_B200_HALO_OVERLAP=0 runs step and exchange back to back
+    bool overlap = !(getenv("WAVECELL_B200_HALO_OVERLAP") && getenv("WAVECELL_B200_HALO_OVERLAP")[0] == '0');
+    for (size_t r = 0; r < G && overlap; ++r) {
+        int64_t h[8];
+        overlap = (G > 1 || dist_slab(Ps[r]->op)) && Ps[r]->op->halo(h) && Ps[r]->op->halo_split_ready();
+    }
+    std::unique_ptr<HaloOverlap> hov;
+    if (overlap) hov.reset(new HaloOverlap(ctx->device));
     WCB_CUDA(cudaEventRecord(ctx->ev0, s));
     bool diverged = false;
     for (int64_t k = 0; k < n_t; ++k) {
+        if (overlap) {
+            for (size_t r = 0; r < G; ++r) {
+                StepArgs& a = args[r];
+                a.cur = cur[r];
+                a.prev = prev[r];
+                a.out = prev[r];
+                a.k = k;
+                a.amp = Ps[r]->amp.p + (k + 1);
+                Ps[r]->op->cdm_step_halo_part(a, 0);   // exchanged rows (+ observers of psi_k)
+            }
+            WCB_CUDA(cudaEventRecord(hov->e_b, s));
+            WCB_CUDA(cudaStreamWaitEvent(hov->s2, hov->e_b, 0));
+            exchange_halos(Ps, prev, hov->s2);        // psi_{k+1} halos, overlapped with ...
+            WCB_CUDA(cudaEventRecord(hov->e_x, hov->s2));
+            for (size_t r = 0; r < G; ++r) Ps[r]->op->cdm_step_halo_part(args[r], 1);   // ... the interior
+            WCB_CUDA(cudaStreamWaitEvent(s, hov->e_x, 0));
+            for (size_t r = 0; r < G; ++r) std::swap(cur[r], prev[r]);
+            if ((k + 1) % check_every == 0) {
+                WCB_CHECK_LAUNCH();
+                if (inspect(k + 1)) { diverged = true; break; }
+            }
+            continue;
+        }
         for (size_t r = 0; r < G; ++r) {
             StepArgs& a = args[r];
             a.cur = cur[r];
@@ -1150,6 +1215,13 @@ int wcb_cdm_plan_step_bytes(const wcb_cdm_plan* plan, double* out) {
 int wcb_operator_halo(const wcb_operator* op, int64_t* out8) {
     if (!op || !out8) return WCB_E_ARG;
     return op->op->halo(out8) ? 1 : 0;
+}
+
+int wcb_operator_step_kernel(const wcb_operator* op, char* out, int64_t cap) {
+    if (!op || !out || cap <= 0) return WCB_E_ARG;
+    const std::string k = op->op->step_kernel();
+    std::snprintf(out, (size_t)cap, "%s", k.c_str());
+    return WCB_OK;
 }
 
 }  // extern "C"

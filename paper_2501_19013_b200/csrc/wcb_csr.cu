@@ -161,6 +161,10 @@ struct CsrOperator final : Operator {
     double sell_bytes = 0.0;   // matrix bytes per apply in the SELL layout
 
     const char* name() const override { return "csr"; }
+    std::string step_kernel() const override {
+        return sell ? "k_sell<true> (SELL-32 slices, shared-stencil types 1/2, fused CDM update)"
+                    : "k_csr_cdm<" + std::to_string(tpr) + ",256> (CSR, fused CDM update)";
+    }
     const std::vector<int64_t>& state_index() const override { return sidx; }
 
     void scatter(const double* src, double* dst) override {

@@ -284,6 +284,8 @@ struct Operator {
     int64_t n_state = 0;    // length of a state vector on the device
     virtual ~Operator() = default;
     virtual const char* name() const = 0;
+    // the kernel(s) one fused time step launches (bench / profile labels)
+    virtual std::string step_kernel() const { return name(); }
     // state index of each compact DOF (host copy, for observers / sources)
     virtual const std::vector<int64_t>& state_index() const = 0;
     // compact <-> state (state slots without a DOF are zero)
@@ -307,6 +309,11 @@ struct Operator {
     // part of step k+1 can overlap the implicit solve of step k; false when
     // the operator cannot split (then only cdm_step is used)
     virtual bool set_step_split(const int64_t* /*ids*/, int64_t /*n*/) { return false; }
+    // slab steps overlapped with the halo exchange: part 0 computes the node
+    // rows the neighbours need (and everything else that must precede the
+    // exchange), part 1 the interior.  false: not split (cdm_step does all).
+    virtual bool halo_split_ready() { return false; }
+    virtual void cdm_step_halo_part(const StepArgs& a, int part) { if (part == 0) cdm_step(a); }
     virtual void cdm_step_part(const StepArgs& a, int part) { if (part == 1) cdm_step(a); }
     // the plan's 1/m state vector (fixed for the plan's lifetime): operators
     // may precompute which cells read it (default: every node loads 1/m)

@@ -767,6 +767,14 @@ struct ScmOperator final : Operator {
     double bytes_step = 0.0;
 
     const char* name() const override { return "scm"; }
+    std::string step_kernel() const override {
+        const std::string P = std::to_string(p);
+        if (dim == 3)
+            return std::string(jsplit3(p) ? "k_scm3j<" : "k_scm3d<") + P + ",STEP> + k_cut_pre<" + P + ">" +
+                   (n_e % 32 == 0 ? " + k_scm3d_zline/zcol" : "");
+        if (ncomp == 2) return "k_ela2d<" + P + ",STEP> (plane strain, fused CDM update)";
+        return (stream2d_off ? "k_scm2d<" : "k_scm2s<") + P + ",STEP> (fused CDM update)";
+    }
     const std::vector<int64_t>& state_index() const override { return sidx; }
     void scatter(const double* src, double* dst) override { launch_scatter(ctx, n, d_sidx.p, src, dst); }
     void gather(const double* src, double* dst) override { launch_gather(ctx, n, d_sidx.p, src, dst); }
@@ -876,12 +884,18 @@ struct ScmOperator final : Operator {
                     mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
-        if (use_stream2d()) {
+        if (use_stream2d() && halo_part < 0) {
             launch2st<P, MODE>(a, mt);
             return;
         }
         const int32_t* ord = part_active >= 0 ? order_part[part_active].p : sub_active ? order_sub.p : order.p;
-        const int64_t n_ord = part_active >= 0 ? n_order_part[part_active] : sub_active ? n_order_sub : n_order;
+        int64_t n_ord = part_active >= 0 ? n_order_part[part_active] : sub_active ? n_order_sub : n_order;
+        StepArgs a2 = a;
+        if (MODE == MODE_STEP && halo_part >= 0) {   // slab step split around the halo exchange
+            ord = order_halo[halo_part].p;
+            n_ord = n_order_halo[halo_part];
+            if (halo_part == 1) a2.obs_out = nullptr;   // observers recorded once, by part 0
+        }
         if (!n_ord) return;
         Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, ord, n_strips, n_rtiles, pitch};
         dim3 grid((unsigned)n_ord);
@@ -905,9 +919,9 @@ struct ScmOperator final : Operator {
             at[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            WCB_CUDA(cudaLaunchKernelEx(&cfg, k_scm2d<P, MODE>, mu, mp, mm, g, mt, tab, sk, a));
+            WCB_CUDA(cudaLaunchKernelEx(&cfg, k_scm2d<P, MODE>, mu, mp, mm, g, mt, tab, sk, a2));
         } else {
-            k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(mu, mp, mm, g, mt, tab, sk, a);
+            k_scm2d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(mu, mp, mm, g, mt, tab, sk, a2);
         }
         ctx->launches++;
     }
@@ -1054,7 +1068,7 @@ struct ScmOperator final : Operator {
                     mt.m[orb(P, i, j)] = m1[i * (P + 1) + j];
                     mt.k[orb(P, i, j)] = k1[i * (P + 1) + j];
                 }
-        launch_cut_pre<P>(ctx, n_cut, KP.p, cut_base.p, pplane, pitch, a.cur, cut_out.p);
+        if (halo_part != 1) launch_cut_pre<P>(ctx, n_cut, KP.p, cut_base.p, pplane, pitch, a.cur, cut_out.p);
         Scm3DGeo g = geo3();
         MinvTab<P> tab{};
         if (MODE == MODE_STEP && a.minv && a.minv == minv_bound && clean.p) {
@@ -1062,7 +1076,8 @@ struct ScmOperator final : Operator {
             for (int i = 0; i < P * P * P; ++i) tab.v[i] = minv_tab[i];
         }
         const CUtensorMap& mu = state_map3<P>(a.cur);
-        launch_scm3d<P, MODE>(ctx, mu, MODE == MODE_STEP ? prev_map3<P>(a.prev) : mu, g, mt, tab, sk, a);
+        launch_scm3d<P, MODE>(ctx, mu, MODE == MODE_STEP ? prev_map3<P>(a.prev) : mu, g, mt, tab, sk, a,
+                              MODE == MODE_STEP ? halo_part : -1);
     }
     Scm3DGeo geo3() const {
         return Scm3DGeo{n_ex, row_lo, row_hi, n_e, n1, pitch, pplane, mask.p, cut_id.p, cut_out.p, cflags.p,
@@ -1296,6 +1311,48 @@ struct ScmOperator final : Operator {
         a.out = y;
         dispatch2d<MODE_APPLY>(a);
         sub_active = false;
+        WCB_CHECK_LAUNCH();
+    }
+    // slab step split around the halo exchange (cdm_step_halo_part)
+    int halo_part = -1;
+    bool halo_split_built = false;
+    DevBuf<int32_t> order_halo[2];           // 2D: tiles writing exchanged rows / the rest
+    int64_t n_order_halo[2] = {0, 0};
+    bool halo_split_ready() override {
+        int64_t h[8];
+        if (!halo(h) || ncomp != 1) return false;
+        if (dim == 3) return n_xc >= 3;
+        if (!halo_split_built) {
+            // tiles holding an owned node row sent to a neighbour: the first
+            // owned row (-> previous slab) and the last p owned rows (-> next)
+            const int64_t TI = (int64_t)rpe_for(p) * p;
+            std::vector<int32_t> part[2];
+            for (int32_t t : order_h) {
+                const int64_t rt = t % n_rtiles;
+                const int64_t I0 = row_lo + rt * TI, I1 = std::min<int64_t>(I0 + TI, row_hi);
+                const bool sends = (has_top && I0 <= row_lo && row_lo < I1) ||
+                                   (!owns_last && I1 > row_hi - p);
+                part[sends ? 0 : 1].push_back(t);
+            }
+            for (int q = 0; q < 2; ++q) {
+                n_order_halo[q] = (int64_t)part[q].size();
+                order_halo[q].alloc(std::max<int64_t>(n_order_halo[q], 1));
+                if (n_order_halo[q]) order_halo[q].upload(part[q].data(), part[q].size(), ctx->stream);
+            }
+            WCB_CUDA(cudaStreamSynchronize(ctx->stream));
+            halo_split_built = true;
+        }
+        return n_order_halo[0] > 0 && n_order_halo[1] > 0;
+    }
+    void cdm_step_halo_part(const StepArgs& a, int part) override {
+        halo_part = part;
+        try {
+            if (dim == 3) dispatch3d<MODE_STEP>(a); else dispatch2d<MODE_STEP>(a);
+        } catch (...) {
+            halo_part = -1;
+            throw;
+        }
+        halo_part = -1;
         WCB_CHECK_LAUNCH();
     }
     // IMEX c rows by cells (set_row_subset / apply_rows)

@@ -71,6 +71,7 @@ struct Scm3DGeo {
     // 1/m stream there.  null: every node loads 1/m.
     const uint8_t* clean;
     double2* zline;           // (n_ex P + 1) x n1 z-lines of the last cell column (n_e % 32 == 0)
+    int64_t xc0 = 0;          // first x chunk of this launch (blockIdx.z + xc0)
 };
 
 template <int P>
@@ -126,9 +127,11 @@ struct Str3 {
     static constexpr size_t SMEM = OFF_BAR + 8 * (S + 1);
 };
 
+// part: -1 all x chunks (+ z column kernels); 0 the first and last chunk
+// (+ z column kernels); 1 the chunks in between
 template <int P, int MODE>
 void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map_p, const Scm3DGeo& g,
-                  const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a);
+                  const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a, int part = -1);
 // clean[c] = 1 when every owned node of local cell c has minv == tab (bitwise)
 template <int P>
 void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean);

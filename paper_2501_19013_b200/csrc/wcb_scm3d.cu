@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     const double* prv = reinterpret_cast<const double*>(smem + T::OFF_PREV);   // [P][WY*P][TZ]
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
-    const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z;
-    if (MODE == MODE_STEP && zs == 0 && yb == 0 && xc == 0) record_observers(a);
+    const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z + g.xc0;
+    if (MODE == MODE_STEP && zs == 0 && yb == 0 && blockIdx.z == 0) record_observers(a);
     if (!g.cflags[(xc * g.n_yb + yb) * g.n_zs + zs]) return;
     const int64_t K0 = zs * T::TZ;
     const int64_t ey0 = yb * WY;
@@ -455,8 +455,8 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, 1)
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     const int yw = w / P, jz = w % P;   // y cell row slot (WY = halo), cell-local z node
-    const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z;
-    if (MODE == MODE_STEP && zs == 0 && yb == 0 && xc == 0) record_observers(a);
+    const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z + g.xc0;
+    if (MODE == MODE_STEP && zs == 0 && yb == 0 && blockIdx.z == 0) record_observers(a);
     if (!g.cflags[(xc * g.n_yb + yb) * g.n_zs + zs]) return;
     const int64_t K0 = zs * T::TZ;
     const int64_t ey0 = yb * WY;
@@ -759,24 +759,41 @@ void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, cons
 }
 
 template <int P, int MODE>
-void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map_p, const Scm3DGeo& g,
-                  const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a) {
+void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map_p, const Scm3DGeo& g0,
+                  const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a0, int part) {
     using T = Str3<P>;
-    dim3 grid((unsigned)g.n_zs, (unsigned)g.n_yb, (unsigned)g.n_xc);
-    if constexpr (jsplit3(P)) {
-        ensure_smem_attr((const void*)k_scm3j<P, MODE>, ctx->device, (size_t)T::SMEM);
-        k_scm3j<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
+    auto launch = [&](int64_t xc0, int64_t nz, bool obs) {
+        if (nz <= 0) return;
+        Scm3DGeo g = g0;
+        g.xc0 = xc0;
+        StepArgs a = a0;
+        if (!obs) a.obs_out = nullptr;
+        dim3 grid((unsigned)g.n_zs, (unsigned)g.n_yb, (unsigned)nz);
+        if constexpr (jsplit3(P)) {
+            ensure_smem_attr((const void*)k_scm3j<P, MODE>, ctx->device, (size_t)T::SMEM);
+            k_scm3j<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
+        } else {
+            ensure_smem_attr((const void*)k_scm3d<P, MODE>, ctx->device, (size_t)T::SMEM);
+            k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
+        }
+        ctx->launches++;
+    };
+    const int64_t n = g0.n_xc;
+    if (part < 0) {
+        launch(0, n, true);
+    } else if (part == 0) {   // chunks holding the rows exchanged with the neighbours
+        launch(0, 1, true);
+        if (n > 1) launch(n - 1, 1, false);
     } else {
-        ensure_smem_attr((const void*)k_scm3d<P, MODE>, ctx->device, (size_t)T::SMEM);
-        k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
+        launch(1, n - 2, false);
     }
-    ctx->launches++;
-    if (g.n_e % 32 == 0) {
+    if (part != 1 && g0.n_e % 32 == 0) {
+        const Scm3DGeo& g = g0;
         WCB_REQUIRE(g.zline, "z-line buffer missing");
         const int64_t nl = (g.n_ex * P + 1) * g.n1;
-        k_scm3d_zline<P><<<(unsigned)ceil_div(nl, 256), 256, 0, ctx->stream>>>(g, mt, a.cur, g.zline);
-        const int64_t n = (g.row_hi - g.row_lo) * g.n1;
-        k_scm3d_zcol<P, MODE><<<(unsigned)ceil_div(n, 128), 128, 0, ctx->stream>>>(g, mt, sk, g.zline, a);
+        k_scm3d_zline<P><<<(unsigned)ceil_div(nl, 256), 256, 0, ctx->stream>>>(g, mt, a0.cur, g.zline);
+        const int64_t nn = (g.row_hi - g.row_lo) * g.n1;
+        k_scm3d_zcol<P, MODE><<<(unsigned)ceil_div(nn, 128), 128, 0, ctx->stream>>>(g, mt, sk, g.zline, a0);
         ctx->launches += 2;
     }
 }
@@ -784,10 +801,10 @@ void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map
 #define WCB_INST3(P)                                                                            \
     template void launch_scm3d<P, MODE_STEP>(Context*, const CUtensorMap&, const CUtensorMap&, const Scm3DGeo&, \
                                              const Mats2<P>&, const MinvTab<P>&, double,        \
-                                             const StepArgs&);                                  \
+                                             const StepArgs&, int);                             \
     template void launch_scm3d<P, MODE_APPLY>(Context*, const CUtensorMap&, const CUtensorMap&, const Scm3DGeo&, \
                                               const Mats2<P>&, const MinvTab<P>&, double,       \
-                                              const StepArgs&);                                 \
+                                              const StepArgs&, int);                            \
     template void launch_clean3d<P>(Context*, const Scm3DGeo&, const MinvTab<P>&, const double*, uint8_t*);
 #define WCB_INSTC(P) \
     template void launch_cut_pre<P>(Context*, int64_t, const double*, const int64_t*, int64_t, int64_t, \

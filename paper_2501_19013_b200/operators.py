@@ -40,6 +40,13 @@ class DeviceOperator:
     def handle(self):
         return self._h
 
+    @property
+    def step_kernel(self) -> str:
+        """The kernel(s) one fused time step of this operator launches."""
+        buf = _lib.C.create_string_buffer(256)
+        _lib.check(_lib.load().wcb_operator_step_kernel(self._h, buf, 256))
+        return buf.value.decode()
+
     def matvec(self, x) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)
         if x.shape != (self.n,):
