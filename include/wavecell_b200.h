@@ -276,6 +276,31 @@ int wcb_imex_plan_cdm_run(wcb_imex_plan* plan, const double* ft, double dt, int6
 int wcb_imex_plan_max_gen_eig(wcb_imex_plan* plan, const double* x0, double tol, int64_t max_iter,
                               double* lam, int64_t* n_iter);
 
+/* ---- native host set-up, voids = union of open balls in [0,1]^d ----
+ * Host-only, multi-threaded C++ (no device).  Replaces the Python set-up of
+ * the ball-void geometries (setup/geometry.py BallVoids, setup/cutcell.py),
+ * restating src/geometry.py:36-41,316-346 and src/assembly.py:310-423,575-592. */
+/* cls[n_e^dim] = 0 outside / 1 inside / 2 cut (before the sliver rule). */
+int wcb_setup_ball_classify(int dim, int64_t n_e, int64_t n_balls, const double* centers, const double* radii,
+                            int8_t* cls);
+/* The sliver rule (src/assembly.py:187-211) on the cut cells (lex ids): sample
+ * certificate, then the physical fraction by 2^dim-section to `depth`;
+ * discard[i] = 1 when cut cell i keeps less than min_fraction. */
+int wcb_setup_ball_slivers(int dim, int64_t n_e, int64_t n_balls, const double* centers, const double* radii,
+                           int64_t n_cut, const int64_t* cut_cells, double min_fraction, int depth,
+                           uint8_t* discard);
+/* Cut-cell integrals of the listed cells (lex ids): K_out (n_cells x L x L)
+ * = sk (K_in + alpha K_out); M_out = sm (M_in + alpha M_out) consistent
+ * (lumping 0, n_cells x L x L), HRZ (1) or row-sum (2) lumped (n_cells x L).
+ * Tables: the dyadic 1D tables of setup/basis.py (offsets[depth+1]; per
+ * interval q GL points xi, weights w, values V and derivatives D (q x N),
+ * m1 / k1 (N x N)).  nthreads <= 0: all host threads (capped at 32). */
+int wcb_setup_ball_cut_cells(int dim, int p, int64_t n_e, int64_t n_balls, const double* centers,
+                             const double* radii, int depth, int q, const int64_t* offsets, const double* xi,
+                             const double* w, const double* V, const double* D, const double* m1,
+                             const double* k1, int64_t n_cells, const int64_t* cells, double alpha, double sk,
+                             double sm, int lumping, int nthreads, double* K_out, double* M_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,8 @@ EXPORTS = (
     "wcb_imex_plan_destroy", "wcb_imex_plan_run", "wcb_dist_unique_id", "wcb_dist_init",
     "wcb_dist_finalize", "wcb_cdm_group_run", "wcb_cdm_plan_step_bytes", "wcb_imex_group_run",
     "wcb_csr_diagonal_check", "wcb_mass_plan_create", "wcb_imex_plan_cdm_run",
-    "wcb_imex_plan_max_gen_eig", "wcb_operator_step_kernel",
+    "wcb_imex_plan_max_gen_eig", "wcb_operator_step_kernel", "wcb_setup_ball_classify",
+    "wcb_setup_ball_cut_cells", "wcb_setup_ball_slivers",
 )
 
 _p = C.c_void_p
@@ -99,6 +100,12 @@ _SIGS = {
     "wcb_operator_apply": (C.c_int, [_p, _dp, _dp]),
     "wcb_operator_halo": (C.c_int, [_p, _i64p]),
     "wcb_operator_step_kernel": (C.c_int, [_p, C.c_char_p, _i64]),
+    "wcb_setup_ball_classify": (C.c_int, [C.c_int, _i64, _i64, _dp, _dp, _i8p]),
+    "wcb_setup_ball_slivers": (C.c_int, [C.c_int, _i64, _i64, _dp, _dp, _i64, _i64p, _d, C.c_int,
+                                         C.POINTER(C.c_uint8)]),
+    "wcb_setup_ball_cut_cells": (C.c_int, [C.c_int, C.c_int, _i64, _i64, _dp, _dp, C.c_int, C.c_int, _i64p,
+                                           _dp, _dp, _dp, _dp, _dp, _dp, _i64, _i64p, _d, _d, _d, C.c_int,
+                                           C.c_int, _dp, _dp]),
     "wcb_max_gen_eig": (C.c_int, [_p, _dp, _dp, _d, _i64, _dp, _i64p]),
     "wcb_max_gen_eig_sub": (C.c_int, [_p, _dp, _i64, _i64p, _dp, _d, _i64, _dp, _i64p]),
     "wcb_cdm_plan_create": (C.c_int, [_p, _dp, _dp, C.POINTER(Observer), C.POINTER(_p)]),

@@ -88,13 +88,17 @@ class Grid:
         origin = np.asarray(geom.domain_lo, dtype=float)
         h = float((geom.domain_hi[0] - geom.domain_lo[0]) / n_e)
         n_cells = n_e ** dim
-        classes = np.empty(n_cells, dtype=np.int8)
-        for s in range(0, n_cells, chunk):
-            ids = np.arange(s, min(n_cells, s + chunk))
-            ijk = np.stack(np.unravel_index(ids, (n_e,) * dim), axis=1)
-            lo = origin + ijk * h
-            classes[s:s + ids.shape[0]] = geom.classify_boxes(lo, lo + h)
-        classes = classes.reshape((n_e,) * dim)
+        from . import native
+        if native.enabled(geom, family):   # C++ per-ball classification (same tests)
+            classes = native.classify(geom, n_e)
+        else:
+            classes = np.empty(n_cells, dtype=np.int8)
+            for s in range(0, n_cells, chunk):
+                ids = np.arange(s, min(n_cells, s + chunk))
+                ijk = np.stack(np.unravel_index(ids, (n_e,) * dim), axis=1)
+                lo = origin + ijk * h
+                classes[s:s + ids.shape[0]] = geom.classify_boxes(lo, lo + h)
+            classes = classes.reshape((n_e,) * dim)
         _discard_slivers(geom, classes, origin, h, min_volume_fraction)
         return cls(geom, basis, origin, h, classes)
 
@@ -153,6 +157,10 @@ def _discard_slivers(geom, classes, origin, h, min_volume_fraction):
     flat = classes.reshape(-1)
     cut = np.flatnonzero(flat == CUT)
     if cut.shape[0] == 0:
+        return
+    from . import native
+    if native.enabled(geom) and np.all(origin == 0.0) and abs(h * classes.shape[0] - 1.0) < 1e-15:
+        flat[cut[native.slivers(geom, classes.shape[0], cut, min_volume_fraction)]] = OUTSIDE
         return
     ijk = np.stack(np.unravel_index(cut, classes.shape), axis=1)
     lo = origin + ijk * h

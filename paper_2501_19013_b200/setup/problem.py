@@ -69,6 +69,9 @@ def integrate_cut_cells(grid, depth, cut, alpha, sk, sm, lumping, n_jobs=None):
     """Physical cut-cell stiffness and (lumped) mass for every cut cell;
     large sets are spread over host processes (each cell is independent)."""
     import os
+    from . import native
+    if native.enabled(grid.geom, grid.basis.family):   # C++ threads (setup/native.py)
+        return native.cut_cells(grid, depth, cut, alpha, sk, sm, lumping)
     n_jobs = n_jobs or int(os.environ.get("WAVECELL_B200_JOBS", 0)) or min(32, os.cpu_count() or 1)
     if _under_profiler():
         n_jobs = 1   # under ncu: forked workers crash the injected tool
