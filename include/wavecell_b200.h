@@ -276,6 +276,17 @@ int wcb_imex_plan_cdm_run(wcb_imex_plan* plan, const double* ft, double dt, int6
 int wcb_imex_plan_max_gen_eig(wcb_imex_plan* plan, const double* x0, double tol, int64_t max_iter,
                               double* lam, int64_t* n_iter);
 
+/* ---- eigenvalue stabilisation -----------------------------
+ * jacobi_eig, src/linalg.py:133-212: batched cyclic Jacobi on the device (n
+ * symmetric L x L matrices, L <= 100): lam (n x L ascending), V (n x L x L,
+ * eigenvectors as columns).  WCB_E_NOCONV after max_sweeps. */
+int wcb_jacobi_eig(wcb_context* ctx, int64_t n, int L, const double* A, int max_sweeps, double tol,
+                   double* lam, double* V);
+/* evs_stabilize, src/stabilization.py:73-102, in place on the n consistent
+ * cut-cell masses M_o (n x L x L); mf_absmax[b] = max |M_f| of cell b. */
+int wcb_evs_stabilize(wcb_context* ctx, int64_t n, int L, double* M_o, const double* mf_absmax,
+                      double epsilon, double f_lambda);
+
 /* ---- native host set-up, voids = union of open balls in [0,1]^d ----
  * Host-only, multi-threaded C++ (no device).  Replaces the Python set-up of
  * the ball-void geometries (setup/geometry.py BallVoids, setup/cutcell.py),

@@ -128,7 +128,10 @@ class ScmProblem:
     # ------------------------------------------------------------ build --
     @classmethod
     def build(cls, grid: Grid, alpha: float, depth: int, rho: float = 1.0, c: float = 1.0,
-              lumping: str = "hrz"):
+              lumping: str = "hrz", epsilon: float = 0.0, f_lambda: float = 1e-2):
+        """``epsilon > 0``: eigenvalue-stabilised cut-cell masses before the
+        lumping (src/assembly.py:584-585, src/stabilization.py:73-102), the
+        batched eigen-solves on the device (stabilization.evs_stabilize)."""
         if grid.basis.family != "lagrange":
             raise ValueError("ScmProblem needs the Lagrange (GLL) family")
         if lumping not in ("hrz", "row_sum", "none"):
@@ -141,7 +144,14 @@ class ScmProblem:
         sm = rho * (h / 2.0) ** d
         m1, k1 = uncut_1d(grid.basis, 0)
         cut = grid.cut_lex
-        cut_K, cut_M = integrate_cut_cells(grid, depth, cut, alpha, sk, sm, lumping)
+        if epsilon > 0.0 and cut.shape[0]:
+            from ..stabilization import evs_stabilize
+            cut_K, M_o = integrate_cut_cells(grid, depth, cut, alpha, sk, sm, "none")
+            _, M_f = integrate_cut_cells(grid, depth, cut, 1.0, sk, sm, "none")
+            M_o = evs_stabilize(M_o, M_f, epsilon, f_lambda)
+            cut_M = M_o if lumping == "none" else (hrz_lump(M_o) if lumping == "hrz" else row_sum_lump(M_o))
+        else:
+            cut_K, cut_M = integrate_cut_cells(grid, depth, cut, alpha, sk, sm, lumping)
         prob = cls(grid=grid, rho=rho, c=c, alpha=alpha, depth=depth, lumping=lumping,
                    sk=sk, sm=sm, m1=m1, k1=k1, cut_K=cut_K, cut_M=cut_M,
                    m_diag=np.zeros(0))

@@ -21,7 +21,9 @@ sys.path.insert(0, str(REF))
 sys.dont_write_bytecode = True
 
 from wavecell import assembly as A                      # noqa: E402
+from wavecell import assembly as A_                     # noqa: E402
 from wavecell import basis as B                         # noqa: E402
+from wavecell import basis as B_                        # noqa: E402
 from wavecell import geometry as G                      # noqa: E402
 from wavecell import harness as H                       # noqa: E402
 from wavecell import linalg as LA                       # noqa: E402
@@ -317,6 +319,33 @@ def gen_tensor():
     save("tensor", **out)
 
 
+def gen_evs():
+    """jacobi_eig and evs_stabilize of the reference on a batch of SPD
+    matrices with clustered small eigenvalues (badly cut cell masses) and on
+    real cut-cell masses of the rotated cube (p=2, n_e=4, alpha 1e-8)."""
+    rng = np.random.default_rng(11)
+    n, B = 27, 12
+    Q = np.linalg.qr(rng.standard_normal((B, n, n)))[0]
+    lam = np.exp(rng.uniform(np.log(1e-9), 0.0, (B, n)))
+    A = np.einsum("bik,bk,bjk->bij", Q, lam, Q)
+    Mf = A + 0.1 * np.eye(n)
+    lam_r, V_r = LA.jacobi_eig(A)
+    evs = S.evs_stabilize(A, Mf, 0.1, 1e-2)
+    geom = G.ImmersedGeometry.from_angles(0.3, 0.5, (10.0, 10.0, 10.0))
+    grid = A_.Grid.build(geom, B_.BasisSpec(family="lagrange", p=2, n_e=4))
+    cache = A_.ElementIntegralCache(grid, octree_depth=2)
+    cut = [tuple(int(v) for v in ijk) for ijk in grid.kept
+           if grid.classes[tuple(ijk)] == G.ElementClass.CUT][:16]
+    Mo_c, Mf_c = [], []
+    for ijk in cut:
+        M_o, K_o, M_f, K_f = A_.element_matrices(grid, ijk, 1e-8, cache=cache)
+        Mo_c.append(M_o)
+        Mf_c.append(M_f)
+    Mo_c, Mf_c = np.array(Mo_c), np.array(Mf_c)
+    evs_c = S.evs_stabilize(Mo_c, Mf_c, 0.01, 1e-2)
+    save("evs", A=A, Mf=Mf, lam=lam_r, V=V_r, evs=evs, Mo_c=Mo_c, Mf_c=Mf_c, evs_c=evs_c)
+
+
 def tensor_csr_ref(ts):
     m, k = sp.csr_matrix(ts.m1), sp.csr_matrix(ts.k1)
     return ts.rho * ts.c ** 2 * (sp.kron(sp.kron(k, m), m) + sp.kron(sp.kron(m, k), m)
@@ -339,3 +368,4 @@ elif __name__ == "__main__":
     gen_bspline_cube("bspline_cube_p2n5", p=2, n_e=5, alpha=1e-6, depth=2)
     gen_tensor()
     gen_paper()
+    gen_evs()
