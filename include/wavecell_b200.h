@@ -213,6 +213,13 @@ int wcb_cdm_plan_destroy(wcb_cdm_plan* plan);
 int wcb_cdm_plan_run(wcb_cdm_plan* plan, const double* ft, double dt, int64_t n_t,
                      const double* psi0, const double* v0, double* psi_out,
                      double* obs_out, wcb_divergence* div, wcb_timings* tm);
+/* Same run with the observers recorded every record_every steps only:
+ * obs_out is n_obs x (n_t / record_every + 1), column j = obs at step
+ * j * record_every -- the exact-hit samples of sample_observers
+ * (src/harness.py:101-131) without moving the full history. */
+int wcb_cdm_plan_run_sampled(wcb_cdm_plan* plan, const double* ft, double dt, int64_t n_t,
+                             int64_t record_every, const double* psi0, const double* v0,
+                             double* psi_out, double* obs_out, wcb_divergence* div, wcb_timings* tm);
 /* Algorithmic bytes one fused time step of this plan moves: 32 B per DOF
  * (psi_k, psi_{k-1}, 1/m, psi_{k+1}) less 8 B per DOF whose 1/m the kernel
  * takes from the interior-cell table (bitwise-checked at plan creation), plus

@@ -38,6 +38,7 @@ EXPORTS = (
     "wcb_csr_diagonal_check", "wcb_mass_plan_create", "wcb_imex_plan_cdm_run",
     "wcb_imex_plan_max_gen_eig", "wcb_operator_step_kernel", "wcb_setup_ball_classify",
     "wcb_setup_ball_cut_cells", "wcb_setup_ball_slivers", "wcb_jacobi_eig", "wcb_evs_stabilize",
+    "wcb_cdm_plan_run_sampled",
 )
 
 _p = C.c_void_p
@@ -116,6 +117,8 @@ _SIGS = {
     "wcb_cdm_plan_step_bytes": (C.c_int, [_p, _dp]),
     "wcb_cdm_plan_run": (C.c_int, [_p, _dp, _d, _i64, _dp, _dp, _dp, _dp,
                                    C.POINTER(Divergence), C.POINTER(Timings)]),
+    "wcb_cdm_plan_run_sampled": (C.c_int, [_p, _dp, _d, _i64, _i64, _dp, _dp, _dp, _dp,
+                                           C.POINTER(Divergence), C.POINTER(Timings)]),
     "wcb_cdm_plan_run_device": (C.c_int, [_p, _p, _d, _i64, _p, _p, _p, _p,
                                           C.POINTER(Divergence), C.POINTER(Timings)]),
     "wcb_imex_plan_create": (C.c_int, [_p, _i64, _i64p, _i64, _i64p, _dp, C.POINTER(LU),

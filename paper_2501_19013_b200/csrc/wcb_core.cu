@@ -806,14 +806,17 @@ struct HaloOverlap {
 static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, double dt, int64_t n_t,
                           const std::vector<const double*>& d_psi0, const std::vector<const double*>& d_v0,
                           const std::vector<double*>& d_psi_out, const std::vector<double*>& d_obs_out,
-                          wcb_divergence* div, wcb_timings* tm) {
+                          wcb_divergence* div, wcb_timings* tm, int64_t rec = 1) {
+    // rec > 1: observers recorded every rec steps only (column k / rec), the
+    // exact step hits src/harness.py:101-131 samples when rec divides n_t
     const size_t G = Ps.size();
     Context* ctx = Ps[0]->op->ctx;
     for (auto* P : Ps) WCB_REQUIRE(P->op->ctx == ctx, "group plans must share one context");
     cudaStream_t s = ctx->stream;
     if (div) { div->step = -1; div->amplitude = 0.0; }
     if (tm) { tm->factorization = 0.0; tm->rhs = 0.0; tm->backward_insertion = 0.0; }
-    const int64_t stride = n_t + 1;
+    WCB_REQUIRE(rec >= 1, "record_every must be >= 1");
+    const int64_t stride = n_t / rec + 1;
     std::vector<double*> cur(G), prev(G);
     for (size_t r = 0; r < G; ++r) {
         wcb_cdm_plan* P = Ps[r];
@@ -861,6 +864,11 @@ static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, do
         }
     }
     WCB_CHECK_LAUNCH();
+    auto gate_obs = [&](size_t r, StepArgs& a, int64_t k) {
+        if (rec == 1) return;
+        a.obs_out = (k % rec == 0 && Ps[r]->n_obs) ? d_obs_out[r] : nullptr;
+        a.obs_col = k / rec;
+    };
     // Keep the psi_k / psi_{k-1} pair resident in L2 across time steps
     // (persisting access-policy window on the stream) when the pair fits the
     // access-policy window and at most twice the persisting set-aside (hit
@@ -931,6 +939,7 @@ static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, do
                 a.out = prev[r];
                 a.k = k;
                 a.amp = Ps[r]->amp.p + (k + 1);
+                gate_obs(r, a, k);
                 Ps[r]->op->cdm_step_halo_part(a, 0);   // exchanged rows (+ observers of psi_k)
             }
             WCB_CUDA(cudaEventRecord(hov->e_b, s));
@@ -953,6 +962,7 @@ static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, do
             a.out = prev[r];   // psi_{k+1} overwrites psi_{k-1} in place
             a.k = k;
             a.amp = Ps[r]->amp.p + (k + 1);
+            gate_obs(r, a, k);
             Ps[r]->op->cdm_step(a);   // also records obs[:, k] from psi_k
             std::swap(cur[r], prev[r]);
         }
@@ -968,7 +978,9 @@ static void run_cdm_group(std::vector<wcb_cdm_plan*>& Ps, const double* d_ft, do
                 StepArgs a = args[r];
                 a.cur = cur[r];
                 a.k = n_t;
-                launch_record_observers(ctx, a);
+                a.obs_out = d_obs_out[r];
+                a.obs_col = rec > 1 ? (n_t % rec == 0 ? n_t / rec : -2) : -1;
+                if (a.obs_col != -2) launch_record_observers(ctx, a);
             }
     WCB_CUDA(cudaEventRecord(ctx->ev1, s));
     WCB_CHECK_LAUNCH();
@@ -1127,7 +1139,14 @@ int wcb_cdm_plan_run_device(wcb_cdm_plan* P, const double* d_ft, double dt, int6
 int wcb_cdm_plan_run(wcb_cdm_plan* P, const double* ft, double dt, int64_t n_t,
                      const double* psi0, const double* v0, double* psi_out, double* obs_out,
                      wcb_divergence* div, wcb_timings* tm) {
+    return wcb_cdm_plan_run_sampled(P, ft, dt, n_t, 1, psi0, v0, psi_out, obs_out, div, tm);
+}
+
+int wcb_cdm_plan_run_sampled(wcb_cdm_plan* P, const double* ft, double dt, int64_t n_t, int64_t record_every,
+                             const double* psi0, const double* v0, double* psi_out, double* obs_out,
+                             wcb_divergence* div, wcb_timings* tm) {
     return guarded([&] {
+        WCB_REQUIRE(record_every >= 1, "record_every must be >= 1");
         WCB_REQUIRE(P && psi_out, "NULL argument");
         WCB_REQUIRE(n_t >= 0, "negative n_t");
         Operator* op = P->op;
@@ -1142,13 +1161,17 @@ int wcb_cdm_plan_run(wcb_cdm_plan* P, const double* ft, double dt, int64_t n_t,
         dft.upload(ft, std::max<int64_t>(n_t, 1), s);
         if (psi0) { dpsi0.alloc(n, s); dpsi0.upload(psi0, n, s); }
         if (v0) { dv0.alloc(n, s); dv0.upload(v0, n, s); }
-        if (obs_out && P->n_obs) dobs.alloc(P->n_obs * (n_t + 1), s);
+        const int64_t ncol = n_t / record_every + 1;
+        if (obs_out && P->n_obs) dobs.alloc(P->n_obs * ncol, s);
         Prefault pf(psi_out, n * sizeof(double));   // fault the output in while the loop runs
-        run_cdm_device(P, dft.p, dt, n_t, dpsi0.p, dv0.p, dout.p, dobs.p, div, tm);
+        {
+            std::vector<wcb_cdm_plan*> Ps{P};
+            run_cdm_group(Ps, dft.p, dt, n_t, {dpsi0.p}, {dv0.p}, {dout.p}, {dobs.p}, div, tm, record_every);
+        }
         pf.join();
         copy_d2h(psi_out, dout.p, n * sizeof(double), s);
         if (obs_out && P->n_obs)
-            WCB_CUDA(cudaMemcpyAsync(obs_out, dobs.p, P->n_obs * (n_t + 1) * sizeof(double),
+            WCB_CUDA(cudaMemcpyAsync(obs_out, dobs.p, P->n_obs * ncol * sizeof(double),
                                      cudaMemcpyDeviceToHost, s));
         WCB_CUDA(cudaStreamSynchronize(s));
         return WCB_OK;

@@ -182,6 +182,7 @@ struct StepArgs {
     const double* obs_val = nullptr;
     double* obs_out = nullptr;
     int64_t obs_stride = 0;
+    int64_t obs_col = -1;               // column written (default: k)
 };
 
 // obs[:, k] = obs_mat @ psi_k in CSR order (scipy csr_matvec); call from
@@ -191,7 +192,7 @@ __device__ __forceinline__ void record_observers(const StepArgs& a) {
     for (int64_t r = threadIdx.x; r < a.n_obs; r += blockDim.x) {
         double s = 0.0;
         for (int64_t j = a.obs_ptr[r]; j < a.obs_ptr[r + 1]; ++j) s += a.obs_val[j] * a.cur[a.obs_idx[j]];
-        a.obs_out[r * a.obs_stride + a.k] = s;
+        a.obs_out[r * a.obs_stride + (a.obs_col >= 0 ? a.obs_col : a.k)] = s;
     }
 }
 

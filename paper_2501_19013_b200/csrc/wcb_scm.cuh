@@ -88,10 +88,13 @@ struct MinvTab {
 #ifndef WCB3D_WY3
 #define WCB3D_WY3 7
 #endif
-// P = 3 runs the z-node-split kernel (k_scm3j, P warps per y cell row) by
-// default; WCB3D_JSPLIT=0 restores the one-warp-per-row kernel (k_scm3d)
+// WCB3D_JSPLIT=1 runs the z-node-split kernel for P = 3 (k_scm3j, P warps
+// per y cell row, 128 registers, 15 warps per SM).  Measured on config 5 it
+// is slower than k_scm3d (3.3-4.0 ms vs 2.9 ms per step: 1.6x the executed
+// instructions, barrier stalls over 15 warps), so the
+// one-warp-per-row kernel is the default.
 #ifndef WCB3D_JSPLIT
-#define WCB3D_JSPLIT 1
+#define WCB3D_JSPLIT 0
 #endif
 #ifndef WCB3D_WYJ
 #define WCB3D_WYJ 4

@@ -182,10 +182,17 @@ class CdmPlan:
         return float(out.value)
 
     def run(self, f_t, dt: float, n_t: int, psi0=None, v0=None,
-            record: bool = True) -> RunResult:
+            record: bool = True, record_every: int = 1) -> RunResult:
+        """``record_every = s`` keeps the observers at steps 0, s, 2s, ...
+        only (``RunResult.t`` / ``obs`` hold those columns): the exact-hit
+        samples of ``sample_observers`` (src/harness.py:101-131) without the
+        full history."""
         n = self.op.n
         dt = float(dt)
         n_t = int(n_t)
+        rec = int(record_every)
+        if rec < 1:
+            raise ValueError("record_every must be >= 1")
         ft = force_table(f_t, dt, n_t)
         psi0_a = None if psi0 is None else np.ascontiguousarray(
             np.array(psi0, dtype=float).reshape(-1))
@@ -194,17 +201,17 @@ class CdmPlan:
             if a is not None and a.shape[0] != n:
                 raise ValueError("initial state has the wrong length")
         psi = np.empty(n)
-        obs = np.empty((self.n_obs, n_t + 1)) if (self.n_obs and record) else None
+        obs = np.empty((self.n_obs, n_t // rec + 1)) if (self.n_obs and record) else None
         div = _lib.Divergence()
         tm = _lib.Timings()
-        code = _lib.load().wcb_cdm_plan_run(
-            self._h, _lib.dptr(ft), dt, n_t, _lib.dptr(psi0_a), _lib.dptr(v0_a),
+        code = _lib.load().wcb_cdm_plan_run_sampled(
+            self._h, _lib.dptr(ft), dt, n_t, rec, _lib.dptr(psi0_a), _lib.dptr(v0_a),
             _lib.dptr(psi), _lib.dptr(obs) if obs is not None else None,
             _lib.C.byref(div), _lib.C.byref(tm))
         if code == _lib.WCB_E_DIVERGED:
             raise DivergenceError(int(div.step), float(div.amplitude))
         _lib.check(code)
-        t = np.arange(n_t + 1) * dt
+        t = np.arange(0, n_t + 1, rec) * dt
         timings = StageTimings(factorization=0.0, rhs=float(tm.rhs),
                                backward_insertion=float(tm.backward_insertion))
         return RunResult(method="cdm", dt=dt, t=t, obs=obs, psi=psi, psi_dot=None,
