@@ -346,20 +346,10 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
         const double chiR = mR == 1 ? 1.0 : 0.0;
         const double chiL = mL == 1 ? 1.0 : 0.0;
         const double* rows = us + (size_t)(rbase + P) * T::UW;
-        // warp-uniform variants: every cell uncut (no masks); halo warp
-        // (output row P only) -- the same sums as the masked general path
-#ifdef WCB2D_NOFAST
-        const bool clean_row = false;
-#else
-        const bool clean_row = __all_sync(0xffffffffu, mR == 1 && mL == 1);
+#ifndef WCB2D_NOTENSOR
+        #pragma unroll
+        for (int c = 0; c < N; ++c) row_contract<P>(mc, kc, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
 #endif
-        if (clean_row) {
-            #pragma unroll
-            for (int c = 0; c < N; ++c) row_contract<P, false, false>(mc, kc, rows + (size_t)c * T::UW, lane, 1.0, 1.0, c, Y);
-        } else {
-            #pragma unroll
-            for (int c = 0; c < N; ++c) row_contract<P>(mc, kc, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
-        }
         const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
         const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
 #ifndef WCB2D_NOCUT

@@ -56,12 +56,15 @@ def test_shared_stencil_slices_bitwise(monkeypatch):
     f = lambda t: ricker(t, 10.0)  # noqa: E731
     x = np.random.default_rng(3).standard_normal(prob.n_dof)
     outs = []
-    for flag in ("1", None):
-        if flag:
-            monkeypatch.setenv("WAVECELL_B200_NO_SHARED_STENCIL", flag)
-        else:
-            monkeypatch.delenv("WAVECELL_B200_NO_SHARED_STENCIL", raising=False)
+    # plain SELL, shared-stencil slices with per-tap loads, and with bands
+    # (runs of consecutive offsets loaded once per warp, taps from shared memory)
+    for flags in ({"WAVECELL_B200_NO_SHARED_STENCIL": "1"}, {"WAVECELL_B200_NO_BANDS": "1"}, {}):
+        for k in ("WAVECELL_B200_NO_SHARED_STENCIL", "WAVECELL_B200_NO_BANDS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in flags.items():
+            monkeypatch.setenv(k, v)
         op = CsrOperator(prob.K)
         outs.append((op @ x, cdm_run(M, op, prob.F_s, f, 1e-4, 200).psi))
-    assert np.array_equal(outs[0][0], outs[1][0])
-    assert np.array_equal(outs[0][1], outs[1][1])
+    for y, psi in outs[1:]:
+        assert np.array_equal(outs[0][0], y)
+        assert np.array_equal(outs[0][1], psi)

@@ -162,8 +162,15 @@ def test_rejects_indefinite_and_nondiagonal_mass():
     from paper_2501_19013_b200 import IndefiniteMatrixError
     with pytest.raises(IndefiniteMatrixError):
         cdm_run(sp.diags([1.0, -1.0, 1.0, 1.0]).tocsr(), K, np.zeros(4), zero_f, 1e-3, 3)
-    with pytest.raises(NotImplementedError):
-        cdm_run(sp.csr_matrix(M.toarray() + 0.05), K, np.zeros(4), zero_f, 1e-3, 3)
+    # a consistent (non-diagonal) mass runs through the device M solves
+    Mc = sp.csr_matrix(M.toarray() + 0.05)
+    F = np.array([0.0, 1.0, 0.5, 0.2])
+    f = lambda t: np.sin(6.0 * t)  # noqa: E731
+    r = cdm_run(Mc, K, F, f, 5e-3, 200)
+    psi_ref, _, _ = O.cdm_run(Mc, K, F, f, 5e-3, 200)
+    assert rel(r.psi, psi_ref) <= 1e-12 and r.fact_dim == 4
+    with pytest.raises(IndefiniteMatrixError):
+        cdm_run(sp.csr_matrix(M.toarray() - 0.5), K, np.zeros(4), zero_f, 1e-3, 3)
 
 
 def test_select_dt_rules():
