@@ -307,6 +307,19 @@ int wcb_setup_ball_classify(int dim, int64_t n_e, int64_t n_balls, const double*
 int wcb_setup_ball_slivers(int dim, int64_t n_e, int64_t n_balls, const double* centers, const double* radii,
                            int64_t n_cut, const int64_t* cut_cells, double min_fraction, int depth,
                            uint8_t* discard);
+/* Compact DOF map of a classified Lagrange grid (src/assembly.py:159-180):
+ * lex_of_compact = NULL counts (returns n_dof, *n_c = number of c DOFs);
+ * then lex_of_compact (n_dof), c_idx (n_c, compact ids) and optionally d_idx
+ * (n_dof - n_c) and compact_of_lex ((p n_e + 1)^dim, -1 off the DOFs) are
+ * filled.  Negative return: -WCB_E_ARG. */
+int64_t wcb_setup_dofmap(int dim, int p, int64_t n_e, const int8_t* cls, int64_t* lex_of_compact,
+                         int64_t* c_idx, int64_t* n_c, int64_t* d_idx, int64_t* compact_of_lex);
+/* Lumped diagonal mass: sm * GLL weight products from the inside cells of
+ * every DOF plus the lumped cut-cell vectors cut_M (n_cut x L) in cut-cell
+ * order (src/assembly.py:586-592). */
+int wcb_setup_lumped_mass(int dim, int p, int64_t n_e, const int8_t* cls, const double* w, double sm,
+                          int64_t n_dof, const int64_t* lex_of_compact, int64_t n_cut, const int64_t* cut_cells,
+                          const double* cut_M, const int64_t* compact_of_lex, double* m);
 /* Cut-cell integrals of the listed cells (lex ids): K_out (n_cells x L x L)
  * = sk (K_in + alpha K_out); M_out = sm (M_in + alpha M_out) consistent
  * (lumping 0, n_cells x L x L), HRZ (1) or row-sum (2) lumped (n_cells x L).

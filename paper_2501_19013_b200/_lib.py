@@ -38,7 +38,7 @@ EXPORTS = (
     "wcb_csr_diagonal_check", "wcb_mass_plan_create", "wcb_imex_plan_cdm_run",
     "wcb_imex_plan_max_gen_eig", "wcb_operator_step_kernel", "wcb_setup_ball_classify",
     "wcb_setup_ball_cut_cells", "wcb_setup_ball_slivers", "wcb_jacobi_eig", "wcb_evs_stabilize",
-    "wcb_cdm_plan_run_sampled",
+    "wcb_cdm_plan_run_sampled", "wcb_setup_dofmap", "wcb_setup_lumped_mass",
 )
 
 _p = C.c_void_p
@@ -102,6 +102,9 @@ _SIGS = {
     "wcb_operator_halo": (C.c_int, [_p, _i64p]),
     "wcb_operator_step_kernel": (C.c_int, [_p, C.c_char_p, _i64]),
     "wcb_setup_ball_classify": (C.c_int, [C.c_int, _i64, _i64, _dp, _dp, _i8p]),
+    "wcb_setup_dofmap": (_i64, [C.c_int, C.c_int, _i64, _i8p, _i64p, _i64p, _i64p, _i64p, _i64p]),
+    "wcb_setup_lumped_mass": (C.c_int, [C.c_int, C.c_int, _i64, _i8p, _dp, _d, _i64, _i64p, _i64, _i64p, _dp,
+                                        _i64p, _dp]),
     "wcb_jacobi_eig": (C.c_int, [_p, _i64, C.c_int, _dp, C.c_int, _d, _dp, _dp]),
     "wcb_evs_stabilize": (C.c_int, [_p, _i64, C.c_int, _dp, _dp, _d, _d]),
     "wcb_setup_ball_slivers": (C.c_int, [C.c_int, _i64, _i64, _dp, _dp, _i64, _i64p, _d, C.c_int,

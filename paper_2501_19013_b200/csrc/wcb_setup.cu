@@ -565,4 +565,156 @@ int wcb_setup_ball_slivers(int dim, int64_t n_e, int64_t n_balls, const double* 
     return WCB_OK;
 }
 
+// Compact DOF map of a classified Lagrange grid (src/assembly.py:159-180,
+// setup/grid.py Grid.dofmap): a node is a DOF when one of its cells is kept
+// (inside or cut), a c DOF when one of its cells is cut; lex = (I n1 + J) [n1
+// + K].  Pass lex_of_compact = NULL to count: returns n_dof (>= 0) or an
+// error code (< 0); *n_c receives the c count.  Threads over node rows.
+int64_t wcb_setup_dofmap(int dim, int p, int64_t n_e, const int8_t* cls, int64_t* lex_of_compact,
+                         int64_t* c_idx, int64_t* n_c, int64_t* d_idx, int64_t* compact_of_lex) {
+    if ((dim != 2 && dim != 3) || p < 1 || n_e <= 0 || !cls) return -WCB_E_ARG;
+    const int d = dim;
+    const int64_t n1 = n_e * p + 1;
+    const int64_t per_row = d == 2 ? n1 : n1 * n1;
+    const int nth = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<int64_t> cnt(n1 + 1, 0), ccnt(n1 + 1, 0);
+    // cells incident to node coordinate I along one axis: (I-1)/p .. I/p within range
+    auto cells_of = [&](int64_t I, int64_t* e, int& ne) {
+        ne = 0;
+        if (I % p == 0) {
+            if (I / p - 1 >= 0) e[ne++] = I / p - 1;
+            if (I / p < n_e) e[ne++] = I / p;
+        } else {
+            e[ne++] = I / p;
+        }
+    };
+    auto node_flags = [&](int64_t I, int64_t J, int64_t K, bool& kept, bool& cut) {
+        int64_t ex[2], ey[2], ez[2] = {0, 0};
+        int nx, ny, nz = 1;
+        cells_of(I, ex, nx);
+        cells_of(J, ey, ny);
+        if (d == 3) cells_of(K, ez, nz);
+        kept = cut = false;
+        for (int a = 0; a < nx; ++a)
+            for (int b = 0; b < ny; ++b)
+                for (int c = 0; c < nz; ++c) {
+                    const int8_t v = d == 2 ? cls[ex[a] * n_e + ey[b]] : cls[(ex[a] * n_e + ey[b]) * n_e + ez[c]];
+                    kept |= v != OUT;
+                    cut |= v == CUTC;
+                }
+    };
+    auto pass = [&](bool fill) {
+        std::atomic<int64_t> next{0};
+        auto worker = [&] {
+            for (;;) {
+                const int64_t I = next.fetch_add(1);
+                if (I >= n1) break;
+                int64_t k = fill ? cnt[I] : 0, kc = fill ? ccnt[I] : 0;
+                int64_t kd = fill ? cnt[I] - ccnt[I] : 0;
+                for (int64_t r = 0; r < per_row; ++r) {
+                    const int64_t J = d == 2 ? r : r / n1, K = d == 2 ? 0 : r % n1;
+                    bool kept, cut;
+                    node_flags(I, J, K, kept, cut);
+                    if (!kept) {
+                        if (fill && compact_of_lex) compact_of_lex[I * per_row + r] = -1;
+                        continue;
+                    }
+                    if (fill) {
+                        lex_of_compact[k] = I * per_row + r;
+                        if (compact_of_lex) compact_of_lex[I * per_row + r] = k;
+                        if (cut) c_idx[kc++] = k;
+                        else if (d_idx) d_idx[kd++] = k;
+                    } else if (cut) {
+                        ++kc;
+                    }
+                    ++k;
+                }
+                if (!fill) { cnt[I + 1] = k; ccnt[I + 1] = kc; }
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < nth; ++t) th.emplace_back(worker);
+        worker();
+        for (auto& x : th) x.join();
+    };
+    pass(false);
+    for (int64_t I = 0; I < n1; ++I) { cnt[I + 1] += cnt[I]; ccnt[I + 1] += ccnt[I]; }
+    if (n_c) *n_c = ccnt[n1];
+    if (lex_of_compact && c_idx) pass(true);
+    return cnt[n1];
+}
+
+// Lumped diagonal mass of a Lagrange cut-cell grid (setup/problem.py
+// _assemble_mass): sm * prod_k w[a_k] from every inside cell of a node (in
+// ascending local position), then the lumped cut-cell vectors in cut-cell
+// order -- the same sums in the same order as the Python assembly.
+int wcb_setup_lumped_mass(int dim, int p, int64_t n_e, const int8_t* cls, const double* w, double sm,
+                          int64_t n_dof, const int64_t* lex_of_compact, int64_t n_cut, const int64_t* cut_cells,
+                          const double* cut_M, const int64_t* compact_of_lex, double* m) {
+    if ((dim != 2 && dim != 3) || p < 1 || n_e <= 0 || !cls || !w || !lex_of_compact || !m) return WCB_E_ARG;
+    const int d = dim;
+    const int64_t n1 = n_e * p + 1;
+    const int nth = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::atomic<int64_t> next{0};
+    auto worker = [&] {
+        for (;;) {
+            const int64_t i0 = next.fetch_add(4096);
+            if (i0 >= n_dof) break;
+            for (int64_t i = i0; i < std::min<int64_t>(n_dof, i0 + 4096); ++i) {
+                const int64_t lex = lex_of_compact[i];
+                int64_t X[3];
+                int64_t r = lex;
+                for (int k = d - 1; k >= 0; --k) { X[k] = r % n1; r /= n1; }
+                // local positions ascending (a before a + p), last axis fastest
+                int64_t la[3][2], ec[3][2];
+                int nl[3];
+                for (int k = 0; k < d; ++k) {
+                    nl[k] = 0;
+                    if (X[k] % p == 0) {
+                        if (X[k] / p < n_e) { la[k][nl[k]] = 0; ec[k][nl[k]++] = X[k] / p; }
+                        if (X[k] / p - 1 >= 0) { la[k][nl[k]] = p; ec[k][nl[k]++] = X[k] / p - 1; }
+                    } else {
+                        la[k][nl[k]] = X[k] % p;
+                        ec[k][nl[k]++] = X[k] / p;
+                    }
+                }
+                double s = 0.0;
+                const int nz = d == 3 ? nl[2] : 1;
+                for (int a = 0; a < nl[0]; ++a)
+                    for (int b = 0; b < nl[1]; ++b)
+                        for (int c = 0; c < nz; ++c) {
+                            const int64_t cell = d == 2 ? ec[0][a] * n_e + ec[1][b]
+                                                        : (ec[0][a] * n_e + ec[1][b]) * n_e + ec[2][c];
+                            if (cls[cell] != IN) continue;
+                            // sm * prod(w): (w_a w_b) w_c first, as np.prod
+                            const double pw = d == 3 ? (w[la[0][a]] * w[la[1][b]]) * w[la[2][c]]
+                                                     : w[la[0][a]] * w[la[1][b]];
+                            s += sm * pw;
+                        }
+                m[i] = s;
+            }
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nth; ++t) th.emplace_back(worker);
+    worker();
+    for (auto& x : th) x.join();
+    // cut-cell lumped vectors, in cut-cell order (np.add.at)
+    const int N = p + 1;
+    const int L = d == 2 ? N * N : N * N * N;
+    for (int64_t e = 0; e < n_cut; ++e) {
+        int64_t c = cut_cells[e], ijk[3] = {0, 0, 0};
+        for (int k = d - 1; k >= 0; --k) { ijk[k] = c % n_e; c /= n_e; }
+        for (int q = 0; q < L; ++q) {
+            int loc[3] = {0, 0, 0}, r = q;
+            for (int k = d - 1; k >= 0; --k) { loc[k] = r % N; r /= N; }
+            int64_t lex = 0;
+            for (int k = 0; k < d; ++k) lex = lex * n1 + ijk[k] * p + loc[k];
+            const int64_t i = compact_of_lex[lex];
+            if (i >= 0) m[i] += cut_M[e * L + q];
+        }
+    }
+    return WCB_OK;
+}
+
 }  // extern "C"

@@ -121,6 +121,13 @@ class Grid:
 
     @cached_property
     def dofmap(self) -> DofMap:
+        from . import native
+        n1 = self.basis.n_funcs
+        if self.basis.family == "lagrange" and native.lib_ok():
+            lex_of_compact, c_idx, d_idx, compact = native.dofmap(self.classes, self.p)
+            dm = DofMap(n1=n1, dim=self.dim, lex_of_compact=lex_of_compact, c_idx=c_idx, d_idx=d_idx)
+            dm.__dict__["compact_of_lex"] = compact
+            return dm
         kept_nodes = _dilate(self.classes != OUTSIDE, self.basis)
         cut_nodes = _dilate(self.classes == CUT, self.basis)
         lex_of_compact = np.flatnonzero(kept_nodes.ravel()).astype(np.int64)

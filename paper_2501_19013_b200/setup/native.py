@@ -33,6 +33,54 @@ def enabled(geom, family: str = "lagrange") -> bool:
     return True
 
 
+def lib_ok() -> bool:
+    """The native library is there (geometry-independent set-up steps)."""
+    if os.environ.get("WAVECELL_B200_PY_SETUP", "0") == "1":
+        return False
+    try:
+        from .. import _lib
+        _lib.load()
+    except ImportError:
+        return False
+    return True
+
+
+def dofmap(classes: np.ndarray, p: int):
+    """(lex_of_compact, c_idx, d_idx, compact_of_lex) of a classified Lagrange
+    grid (Grid.dofmap), all from one threaded pass."""
+    from .. import _lib
+    d, n_e = classes.ndim, classes.shape[0]
+    cls = np.ascontiguousarray(classes, dtype=np.int8).reshape(-1)
+    lib = _lib.load()
+    nc = _lib.C.c_int64(0)
+    n = lib.wcb_setup_dofmap(d, int(p), int(n_e), _lib.i8ptr(cls), None, None, _lib.C.byref(nc), None, None)
+    if n < 0:
+        _lib.check(int(-n))
+    lex = np.empty(n, dtype=np.int64)
+    c = np.empty(max(nc.value, 1), dtype=np.int64)
+    dd = np.empty(max(n - nc.value, 1), dtype=np.int64)
+    compact = np.empty((int(n_e) * int(p) + 1) ** d, dtype=np.int64)
+    lib.wcb_setup_dofmap(d, int(p), int(n_e), _lib.i8ptr(cls), _lib.i64ptr(lex), _lib.i64ptr(c),
+                         _lib.C.byref(nc), _lib.i64ptr(dd), _lib.i64ptr(compact))
+    return lex, c[: nc.value], dd[: n - nc.value], compact
+
+
+def lumped_mass(grid, w, sm: float, cut_M) -> np.ndarray:
+    """ScmProblem._assemble_mass (same sums, same order)."""
+    from .. import _lib
+    cls = np.ascontiguousarray(grid.classes, dtype=np.int8).reshape(-1)
+    dm = grid.dofmap
+    m = np.empty(dm.n_dof)
+    cm = np.ascontiguousarray(cut_M, dtype=np.float64).reshape(-1)
+    cut = np.ascontiguousarray(grid.cut_lex if cm.size else np.zeros(0), dtype=np.int64)
+    _lib.check(_lib.load().wcb_setup_lumped_mass(
+        grid.dim, grid.p, grid.n_e, _lib.i8ptr(cls), _lib.dptr(np.ascontiguousarray(w, dtype=np.float64)),
+        float(sm), dm.n_dof, _lib.i64ptr(np.ascontiguousarray(dm.lex_of_compact)), cut.shape[0],
+        _lib.i64ptr(cut) if cut.size else None, _lib.dptr(cm) if cm.size else None,
+        _lib.i64ptr(np.ascontiguousarray(dm.compact_of_lex)), _lib.dptr(m)))
+    return m
+
+
 def classify(geom: BallVoids, n_e: int) -> np.ndarray:
     """Cell classes (0 outside, 1 inside, 2 cut) of the n_e^d grid on [0,1]^d."""
     from .. import _lib

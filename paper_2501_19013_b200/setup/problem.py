@@ -169,6 +169,10 @@ class ScmProblem:
         d, p, n_e = g.dim, g.p, g.n_e
         n1 = g.basis.n_funcs
         w = gll_rule(p)[1]
+        from . import native
+        if native.lib_ok():
+            return native.lumped_mass(g, w, self.sm, self.cut_M if self.lumping != "none" else
+                                      np.zeros((0, (p + 1) ** d)))
         uncut = (g.classes == INSIDE).astype(float)
         node = np.zeros((n1,) * d)
         for local in np.ndindex(*([p + 1] * d)):

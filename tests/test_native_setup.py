@@ -33,6 +33,8 @@ def test_native_setup_matches_python(name, n_e, lumping, monkeypatch):
     assert np.array_equal(py.grid.classes, nat.grid.classes)
     assert np.array_equal(py.grid.dofmap.lex_of_compact, nat.grid.dofmap.lex_of_compact)
     assert np.array_equal(py.grid.cut_lex, nat.grid.cut_lex)
+    assert np.array_equal(py.grid.dofmap.c_idx, nat.grid.dofmap.c_idx)
+    assert np.array_equal(py.grid.dofmap.d_idx, nat.grid.dofmap.d_idx)
     scale = np.abs(py.cut_K).max()
     assert np.abs(nat.cut_K - py.cut_K).max() <= 1e-14 * scale
     assert np.abs(nat.cut_M - py.cut_M).max() <= 2e-14 * np.abs(py.cut_M).max()
