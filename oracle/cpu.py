@@ -28,6 +28,9 @@ def load():
         lib.wco_cdm_run.restype = C.c_int64
         lib.wco_cdm_run.argtypes = [C.c_int64, P, P, P, P, P, P, C.c_double, C.c_int64, P, P,
                                     P, C.c_int]
+        lib.wco_cdm_run_obs.restype = C.c_int64
+        lib.wco_cdm_run_obs.argtypes = [C.c_int64, P, P, P, P, P, P, C.c_double, C.c_int64, P, P,
+                                        P, C.c_int, C.c_int64, P, P, P, P]
         lib.wco_max_threads.restype = C.c_int
         _lib = lib
     return _lib
@@ -62,9 +65,9 @@ def scm_csr(prob) -> sp.csr_matrix:
     return sp.csr_matrix((data, indices, indptr), shape=(n, n))
 
 
-def cdm_run(K, m, F, ft, dt, n_t, psi0=None, v0=None, threads=0):
+def cdm_run(K, m, F, ft, dt, n_t, psi0=None, v0=None, threads=0, obs_mat=None):
     """Reference CDM loop (src/timeint.py:159-193) on the host.
-    Returns (psi, diverged_step)."""
+    Returns (psi, diverged_step), or (psi, obs, diverged_step) with obs_mat."""
     lib = load()
     K = sp.csr_matrix(K)
     indptr = np.ascontiguousarray(K.indptr, dtype=np.int64)
@@ -77,6 +80,16 @@ def cdm_run(K, m, F, ft, dt, n_t, psi0=None, v0=None, threads=0):
     out = np.empty(n)
     p0 = None if psi0 is None else np.ascontiguousarray(psi0, dtype=np.float64)
     q0 = None if v0 is None else np.ascontiguousarray(v0, dtype=np.float64)
+    if obs_mat is not None:
+        A = sp.csr_matrix(obs_mat)
+        op_ = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        oi = np.ascontiguousarray(A.indices, dtype=np.int64)
+        ov = np.ascontiguousarray(A.data, dtype=np.float64)
+        obs = np.zeros((A.shape[0], int(n_t) + 1))
+        div = lib.wco_cdm_run_obs(n, _p(indptr), _p(indices), _p(data), _p(m), _p(F), _p(ft), float(dt),
+                                  int(n_t), _p(p0), _p(q0), _p(out), int(threads), A.shape[0], _p(op_),
+                                  _p(oi), _p(ov), _p(obs))
+        return out, obs, int(div)
     div = lib.wco_cdm_run(n, _p(indptr), _p(indices), _p(data), _p(m), _p(F), _p(ft), float(dt),
                           int(n_t), _p(p0), _p(q0), _p(out), int(threads))
     return out, int(div)

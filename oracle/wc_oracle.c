@@ -129,11 +129,15 @@ int64_t wco_scm_csr(int dim, int p, int64_t n_e, const double* k1, const double*
     return total;
 }
 
-/* CDM, src/timeint.py:159-193 (no observers).  Returns the first diverged
- * step (max|psi| > 1e12 or non-finite) or 0. */
-int64_t wco_cdm_run(int64_t n, const int64_t* indptr, const int64_t* indices, const double* data,
-                    const double* m, const double* F, const double* ft, double dt, int64_t n_t,
-                    const double* psi0, const double* v0, double* psi_out, int nthreads) {
+/* CDM, src/timeint.py:159-193.  Observers (CSR obs_ptr/obs_idx/obs_val,
+ * n_obs rows; NULL for none) are recorded into obs_out (n_obs x (n_t+1))
+ * every step as _Recorder does (src/timeint.py:97-106).  Returns the first
+ * diverged step (max|psi| > 1e12 or non-finite) or 0. */
+int64_t wco_cdm_run_obs(int64_t n, const int64_t* indptr, const int64_t* indices, const double* data,
+                        const double* m, const double* F, const double* ft, double dt, int64_t n_t,
+                        const double* psi0, const double* v0, double* psi_out, int nthreads,
+                        int64_t n_obs, const int64_t* obs_ptr, const int64_t* obs_idx, const double* obs_val,
+                        double* obs_out) {
     if (nthreads > 0) omp_set_num_threads(nthreads);
     double* psi = (double*)malloc(sizeof(double) * (n ? n : 1));
     double* prev = (double*)malloc(sizeof(double) * (n ? n : 1));
@@ -149,6 +153,13 @@ int64_t wco_cdm_run(int64_t n, const int64_t* indptr, const int64_t* indices, co
         psi[i] = p0;
         prev[i] = p0 - dt * (v0 ? v0[i] : 0.0) + c * a;
     }
+#define WCO_RECORD(col)                                                                    \
+    for (int64_t r = 0; r < n_obs; ++r) {                                                  \
+        double s = 0.0;                                                                    \
+        for (int64_t j = obs_ptr[r]; j < obs_ptr[r + 1]; ++j) s += obs_val[j] * psi[obs_idx[j]]; \
+        obs_out[r * (n_t + 1) + (col)] = s;                                                \
+    }
+    if (obs_out) { WCO_RECORD(0) }
     for (int64_t k = 0; k < n_t && !diverged; ++k) {
         const double f = ft[k];
         double amp = 0.0;
@@ -164,11 +175,20 @@ int64_t wco_cdm_run(int64_t n, const int64_t* indptr, const int64_t* indices, co
             if (av > amp) amp = av;
         }
         double* t = prev; prev = psi; psi = nxt; nxt = t;
+        if (obs_out) { WCO_RECORD(k + 1) }
         if (amp > 1.0e12) diverged = k + 1;
     }
+#undef WCO_RECORD
     memcpy(psi_out, psi, sizeof(double) * n);
     free(psi); free(prev); free(nxt);
     return diverged;
+}
+
+int64_t wco_cdm_run(int64_t n, const int64_t* indptr, const int64_t* indices, const double* data,
+                    const double* m, const double* F, const double* ft, double dt, int64_t n_t,
+                    const double* psi0, const double* v0, double* psi_out, int nthreads) {
+    return wco_cdm_run_obs(n, indptr, indices, data, m, F, ft, dt, n_t, psi0, v0, psi_out, nthreads, 0, NULL,
+                           NULL, NULL, NULL);
 }
 
 int wco_max_threads(void) { return omp_get_max_threads(); }

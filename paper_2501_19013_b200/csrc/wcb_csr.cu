@@ -89,14 +89,8 @@ __global__ void __launch_bounds__(256) k_sell(int64_t n, const uint8_t* __restri
                                               const int64_t* __restrict__ p_ptr,
                                               const int32_t* __restrict__ p_off,
                                               const double* __restrict__ p_val,
-                                              const int32_t* __restrict__ b_ptr,
-                                              const int32_t* __restrict__ b_lo,
-                                              const int32_t* __restrict__ b_end,
                                               const double* __restrict__ x, double* __restrict__ y,
                                               StepArgs a) {
-    // per warp two band buffers of 64 doubles (band = run of consecutive
-    // offsets of a shared-pattern slice: loaded once, taps from shared memory)
-    __shared__ double band_buf[8][2][64];
     if (STEP) {
         pdl_trigger();
         pdl_wait();   // the previous step's psi is complete from here on
@@ -116,43 +110,7 @@ __global__ void __launch_bounds__(256) k_sell(int64_t n, const uint8_t* __restri
     if (valid) {
         const int w = __ldg(swid + s);
         const int t = __ldg(stype + s);
-        const int32_t bq0 = b_ptr ? __ldg(b_ptr + s) : 0, nbq = b_ptr ? __ldg(b_ptr + s + 1) - bq0 : 0;
-        if (t >= 1 && nbq > 0) {
-            // bands: the warp loads x[row0 + lo .. row0 + lo + 31 + width - 1]
-            // once (two coalesced loads per lane) and reads the taps from
-            // shared memory; taps in stored (CSR) order -- the same sums
-            const int64_t pb = __ldg(p_ptr + s);
-            const int64_t eb = t == 1 ? __ldg(e_ptr + s) + r : 0;
-            const int64_t row0 = row - r;
-            const int wq = (threadIdx.x >> 5) & 7;
-            double v0, v1;
-            auto fetch = [&](int b) {
-                const int lo = __ldg(b_lo + bq0 + b);
-                const int wd = __ldg(b_end + bq0 + b) - lo;   // offsets lo .. lo+wd
-                v0 = __ldg(x + row0 + lo + r);
-                v1 = r < wd ? __ldg(x + row0 + lo + 32 + r) : 0.0;
-            };
-            fetch(0);
-            int k = 0;
-            for (int b = 0; b < nbq; ++b) {
-                double* buf = band_buf[wq][b & 1];
-                buf[r] = v0;
-                buf[32 + r] = v1;
-                __syncwarp();
-                const int lo = __ldg(b_lo + bq0 + b);
-                const int ke = b + 1 < nbq ? -1 : w;
-                if (b + 1 < nbq) fetch(b + 1);
-                // taps of this band: offsets in [lo, b_end]
-                const int hi = __ldg(b_end + bq0 + b);
-                for (; k < w; ++k) {
-                    const int off = __ldg(p_off + pb + k);
-                    if (off > hi) break;
-                    const double val = t == 2 ? __ldg(p_val + pb + k) : __ldg(e_val + eb + 32 * (int64_t)k);
-                    acc = fma(val, buf[r + off - lo], acc);
-                }
-                (void)ke;
-            }
-        } else if (t == 2) {
+        if (t == 2) {
             const int64_t pb = __ldg(p_ptr + s);
             #pragma unroll 8
             for (int k = 0; k < w; ++k)
@@ -201,9 +159,7 @@ struct CsrOperator final : Operator {
     DevBuf<int32_t> e_idx, p_off;
     DevBuf<double> e_val, p_val;
     double sell_bytes = 0.0;   // matrix bytes per apply in the SELL layout
-    DevBuf<int32_t> b_ptr, b_lo, b_end;   // per slice: bands of its shared pattern
-    bool bands = false;
-    const int32_t* band_p() const { return bands ? b_ptr.p : nullptr; }
+
 
     const char* name() const override { return "csr"; }
     std::string step_kernel() const override {
@@ -239,8 +195,7 @@ struct CsrOperator final : Operator {
         if (sell) {
             StepArgs a;
             k_sell<false><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(
-                n, s_type.p, s_wid.p, e_ptr.p, e_idx.p, e_val.p, p_ptr.p, p_off.p, p_val.p, band_p(), b_lo.p,
-                b_end.p, x, y, a);
+                n, s_type.p, s_wid.p, e_ptr.p, e_idx.p, e_val.p, p_ptr.p, p_off.p, p_val.p, x, y, a);
             ctx->launches++;
             WCB_CHECK_LAUNCH();
             return;
@@ -271,7 +226,6 @@ struct CsrOperator final : Operator {
             WCB_CUDA(cudaLaunchKernelEx(&cfg, k_sell<true>, n, (const uint8_t*)s_type.p, (const int32_t*)s_wid.p,
                                         (const int64_t*)e_ptr.p, (const int32_t*)e_idx.p, (const double*)e_val.p,
                                         (const int64_t*)p_ptr.p, (const int32_t*)p_off.p, (const double*)p_val.p,
-                                        (const int32_t*)band_p(), (const int32_t*)b_lo.p, (const int32_t*)b_end.p,
                                         a.cur, (double*)none, a));
             ctx->launches++;
             WCB_CHECK_LAUNCH();
@@ -390,34 +344,6 @@ Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* h_indptr,
             mb += 1.0 + 4.0 + 16.0;
         }
         op->sell_bytes = mb;
-        // bands of the shared patterns (runs of offsets with gaps <= 1, at
-        // most 33 wide): WAVECELL_B200_NO_BANDS=1 keeps per-tap loads
-        if (!getenv("WAVECELL_B200_NO_BANDS")) {
-            std::vector<int32_t> bp(n_sl + 1, 0), bl, be;
-            for (int64_t sl = 0; sl < n_sl; ++sl) {
-                bp[sl] = (int32_t)bl.size();
-                if (st[sl] >= 1) {
-                    const int32_t* o = po.data() + pp[sl];
-                    const int64_t w = sw[sl];
-                    int64_t k = 0;
-                    while (k < w) {
-                        const int32_t lo = o[k];
-                        int32_t hi = lo;
-                        ++k;
-                        while (k < w && o[k] <= hi + 1 && o[k] - lo <= 32) hi = o[k++];
-                        bl.push_back(lo);
-                        be.push_back(hi);
-                    }
-                }
-            }
-            bp[n_sl] = (int32_t)bl.size();
-            if (!bl.empty()) {
-                op->b_ptr.alloc(bp.size()); op->b_ptr.upload(bp.data(), bp.size(), s);
-                op->b_lo.alloc(bl.size()); op->b_lo.upload(bl.data(), bl.size(), s);
-                op->b_end.alloc(be.size()); op->b_end.upload(be.data(), be.size(), s);
-                op->bands = true;
-            }
-        }
         if (ei.empty()) ei.push_back(0);
         if (ev.empty()) ev.push_back(0.0);
         if (po.empty()) po.push_back(0);

@@ -172,9 +172,9 @@ static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp
     T.ring_ok = false;
     if (!ok || off.empty()) return;
     cpiece[T.n_comp] = (int32_t)off.size();
-    const int64_t avail = (int64_t)TRSV_SMEM - T.max_size * 8 - 256;
+    const int64_t avail = (int64_t)TRSV_SMEM - T.max_size * 8 - 1024;
     T.ring_depth = (int)std::min<int64_t>(4, avail / TRSV_PIECE_BYTES);
-    if (T.ring_depth < 2) return;
+    if (avail < 2 * TRSV_PIECE_BYTES) return;   // the circular buffer holds >= 2 of the largest pieces
     T.max_pieces = maxp;
     T.blob.alloc(blob.size(), s); T.blob.upload(blob.data(), blob.size(), s);
     T.piece_off.alloc(off.size(), s); T.piece_off.upload(off.data(), off.size(), s);
@@ -624,57 +624,71 @@ __global__ void __launch_bounds__(NW * 32) k_trsv_pf(
 }
 
 // Producer / consumer level solve (default): one CTA per component, the
-// unknowns in shared memory.  Warp 0 (one lane) streams the component's level
-// pieces into a ring of DEPTH slots with one bulk copy each (mbarrier
-// complete_tx), gated by "slot free" mbarriers; NC consumer warps solve a
-// piece (row groups of GW lanes, rows strided over the groups), meet at a
-// named barrier (x of the piece visible) and release the slot.  A level
-// costs one consumer barrier plus its rows; the staging never occupies the
+// unknowns in shared memory.  One producer thread streams the component's
+// level pieces (one bulk copy each, mbarrier complete_tx) into a circular
+// byte buffer -- pieces are packed back to back, so a run of narrow levels
+// (median 2-3 rows, ~1.5 KB) keeps dozens of pieces in flight -- and never
+// overtakes the release counters the consumers publish.  NC consumer warps
+// solve a piece (row groups of GW lanes, rows strided over the groups), meet
+// at a named barrier (x of the piece visible) and release it.  A level costs
+// one consumer barrier plus its rows; the staging never occupies the
 // consumers.  Same lane order and shuffle tree as k_trsv_comp (bitwise equal).
-template <int NC, int DEPTH>
+constexpr int TRSV_QK = 64;                       // pieces in flight (mbarrier ring)
+constexpr int64_t TRSV_RING_MIN = 2 * TRSV_PIECE_BYTES;
+
+template <int NC>
 __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
     const int32_t* __restrict__ comp_order, const int32_t* __restrict__ comp_rows,
     const int32_t* __restrict__ comp_piece, const int64_t* __restrict__ piece_off,
     const int32_t* __restrict__ piece_bytes, const unsigned char* __restrict__ blob,
     const int32_t* __restrict__ rows, const double* __restrict__ b, double* __restrict__ x, int max_size,
-    int recip) {
+    int ring_bytes, int recip) {
     constexpr int GW = WCB_TRSV_GW;
     constexpr int G = NC * 32 / GW;
     extern __shared__ __align__(128) unsigned char smraw[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
-    uint64_t* empty = full + DEPTH;
-    unsigned char* ring = smraw + 128;
-    double* xl = reinterpret_cast<double*>(ring + (size_t)DEPTH * TRSV_PIECE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smraw);                 // [QK]
+    int* poff = reinterpret_cast<int*>(smraw + TRSV_QK * 8);             // [QK] ring offset of piece q
+    volatile long long* rel = reinterpret_cast<volatile long long*>(smraw + TRSV_QK * 12);   // [2]
+    unsigned char* ring = smraw + ((TRSV_QK * 12 + 16 + 127) / 128) * 128;
+    double* xl = reinterpret_cast<double*>(ring + ring_bytes);
     const int c = comp_order[blockIdx.x];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
     const int q0 = comp_piece[c], nq = comp_piece[c + 1] - q0;
     if (threadIdx.x == 0) {
-        for (int d = 0; d < DEPTH; ++d) {
-            mbar_init(&full[d], 1);
-            mbar_init(&empty[d], 1);
-        }
+        for (int d = 0; d < TRSV_QK; ++d) mbar_init(&full[d], 1);
+        rel[0] = 0;   // pieces released by the consumers
+        rel[1] = 0;   // ring bytes released (cumulative)
     }
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) xl[k - r0] = b[rows[k]];
     __syncthreads();
     if (warp == 0) {   // producer
-        if (lane == 0)
+        if (lane == 0) {
+            long long pos = 0;   // cumulative ring position
             for (int q = 0; q < nq; ++q) {
-                const int d = q % DEPTH;
-                mbar_wait(&empty[d], (uint32_t)(((q / DEPTH) & 1) ^ 1));
                 const uint32_t nb = (uint32_t)piece_bytes[q0 + q];
+                long long at = pos % ring_bytes;
+                long long need = nb;
+                if (at + nb > ring_bytes) { need += ring_bytes - at; at = 0; }   // wrap: skip the tail
+                // wait for ring space and a free mbarrier slot
+                while (pos + need - rel[1] > ring_bytes || q - rel[0] >= TRSV_QK) __nanosleep(32);
+                pos += need;
+                const int d = q % TRSV_QK;
+                poff[d] = (int)at;
                 mbar_expect_tx(&full[d], nb);
-                bulk_load(ring + (size_t)d * TRSV_PIECE_BYTES, blob + piece_off[q0 + q], nb, &full[d]);
+                bulk_load(ring + at, blob + piece_off[q0 + q], nb, &full[d]);
             }
+        }
         __syncwarp();
     } else {
         const int ct = threadIdx.x - 32;
         const int grp = ct / GW, l16 = lane % GW;
         const unsigned hmask = (GW == 32 ? 0xffffffffu : ((1u << GW) - 1u)) << ((lane / GW) * GW);
+        long long done_bytes = 0;   // consumer thread 0: cumulative end of the released pieces
         for (int q = 0; q < nq; ++q) {
-            const int d = q % DEPTH;
-            mbar_wait(&full[d], (uint32_t)((q / DEPTH) & 1));
-            const unsigned char* pc = ring + (size_t)d * TRSV_PIECE_BYTES;
+            const int d = q % TRSV_QK;
+            mbar_wait(&full[d], (uint32_t)((q / TRSV_QK) & 1));
+            const unsigned char* pc = ring + poff[d];
             const int32_t* hdr = reinterpret_cast<const int32_t*>(pc);
             const int nrow = hdr[0], k0 = hdr[1], ne = hdr[2];
             const int32_t* rp = reinterpret_cast<const int32_t*>(pc + 16);
@@ -694,28 +708,41 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
                 }
             }
             asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");   // piece solved by every consumer
-            if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32_imex(&empty[d])) : "memory");
+            if (ct == 0) {
+                // replay the producer's placement to publish the released bytes
+                const long long nb = piece_bytes[q0 + q];
+                long long at = done_bytes % ring_bytes, need = nb;
+                if (at + nb > ring_bytes) need += ring_bytes - at;
+                done_bytes += need;
+                __threadfence_block();
+                rel[1] = done_bytes;
+                rel[0] = q + 1;
+            }
         }
     }
     __syncthreads();
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) x[rows[k]] = xl[k - r0];
 }
 
-template <int NC, int DEPTH>
+static int trsv_ring_bytes(const TriSched& T) {
+    const int64_t head = ((TRSV_QK * 12 + 16 + 127) / 128) * 128;
+    int64_t avail = (int64_t)TRSV_SMEM - head - T.max_size * 8;
+    avail = avail / 128 * 128;
+    return (int)std::min<int64_t>(avail, 160 * 1024);
+}
+
+template <int NC>
 static void launch_trsv_ring(Context* ctx, const TriSched& T, const double* b, double* x) {
-    const size_t sm = 128 + (size_t)DEPTH * TRSV_PIECE_BYTES + (size_t)T.max_size * 8;
-    ensure_smem_attr((const void*)k_trsv_ring<NC, DEPTH>, ctx->device, sm);
-    k_trsv_ring<NC, DEPTH><<<(unsigned)T.n_comp, (NC + 1) * 32, sm, ctx->stream>>>(
+    const int rb = trsv_ring_bytes(T);
+    const size_t sm = ((TRSV_QK * 12 + 16 + 127) / 128) * 128 + (size_t)rb + (size_t)T.max_size * 8;
+    ensure_smem_attr((const void*)k_trsv_ring<NC>, ctx->device, sm);
+    k_trsv_ring<NC><<<(unsigned)T.n_comp, (NC + 1) * 32, sm, ctx->stream>>>(
         T.comp_order.p, T.comp_rows.p, T.comp_piece.p, T.piece_off.p, T.piece_bytes.p, T.blob.p, T.rows.p, b, x,
-        (int)T.max_size, T.recip ? 1 : 0);
+        (int)T.max_size, rb, T.recip ? 1 : 0);
 }
 template <int NC>
 static void launch_trsv_ring_d(Context* ctx, const TriSched& T, const double* b, double* x) {
-    switch (T.ring_depth) {
-        case 2: launch_trsv_ring<NC, 2>(ctx, T, b, x); break;
-        case 3: launch_trsv_ring<NC, 3>(ctx, T, b, x); break;
-        default: launch_trsv_ring<NC, 4>(ctx, T, b, x); break;
-    }
+    launch_trsv_ring<NC>(ctx, T, b, x);
 }
 
 template <int NW>

@@ -56,10 +56,9 @@ def test_shared_stencil_slices_bitwise(monkeypatch):
     f = lambda t: ricker(t, 10.0)  # noqa: E731
     x = np.random.default_rng(3).standard_normal(prob.n_dof)
     outs = []
-    # plain SELL, shared-stencil slices with per-tap loads, and with bands
-    # (runs of consecutive offsets loaded once per warp, taps from shared memory)
-    for flags in ({"WAVECELL_B200_NO_SHARED_STENCIL": "1"}, {"WAVECELL_B200_NO_BANDS": "1"}, {}):
-        for k in ("WAVECELL_B200_NO_SHARED_STENCIL", "WAVECELL_B200_NO_BANDS"):
+    # plain SELL and shared-stencil slices
+    for flags in ({"WAVECELL_B200_NO_SHARED_STENCIL": "1"}, {}):
+        for k in ("WAVECELL_B200_NO_SHARED_STENCIL",):
             monkeypatch.delenv(k, raising=False)
         for k, v in flags.items():
             monkeypatch.setenv(k, v)

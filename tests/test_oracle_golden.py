@@ -110,3 +110,14 @@ def test_c_port_divergence_step_matches_reference():
     assert div == 0 and np.array_equal(psi, g["stable_psi"])
     _, div = _c_cdm(one, np.ones(1), np.zeros(1), lambda t: 0.0, 2.01, 10000, psi0=np.ones(1))
     assert div == int(g["div_step"])
+
+
+def test_c_port_observers_bitwise():
+    g = load_golden("cube_p2n4")
+    from oracle import cpu
+    from paper_2501_19013_b200.timeint import force_table
+    f = lambda t: O.ricker(t, 10.0)  # noqa: E731
+    dt, n_t = float(g["dt"]), int(g["n_t"])
+    psi, obs, div = cpu.cdm_run(csr_from(g, "K"), g["M"], g["F"], force_table(f, dt, n_t), dt, n_t,
+                                threads=2, obs_mat=csr_from(g, "obs"))
+    assert div == 0 and np.array_equal(psi, g["psi"]) and np.array_equal(obs, g["obs"])
