@@ -45,7 +45,7 @@ struct Tile2E {
     static constexpr size_t OFF_MINV = OFF_PREV + 2 * E_R;    // [comp]
     static constexpr size_t OFF_CARRY = OFF_MINV + 2 * E_R;   // [comp][RPE+1][P][32]
     static constexpr size_t OFF_BAR = OFF_CARRY + (size_t)2 * (RPE + 1) * P * 32 * 8;
-    static constexpr size_t SMEM = OFF_BAR + 8;
+    static constexpr size_t SMEM = OFF_BAR + 16;   // [0] u tiles, [1] epilogue tiles
 };
 
 // 1D factors: y pass uses m1, k1, G; x pass uses per-component scaled
@@ -280,6 +280,7 @@ __device__ __forceinline__ void ela2d_warp(const Scm2DGeo& g, const EMats<P>& mt
             for (int j = 0; j < P; ++j)
                 if (!edge || Jl + j < g.n1y) a.out[base + j] = Y[r][j];
         } else {
+            if (r == 0) mbar_wait(bar + 1, 0);
             const double* urow = us + (size_t)(rbase + r + P) * T::UW + T::CO + P + lane * P;
             const double* ps = reinterpret_cast<const double*>(smem + T::OFF_PREV + O * T::E_R) +
                                (size_t)(wi * P + r) * T::TJ + lane * P;
@@ -326,18 +327,23 @@ __global__ void __launch_bounds__(Tile2E<P>::NWARP * 32, WCB_ELA_MINB) k_ela2d(
     if (MODE == MODE_STEP && blockIdx.x == 0) record_observers(a);
     const int64_t J0 = strip * T::TJ, I0 = g.row_lo + rtile * T::TI;
     const bool tcl = MODE == MODE_STEP && g.tclean && __ldg(g.tclean + tid) != 0;
+    // the contraction waits for the u tiles only ([0]); psi_{k-1} / 1/m ([1])
+    // keep streaming until the epilogue
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
         const bool epi = MODE == MODE_STEP;
-        mbar_expect_tx(bar, (uint32_t)(2 * T::U_BYTES + (epi ? (tcl ? 2 : 4) * T::E_BYTES : 0)));
+        mbar_expect_tx(bar, (uint32_t)(2 * T::U_BYTES));
         const int32_t xu = (int32_t)(J0 - P - T::CO + PADJ), xe = (int32_t)(J0 + PADJ);
         tma_load_2d(smem, &tm_u, xu, (int32_t)I0, bar);
         tma_load_2d(smem + T::OFF_U1, &tm_u, xu, (int32_t)I0 + rows, bar);
         if (epi) {
+            mbar_expect_tx(bar + 1, (uint32_t)((tcl ? 2 : 4) * T::E_BYTES));
             for (int o = 0; o < 2; ++o) {
-                tma_load_2d(smem + T::OFF_PREV + o * T::E_R, &tm_prev, xe, (int32_t)(I0 + P) + o * rows, bar);
+                tma_load_2d(smem + T::OFF_PREV + o * T::E_R, &tm_prev, xe, (int32_t)(I0 + P) + o * rows, bar + 1);
                 if (!tcl)
-                    tma_load_2d(smem + T::OFF_MINV + o * T::E_R, &tm_minv, xe, (int32_t)(I0 + P) + o * rows, bar);
+                    tma_load_2d(smem + T::OFF_MINV + o * T::E_R, &tm_minv, xe, (int32_t)(I0 + P) + o * rows,
+                                bar + 1);
             }
         }
     }

@@ -70,7 +70,7 @@ struct Tile2 {
     static constexpr size_t OFF_MINV = OFF_PREV + (E_BYTES + 127) / 128 * 128;
     static constexpr size_t OFF_CARRY = OFF_MINV + (E_BYTES + 127) / 128 * 128;   // [RPE+1][P][32]
     static constexpr size_t OFF_BAR = OFF_CARRY + (size_t)(RPE + 1) * P * 32 * 8;
-    static constexpr size_t SMEM = OFF_BAR + 8;
+    static constexpr size_t SMEM = OFF_BAR + 16;   // [0] psi_k tile, [1] epilogue tiles
 };
 
 // Local geometry of a 2D operator.  x (axis 0) may be a slab of the global
@@ -293,14 +293,18 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
     const bool tcl = MODE == MODE_STEP && g.tclean && __ldg(g.tclean + tid) != 0;
     if (MODE == MODE_STEP) pdl_wait();   // the previous step's psi is complete from here on
     if (MODE == MODE_STEP && blockIdx.x == 0) record_observers(a);
+    // two barriers: the contraction starts as soon as the psi_k tile lands,
+    // psi_{k-1} / 1/m (epilogue only) keep streaming meanwhile
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
         const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
-        mbar_expect_tx(bar, (uint32_t)(T::U_BYTES + (epi ? (tcl ? 1 : 2) * T::E_BYTES : 0)));
+        mbar_expect_tx(bar, (uint32_t)T::U_BYTES);
         tma_load_2d(smem, &tm_u, (int32_t)(J0 - P - T::CO + PADJ), (int32_t)I0, bar);
         if (epi) {
-            tma_load_2d(smem + T::OFF_PREV, &tm_prev, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar);
-            if (!tcl) tma_load_2d(smem + T::OFF_MINV, &tm_minv, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar);
+            mbar_expect_tx(bar + 1, (uint32_t)((tcl ? 1 : 2) * T::E_BYTES));
+            tma_load_2d(smem + T::OFF_PREV, &tm_prev, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar + 1);
+            if (!tcl) tma_load_2d(smem + T::OFF_MINV, &tm_minv, (int32_t)(J0 + PADJ), (int32_t)(I0 + P), bar + 1);
         }
     }
     // cell codes (and the epilogue's psi_{k-1}, 1/m) while the tile is in flight
@@ -386,6 +390,7 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
             } else {
                 double up[P], mi[P];
                 if constexpr (WCB2D_EPI_TMA != 0) {
+                    if (r == 0) mbar_wait(bar + 1, 0);
                     const double* ps = reinterpret_cast<const double*>(smem + T::OFF_PREV) +
                                        (size_t)(w * P + r) * T::TJ + lane * P;
                     const double* msm = reinterpret_cast<const double*>(smem + T::OFF_MINV) +
