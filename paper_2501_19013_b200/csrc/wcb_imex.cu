@@ -116,7 +116,7 @@ static std::vector<int64_t> factor_components(int64_t n, const wcb_lu* lu, int64
 }
 
 // Segment layout of one piece (rows [k0, k1) of one level, every offset a
-// multiple of 16 bytes): int32 hdr[4] = {nrow, k0, ne, 0}; int32 rptr[nrow+1]
+// multiple of 16 bytes): int32 hdr[4] = {nrow, k0, ne, bytes}; int32 rptr[nrow+1]
 // (entry offsets within the piece); double pivot[nrow]; double val[ne];
 // int32 col[ne].  The whole piece is one bulk copy.
 constexpr int64_t TRSV_PIECE_BYTES = 24 * 1024;
@@ -152,6 +152,7 @@ static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp
                 hdr[0] = (int32_t)nrow;
                 hdr[1] = (int32_t)k;
                 hdr[2] = (int32_t)ne;
+                hdr[3] = (int32_t)sz;
                 int32_t* rp = reinterpret_cast<int32_t*>(p + 16);
                 for (int64_t q = 0; q <= nrow; ++q) rp[q] = sptr[k + q] - sptr[k];
                 double* dg = reinterpret_cast<double*>(p + 16 + pad16(4 * (nrow + 1)));
@@ -662,24 +663,32 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
     }
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) xl[k - r0] = b[rows[k]];
     __syncthreads();
-    if (warp == 0) {   // producer
-        if (lane == 0) {
-            long long pos = 0;   // cumulative ring position
-            for (int q = 0; q < nq; ++q) {
-                const uint32_t nb = (uint32_t)piece_bytes[q0 + q];
-                long long at = pos % ring_bytes;
-                long long need = nb;
-                if (at + nb > ring_bytes) { need += ring_bytes - at; at = 0; }   // wrap: skip the tail
-                // wait for ring space and a free mbarrier slot
-                while (pos + need - rel[1] > ring_bytes || q - rel[0] >= TRSV_QK) __nanosleep(32);
-                pos += need;
-                const int d = q % TRSV_QK;
-                poff[d] = (int)at;
-                mbar_expect_tx(&full[d], nb);
-                bulk_load(ring + at, blob + piece_off[q0 + q], nb, &full[d]);
+    if (warp == 0) {   // producer warp: piece sizes / offsets fetched 32 at a time
+        long long pos = 0;   // cumulative ring position
+        for (int qb = 0; qb < nq; qb += 32) {
+            const int qq = qb + lane;
+            const uint32_t nb_l = qq < nq ? (uint32_t)piece_bytes[q0 + qq] : 0u;
+            const int64_t off_l = qq < nq ? piece_off[q0 + qq] : 0;
+            const int nbat = min(32, nq - qb);
+            for (int i = 0; i < nbat; ++i) {
+                const uint32_t nb = __shfl_sync(0xffffffffu, nb_l, i);
+                const int64_t off = __shfl_sync(0xffffffffu, off_l, i);
+                if (lane == 0) {
+                    const int q = qb + i;
+                    long long at = pos % ring_bytes;
+                    long long need = nb;
+                    if (at + nb > ring_bytes) { need += ring_bytes - at; at = 0; }   // wrap: skip the tail
+                    // wait for ring space and a free mbarrier slot
+                    while (pos + need - rel[1] > ring_bytes || q - rel[0] >= TRSV_QK) __nanosleep(20);
+                    pos += need;
+                    const int d = q % TRSV_QK;
+                    poff[d] = (int)at;
+                    mbar_expect_tx(&full[d], nb);
+                    bulk_load(ring + at, blob + off, nb, &full[d]);
+                }
+                __syncwarp();
             }
         }
-        __syncwarp();
     } else {
         const int ct = threadIdx.x - 32;
         const int grp = ct / GW, l16 = lane % GW;
@@ -710,7 +719,7 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
             asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");   // piece solved by every consumer
             if (ct == 0) {
                 // replay the producer's placement to publish the released bytes
-                const long long nb = piece_bytes[q0 + q];
+                const long long nb = hdr[3];
                 long long at = done_bytes % ring_bytes, need = nb;
                 if (at + nb > ring_bytes) need += ring_bytes - at;
                 done_bytes += need;
