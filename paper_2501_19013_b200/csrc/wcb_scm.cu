@@ -765,7 +765,7 @@ struct ScmOperator final : Operator {
     std::string step_kernel() const override {
         const std::string P = std::to_string(p);
         if (dim == 3)
-            return std::string(jsplit3(p) ? "k_scm3j<" : "k_scm3d<") + P + ",STEP> + k_cut_pre<" + P + ">" +
+            return std::string("k_scm3d<") + P + ",STEP> + k_cut_pre<" + P + ">" +
                    (n_e % 32 == 0 ? " + k_scm3d_zline/zcol" : "");
         if (ncomp == 2) return "k_ela2d<" + P + ",STEP> (plane strain, fused CDM update)";
         return (stream2d_off ? "k_scm2d<" : "k_scm2s<") + P + ",STEP> (fused CDM update)";

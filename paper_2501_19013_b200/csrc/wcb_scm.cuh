@@ -88,33 +88,15 @@ struct MinvTab {
 #ifndef WCB3D_WY3
 #define WCB3D_WY3 7
 #endif
-// WCB3D_JSPLIT=1 runs the z-node-split kernel for P = 3 (k_scm3j, P warps
-// per y cell row, 128 registers, 15 warps per SM).  Measured on config 5 it
-// is slower than k_scm3d (3.3-4.0 ms vs 2.9 ms per step: 1.6x the executed
-// instructions, barrier stalls over 15 warps), so the
-// one-warp-per-row kernel is the default.
-#ifndef WCB3D_JSPLIT
-#define WCB3D_JSPLIT 0
-#endif
-#ifndef WCB3D_WYJ
-#define WCB3D_WYJ 4
-#endif
-__host__ __device__ constexpr bool jsplit3(int P) { return WCB3D_JSPLIT && P == 3; }
-__host__ __device__ constexpr int wy_for3(int P) {
-    return jsplit3(P) ? WCB3D_WYJ : P <= 2 ? 7 : P == 3 ? WCB3D_WY3 : 2;
-}
+__host__ __device__ constexpr int wy_for3(int P) { return P <= 2 ? 7 : P == 3 ? WCB3D_WY3 : 2; }
 // resident CTAs per SM the launch bounds ask for
-__host__ __device__ constexpr int cpsm_for3(int P) {
-    return jsplit3(P) ? 1 : P == 3 && WCB3D_WY3 >= 7 ? 1 : P <= 3 ? 2 : 1;
-}
+__host__ __device__ constexpr int cpsm_for3(int P) { return P == 3 && WCB3D_WY3 >= 7 ? 1 : P <= 3 ? 2 : 1; }
 __host__ __device__ constexpr int la_for3(int P) { return P <= 3 ? P : 1; }
 
 template <int P>
 struct Str3 {
     static constexpr int WY = wy_for3(P);
-    // k_scm3d: one warp per y cell row (+ halo warp); k_scm3j: P warps per
-    // row, warp j owning the cell-local z node j of its lane's cell
-    static constexpr int NWARP = jsplit3(P) ? (WY + 1) * P : WY + 1;
+    static constexpr int NWARP = WY + 1;            // one warp per y cell row + the halo warp
     static constexpr int TZ = 32 * P;               // owned node columns (z)
     static constexpr int CO = P & 1;                // 16-byte TMA alignment offset
     static constexpr int UW = ((TZ + P + 1 + CO) + 1) / 2 * 2;
@@ -124,10 +106,11 @@ struct Str3 {
     static constexpr int SLOT = (PLANE * 8 + 127) / 128 * 128 / 8;   // slot stride (doubles, 128 B aligned)
     static constexpr size_t RING_BYTES = (size_t)S * SLOT * 8;
     static constexpr size_t OFF_XCH = (RING_BYTES + 127) / 128 * 128;   // [NWARP][P+1][P or 1][32]
-    static constexpr size_t OFF_PREV = OFF_XCH + (size_t)NWARP * (P + 1) * (jsplit3(P) ? 1 : P) * 32 * 8;   // [P][WY*P][TZ]
+    static constexpr size_t OFF_PREV = OFF_XCH + (size_t)NWARP * (P + 1) * P * 32 * 8;   // [P][WY*P][TZ]
     static constexpr size_t PREV_BYTES = (size_t)P * WY * P * TZ * 8;
     static constexpr size_t OFF_BAR = OFF_PREV + (PREV_BYTES + 127) / 128 * 128;
-    static constexpr size_t SMEM = OFF_BAR + 8 * (S + 1);
+    // mbarriers: full[S], prev, rowdone, xfull[NWARP], xempty[NWARP]
+    static constexpr size_t SMEM = OFF_BAR + 8 * (S + 2 + 2 * NWARP);
 };
 
 // part: -1 all x chunks (+ z column kernels); 0 the first and last chunk

@@ -212,7 +212,7 @@ void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t
 // node value is the same fixed-order sum whatever the chunking (slabs too).
 template <int P, int MODE>
 __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
-    k_scm3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_p, Scm3DGeo g,
+    k_scm3d_v1(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_p, Scm3DGeo g,
             Mats2<P> mt, MinvTab<P> mtab, double sk, StepArgs a) {
     using T = Str3<P>;
     constexpr int N = P + 1;
@@ -429,229 +429,309 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
 }
 
-// z-node-split variant of k_scm3d (default for P = 3): the P warps of a y cell
-// row share its lanes' cells, warp j owning cell-local z node j (warp j = 0
-// also takes the left neighbour cell's node P).  Per thread the x pass keeps
-// Y[P+1][P] (x plane, y node) of one z node instead of all P, which cuts the
-// registers enough for P x (WY+1) warps per SM (15 vs 8 for P = 3).  Same
-// streaming scheme: TMA ring of node planes, a full cell row of look-ahead,
-// plane-P reuse, one exchange of the shared y node row per cell row, cut-cell
-// products from k_cut_pre, carry of x plane P, chunking-invariant sums.
+// Dataflow version of the streaming stencil (default).  Same sums in the same
+// order as k_scm3d_v1 (bitwise equal fields), but no block barrier inside the
+// x loop: warps run loosely coupled through mbarriers --
+//   full[s]    TMA ring slot s landed (as before)
+//   rowdone    every compute warp is past cell row t (its epilogue included):
+//              the halo/producer warp waits on it before refilling row t's ring
+//              slots and the psi_{k-1} buffer
+//   xfull[w] / xempty[w]   the shared y node row of warp w (YP) handed to the
+//              warp below it, single buffer with a full/empty handshake
+// so a warp delayed by cut cells or a non-table 1/m row no longer stalls the
+// other seven (ncu on v1: 17 % barrier stalls).  `live` and `reuse` are
+// warp-level votes (both only skip work whose result is identical).  The cell
+// codes of row t+1 are loaded during row t.  Accumulators start from their
+// first product instead of being zeroed (v1: 11 % of all instructions were
+// CS2R zeroing).  Epilogue: lanes whose cell takes 1/m from the interior
+// table and whose rows hold no source node run a branch-free path with the
+// table as immediate constants and all loads of a node row issued before its
+// arithmetic (v1: a dependent constant/global load per node, 20 % long
+// scoreboard stalls); other lanes keep the general path.
 template <int P, int MODE>
-__global__ void __launch_bounds__(Str3<P>::NWARP * 32, 1)
-    k_scm3j(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_p, Scm3DGeo g,
+__global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
+    k_scm3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_p, Scm3DGeo g,
             Mats2<P> mt, MinvTab<P> mtab, double sk, StepArgs a) {
     using T = Str3<P>;
     constexpr int N = P + 1;
     constexpr int WY = T::WY;
     constexpr int S = T::S;
-    constexpr int L = N * N * N;
+    constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ __align__(128) unsigned char smem[];
     const double* ring = reinterpret_cast<const double*>(smem);
-    double* xch = reinterpret_cast<double*>(smem + T::OFF_XCH);   // [NWARP][N][32]
+    double* xch = reinterpret_cast<double*>(smem + T::OFF_XCH);   // [NWARP][N*P][32]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
-    uint64_t* pbar = full + S;
+    uint64_t* pbar = full + S;                                           // psi_{k-1} of a cell row
+    uint64_t* rowdone = pbar + 1;
+    uint64_t* xfull = rowdone + 1;
+    uint64_t* xempty = xfull + T::NWARP;
     const double* prv = reinterpret_cast<const double*>(smem + T::OFF_PREV);   // [P][WY*P][TZ]
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
-    const int yw = w / P, jz = w % P;   // y cell row slot (WY = halo), cell-local z node
     const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z + g.xc0;
     if (MODE == MODE_STEP && zs == 0 && yb == 0 && blockIdx.z == 0) record_observers(a);
     if (!g.cflags[(xc * g.n_yb + yb) * g.n_zs + zs]) return;
     const int64_t K0 = zs * T::TZ;
     const int64_t ey0 = yb * WY;
-    const int64_t exA = 1 + xc * g.xc;
+    const int64_t exA = 1 + xc * g.xc;                                   // first row with an epilogue
     const int64_t exE = exA + g.xc < g.ex_last + 1 ? exA + g.xc : g.ex_last + 1;
-    const int64_t G0 = (exA - 1) * P, G1 = (exE - 1) * P + P;
-    const bool halo = (yw == WY);
-    const int64_t ey = halo ? ey0 - 1 : ey0 + yw;
+    const int64_t G0 = (exA - 1) * P;
+    const int nplanes = (int)(exE - exA + 1) * P + 1;                    // node planes streamed (G0 ..)
+    const bool halo = (w == WY);
+    const int64_t ey = halo ? ey0 - 1 : ey0 + w;                         // this warp's cell row
     const int64_t ez = K0 / P + lane;
-    const int trow = (halo ? 0 : yw + 1) * P;
-    const bool producer = halo && jz == 0 && lane == 0;
-    auto issue = [&](int64_t gp) {
-        const int s = (int)((gp - G0) % S);
+    const int trow = (halo ? 0 : w + 1) * P;                             // tile row of node row ey*P
+    auto issue = [&](int lp) {   // streamed plane lp (global plane G0 + lp) -> its ring slot
+        const int s = lp % S;
         mbar_expect_tx(&full[s], (uint32_t)(T::PLANE * 8));
         tma_load_3d(smem + (size_t)s * T::SLOT * 8, &tm_u, (int32_t)(K0 - P - T::CO + PADJ),
-                    (int32_t)(ey0 * P), (int32_t)(gp + P), &full[s]);
+                    (int32_t)(ey0 * P), (int32_t)(G0 + lp + P), &full[s]);
     };
     if (threadIdx.x == 0) {
         #pragma unroll
         for (int s = 0; s < S + 1; ++s) mbar_init(&full[s], 1);
+        mbar_init(rowdone, WY * 32);
+        for (int q = 0; q < T::NWARP; ++q) {
+            mbar_init(&xfull[q], 32);
+            mbar_init(&xempty[q], 32);
+        }
     }
     __syncthreads();
-    if (producer)
-        for (int64_t gp = G0; gp <= G1 && gp < G0 + S; ++gp) issue(gp);
-    // z pass coefficients of this thread's node: m1[jz][d], k1[jz][d] (own
-    // cell, d = 0..P) and m1[P][d], k1[P][d] (left cell, jz = 0 only)
-    double zm[N], zk[N];
+    if (halo && lane == 0)
+        for (int lp = 0; lp < nplanes && lp < S; ++lp) issue(lp);
+    double mc[orb_count(P)], kc[orb_count(P)];
     #pragma unroll
-    for (int d = 0; d < N; ++d) {
-        zm[d] = 0.0;
-        zk[d] = 0.0;
-        #pragma unroll
-        for (int q = 0; q < P; ++q)
-            if (q == jz) { zm[d] = mt.m[orb(P, q, d)]; zk[d] = mt.k[orb(P, q, d)]; }
-    }
+    for (int i = 0; i < orb_count(P); ++i) { mc[i] = mt.m[i]; kc[i] = mt.k[i]; }
     const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
+    const double f0 = f * 0.0;
     const int64_t s_ = g.n_e + 2;
-    const int up = halo ? WY : (yw == 0 ? WY : yw - 1);   // exchange source row slot
-    double Y[N][P];
-    #pragma unroll
-    for (int r = 0; r < N; ++r)
-        #pragma unroll
-        for (int b = 0; b < P; ++b) Y[r][b] = 0.0;
-    unsigned long long amp = 0ULL;
-    double Au[N], Bu[N], YP[N];
-    bool pxRR = false, pxRL = false;
-    for (int64_t ex = exA - 1; ex < exE; ++ex) {
-        uint8_t cRR = 0, cRL = 0, cUR = 0, cUL = 0;
+    const int up = w == 0 ? WY : w - 1;              // exchange source warp (compute warps)
+    const bool sends = halo || w < WY - 1;           // the last compute warp's row P belongs to the next block
+    double* const xw = xch + (size_t)w * N * P * 32 + lane;
+    const double* const xr = xch + (size_t)up * N * P * 32 + lane;
+    // cell codes of (ex, ey, ez), (ex, ey, ez-1), (ex, ey-1, ez), (ex, ey-1, ez-1), packed
+    auto codes = [&](int64_t ex) -> uint32_t {
+        uint32_t cRR = 0, cRL = 0, cUR = 0, cUL = 0;
         if (ex >= 0 && ex < g.n_ex && ez <= g.n_e && ey >= -1 && ey <= g.n_e) {
             const uint8_t* mrow = g.mask + ((ex + 1) * s_ + (ey + 1)) * s_;
             if (ey < g.n_e && ey >= 0) { cRR = __ldg(mrow + ez + 1); cRL = __ldg(mrow + ez); }
             if (!halo && ey >= 1) { cUR = __ldg(mrow - s_ + ez + 1); cUL = __ldg(mrow - s_ + ez); }
         }
-        const double xRR = cRR == 1, xRL = (jz == 0 && cRL == 1) ? 1.0 : 0.0;
-        const bool cln = g.clean && cRR == 1 && ex >= 1 && __ldg(g.clean + (ex * g.n_e + ey) * g.n_e + ez) != 0;
-        const bool live = __syncthreads_or((cRR | cRL) != 0);
-        const bool reuse = ex > exA - 1 && !__syncthreads_or((cRR == 1) != pxRR || (cRL == 1) != pxRL);
+        return cRR | (cRL << 8) | (cUR << 16) | (cUL << 24);
+    };
+    auto clean_of = [&](int64_t ex) -> uint32_t {
+        if (halo || !g.clean || ex < 1 || ex >= g.n_ex || ey >= g.n_e || ez >= g.n_e) return 0u;
+        return __ldg(g.clean + (ex * g.n_e + ey) * g.n_e + ez);
+    };
+    double Y[N][P][P];
+    #pragma unroll
+    for (int b = 0; b < P; ++b)
+        #pragma unroll
+        for (int j = 0; j < P; ++j) Y[0][b][j] = 0.0;
+    unsigned long long amp = 0ULL;
+    // Au/Bu persist across cell rows: plane P of row ex is plane 0 of row
+    // ex+1, so when none of this warp's uncut flags changes between the rows
+    // its y/z contraction is reused instead of recomputed.  YP accumulates this
+    // warp's contribution to the next warp's node row 0 (y-local row P) for
+    // every x plane of the row; it is handed over once per cell row.
+    double Au[N][P], Bu[N][P];
+    double YP[N][P];
+    #pragma unroll
+    for (int b = 0; b < N; ++b)
+        #pragma unroll
+        for (int j = 0; j < P; ++j) { Au[b][j] = 0.0; Bu[b][j] = 0.0; }
+    bool pxRR = false, pxRL = false;
+    uint32_t ncode = codes(exA - 1), nclean = clean_of(exA - 1);
+    int t = 0;                                        // row index within the chunk
+    for (int64_t ex = exA - 1; ex < exE; ++ex, ++t) {
+        const uint32_t code = ncode;
+        const uint32_t cRR = code & 0xff, cRL = (code >> 8) & 0xff;
+        const bool cln = cRR == 1 && nclean != 0;
+        if (ex + 1 < exE) { ncode = codes(ex + 1); nclean = clean_of(ex + 1); }
+        const double xRR = cRR == 1, xRL = cRL == 1;
+        const bool live = __any_sync(FULL, (cRR | cRL) != 0);
+#if WCB3D_REUSE
+        const bool reuse = t > 0 && !__any_sync(FULL, (cRR == 1) != pxRR || (cRL == 1) != pxRL);
+#else
+        const bool reuse = false;
+#endif
         pxRR = cRR == 1;
         pxRL = cRL == 1;
-        if (producer && ex >= exA) {
-            #pragma unroll 1
-            for (int q = 0; q < P; ++q) {
-                const int64_t np = (ex - 1) * P + q + S;
-                if (np <= G1) issue(np);
+        if (halo && t > 0) {   // refill row t-1's planes (a full row of look-ahead), psi_{k-1} of row t
+            mbar_wait(rowdone, (uint32_t)((t - 1) & 1));
+            if (lane == 0) {
+                #pragma unroll 1
+                for (int q = 0; q < P; ++q) {
+                    const int lp = (t - 1) * P + q + S;
+                    if (lp < nplanes) issue(lp);
+                }
+                if (MODE == MODE_STEP) {
+                    mbar_expect_tx(pbar, (uint32_t)T::PREV_BYTES);
+                    tma_load_3d(smem + T::OFF_PREV, &tm_p, (int32_t)(K0 + PADJ), (int32_t)(ey0 * P + P),
+                                (int32_t)(ex * P + P), pbar);
+                }
             }
-            if (MODE == MODE_STEP) {
-                mbar_expect_tx(pbar, (uint32_t)T::PREV_BYTES);
-                tma_load_3d(smem + T::OFF_PREV, &tm_p, (int32_t)(K0 + PADJ), (int32_t)(ey0 * P + P),
-                            (int32_t)(ex * P + P), pbar);
-            }
+            __syncwarp();
         }
         #pragma unroll
-        for (int r = 0; r < N; ++r) YP[r] = 0.0;
-        #pragma unroll
         for (int c = 0; c < N; ++c) {
-            if (!(c == 0 && reuse)) {
-                const int64_t gp = ex * P + c;
-                const int slot = (int)((gp - G0) % S);
+            if (!(c == 0 && reuse)) {   // warp-uniform
+                const int lp = t * P + c;
+                const int slot = lp % S;
                 const double* plane = ring + (size_t)slot * T::SLOT;
-                #pragma unroll
-                for (int b = 0; b < N; ++b) { Au[b] = 0.0; Bu[b] = 0.0; }
-                mbar_wait(&full[slot], (uint32_t)(((gp - G0) / S) & 1));
+                mbar_wait(&full[slot], (uint32_t)((lp / S) & 1));
                 if (live) {
                     #pragma unroll
                     for (int e = 0; e < N; ++e) {
-                        const double* own = plane + (size_t)(trow + e) * T::UW + T::CO + P + lane * P;
-                        // own cell: node jz from nodes 0..P (the right one is the next cell's node 0)
-                        double s1 = zm[P] * own[P], s2 = zk[P] * own[P];
+                        double zmR[P], zkR[P], zmL, zkL;
+                        zpass_row<P>(mc, kc, plane + (size_t)(trow + e) * T::UW, lane, zmR, zkR, zmL, zkL);
+                        double am[P], ak[P];
                         #pragma unroll
-                        for (int d = 0; d < P; ++d) {
-                            s1 = fma(zm[d], own[d], s1);
-                            s2 = fma(zk[d], own[d], s2);
-                        }
-                        double am = xRR * s1, ak = xRR * s2;
-                        if (jz == 0) {   // left cell: its node P is our node 0
-                            double l1 = mt.m[orb(P, P, P)] * own[0], l2 = mt.k[orb(P, P, P)] * own[0];
-                            #pragma unroll
-                            for (int d = 0; d < P; ++d) {
-                                l1 = fma(mt.m[orb(P, P, d)], own[d - P], l1);
-                                l2 = fma(mt.k[orb(P, P, d)], own[d - P], l2);
-                            }
-                            am = fma(xRL, l1, am);
-                            ak = fma(xRL, l2, ak);
-                        }
+                        for (int j = 0; j < P; ++j) { am[j] = xRR * zmR[j]; ak[j] = xRR * zkR[j]; }
+                        am[0] = fma(xRL, zmL, am[0]);
+                        ak[0] = fma(xRL, zkL, ak[0]);
                         #pragma unroll
                         for (int b = 0; b < N; ++b) {
                             if (halo && b < P) continue;
-                            Au[b] = fma(mt.m[orb(P, b, e)], am, Au[b]);
-                            Bu[b] = fma(mt.k[orb(P, b, e)], am, fma(mt.m[orb(P, b, e)], ak, Bu[b]));
+                            #pragma unroll
+                            for (int j = 0; j < P; ++j) {
+                                if (e == 0) {   // first product starts the sum (== fma onto 0)
+                                    Au[b][j] = mc[orb(P, b, e)] * am[j];
+                                    Bu[b][j] = fma(kc[orb(P, b, e)], am[j], mc[orb(P, b, e)] * ak[j]);
+                                } else {
+                                    Au[b][j] = fma(mc[orb(P, b, e)], am[j], Au[b][j]);
+                                    Bu[b][j] = fma(kc[orb(P, b, e)], am[j], fma(mc[orb(P, b, e)], ak[j], Bu[b][j]));
+                                }
+                            }
                         }
                     }
+                } else {
+                    #pragma unroll
+                    for (int b = 0; b < N; ++b)
+                        #pragma unroll
+                        for (int j = 0; j < P; ++j) { Au[b][j] = 0.0; Bu[b][j] = 0.0; }
                 }
             }
+            // x pass (plane 0 of a reused row takes the previous row's plane-P Au/Bu)
             #pragma unroll
             for (int r = 0; r < N; ++r) {
-                YP[r] = fma(mt.k[orb(P, r, c)], Au[P], fma(mt.m[orb(P, r, c)], Bu[P], YP[r]));
+                #pragma unroll
+                for (int j = 0; j < P; ++j) {
+                    if (c == 0) YP[r][j] = fma(kc[orb(P, r, c)], Au[P][j], mc[orb(P, r, c)] * Bu[P][j]);
+                    else YP[r][j] = fma(kc[orb(P, r, c)], Au[P][j], fma(mc[orb(P, r, c)], Bu[P][j], YP[r][j]));
+                }
                 if (!halo) {
                     #pragma unroll
                     for (int b = 0; b < P; ++b)
-                        Y[r][b] = fma(mt.k[orb(P, r, c)], Au[b], fma(mt.m[orb(P, r, c)], Bu[b], Y[r][b]));
+                        #pragma unroll
+                        for (int j = 0; j < P; ++j) {
+                            if (c == 0 && r > 0)
+                                Y[r][b][j] = fma(kc[orb(P, r, c)], Au[b][j], mc[orb(P, r, c)] * Bu[b][j]);
+                            else
+                                Y[r][b][j] = fma(kc[orb(P, r, c)], Au[b][j], fma(mc[orb(P, r, c)], Bu[b][j], Y[r][b][j]));
+                        }
                 }
             }
         }
-        {
-            double* xw = xch + (size_t)w * N * 32 + lane;
+        // hand the shared y node row to the warp below (single buffer, full/empty)
+        if (sends) {
+            if (t > 0) mbar_wait(&xempty[w], (uint32_t)((t - 1) & 1));
             #pragma unroll
-            for (int r = 0; r < N; ++r) xw[r * 32] = YP[r];
+            for (int r = 0; r < N; ++r)
+                #pragma unroll
+                for (int j = 0; j < P; ++j) xw[(r * P + j) * 32] = YP[r][j];
+            mbar_arrive(&xfull[w]);
         }
-        __syncthreads();
         if (!halo) {
-            const double* xr = xch + (size_t)(up * P + jz) * N * 32 + lane;
+            mbar_wait(&xfull[up], (uint32_t)(t & 1));
             #pragma unroll
-            for (int r = 0; r < N; ++r) Y[r][0] += xr[r * 32];
-            // cut cells (K_o u_e / sk from k_cut_pre): own row, then the y-up
-            // row's local row P (our node row 0); left cell before own cell
-            const int64_t cbase = (ex * g.n_e + ey) * g.n_e + ez;
-            if (jz == 0 && cRL == 2) {
-                const double* o = g.cut_out + (int64_t)__ldg(g.cut_id + cbase - 1) * L;
+            for (int r = 0; r < N; ++r)
                 #pragma unroll
-                for (int a2 = 0; a2 < N; ++a2)
+                for (int j = 0; j < P; ++j) Y[r][0][j] += xr[(r * P + j) * 32];
+            mbar_arrive(&xempty[up]);
+            // dense cut cells: own y row (ey) and the y-up row (ey-1)
+            const uint32_t cUR = (code >> 16) & 0xff, cUL = code >> 24;
+            const unsigned clR = __ballot_sync(FULL, cRR == 2);
+            const bool edR = __shfl_sync(FULL, cRL == 2, 0);
+            if (clR || edR) cut_cells_warp3<P>(g, ex, ey, K0 / P, lane, clR, edR, false, Y);
+            const unsigned clU = __ballot_sync(FULL, cUR == 2);
+            const bool edU = __shfl_sync(FULL, cUL == 2, 0);
+            if (clU || edU) cut_cells_warp3<P>(g, ex, ey - 1, K0 / P, lane, clU, edU, true, Y);
+            if (t > 0) {
+                if (MODE == MODE_STEP) mbar_wait(pbar, (uint32_t)((t - 1) & 1));
+                const int64_t Kl = K0 + lane * P;
+                const int64_t base0 = (ex * P + P) * g.pplane + (ey * P + P) * g.prow + Kl + PADJ;
+                const int64_t baseL = base0 + (P - 1) * (g.pplane + g.prow) + (P - 1);
+                bool fast = false;
+                if constexpr (MODE == MODE_STEP) fast = cln && (baseL < a.F.lo || base0 > a.F.hi);
+                if (fast) {
+                    // every node of the cell is an owned DOF with the table's 1/m, no source node
+                    const double* up0 = prv + (size_t)(w * P) * T::TZ + lane * P;
+                    const int u0 = trow * T::UW + T::CO + P + lane * P;
                     #pragma unroll
-                    for (int b = 0; b < P; ++b) Y[a2][b] += __ldcg(o + (a2 * N + b) * N + P);
-            }
-            if (cRR == 2) {
-                const double* o = g.cut_out + (int64_t)__ldg(g.cut_id + cbase) * L;
-                #pragma unroll
-                for (int a2 = 0; a2 < N; ++a2)
+                    for (int r = 0; r < P; ++r) {
+                        const double* pl = ring + (size_t)((t * P + r) % S) * T::SLOT + u0;
+                        double* orow = a.out + base0 + r * g.pplane;
+                        #pragma unroll
+                        for (int b = 0; b < P; ++b) {
+                            double uu[P], pp[P], v[P];
+                            #pragma unroll
+                            for (int j = 0; j < P; ++j) {
+                                uu[j] = pl[b * T::UW + j];
+                                pp[j] = up0[((size_t)r * WY * P + b) * T::TZ + j];
+                            }
+                            #pragma unroll
+                            for (int j = 0; j < P; ++j)
+                                v[j] = leapfrog(uu[j], pp[j], sk * Y[r][b][j], mtab.v[(r * P + b) * P + j], f0, a.dt2);
+                            #pragma unroll
+                            for (int j = 0; j < P; ++j) {
+                                orow[b * g.prow + j] = v[j];
+                                const unsigned long long bits = amp_bits(v[j]);
+                                amp = bits > amp ? bits : amp;
+                            }
+                        }
+                    }
+                } else {
                     #pragma unroll
-                    for (int b = 0; b < P; ++b) Y[a2][b] += __ldcg(o + (a2 * N + b) * N + jz);
-            }
-            if (jz == 0 && cUL == 2) {
-                const double* o = g.cut_out + (int64_t)__ldg(g.cut_id + cbase - g.n_e - 1) * L;
-                #pragma unroll
-                for (int a2 = 0; a2 < N; ++a2) Y[a2][0] += __ldcg(o + (a2 * N + P) * N + P);
-            }
-            if (cUR == 2) {
-                const double* o = g.cut_out + (int64_t)__ldg(g.cut_id + cbase - g.n_e) * L;
-                #pragma unroll
-                for (int a2 = 0; a2 < N; ++a2) Y[a2][0] += __ldcg(o + (a2 * N + P) * N + jz);
-            }
-            if (ex >= exA) {
-                if (MODE == MODE_STEP) mbar_wait(pbar, (uint32_t)((ex - exA) & 1));
-                const int64_t Kn = K0 + lane * P + jz;
-                #pragma unroll
-                for (int r = 0; r < P; ++r) {
-                    const int64_t I = ex * P + r;
-                    if (I >= g.row_hi) break;
-                    const double* pl = ring + (size_t)((I - G0) % S) * T::SLOT;
-                    #pragma unroll
-                    for (int b = 0; b < P; ++b) {
-                        const int64_t J = ey * P + b;
-                        if (J >= g.n1 || Kn >= g.n1) break;
-                        const int64_t base = (I + P) * g.pplane + (J + P) * g.prow + Kn + PADJ;
-                        if constexpr (MODE == MODE_APPLY) {
-                            a.out[base] = sk * Y[r][b];
-                        } else {
-                            const double u = pl[(size_t)(trow + b) * T::UW + T::CO + P + lane * P + jz];
-                            const bool src = base >= a.F.lo && base <= a.F.hi;
-                            const double fF = src ? f * source_at(a.F, base) : f * 0.0;
-                            const double mi = cln ? mtab.v[(r * P + b) * P + jz] : __ldg(a.minv + base);
-                            const double upv = prv[((size_t)r * WY * P + yw * P + b) * T::TZ + lane * P + jz];
-                            const double v = leapfrog(u, upv, sk * Y[r][b], mi, fF, a.dt2);
-                            a.out[base] = v;
-                            const unsigned long long bits = mi != 0.0 ? amp_bits(v) : 0ULL;
-                            amp = bits > amp ? bits : amp;
+                    for (int r = 0; r < P; ++r) {
+                        const int64_t I = ex * P + r;
+                        if (I >= g.row_hi) break;
+                        const double* pl = ring + (size_t)((t * P + r) % S) * T::SLOT;
+                        #pragma unroll
+                        for (int b = 0; b < P; ++b) {
+                            const int64_t J = ey * P + b;
+                            if (J >= g.n1) break;
+                            const int64_t base = (I + P) * g.pplane + (J + P) * g.prow + Kl + PADJ;
+                            if constexpr (MODE == MODE_APPLY) {
+                                #pragma unroll
+                                for (int j = 0; j < P; ++j)
+                                    if (Kl + j < g.n1) a.out[base + j] = sk * Y[r][b][j];
+                            } else {
+                                const double* urow = pl + (size_t)(trow + b) * T::UW + T::CO + P + lane * P;
+                                const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
+                                #pragma unroll
+                                for (int j = 0; j < P; ++j) {
+                                    if (Kl + j < g.n1) {
+                                        const double fF = src ? f * source_at(a.F, base + j) : f0;
+                                        const double mi = cln ? mtab.v[(r * P + b) * P + j] : __ldg(a.minv + base + j);
+                                        const double upv = prv[((size_t)r * WY * P + w * P + b) * T::TZ + lane * P + j];
+                                        const double v = leapfrog(urow[j], upv, sk * Y[r][b][j], mi, fF, a.dt2);
+                                        a.out[base + j] = v;
+                                        const unsigned long long bits = mi != 0.0 ? amp_bits(v) : 0ULL;
+                                        amp = bits > amp ? bits : amp;
+                                    }
+                                }
+                            }
                         }
                     }
                 }
             }
+            // x plane P of cell row ex is plane 0 of cell row ex+1
             #pragma unroll
-            for (int b = 0; b < P; ++b) {
-                Y[0][b] = Y[P][b];
+            for (int b = 0; b < P; ++b)
                 #pragma unroll
-                for (int r = 1; r < N; ++r) Y[r][b] = 0.0;
-            }
+                for (int j = 0; j < P; ++j) Y[0][b][j] = Y[P][b][j];
+            mbar_arrive(rowdone);
         }
     }
     if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
@@ -769,9 +849,10 @@ void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map
         StepArgs a = a0;
         if (!obs) a.obs_out = nullptr;
         dim3 grid((unsigned)g.n_zs, (unsigned)g.n_yb, (unsigned)nz);
-        if constexpr (jsplit3(P)) {
-            ensure_smem_attr((const void*)k_scm3j<P, MODE>, ctx->device, (size_t)T::SMEM);
-            k_scm3j<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
+        static const bool v1 = [] { const char* e = getenv("WCB3D_V1"); return e && e[0] == '1'; }();
+        if (v1) {
+            ensure_smem_attr((const void*)k_scm3d_v1<P, MODE>, ctx->device, (size_t)T::SMEM);
+            k_scm3d_v1<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
         } else {
             ensure_smem_attr((const void*)k_scm3d<P, MODE>, ctx->device, (size_t)T::SMEM);
             k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
