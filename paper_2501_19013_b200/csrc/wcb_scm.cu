@@ -718,7 +718,8 @@ struct ScmOperator final : Operator {
     int64_t pplane = 0, n_zs = 0, n_yb = 0, n_xc = 0, xc3 = 0, ex_last = 0;   // 3D streaming grid
     int64_t probe_base = -1;          // 3D: state index of an interior uncut cell's node (0,0,0)
     std::vector<double> minv_tab;     // its P^3 owned 1/m values (bind_minv)
-    DevBuf<uint8_t> clean;            // 3D: per local cell: owned 1/m == minv_tab
+    DevBuf<uint8_t> clean;            // 3D: per local cell: 1/m class (1: owned 1/m == minv_tab, 2: no DOF)
+    DevBuf<uint8_t> cinfo;            // 3D: mask with the class in bits 2-3
     DevBuf<uint8_t> tclean;           // 2D: per tile
     DevBuf<uint8_t> sflags;           // elastic streaming step: per (x chunk, strip) owns a DOF
     int64_t n_xs = 0, xs_len = 0;     // elastic streaming step: x chunks, cell rows per chunk
@@ -1068,6 +1069,7 @@ struct ScmOperator final : Operator {
         MinvTab<P> tab{};
         if (MODE == MODE_STEP && a.minv && a.minv == minv_bound && clean.p) {
             g.clean = clean.p;
+            g.mask = cinfo.p;   // codes + 1/m classes
             for (int i = 0; i < P * P * P; ++i) tab.v[i] = minv_tab[i];
         }
         const CUtensorMap& mu = state_map3<P>(a.cur);
@@ -1092,13 +1094,15 @@ struct ScmOperator final : Operator {
             tab.v[i] = h[i];
         }
         if (!clean.p) clean.alloc((size_t)n_ex * n_e * n_e);
-        launch_clean3d<P>(ctx, geo3(), tab, d_minv, clean.p);
+        if (!cinfo.p) cinfo.alloc(mask.n);
+        WCB_CUDA(cudaMemcpyAsync(cinfo.p, mask.p, mask.n, cudaMemcpyDeviceToDevice, ctx->stream));
+        launch_clean3d<P>(ctx, geo3(), tab, d_minv, clean.p, cinfo.p);
         WCB_CHECK_LAUNCH();
         std::vector<uint8_t> hc(clean.n);
         WCB_CUDA(cudaMemcpyAsync(hc.data(), clean.p, hc.size(), cudaMemcpyDeviceToHost, ctx->stream));
         WCB_CUDA(cudaStreamSynchronize(ctx->stream));
         int64_t nclean = 0;
-        for (uint8_t v : hc) nclean += v;
+        for (uint8_t v : hc) nclean += v == 1;
         minv_skipped = (double)nclean * P * P * P;
         minv_tab = h;
         minv_bound = d_minv;

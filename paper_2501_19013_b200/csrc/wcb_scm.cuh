@@ -66,9 +66,10 @@ struct Scm3DGeo {
     int64_t n_xc;             // x chunks
     int64_t xc;               // x cell rows per chunk
     int64_t ex_last;          // last local x cell row holding an owned node plane
-    // cells whose P^3 owned nodes all carry the interior 1/m of minv_tab
-    // (bitwise, checked on the device once per plan): the epilogue skips the
-    // 1/m stream there.  null: every node loads 1/m.
+    // non-null: `mask` carries the 1/m class of every cell in bits 2-3
+    // (k_clean3d, once per plan: 1 = the P^3 owned nodes all carry the interior
+    // 1/m of minv_tab, bitwise -- the epilogue skips the 1/m stream there;
+    // 2 = no owned node is a DOF).  null: every node loads 1/m.
     const uint8_t* clean;
     double2* zline;           // (n_ex P + 1) x n1 z-lines of the last cell column (n_e % 32 == 0)
     int64_t xc0 = 0;          // first x chunk of this launch (blockIdx.z + xc0)
@@ -110,7 +111,10 @@ struct Str3 {
     static constexpr size_t PREV_BYTES = (size_t)P * WY * P * TZ * 8;
     static constexpr size_t OFF_BAR = OFF_PREV + (PREV_BYTES + 127) / 128 * 128;
     // mbarriers: full[S], prev, rowdone, xfull[NWARP], xempty[NWARP]
-    static constexpr size_t SMEM = OFF_BAR + 8 * (S + 2 + 2 * NWARP);
+    static constexpr size_t OFF_TAB = OFF_BAR + 8 * (S + 2 + 2 * NWARP);   // interior 1/m table [P][P][P]
+    static constexpr int CODE_W = 36;                                      // cells ez0-1 .. ez0+31 (+ pad)
+    static constexpr size_t OFF_CODE = OFF_TAB + 8 * P * P * P;            // cell codes [2][WY+1][CODE_W]
+    static constexpr size_t SMEM = OFF_CODE + 2 * (WY + 1) * CODE_W;
 };
 
 // part: -1 all x chunks (+ z column kernels); 0 the first and last chunk
@@ -118,9 +122,11 @@ struct Str3 {
 template <int P, int MODE>
 void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map_p, const Scm3DGeo& g,
                   const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a, int part = -1);
-// clean[c] = 1 when every owned node of local cell c has minv == tab (bitwise)
+// clean[c] = 1/m class of local cell c (1: minv == tab bitwise on every owned
+// node, 2: no DOF); cinfo = mask with the class in bits 2-3
 template <int P>
-void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean);
+void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean,
+                    uint8_t* cinfo);
 // packed lower triangle of a cut cell's K_o / sk, stride padded to 16 bytes
 __host__ __device__ constexpr int cut_lp_stride(int P) {
     return (((P + 1) * (P + 1) * (P + 1)) * (((P + 1) * (P + 1) * (P + 1)) + 1) / 2 + 1) / 2 * 2;

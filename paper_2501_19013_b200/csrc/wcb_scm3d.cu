@@ -210,244 +210,24 @@ void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t
 // (epilogue), and Y[P] becomes Y[0] of the next cell row.  Each chunk of x
 // cell rows starts one row early (no epilogue) to build that carry, so every
 // node value is the same fixed-order sum whatever the chunking (slabs too).
-template <int P, int MODE>
-__global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
-    k_scm3d_v1(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_p, Scm3DGeo g,
-            Mats2<P> mt, MinvTab<P> mtab, double sk, StepArgs a) {
-    using T = Str3<P>;
-    constexpr int N = P + 1;
-    constexpr int WY = T::WY;
-    constexpr int S = T::S;
-    extern __shared__ __align__(128) unsigned char smem[];
-    const double* ring = reinterpret_cast<const double*>(smem);
-    double* xch = reinterpret_cast<double*>(smem + T::OFF_XCH);   // [2][NWARP][2P][32]
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
-    uint64_t* pbar = full + S;                                           // psi_{k-1} of a cell row
-    const double* prv = reinterpret_cast<const double*>(smem + T::OFF_PREV);   // [P][WY*P][TZ]
-    const int lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
-    const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z + g.xc0;
-    if (MODE == MODE_STEP && zs == 0 && yb == 0 && blockIdx.z == 0) record_observers(a);
-    if (!g.cflags[(xc * g.n_yb + yb) * g.n_zs + zs]) return;
-    const int64_t K0 = zs * T::TZ;
-    const int64_t ey0 = yb * WY;
-    const int64_t exA = 1 + xc * g.xc;                                   // first row with an epilogue
-    const int64_t exE = exA + g.xc < g.ex_last + 1 ? exA + g.xc : g.ex_last + 1;
-    const int64_t G0 = (exA - 1) * P, G1 = (exE - 1) * P + P;           // node planes streamed
-    const bool halo = (w == WY);
-    const int64_t ey = halo ? ey0 - 1 : ey0 + w;                         // this warp's cell row
-    const int64_t ez = K0 / P + lane;
-    const int trow = (halo ? 0 : w + 1) * P;                             // tile row of node row ey*P
-    const bool producer = halo && lane == 0;
-    auto issue = [&](int64_t gp) {   // plane gp -> its ring slot
-        const int s = (int)((gp - G0) % S);
-        mbar_expect_tx(&full[s], (uint32_t)(T::PLANE * 8));
-        tma_load_3d(smem + (size_t)s * T::SLOT * 8, &tm_u, (int32_t)(K0 - P - T::CO + PADJ),
-                    (int32_t)(ey0 * P), (int32_t)(gp + P), &full[s]);
-    };
-    if (threadIdx.x == 0) {
-        #pragma unroll
-        for (int s = 0; s < S + 1; ++s) mbar_init(&full[s], 1);
-    }
-    __syncthreads();
-    if (producer)
-        for (int64_t gp = G0; gp <= G1 && gp < G0 + S; ++gp) issue(gp);
-    double mc[orb_count(P)], kc[orb_count(P)];
-    #pragma unroll
-    for (int i = 0; i < orb_count(P); ++i) { mc[i] = mt.m[i]; kc[i] = mt.k[i]; }
-    const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
-    const int64_t s_ = g.n_e + 2;
-    const int up = halo ? WY : (w == 0 ? WY : w - 1);   // exchange source warp
-    double Y[N][P][P];
-    #pragma unroll
-    for (int r = 0; r < N; ++r)
-        #pragma unroll
-        for (int b = 0; b < P; ++b)
-            #pragma unroll
-            for (int j = 0; j < P; ++j) Y[r][b][j] = 0.0;
-    unsigned long long amp = 0ULL;
-    // Au/Bu persist across cell rows: plane P of row ex is plane 0 of row
-    // ex+1, so when no uncut flag of the CTA changes between the rows its
-    // y/z contraction is reused instead of recomputed.  YP accumulates this
-    // warp's contribution to the next warp's node row 0 (y-local row P) for
-    // every x plane of the row; it is exchanged once per cell row.
-    double Au[N][P], Bu[N][P];
-    double YP[N][P];
-    bool pxRR = false, pxRL = false;
-    for (int64_t ex = exA - 1; ex < exE; ++ex) {
-        // codes of (ex, ey, ez), (ex, ey, ez-1), (ex, ey-1, ez), (ex, ey-1, ez-1)
-        uint8_t cRR = 0, cRL = 0, cUR = 0, cUL = 0;
-        if (ex >= 0 && ex < g.n_ex && ez <= g.n_e && ey >= -1 && ey <= g.n_e) {
-            const uint8_t* mrow = g.mask + ((ex + 1) * s_ + (ey + 1)) * s_;
-            if (ey < g.n_e && ey >= 0) { cRR = __ldg(mrow + ez + 1); cRL = __ldg(mrow + ez); }
-            if (!halo && ey >= 1) { cUR = __ldg(mrow - s_ + ez + 1); cUL = __ldg(mrow - s_ + ez); }
-        }
-        const double xRR = cRR == 1, xRL = cRL == 1;
-        const bool cln = g.clean && cRR == 1 && ex >= 1 && __ldg(g.clean + (ex * g.n_e + ey) * g.n_e + ez) != 0;
-        // row-start barrier: every warp is past row ex-1's epilogue
-        const bool live = __syncthreads_or((cRR | cRL) != 0);   // any uncut/cut work in this CTA row
-#if WCB3D_REUSE
-        const bool reuse = ex > exA - 1 && !__syncthreads_or((cRR == 1) != pxRR || (cRL == 1) != pxRL);
-#else
-        const bool reuse = false;
-#endif
-        pxRR = cRR == 1;
-        pxRL = cRL == 1;
-        if (producer && ex >= exA) {   // refill row ex-1's planes (a full row of look-ahead)
-            #pragma unroll 1
-            for (int q = 0; q < P; ++q) {
-                const int64_t np = (ex - 1) * P + q + S;
-                if (np <= G1) issue(np);
-            }
-            if (MODE == MODE_STEP) {   // psi_{k-1} of row ex's owned nodes for its epilogue
-                mbar_expect_tx(pbar, (uint32_t)T::PREV_BYTES);
-                tma_load_3d(smem + T::OFF_PREV, &tm_p, (int32_t)(K0 + PADJ), (int32_t)(ey0 * P + P),
-                            (int32_t)(ex * P + P), pbar);
-            }
-        }
-        #pragma unroll
-        for (int a2 = 0; a2 < N; ++a2)
-            #pragma unroll
-            for (int j = 0; j < P; ++j) YP[a2][j] = 0.0;
-        #pragma unroll
-        for (int c = 0; c < N; ++c) {
-          if (!(c == 0 && reuse)) {   // CTA-uniform
-            const int64_t gp = ex * P + c;
-            const int slot = (int)((gp - G0) % S);
-            const double* plane = ring + (size_t)slot * T::SLOT;
-            #pragma unroll
-            for (int b = 0; b < N; ++b)
-                #pragma unroll
-                for (int j = 0; j < P; ++j) { Au[b][j] = 0.0; Bu[b][j] = 0.0; }
-            mbar_wait(&full[slot], (uint32_t)(((gp - G0) / S) & 1));
-            if (live) {
-                #pragma unroll
-                for (int e = 0; e < N; ++e) {
-                    double zmR[P], zkR[P], zmL, zkL;
-                    zpass_row<P>(mc, kc, plane + (size_t)(trow + e) * T::UW, lane, zmR, zkR, zmL, zkL);
-                    double am[P], ak[P];
-                    #pragma unroll
-                    for (int j = 0; j < P; ++j) { am[j] = xRR * zmR[j]; ak[j] = xRR * zkR[j]; }
-                    am[0] = fma(xRL, zmL, am[0]);
-                    ak[0] = fma(xRL, zkL, ak[0]);
-                    #pragma unroll
-                    for (int b = 0; b < N; ++b) {
-                        if (halo && b < P) continue;
-                        #pragma unroll
-                        for (int j = 0; j < P; ++j) {
-                            Au[b][j] = fma(mc[orb(P, b, e)], am[j], Au[b][j]);
-                            Bu[b][j] = fma(kc[orb(P, b, e)], am[j], fma(mc[orb(P, b, e)], ak[j], Bu[b][j]));
-                        }
-                    }
-                }
-            }
-          }
-            // x pass (plane 0 of a reused row takes the previous row's plane-P Au/Bu)
-            #pragma unroll
-            for (int r = 0; r < N; ++r) {
-                #pragma unroll
-                for (int j = 0; j < P; ++j)
-                    YP[r][j] = fma(kc[orb(P, r, c)], Au[P][j], fma(mc[orb(P, r, c)], Bu[P][j], YP[r][j]));
-                if (!halo) {
-                    #pragma unroll
-                    for (int b = 0; b < P; ++b)
-                        #pragma unroll
-                        for (int j = 0; j < P; ++j)
-                            Y[r][b][j] = fma(kc[orb(P, r, c)], Au[b][j], fma(mc[orb(P, r, c)], Bu[b][j], Y[r][b][j]));
-                }
-            }
-        }
-        // y exchange of the shared node row: own + row above's contribution
-        {
-            double* xw = xch + (size_t)w * N * P * 32 + lane;
-            #pragma unroll
-            for (int r = 0; r < N; ++r)
-                #pragma unroll
-                for (int j = 0; j < P; ++j) xw[(r * P + j) * 32] = YP[r][j];
-        }
-        __syncthreads();
-        if (!halo) {
-            const double* xr = xch + (size_t)up * N * P * 32 + lane;
-            #pragma unroll
-            for (int r = 0; r < N; ++r)
-                #pragma unroll
-                for (int j = 0; j < P; ++j) Y[r][0][j] += xr[(r * P + j) * 32];
-            // dense cut cells: own y row (ey) and the y-up row (ey-1)
-            const unsigned clR = __ballot_sync(0xffffffffu, cRR == 2);
-            const bool edR = __shfl_sync(0xffffffffu, cRL == 2, 0);
-            if (clR || edR) cut_cells_warp3<P>(g, ex, ey, K0 / P, lane, clR, edR, false, Y);
-            const unsigned clU = __ballot_sync(0xffffffffu, cUR == 2);
-            const bool edU = __shfl_sync(0xffffffffu, cUL == 2, 0);
-            if (clU || edU) cut_cells_warp3<P>(g, ex, ey - 1, K0 / P, lane, clU, edU, true, Y);
-            if (ex >= exA) {
-                if (MODE == MODE_STEP) mbar_wait(pbar, (uint32_t)((ex - exA) & 1));
-                const int64_t Kl = K0 + lane * P;
-                #pragma unroll
-                for (int r = 0; r < P; ++r) {
-                    const int64_t I = ex * P + r;
-                    if (I >= g.row_hi) break;
-                    const double* pl = ring + (size_t)((I - G0) % S) * T::SLOT;
-                    #pragma unroll
-                    for (int b = 0; b < P; ++b) {
-                        const int64_t J = ey * P + b;
-                        if (J >= g.n1) break;
-                        const int64_t base = (I + P) * g.pplane + (J + P) * g.prow + Kl + PADJ;
-                        if constexpr (MODE == MODE_APPLY) {
-                            #pragma unroll
-                            for (int j = 0; j < P; ++j)
-                                if (Kl + j < g.n1) a.out[base + j] = sk * Y[r][b][j];
-                        } else {
-                            const double* urow = pl + (size_t)(trow + b) * T::UW + T::CO + P + lane * P;
-                            const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
-                            #pragma unroll
-                            for (int j = 0; j < P; ++j) {
-                                if (Kl + j < g.n1) {
-                                    const double fF = src ? f * source_at(a.F, base + j) : f * 0.0;
-                                    const double mi = cln ? mtab.v[(r * P + b) * P + j] : __ldg(a.minv + base + j);
-                                    const double up = prv[((size_t)r * WY * P + w * P + b) * T::TZ + lane * P + j];
-                                    const double v = leapfrog(urow[j], up, sk * Y[r][b][j], mi, fF, a.dt2);
-                                    a.out[base + j] = v;
-                                    const unsigned long long bits = mi != 0.0 ? amp_bits(v) : 0ULL;
-                                    amp = bits > amp ? bits : amp;
-                                }
-                            }
-                        }
-                    }
-                }
-            }
-            // x plane P of cell row ex is plane 0 of cell row ex+1
-            #pragma unroll
-            for (int b = 0; b < P; ++b)
-                #pragma unroll
-                for (int j = 0; j < P; ++j) {
-                    Y[0][b][j] = Y[P][b][j];
-                    #pragma unroll
-                    for (int r = 1; r < N; ++r) Y[r][b][j] = 0.0;
-                }
-        }
-    }
-    if constexpr (MODE == MODE_STEP) block_amp_max<T::NWARP * 32>(amp, a.amp);
-}
-
-// Dataflow version of the streaming stencil (default).  Same sums in the same
-// order as k_scm3d_v1 (bitwise equal fields), but no block barrier inside the
-// x loop: warps run loosely coupled through mbarriers --
-//   full[s]    TMA ring slot s landed (as before)
-//   rowdone    every compute warp is past cell row t (its epilogue included):
-//              the halo/producer warp waits on it before refilling row t's ring
-//              slots and the psi_{k-1} buffer
+//
+// No block barrier inside the x loop: the warps run loosely coupled through
+// mbarriers (ncu on the barrier version: 17 % barrier stalls, every warp
+// waiting for the slowest three times per row) --
+//   full[s]    TMA ring slot s landed
+//   rowdone    every compute warp is past cell row t (epilogue included)
+//   pbar       the halo/producer warp's per-row post: after rowdone(t-1) it
+//              stores the cell codes of row t+1 (loaded during its row t) into
+//              the shared code buffer, refills row t-1's ring slots and fetches
+//              psi_{k-1} of row t; compute warps wait on it before their epilogue
 //   xfull[w] / xempty[w]   the shared y node row of warp w (YP) handed to the
 //              warp below it, single buffer with a full/empty handshake
-// so a warp delayed by cut cells or a non-table 1/m row no longer stalls the
-// other seven (ncu on v1: 17 % barrier stalls).  `live` and `reuse` are
-// warp-level votes (both only skip work whose result is identical).  The cell
-// codes of row t+1 are loaded during row t.  Accumulators start from their
-// first product instead of being zeroed (v1: 11 % of all instructions were
-// CS2R zeroing).  Epilogue: lanes whose cell takes 1/m from the interior
-// table and whose rows hold no source node run a branch-free path with the
-// table as immediate constants and all loads of a node row issued before its
-// arithmetic (v1: a dependent constant/global load per node, 20 % long
-// scoreboard stalls); other lanes keep the general path.
+// `live` and `reuse` are warp-level votes (both only skip work whose result
+// is identical).  Accumulators start from their first product instead of
+// being zeroed.  Epilogue, one x plane (P x P nodes per thread) at a time:
+// every load of the plane is issued before its arithmetic; 1/m comes from the
+// interior table (class 1 cells), is 0 (class 2: no owned node is a DOF,
+// nothing is stored) or is loaded (class 0, prefetched into L2 at row start).
 template <int P, int MODE>
 __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     k_scm3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_p, Scm3DGeo g,
@@ -456,16 +236,21 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     constexpr int N = P + 1;
     constexpr int WY = T::WY;
     constexpr int S = T::S;
+    constexpr int CW = T::CODE_W;
     constexpr unsigned FULL = 0xffffffffu;
+    constexpr bool LATE_REFILL = S >= 2 * P + 1;   // the ring holds two full cell rows
+    constexpr int EB = P <= 3 ? P : 1;             // node rows per batch of epilogue loads
     extern __shared__ __align__(128) unsigned char smem[];
     const double* ring = reinterpret_cast<const double*>(smem);
     double* xch = reinterpret_cast<double*>(smem + T::OFF_XCH);   // [NWARP][N*P][32]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
-    uint64_t* pbar = full + S;                                           // psi_{k-1} of a cell row
+    uint64_t* pbar = full + S;
     uint64_t* rowdone = pbar + 1;
     uint64_t* xfull = rowdone + 1;
     uint64_t* xempty = xfull + T::NWARP;
     const double* prv = reinterpret_cast<const double*>(smem + T::OFF_PREV);   // [P][WY*P][TZ]
+    double* stab = reinterpret_cast<double*>(smem + T::OFF_TAB);
+    uint8_t* cbuf = smem + T::OFF_CODE;                                    // [2][WY+1][CW]
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z + g.xc0;
@@ -479,13 +264,36 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     const int nplanes = (int)(exE - exA + 1) * P + 1;                    // node planes streamed (G0 ..)
     const bool halo = (w == WY);
     const int64_t ey = halo ? ey0 - 1 : ey0 + w;                         // this warp's cell row
-    const int64_t ez = K0 / P + lane;
     const int trow = (halo ? 0 : w + 1) * P;                             // tile row of node row ey*P
+    const int64_t s_ = g.n_e + 2;
     auto issue = [&](int lp) {   // streamed plane lp (global plane G0 + lp) -> its ring slot
         const int s = lp % S;
         mbar_expect_tx(&full[s], (uint32_t)(T::PLANE * 8));
         tma_load_3d(smem + (size_t)s * T::SLOT * 8, &tm_u, (int32_t)(K0 - P - T::CO + PADJ),
                     (int32_t)(ey0 * P), (int32_t)(G0 + lp + P), &full[s]);
+    };
+    // Cell codes of one x cell row for the whole CTA: rows ey0-1 .. ey0+WY-1,
+    // cells ez0-1 .. ez0+31 (ring coordinates: +1), one byte each (bits 0-1:
+    // 0 out, 1 uncut, 2 cut; bits 2-3: 1/m class).  Loaded by the halo warp:
+    // lane l takes column l of every row, lanes 0..WY the last column.
+    uint32_t hc[WY + 2];
+    const int64_t ez0 = K0 / P;
+    auto load_codes = [&](int64_t ex) {
+        const bool in = ex >= 0 && ex < g.n_ex;
+        const uint8_t* base = g.mask + ((ex + 1) * s_ + ey0) * s_ + ez0;    // (ex, ey0-1, ez0-1)
+        #pragma unroll
+        for (int q = 0; q <= WY; ++q) {
+            hc[q] = 0;
+            if (in && ey0 + q < s_ && ez0 + lane < s_) hc[q] = __ldg(base + q * s_ + lane);
+        }
+        hc[WY + 1] = 0;
+        if (in && lane <= WY && ey0 + lane < s_ && ez0 + 32 < s_) hc[WY + 1] = __ldg(base + lane * s_ + 32);
+    };
+    auto store_codes = [&](int buf) {
+        uint8_t* c = cbuf + buf * (WY + 1) * CW;
+        #pragma unroll
+        for (int q = 0; q <= WY; ++q) c[q * CW + lane] = (uint8_t)hc[q];
+        if (lane <= WY) c[lane * CW + 32] = (uint8_t)hc[WY + 1];
     };
     if (threadIdx.x == 0) {
         #pragma unroll
@@ -496,6 +304,11 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
             mbar_init(&xempty[q], 32);
         }
     }
+    if (threadIdx.x < P * P * P) stab[threadIdx.x] = mtab.v[threadIdx.x];
+    if (halo) {
+        load_codes(exA - 1);
+        store_codes(0);
+    }
     __syncthreads();
     if (halo && lane == 0)
         for (int lp = 0; lp < nplanes && lp < S; ++lp) issue(lp);
@@ -504,25 +317,11 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     for (int i = 0; i < orb_count(P); ++i) { mc[i] = mt.m[i]; kc[i] = mt.k[i]; }
     const double f = (MODE == MODE_STEP) ? __ldg(a.ft + a.k) : 0.0;
     const double f0 = f * 0.0;
-    const int64_t s_ = g.n_e + 2;
     const int up = w == 0 ? WY : w - 1;              // exchange source warp (compute warps)
     const bool sends = halo || w < WY - 1;           // the last compute warp's row P belongs to the next block
     double* const xw = xch + (size_t)w * N * P * 32 + lane;
     const double* const xr = xch + (size_t)up * N * P * 32 + lane;
-    // cell codes of (ex, ey, ez), (ex, ey, ez-1), (ex, ey-1, ez), (ex, ey-1, ez-1), packed
-    auto codes = [&](int64_t ex) -> uint32_t {
-        uint32_t cRR = 0, cRL = 0, cUR = 0, cUL = 0;
-        if (ex >= 0 && ex < g.n_ex && ez <= g.n_e && ey >= -1 && ey <= g.n_e) {
-            const uint8_t* mrow = g.mask + ((ex + 1) * s_ + (ey + 1)) * s_;
-            if (ey < g.n_e && ey >= 0) { cRR = __ldg(mrow + ez + 1); cRL = __ldg(mrow + ez); }
-            if (!halo && ey >= 1) { cUR = __ldg(mrow - s_ + ez + 1); cUL = __ldg(mrow - s_ + ez); }
-        }
-        return cRR | (cRL << 8) | (cUR << 16) | (cUL << 24);
-    };
-    auto clean_of = [&](int64_t ex) -> uint32_t {
-        if (halo || !g.clean || ex < 1 || ex >= g.n_ex || ey >= g.n_e || ez >= g.n_e) return 0u;
-        return __ldg(g.clean + (ex * g.n_e + ey) * g.n_e + ez);
-    };
+    const int crow = halo ? 0 : w + 1;               // this warp's row of the code buffer
     double Y[N][P][P];
     #pragma unroll
     for (int b = 0; b < P; ++b)
@@ -541,13 +340,53 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
         #pragma unroll
         for (int j = 0; j < P; ++j) { Au[b][j] = 0.0; Bu[b][j] = 0.0; }
     bool pxRR = false, pxRL = false;
-    uint32_t ncode = codes(exA - 1), nclean = clean_of(exA - 1);
     int t = 0;                                        // row index within the chunk
+    // halo warp, once per row: codes of row t+1 -> shared, ring refill, psi_{k-1}
+    auto post = [&](int64_t ex) {
+        if (t > 0) mbar_wait(rowdone, (uint32_t)((t - 1) & 1));
+        store_codes((t + 1) & 1);
+        __syncwarp();
+        if (lane == 0) {
+            if (t > 0) {
+                #pragma unroll 1
+                for (int q = 0; q < P; ++q) {
+                    const int lp = (t - 1) * P + q + S;
+                    if (lp < nplanes) issue(lp);
+                }
+            }
+            if (MODE == MODE_STEP && t > 0) {
+                mbar_expect_tx(pbar, (uint32_t)T::PREV_BYTES);
+                tma_load_3d(smem + T::OFF_PREV, &tm_p, (int32_t)(K0 + PADJ), (int32_t)(ey0 * P + P),
+                            (int32_t)(ex * P + P), pbar);
+            } else {
+                mbar_arrive(pbar);
+            }
+        }
+        __syncwarp();
+    };
     for (int64_t ex = exA - 1; ex < exE; ++ex, ++t) {
-        const uint32_t code = ncode;
-        const uint32_t cRR = code & 0xff, cRL = (code >> 8) & 0xff;
-        const bool cln = cRR == 1 && nclean != 0;
-        if (ex + 1 < exE) { ncode = codes(ex + 1); nclean = clean_of(ex + 1); }
+        const uint8_t* crw = cbuf + ((t & 1) * (WY + 1) + crow) * CW + lane;
+        const uint32_t bRR = crw[1];
+        const uint32_t cRR = bRR & 3, cRL = crw[0] & 3;
+        const uint32_t cUR = halo ? 0u : (crw[1 - CW] & 3u), cUL = halo ? 0u : (crw[-CW] & 3u);
+        const uint32_t cls = (MODE == MODE_STEP) ? (bRR >> 2) : 0u;
+        if (halo) {
+            load_codes(ex + 1 < exE ? ex + 1 : -1);
+            if (!LATE_REFILL) post(ex);
+        }
+        const int64_t Kl = K0 + lane * P;
+        const int64_t base0 = (ex * P + P) * g.pplane + (ey * P + P) * g.prow + Kl + PADJ;
+        if (MODE == MODE_STEP && !halo && t > 0 && cls == 0) {
+            // 1/m of this cell is loaded in the epilogue: start it towards L2 now
+            #pragma unroll
+            for (int r = 0; r < P; ++r)
+                #pragma unroll
+                for (int b = 0; b < P; ++b) {
+                    const double* q = a.minv + base0 + r * g.pplane + b * g.prow;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(q + P - 1));
+                }
+        }
         const double xRR = cRR == 1, xRL = cRL == 1;
         const bool live = __any_sync(FULL, (cRR | cRL) != 0);
 #if WCB3D_REUSE
@@ -557,22 +396,6 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
 #endif
         pxRR = cRR == 1;
         pxRL = cRL == 1;
-        if (halo && t > 0) {   // refill row t-1's planes (a full row of look-ahead), psi_{k-1} of row t
-            mbar_wait(rowdone, (uint32_t)((t - 1) & 1));
-            if (lane == 0) {
-                #pragma unroll 1
-                for (int q = 0; q < P; ++q) {
-                    const int lp = (t - 1) * P + q + S;
-                    if (lp < nplanes) issue(lp);
-                }
-                if (MODE == MODE_STEP) {
-                    mbar_expect_tx(pbar, (uint32_t)T::PREV_BYTES);
-                    tma_load_3d(smem + T::OFF_PREV, &tm_p, (int32_t)(K0 + PADJ), (int32_t)(ey0 * P + P),
-                                (int32_t)(ex * P + P), pbar);
-                }
-            }
-            __syncwarp();
-        }
         #pragma unroll
         for (int c = 0; c < N; ++c) {
             if (!(c == 0 && reuse)) {   // warp-uniform
@@ -642,6 +465,9 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
                 for (int j = 0; j < P; ++j) xw[(r * P + j) * 32] = YP[r][j];
             mbar_arrive(&xfull[w]);
         }
+        // with a two-row ring the halo warp posts after its own row, so that warp 0
+        // never waits for the shared node row behind the row-done wait
+        if (LATE_REFILL && halo) post(ex);
         if (!halo) {
             mbar_wait(&xfull[up], (uint32_t)(t & 1));
             #pragma unroll
@@ -650,76 +476,72 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
                 for (int j = 0; j < P; ++j) Y[r][0][j] += xr[(r * P + j) * 32];
             mbar_arrive(&xempty[up]);
             // dense cut cells: own y row (ey) and the y-up row (ey-1)
-            const uint32_t cUR = (code >> 16) & 0xff, cUL = code >> 24;
             const unsigned clR = __ballot_sync(FULL, cRR == 2);
             const bool edR = __shfl_sync(FULL, cRL == 2, 0);
             if (clR || edR) cut_cells_warp3<P>(g, ex, ey, K0 / P, lane, clR, edR, false, Y);
             const unsigned clU = __ballot_sync(FULL, cUR == 2);
             const bool edU = __shfl_sync(FULL, cUL == 2, 0);
             if (clU || edU) cut_cells_warp3<P>(g, ex, ey - 1, K0 / P, lane, clU, edU, true, Y);
+            mbar_wait(pbar, (uint32_t)(t & 1));   // codes of row t+1 visible, psi_{k-1} of row t landed
             if (t > 0) {
-                if (MODE == MODE_STEP) mbar_wait(pbar, (uint32_t)((t - 1) & 1));
-                const int64_t Kl = K0 + lane * P;
-                const int64_t base0 = (ex * P + P) * g.pplane + (ey * P + P) * g.prow + Kl + PADJ;
-                const int64_t baseL = base0 + (P - 1) * (g.pplane + g.prow) + (P - 1);
-                bool fast = false;
-                if constexpr (MODE == MODE_STEP) fast = cln && (baseL < a.F.lo || base0 > a.F.hi);
-                if (fast) {
-                    // every node of the cell is an owned DOF with the table's 1/m, no source node
-                    const double* up0 = prv + (size_t)(w * P) * T::TZ + lane * P;
-                    const int u0 = trow * T::UW + T::CO + P + lane * P;
+                if constexpr (MODE == MODE_APPLY) {
                     #pragma unroll
                     for (int r = 0; r < P; ++r) {
-                        const double* pl = ring + (size_t)((t * P + r) % S) * T::SLOT + u0;
-                        double* orow = a.out + base0 + r * g.pplane;
+                        if (ex * P + r >= g.row_hi) break;
                         #pragma unroll
                         for (int b = 0; b < P; ++b) {
-                            double uu[P], pp[P], v[P];
-                            #pragma unroll
-                            for (int j = 0; j < P; ++j) {
-                                uu[j] = pl[b * T::UW + j];
-                                pp[j] = up0[((size_t)r * WY * P + b) * T::TZ + j];
-                            }
+                            if (ey * P + b >= g.n1) break;
                             #pragma unroll
                             for (int j = 0; j < P; ++j)
-                                v[j] = leapfrog(uu[j], pp[j], sk * Y[r][b][j], mtab.v[(r * P + b) * P + j], f0, a.dt2);
-                            #pragma unroll
-                            for (int j = 0; j < P; ++j) {
-                                orow[b * g.prow + j] = v[j];
-                                const unsigned long long bits = amp_bits(v[j]);
-                                amp = bits > amp ? bits : amp;
-                            }
+                                if (Kl + j < g.n1) a.out[base0 + r * g.pplane + b * g.prow + j] = sk * Y[r][b][j];
                         }
                     }
-                } else {
+                } else if (!__all_sync(FULL, cls == 2)) {
+                    const int64_t baseL = base0 + (P - 1) * (g.pplane + g.prow) + (P - 1);
+                    const bool anysrc = !(baseL < a.F.lo || base0 > a.F.hi);
+                    const double* up0 = prv + (size_t)(w * P) * T::TZ + lane * P;
+                    const int u0 = trow * T::UW + T::CO + P + lane * P;
+                    bool kin[P];
+                    #pragma unroll
+                    for (int j = 0; j < P; ++j) kin[j] = Kl + j < g.n1;
                     #pragma unroll
                     for (int r = 0; r < P; ++r) {
-                        const int64_t I = ex * P + r;
-                        if (I >= g.row_hi) break;
-                        const double* pl = ring + (size_t)((t * P + r) % S) * T::SLOT;
+                        const bool okr = ex * P + r < g.row_hi && cls != 2;
+                        const double* pl = ring + (size_t)((t * P + r) % S) * T::SLOT + u0;
+                        const int64_t baser = base0 + r * g.pplane;
                         #pragma unroll
-                        for (int b = 0; b < P; ++b) {
-                            const int64_t J = ey * P + b;
-                            if (J >= g.n1) break;
-                            const int64_t base = (I + P) * g.pplane + (J + P) * g.prow + Kl + PADJ;
-                            if constexpr (MODE == MODE_APPLY) {
-                                #pragma unroll
-                                for (int j = 0; j < P; ++j)
-                                    if (Kl + j < g.n1) a.out[base + j] = sk * Y[r][b][j];
-                            } else {
-                                const double* urow = pl + (size_t)(trow + b) * T::UW + T::CO + P + lane * P;
-                                const bool src = base + P - 1 >= a.F.lo && base <= a.F.hi;
+                        for (int b0 = 0; b0 < P; b0 += EB) {   // EB node rows per batch of loads
+                            double mi[EB][P], uu[EB][P], pp[EB][P], fF[EB][P];
+                            #pragma unroll
+                            for (int bb = 0; bb < EB; ++bb) {
+                                const int b = b0 + bb;
+                                const bool okb = okr && ey * P + b < g.n1;
                                 #pragma unroll
                                 for (int j = 0; j < P; ++j) {
-                                    if (Kl + j < g.n1) {
-                                        const double fF = src ? f * source_at(a.F, base + j) : f0;
-                                        const double mi = cln ? mtab.v[(r * P + b) * P + j] : __ldg(a.minv + base + j);
-                                        const double upv = prv[((size_t)r * WY * P + w * P + b) * T::TZ + lane * P + j];
-                                        const double v = leapfrog(urow[j], upv, sk * Y[r][b][j], mi, fF, a.dt2);
-                                        a.out[base + j] = v;
-                                        const unsigned long long bits = mi != 0.0 ? amp_bits(v) : 0ULL;
-                                        amp = bits > amp ? bits : amp;
-                                    }
+                                    mi[bb][j] = cls == 1 ? stab[(r * P + b) * P + j] : 0.0;
+                                    if (cls == 0 && okb && kin[j]) mi[bb][j] = __ldg(a.minv + baser + b * g.prow + j);
+                                    uu[bb][j] = pl[b * T::UW + j];
+                                    pp[bb][j] = up0[((size_t)r * WY * P + b) * T::TZ + j];
+                                    fF[bb][j] = f0;
+                                }
+                            }
+                            if (anysrc) {   // rare: a source node in this cell's index range
+                                #pragma unroll
+                                for (int bb = 0; bb < EB; ++bb)
+                                    #pragma unroll
+                                    for (int j = 0; j < P; ++j)
+                                        fF[bb][j] = f * source_at(a.F, baser + (b0 + bb) * g.prow + j);
+                            }
+                            #pragma unroll
+                            for (int bb = 0; bb < EB; ++bb) {
+                                const int b = b0 + bb;
+                                const bool okb = okr && ey * P + b < g.n1;
+                                #pragma unroll
+                                for (int j = 0; j < P; ++j) {
+                                    const double v = leapfrog(uu[bb][j], pp[bb][j], sk * Y[r][b][j], mi[bb][j], fF[bb][j], a.dt2);
+                                    if (okb && kin[j]) a.out[baser + b * g.prow + j] = v;
+                                    const unsigned long long bits = mi[bb][j] != 0.0 ? amp_bits(v) : 0ULL;
+                                    amp = bits > amp ? bits : amp;
                                 }
                             }
                         }
@@ -731,6 +553,10 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
             for (int b = 0; b < P; ++b)
                 #pragma unroll
                 for (int j = 0; j < P; ++j) Y[0][b][j] = Y[P][b][j];
+            // one arrival per warp and phase: the ring holds two cell rows, so
+            // a warp could otherwise finish row t+1 (and arrive twice) before
+            // a slower warp has arrived for row t
+            if (t > 0) mbar_wait(rowdone, (uint32_t)((t - 1) & 1));
             mbar_arrive(rowdone);
         }
     }
@@ -781,7 +607,7 @@ __global__ void __launch_bounds__(128) k_scm3d_zcol(Scm3DGeo g, Mats2<P> mt, dou
                 const int ib = (int)(J - ey * P);
                 if (ey < 0 || ey >= g.n_e || ib > P) continue;
                 const int64_t ez = g.n_e - 1;
-                const uint8_t code = g.mask[((ex + 1) * s_ + (ey + 1)) * s_ + ez + 1];
+                const uint8_t code = g.mask[((ex + 1) * s_ + (ey + 1)) * s_ + ez + 1] & 3;
                 if (code == 1) {
                     double s = 0.0;
                     #pragma unroll
@@ -814,27 +640,39 @@ __global__ void __launch_bounds__(128) k_scm3d_zcol(Scm3DGeo g, Mats2<P> mt, dou
     if constexpr (MODE == MODE_STEP) block_amp_max<128>(amp, a.amp);
 }
 
+// 1/m class of every local cell c: 1 when every owned node carries the
+// interior table's 1/m (bitwise), 2 when none of them is a DOF (1/m == +0
+// everywhere: the step neither loads 1/m nor stores there), else 0.  The
+// class goes into bits 2-3 of the cell's code byte (cinfo = mask | cls << 2).
 template <int P>
-__global__ void k_clean3d(Scm3DGeo g, MinvTab<P> tab, const double* __restrict__ minv, uint8_t* clean) {
+__global__ void k_clean3d(Scm3DGeo g, MinvTab<P> tab, const double* __restrict__ minv, uint8_t* clean,
+                          uint8_t* cinfo) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nc = g.n_ex * g.n_e * g.n_e;
     if (c >= nc) return;
     const int64_t ex = c / (g.n_e * g.n_e), ey = (c / g.n_e) % g.n_e, ez = c % g.n_e;
-    bool ok = ex >= 1;
-    for (int q = 0; q < P && ok; ++q)
-        for (int r = 0; r < P && ok; ++r)
-            for (int j = 0; j < P && ok; ++j) {
+    bool ok = ex >= 1, zero = true;
+    for (int q = 0; q < P; ++q)
+        for (int r = 0; r < P; ++r)
+            for (int j = 0; j < P; ++j) {
                 const int64_t I = ex * P + q;
                 const int64_t s = (I + P) * g.pplane + (ey * P + r + P) * g.prow + ez * P + j + PADJ;
-                ok = I < g.row_hi && __double_as_longlong(minv[s]) == __double_as_longlong(tab.v[(q * P + r) * P + j]);
+                const long long bits = __double_as_longlong(minv[s]);
+                ok = ok && I < g.row_hi && bits == __double_as_longlong(tab.v[(q * P + r) * P + j]);
+                zero = zero && bits == 0LL;
             }
-    clean[c] = ok ? 1 : 0;
+    const uint8_t cls = ok ? 1 : zero ? 2 : 0;
+    clean[c] = cls;
+    const int64_t s_ = g.n_e + 2;
+    const int64_t m = ((ex + 1) * s_ + (ey + 1)) * s_ + ez + 1;
+    cinfo[m] = (uint8_t)((g.mask[m] & 3) | (cls << 2));
 }
 
 template <int P>
-void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean) {
+void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean,
+                    uint8_t* cinfo) {
     const int64_t nc = g.n_ex * g.n_e * g.n_e;
-    k_clean3d<P><<<(unsigned)ceil_div(nc, 256), 256, 0, ctx->stream>>>(g, tab, minv, clean);
+    k_clean3d<P><<<(unsigned)ceil_div(nc, 256), 256, 0, ctx->stream>>>(g, tab, minv, clean, cinfo);
     ctx->launches++;
 }
 
@@ -849,14 +687,8 @@ void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map
         StepArgs a = a0;
         if (!obs) a.obs_out = nullptr;
         dim3 grid((unsigned)g.n_zs, (unsigned)g.n_yb, (unsigned)nz);
-        static const bool v1 = [] { const char* e = getenv("WCB3D_V1"); return e && e[0] == '1'; }();
-        if (v1) {
-            ensure_smem_attr((const void*)k_scm3d_v1<P, MODE>, ctx->device, (size_t)T::SMEM);
-            k_scm3d_v1<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
-        } else {
-            ensure_smem_attr((const void*)k_scm3d<P, MODE>, ctx->device, (size_t)T::SMEM);
-            k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
-        }
+        ensure_smem_attr((const void*)k_scm3d<P, MODE>, ctx->device, (size_t)T::SMEM);
+        k_scm3d<P, MODE><<<grid, T::NWARP * 32, T::SMEM, ctx->stream>>>(map_u, map_p, g, mt, mtab, sk, a);
         ctx->launches++;
     };
     const int64_t n = g0.n_xc;
@@ -886,7 +718,7 @@ void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map
     template void launch_scm3d<P, MODE_APPLY>(Context*, const CUtensorMap&, const CUtensorMap&, const Scm3DGeo&, \
                                               const Mats2<P>&, const MinvTab<P>&, double,       \
                                               const StepArgs&, int);                            \
-    template void launch_clean3d<P>(Context*, const Scm3DGeo&, const MinvTab<P>&, const double*, uint8_t*);
+    template void launch_clean3d<P>(Context*, const Scm3DGeo&, const MinvTab<P>&, const double*, uint8_t*, uint8_t*);
 #define WCB_INSTC(P) \
     template void launch_cut_pre<P>(Context*, int64_t, const double*, const int64_t*, int64_t, int64_t, \
                                     const double*, double*);
