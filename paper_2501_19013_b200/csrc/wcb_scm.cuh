@@ -114,7 +114,8 @@ struct Str3 {
     static constexpr size_t OFF_TAB = OFF_BAR + 8 * (S + 2 + 2 * NWARP);   // interior 1/m table [P][P][P]
     static constexpr int CODE_W = 36;                                      // cells ez0-1 .. ez0+31 (+ pad)
     static constexpr size_t OFF_CODE = OFF_TAB + 8 * P * P * P;            // cell codes [2][WY+1][CODE_W]
-    static constexpr size_t SMEM = OFF_CODE + 2 * (WY + 1) * CODE_W;
+    static constexpr size_t OFF_XTAB = (OFF_CODE + 2 * (WY + 1) * CODE_W + 15) / 16 * 16;   // x pass factors [P+1][2][P+1]
+    static constexpr size_t SMEM = OFF_XTAB + 8 * 2 * (P + 1) * (P + 1);
 };
 
 // part: -1 all x chunks (+ z column kernels); 0 the first and last chunk

@@ -223,8 +223,9 @@ void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t
 //   xfull[w] / xempty[w]   the shared y node row of warp w (YP) handed to the
 //              warp below it, single buffer with a full/empty handshake
 // `live` and `reuse` are warp-level votes (both only skip work whose result
-// is identical).  Accumulators start from their first product instead of
-// being zeroed.  Epilogue, one x plane (P x P nodes per thread) at a time:
+// is identical).  The P+1 planes of a row run through one rolled loop (x pass
+// factors from shared memory): unrolled, the kernel was 83 KB of code and
+// ncu showed 11 % instruction-fetch stalls.  Epilogue, one x plane (P x P nodes per thread) at a time:
 // every load of the plane is issued before its arithmetic; 1/m comes from the
 // interior table (class 1 cells), is 0 (class 2: no owned node is a DOF,
 // nothing is stored) or is loaded (class 0, prefetched into L2 at row start).
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     const double* prv = reinterpret_cast<const double*>(smem + T::OFF_PREV);   // [P][WY*P][TZ]
     double* stab = reinterpret_cast<double*>(smem + T::OFF_TAB);
     uint8_t* cbuf = smem + T::OFF_CODE;                                    // [2][WY+1][CW]
+    double* xtab = reinterpret_cast<double*>(smem + T::OFF_XTAB);          // [c][k1[.][c] | m1[.][c]]
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     const int64_t zs = blockIdx.x, yb = blockIdx.y, xc = blockIdx.z + g.xc0;
@@ -305,6 +307,15 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
         }
     }
     if (threadIdx.x < P * P * P) stab[threadIdx.x] = mtab.v[threadIdx.x];
+    if (threadIdx.x == 32) {
+        #pragma unroll
+        for (int c = 0; c < N; ++c)
+            #pragma unroll
+            for (int r = 0; r < N; ++r) {
+                xtab[(c * 2 + 0) * N + r] = mt.k[orb(P, r, c)];
+                xtab[(c * 2 + 1) * N + r] = mt.m[orb(P, r, c)];
+            }
+    }
     if (halo) {
         load_codes(exA - 1);
         store_codes(0);
@@ -396,7 +407,22 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
 #endif
         pxRR = cRR == 1;
         pxRL = cRL == 1;
+        // the planes of the row in a rolled loop (one copy of the y/z
+        // contraction in the instruction cache); x pass factors of plane c
+        // from shared memory
         #pragma unroll
+        for (int r = 0; r < N; ++r)
+            #pragma unroll
+            for (int j = 0; j < P; ++j) YP[r][j] = 0.0;
+        if (!halo) {
+            #pragma unroll
+            for (int r = 1; r < N; ++r)
+                #pragma unroll
+                for (int b = 0; b < P; ++b)
+                    #pragma unroll
+                    for (int j = 0; j < P; ++j) Y[r][b][j] = 0.0;
+        }
+        #pragma unroll 1
         for (int c = 0; c < N; ++c) {
             if (!(c == 0 && reuse)) {   // warp-uniform
                 const int lp = t * P + c;
@@ -436,23 +462,17 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
                 }
             }
             // x pass (plane 0 of a reused row takes the previous row's plane-P Au/Bu)
+            const double* xt = xtab + c * 2 * N;
             #pragma unroll
             for (int r = 0; r < N; ++r) {
+                const double xk = xt[r], xm = xt[N + r];
                 #pragma unroll
-                for (int j = 0; j < P; ++j) {
-                    if (c == 0) YP[r][j] = fma(kc[orb(P, r, c)], Au[P][j], mc[orb(P, r, c)] * Bu[P][j]);
-                    else YP[r][j] = fma(kc[orb(P, r, c)], Au[P][j], fma(mc[orb(P, r, c)], Bu[P][j], YP[r][j]));
-                }
+                for (int j = 0; j < P; ++j) YP[r][j] = fma(xk, Au[P][j], fma(xm, Bu[P][j], YP[r][j]));
                 if (!halo) {
                     #pragma unroll
                     for (int b = 0; b < P; ++b)
                         #pragma unroll
-                        for (int j = 0; j < P; ++j) {
-                            if (c == 0 && r > 0)
-                                Y[r][b][j] = fma(kc[orb(P, r, c)], Au[b][j], mc[orb(P, r, c)] * Bu[b][j]);
-                            else
-                                Y[r][b][j] = fma(kc[orb(P, r, c)], Au[b][j], fma(mc[orb(P, r, c)], Bu[b][j], Y[r][b][j]));
-                        }
+                        for (int j = 0; j < P; ++j) Y[r][b][j] = fma(xk, Au[b][j], fma(xm, Bu[b][j], Y[r][b][j]));
                 }
             }
         }
