@@ -94,26 +94,30 @@ __device__ __forceinline__ void cut_cells_warp3(const Scm3DGeo& g, int64_t ex, i
     }
 }
 
-// Cut-cell products u_e -> K_o u_e / sk.  Persistent warps walk the cut
+// Cut-cell products u_e -> K_o u_e / sk.  Persistent warp groups walk the cut
 // cells with a two-deep pipeline: the packed lower triangle of the next
 // cell's K_o / sk (L(L+1)/2 doubles, one 1D bulk copy) and its u_e (cp.async
 // gather from the state) land in shared memory while the current cell is
-// multiplied.  Lane r forms row r in ascending column order (running packed
+// multiplied.  A group is G = ceil(L/32) warps (two for P = 3), one row per
+// lane: lane r forms row r in ascending column order (running packed
 // indices: m <= r along row r, m > r down column r) -- the same sums as a
-// dense symmetric row.
+// dense symmetric row.  (One warp per cell with two rows per lane left the
+// SM at 6 warps, stalled on shared-memory latency: ncu, 312 us on config 5.)
 template <int P>
 struct CutPre {
     static constexpr int N = P + 1;
     static constexpr int L = N * N * N;
     static constexpr int LP = L * (L + 1) / 2;
     static constexpr int LPS = cut_lp_stride(P);                        // 16-byte multiple
-    static constexpr int W = P <= 2 ? 8 : P == 3 ? 6 : 1;               // warps per CTA
-    static constexpr int NS = 2;                                        // pipeline stages per warp (6 warps x 2 beat 4 x 3)
+    static constexpr int G = (L + 31) / 32 > 4 ? 4 : (L + 31) / 32;     // warps per cell
+    static constexpr int NG = P <= 2 ? 8 : P == 3 ? 6 : 1;              // groups per CTA
+    static constexpr int W = NG * G;                                    // warps per CTA
+    static constexpr int NS = 2;                                        // pipeline stages per group
     static constexpr size_t KB = ((size_t)LPS * 8 + 127) / 128 * 128;   // packed matrix buffer
     static constexpr size_t UB = ((size_t)L * 8 + 127) / 128 * 128;     // u_e buffer
-    static constexpr size_t PER_WARP = NS * (KB + UB);
-    static constexpr size_t OFF_BAR = W * PER_WARP;
-    static constexpr size_t SMEM = OFF_BAR + W * NS * 8;
+    static constexpr size_t PER_GROUP = NS * (KB + UB);
+    static constexpr size_t OFF_BAR = NG * PER_GROUP;
+    static constexpr size_t SMEM = OFF_BAR + NG * NS * 8;
 };
 
 __device__ __forceinline__ void cp_async8_g(void* dst, const void* src) {
@@ -121,33 +125,38 @@ __device__ __forceinline__ void cp_async8_g(void* dst, const void* src) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(256) k_cut_pre(int64_t n_cut, const double* __restrict__ KP,
-                                                 const int64_t* __restrict__ cut_base, int64_t pplane,
-                                                 int64_t prow, const double* __restrict__ u,
-                                                 double* __restrict__ out) {
+__global__ void __launch_bounds__(CutPre<P>::W * 32) k_cut_pre(int64_t n_cut, const double* __restrict__ KP,
+                                                               const int64_t* __restrict__ cut_base, int64_t pplane,
+                                                               int64_t prow, const double* __restrict__ u,
+                                                               double* __restrict__ out) {
     using C = CutPre<P>;
-    constexpr int N = C::N, L = C::L;
+    constexpr int N = C::N, L = C::L, G = C::G, NS = C::NS;
     extern __shared__ __align__(128) unsigned char smc[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    unsigned char* mine = smc + (size_t)w * C::PER_WARP;
-    constexpr int NS = C::NS;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smc + C::OFF_BAR) + NS * w;
-    const int64_t stride = (int64_t)gridDim.x * C::W;
-    const int64_t e0 = (int64_t)blockIdx.x * C::W + w;
-    if (lane == 0) {
+    const int grp = w / G, sub = w % G;           // group and warp within the group
+    const int gt = sub * 32 + lane;               // thread within the group
+    unsigned char* mine = smc + (size_t)grp * C::PER_GROUP;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smc + C::OFF_BAR) + NS * grp;
+    const int64_t stride = (int64_t)gridDim.x * C::NG;
+    const int64_t e0 = (int64_t)blockIdx.x * C::NG + grp;
+    auto gsync = [&]() {   // the group's warps
+        if (G == 1) __syncwarp();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(G * 32) : "memory");
+    };
+    if (gt == 0) {
         #pragma unroll
         for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
     }
-    __syncwarp();
+    gsync();
     auto fetch = [&](int64_t e, int buf) {   // K_o by bulk copy, u_e by cp.async
         double* kp = reinterpret_cast<double*>(mine + buf * (C::KB + C::UB));
         double* uu = reinterpret_cast<double*>(mine + buf * (C::KB + C::UB) + C::KB);
-        if (lane == 0) {
+        if (gt == 0) {
             mbar_expect_tx(&bar[buf], (uint32_t)(C::LPS * 8));
             bulk_load(kp, KP + e * C::LPS, (uint32_t)(C::LPS * 8), &bar[buf]);
         }
         const int64_t base = cut_base[e];
-        for (int m = lane; m < L; m += 32) {
+        for (int m = gt; m < L; m += G * 32) {
             const int a = m / (N * N), b = (m / N) % N, j = m % N;
             cp_async8_g(uu + m, u + base + a * pplane + b * prow + j);
         }
@@ -168,11 +177,11 @@ __global__ void __launch_bounds__(256) k_cut_pre(int64_t n_cut, const double* __
         if (en < n_cut) fetch(en, (it + NS - 1) % NS);
         else asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1) : "memory");
-        __syncwarp();   // every lane's u_e gather of this cell is visible
+        gsync();   // every thread's u_e gather of this cell is visible
         mbar_wait(&bar[buf], (uint32_t)((it / NS) & 1));
         const double* kp = reinterpret_cast<const double*>(mine + buf * (C::KB + C::UB));
         const double* uu = reinterpret_cast<const double*>(mine + buf * (C::KB + C::UB) + C::KB);
-        for (int r = lane; r < L; r += 32) {
+        for (int r = gt; r < L; r += G * 32) {
             double t = 0.0;
             int idx = r * (r + 1) / 2;   // (r, 0)
             #pragma unroll 8
@@ -185,7 +194,7 @@ __global__ void __launch_bounds__(256) k_cut_pre(int64_t n_cut, const double* __
             }
             out[e * L + r] = t;
         }
-        __syncwarp();   // buffer reused NS cells later
+        gsync();   // buffer reused NS cells later
     }
 }
 
@@ -195,7 +204,7 @@ void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t
     if (!n_cut) return;
     using C = CutPre<P>;
     ensure_smem_attr((const void*)k_cut_pre<P>, ctx->device, (size_t)C::SMEM);
-    const int64_t blocks = std::min<int64_t>(ceil_div(n_cut, C::W), (int64_t)ctx->sm_count * std::max<int64_t>(1, (int64_t)(220 * 1024 / C::SMEM)));
+    const int64_t blocks = std::min<int64_t>(ceil_div(n_cut, C::NG), (int64_t)ctx->sm_count * std::max<int64_t>(1, (int64_t)(220 * 1024 / C::SMEM)));
     k_cut_pre<P><<<(unsigned)blocks, 32 * C::W, C::SMEM, ctx->stream>>>(n_cut, KP, cut_base, pplane, prow, u, out);
     ctx->launches++;
 }
