@@ -115,65 +115,151 @@ static std::vector<int64_t> factor_components(int64_t n, const wcb_lu* lu, int64
     return comp;
 }
 
-// Segment layout of one piece (rows [k0, k1) of one level, every offset a
-// multiple of 16 bytes): int32 hdr[4] = {nrow, k0, ne, bytes}; int32 rptr[nrow+1]
-// (entry offsets within the piece); double pivot[nrow]; double val[ne];
-// int32 col[ne].  The whole piece is one bulk copy.
+// Segment layout of one piece (every offset a multiple of 16 bytes):
+// int32 hdr[8] = {nrow, k0, ne, bytes, kind, gbase, 0, 0}, then
+//   kind 0 (rows [k0, k0+nrow) of one level): int32 rptr[nrow+1] (entry offsets
+//     within the piece); double pivot[nrow]; double val[ne]; int32 col[ne]:
+//     x_k = (x_k - sum val x_col) * pivot
+//   kind 1 (rows of a group of narrow levels, entries outside the group only):
+//     same arrays; t[k0 + k - gbase] = x_k - sum val x_col (scratch, no pivot)
+//   kind 2 (the group's dense part): double W[nrow (nrow+1) / 2], the packed
+//     rows of inv(T), T the group's triangular block with its diagonal:
+//     x_k = sum_{j <= k} W[k][j] t[j]
+// The whole piece is one bulk copy.
+//
+// Groups: the factors' dependency chains end in long runs of levels holding
+// one or two rows (the dense trailing triangle of a patch: on config 4 the
+// longest patch has 454 levels, the last 230 of one row each, 130-250 entries
+// per row), where the level-scheduled solve pays one consumer barrier and one
+// serial dot product per row.  A run of consecutive levels of at most
+// TRSV_NARROW rows each (up to TRSV_GMAX rows in total) is solved in two
+// parallel steps instead: the entries outside the run for all its rows at
+// once (kind 1), then the multiplication by the host-inverted triangular block
+// (kind 2).  Mathematically the same solve; the rounding differs (bounded by
+// the parity tests).  WAVECELL_B200_TRSV_GROUPS=0 keeps one piece per level.
 constexpr int64_t TRSV_PIECE_BYTES = 24 * 1024;
+constexpr int TRSV_GMAX = 64;      // rows per group (dense part: 16.6 KB)
+constexpr int TRSV_NARROW = 16;    // a level joins a group when it has at most this many rows
+constexpr int TRSV_HDR = 32;
 static inline int64_t pad16(int64_t b) { return (b + 15) / 16 * 16; }
 static inline int64_t piece_size(int64_t nrow, int64_t ne) {
-    return 16 + pad16(4 * (nrow + 1)) + pad16(8 * nrow) + pad16(8 * ne) + pad16(4 * ne);
+    return TRSV_HDR + pad16(4 * (nrow + 1)) + pad16(8 * nrow) + pad16(8 * ne) + pad16(4 * ne);
 }
 static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp_rows,
                         const std::vector<int32_t>& comp_lvl, const std::vector<int32_t>& lvl_off,
                         const std::vector<int32_t>& sptr, const std::vector<double>& sdiag,
-                        const std::vector<double>& sval, const std::vector<int32_t>& slcol, cudaStream_t s) {
+                        const std::vector<double>& tdiag, const std::vector<double>& sval,
+                        const std::vector<int32_t>& slcol, cudaStream_t s) {
     std::vector<int64_t> off;
     std::vector<int32_t> bytes, cpiece(T.n_comp + 1, 0);
     std::vector<unsigned char> blob;
     int64_t maxp = 0;
     bool ok = true;
-    for (int64_t c = 0; c < T.n_comp; ++c) {
+    const bool groups = !(getenv("WAVECELL_B200_TRSV_GROUPS") && getenv("WAVECELL_B200_TRSV_GROUPS")[0] == '0');
+    // rows [k, e) (schedule order) as pieces of `kind`; entries with a column
+    // slot >= slot_lo are skipped (kind 1: they are in the dense part)
+    auto emit_rows = [&](int64_t k, int64_t e, int kind, int64_t gbase, int64_t slot_lo) {
+        std::vector<int32_t> cnt;   // kept entries per row
+        cnt.reserve(e - k);
+        for (int64_t r = k; r < e; ++r) {
+            int32_t c = 0;
+            for (int32_t j = sptr[r]; j < sptr[r + 1]; ++j) c += slcol[j] < slot_lo;
+            cnt.push_back(c);
+        }
+        int64_t r0 = k;
+        while (r0 < e && ok) {
+            int64_t r1 = r0, ne = 0;
+            if (piece_size(1, cnt[r0 - k]) > TRSV_PIECE_BYTES) { ok = false; break; }
+            while (r1 < e && piece_size(r1 + 1 - r0, ne + cnt[r1 - k]) <= TRSV_PIECE_BYTES) { ne += cnt[r1 - k]; ++r1; }
+            const int64_t nrow = r1 - r0;
+            const int64_t sz = piece_size(nrow, ne);
+            const int64_t base = (int64_t)blob.size();
+            blob.resize(base + sz, 0);
+            unsigned char* p = blob.data() + base;
+            int32_t* hdr = reinterpret_cast<int32_t*>(p);
+            hdr[0] = (int32_t)nrow;
+            hdr[1] = (int32_t)r0;
+            hdr[2] = (int32_t)ne;
+            hdr[3] = (int32_t)sz;
+            hdr[4] = kind;
+            hdr[5] = (int32_t)gbase;
+            int32_t* rp = reinterpret_cast<int32_t*>(p + TRSV_HDR);
+            double* dg = reinterpret_cast<double*>(p + TRSV_HDR + pad16(4 * (nrow + 1)));
+            double* vv = dg + pad16(8 * nrow) / 8;
+            int32_t* cc = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(vv) + pad16(8 * ne));
+            int32_t at = 0;
+            for (int64_t q = 0; q < nrow; ++q) {
+                rp[q] = at;
+                dg[q] = sdiag[r0 + q];
+                for (int32_t j = sptr[r0 + q]; j < sptr[r0 + q + 1]; ++j)
+                    if (slcol[j] < slot_lo) { vv[at] = sval[j]; cc[at] = slcol[j]; ++at; }
+            }
+            rp[nrow] = at;
+            off.push_back(base);
+            bytes.push_back((int32_t)sz);
+            r0 = r1;
+        }
+    };
+    for (int64_t c = 0; c < T.n_comp && ok; ++c) {
         cpiece[c] = (int32_t)off.size();
-        for (int32_t l = comp_lvl[c]; l < comp_lvl[c + 1]; ++l) {
-            int64_t k = lvl_off[l];
-            const int64_t e = lvl_off[l + 1];
-            while (k < e) {
-                // grow the piece row by row while it fits the slot
-                int64_t k1 = k + 1;
-                if (piece_size(1, sptr[k + 1] - sptr[k]) > TRSV_PIECE_BYTES) { ok = false; break; }
-                while (k1 < e && piece_size(k1 + 1 - k, sptr[k1 + 1] - sptr[k]) <= TRSV_PIECE_BYTES) ++k1;
-                const int64_t nrow = k1 - k, ne = sptr[k1] - sptr[k];
-                const int64_t sz = piece_size(nrow, ne);
+        const int64_t start = comp_rows[c];
+        int32_t l = comp_lvl[c];
+        const int32_t lend = comp_lvl[c + 1];
+        while (l < lend && ok) {
+            // a run of narrow levels?
+            int32_t l2 = l;
+            int64_t tot = 0;
+            while (groups && l2 < lend && lvl_off[l2 + 1] - lvl_off[l2] <= TRSV_NARROW &&
+                   tot + (lvl_off[l2 + 1] - lvl_off[l2]) <= TRSV_GMAX) {
+                tot += lvl_off[l2 + 1] - lvl_off[l2];
+                ++l2;
+            }
+            if (l2 - l >= 2) {
+                const int64_t ka = lvl_off[l], kb = lvl_off[l2], nr = kb - ka;
+                const int64_t slot_lo = ka - start;   // first local slot of the group
+                emit_rows(ka, kb, 1, ka, slot_lo);
+                // T = the group's triangular block (schedule order), W = inv(T)
+                std::vector<double> Tm((size_t)nr * nr, 0.0), W((size_t)nr * nr, 0.0);
+                for (int64_t r = 0; r < nr; ++r) {
+                    Tm[r * nr + r] = tdiag[ka + r];
+                    for (int32_t j = sptr[ka + r]; j < sptr[ka + r + 1]; ++j)
+                        if (slcol[j] >= slot_lo) Tm[r * nr + (slcol[j] - slot_lo)] = sval[j];
+                }
+                for (int64_t col = 0; col < nr; ++col) {   // forward substitution on unit vectors
+                    for (int64_t r = col; r < nr; ++r) {
+                        double acc = r == col ? 1.0 : 0.0;
+                        for (int64_t j = col; j < r; ++j) acc -= Tm[r * nr + j] * W[j * nr + col];
+                        W[r * nr + col] = acc / Tm[r * nr + r];
+                    }
+                }
+                const int64_t sz = TRSV_HDR + pad16(8 * nr * (nr + 1) / 2);
                 const int64_t base = (int64_t)blob.size();
                 blob.resize(base + sz, 0);
                 unsigned char* p = blob.data() + base;
                 int32_t* hdr = reinterpret_cast<int32_t*>(p);
-                hdr[0] = (int32_t)nrow;
-                hdr[1] = (int32_t)k;
-                hdr[2] = (int32_t)ne;
+                hdr[0] = (int32_t)nr;
+                hdr[1] = (int32_t)ka;
+                hdr[2] = 0;
                 hdr[3] = (int32_t)sz;
-                int32_t* rp = reinterpret_cast<int32_t*>(p + 16);
-                for (int64_t q = 0; q <= nrow; ++q) rp[q] = sptr[k + q] - sptr[k];
-                double* dg = reinterpret_cast<double*>(p + 16 + pad16(4 * (nrow + 1)));
-                for (int64_t q = 0; q < nrow; ++q) dg[q] = sdiag[k + q];
-                double* vv = dg + pad16(8 * nrow) / 8;
-                std::memcpy(vv, sval.data() + sptr[k], 8 * ne);
-                int32_t* cc = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(vv) + pad16(8 * ne));
-                std::memcpy(cc, slcol.data() + sptr[k], 4 * ne);
+                hdr[4] = 2;
+                hdr[5] = (int32_t)ka;
+                double* wp = reinterpret_cast<double*>(p + TRSV_HDR);
+                for (int64_t r = 0; r < nr; ++r)
+                    for (int64_t j = 0; j <= r; ++j) wp[r * (r + 1) / 2 + j] = W[r * nr + j];
                 off.push_back(base);
                 bytes.push_back((int32_t)sz);
-                k = k1;
+                l = l2;
+            } else {
+                emit_rows(lvl_off[l], lvl_off[l + 1], 0, 0, INT64_MAX);
+                ++l;
             }
-            if (!ok) break;
         }
-        if (!ok) break;
         maxp = std::max<int64_t>(maxp, (int64_t)off.size() - cpiece[c]);
     }
     T.ring_ok = false;
     if (!ok || off.empty()) return;
     cpiece[T.n_comp] = (int32_t)off.size();
-    const int64_t avail = (int64_t)TRSV_SMEM - T.max_size * 8 - 1024;
+    const int64_t avail = (int64_t)TRSV_SMEM - T.max_size * 8 - 1024 - TRSV_GMAX * 8;
     T.ring_depth = (int)std::min<int64_t>(4, avail / TRSV_PIECE_BYTES);
     if (avail < 2 * TRSV_PIECE_BYTES) return;   // the circular buffer holds >= 2 of the largest pieces
     T.max_pieces = maxp;
@@ -234,7 +320,7 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
     const bool recip = !(getenv("WAVECELL_B200_TRSV_DIV") && getenv("WAVECELL_B200_TRSV_DIV")[0] == '1');
     T.recip = recip;
     std::vector<int32_t> sptr(n + 1, 0), slcol;
-    std::vector<double> sval, sdiag(n, 0.0);
+    std::vector<double> sval, sdiag(n, 0.0), tdiag(n, 0.0);
     slcol.reserve(ptr[n]);
     sval.reserve(ptr[n]);
     for (int64_t k2 = 0; k2 < n; ++k2) {
@@ -243,6 +329,7 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
         for (int64_t j = ptr[i]; j < ptr[i + 1]; ++j) {
             if (idx[j] == i) {
                 sdiag[k2] = recip ? 1.0 / val[j] : val[j];
+                tdiag[k2] = val[j];
             } else {
                 slcol.push_back(pos[idx[j]]);
                 sval.push_back(val[j]);
@@ -304,7 +391,7 @@ static void build_sched(TriSched& T, int64_t n, const int64_t* ptr, const int32_
     T.comp_order.alloc(std::max<int64_t>(n_comp, 1), s);
     T.comp_order.upload(co.data(), n_comp, s);
     WCB_CUDA(cudaStreamSynchronize(s));
-    pack_pieces(T, n, comp_rows, comp_lvl, lvl_off, sptr, sdiag, sval, slcol, s);
+    pack_pieces(T, n, comp_rows, comp_lvl, lvl_off, sptr, sdiag, tdiag, sval, slcol, s);
 }
 
 struct DevLU {
@@ -652,6 +739,7 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
     volatile long long* rel = reinterpret_cast<volatile long long*>(smraw + TRSV_QK * 12);   // [2]
     unsigned char* ring = smraw + ((TRSV_QK * 12 + 16 + 127) / 128) * 128;
     double* xl = reinterpret_cast<double*>(ring + ring_bytes);
+    double* ts = xl + max_size;   // group scratch [TRSV_GMAX]
     const int c = comp_order[blockIdx.x];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
@@ -699,21 +787,34 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
             mbar_wait(&full[d], (uint32_t)((q / TRSV_QK) & 1));
             const unsigned char* pc = ring + poff[d];
             const int32_t* hdr = reinterpret_cast<const int32_t*>(pc);
-            const int nrow = hdr[0], k0 = hdr[1], ne = hdr[2];
-            const int32_t* rp = reinterpret_cast<const int32_t*>(pc + 16);
-            const double* dg = reinterpret_cast<const double*>(pc + 16 + ((4 * (nrow + 1) + 15) / 16) * 16);
-            const double* vv = dg + ((8 * nrow + 15) / 16) * 2;
-            const int32_t* cc = reinterpret_cast<const int32_t*>(reinterpret_cast<const unsigned char*>(vv) +
-                                                                 ((8 * (int64_t)ne + 15) / 16) * 16);
-            for (int k = grp; k < nrow; k += G) {
-                double sacc = 0.0;
-                const int p1 = rp[k + 1];
-                for (int j = rp[k] + l16; j < p1; j += GW) sacc = fma(vv[j], xl[cc[j]], sacc);
-                #pragma unroll
-                for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
-                if (l16 == 0) {
-                    const int i = k0 + k - r0;
-                    xl[i] = recip ? (xl[i] - sacc) * dg[k] : (xl[i] - sacc) / dg[k];
+            const int nrow = hdr[0], k0 = hdr[1], ne = hdr[2], kind = hdr[4], gbase = hdr[5];
+            if (kind == 2) {   // dense part of a group: x = W t
+                const double* W = reinterpret_cast<const double*>(pc + TRSV_HDR);
+                for (int k = grp; k < nrow; k += G) {
+                    double sacc = 0.0;
+                    const double* wr = W + k * (k + 1) / 2;
+                    for (int j = l16; j <= k; j += GW) sacc = fma(wr[j], ts[j], sacc);
+                    #pragma unroll
+                    for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
+                    if (l16 == 0) xl[k0 + k - r0] = sacc;
+                }
+            } else {
+                const int32_t* rp = reinterpret_cast<const int32_t*>(pc + TRSV_HDR);
+                const double* dg = reinterpret_cast<const double*>(pc + TRSV_HDR + ((4 * (nrow + 1) + 15) / 16) * 16);
+                const double* vv = dg + ((8 * nrow + 15) / 16) * 2;
+                const int32_t* cc = reinterpret_cast<const int32_t*>(reinterpret_cast<const unsigned char*>(vv) +
+                                                                     ((8 * (int64_t)ne + 15) / 16) * 16);
+                for (int k = grp; k < nrow; k += G) {
+                    double sacc = 0.0;
+                    const int p1 = rp[k + 1];
+                    for (int j = rp[k] + l16; j < p1; j += GW) sacc = fma(vv[j], xl[cc[j]], sacc);
+                    #pragma unroll
+                    for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
+                    if (l16 == 0) {
+                        const int i = k0 + k - r0;
+                        if (kind == 1) ts[k0 + k - gbase] = xl[i] - sacc;
+                        else xl[i] = recip ? (xl[i] - sacc) * dg[k] : (xl[i] - sacc) / dg[k];
+                    }
                 }
             }
             asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");   // piece solved by every consumer
@@ -735,7 +836,7 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
 
 static int trsv_ring_bytes(const TriSched& T) {
     const int64_t head = ((TRSV_QK * 12 + 16 + 127) / 128) * 128;
-    int64_t avail = (int64_t)TRSV_SMEM - head - T.max_size * 8;
+    int64_t avail = (int64_t)TRSV_SMEM - head - T.max_size * 8 - TRSV_GMAX * 8;
     avail = avail / 128 * 128;
     return (int)std::min<int64_t>(avail, 160 * 1024);
 }
@@ -743,7 +844,7 @@ static int trsv_ring_bytes(const TriSched& T) {
 template <int NC>
 static void launch_trsv_ring(Context* ctx, const TriSched& T, const double* b, double* x) {
     const int rb = trsv_ring_bytes(T);
-    const size_t sm = ((TRSV_QK * 12 + 16 + 127) / 128) * 128 + (size_t)rb + (size_t)T.max_size * 8;
+    const size_t sm = ((TRSV_QK * 12 + 16 + 127) / 128) * 128 + (size_t)rb + (size_t)T.max_size * 8 + TRSV_GMAX * 8;
     ensure_smem_attr((const void*)k_trsv_ring<NC>, ctx->device, sm);
     k_trsv_ring<NC><<<(unsigned)T.n_comp, (NC + 1) * 32, sm, ctx->stream>>>(
         T.comp_order.p, T.comp_rows.p, T.comp_piece.p, T.piece_off.p, T.piece_bytes.p, T.blob.p, T.rows.p, b, x,

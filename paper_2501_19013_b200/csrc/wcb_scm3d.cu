@@ -236,8 +236,10 @@ void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t
 // factors from shared memory): unrolled, the kernel was 83 KB of code and
 // ncu showed 11 % instruction-fetch stalls.  Epilogue, one x plane (P x P nodes per thread) at a time:
 // every load of the plane is issued before its arithmetic; 1/m comes from the
-// interior table (class 1 cells), is 0 (class 2: no owned node is a DOF,
-// nothing is stored) or is loaded (class 0, prefetched into L2 at row start).
+// interior table (class 1 cells), is 0 without a load (class 2: 1/m == 0 on
+// every owned node -- voids, and the implicit rows of an IMEX / consistent-mass
+// plan, whose slots still receive 2 psi_k - psi_{k-1}) or is loaded (class 0,
+// prefetched into L2 at row start).
 template <int P, int MODE>
 __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
     k_scm3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_p, Scm3DGeo g,
@@ -525,7 +527,7 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
                                 if (Kl + j < g.n1) a.out[base0 + r * g.pplane + b * g.prow + j] = sk * Y[r][b][j];
                         }
                     }
-                } else if (!__all_sync(FULL, cls == 2)) {
+                } else {
                     const int64_t baseL = base0 + (P - 1) * (g.pplane + g.prow) + (P - 1);
                     const bool anysrc = !(baseL < a.F.lo || base0 > a.F.hi);
                     const double* up0 = prv + (size_t)(w * P) * T::TZ + lane * P;
@@ -535,7 +537,7 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
                     for (int j = 0; j < P; ++j) kin[j] = Kl + j < g.n1;
                     #pragma unroll
                     for (int r = 0; r < P; ++r) {
-                        const bool okr = ex * P + r < g.row_hi && cls != 2;
+                        const bool okr = ex * P + r < g.row_hi;
                         const double* pl = ring + (size_t)((t * P + r) % S) * T::SLOT + u0;
                         const int64_t baser = base0 + r * g.pplane;
                         #pragma unroll
@@ -616,45 +618,68 @@ __global__ void __launch_bounds__(256) k_scm3d_zline(Scm3DGeo g, Mats2<P> mt, co
     zl[t] = make_double2(zm, zk);
 }
 
+// four threads per node, one per adjacent cell (ex, ey, n_e-1); lane 0 of the
+// quad adds the contributions in the fixed order (ex-1, ey-1), (ex-1, ey),
+// (ex, ey-1), (ex, ey) and runs the epilogue
 template <int P, int MODE>
 __global__ void __launch_bounds__(128) k_scm3d_zcol(Scm3DGeo g, Mats2<P> mt, double sk, const double2* __restrict__ zl,
                                                    StepArgs a) {
     constexpr int N = P + 1;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = t4 >> 2;
+    const int q4 = (int)(t4 & 3);
     const int64_t n_pl = g.row_hi - g.row_lo;
-    unsigned long long amp = 0ULL;
-    if (t < n_pl * g.n1) {
-        const int64_t I = g.row_lo + t / g.n1, J = t % g.n1, K = g.n1 - 1;
-        const int64_t s_ = g.n_e + 2;
-        double acc = 0.0;
-        for (int dx = 1; dx >= 0; --dx) {
-            const int64_t ex = I / P - dx;
-            const int ia = (int)(I - ex * P);
-            if (ex < 0 || ex >= g.n_ex || ia > P) continue;
-            for (int dy = 1; dy >= 0; --dy) {
-                const int64_t ey = J / P - dy;
-                const int ib = (int)(J - ey * P);
-                if (ey < 0 || ey >= g.n_e || ib > P) continue;
-                const int64_t ez = g.n_e - 1;
-                const uint8_t code = g.mask[((ex + 1) * s_ + (ey + 1)) * s_ + ez + 1] & 3;
-                if (code == 1) {
-                    double s = 0.0;
+    const bool node = t < n_pl * g.n1;
+    const int64_t I = g.row_lo + (node ? t / g.n1 : 0), J = node ? t % g.n1 : 0, K = g.n1 - 1;
+    const int64_t s_ = g.n_e + 2;
+    double s = 0.0;
+    bool has = false;
+    if (node) {
+        const int dx = 1 - (q4 >> 1), dy = 1 - (q4 & 1);
+        const int64_t ex = I / P - dx, ey = J / P - dy;
+        const int ia = (int)(I - ex * P), ib = (int)(J - ey * P);
+        if (ex >= 0 && ex < g.n_ex && ia <= P && ey >= 0 && ey < g.n_e && ib <= P) {
+            const int64_t ez = g.n_e - 1;
+            const uint8_t code = g.mask[((ex + 1) * s_ + (ey + 1)) * s_ + ez + 1] & 3;
+            if (code == 1) {
+                has = true;
+                double2 z[N][N];
+                #pragma unroll
+                for (int q = 0; q < N; ++q)
                     #pragma unroll
-                    for (int q = 0; q < N; ++q)
-                        #pragma unroll
-                        for (int r = 0; r < N; ++r) {
-                            const double2 z = zl[(ex * P + q) * g.n1 + ey * P + r];
-                            const double mq = mt.m[orb(P, ia, q)], kq = mt.k[orb(P, ia, q)];
-                            const double mr = mt.m[orb(P, ib, r)], kr = mt.k[orb(P, ib, r)];
-                            s = fma(kq * mr + mq * kr, z.x, fma(mq * mr, z.y, s));
-                        }
-                    acc += s;
-                } else if (code == 2) {
-                    const int32_t id = g.cut_id[(ex * g.n_e + ey) * g.n_e + ez];
-                    acc += g.cut_out[(int64_t)id * N * N * N + (ia * N + ib) * N + P];
+                    for (int r = 0; r < N; ++r) z[q][r] = zl[(ex * P + q) * g.n1 + ey * P + r];
+                double mq[N], kq[N], mr[N], kr[N];
+                #pragma unroll
+                for (int q = 0; q < N; ++q) {   // ia, ib are runtime: select the factor rows
+                    mq[q] = kq[q] = mr[q] = kr[q] = 0.0;
+                    #pragma unroll
+                    for (int i = 0; i < N; ++i) {
+                        if (i == ia) { mq[q] = mt.m[orb(P, i, q)]; kq[q] = mt.k[orb(P, i, q)]; }
+                        if (i == ib) { mr[q] = mt.m[orb(P, i, q)]; kr[q] = mt.k[orb(P, i, q)]; }
+                    }
                 }
+                #pragma unroll
+                for (int q = 0; q < N; ++q)
+                    #pragma unroll
+                    for (int r = 0; r < N; ++r)
+                        s = fma(kq[q] * mr[r] + mq[q] * kr[r], z[q][r].x, fma(mq[q] * mr[r], z[q][r].y, s));
+            } else if (code == 2) {
+                has = true;
+                const int32_t id = g.cut_id[(ex * g.n_e + ey) * g.n_e + ez];
+                s = g.cut_out[(int64_t)id * N * N * N + (ia * N + ib) * N + P];
             }
         }
+    }
+    double acc = 0.0;
+    const int qb = (threadIdx.x & 31) & ~3;
+    #pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+        const double v = __shfl_sync(0xffffffffu, s, qb + qq);
+        const bool h = __shfl_sync(0xffffffffu, has ? 1 : 0, qb + qq) != 0;
+        if (h) acc += v;
+    }
+    unsigned long long amp = 0ULL;
+    if (node && q4 == 0) {
         const int64_t base = (I + P) * g.pplane + (J + P) * g.prow + K + PADJ;
         if constexpr (MODE == MODE_APPLY) {
             a.out[base] = sk * acc;
@@ -670,8 +695,8 @@ __global__ void __launch_bounds__(128) k_scm3d_zcol(Scm3DGeo g, Mats2<P> mt, dou
 }
 
 // 1/m class of every local cell c: 1 when every owned node carries the
-// interior table's 1/m (bitwise), 2 when none of them is a DOF (1/m == +0
-// everywhere: the step neither loads 1/m nor stores there), else 0.  The
+// interior table's 1/m (bitwise), 2 when 1/m == +0 on all of them (the step
+// does not load 1/m there), else 0.  The
 // class goes into bits 2-3 of the cell's code byte (cinfo = mask | cls << 2).
 template <int P>
 __global__ void k_clean3d(Scm3DGeo g, MinvTab<P> tab, const double* __restrict__ minv, uint8_t* clean,
@@ -735,7 +760,7 @@ void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map
         const int64_t nl = (g.n_ex * P + 1) * g.n1;
         k_scm3d_zline<P><<<(unsigned)ceil_div(nl, 256), 256, 0, ctx->stream>>>(g, mt, a0.cur, g.zline);
         const int64_t nn = (g.row_hi - g.row_lo) * g.n1;
-        k_scm3d_zcol<P, MODE><<<(unsigned)ceil_div(nn, 128), 128, 0, ctx->stream>>>(g, mt, sk, g.zline, a0);
+        k_scm3d_zcol<P, MODE><<<(unsigned)ceil_div(4 * nn, 128), 128, 0, ctx->stream>>>(g, mt, sk, g.zline, a0);
         ctx->launches += 2;
     }
 }
