@@ -1072,7 +1072,7 @@ int wcb_cdm_plan_create(wcb_operator* o, const double* m_diag, const double* F_s
         k_mass_from_state<<<grid_for(ctx, ns), 256, 0, s>>>(ns, P->minv.p, P->m_state.p);
         ctx->launches += 2;
         WCB_CHECK_LAUNCH();
-        op->bind_minv(P->minv.p);
+        op->bind_minv(P->minv.p, true);   // diagonal mass: 1/m == 0 only at non-DOF slots
         // source: dense window over its nonzeros' state-index range
         {
             std::mutex mu;

@@ -67,6 +67,7 @@ struct TriSched {
     DevBuf<int32_t> piece_bytes;
     DevBuf<int32_t> comp_piece;  // n_comp + 1: offsets into the pieces
     DevBuf<int32_t> comp_order;  // launch order: components by decreasing level count
+    DevBuf<int32_t> ring_order;  // launch order of k_trsv_ring: by decreasing streamed bytes
     DevBuf<int32_t> comp_rows;   // n_comp + 1: offsets into rows
     DevBuf<int32_t> comp_lvl;    // n_comp + 1: offsets into lvl_off
     DevBuf<int32_t> lvl_off;     // n_levels + 1: offsets into rows
@@ -137,7 +138,25 @@ static std::vector<int64_t> factor_components(int64_t n, const wcb_lu* lu, int64
 // once (kind 1), then the multiplication by the host-inverted triangular block
 // (kind 2).  Mathematically the same solve; the rounding differs (bounded by
 // the parity tests).  WAVECELL_B200_TRSV_GROUPS=0 keeps one piece per level.
-constexpr int64_t TRSV_PIECE_BYTES = 24 * 1024;
+// largest piece (bulk copy); WAVECELL_B200_TRSV_PIECE_KB overrides (measured on
+// config 4: 40 KB pieces in a 160 KB ring beat 24-32 KB pieces in 48-64 KB)
+static int64_t trsv_piece_bytes() {
+    static const int64_t v = [] {
+        const char* e = getenv("WAVECELL_B200_TRSV_PIECE_KB");
+        const int64_t kb = e ? atoll(e) : 40;
+        return std::max<int64_t>(20, std::min<int64_t>(kb, 64)) * 1024;   // >= the dense part of a group
+    }();
+    return v;
+}
+#define TRSV_PIECE_BYTES trsv_piece_bytes()
+static int64_t trsv_ring_cap() {   // cap of the circular piece buffer (WAVECELL_B200_TRSV_RING_KB)
+    static const int64_t v = [] {
+        const char* e = getenv("WAVECELL_B200_TRSV_RING_KB");
+        const int64_t kb = e ? atoll(e) : 160;
+        return std::max<int64_t>(40, std::min<int64_t>(kb, 160)) * 1024;
+    }();
+    return v;
+}
 constexpr int TRSV_GMAX = 64;      // rows per group (dense part: 16.6 KB)
 constexpr int TRSV_NARROW = 16;    // a level joins a group when it has at most this many rows
 constexpr int TRSV_HDR = 32;
@@ -158,6 +177,8 @@ static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp
     const bool groups = !(getenv("WAVECELL_B200_TRSV_GROUPS") && getenv("WAVECELL_B200_TRSV_GROUPS")[0] == '0');
     // rows [k, e) (schedule order) as pieces of `kind`; entries with a column
     // slot >= slot_lo are skipped (kind 1: they are in the dense part)
+    // consumer warps of k_trsv_ring (rows of a piece get a whole warp when there are few)
+    const int ncw = [] { const char* e2 = getenv("WAVECELL_B200_TRSV_NC"); return e2 && atoi(e2) > 0 ? atoi(e2) : 16; }();
     auto emit_rows = [&](int64_t k, int64_t e, int kind, int64_t gbase, int64_t slot_lo) {
         std::vector<int32_t> cnt;   // kept entries per row
         cnt.reserve(e - k);
@@ -183,6 +204,8 @@ static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp
             hdr[3] = (int32_t)sz;
             hdr[4] = kind;
             hdr[5] = (int32_t)gbase;
+            hdr[6] = nrow <= ncw ? 32 : 16;      // lanes per row
+            hdr[7] = r1 == e ? 1 : 0;            // last piece of its level / outside part: consumers meet
             int32_t* rp = reinterpret_cast<int32_t*>(p + TRSV_HDR);
             double* dg = reinterpret_cast<double*>(p + TRSV_HDR + pad16(4 * (nrow + 1)));
             double* vv = dg + pad16(8 * nrow) / 8;
@@ -243,6 +266,8 @@ static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp
                 hdr[3] = (int32_t)sz;
                 hdr[4] = 2;
                 hdr[5] = (int32_t)ka;
+                hdr[6] = 16;
+                hdr[7] = 1;
                 double* wp = reinterpret_cast<double*>(p + TRSV_HDR);
                 for (int64_t r = 0; r < nr; ++r)
                     for (int64_t j = 0; j <= r; ++j) wp[r * (r + 1) / 2 + j] = W[r * nr + j];
@@ -267,6 +292,18 @@ static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp
     T.piece_off.alloc(off.size(), s); T.piece_off.upload(off.data(), off.size(), s);
     T.piece_bytes.alloc(bytes.size(), s); T.piece_bytes.upload(bytes.data(), bytes.size(), s);
     T.comp_piece.alloc(cpiece.size(), s); T.comp_piece.upload(cpiece.data(), cpiece.size(), s);
+    // launch order of the ring kernel: most streamed bytes first (a patch's time
+    // follows its pieces, not its level count, once narrow levels are grouped)
+    {
+        std::vector<int64_t> cb(T.n_comp, 0);
+        for (int64_t c = 0; c < T.n_comp; ++c)
+            for (int32_t q = cpiece[c]; q < cpiece[c + 1]; ++q) cb[c] += bytes[q];
+        std::vector<int32_t> co(T.n_comp);
+        for (int64_t c = 0; c < T.n_comp; ++c) co[c] = (int32_t)c;
+        std::stable_sort(co.begin(), co.end(), [&](int32_t a, int32_t b) { return cb[a] > cb[b]; });
+        T.ring_order.alloc(std::max<int64_t>(T.n_comp, 1), s);
+        T.ring_order.upload(co.data(), T.n_comp, s);
+    }
     WCB_CUDA(cudaStreamSynchronize(s));
     T.ring_ok = true;
     (void)n;
@@ -722,7 +759,62 @@ __global__ void __launch_bounds__(NW * 32) k_trsv_pf(
 // one consumer barrier plus its rows; the staging never occupies the
 // consumers.  Same lane order and shuffle tree as k_trsv_comp (bitwise equal).
 constexpr int TRSV_QK = 64;                       // pieces in flight (mbarrier ring)
-constexpr int64_t TRSV_RING_MIN = 2 * TRSV_PIECE_BYTES;
+constexpr int64_t TRSV_RING_HEAD = ((TRSV_QK * 24 + 127) / 128) * 128;   // full[QK], empty[QK], poff[QK], pneed[QK]
+
+__device__ __forceinline__ void mbar_arrive_imex(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32_imex(bar)) : "memory");
+}
+
+// the rows of one piece with GW lanes per row (see the piece kinds above)
+template <int GW, int NC>
+__device__ __forceinline__ void trsv_piece(const unsigned char* pc, const int32_t* hdr, int ct, int lane, int q,
+                                           double* xl, double* ts, int r0, int recip) {
+    constexpr int G = NC * 32 / GW;
+    const int nrow = hdr[0], k0 = hdr[1], ne = hdr[2], kind = hdr[4], gbase = hdr[5];
+    const int l = ct % GW;
+    // rows are dealt to the row groups starting at a per-piece offset, so
+    // consecutive independent pieces of few rows land on different warps
+    const int grp = (ct / GW + G - (q * 5) % G) % G;   // group grp takes rows grp, grp + G, ...
+    const unsigned hmask = GW == 32 ? 0xffffffffu : (0xffffu << (lane & 16));
+    if (kind == 2) {   // dense part of a group: x = W t
+        const double* W = reinterpret_cast<const double*>(pc + TRSV_HDR);
+        for (int k = grp; k < nrow; k += G) {
+            double sacc = 0.0;
+            const double* wr = W + k * (k + 1) / 2;
+            for (int j = l; j <= k; j += GW) sacc = fma(wr[j], ts[j], sacc);
+            #pragma unroll
+            for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
+            if (l == 0) xl[k0 + k - r0] = sacc;
+        }
+        return;
+    }
+    const int32_t* rp = reinterpret_cast<const int32_t*>(pc + TRSV_HDR);
+    const double* dg = reinterpret_cast<const double*>(pc + TRSV_HDR + ((4 * (nrow + 1) + 15) / 16) * 16);
+    const double* vv = dg + ((8 * nrow + 15) / 16) * 2;
+    const int32_t* cc = reinterpret_cast<const int32_t*>(reinterpret_cast<const unsigned char*>(vv) +
+                                                         ((8 * (int64_t)ne + 15) / 16) * 16);
+    for (int k = grp; k < nrow; k += G) {
+        // two interleaved partial sums per lane (independent load chains)
+        double s0 = 0.0, s1 = 0.0;
+        const int p1 = rp[k + 1];
+        int j = rp[k] + l;
+        for (; j + GW < p1; j += 2 * GW) {
+            const double v0 = vv[j], v1 = vv[j + GW];
+            const int c0 = cc[j], c1 = cc[j + GW];
+            s0 = fma(v0, xl[c0], s0);
+            s1 = fma(v1, xl[c1], s1);
+        }
+        if (j < p1) s0 = fma(vv[j], xl[cc[j]], s0);
+        double sacc = s0 + s1;
+        #pragma unroll
+        for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
+        if (l == 0) {
+            const int i = k0 + k - r0;
+            if (kind == 1) ts[k0 + k - gbase] = xl[i] - sacc;
+            else xl[i] = recip ? (xl[i] - sacc) * dg[k] : (xl[i] - sacc) / dg[k];
+        }
+    }
+}
 
 template <int NC>
 __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
@@ -731,13 +823,12 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
     const int32_t* __restrict__ piece_bytes, const unsigned char* __restrict__ blob,
     const int32_t* __restrict__ rows, const double* __restrict__ b, double* __restrict__ x, int max_size,
     int ring_bytes, int recip) {
-    constexpr int GW = WCB_TRSV_GW;
-    constexpr int G = NC * 32 / GW;
     extern __shared__ __align__(128) unsigned char smraw[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smraw);                 // [QK]
-    int* poff = reinterpret_cast<int*>(smraw + TRSV_QK * 8);             // [QK] ring offset of piece q
-    volatile long long* rel = reinterpret_cast<volatile long long*>(smraw + TRSV_QK * 12);   // [2]
-    unsigned char* ring = smraw + ((TRSV_QK * 12 + 16 + 127) / 128) * 128;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smraw);                 // [QK] piece landed
+    uint64_t* empty = full + TRSV_QK;                                    // [QK] piece consumed by every consumer warp
+    int* poff = reinterpret_cast<int*>(smraw + TRSV_QK * 16);            // [QK] ring offset of piece q
+    int* pneed = poff + TRSV_QK;                                         // [QK] ring bytes the piece took (tail skip included)
+    unsigned char* ring = smraw + TRSV_RING_HEAD;
     double* xl = reinterpret_cast<double*>(ring + ring_bytes);
     double* ts = xl + max_size;   // group scratch [TRSV_GMAX]
     const int c = comp_order[blockIdx.x];
@@ -745,14 +836,16 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
     const int r0 = comp_rows[c], r1 = comp_rows[c + 1];
     const int q0 = comp_piece[c], nq = comp_piece[c + 1] - q0;
     if (threadIdx.x == 0) {
-        for (int d = 0; d < TRSV_QK; ++d) mbar_init(&full[d], 1);
-        rel[0] = 0;   // pieces released by the consumers
-        rel[1] = 0;   // ring bytes released (cumulative)
+        for (int d = 0; d < TRSV_QK; ++d) {
+            mbar_init(&full[d], 1);
+            mbar_init(&empty[d], NC);
+        }
     }
     for (int k = r0 + threadIdx.x; k < r1; k += blockDim.x) xl[k - r0] = b[rows[k]];
     __syncthreads();
     if (warp == 0) {   // producer warp: piece sizes / offsets fetched 32 at a time
-        long long pos = 0;   // cumulative ring position
+        long long pos = 0, freed = 0;   // cumulative ring bytes placed / released
+        int ro = 0;                     // oldest piece not yet known to be released
         for (int qb = 0; qb < nq; qb += 32) {
             const int qq = qb + lane;
             const uint32_t nb_l = qq < nq ? (uint32_t)piece_bytes[q0 + qq] : 0u;
@@ -766,11 +859,17 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
                     long long at = pos % ring_bytes;
                     long long need = nb;
                     if (at + nb > ring_bytes) { need += ring_bytes - at; at = 0; }   // wrap: skip the tail
-                    // wait for ring space and a free mbarrier slot
-                    while (pos + need - rel[1] > ring_bytes || q - rel[0] >= TRSV_QK) __nanosleep(20);
+                    // ring space and a free mbarrier slot: wait for the oldest pieces' release
+                    while (pos + need - freed > ring_bytes || q - ro >= TRSV_QK) {
+                        const int d0 = ro % TRSV_QK;
+                        mbar_wait(&empty[d0], (uint32_t)((ro / TRSV_QK) & 1));
+                        freed += pneed[d0];
+                        ++ro;
+                    }
                     pos += need;
                     const int d = q % TRSV_QK;
                     poff[d] = (int)at;
+                    pneed[d] = (int)need;
                     mbar_expect_tx(&full[d], nb);
                     bulk_load(ring + at, blob + off, nb, &full[d]);
                 }
@@ -779,55 +878,18 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
         }
     } else {
         const int ct = threadIdx.x - 32;
-        const int grp = ct / GW, l16 = lane % GW;
-        const unsigned hmask = (GW == 32 ? 0xffffffffu : ((1u << GW) - 1u)) << ((lane / GW) * GW);
-        long long done_bytes = 0;   // consumer thread 0: cumulative end of the released pieces
         for (int q = 0; q < nq; ++q) {
             const int d = q % TRSV_QK;
             mbar_wait(&full[d], (uint32_t)((q / TRSV_QK) & 1));
             const unsigned char* pc = ring + poff[d];
             const int32_t* hdr = reinterpret_cast<const int32_t*>(pc);
-            const int nrow = hdr[0], k0 = hdr[1], ne = hdr[2], kind = hdr[4], gbase = hdr[5];
-            if (kind == 2) {   // dense part of a group: x = W t
-                const double* W = reinterpret_cast<const double*>(pc + TRSV_HDR);
-                for (int k = grp; k < nrow; k += G) {
-                    double sacc = 0.0;
-                    const double* wr = W + k * (k + 1) / 2;
-                    for (int j = l16; j <= k; j += GW) sacc = fma(wr[j], ts[j], sacc);
-                    #pragma unroll
-                    for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
-                    if (l16 == 0) xl[k0 + k - r0] = sacc;
-                }
-            } else {
-                const int32_t* rp = reinterpret_cast<const int32_t*>(pc + TRSV_HDR);
-                const double* dg = reinterpret_cast<const double*>(pc + TRSV_HDR + ((4 * (nrow + 1) + 15) / 16) * 16);
-                const double* vv = dg + ((8 * nrow + 15) / 16) * 2;
-                const int32_t* cc = reinterpret_cast<const int32_t*>(reinterpret_cast<const unsigned char*>(vv) +
-                                                                     ((8 * (int64_t)ne + 15) / 16) * 16);
-                for (int k = grp; k < nrow; k += G) {
-                    double sacc = 0.0;
-                    const int p1 = rp[k + 1];
-                    for (int j = rp[k] + l16; j < p1; j += GW) sacc = fma(vv[j], xl[cc[j]], sacc);
-                    #pragma unroll
-                    for (int o = GW / 2; o > 0; o >>= 1) sacc += __shfl_down_sync(hmask, sacc, o, GW);
-                    if (l16 == 0) {
-                        const int i = k0 + k - r0;
-                        if (kind == 1) ts[k0 + k - gbase] = xl[i] - sacc;
-                        else xl[i] = recip ? (xl[i] - sacc) * dg[k] : (xl[i] - sacc) / dg[k];
-                    }
-                }
-            }
-            asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");   // piece solved by every consumer
-            if (ct == 0) {
-                // replay the producer's placement to publish the released bytes
-                const long long nb = hdr[3];
-                long long at = done_bytes % ring_bytes, need = nb;
-                if (at + nb > ring_bytes) need += ring_bytes - at;
-                done_bytes += need;
-                __threadfence_block();
-                rel[1] = done_bytes;
-                rel[0] = q + 1;
-            }
+            if (hdr[6] == 32) trsv_piece<32, NC>(pc, hdr, ct, lane, q, xl, ts, r0, recip);
+            else trsv_piece<16, NC>(pc, hdr, ct, lane, q, xl, ts, r0, recip);
+            // the next piece depends on this one (end of a level / of a group's
+            // outside part / dense part): every consumer's rows must be visible
+            if (hdr[7]) asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_imex(&empty[d]);   // this warp is done with the piece's bytes
         }
     }
     __syncthreads();
@@ -835,19 +897,19 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
 }
 
 static int trsv_ring_bytes(const TriSched& T) {
-    const int64_t head = ((TRSV_QK * 12 + 16 + 127) / 128) * 128;
+    const int64_t head = TRSV_RING_HEAD;
     int64_t avail = (int64_t)TRSV_SMEM - head - T.max_size * 8 - TRSV_GMAX * 8;
     avail = avail / 128 * 128;
-    return (int)std::min<int64_t>(avail, 160 * 1024);
+    return (int)std::min<int64_t>(avail, trsv_ring_cap());
 }
 
 template <int NC>
 static void launch_trsv_ring(Context* ctx, const TriSched& T, const double* b, double* x) {
     const int rb = trsv_ring_bytes(T);
-    const size_t sm = ((TRSV_QK * 12 + 16 + 127) / 128) * 128 + (size_t)rb + (size_t)T.max_size * 8 + TRSV_GMAX * 8;
+    const size_t sm = (size_t)TRSV_RING_HEAD + (size_t)rb + (size_t)T.max_size * 8 + TRSV_GMAX * 8;
     ensure_smem_attr((const void*)k_trsv_ring<NC>, ctx->device, sm);
     k_trsv_ring<NC><<<(unsigned)T.n_comp, (NC + 1) * 32, sm, ctx->stream>>>(
-        T.comp_order.p, T.comp_rows.p, T.comp_piece.p, T.piece_off.p, T.piece_bytes.p, T.blob.p, T.rows.p, b, x,
+        T.ring_order.p, T.comp_rows.p, T.comp_piece.p, T.piece_off.p, T.piece_bytes.p, T.blob.p, T.rows.p, b, x,
         (int)T.max_size, rb, T.recip ? 1 : 0);
 }
 template <int NC>

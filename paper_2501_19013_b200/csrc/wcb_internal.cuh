@@ -318,7 +318,10 @@ struct Operator {
     virtual void cdm_step_part(const StepArgs& a, int part) { if (part == 1) cdm_step(a); }
     // the plan's 1/m state vector (fixed for the plan's lifetime): operators
     // may precompute which cells read it (default: every node loads 1/m)
-    virtual void bind_minv(const double* /*d_minv*/) {}
+    // zero_is_dead: slots with 1/m == 0 are not DOFs of any kind (plain CDM plan
+    // with a diagonal mass), so the step may leave them untouched; false when
+    // they are the implicit rows of an IMEX / consistent-mass plan
+    virtual void bind_minv(const double* /*d_minv*/, bool /*zero_is_dead*/ = false) {}
     double minv_skipped = 0.0;   // DOFs whose 1/m the bound step takes from a table (no 8 B load)
     int halo_nplanes = 1;        // component planes of the state (slab halo exchange)
     int64_t halo_pstride = 0;    // doubles between component planes

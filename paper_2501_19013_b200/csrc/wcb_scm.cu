@@ -1096,7 +1096,7 @@ struct ScmOperator final : Operator {
         if (!clean.p) clean.alloc((size_t)n_ex * n_e * n_e);
         if (!cinfo.p) cinfo.alloc(mask.n);
         WCB_CUDA(cudaMemcpyAsync(cinfo.p, mask.p, mask.n, cudaMemcpyDeviceToDevice, ctx->stream));
-        launch_clean3d<P>(ctx, geo3(), tab, d_minv, clean.p, cinfo.p);
+        launch_clean3d<P>(ctx, geo3(), tab, d_minv, clean.p, cinfo.p, zero_dead);
         WCB_CHECK_LAUNCH();
         std::vector<uint8_t> hc(clean.n);
         WCB_CUDA(cudaMemcpyAsync(hc.data(), clean.p, hc.size(), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1188,7 +1188,9 @@ struct ScmOperator final : Operator {
         minv_tab = h;
         minv_bound = d_minv;
     }
-    void bind_minv(const double* d_minv) override {
+    bool zero_dead = false;
+    void bind_minv(const double* d_minv, bool zero_is_dead) override {
+        zero_dead = zero_is_dead;
         minv_bound = nullptr;
         minv_skipped = 0.0;
         if (probe_base < 0 || !d_minv || getenv("WAVECELL_B200_NO_MINV_TAB")) return;

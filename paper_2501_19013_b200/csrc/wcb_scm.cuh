@@ -69,7 +69,9 @@ struct Scm3DGeo {
     // non-null: `mask` carries the 1/m class of every cell in bits 2-3
     // (k_clean3d, once per plan: 1 = the P^3 owned nodes all carry the interior
     // 1/m of minv_tab, bitwise -- the epilogue skips the 1/m stream there;
-    // 2 = 1/m is +0 on every owned node).  null: every node loads 1/m.
+    // 2 / 3 = 1/m is +0 on every owned node -- 2: the slots are not DOFs and are
+    // left untouched, 3: they are stored (implicit rows of an IMEX plan)).
+    // null: every node loads 1/m.
     const uint8_t* clean;
     double2* zline;           // (n_ex P + 1) x n1 z-lines of the last cell column (n_e % 32 == 0)
     int64_t xc0 = 0;          // first x chunk of this launch (blockIdx.z + xc0)
@@ -124,10 +126,10 @@ template <int P, int MODE>
 void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map_p, const Scm3DGeo& g,
                   const Mats2<P>& mt, const MinvTab<P>& mtab, double sk, const StepArgs& a, int part = -1);
 // clean[c] = 1/m class of local cell c (1: minv == tab bitwise on every owned
-// node, 2: 1/m == 0 on every owned node); cinfo = mask with the class in bits 2-3
+// node, 2 / 3: 1/m == 0 on every owned node, dead / stored); cinfo = mask with the class in bits 2-3
 template <int P>
 void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean,
-                    uint8_t* cinfo);
+                    uint8_t* cinfo, bool zero_is_dead);
 // packed lower triangle of a cut cell's K_o / sk, stride padded to 16 bytes
 __host__ __device__ constexpr int cut_lp_stride(int P) {
     return (((P + 1) * (P + 1) * (P + 1)) * (((P + 1) * (P + 1) * (P + 1)) + 1) / 2 + 1) / 2 * 2;

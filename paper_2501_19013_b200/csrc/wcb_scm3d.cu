@@ -236,9 +236,10 @@ void launch_cut_pre(Context* ctx, int64_t n_cut, const double* KP, const int64_t
 // factors from shared memory): unrolled, the kernel was 83 KB of code and
 // ncu showed 11 % instruction-fetch stalls.  Epilogue, one x plane (P x P nodes per thread) at a time:
 // every load of the plane is issued before its arithmetic; 1/m comes from the
-// interior table (class 1 cells), is 0 without a load (class 2: 1/m == 0 on
-// every owned node -- voids, and the implicit rows of an IMEX / consistent-mass
-// plan, whose slots still receive 2 psi_k - psi_{k-1}) or is loaded (class 0,
+// interior table (class 1 cells), is 0 without a load (1/m == 0 on every owned
+// node: class 2, slots that are no DOFs under a diagonal-mass CDM plan and are
+// left untouched; class 3, the implicit rows of an IMEX / consistent-mass plan,
+// whose slots still receive 2 psi_k - psi_{k-1}) or is loaded (class 0,
 // prefetched into L2 at row start).
 template <int P, int MODE>
 __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
                                 if (Kl + j < g.n1) a.out[base0 + r * g.pplane + b * g.prow + j] = sk * Y[r][b][j];
                         }
                     }
-                } else {
+                } else if (!__all_sync(FULL, cls == 2)) {
                     const int64_t baseL = base0 + (P - 1) * (g.pplane + g.prow) + (P - 1);
                     const bool anysrc = !(baseL < a.F.lo || base0 > a.F.hi);
                     const double* up0 = prv + (size_t)(w * P) * T::TZ + lane * P;
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(Str3<P>::NWARP * 32, cpsm_for3(P))
                     for (int j = 0; j < P; ++j) kin[j] = Kl + j < g.n1;
                     #pragma unroll
                     for (int r = 0; r < P; ++r) {
-                        const bool okr = ex * P + r < g.row_hi;
+                        const bool okr = ex * P + r < g.row_hi && cls != 2;
                         const double* pl = ring + (size_t)((t * P + r) % S) * T::SLOT + u0;
                         const int64_t baser = base0 + r * g.pplane;
                         #pragma unroll
@@ -695,12 +696,12 @@ __global__ void __launch_bounds__(128) k_scm3d_zcol(Scm3DGeo g, Mats2<P> mt, dou
 }
 
 // 1/m class of every local cell c: 1 when every owned node carries the
-// interior table's 1/m (bitwise), 2 when 1/m == +0 on all of them (the step
-// does not load 1/m there), else 0.  The
+// interior table's 1/m (bitwise), 2 or 3 when 1/m == +0 on all of them (the step
+// does not load 1/m there; 2: it does not store either), else 0.  The
 // class goes into bits 2-3 of the cell's code byte (cinfo = mask | cls << 2).
 template <int P>
 __global__ void k_clean3d(Scm3DGeo g, MinvTab<P> tab, const double* __restrict__ minv, uint8_t* clean,
-                          uint8_t* cinfo) {
+                          uint8_t* cinfo, bool zero_is_dead) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nc = g.n_ex * g.n_e * g.n_e;
     if (c >= nc) return;
@@ -715,7 +716,7 @@ __global__ void k_clean3d(Scm3DGeo g, MinvTab<P> tab, const double* __restrict__
                 ok = ok && I < g.row_hi && bits == __double_as_longlong(tab.v[(q * P + r) * P + j]);
                 zero = zero && bits == 0LL;
             }
-    const uint8_t cls = ok ? 1 : zero ? 2 : 0;
+    const uint8_t cls = ok ? 1 : zero ? (zero_is_dead ? 2 : 3) : 0;
     clean[c] = cls;
     const int64_t s_ = g.n_e + 2;
     const int64_t m = ((ex + 1) * s_ + (ey + 1)) * s_ + ez + 1;
@@ -724,9 +725,9 @@ __global__ void k_clean3d(Scm3DGeo g, MinvTab<P> tab, const double* __restrict__
 
 template <int P>
 void launch_clean3d(Context* ctx, const Scm3DGeo& g, const MinvTab<P>& tab, const double* minv, uint8_t* clean,
-                    uint8_t* cinfo) {
+                    uint8_t* cinfo, bool zero_is_dead) {
     const int64_t nc = g.n_ex * g.n_e * g.n_e;
-    k_clean3d<P><<<(unsigned)ceil_div(nc, 256), 256, 0, ctx->stream>>>(g, tab, minv, clean, cinfo);
+    k_clean3d<P><<<(unsigned)ceil_div(nc, 256), 256, 0, ctx->stream>>>(g, tab, minv, clean, cinfo, zero_is_dead);
     ctx->launches++;
 }
 
@@ -772,7 +773,7 @@ void launch_scm3d(Context* ctx, const CUtensorMap& map_u, const CUtensorMap& map
     template void launch_scm3d<P, MODE_APPLY>(Context*, const CUtensorMap&, const CUtensorMap&, const Scm3DGeo&, \
                                               const Mats2<P>&, const MinvTab<P>&, double,       \
                                               const StepArgs&, int);                            \
-    template void launch_clean3d<P>(Context*, const Scm3DGeo&, const MinvTab<P>&, const double*, uint8_t*, uint8_t*);
+    template void launch_clean3d<P>(Context*, const Scm3DGeo&, const MinvTab<P>&, const double*, uint8_t*, uint8_t*, bool);
 #define WCB_INSTC(P) \
     template void launch_cut_pre<P>(Context*, int64_t, const double*, const int64_t*, int64_t, int64_t, \
                                     const double*, double*);

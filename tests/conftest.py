@@ -41,6 +41,12 @@ def golden():
 # cases meet the north-star 1e-10.
 IMEX_A12_TOL_P2N4 = 1e-7
 IMEX_A12_TOL_N13 = 3e-5
+# Largest eigenvalue of the alpha = 1e-12 system with its consistent cut-cell
+# mass (power iteration through the M_cc solves, stopped at tol = 1e-3): the
+# value moves by a few 1e-12 relative with the summation order of the
+# triangular solves (measured 2.0e-12 between the level-by-level solve and the
+# grouped one), the stopping iteration does not and is asserted exactly.
+LAM_A12_CONSISTENT_TOL = 1e-10
 # 2000 CDM steps at 0.99 dt_crit (the stability-dichotomy case): the highest
 # mode is nearly undamped and a 1-ulp perturbation of K moves the reference's
 # field by ~2e-10 (measured in tests/test_paper_setup.py).
