@@ -191,3 +191,26 @@ def test_2d_streaming_kernel_bitwise_vs_tile_kernel(p, n_e, monkeypatch):
     for y, psi in outs[1:]:
         assert np.array_equal(y, outs[0][0])
         assert np.array_equal(psi, outs[0][1])
+
+
+def test_3d_minv_classes_bitwise(monkeypatch):
+    """The 3D step takes 1/m by cell class (interior table / +0 without a load,
+    untouched under a diagonal-mass plan / loaded).  Fields are bitwise those
+    of the run that loads 1/m everywhere (WAVECELL_B200_NO_MINV_TAB)."""
+    from paper_2501_19013_b200.setup.configs import build_scm as _b
+    from paper_2501_19013_b200.setup.configs import CONFIGS as _C
+    from dataclasses import replace
+    cfg = replace(_C["config5"], p=3, n_e=36, n_random=6, r_range=(0.03, 0.08), name="c5c")
+    prob = _b(cfg)
+    M = prob.mass_matrix()
+    f = lambda t: ricker(t, 10.0)
+    outs = []
+    for flag in (None, "1"):
+        if flag is None:
+            monkeypatch.delenv("WAVECELL_B200_NO_MINV_TAB", raising=False)
+        else:
+            monkeypatch.setenv("WAVECELL_B200_NO_MINV_TAB", flag)
+        op = prob.device_operator()
+        outs.append(cdm_run(M, op, prob.F_s, f, 1e-3 / 36, 80).psi)
+    assert np.abs(outs[0]).max() > 0
+    assert np.array_equal(outs[0], outs[1])
