@@ -351,17 +351,8 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
         const double chiL = mL == 1 ? 1.0 : 0.0;
         const double* rows = us + (size_t)(rbase + P) * T::UW;
 #ifndef WCB2D_NOTENSOR
-        // a warp whose 33 cells are all uncut skips the mask products (chi = 1:
-        // x * 1.0 and fma(1.0, l, w) round like x and w + l)
-        const bool uni = __all_sync(0xffffffffu, mR == 1 && mL == 1);
-        if (uni) {
-            #pragma unroll
-            for (int c = 0; c < N; ++c)
-                row_contract<P, false, false>(mc, kc, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
-        } else {
-            #pragma unroll
-            for (int c = 0; c < N; ++c) row_contract<P>(mc, kc, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
-        }
+        #pragma unroll
+        for (int c = 0; c < N; ++c) row_contract<P>(mc, kc, rows + (size_t)c * T::UW, lane, chiR, chiL, c, Y);
 #endif
         const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
         const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
