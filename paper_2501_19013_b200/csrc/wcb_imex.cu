@@ -179,6 +179,24 @@ static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp
     // slot >= slot_lo are skipped (kind 1: they are in the dense part)
     // consumer warps of k_trsv_ring (rows of a piece get a whole warp when there are few)
     const int ncw = [] { const char* e2 = getenv("WAVECELL_B200_TRSV_NC"); return e2 && atoi(e2) > 0 ? atoi(e2) : 16; }();
+    // lanes per row of a piece: fewest (passes over the row groups) x (latency
+    // of one pass), a pass costing a fixed part, the row's multiply-add steps
+    // (two per lane in flight) and the shuffle tree
+    auto lanes_for = [&](int64_t nrow, int64_t ne) {
+        const double per_row = nrow > 0 ? (double)ne / (double)nrow : 0.0;
+        int best = 16;
+        double best_cost = 1e300;
+        for (int gw : {2, 4, 8, 16, 32}) {
+            const int64_t groups = (int64_t)ncw * 32 / gw;
+            const double passes = (double)((nrow + groups - 1) / groups);
+            int lg = 0;
+            while ((1 << lg) < gw) ++lg;
+            const double iters = std::ceil(per_row / (2.0 * gw));
+            const double cost = passes * (300.0 + 80.0 * iters + 30.0 * lg);
+            if (cost < best_cost) { best_cost = cost; best = gw; }
+        }
+        return best;
+    };
     auto emit_rows = [&](int64_t k, int64_t e, int kind, int64_t gbase, int64_t slot_lo) {
         std::vector<int32_t> cnt;   // kept entries per row
         cnt.reserve(e - k);
@@ -204,7 +222,7 @@ static void pack_pieces(TriSched& T, int64_t n, const std::vector<int32_t>& comp
             hdr[3] = (int32_t)sz;
             hdr[4] = kind;
             hdr[5] = (int32_t)gbase;
-            hdr[6] = nrow <= ncw ? 32 : 16;      // lanes per row
+            hdr[6] = lanes_for(nrow, ne);        // lanes per row
             hdr[7] = r1 == e ? 1 : 0;            // last piece of its level / outside part: consumers meet
             int32_t* rp = reinterpret_cast<int32_t*>(p + TRSV_HDR);
             double* dg = reinterpret_cast<double*>(p + TRSV_HDR + pad16(4 * (nrow + 1)));
@@ -775,7 +793,7 @@ __device__ __forceinline__ void trsv_piece(const unsigned char* pc, const int32_
     // rows are dealt to the row groups starting at a per-piece offset, so
     // consecutive independent pieces of few rows land on different warps
     const int grp = (ct / GW + G - (q * 5) % G) % G;   // group grp takes rows grp, grp + G, ...
-    const unsigned hmask = GW == 32 ? 0xffffffffu : (0xffffu << (lane & 16));
+    const unsigned hmask = GW == 32 ? 0xffffffffu : (((1u << GW) - 1u) << (lane & ~(GW - 1)));
     if (kind == 2) {   // dense part of a group: x = W t
         const double* W = reinterpret_cast<const double*>(pc + TRSV_HDR);
         for (int k = grp; k < nrow; k += G) {
@@ -883,8 +901,13 @@ __global__ void __launch_bounds__((NC + 1) * 32) k_trsv_ring(
             mbar_wait(&full[d], (uint32_t)((q / TRSV_QK) & 1));
             const unsigned char* pc = ring + poff[d];
             const int32_t* hdr = reinterpret_cast<const int32_t*>(pc);
-            if (hdr[6] == 32) trsv_piece<32, NC>(pc, hdr, ct, lane, q, xl, ts, r0, recip);
-            else trsv_piece<16, NC>(pc, hdr, ct, lane, q, xl, ts, r0, recip);
+            switch (hdr[6]) {   // lanes per row, chosen per piece on the host
+                case 32: trsv_piece<32, NC>(pc, hdr, ct, lane, q, xl, ts, r0, recip); break;
+                case 8: trsv_piece<8, NC>(pc, hdr, ct, lane, q, xl, ts, r0, recip); break;
+                case 4: trsv_piece<4, NC>(pc, hdr, ct, lane, q, xl, ts, r0, recip); break;
+                case 2: trsv_piece<2, NC>(pc, hdr, ct, lane, q, xl, ts, r0, recip); break;
+                default: trsv_piece<16, NC>(pc, hdr, ct, lane, q, xl, ts, r0, recip); break;
+            }
             // the next piece depends on this one (end of a level / of a group's
             // outside part / dense part): every consumer's rows must be visible
             if (hdr[7]) asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
