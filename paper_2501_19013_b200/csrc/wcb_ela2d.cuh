@@ -259,7 +259,7 @@ __device__ __forceinline__ void ela2d_warp(const Scm2DGeo& g, const EMats<P>& mt
                                                lane, chiR, chiL, c, Y);
         const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
         const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
-        if (cl || ed) cut_cells_warp_e<P, O, T::UW, T::CO>(g, u0 + r0, u1 + r0, lane, cl, ed, cid, cidL, Y);
+        if ((cl || ed) && g.KT) cut_cells_warp_e<P, O, T::UW, T::CO>(g, u0 + r0, u1 + r0, lane, cl, ed, cid, cidL, Y);
     }
     #pragma unroll
     for (int j = 0; j < P; ++j) carry[((halo ? 0 : wi + 1) * P + j) * 32 + lane] = Y[P][j];

@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(Tile2<P>::NWARP * 32, WCB2D_MINB) k_scm2d(
         const unsigned cl = __ballot_sync(0xffffffffu, mR == 2);
         const bool ed = __shfl_sync(0xffffffffu, mL == 2, 0);
 #ifndef WCB2D_NOCUT
-        if (cl || ed) cut_cells_warp<P, T::UW, T::CO>(g, rows, ex, J0 / P, lane, cl, ed, cid, cidL, Y);
+        if ((cl || ed) && g.KT) cut_cells_warp<P, T::UW, T::CO>(g, rows, ex, J0 / P, lane, cl, ed, cid, cidL, Y);
 #endif
     }
     // row a = P of element row ex is row a = 0 of element row ex+1
@@ -747,6 +747,11 @@ struct ScmOperator final : Operator {
     int64_t n_order_sub = 0;
     bool sub_ready = false, sub_active = false;
     std::vector<int32_t> order_h;            // host copy of the dispatch order
+    std::vector<uint8_t> mask_h;             // 2D: host copy of the cell codes (zero ring)
+    // step split (IMEX): every node of every cut cell is an implicit row, whose
+    // explicit K psi is multiplied by 1/m = 0 -- the part steps skip the dense
+    // cut-cell products
+    bool part_skip_cut = false;
     DevBuf<int32_t> order_part[2];           // step split: far / near tiles (dispatch order kept)
     int64_t n_order_part[2] = {0, 0};
     int part_active = -1;
@@ -894,6 +899,7 @@ struct ScmOperator final : Operator {
         }
         if (!n_ord) return;
         Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, ord, n_strips, n_rtiles, pitch};
+        if (MODE == MODE_STEP && part_active >= 0 && part_skip_cut) g.KT = nullptr;   // cut cells act on implicit rows only
         dim3 grid((unsigned)n_ord);
         const CUtensorMap& mu = state_map<P>(a.cur);
         const bool epi = WCB2D_EPI_TMA && MODE == MODE_STEP;
@@ -995,6 +1001,7 @@ struct ScmOperator final : Operator {
         if (!n_ord) return;
         const EMats<P> mt = emats<P>();
         Scm2DGeo g{n_ex, n_e, n1, row_lo, row_hi, mask.p, cut_id.p, KT.p, cflags.p, ord, n_strips, n_rtiles, pitch};
+        if (MODE == MODE_STEP && part_active >= 0 && part_skip_cut) g.KT = nullptr;   // cut cells act on implicit rows only
         const CUtensorMap& mu_ = state_map_e<P>(a.cur, 0);
         const bool epi = MODE == MODE_STEP;
         const CUtensorMap& mp = epi ? state_map_e<P>(a.prev, 1) : mu_;
@@ -1283,6 +1290,23 @@ struct ScmOperator final : Operator {
                     if (row >= I0 - p && row <= I0 + TI && col >= J0 - p - 1 && col <= J0 + TJ + 1)
                         near[st * n_rtiles + rt] = 1;
                 }
+        }
+        // are all nodes of all cut cells implicit rows?
+        part_skip_cut = false;
+        if (!mask_h.empty() && !getenv("WAVECELL_B200_IMEX_KEEP_CUT")) {
+            std::vector<uint8_t> is_c((size_t)plane * ncomp, 0);
+            for (int64_t k = 0; k < n_ids; ++k) is_c[sidx[ids[k]]] = 1;
+            bool all = true;
+            const int64_t ms_ = n_e + 2;
+            for (int64_t ex = 0; ex < n_ex && all; ++ex)
+                for (int64_t ey = 0; ey < n_e && all; ++ey) {
+                    if (mask_h[(ex + 1) * ms_ + ey + 1] != 2) continue;
+                    for (int a = 0; a <= p && all; ++a)
+                        for (int b = 0; b <= p && all; ++b)
+                            for (int cc = 0; cc < ncomp && all; ++cc)
+                                all = is_c[cc * plane + (ex * p + a + p) * pitch + ey * p + b + PADJ] != 0;
+                }
+            part_skip_cut = all;
         }
         std::vector<int32_t> part[2];
         for (int32_t t : order_h) part[near[t] ? 1 : 0].push_back(t);
@@ -1646,6 +1670,7 @@ static Operator* build_scm_operator(Context* ctx, const wcb_scm_desc* d, int nco
         mask.assign((op->n_ex + 2) * s_, 0);
         for (int64_t i = 0; i < op->n_ex; ++i)
             for (int64_t j = 0; j < n_e; ++j) mask[(i + 1) * s_ + (j + 1)] = (uint8_t)cls[i * n_e + j];
+        op->mask_h = mask;
     } else {
         const int64_t s_ = n_e + 2;
         mask.assign((op->n_ex + 2) * s_ * s_, 0);
