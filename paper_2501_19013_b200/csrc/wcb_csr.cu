@@ -8,6 +8,10 @@
 // divergence amplitude into the same pass (one HBM pass per step).
 #include "wcb_internal.cuh"
 
+#include <cmath>
+#include <map>
+#include <type_traits>
+
 #include <algorithm>
 #include <numeric>
 #include <cstring>
@@ -80,6 +84,16 @@ __global__ void __launch_bounds__(BLOCK) k_csr_cdm(int64_t n, const int64_t* __r
 // slices store every index and value (type 0; padding entries point at the
 // row with value 0).  Row sums run in stored (CSR) order in every type, so
 // results are bitwise those of the plain SELL layout.
+// The stencil shared by most type-2 slices of a matrix (type 3): its offsets
+// and values travel as a kernel parameter, so a multiply-add is one x load plus
+// a constant-bank operand instead of three loads (value, offset, x).
+constexpr int SELL_GP_MAX = 64;
+struct SellPattern {
+    int32_t w = 0;
+    int32_t off[SELL_GP_MAX];
+    double val[SELL_GP_MAX];
+};
+
 template <bool STEP>
 __global__ void __launch_bounds__(256) k_sell(int64_t n, const uint8_t* __restrict__ stype,
                                               const int32_t* __restrict__ swid,
@@ -90,7 +104,7 @@ __global__ void __launch_bounds__(256) k_sell(int64_t n, const uint8_t* __restri
                                               const int32_t* __restrict__ p_off,
                                               const double* __restrict__ p_val,
                                               const double* __restrict__ x, double* __restrict__ y,
-                                              StepArgs a) {
+                                              const __grid_constant__ SellPattern gp, StepArgs a) {
     if (STEP) {
         pdl_trigger();
         pdl_wait();   // the previous step's psi is complete from here on
@@ -110,7 +124,44 @@ __global__ void __launch_bounds__(256) k_sell(int64_t n, const uint8_t* __restri
     if (valid) {
         const int w = __ldg(swid + s);
         const int t = __ldg(stype + s);
-        if (t == 2) {
+        if (t == 3) {
+            // compile-time widths of the B-spline box stencils ((2p+1)^2): no
+            // loop-exit branch between the taps, so the x loads are batched
+            const double* xr = x + row;
+            auto taps = [&](auto wc) {
+                constexpr int WT = decltype(wc)::value;
+                #pragma unroll
+                for (int k = 0; k < WT; ++k) acc = fma(gp.val[k], __ldg(xr + gp.off[k]), acc);
+            };
+            if (gp.w == 49) taps(std::integral_constant<int, 49>{});
+            else if (gp.w == 25) taps(std::integral_constant<int, 25>{});
+            else if (gp.w == 9) taps(std::integral_constant<int, 9>{});
+            else {
+                #pragma unroll
+                for (int k = 0; k < SELL_GP_MAX; ++k) {
+                    if (k >= gp.w) break;
+                    acc = fma(gp.val[k], __ldg(xr + gp.off[k]), acc);
+                }
+            }
+        } else if (t == 4) {
+            // the matrix-wide values with this slice's own offsets, which come in
+            // the same runs of consecutive columns (a compact DOF numbering
+            // shifts whole neighbour rows): one offset load per run
+            const int64_t pb = __ldg(p_ptr + s);
+            const double* xr = x + row;
+            auto runs = [&](auto rc) {
+                constexpr int RL = decltype(rc)::value;   // RL runs of RL taps
+                #pragma unroll
+                for (int q = 0; q < RL; ++q) {
+                    const double* xb = xr + __ldg(p_off + pb + q * RL);
+                    #pragma unroll
+                    for (int d = 0; d < RL; ++d) acc = fma(gp.val[q * RL + d], __ldg(xb + d), acc);
+                }
+            };
+            if (gp.w == 49) runs(std::integral_constant<int, 7>{});
+            else if (gp.w == 25) runs(std::integral_constant<int, 5>{});
+            else runs(std::integral_constant<int, 3>{});
+        } else if (t == 2) {
             const int64_t pb = __ldg(p_ptr + s);
             #pragma unroll 8
             for (int k = 0; k < w; ++k)
@@ -159,11 +210,12 @@ struct CsrOperator final : Operator {
     DevBuf<int32_t> e_idx, p_off;
     DevBuf<double> e_val, p_val;
     double sell_bytes = 0.0;   // matrix bytes per apply in the SELL layout
+    SellPattern gpat;          // the matrix-wide stencil of its type-3 slices (w = 0: none)
 
 
     const char* name() const override { return "csr"; }
     std::string step_kernel() const override {
-        return sell ? "k_sell<true> (SELL-32 slices, shared-stencil types 1/2, fused CDM update)"
+        return sell ? "k_sell<true> (SELL-32 slices, shared-stencil types 1-4, fused CDM update)"
                     : "k_csr_cdm<" + std::to_string(tpr) + ",256> (CSR, fused CDM update)";
     }
     const std::vector<int64_t>& state_index() const override { return sidx; }
@@ -195,7 +247,7 @@ struct CsrOperator final : Operator {
         if (sell) {
             StepArgs a;
             k_sell<false><<<(unsigned)ceil_div(n, 256), 256, 0, ctx->stream>>>(
-                n, s_type.p, s_wid.p, e_ptr.p, e_idx.p, e_val.p, p_ptr.p, p_off.p, p_val.p, x, y, a);
+                n, s_type.p, s_wid.p, e_ptr.p, e_idx.p, e_val.p, p_ptr.p, p_off.p, p_val.p, x, y, gpat, a);
             ctx->launches++;
             WCB_CHECK_LAUNCH();
             return;
@@ -226,7 +278,7 @@ struct CsrOperator final : Operator {
             WCB_CUDA(cudaLaunchKernelEx(&cfg, k_sell<true>, n, (const uint8_t*)s_type.p, (const int32_t*)s_wid.p,
                                         (const int64_t*)e_ptr.p, (const int32_t*)e_idx.p, (const double*)e_val.p,
                                         (const int64_t*)p_ptr.p, (const int32_t*)p_off.p, (const double*)p_val.p,
-                                        a.cur, (double*)none, a));
+                                        a.cur, (double*)none, gpat, a));
             ctx->launches++;
             WCB_CHECK_LAUNCH();
             return;
@@ -335,12 +387,57 @@ Operator* make_csr_operator(Context* ctx, int64_t n, const int64_t* h_indptr,
                 if (!with_idx) ei.resize(ev.size(), 0);   // keep e_idx aligned with e_val
             }
         }
+        // the most common type-2 stencil becomes the kernel-parameter pattern
+        if (!getenv("WAVECELL_B200_NO_SELL_GP")) {
+            std::map<std::vector<unsigned char>, int64_t> freq;
+            auto key_of = [&](int64_t sl) {
+                const int64_t w = sw[sl];
+                std::vector<unsigned char> k(w * 12);
+                std::memcpy(k.data(), po.data() + pp[sl], w * 4);
+                std::memcpy(k.data() + w * 4, pv.data() + pp[sl], w * 8);
+                return k;
+            };
+            int64_t best_sl = -1, best_n = 0;
+            for (int64_t sl = 0; sl < n_sl; ++sl)
+                if (st[sl] == 2 && sw[sl] <= SELL_GP_MAX) {
+                    const int64_t c = ++freq[key_of(sl)];
+                    if (c > best_n) { best_n = c; best_sl = sl; }
+                }
+            if (best_sl >= 0 && best_n * 4 >= n_sl) {   // at least a quarter of the slices
+                const std::vector<unsigned char> kb = key_of(best_sl);
+                op->gpat.w = sw[best_sl];
+                for (int k = 0; k < sw[best_sl]; ++k) {
+                    op->gpat.off[k] = po[pp[best_sl] + k];
+                    op->gpat.val[k] = pv[pp[best_sl] + k];
+                }
+                for (int64_t sl = 0; sl < n_sl; ++sl)
+                    if (st[sl] == 2 && sw[sl] == sw[best_sl] && key_of(sl) == kb) st[sl] = 3;
+                // type 4: same values, own offsets in the same RL runs of RL
+                // consecutive columns (box stencils of 9, 25 or 49 taps)
+                const int wd = op->gpat.w;
+                const int RL = wd == 49 ? 7 : wd == 25 ? 5 : wd == 9 ? 3 : 0;
+                auto runs_ok = [&](const int32_t* o) {
+                    for (int q = 0; q < RL; ++q)
+                        for (int d2 = 1; d2 < RL; ++d2)
+                            if (o[q * RL + d2] != o[q * RL] + d2) return false;
+                    return true;
+                };
+                if (RL && runs_ok(op->gpat.off)) {
+                    for (int64_t sl = 0; sl < n_sl; ++sl) {
+                        if (st[sl] != 2 || sw[sl] != wd) continue;
+                        if (std::memcmp(pv.data() + pp[sl], op->gpat.val, (size_t)wd * 8) != 0) continue;
+                        if (runs_ok(po.data() + pp[sl])) st[sl] = 4;
+                    }
+                }
+            }
+        }
         // bytes one apply reads from the matrix: per-entry arrays of type 0/1
         // slices + one pattern per type 1/2 slice + slice headers
         double mb = 0.0;
         for (int64_t sl = 0; sl < n_sl; ++sl) {
             const double w = sw[sl];
-            mb += st[sl] == 0 ? 32.0 * w * 12.0 : st[sl] == 1 ? 32.0 * w * 8.0 + w * 4.0 : w * 12.0;
+            mb += st[sl] == 0 ? 32.0 * w * 12.0 : st[sl] == 1 ? 32.0 * w * 8.0 + w * 4.0 : st[sl] == 2 ? w * 12.0
+                  : st[sl] == 4 ? 4.0 * std::sqrt(w) : 0.0;
             mb += 1.0 + 4.0 + 16.0;
         }
         op->sell_bytes = mb;
