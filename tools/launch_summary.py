@@ -4,7 +4,11 @@ rows = [r for r in csv.reader(l for l in open(sys.argv[1]) if not l.startswith("
 hdr = rows[0]
 ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
 agg = collections.OrderedDict()
-for r in rows[1:]:
+body = rows[1:]
+if "--step" in sys.argv:   # keep the stepping loop: from the launch before the first MODE_STEP (..., 0>) kernel on
+    first = next((i for i, r in enumerate(body) if len(r) > ki and re.search(r", \(int\)0>|, 0>", r[ki])), 0)
+    body = body[max(first - 1, 0):]
+for r in body:
     if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
         continue
     name = re.sub(r"\(.*$", "", r[ki].replace("(int)", "")).replace("void ", "")
