@@ -99,9 +99,9 @@ __device__ __forceinline__ void cut_cells_warp3(const Scm3DGeo& g, int64_t ex, i
 // cell's K_o / sk (L(L+1)/2 doubles, one 1D bulk copy) and its u_e (cp.async
 // gather from the state) land in shared memory while the current cell is
 // multiplied.  A group is G = ceil(L/32) warps (two for P = 3), one row per
-// lane: lane r forms row r in ascending column order (running packed
-// indices: m <= r along row r, m > r down column r) -- the same sums as a
-// dense symmetric row.  (One warp per cell with two rows per lane left the
+// lane: lane r forms row r in ascending column order (m <= r along row r,
+// m > r down column r of the packed triangle) -- the same sums as a dense
+// symmetric row.  (One warp per cell with two rows per lane left the
 // SM at 6 warps, stalled on shared-memory latency: ncu, 312 us on config 5.)
 template <int P>
 struct CutPre {
@@ -182,15 +182,16 @@ __global__ void __launch_bounds__(CutPre<P>::W * 32) k_cut_pre(int64_t n_cut, co
         const double* kp = reinterpret_cast<const double*>(mine + buf * (C::KB + C::UB));
         const double* uu = reinterpret_cast<const double*>(mine + buf * (C::KB + C::UB) + C::KB);
         for (int r = gt; r < L; r += G * 32) {
+            // row r in ascending column order from the packed lower triangle:
+            // (r, m) for m <= r, (m, r) below the diagonal.  One loop for both
+            // parts (the lanes of a warp switch at different m: two loops
+            // diverged for half of the columns); column indices are constants.
             double t = 0.0;
-            int idx = r * (r + 1) / 2;   // (r, 0)
-            #pragma unroll 8
-            for (int m = 0; m <= r; ++m) t = fma(kp[idx + m], uu[m], t);
-            idx = (r + 1) * (r + 2) / 2 + r;   // (r+1, r)
-            #pragma unroll 8
-            for (int m = r + 1; m < L; ++m) {
+            const int tr = r * (r + 1) / 2;
+            #pragma unroll
+            for (int m = 0; m < L; ++m) {
+                const int idx = m <= r ? tr + m : m * (m + 1) / 2 + r;
                 t = fma(kp[idx], uu[m], t);
-                idx += m + 1;
             }
             out[e * L + r] = t;
         }

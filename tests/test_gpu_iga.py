@@ -56,9 +56,10 @@ def test_shared_stencil_slices_bitwise(monkeypatch):
     f = lambda t: ricker(t, 10.0)  # noqa: E731
     x = np.random.default_rng(3).standard_normal(prob.n_dof)
     outs = []
-    # plain SELL and shared-stencil slices
-    for flags in ({"WAVECELL_B200_NO_SHARED_STENCIL": "1"}, {}):
-        for k in ("WAVECELL_B200_NO_SHARED_STENCIL",):
+    # plain SELL; shared-stencil slices without and with the kernel-parameter
+    # stencil (slice types 3 / 4)
+    for flags in ({"WAVECELL_B200_NO_SHARED_STENCIL": "1"}, {"WAVECELL_B200_NO_SELL_GP": "1"}, {}):
+        for k in ("WAVECELL_B200_NO_SHARED_STENCIL", "WAVECELL_B200_NO_SELL_GP"):
             monkeypatch.delenv(k, raising=False)
         for k, v in flags.items():
             monkeypatch.setenv(k, v)
