@@ -190,19 +190,36 @@ def partition_imex(prob, world: int):
     ok = np.zeros(n_e + 1, dtype=bool)
     for c in range(2, n_e):
         ok[c] = not (cut_rows[c - 2] or cut_rows[c - 1] or cut_rows[c])
-    base = partition(prob, world)
-    cuts = [0]
-    for r in range(1, world):
-        want = base[r][0]
-        cand = np.flatnonzero(ok)
-        cand = cand[cand > cuts[-1]]
-        if cand.size == 0:
-            raise ValueError("no admissible slab cut (every cell row pair holds a cut cell)")
-        c = int(cand[np.argmin(np.abs(cand - want))])
-        cuts.append(c)
-    cuts.append(n_e)
-    if any(b <= a for a, b in zip(cuts[:-1], cuts[1:])):
+    # admissible cuts are scarce (config 4: 120 of 1024 rows, none between rows
+    # 651 and 980), so the cuts are chosen by dynamic programming: smallest
+    # largest slab, then smallest sum of squared sizes
+    cand = [0] + [int(c) for c in np.flatnonzero(ok)] + [n_e]
+    m = len(cand)
+    INF = (float("inf"), float("inf"))
+    # best[k][i]: (max size, sum of squares) of rows cand[i]..n_e split into k slabs
+    best = [[INF] * m for _ in range(world + 1)]
+    nxt = [[-1] * m for _ in range(world + 1)]
+    for i in range(m - 1):
+        sz = cand[-1] - cand[i]
+        best[1][i] = (sz, sz * sz)
+    for k in range(2, world + 1):
+        for i in range(m - k):
+            for j in range(i + 1, m - k + 1):
+                tail = best[k - 1][j]
+                if tail == INF:
+                    continue
+                sz = cand[j] - cand[i]
+                v = (max(sz, tail[0]), sz * sz + tail[1])
+                if v < best[k][i]:
+                    best[k][i] = v
+                    nxt[k][i] = j
+    if world > m - 1 or best[world][0] == INF:
         raise ValueError(f"cannot cut {n_e} cell rows into {world} admissible slabs")
+    cuts, i = [0], 0
+    for k in range(world, 1, -1):
+        i = nxt[k][i]
+        cuts.append(cand[i])
+    cuts.append(n_e)
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
