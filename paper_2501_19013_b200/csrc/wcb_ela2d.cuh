@@ -18,11 +18,15 @@
 #pragma once
 // (included inside namespace wcb by wcb_scm.cu)
 
+// p = 5: five cell rows per tile, one CTA of 12 warps per SM (227 KB of shared
+// memory).  Since the IMEX part steps skip the dense cut-cell products the
+// halo warps' redundant row is the dominant overhead: measured on config 4,
+// IMEX step 1315 (RPE 2, two CTAs per SM) / 1238 (3) / 1206 (4) / 1135 us (5).
 #ifndef WCB_ELA_RPE5
-#define WCB_ELA_RPE5 2
+#define WCB_ELA_RPE5 5
 #endif
 #ifndef WCB_ELA_MINB
-#define WCB_ELA_MINB 2
+#define WCB_ELA_MINB 1
 #endif
 __host__ __device__ constexpr int rpe_e(int P) { return P <= 3 ? 3 : P == 5 ? WCB_ELA_RPE5 : 2; }
 
